@@ -1,0 +1,428 @@
+#!/usr/bin/env python
+"""bench.py -- ParoQuant decode-linear benchmark on B200 (BASELINE.json metric:
+"decode linear us & HBM GB/s (% of peak); rotation overhead vs plain W4A16").
+
+One step = one pass of the runtime hot path (scale + 8 Givens
+layers fused into the activation staging + group-wise INT4 dequant GEMV + epilogue)
+over the seven linears of one LLaMA-3-8B decoder layer at bs=1 (BASELINE.json
+configs[1]: q/k/v/o 4096x4096/1024, gate/up/down 4096x14336), random fp16 weights
+packed with paro_pack (W4 g128, 8 Alg. A1 rotations) and random fp16 activations.
+Steps cycle through a pool of layers whose packed weights exceed the 126 MB L2
+(inputs larger than L2), so every step streams its weights from HBM.
+
+value = algorithmic weight+param+activation bytes per step / device time per step
+(GB/s, higher is better).  Multi-GPU (torchrun): every linear is sharded by output
+channel across ranks and y is all-gathered with NCCL (strong scaling; value counts
+the whole layer's bytes once).
+
+--impl reference: the fp64 CPU oracle (oracle/) on a bounded sample of the same
+workload, same metric (there is no reference implementation to install: the
+reference is a paper).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "decode linear HBM GB/s (LLaMA-3-8B layer, bs=1, W4 g128, 8 Givens layers)"
+WORKLOAD = "llama3-8b decode linears bs=1 (q,k,v,o,gate,up,down), W4 g128, L=8 rotations of <=64 pairs"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
+
+
+def algorithmic_bytes(N, K, B=1, L=8, P=64):
+    """W4A16 0.5195 B/weight + rotation params 6 B/pair + 4 B/channel s
+    + activations 2BK in, 2BN out."""
+    G = K // 128
+    w = N * K // 2 + N * G * 2 + N * G // 2
+    rot = G * L * P * 6 + 4 * K
+    act = 2 * B * K + 2 * B * N
+    return w + rot + act, w
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        import tempfile
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sms, mx, reasons = [], None, set()
+        try:
+            for line in open(self.path):
+                f = [c.strip() for c in line.split(",")]
+                if len(f) < 9:
+                    continue
+                try:
+                    sms.append(float(f[1]))
+                    mx = float(f[2])
+                except ValueError:
+                    continue
+                names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+                for n, v in zip(names, f[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+        except Exception:
+            pass
+        if not sms:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sms), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ----------------------------------------------------------------------------- workload
+def build_layer_pool(torch, paro, shapes, rank, world, n_layers, dev, seed=0):
+    """Pack n_layers copies of the decoder layer's linears (this rank's row shard).
+    Pairs/angles/scales are generated once per shape (speed does not depend on their
+    values); the weights differ per layer."""
+    G_cache = {}
+    pool = []
+    for li in range(n_layers):
+        layer = []
+        for name, (N, K) in shapes.items():
+            if (N, K) not in G_cache:
+                p = synth.make_problem(8, K, 1, seed=seed + N % 97)
+                G_cache[(N, K)] = (torch.from_numpy(p["s"]).to(dev), torch.from_numpy(p["theta"]).to(dev),
+                                   torch.from_numpy(p["pairs"]).to(dev))
+            s, th, pr = G_cache[(N, K)]
+            r0, r1 = paro.shard_rows(N, world, rank)
+            g = torch.Generator(device=dev).manual_seed(seed * 1000 + li * 17 + N + K)
+            W = (torch.randn((r1 - r0, K), generator=g, device=dev, dtype=torch.float32) * 0.02).to(torch.float16)
+            packed = paro.paro_pack(W, s, th, pr)
+            del W
+            layer.append((name, N, K, packed))
+        pool.append(layer)
+    return pool
+
+
+def run_paro(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_10645_b200 as paro
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    shapes = synth.LLAMA3_8B_DECODE
+    B = args.batch
+    comm = None
+    if world > 1:
+        uid = paro.paro_comm_unique_id() if rank == 0 else b"\0" * 128
+        t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
+        dist.broadcast(t, 0)
+        comm = paro.paro_comm_init(bytes(t.cpu().tolist()), rank, world)
+
+    layer_bytes = sum(algorithmic_bytes(N, K, B)[0] for N, K in shapes.values())
+    weight_bytes_rank = sum(algorithmic_bytes(N // world, K, B)[1] for N, K in shapes.values())
+    n_layers = max(2, int(np.ceil(4 * L2_BYTES / max(weight_bytes_rank, 1))))
+    n_layers = min(n_layers, 64)
+    pool = build_layer_pool(torch, paro, shapes, rank, world, n_layers, dev)
+    g = torch.Generator(device=dev).manual_seed(123 + rank * 0)
+    xs = {K: torch.randn((B, K), generator=g, device=dev).to(torch.float16) for _, K in shapes.values()}
+    ys = {name: torch.empty((B, N), dtype=torch.float16, device=dev) for name, (N, K) in shapes.items()}
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
+
+    def run_step(li, flags, pdl=True):
+        f = flags | (paro.PARO_LINEAR_PDL if pdl else 0)
+        for name, N, K, packed in pool[li % n_layers]:
+            if world == 1:
+                paro.paro_linear(xs[K], packed, y=ys[name], flags=f, workspace=ws, stream=stream)
+            else:
+                paro.paro_linear_allgather(xs[K], packed, comm, rank, world, y=ys[name], flags=f, workspace=ws,
+                                           stream=stream)
+
+    def capture(flags, steps_in_graph):
+        gph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            for li in range(2):
+                run_step(li, flags)
+            stream.synchronize()
+            with torch.cuda.graph(gph, stream=stream):
+                for li in range(steps_in_graph):
+                    run_step(li, flags)
+        return gph
+
+    def timed(flags, steps, warmup):
+        """Graph of `steps` consecutive steps (layers cycle through the pool); returns
+        max-over-ranks ms per step measured with CUDA events on the launch stream."""
+        gph = capture(flags, steps)
+        for _ in range(max(1, warmup // max(steps, 1) + 1)):
+            gph.replay()
+        stream.synchronize()
+        t_end = time.time() + args.load_s  # untimed load so the clock sampler sees the loaded state
+        while time.time() < t_end:
+            gph.replay()
+            stream.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        gph.replay()
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    # warm-up steps (untimed), then exactly K timed steps (in one graph replay)
+    with ClockSampler(local) as clk:
+        ms_step = timed(0, args.steps, args.warmup)
+        ms_norot = timed(paro.PARO_LINEAR_NO_ROTATION, args.steps, args.warmup)
+    clocks = clk.summary()
+
+    # per-linear timings (rank 0 view, same pool cycling), rotation on / off
+    per_linear = {}
+    if world == 1:
+        for name, (N, K) in shapes.items():
+            res = {}
+            for tag, fl in (("rot", 0), ("norot", paro.PARO_LINEAR_NO_ROTATION)):
+                gph = torch.cuda.CUDAGraph()
+                reps = 100
+                with torch.cuda.stream(stream):
+                    for li in range(2):
+                        lin = [e for e in pool[li % n_layers] if e[0] == name][0]
+                        paro.paro_linear(xs[K], lin[3], y=ys[name], flags=fl | paro.PARO_LINEAR_PDL, workspace=ws,
+                                         stream=stream)
+                    stream.synchronize()
+                    with torch.cuda.graph(gph, stream=stream):
+                        for li in range(reps):
+                            lin = [e for e in pool[li % n_layers] if e[0] == name][0]
+                            paro.paro_linear(xs[K], lin[3], y=ys[name], flags=fl | paro.PARO_LINEAR_PDL,
+                                             workspace=ws, stream=stream)
+                gph.replay()
+                stream.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                gph.replay()
+                e1.record(stream)
+                e1.synchronize()
+                res[tag] = e0.elapsed_time(e1) / reps * 1000.0  # us
+            ab, wb = algorithmic_bytes(N, K, B)
+            per_linear[name] = {"N": N, "K": K, "us": round(res["rot"], 3), "us_norot": round(res["norot"], 3),
+                                "GBps": round(ab / res["rot"] / 1e3, 1),
+                                "rot_overhead": round(res["rot"] / res["norot"] - 1.0, 4)}
+
+    # end-to-end through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if True:
+        hx = {K: xs[K].cpu().pin_memory() for K in xs}
+        hy = {name: torch.empty((B, N), dtype=torch.float16).pin_memory() for name, (N, K) in shapes.items()}
+        h2d = sum(t.numel() * 2 for t in hx.values())
+        d2h = sum(t.numel() * 2 for t in hy.values())
+        n_e2e = max(10, min(args.steps, 200))
+
+        def e2e_step(li):
+            with torch.cuda.stream(stream):
+                for K, t in hx.items():
+                    xs[K].copy_(t, non_blocking=True)
+                run_step(li, 0, pdl=False)
+                for name, t in hy.items():
+                    t.copy_(ys[name], non_blocking=True)
+
+        for li in range(3):
+            e2e_step(li)
+        stream.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for li in range(n_e2e):
+            e2e_step(li)
+        e1.record(stream)
+        e1.synchronize()
+        ms_e2e = e0.elapsed_time(e1) / n_e2e
+        if world > 1:
+            t = torch.tensor([ms_e2e], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+        e2e = {"value": round(layer_bytes / (ms_e2e * 1e-3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms_e2e, 4),
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "api": "paper_2511_10645_b200.paro_linear per linear (ctypes), pinned host x/y"}
+
+    if comm is not None:
+        torch.cuda.synchronize()
+        paro.paro_comm_destroy(comm)
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks = load_peaks()
+    gbps = layer_bytes / (ms_step * 1e-3) / 1e9
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    out = {
+        "metric": METRIC, "value": round(gbps, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "us_per_step": round(ms_step * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f16 act / int4 weight / f32 acc",
+        "data": "synthetic (random fp16 W ~ N(0,0.02^2) packed W4 g128 with Alg. A1 pairs, random theta/s; x ~ N(0,1))",
+        "config": {"workload": WORKLOAD, "batch": B, "pool_layers": n_layers,
+                   "l2": f"inputs larger than L2: weight pool {n_layers} layers x "
+                         f"{weight_bytes_rank / 1e6:.1f} MB/rank > 126 MB L2, cycled per step",
+                   "parallelism": f"N-shard x{world} + NCCL all-gather" if world > 1 else "single GPU",
+                   "bytes_per_step": layer_bytes},
+        "rotation_overhead": round(ms_step / ms_norot - 1.0, 4), "us_per_step_norot": round(ms_norot * 1e3, 3),
+        "per_linear": per_linear,
+        "roofline": {"bound": "hbm", "achieved": round(gbps, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(gbps / peak, 4), "traffic": None,
+                     "kernel": "paro_gemv_kernel (all 7 launches/step)",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not peaks.get("_fallback") else "fallback 6.65 TB/s",
+                     "achieved_def": "algorithmic bytes per step / device time per step (7 GEMV launches, gaps included)"},
+        "clocks": clocks, "e2e": e2e, "gpu_launches": 7 * args.steps * (2 if world > 1 else 1),
+        "gpu_launches_note": "7 paro_gemv_kernel launches per step" + (" + 7 ncclAllGather" if world > 1 else ""),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args)
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        out["roofline"]["traffic"] = prof.get("traffic_per_step")
+        out["roofline"]["traffic_src"] = prof.get("source")
+    except Exception:
+        pass
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- the oracle as baseline
+def oracle_sample(frac_rows=0.125, seed=0):
+    """A bounded sample of one step for the fp64 oracle: every linear of the layer, a
+    fraction of its output rows (rows are independent in the fold, the RTN and the dot).
+    The oracle pack (offline) is done here, untimed."""
+    import oracle as O
+    items = []
+    for name, (N, K) in synth.LLAMA3_8B_DECODE.items():
+        n = max(1, int(N * frac_rows))
+        p = synth.make_problem(n, K, 1, seed=seed + N % 97, outliers=False)
+        pk = O.oracle_pack(p["W"], p["s"], p["theta"], p["pairs"])
+        items.append((p, pk, algorithmic_bytes(n, K, 1)[0]))
+    return items
+
+
+def oracle_time(items):
+    """Run oracle_linear (scale + rotations + fp64 dequant-dot) over the sample; (bytes, s)."""
+    import oracle as O
+    tb, tt = 0, 0.0
+    for p, pk, b in items:
+        t0 = time.perf_counter()
+        O.oracle_linear(p["x"], pk, p["s"], p["theta"], p["pairs"])
+        tt += time.perf_counter() - t0
+        tb += b
+    return tb, tt
+
+
+def cpu_baseline(args):
+    from threadpoolctl import threadpool_limits
+    items = oracle_sample(0.125)
+    with threadpool_limits(limits=1):
+        oracle_time(items)  # warm
+        b, t = oracle_time(items)
+    return {"value": round(b / t / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": "oracle_linear (fp64 numpy) on 1/8 of the output rows of each of the 7 LLaMA-3-8B linears, "
+                      "bs=1, BLAS limited to 1 thread; oracle pack (offline) untimed"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from threadpoolctl import threadpool_limits
+    frac = 1.0 / 64
+    items = oracle_sample(frac)
+    with threadpool_limits(limits=1):
+        for _ in range(args.warmup):
+            oracle_time(items)
+        tb, tt = 0, 0.0
+        for i in range(args.steps):
+            b, t = oracle_time(items)
+            tb += b
+            tt += t
+    v = tb / tt / 1e9
+    ms = tt / args.steps * 1e3
+    sample = ("oracle_linear (fp64 numpy, 1 thread) on 1/64 of the output rows of each of the 7 LLaMA-3-8B "
+              "linears per step, bs=1; oracle pack (offline) done once, untimed")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "batch": 1},
+        "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--impl", default="paro", choices=["paro", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--load-s", type=float, default=1.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_paro(args)
+
+
+if __name__ == "__main__":
+    main()

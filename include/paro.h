@@ -1,0 +1,197 @@
+/*
+ * paro.h -- C ABI of the B200 (sm_100a) ParoQuant hot path.
+ *
+ * ParoQuant (arXiv 2511.10645): scaled pairwise rotation + group-wise INT4
+ * weight-only linear.  Paper text: /root/reference/PAPER.md (cited as PAPER.md:L).
+ *
+ *   y = (X T^{-1}) Q(T W)^T + b            Eq. 2
+ *   T = (prod_{t=1..L} R(P_t, Theta_t)) diag(alpha)   Eq. 8
+ *   Q = group-wise RTN, group g = 128      Eq. 1, Fig. 2
+ *
+ * Conventions:
+ *   - W is the PyTorch nn.Linear.weight layout [N, K] row-major (N = D_out,
+ *     K = D_in; the paper writes W in R^{D_in x D_out}).
+ *   - s is the ACTIVATION multiplier, s = 1/alpha.  The weights get w/s, the
+ *     activations s*x (Eq. 2 puts T on W and T^{-1} on X).
+ *   - pairs are group-local, 0-based (i, j) with i < j < g, int16, shape
+ *     [K/g, L, P, 2]; (-1, -1) marks an absent slot at ANY position (a short
+ *     rotation).  theta is fp32 radians, shape [K/g, L, P].
+ *   - Rotations are applied scale-first, then t = 1..L ("applied sequentially
+ *     after channel-wise scaling"), with the SAME +theta on both
+ *     sides: w_n <- R diag(alpha) w_n and x <- R diag(s) x (Eq. 5, PAPER.md:133-138,
+ *     re-expressed for column vectors).
+ *
+ * Threading / ownership:
+ *   - The caller owns every device buffer (it allocates the packed buffers after
+ *     paro_pack_sizes, and the workspace after paro_linear_workspace).
+ *   - The library keeps no pointers across calls.  paro_linear and
+ *     paro_transform_activations allocate nothing and never synchronise; they
+ *     enqueue on the caller's stream (a cudaStream_t passed as void*).
+ *   - Errors are returned as paro_status; a human-readable message for the
+ *     calling thread is available from paro_last_error().
+ *   - Pointers marked "device" must be CUDA device (or managed) pointers of the
+ *     current device; "host" pointers are plain CPU memory.
+ */
+#ifndef PARO_H_
+#define PARO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PARO_GROUP 128       /* g: quantisation group = rotation group */
+#define PARO_MAX_ROT 8       /* L: "8 independent rotations"; L in [0, 8] (Table 6: 0,2,4,8) */
+#define PARO_SLOTS 64        /* g/2: max pairs per independent rotation */
+#define PARO_BITS 4          /* INT4 */
+
+typedef enum {
+  PARO_OK = 0,
+  PARO_ERR_INVALID_ARGUMENT = 1, /* bad size, NULL/misaligned pointer, s<=0, non-finite, fp16 scale overflow */
+  PARO_ERR_SHAPE = 2,            /* dimension mismatch between arguments */
+  PARO_ERR_PAIRS = 3,            /* pairs violate Definition 1 or i<j<g / no cross-rotation repeat */
+  PARO_ERR_UNSUPPORTED = 4,      /* K % 128 != 0, group != 128, n_rot > 8, dtype not supported */
+  PARO_ERR_CUDA = 5,             /* CUDA runtime error (message in paro_last_error) */
+  PARO_ERR_NCCL = 6              /* NCCL error or libnccl.so.2 not loadable */
+} paro_status;
+
+typedef enum { PARO_F16 = 0, PARO_BF16 = 1, PARO_F32 = 2 } paro_dtype;
+
+/* Byte sizes of the packed buffers of one linear layer (all device buffers,
+ * each must be 16-byte aligned).  Layout (private to the kernels; tests read it
+ * only through paro_unpack_logical):
+ *   codes  : N*K/2       INT4 codes, row-major [N][K/2]; byte k/2 holds k even in
+ *                        its low nibble, k odd in its high nibble.
+ *   scales : N*G*2 + 16  fp16 [N][G] group scales S (G = K/128), +16 B tail pad.
+ *   zeros  : N*ceil(G/2) + 16   uint4 zero points [N][G], nibble-packed like codes.
+ *   rot_cs : G*L*64*8    fp32 (cos theta, sin theta) per (group, rotation, slot).
+ *   rot_idx: G*L*64*2    u8 (i, j) per slot; absent slots hold (128, 128).
+ *   svec   : K*4         fp32 s.
+ * Algorithmic weight bytes are N*K/2 + N*G*2 + N*G/2 (0.5195 B/weight). */
+typedef struct {
+  size_t codes, scales, zeros, rot_cs, rot_idx, svec;
+} paro_packed_sizes;
+
+typedef struct {
+  void *codes, *scales, *zeros, *rot_cs, *rot_idx, *svec; /* caller-owned device buffers */
+  int64_t N, K;                                           /* output / input channels */
+  int32_t group;                                          /* must be 128 */
+  int32_t n_rot;                                          /* L in [0, 8] */
+} paro_packed;
+
+/* Flags for paro_linear / paro_linear_allgather. */
+#define PARO_LINEAR_NO_ROTATION 0x1u /* u = x: skip s and the rotations (plain W4A16; rotation-overhead baseline only) */
+#define PARO_LINEAR_PDL 0x2u         /* launch with programmatic dependent launch: weight prefetch may start before
+                                        the previous kernel on the stream finishes (weights must not be written by it) */
+#define PARO_LINEAR_FORCE_GEMV 0x4u  /* force the decode GEMV kernel for any B (tiles of <= 8 tokens) */
+#define PARO_LINEAR_FORCE_GEMM 0x8u  /* force the prefill (tcgen05) path for any B */
+
+/* Sizes of the packed buffers for an [N, K] weight with group size `group`
+ * (must be 128) and n_rot rotations (0..8).  Returns PARO_ERR_UNSUPPORTED for
+ * K % 128 != 0, group != 128 or n_rot > 8; PARO_ERR_INVALID_ARGUMENT for N, K <= 0
+ * or out == NULL. */
+paro_status paro_pack_sizes(int64_t N, int64_t K, int32_t group, int32_t n_rot, paro_packed_sizes* out);
+
+/* paro_pack: fold T into W and RTN-quantise ("We then quantize TW instead of W").
+ *   W      device fp16 [N, K]
+ *   s      device fp32 [K]            activation multiplier s = 1/alpha, finite, > 0
+ *   theta  device fp32 [K/128, n_rot, n_pairs]
+ *   pairs  device int16 [K/128, n_rot, n_pairs, 2]
+ *   n_pairs P in [1, 64]; ignored when n_rot == 0 (theta/pairs may then be NULL)
+ *   out    host struct whose buffer pointers the caller filled (sizes from paro_pack_sizes);
+ *          the call sets out->N, K, group, n_rot.
+ * Per weight row w_n and group gamma (fp64 throughout, each product/sum rounded
+ * separately, no FMA):  v = w/s; for t = 1..L, each pair (i, j):
+ *   v_i <- cos*v_i - sin*v_j,  v_j <- sin*v_i + cos*v_j      (Eq. 4)
+ * then Eq. 1 on the 128 values: S = fp16_rne((max-min)/15) floored at 2^-24,
+ * z = clamp(-rint(min/S), 0, 15), q = clamp(rint(v/S) + z, 0, 15) (round half even).
+ * cos/sin are evaluated on the host in fp64 with the C library (Q6).
+ * Synchronous: copies s/theta/pairs to the host to validate them (Definition 1,
+ * i<j<128, no pair repeated across the rotations of a group, s > 0 finite),
+ * allocates one temporary of K/128*n_rot*64*16 + 64 bytes with cudaMallocAsync,
+ * and returns after the kernel finished.  Errors: PARO_ERR_PAIRS,
+ * PARO_ERR_INVALID_ARGUMENT (also for non-finite W or an fp16 scale overflow),
+ * PARO_ERR_UNSUPPORTED, PARO_ERR_CUDA. */
+paro_status paro_pack(const void* W, const float* s, const float* theta, const int16_t* pairs, int64_t N,
+                      int64_t K, int32_t group, int32_t n_rot, int32_t n_pairs, paro_packed* out, void* stream);
+
+/* Workspace bytes paro_linear needs for this call shape (0 is possible).
+ * `on_the_fly` != 0 when paro_linear will be given s/theta/pairs pointers. */
+size_t paro_linear_workspace(int64_t B, int64_t N, int64_t K, int32_t n_rot, int32_t n_pairs, int32_t on_the_fly,
+                             uint32_t flags);
+
+/* paro_linear: y = (T^{-1} x) . dequant(Q)^T + bias for every token (Eq. 2).
+ *   x       device [B, K] fp16 or bf16 (x_dtype), row-major
+ *   packed  host struct from paro_pack (device buffers inside)
+ *   s, theta, pairs  NULL: use the transform captured in `packed` (normal use).
+ *           Non-NULL (all three, device, shapes as in paro_pack with n_pairs):
+ *           the transform is prepared on the fly on the GPU (fp32 sincos) into the
+ *           workspace; NOT validated -- the caller guarantees Definition 1.
+ *   bias    device fp32 [N] or NULL
+ *   y       device [B, N] (y_dtype fp16, bf16 or fp32), row-major
+ *   flags   PARO_LINEAR_*
+ * Decode (B <= 16): one fused kernel -- the scale + L rotations are applied to the
+ * activation while it is staged in shared memory (never written to HBM), the
+ * packed INT4 stream is bulk-copied (TMA engine) into a shared-memory ring and
+ * dequantised in registers, fp32 accumulate.  Prefill (B > 16): activation
+ * transform into an fp16 workspace, then a tcgen05/TMEM GEMM with an in-kernel
+ * INT4 -> fp16 dequant producer.
+ * Asynchronous, no allocation.  Errors: PARO_ERR_SHAPE (packed vs call), PARO_ERR_INVALID_ARGUMENT
+ * (NULL/misaligned pointers, B <= 0, workspace too small), PARO_ERR_UNSUPPORTED (dtypes), PARO_ERR_CUDA.
+ * Precision: x' and dequantised weights are never rounded to bf16; |s*x| and |x'| must be < 65504. */
+paro_status paro_linear(const void* x, paro_dtype x_dtype, int64_t B, const paro_packed* packed, const float* s,
+                        const float* theta, const int16_t* pairs, int32_t n_pairs, const float* bias, void* y,
+                        paro_dtype y_dtype, uint32_t flags, void* workspace, size_t workspace_bytes, void* stream);
+
+/* paro_transform_activations: x' = R_L ... R_1 diag(s) x for every token (the
+ * activation side of Eq. 2 / Eq. 5), written as fp16 [B, K] (x_out, device).
+ * Uses the transform captured in `packed` (its codes/scales/zeros are not read).
+ * Used by the prefill path and exported for tests / the rotation microbenchmark
+ * (fig:kernel-speedup).  Asynchronous. */
+paro_status paro_transform_activations(const void* x, paro_dtype x_dtype, int64_t B, const paro_packed* packed,
+                                       void* x_out, void* stream);
+
+/* Test-only: expand the packed weight to logical arrays (device):
+ * codes u8 [N, K], scales fp16 [N, K/128], zeros u8 [N, K/128].  Asynchronous. */
+paro_status paro_unpack_logical(const paro_packed* packed, void* codes_u8, void* scales_f16, void* zeros_u8,
+                                void* stream);
+
+/* ---- output-channel (N) sharding over NVLink ----
+ * Rank r of G owns rows [r*N/G, (r+1)*N/G) of W, packed with paro_pack on that
+ * row slice (identical, bitwise, to the same rows of the full pack).  Every rank
+ * holds the full x, applies the (cheap) transform locally, runs the GEMV on its
+ * shard, and an NCCL all-gather of y runs on the same stream.
+ * libnccl.so.2 is loaded at first use with dlopen (the copy already mapped by the
+ * process, e.g. PyTorch's, is reused). */
+#define PARO_NCCL_UNIQUE_ID_BYTES 128
+
+/* Fill `uid` (host, 128 bytes) with a fresh ncclUniqueId.  Call on one rank and
+ * broadcast the bytes (e.g. over a torch.distributed process group). */
+paro_status paro_comm_unique_id(void* uid);
+/* Create an NCCL communicator for (rank, world) from the broadcast uid; *comm
+ * receives an opaque handle (an ncclComm_t).  Collective over all ranks. */
+paro_status paro_comm_init(const void* uid, int32_t rank, int32_t world, void** comm);
+paro_status paro_comm_destroy(void* comm);
+
+/* Sharded linear: packed_shard holds this rank's N/world rows; y_full is device
+ * [B, N] (N = packed_shard->N * world) in y_dtype.  workspace must hold
+ * paro_linear_allgather_workspace(...) bytes.  Errors as paro_linear, plus
+ * PARO_ERR_NCCL. */
+size_t paro_linear_allgather_workspace(int64_t B, int64_t N_shard, int64_t K, int32_t world, paro_dtype y_dtype,
+                                       uint32_t flags);
+paro_status paro_linear_allgather(const void* x, paro_dtype x_dtype, int64_t B, const paro_packed* packed_shard,
+                                  const float* bias_shard, void* y_full, paro_dtype y_dtype, uint32_t flags,
+                                  void* workspace, size_t workspace_bytes, void* comm, int32_t rank, int32_t world,
+                                  void* stream);
+
+/* Message of the last error on the calling thread ("" if none). */
+const char* paro_last_error(void);
+/* Library version string. */
+const char* paro_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARO_H_ */

@@ -1,0 +1,257 @@
+"""paper_2511_10645_b200 -- B200-native ParoQuant hot path (scaled pairwise rotation +
+INT4 weight-only linear), arXiv 2511.10645.
+
+Thin ctypes binding over the C ABI in include/paro.h (libparo.so, built in-tree by
+``_build.build()``).  Every function here only marshals arguments: torch tensors
+-> device pointers + the current CUDA stream.  All arithmetic runs in the CUDA
+kernels of libparo.so; there is no CPU fallback -- if the library is missing,
+importing this package raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libparo.so")
+
+PARO_OK, PARO_ERR_INVALID_ARGUMENT, PARO_ERR_SHAPE, PARO_ERR_PAIRS, PARO_ERR_UNSUPPORTED, PARO_ERR_CUDA, \
+    PARO_ERR_NCCL = range(7)
+STATUS_NAMES = {0: "ok", 1: "invalid_argument", 2: "shape", 3: "pairs", 4: "unsupported", 5: "cuda", 6: "nccl"}
+PARO_F16, PARO_BF16, PARO_F32 = 0, 1, 2
+PARO_LINEAR_NO_ROTATION = 0x1
+PARO_LINEAR_PDL = 0x2
+PARO_LINEAR_FORCE_GEMV = 0x4
+PARO_LINEAR_FORCE_GEMM = 0x8
+GROUP = 128
+SLOTS = 64
+
+
+class ParoError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"paro {STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+        self.kind = STATUS_NAMES.get(status, str(status))
+
+
+class paro_packed_sizes(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_size_t) for n in ("codes", "scales", "zeros", "rot_cs", "rot_idx", "svec")]
+
+
+class paro_packed(ctypes.Structure):
+    _fields_ = [("codes", ctypes.c_void_p), ("scales", ctypes.c_void_p), ("zeros", ctypes.c_void_p),
+                ("rot_cs", ctypes.c_void_p), ("rot_idx", ctypes.c_void_p), ("svec", ctypes.c_void_p),
+                ("N", ctypes.c_int64), ("K", ctypes.c_int64), ("group", ctypes.c_int32), ("n_rot", ctypes.c_int32)]
+
+
+# (name, restype, argtypes) of every symbol declared in include/paro.h
+_P, _I64, _I32, _U32, _SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_size_t
+_PP = ctypes.POINTER(paro_packed)
+SIGNATURES = {
+    "paro_pack_sizes": (ctypes.c_int, [_I64, _I64, _I32, _I32, ctypes.POINTER(paro_packed_sizes)]),
+    "paro_pack": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _I32, _I32, _I32, _PP, _P]),
+    "paro_linear_workspace": (_SZ, [_I64, _I64, _I64, _I32, _I32, _I32, _U32]),
+    "paro_linear": (ctypes.c_int, [_P, ctypes.c_int, _I64, _PP, _P, _P, _P, _I32, _P, _P, ctypes.c_int, _U32, _P,
+                                   _SZ, _P]),
+    "paro_transform_activations": (ctypes.c_int, [_P, ctypes.c_int, _I64, _PP, _P, _P]),
+    "paro_unpack_logical": (ctypes.c_int, [_PP, _P, _P, _P, _P]),
+    "paro_comm_unique_id": (ctypes.c_int, [_P]),
+    "paro_comm_init": (ctypes.c_int, [_P, _I32, _I32, ctypes.POINTER(ctypes.c_void_p)]),
+    "paro_comm_destroy": (ctypes.c_int, [_P]),
+    "paro_linear_allgather_workspace": (_SZ, [_I64, _I64, _I64, _I32, ctypes.c_int, _U32]),
+    "paro_linear_allgather": (ctypes.c_int, [_P, ctypes.c_int, _I64, _PP, _P, _P, ctypes.c_int, _U32, _P, _SZ, _P,
+                                             _I32, _I32, _P]),
+    "paro_last_error": (ctypes.c_char_p, []),
+    "paro_version": (ctypes.c_char_p, []),
+}
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_lib = _load()
+
+
+def last_error() -> str:
+    return (_lib.paro_last_error() or b"").decode()
+
+
+def _check(st: int) -> None:
+    if st != PARO_OK:
+        raise ParoError(st, last_error())
+
+
+# ---------------------------------------------------------------- torch marshalling helpers
+def _torch():
+    import torch
+    return torch
+
+
+def _stream(stream=None) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _dt(t) -> int:
+    torch = _torch()
+    return {torch.float16: PARO_F16, torch.bfloat16: PARO_BF16, torch.float32: PARO_F32}[t.dtype]
+
+
+@dataclass
+class PackedLinear:
+    """Device buffers of one packed linear layer (caller-owned torch tensors) and the
+    C struct that points at them."""
+    codes: object
+    scales: object
+    zeros: object
+    rot_cs: object
+    rot_idx: object
+    svec: object
+    N: int
+    K: int
+    n_rot: int
+
+    def struct(self) -> paro_packed:
+        return paro_packed(_ptr(self.codes), _ptr(self.scales), _ptr(self.zeros), _ptr(self.rot_cs),
+                           _ptr(self.rot_idx), _ptr(self.svec), self.N, self.K, GROUP, self.n_rot)
+
+    def nbytes_algorithmic(self) -> int:
+        """W4A16 bytes the GEMV must stream: codes + fp16 scales + uint4 zeros."""
+        G = self.K // GROUP
+        return self.N * self.K // 2 + self.N * G * 2 + self.N * G // 2
+
+
+def paro_pack_sizes(N: int, K: int, group: int = GROUP, n_rot: int = 8) -> paro_packed_sizes:
+    out = paro_packed_sizes()
+    _check(_lib.paro_pack_sizes(N, K, group, n_rot, ctypes.byref(out)))
+    return out
+
+
+def alloc_packed(N: int, K: int, n_rot: int = 8, device="cuda") -> PackedLinear:
+    torch = _torch()
+    sz = paro_pack_sizes(N, K, GROUP, n_rot)
+
+    def buf(n):
+        return torch.empty(max(int(n), 16), dtype=torch.uint8, device=device)
+
+    return PackedLinear(buf(sz.codes), buf(sz.scales), buf(sz.zeros), buf(sz.rot_cs), buf(sz.rot_idx),
+                        buf(sz.svec), N, K, n_rot)
+
+
+def paro_pack(W, s, theta, pairs, group: int = GROUP, out: PackedLinear | None = None, stream=None) -> PackedLinear:
+    """W fp16 [N,K], s fp32 [K], theta fp32 [K/128,L,P], pairs int16 [K/128,L,P,2] (all CUDA)."""
+    N, K = W.shape
+    L = 0 if theta is None else theta.shape[1]
+    P = 0 if theta is None else theta.shape[2]
+    if out is None:
+        out = alloc_packed(N, K, L, device=W.device)
+    st = out.struct()
+    _check(_lib.paro_pack(_ptr(W), _ptr(s), _ptr(theta), _ptr(pairs), N, K, group, L, P, ctypes.byref(st),
+                          _stream(stream)))
+    return out
+
+
+def paro_linear_workspace(B: int, N: int, K: int, n_rot: int = 8, n_pairs: int = 64, on_the_fly: bool = False,
+                          flags: int = 0) -> int:
+    return int(_lib.paro_linear_workspace(B, N, K, n_rot, n_pairs, int(on_the_fly), flags))
+
+
+def paro_linear(x, packed: PackedLinear, s=None, theta=None, pairs=None, bias=None, y=None, out_dtype=None,
+                flags: int = 0, workspace=None, stream=None):
+    """y[B,N] = transform(x) . dequant(Q)^T + bias.  x fp16/bf16 [B,K] (CUDA)."""
+    torch = _torch()
+    B = x.shape[0]
+    if y is None:
+        y = torch.empty((B, packed.N), dtype=out_dtype or x.dtype, device=x.device)
+    P = 0 if theta is None else theta.shape[2]
+    need = paro_linear_workspace(B, packed.N, packed.K, packed.n_rot, P or 64, s is not None, flags)
+    if need and (workspace is None or workspace.numel() < need):
+        workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+    st = packed.struct()
+    _check(_lib.paro_linear(_ptr(x), _dt(x), B, ctypes.byref(st), _ptr(s), _ptr(theta), _ptr(pairs), P, _ptr(bias),
+                            _ptr(y), _dt(y), flags, _ptr(workspace), 0 if workspace is None else workspace.numel(),
+                            _stream(stream)))
+    return y
+
+
+def paro_transform_activations(x, packed: PackedLinear, out=None, stream=None):
+    torch = _torch()
+    if out is None:
+        out = torch.empty(x.shape, dtype=torch.float16, device=x.device)
+    st = packed.struct()
+    _check(_lib.paro_transform_activations(_ptr(x), _dt(x), x.shape[0], ctypes.byref(st), _ptr(out),
+                                           _stream(stream)))
+    return out
+
+
+def paro_unpack_logical(packed: PackedLinear, stream=None):
+    torch = _torch()
+    dev = packed.codes.device
+    G = packed.K // GROUP
+    codes = torch.empty((packed.N, packed.K), dtype=torch.uint8, device=dev)
+    scales = torch.empty((packed.N, G), dtype=torch.float16, device=dev)
+    zeros = torch.empty((packed.N, G), dtype=torch.uint8, device=dev)
+    st = packed.struct()
+    _check(_lib.paro_unpack_logical(ctypes.byref(st), _ptr(codes), _ptr(scales), _ptr(zeros), _stream(stream)))
+    return codes, scales, zeros
+
+
+# ---------------------------------------------------------------- NCCL-sharded linear
+def paro_comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.paro_comm_unique_id(buf))
+    return buf.raw
+
+
+def paro_comm_init(uid: bytes, rank: int, world: int) -> int:
+    comm = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(uid, 128)
+    _check(_lib.paro_comm_init(buf, rank, world, ctypes.byref(comm)))
+    return comm.value
+
+
+def paro_comm_destroy(comm: int) -> None:
+    _check(_lib.paro_comm_destroy(comm))
+
+
+def paro_linear_allgather(x, packed_shard: PackedLinear, comm: int, rank: int, world: int, bias_shard=None, y=None,
+                          out_dtype=None, flags: int = 0, workspace=None, stream=None):
+    torch = _torch()
+    B = x.shape[0]
+    N = packed_shard.N * world
+    if y is None:
+        y = torch.empty((B, N), dtype=out_dtype or x.dtype, device=x.device)
+    need = int(_lib.paro_linear_allgather_workspace(B, packed_shard.N, packed_shard.K, world, _dt(y), flags))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+    st = packed_shard.struct()
+    _check(_lib.paro_linear_allgather(_ptr(x), _dt(x), B, ctypes.byref(st), _ptr(bias_shard), _ptr(y), _dt(y), flags,
+                                      _ptr(workspace), workspace.numel(), comm, rank, world, _stream(stream)))
+    return y
+
+
+def shard_rows(N: int, world: int, rank: int) -> tuple[int, int]:
+    """Row range [r0, r1) of output channels owned by `rank`."""
+    if N % world:
+        raise ParoError(PARO_ERR_SHAPE, f"N={N} not divisible by world={world}")
+    n = N // world
+    return rank * n, (rank + 1) * n
+
+
+def version() -> str:
+    return _lib.paro_version().decode()

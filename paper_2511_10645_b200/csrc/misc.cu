@@ -1,0 +1,178 @@
+// misc.cu -- standalone activation transform (prefill pre-stage / microbenchmark),
+// on-the-fly transform preparation, logical unpack (tests), all-gather permute.
+#include <cstdint>
+
+#include "paro_internal.h"
+#include "ptx.cuh"
+
+namespace paro {
+
+constexpr int TGRP = 128;
+constexpr int TOK_PER_WARP = 8;
+
+// x' = R_L ... R_1 diag(s) x per (token, group); Eq. 5 in column form,
+// the scale first.  One warp = one group x TOK_PER_WARP tokens; the
+// rotation parameters of the group (L <= 8 rotations x 2 slots per lane) stay in
+// registers ("the rotation parameters ... fit into registers"), the
+// 128 activations of the group in shared memory.
+__global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__ x, int x_bf16, int64_t B, int64_t K,
+                                                        int L, const float* __restrict__ svec,
+                                                        const float2* __restrict__ rot_cs,
+                                                        const uchar2* __restrict__ rot_idx, int rotate,
+                                                        __half* __restrict__ xo, int pdl) {
+  __shared__ float scr_all[8][132];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* scr = scr_all[warp];
+  const int G = static_cast<int>(K / TGRP);
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + warp;  // (token tile, group)
+  const int gam = static_cast<int>(item % G);
+  const int64_t b0 = (item / G) * TOK_PER_WARP;
+  if (b0 >= B) return;
+  float2 cs0[8], cs1[8];
+  uchar2 ix0[8], ix1[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    if (t < L && rotate) {
+      const int64_t e = (static_cast<int64_t>(gam) * L + t) * 64;
+      cs0[t] = rot_cs[e + lane];
+      cs1[t] = rot_cs[e + lane + 32];
+      ix0[t] = rot_idx[e + lane];
+      ix1[t] = rot_idx[e + lane + 32];
+    } else {
+      cs0[t] = cs1[t] = make_float2(1.f, 0.f);
+      ix0[t] = ix1[t] = make_uchar2(128, 128);
+    }
+  }
+  float sv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) sv[i] = rotate ? svec[gam * TGRP + lane + 32 * i] : 1.f;
+  if (pdl) pdl_wait();
+  for (int64_t b = b0; b < b0 + TOK_PER_WARP && b < B; ++b) {
+    const int64_t base = b * K + static_cast<int64_t>(gam) * TGRP;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = lane + 32 * i;
+      const float v = x_bf16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(x)[base + k])
+                             : __half2float(static_cast<const __half*>(x)[base + k]);
+      scr[k] = v * sv[i];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      if (t >= L || !rotate) break;
+      const float a0 = scr[ix0[t].x], c0 = scr[ix0[t].y];
+      const float a1 = scr[ix1[t].x], c1 = scr[ix1[t].y];
+      scr[ix0[t].x] = cs0[t].x * a0 - cs0[t].y * c0;
+      scr[ix0[t].y] = cs0[t].y * a0 + cs0[t].x * c0;
+      scr[ix1[t].x] = cs1[t].x * a1 - cs1[t].y * c1;
+      scr[ix1[t].y] = cs1[t].y * a1 + cs1[t].x * c1;
+      __syncwarp();
+    }
+    const __half2 h01 = __floats2half2_rn(scr[4 * lane], scr[4 * lane + 1]);
+    const __half2 h23 = __floats2half2_rn(scr[4 * lane + 2], scr[4 * lane + 3]);
+    uint2 pk;
+    pk.x = *reinterpret_cast<const uint32_t*>(&h01);
+    pk.y = *reinterpret_cast<const uint32_t*>(&h23);
+    *reinterpret_cast<uint2*>(xo + base + 4 * lane) = pk;
+    __syncwarp();
+  }
+  if (pdl) pdl_launch_dependents();
+}
+
+cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, int L, const float* svec,
+                             const float2* rot_cs, const uchar2* rot_idx, int rotate, void* x_out, int pdl,
+                             cudaStream_t st) {
+  const int64_t G = K / TGRP;
+  const int64_t items = ((B + TOK_PER_WARP - 1) / TOK_PER_WARP) * G;
+  const int64_t blocks = (items + 7) / 8;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (pdl) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, transform_kernel, x, x_bf16, B, K, L, svec, rot_cs, rot_idx, rotate,
+                            static_cast<__half*>(x_out), pdl);
+}
+
+// On-the-fly preparation of (cos, sin, i, j) from device theta / pairs (no validation).
+__global__ void prepare_transform_kernel(const float* __restrict__ theta, const int16_t* __restrict__ pairs, int G,
+                                         int L, int P, float2* __restrict__ rot_cs, uchar2* __restrict__ rot_idx) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // (gamma, t, slot<64)
+  if (e >= static_cast<int64_t>(G) * L * 64) return;
+  const int slot = static_cast<int>(e % 64);
+  const int64_t gt = e / 64;
+  float2 cs = make_float2(1.f, 0.f);
+  uchar2 ij = make_uchar2(128, 128);
+  if (slot < P) {
+    const int64_t src = gt * P + slot;
+    const int i = pairs[2 * src], j = pairs[2 * src + 1];
+    if (i >= 0 && j >= 0 && i < 128 && j < 128) {
+      float s, c;
+      sincosf(theta[src], &s, &c);
+      cs = make_float2(c, s);
+      ij = make_uchar2(static_cast<unsigned char>(i), static_cast<unsigned char>(j));
+    }
+  }
+  rot_cs[e] = cs;
+  rot_idx[e] = ij;
+}
+
+cudaError_t launch_prepare_transform(const float* theta, const int16_t* pairs, int G, int L, int P, float2* rot_cs,
+                                     uchar2* rot_idx, cudaStream_t st) {
+  const int64_t n = static_cast<int64_t>(G) * L * 64;
+  if (n == 0) return cudaSuccess;
+  prepare_transform_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(theta, pairs, G, L, P, rot_cs,
+                                                                                   rot_idx);
+  return cudaGetLastError();
+}
+
+__global__ void unpack_kernel(const uint8_t* __restrict__ codes, const uint8_t* __restrict__ zeros, int64_t N,
+                              int64_t K, uint8_t* __restrict__ cu8, uint8_t* __restrict__ zu8) {
+  const int64_t G = K / TGRP, ZB = (G + 1) / 2;
+  const int64_t tot = N * (K / 2);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < tot;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint8_t b = codes[i];
+    cu8[2 * i] = b & 15;
+    cu8[2 * i + 1] = b >> 4;
+  }
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < N * G;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t n = i / G, g = i % G;
+    const uint8_t b = zeros[n * ZB + g / 2];
+    zu8[i] = (g & 1) ? (b >> 4) : (b & 15);
+  }
+}
+
+cudaError_t launch_unpack(const uint8_t* codes, const uint8_t* zeros, int64_t N, int64_t K, uint8_t* codes_u8,
+                          uint8_t* zeros_u8, cudaStream_t st) {
+  unpack_kernel<<<1024, 256, 0, st>>>(codes, zeros, N, K, codes_u8, zeros_u8);
+  return cudaGetLastError();
+}
+
+// [world][B][Ns] (rank-major all-gather result) -> [B][world*Ns]
+__global__ void permute_gather_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int world,
+                                      int64_t B, int64_t Ns, int eb) {
+  const int64_t tot = static_cast<int64_t>(world) * B * Ns;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < tot;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / (B * Ns), rem = i % (B * Ns), b = rem / Ns, n = rem % Ns;
+    const int64_t d = b * (world * Ns) + r * Ns + n;
+    for (int e = 0; e < eb; ++e) dst[d * eb + e] = src[i * eb + e];
+  }
+}
+
+cudaError_t launch_permute_gather(const void* src, void* dst, int world, int64_t B, int64_t Ns, int elem_bytes,
+                                  cudaStream_t st) {
+  permute_gather_kernel<<<256, 256, 0, st>>>(static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), world, B,
+                                             Ns, elem_bytes);
+  return cudaGetLastError();
+}
+
+}  // namespace paro

@@ -1,0 +1,436 @@
+// paro_api.cu -- the C ABI declared in include/paro.h: argument checking, host-side
+// transform preparation (paro_pack), kernel dispatch, NCCL all-gather.
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <set>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/paro.h"
+#include "paro_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+paro_status fail(paro_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+paro_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(PARO_ERR_CUDA, "%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+constexpr int kG = PARO_GROUP;
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+size_t dtype_bytes(paro_dtype d) { return d == PARO_F32 ? 4 : 2; }
+
+size_t align256(size_t v) { return (v + 255) / 256 * 256; }
+
+}  // namespace
+
+extern "C" {
+
+const char* paro_last_error(void) { return g_err.c_str(); }
+const char* paro_version(void) { return "paro-b200 0.1 (sm_100a)"; }
+
+paro_status paro_pack_sizes(int64_t N, int64_t K, int32_t group, int32_t n_rot, paro_packed_sizes* out) {
+  if (!out) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_pack_sizes: out is NULL");
+  if (N <= 0 || K <= 0) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_pack_sizes: N and K must be > 0");
+  if (group != kG) return fail(PARO_ERR_UNSUPPORTED, "paro_pack_sizes: group must be 128 (got %d)", group);
+  if (K % kG) return fail(PARO_ERR_UNSUPPORTED, "paro_pack_sizes: K %% 128 != 0 (K=%lld)", (long long)K);
+  if (n_rot < 0 || n_rot > PARO_MAX_ROT)
+    return fail(PARO_ERR_UNSUPPORTED, "paro_pack_sizes: n_rot must be in [0, 8] (got %d)", n_rot);
+  const int64_t G = K / kG;
+  out->codes = static_cast<size_t>(N * K / 2);
+  out->scales = static_cast<size_t>(N * G * 2 + 16);
+  out->zeros = static_cast<size_t>(N * ceil_div(G, 2) + 16);
+  out->rot_cs = static_cast<size_t>(G * n_rot * PARO_SLOTS * 8);
+  out->rot_idx = static_cast<size_t>(G * n_rot * PARO_SLOTS * 2);
+  out->svec = static_cast<size_t>(K * 4);
+  return PARO_OK;
+}
+
+paro_status paro_pack(const void* W, const float* s, const float* theta, const int16_t* pairs, int64_t N, int64_t K,
+                      int32_t group, int32_t n_rot, int32_t n_pairs, paro_packed* out, void* stream) {
+  paro_packed_sizes sz;
+  paro_status st = paro_pack_sizes(N, K, group, n_rot, &sz);
+  if (st != PARO_OK) return st;
+  if (!W || !s || !out) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_pack: W, s, out must be non-NULL");
+  if (n_rot > 0 && (!theta || !pairs))
+    return fail(PARO_ERR_INVALID_ARGUMENT, "paro_pack: theta/pairs must be non-NULL when n_rot > 0");
+  if (n_rot > 0 && (n_pairs < 1 || n_pairs > PARO_SLOTS))
+    return fail(PARO_ERR_INVALID_ARGUMENT, "paro_pack: n_pairs must be in [1, 64] (got %d)", n_pairs);
+  if (!out->codes || !out->scales || !out->zeros || !out->svec || (n_rot > 0 && (!out->rot_cs || !out->rot_idx)))
+    return fail(PARO_ERR_INVALID_ARGUMENT, "paro_pack: packed buffers must be allocated");
+  if (!aligned16(W) || !aligned16(out->codes) || !aligned16(out->scales) || !aligned16(out->zeros) ||
+      !aligned16(out->svec) || !aligned16(out->rot_cs) || !aligned16(out->rot_idx))
+    return fail(PARO_ERR_INVALID_ARGUMENT, "paro_pack: buffers must be 16-byte aligned");
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  const int64_t G = K / kG;
+  const int L = n_rot, P = n_rot > 0 ? n_pairs : 0;
+
+  // ---- copy the (small) transform to the host and validate it
+  std::vector<float> hs(K), hth(static_cast<size_t>(G * L * P));
+  std::vector<int16_t> hpr(static_cast<size_t>(G * L * P * 2));
+  cudaError_t e = cudaMemcpyAsync(hs.data(), s, K * 4, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess && L > 0)
+    e = cudaMemcpyAsync(hth.data(), theta, hth.size() * 4, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess && L > 0)
+    e = cudaMemcpyAsync(hpr.data(), pairs, hpr.size() * 2, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  if (e != cudaSuccess) return cuda_fail(e, "paro_pack: copying s/theta/pairs");
+  for (int64_t k = 0; k < K; ++k)
+    if (!std::isfinite(hs[k]) || !(hs[k] > 0.f))
+      return fail(PARO_ERR_INVALID_ARGUMENT, "paro_pack: s[%lld] must be finite and > 0", (long long)k);
+  // prepared transform: fp64 (cos, sin) for the fold, fp32 copies + u8 indices for the runtime
+  std::vector<double> cs64(static_cast<size_t>(G * L * PARO_SLOTS * 2), 0.0);
+  std::vector<float> cs32(static_cast<size_t>(G * L * PARO_SLOTS * 2), 0.f);
+  std::vector<uint8_t> idx(static_cast<size_t>(G * L * PARO_SLOTS * 2), 128);
+  for (int64_t g = 0; g < G; ++g) {
+    std::set<std::pair<int, int>> seen;
+    for (int t = 0; t < L; ++t) {
+      bool used[kG] = {false};
+      for (int p = 0; p < PARO_SLOTS; ++p) {
+        const size_t o = static_cast<size_t>((g * L + t) * PARO_SLOTS + p);
+        cs64[2 * o] = 1.0;
+        cs32[2 * o] = 1.f;
+        if (p >= P) continue;
+        const size_t src = static_cast<size_t>((g * L + t) * P + p);
+        const int i = hpr[2 * src], j = hpr[2 * src + 1];
+        if (i == -1 && j == -1) continue;  // absent slot (short rotation)
+        if (i < 0 || j < 0 || i >= kG || j >= kG)
+          return fail(PARO_ERR_PAIRS, "pairs[%lld,%d,%d] = (%d,%d) out of [0,128)", (long long)g, t, p, i, j);
+        if (!(i < j)) return fail(PARO_ERR_PAIRS, "pairs[%lld,%d,%d] = (%d,%d): need i < j", (long long)g, t, p, i, j);
+        if (used[i] || used[j])
+          return fail(PARO_ERR_PAIRS, "rotation (%lld,%d) uses a channel twice (Definition 1)", (long long)g, t);
+        used[i] = used[j] = true;
+        if (!seen.insert({i, j}).second)
+          return fail(PARO_ERR_PAIRS, "group %lld repeats pair (%d,%d) across rotations", (long long)g, i, j);
+        const float th = hth[src];
+        if (!std::isfinite(th))
+          return fail(PARO_ERR_INVALID_ARGUMENT, "theta[%lld,%d,%d] is not finite", (long long)g, t, p);
+        const double c = std::cos(static_cast<double>(th)), sn = std::sin(static_cast<double>(th));
+        cs64[2 * o] = c;
+        cs64[2 * o + 1] = sn;
+        cs32[2 * o] = static_cast<float>(c);
+        cs32[2 * o + 1] = static_cast<float>(sn);
+        idx[2 * o] = static_cast<uint8_t>(i);
+        idx[2 * o + 1] = static_cast<uint8_t>(j);
+      }
+    }
+  }
+  // ---- device temporaries: fp64 (cos, sin) table, status word
+  const size_t cs_bytes = cs64.size() * sizeof(double);
+  const size_t tmp_bytes = align256(cs_bytes) + 256;
+  void* tmp = nullptr;
+  e = cudaMallocAsync(&tmp, tmp_bytes, cs);
+  if (e != cudaSuccess) return cuda_fail(e, "paro_pack: cudaMallocAsync");
+  uint8_t* tb = static_cast<uint8_t*>(tmp);
+  int* status = reinterpret_cast<int*>(tb + align256(cs_bytes));
+  e = cudaMemsetAsync(status, 0, 4, cs);
+  if (e == cudaSuccess && cs_bytes) e = cudaMemcpyAsync(tb, cs64.data(), cs_bytes, cudaMemcpyHostToDevice, cs);
+  if (e == cudaSuccess && L > 0) e = cudaMemcpyAsync(out->rot_cs, cs32.data(), cs32.size() * 4, cudaMemcpyHostToDevice, cs);
+  if (e == cudaSuccess && L > 0) e = cudaMemcpyAsync(out->rot_idx, idx.data(), idx.size(), cudaMemcpyHostToDevice, cs);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out->svec, s, K * 4, cudaMemcpyDeviceToDevice, cs);
+  // zero the padding tails of scales/zeros (read by 16-byte bulk copies)
+  if (e == cudaSuccess) e = cudaMemsetAsync(static_cast<uint8_t*>(out->scales) + N * G * 2, 0, 16, cs);
+  if (e == cudaSuccess) e = cudaMemsetAsync(static_cast<uint8_t*>(out->zeros) + N * ceil_div(G, 2), 0, 16, cs);
+  // idx buffer for the fold: same u8 table; use the packed rot_idx when L > 0
+  if (e == cudaSuccess)
+    e = paro::launch_pack(W, s, tb, out->rot_idx, N, K, L, out->codes, out->scales, out->zeros, status, cs);
+  int hstatus = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&hstatus, status, 4, cudaMemcpyDeviceToHost, cs);
+  cudaError_t e2 = cudaFreeAsync(tmp, cs);
+  if (e == cudaSuccess) e = e2;
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  if (e != cudaSuccess) return cuda_fail(e, "paro_pack");
+  if (hstatus & 1) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_pack: W (or the folded W) is not finite");
+  if (hstatus & 2) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_pack: a group's fp16 scale overflows");
+  out->N = N;
+  out->K = K;
+  out->group = group;
+  out->n_rot = n_rot;
+  return PARO_OK;
+}
+
+static bool use_prefill(int64_t B, int64_t N, int64_t K, uint32_t flags) {
+  if (flags & PARO_LINEAR_FORCE_GEMV) return false;
+  if (!paro::prefill_supported(B, N, K)) return false;
+  return (flags & PARO_LINEAR_FORCE_GEMM) || B > 16;
+}
+
+size_t paro_linear_workspace(int64_t B, int64_t N, int64_t K, int32_t n_rot, int32_t n_pairs, int32_t on_the_fly,
+                             uint32_t flags) {
+  (void)n_pairs;
+  size_t ws = 0;
+  if (on_the_fly && n_rot > 0) {
+    const int64_t G = K / kG;
+    ws += align256(static_cast<size_t>(G * n_rot * PARO_SLOTS * 8));
+    ws += align256(static_cast<size_t>(G * n_rot * PARO_SLOTS * 2));
+  }
+  if (use_prefill(B, N, K, flags)) ws += align256(static_cast<size_t>(B * K * 2));
+  return ws;
+}
+
+static paro_status check_packed(const paro_packed* p) {
+  if (!p) return fail(PARO_ERR_INVALID_ARGUMENT, "packed is NULL");
+  if (p->group != kG) return fail(PARO_ERR_UNSUPPORTED, "packed->group must be 128");
+  if (p->N <= 0 || p->K <= 0 || p->K % kG) return fail(PARO_ERR_SHAPE, "packed has invalid N/K");
+  if (p->n_rot < 0 || p->n_rot > PARO_MAX_ROT) return fail(PARO_ERR_UNSUPPORTED, "packed->n_rot out of [0, 8]");
+  if (!p->codes || !p->scales || !p->zeros || !p->svec || (p->n_rot > 0 && (!p->rot_cs || !p->rot_idx)))
+    return fail(PARO_ERR_INVALID_ARGUMENT, "packed buffers must be non-NULL");
+  if (!aligned16(p->codes) || !aligned16(p->scales) || !aligned16(p->zeros) || !aligned16(p->svec) ||
+      !aligned16(p->rot_cs) || !aligned16(p->rot_idx))
+    return fail(PARO_ERR_INVALID_ARGUMENT, "packed buffers must be 16-byte aligned");
+  return PARO_OK;
+}
+
+paro_status paro_linear(const void* x, paro_dtype x_dtype, int64_t B, const paro_packed* packed, const float* s,
+                        const float* theta, const int16_t* pairs, int32_t n_pairs, const float* bias, void* y,
+                        paro_dtype y_dtype, uint32_t flags, void* workspace, size_t workspace_bytes, void* stream) {
+  paro_status st = check_packed(packed);
+  if (st != PARO_OK) return st;
+  if (!x || !y) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear: x and y must be non-NULL");
+  if (B <= 0) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear: B must be > 0");
+  if (x_dtype != PARO_F16 && x_dtype != PARO_BF16)
+    return fail(PARO_ERR_UNSUPPORTED, "paro_linear: x must be fp16 or bf16");
+  if (y_dtype != PARO_F16 && y_dtype != PARO_BF16 && y_dtype != PARO_F32)
+    return fail(PARO_ERR_UNSUPPORTED, "paro_linear: y must be fp16, bf16 or fp32");
+  if (!aligned16(x) || !aligned16(y)) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear: x, y must be 16-byte aligned");
+  const int on_the_fly = (s || theta || pairs) ? 1 : 0;
+  const int64_t N = packed->N, K = packed->K, G = K / kG;
+  const int L = packed->n_rot;
+  if (on_the_fly && (!s || (L > 0 && (!theta || !pairs))))
+    return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear: give all of s/theta/pairs or none");
+  if (on_the_fly && L > 0 && (n_pairs < 1 || n_pairs > PARO_SLOTS))
+    return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear: n_pairs must be in [1, 64]");
+  const size_t need = paro_linear_workspace(B, N, K, L, n_pairs, on_the_fly, flags);
+  if (workspace_bytes < need || (need && !workspace))
+    return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear: workspace too small (%zu < %zu)", workspace_bytes, need);
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  const int rotate = (flags & PARO_LINEAR_NO_ROTATION) ? 0 : 1;
+  const int pdl = (flags & PARO_LINEAR_PDL) ? 1 : 0;
+  const float2* rot_cs = static_cast<const float2*>(packed->rot_cs);
+  const uchar2* rot_idx = static_cast<const uchar2*>(packed->rot_idx);
+  const float* svec = static_cast<const float*>(packed->svec);
+  uint8_t* wsp = static_cast<uint8_t*>(workspace);
+  if (on_the_fly) {
+    svec = s;
+    if (L > 0) {
+      float2* wcs = reinterpret_cast<float2*>(wsp);
+      wsp += align256(static_cast<size_t>(G * L * PARO_SLOTS * 8));
+      uchar2* widx = reinterpret_cast<uchar2*>(wsp);
+      wsp += align256(static_cast<size_t>(G * L * PARO_SLOTS * 2));
+      cudaError_t e = paro::launch_prepare_transform(theta, pairs, static_cast<int>(G), L, n_pairs, wcs, widx, cs);
+      if (e != cudaSuccess) return cuda_fail(e, "paro_linear: prepare transform");
+      rot_cs = wcs;
+      rot_idx = widx;
+    }
+  }
+  const size_t xe = 2, ye = dtype_bytes(y_dtype);
+  if (use_prefill(B, N, K, flags)) {
+    void* xq = wsp;
+    cudaError_t e = paro::launch_transform(x, x_dtype == PARO_BF16, B, K, L, svec, rot_cs, rot_idx, rotate, xq, pdl, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "paro_linear: activation transform");
+    e = paro::launch_prefill_gemm(xq, B, static_cast<const uint8_t*>(packed->codes),
+                                  static_cast<const uint8_t*>(packed->scales), static_cast<const uint8_t*>(packed->zeros),
+                                  bias, y, static_cast<int>(y_dtype), N, K, pdl, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "paro_linear: prefill GEMM");
+    return PARO_OK;
+  }
+  // decode GEMV over token tiles
+  int bt = B >= 4 ? 4 : (B >= 2 ? 2 : 1);
+  paro::GemvConfig cfg;
+  const char* why = "";
+  while (!paro::plan_gemv(bt, N, K, L, rotate, &cfg, &why)) {
+    if (bt == 1) return fail(PARO_ERR_UNSUPPORTED, "paro_linear: %s", why);
+    bt /= 2;
+  }
+  for (int64_t b0 = 0; b0 < B; b0 += cfg.BT) {
+    paro::GemvArgs& a = cfg.a;
+    a.x = static_cast<const uint8_t*>(x) + b0 * K * xe;
+    a.x_bf16 = x_dtype == PARO_BF16;
+    a.B = static_cast<int>(std::min<int64_t>(cfg.BT, B - b0));
+    a.codes = static_cast<const uint8_t*>(packed->codes);
+    a.scales = static_cast<const uint8_t*>(packed->scales);
+    a.zeros = static_cast<const uint8_t*>(packed->zeros);
+    a.rot_cs = rot_cs;
+    a.rot_idx = rot_idx;
+    a.svec = svec;
+    a.bias = bias;
+    a.y = static_cast<uint8_t*>(y) + b0 * N * ye;
+    a.y_dtype = static_cast<int>(y_dtype);
+    a.pdl = pdl;
+    cudaError_t e = paro::launch_gemv(cfg, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "paro_linear: decode GEMV launch");
+  }
+  return PARO_OK;
+}
+
+paro_status paro_transform_activations(const void* x, paro_dtype x_dtype, int64_t B, const paro_packed* packed,
+                                       void* x_out, void* stream) {
+  paro_status st = check_packed(packed);
+  if (st != PARO_OK) return st;
+  if (!x || !x_out || B <= 0) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_transform_activations: bad x/x_out/B");
+  if (x_dtype != PARO_F16 && x_dtype != PARO_BF16) return fail(PARO_ERR_UNSUPPORTED, "x must be fp16 or bf16");
+  cudaError_t e = paro::launch_transform(x, x_dtype == PARO_BF16, B, packed->K, packed->n_rot,
+                                         static_cast<const float*>(packed->svec),
+                                         static_cast<const float2*>(packed->rot_cs),
+                                         static_cast<const uchar2*>(packed->rot_idx), 1, x_out, 0,
+                                         static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "paro_transform_activations");
+  return PARO_OK;
+}
+
+paro_status paro_unpack_logical(const paro_packed* packed, void* codes_u8, void* scales_f16, void* zeros_u8,
+                                void* stream) {
+  paro_status st = check_packed(packed);
+  if (st != PARO_OK) return st;
+  if (!codes_u8 || !scales_f16 || !zeros_u8) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_unpack_logical: NULL output");
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  const int64_t N = packed->N, K = packed->K, G = K / kG;
+  cudaError_t e = cudaMemcpyAsync(scales_f16, packed->scales, N * G * 2, cudaMemcpyDeviceToDevice, cs);
+  if (e == cudaSuccess)
+    e = paro::launch_unpack(static_cast<const uint8_t*>(packed->codes), static_cast<const uint8_t*>(packed->zeros), N,
+                            K, static_cast<uint8_t*>(codes_u8), static_cast<uint8_t*>(zeros_u8), cs);
+  if (e != cudaSuccess) return cuda_fail(e, "paro_unpack_logical");
+  return PARO_OK;
+}
+
+// ============================================================================ NCCL (dlopen)
+typedef struct {
+  char internal[PARO_NCCL_UNIQUE_ID_BYTES];
+} nccl_uid_t;
+typedef int (*nccl_get_uid_fn)(nccl_uid_t*);
+typedef int (*nccl_init_rank_fn)(void**, int, nccl_uid_t, int);
+typedef int (*nccl_destroy_fn)(void*);
+typedef int (*nccl_allgather_fn)(const void*, void*, size_t, int, void*, cudaStream_t);
+typedef const char* (*nccl_errstr_fn)(int);
+
+static struct {
+  std::once_flag once;
+  void* h = nullptr;
+  nccl_get_uid_fn get_uid = nullptr;
+  nccl_init_rank_fn init_rank = nullptr;
+  nccl_destroy_fn destroy = nullptr;
+  nccl_allgather_fn allgather = nullptr;
+  nccl_errstr_fn errstr = nullptr;
+} g_nccl;
+
+static bool nccl_load() {
+  std::call_once(g_nccl.once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      g_nccl.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+      if (!g_nccl.h) g_nccl.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (g_nccl.h) break;
+    }
+    if (!g_nccl.h) return;
+    g_nccl.get_uid = reinterpret_cast<nccl_get_uid_fn>(dlsym(g_nccl.h, "ncclGetUniqueId"));
+    g_nccl.init_rank = reinterpret_cast<nccl_init_rank_fn>(dlsym(g_nccl.h, "ncclCommInitRank"));
+    g_nccl.destroy = reinterpret_cast<nccl_destroy_fn>(dlsym(g_nccl.h, "ncclCommDestroy"));
+    g_nccl.allgather = reinterpret_cast<nccl_allgather_fn>(dlsym(g_nccl.h, "ncclAllGather"));
+    g_nccl.errstr = reinterpret_cast<nccl_errstr_fn>(dlsym(g_nccl.h, "ncclGetErrorString"));
+  });
+  return g_nccl.get_uid && g_nccl.init_rank && g_nccl.destroy && g_nccl.allgather;
+}
+
+static paro_status nccl_fail(int r, const char* where) {
+  return fail(PARO_ERR_NCCL, "%s: nccl error %d (%s)", where, r, g_nccl.errstr ? g_nccl.errstr(r) : "?");
+}
+
+paro_status paro_comm_unique_id(void* uid) {
+  if (!uid) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_comm_unique_id: NULL");
+  if (!nccl_load()) return fail(PARO_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  nccl_uid_t u;
+  int r = g_nccl.get_uid(&u);
+  if (r) return nccl_fail(r, "ncclGetUniqueId");
+  std::memcpy(uid, &u, sizeof(u));
+  return PARO_OK;
+}
+
+paro_status paro_comm_init(const void* uid, int32_t rank, int32_t world, void** comm) {
+  if (!uid || !comm || world < 1 || rank < 0 || rank >= world)
+    return fail(PARO_ERR_INVALID_ARGUMENT, "paro_comm_init: bad arguments");
+  if (!nccl_load()) return fail(PARO_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  nccl_uid_t u;
+  std::memcpy(&u, uid, sizeof(u));
+  int r = g_nccl.init_rank(comm, world, u, rank);
+  if (r) return nccl_fail(r, "ncclCommInitRank");
+  return PARO_OK;
+}
+
+paro_status paro_comm_destroy(void* comm) {
+  if (!comm) return PARO_OK;
+  if (!nccl_load()) return fail(PARO_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  int r = g_nccl.destroy(comm);
+  if (r) return nccl_fail(r, "ncclCommDestroy");
+  return PARO_OK;
+}
+
+size_t paro_linear_allgather_workspace(int64_t B, int64_t N_shard, int64_t K, int32_t world, paro_dtype y_dtype,
+                                       uint32_t flags) {
+  size_t ws = align256(static_cast<size_t>(B * N_shard) * dtype_bytes(y_dtype));  // local y
+  if (B > 1) ws += align256(static_cast<size_t>(world) * B * N_shard * dtype_bytes(y_dtype));  // rank-major gather
+  ws += paro_linear_workspace(B, N_shard, K, PARO_MAX_ROT, PARO_SLOTS, 0, flags);
+  return ws;
+}
+
+paro_status paro_linear_allgather(const void* x, paro_dtype x_dtype, int64_t B, const paro_packed* packed_shard,
+                                  const float* bias_shard, void* y_full, paro_dtype y_dtype, uint32_t flags,
+                                  void* workspace, size_t workspace_bytes, void* comm, int32_t rank, int32_t world,
+                                  void* stream) {
+  paro_status st = check_packed(packed_shard);
+  if (st != PARO_OK) return st;
+  if (!comm || world < 1 || rank < 0 || rank >= world)
+    return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear_allgather: bad comm/rank/world");
+  if (!y_full || !workspace) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear_allgather: NULL y_full/workspace");
+  const int64_t Ns = packed_shard->N, K = packed_shard->K;
+  const size_t need = paro_linear_allgather_workspace(B, Ns, K, world, y_dtype, flags);
+  if (workspace_bytes < need)
+    return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear_allgather: workspace too small (%zu < %zu)", workspace_bytes,
+                need);
+  if (!nccl_load()) return fail(PARO_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  const size_t ye = dtype_bytes(y_dtype);
+  uint8_t* wsp = static_cast<uint8_t*>(workspace);
+  uint8_t* y_local = wsp;
+  wsp += align256(static_cast<size_t>(B * Ns) * ye);
+  uint8_t* gather = nullptr;
+  if (B > 1) {
+    gather = wsp;
+    wsp += align256(static_cast<size_t>(world) * B * Ns * ye);
+  }
+  const size_t rest = workspace_bytes - static_cast<size_t>(wsp - static_cast<uint8_t*>(workspace));
+  st = paro_linear(x, x_dtype, B, packed_shard, nullptr, nullptr, nullptr, 0, bias_shard, y_local, y_dtype, flags, wsp,
+                   rest, stream);
+  if (st != PARO_OK) return st;
+  // all-gather y over NVLink/NVSwitch on the same stream (rank-major [world][B][Ns])
+  int r = g_nccl.allgather(y_local, B > 1 ? gather : y_full, static_cast<size_t>(B * Ns) * ye, /*ncclInt8*/ 0, comm,
+                           cs);
+  if (r) return nccl_fail(r, "ncclAllGather");
+  if (B > 1) {
+    cudaError_t e = paro::launch_permute_gather(gather, y_full, world, B, Ns, static_cast<int>(ye), cs);
+    if (e != cudaSuccess) return cuda_fail(e, "paro_linear_allgather: permute");
+  }
+  return PARO_OK;
+}
+
+}  // extern "C"

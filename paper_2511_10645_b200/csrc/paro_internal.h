@@ -1,0 +1,70 @@
+// paro_internal.h -- declarations shared by the host API and the kernels (not installed).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace paro {
+
+// ---------------------------------------------------------------- pack
+cudaError_t launch_pack(const void* W, const float* s, const void* cs64, const void* idx, int64_t N, int64_t K, int L,
+                        void* codes, void* scales, void* zeros, int* status, cudaStream_t st);
+
+// ---------------------------------------------------------------- decode GEMV
+struct GemvArgs {
+  const void* x;  // [B][K] fp16 / bf16
+  int x_bf16;
+  int B;          // live tokens in this launch (<= BT)
+  const uint8_t* codes;
+  const uint8_t* scales;  // fp16 bytes
+  const uint8_t* zeros;
+  const float2* rot_cs;
+  const uchar2* rot_idx;
+  const float* svec;
+  const float* bias;
+  void* y;  // [B][N]
+  int y_dtype;
+  int N, K, G, L;
+  int rotate;
+  int pdl;
+  int WK;         // warps along K (one 512*J K-slice each)
+  int RG;         // row groups (warps along rows)
+  int SR;         // rows per stage (even)
+  int S;          // ring depth
+  int rows_base, rows_extra, rows_max;
+  uint32_t slot_bytes, sc_off, z_off;  // per-stage slot layout
+  uint32_t off_u, off_scr, off_part, off_ring, off_bar, smem_total;
+};
+
+struct GemvConfig {
+  int BT, J, CL, grid;
+  GemvArgs a;
+};
+
+// Plan a launch (pure host arithmetic, no CUDA calls except a cached device query).
+bool plan_gemv(int B_tile, int64_t N, int64_t K, int L, int rotate, GemvConfig* cfg, const char** why);
+cudaError_t launch_gemv(const GemvConfig& cfg, cudaStream_t st);
+
+// ---------------------------------------------------------------- activation transform (prefill pre-stage)
+cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, int L, const float* svec,
+                             const float2* rot_cs, const uchar2* rot_idx, int rotate, void* x_out, int pdl,
+                             cudaStream_t st);
+
+// ---------------------------------------------------------------- on-the-fly transform preparation
+cudaError_t launch_prepare_transform(const float* theta, const int16_t* pairs, int G, int L, int P, float2* rot_cs,
+                                     uchar2* rot_idx, cudaStream_t st);
+
+// ---------------------------------------------------------------- misc
+cudaError_t launch_unpack(const uint8_t* codes, const uint8_t* zeros, int64_t N, int64_t K, uint8_t* codes_u8,
+                          uint8_t* zeros_u8, cudaStream_t st);
+cudaError_t launch_permute_gather(const void* src, void* dst, int world, int64_t B, int64_t Ns, int elem_bytes,
+                                  cudaStream_t st);
+
+// ---------------------------------------------------------------- prefill GEMM (tcgen05)
+bool prefill_supported(int64_t B, int64_t N, int64_t K);
+cudaError_t launch_prefill_gemm(const void* xq /*fp16 [B][K]*/, int64_t B, const uint8_t* codes, const uint8_t* scales,
+                                const uint8_t* zeros, const float* bias, void* y, int y_dtype, int64_t N, int64_t K,
+                                int pdl, cudaStream_t st);
+
+int device_sm_count();
+
+}  // namespace paro

@@ -1,0 +1,204 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle on the same seeded
+inputs.  Bar (north_star): packed codes / fp16 scales / zeros bit-exact; outputs within
+normwise max-relative error 2e-3 of the quantised oracle."""
+import math
+import zlib
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-3
+
+
+@pytest.fixture(scope="module")
+def paro():
+    import paper_2511_10645_b200 as m
+    return m
+
+
+def dev_tensors(p):
+    d = torch.device("cuda")
+    out = dict(W=torch.from_numpy(p["W"]).to(d), s=torch.from_numpy(p["s"]).to(d),
+               theta=torch.from_numpy(p["theta"]).to(d), pairs=torch.from_numpy(p["pairs"]).to(d))
+    if p["x"].dtype == np.float32:          # bf16 request
+        out["x"] = torch.from_numpy(p["x"]).to(d).to(torch.bfloat16)
+    else:
+        out["x"] = torch.from_numpy(p["x"]).to(d)
+    out["bias"] = None if p["bias"] is None else torch.from_numpy(p["bias"]).to(d)
+    return out
+
+
+def x_as_used(t):
+    """The exact activation values the GPU saw (bf16 rounding happens in torch)."""
+    return t["x"].float().cpu().numpy()
+
+
+def check_pack(paro, p, t, rows=None):
+    packed = paro.paro_pack(t["W"], t["s"], t["theta"], t["pairs"])
+    codes, scales, zeros = (a.cpu().numpy() for a in paro.paro_unpack_logical(packed))
+    Wn = p["W"] if rows is None else p["W"][rows]
+    ref = O.oracle_pack(Wn, p["s"], p["theta"], p["pairs"])
+    if rows is not None:
+        codes, scales, zeros = codes[rows], scales[rows], zeros[rows]
+    assert np.array_equal(scales.view(np.uint16), ref["scales"].view(np.uint16)), \
+        f"{np.sum(scales.view(np.uint16) != ref['scales'].view(np.uint16))} scales differ"
+    assert np.array_equal(zeros, ref["zeros"]), f"{np.sum(zeros != ref['zeros'])} zeros differ"
+    assert np.array_equal(codes, ref["codes"]), f"{np.sum(codes != ref['codes'])} codes differ"
+    return packed, ref
+
+
+CASES = {
+    "P1_c1": dict(N=256, K=256, B=1),
+    "P2_identity": dict(N=256, K=256, B=1, theta_mode="zero", s_mode="ones"),
+    "P4_quarter": dict(N=256, K=256, B=1, theta_mode="quarter"),
+    "P4_eighth": dict(N=256, K=256, B=1, theta_mode="eighth"),
+    "P5_outliers_zero_group": dict(N=1024, K=4096, B=3, zero_group=True),
+    "ragged_rows": dict(N=389 * 2 + 1, K=640, B=2, with_bias=True),
+    "qwen_k2560": dict(N=1024, K=2560, B=1),
+    "bigK_9728": dict(N=512, K=9728, B=1),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_pack_and_linear(paro, name):
+    kw = dict(CASES[name])
+    N, K, B = kw.pop("N"), kw.pop("K"), kw.pop("B")
+    p = synth.make_problem(N, K, B, seed=zlib.crc32(name.encode()) % 1000, **kw)
+    t = dev_tensors(p)
+    packed, ref = check_pack(paro, p, t)
+    y = paro.paro_linear(t["x"], packed, bias=t["bias"])
+    y_ref = O.oracle_linear(x_as_used(t), ref, p["s"], p["theta"], p["pairs"], bias=p["bias"])
+    err = O.normwise_error(y.float().cpu().numpy(), y_ref)
+    assert err <= TOL, f"{name}: normwise error {err:.3e}"
+
+
+def test_single_pair_closed_form(paro):
+    p = synth.single_pair_problem(N=256, K=256, group=1, layer=3, i=5, j=77, theta=math.pi / 4)
+    t = dev_tensors(p)
+    packed, ref = check_pack(paro, p, t)
+    y = paro.paro_linear(t["x"], packed)
+    y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"])
+    assert O.normwise_error(y.float().cpu().numpy(), y_ref) <= TOL
+
+
+def test_short_layers(paro):
+    p = synth.force_short_layers(synth.make_problem(512, 1024, 2, seed=21), seed=3, frac=0.2)
+    t = dev_tensors(p)
+    packed, ref = check_pack(paro, p, t)
+    y = paro.paro_linear(t["x"], packed)
+    y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"])
+    assert O.normwise_error(y.float().cpu().numpy(), y_ref) <= TOL
+
+
+@pytest.mark.parametrize("n_rot", [0, 2, 4])
+def test_fewer_rotations(paro, n_rot):
+    """Table 6 varies #IR in {0, 2, 4, 8}."""
+    p = synth.make_problem(256, 512, 1, seed=30 + n_rot, n_rot=max(n_rot, 1))
+    if n_rot == 0:
+        p["theta"] = p["theta"][:, :0]
+        p["pairs"] = p["pairs"][:, :0]
+    else:
+        p["theta"] = p["theta"][:, :n_rot].copy()
+        p["pairs"] = p["pairs"][:, :n_rot].copy()
+    t = dev_tensors(p)
+    packed, ref = check_pack(paro, p, t)
+    y = paro.paro_linear(t["x"], packed)
+    y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"])
+    assert O.normwise_error(y.float().cpu().numpy(), y_ref) <= TOL
+
+
+@pytest.mark.parametrize("B", [1, 2, 3, 4, 7, 16])
+def test_batch_tails(paro, B):
+    p = synth.make_problem(1024, 4096, B, seed=40 + B)
+    t = dev_tensors(p)
+    packed, ref = check_pack(paro, p, t)
+    y = paro.paro_linear(t["x"], packed, flags=paro.PARO_LINEAR_FORCE_GEMV)
+    y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"])
+    assert O.normwise_error(y.float().cpu().numpy(), y_ref) <= TOL
+
+
+@pytest.mark.parametrize("out_dtype", ["f16", "bf16", "f32"])
+def test_dtypes(paro, out_dtype):
+    """bf16 activations in, fp16/bf16/fp32 out.  bf16 output is compared against
+    bf16_rne(y_ref) with 2e-3*max|y_ref| + half a bf16 ulp."""
+    p = synth.make_problem(512, 1024, 2, seed=50, x_dtype="bf16")
+    t = dev_tensors(p)
+    packed, ref = check_pack(paro, p, t)
+    odt = {"f16": torch.float16, "bf16": torch.bfloat16, "f32": torch.float32}[out_dtype]
+    y = paro.paro_linear(t["x"], packed, out_dtype=odt).float().cpu().numpy()
+    y_ref = O.oracle_linear(x_as_used(t), ref, p["s"], p["theta"], p["pairs"])
+    if out_dtype == "bf16":
+        yr = torch.from_numpy(y_ref).to(torch.bfloat16).float().numpy()
+        ulp = np.abs(yr) * 2.0 ** -8
+        assert np.all(np.abs(y - yr) <= TOL * np.max(np.abs(y_ref)) + ulp)
+    else:
+        assert O.normwise_error(y, y_ref) <= TOL
+
+
+def test_no_rotation_flag_is_plain_w4a16(paro):
+    """PARO_LINEAR_NO_ROTATION: u = x (overhead baseline) == oracle dot without the transform."""
+    p = synth.make_problem(512, 1024, 1, seed=60)
+    t = dev_tensors(p)
+    packed, ref = check_pack(paro, p, t)
+    y = paro.paro_linear(t["x"], packed, flags=paro.PARO_LINEAR_NO_ROTATION)
+    y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"], rotate=False)
+    assert O.normwise_error(y.float().cpu().numpy(), y_ref) <= TOL
+
+
+def test_on_the_fly_transform(paro):
+    p = synth.make_problem(256, 512, 2, seed=61)
+    t = dev_tensors(p)
+    packed, ref = check_pack(paro, p, t)
+    y = paro.paro_linear(t["x"], packed, s=t["s"], theta=t["theta"], pairs=t["pairs"])
+    y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"])
+    assert O.normwise_error(y.float().cpu().numpy(), y_ref) <= TOL
+
+
+def test_transform_activations(paro):
+    """Activation side alone (Eq. 5 in column form): fp16 x' within fp16 rounding of the oracle."""
+    p = synth.make_problem(8, 1024, 37, seed=62)
+    t = dev_tensors(p)
+    packed, _ = check_pack(paro, p, t)
+    xp = paro.paro_transform_activations(t["x"], packed).float().cpu().numpy()
+    ref = O.transform_activations(p["x"], p["s"], p["theta"], p["pairs"])
+    assert np.all(np.abs(xp - ref) <= 2.0 ** -10 * np.abs(ref) + 1e-6 * np.max(np.abs(ref)))
+
+
+def test_pack_errors(paro):
+    p = synth.make_problem(64, 256, 1, seed=63)
+    t = dev_tensors(p)
+    bad = t["pairs"].clone()
+    bad[0, 0, 1] = bad[0, 0, 0]
+    with pytest.raises(paro.ParoError) as e:
+        paro.paro_pack(t["W"], t["s"], t["theta"], bad)
+    assert e.value.kind == "pairs"
+    s_bad = t["s"].clone()
+    s_bad[5] = -1.0
+    with pytest.raises(paro.ParoError) as e:
+        paro.paro_pack(t["W"], s_bad, t["theta"], t["pairs"])
+    assert e.value.kind == "invalid_argument"
+    W_bad = t["W"].clone()
+    W_bad[3, 7] = float("inf")
+    with pytest.raises(paro.ParoError) as e:
+        paro.paro_pack(W_bad, t["s"], t["theta"], t["pairs"])
+    assert e.value.kind == "invalid_argument"
+
+
+@pytest.mark.parametrize("name,N,K", [("q_proj", 4096, 4096), ("down_proj", 4096, 14336), ("gate_proj", 14336, 4096)])
+def test_full_size_sampled(paro, name, N, K):
+    """BASELINE configs[1] at full size, in the launch configuration bench.py times:
+    pack bit-exact and outputs within tolerance on sampled rows (rows are independent
+    in the fold, the RTN and the dot, so the oracle runs on the sampled rows only)."""
+    p = synth.make_problem(N, K, 1, seed=70)
+    t = dev_tensors(p)
+    rows = np.sort(np.random.default_rng(0).choice(N, size=64, replace=False))
+    packed, ref = check_pack(paro, p, t, rows=rows)
+    y = paro.paro_linear(t["x"], packed, flags=paro.PARO_LINEAR_PDL).float().cpu().numpy()[:, rows]
+    y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"])
+    assert O.normwise_error(y, y_ref) <= TOL

@@ -194,20 +194,22 @@ def run_paro(args):
         """Graph of `steps` consecutive steps (layers cycle through the pool); returns
         max-over-ranks ms per step measured with CUDA events on the launch stream."""
         gph = capture(flags, steps)
-        for _ in range(max(1, warmup // max(steps, 1) + 1)):
-            gph.replay()
-        stream.synchronize()
-        t_end = time.time() + args.load_s  # untimed load so the clock sampler sees the loaded state
-        while time.time() < t_end:
-            gph.replay()
+        with torch.cuda.stream(stream):
+            for _ in range(max(1, warmup // max(steps, 1) + 1)):
+                gph.replay()
             stream.synchronize()
+            t_end = time.time() + args.load_s  # untimed load so the clock sampler sees the loaded state
+            while time.time() < t_end:
+                gph.replay()
+                stream.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        gph.replay()
-        e1.record(stream)
+        with torch.cuda.stream(stream):  # CUDAGraph.replay() launches on the current stream
+            e0.record(stream)
+            gph.replay()
+            e1.record(stream)
         e1.synchronize()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / steps
@@ -242,12 +244,13 @@ def run_paro(args):
                             lin = [e for e in pool[li % n_layers] if e[0] == name][0]
                             paro.paro_linear(xs[K], lin[3], y=ys[name], flags=fl | paro.PARO_LINEAR_PDL,
                                              workspace=ws, stream=stream)
-                gph.replay()
-                stream.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                gph.replay()
-                e1.record(stream)
+                with torch.cuda.stream(stream):
+                    gph.replay()
+                    stream.synchronize()
+                    e0.record(stream)
+                    gph.replay()
+                    e1.record(stream)
                 e1.synchronize()
                 res[tag] = e0.elapsed_time(e1) / reps * 1000.0  # us
             ab, wb = algorithmic_bytes(N, K, B)

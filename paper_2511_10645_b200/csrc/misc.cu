@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
                                                         int L, const float* __restrict__ svec,
                                                         const float2* __restrict__ rot_cs,
                                                         const uchar2* __restrict__ rot_idx, int rotate,
-                                                        __half* __restrict__ xo, int pdl) {
+                                                        __half* __restrict__ xo, int pdl, int perm8) {
   __shared__ float scr_all[8][132];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* scr = scr_all[warp];
@@ -68,8 +68,13 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
       scr[ix1[t].y] = cs1[t].y * a1 + cs1[t].x * c1;
       __syncwarp();
     }
-    const __half2 h01 = __floats2half2_rn(scr[4 * lane], scr[4 * lane + 1]);
-    const __half2 h23 = __floats2half2_rn(scr[4 * lane + 2], scr[4 * lane + 3]);
+    // natural order: lane writes channels 4l..4l+3.  perm8 (prefill operand order): each
+    // 8-channel block stored as (0,4,1,5,2,6,3,7); lane writes half (l&1) of block l/2.
+    const int b8 = (lane >> 1) * 8, hh = lane & 1;
+    const int c0 = perm8 ? b8 + 2 * hh : 4 * lane;
+    const int d = perm8 ? 4 : 1;
+    const __half2 h01 = __floats2half2_rn(scr[c0], scr[c0 + d]);
+    const __half2 h23 = __floats2half2_rn(scr[c0 + (perm8 ? 1 : 2)], scr[c0 + (perm8 ? 5 : 3)]);
     uint2 pk;
     pk.x = *reinterpret_cast<const uint32_t*>(&h01);
     pk.y = *reinterpret_cast<const uint32_t*>(&h23);
@@ -81,7 +86,7 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
 
 cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, int L, const float* svec,
                              const float2* rot_cs, const uchar2* rot_idx, int rotate, void* x_out, int pdl,
-                             cudaStream_t st) {
+                             int perm8, cudaStream_t st) {
   const int64_t G = K / TGRP;
   const int64_t items = ((B + TOK_PER_WARP - 1) / TOK_PER_WARP) * G;
   const int64_t blocks = (items + 7) / 8;
@@ -97,7 +102,7 @@ cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, in
     cfg.numAttrs = 1;
   }
   return cudaLaunchKernelEx(&cfg, transform_kernel, x, x_bf16, B, K, L, svec, rot_cs, rot_idx, rotate,
-                            static_cast<__half*>(x_out), pdl);
+                            static_cast<__half*>(x_out), pdl, perm8);
 }
 
 // On-the-fly preparation of (cos, sin, i, j) from device theta / pairs (no validation).

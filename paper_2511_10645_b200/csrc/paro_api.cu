@@ -247,7 +247,7 @@ paro_status paro_linear(const void* x, paro_dtype x_dtype, int64_t B, const paro
   const size_t xe = 2, ye = dtype_bytes(y_dtype);
   if (use_prefill(B, N, K, flags)) {
     void* xq = wsp;
-    cudaError_t e = paro::launch_transform(x, x_dtype == PARO_BF16, B, K, L, svec, rot_cs, rot_idx, rotate, xq, pdl, cs);
+    cudaError_t e = paro::launch_transform(x, x_dtype == PARO_BF16, B, K, L, svec, rot_cs, rot_idx, rotate, xq, pdl, 1, cs);
     if (e != cudaSuccess) return cuda_fail(e, "paro_linear: activation transform");
     e = paro::launch_prefill_gemm(xq, B, static_cast<const uint8_t*>(packed->codes),
                                   static_cast<const uint8_t*>(packed->scales), static_cast<const uint8_t*>(packed->zeros),
@@ -293,7 +293,7 @@ paro_status paro_transform_activations(const void* x, paro_dtype x_dtype, int64_
   cudaError_t e = paro::launch_transform(x, x_dtype == PARO_BF16, B, packed->K, packed->n_rot,
                                          static_cast<const float*>(packed->svec),
                                          static_cast<const float2*>(packed->rot_cs),
-                                         static_cast<const uchar2*>(packed->rot_idx), 1, x_out, 0,
+                                         static_cast<const uchar2*>(packed->rot_idx), 1, x_out, 0, 0,
                                          static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "paro_transform_activations");
   return PARO_OK;

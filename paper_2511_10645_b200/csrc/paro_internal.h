@@ -47,7 +47,7 @@ cudaError_t launch_gemv(const GemvConfig& cfg, cudaStream_t st);
 // ---------------------------------------------------------------- activation transform (prefill pre-stage)
 cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, int L, const float* svec,
                              const float2* rot_cs, const uchar2* rot_idx, int rotate, void* x_out, int pdl,
-                             cudaStream_t st);
+                             int perm8, cudaStream_t st);
 
 // ---------------------------------------------------------------- on-the-fly transform preparation
 cudaError_t launch_prepare_transform(const float* theta, const int16_t* pairs, int G, int L, int P, float2* rot_cs,

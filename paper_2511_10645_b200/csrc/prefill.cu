@@ -1,13 +1,303 @@
-// prefill.cu -- placeholder until the tcgen05 GEMM lands.
+// prefill.cu -- prefill path (B > 16 tokens): tcgen05 / TMEM GEMM with an in-kernel
+// INT4 -> fp16 dequant producer (epilogue a8).
+//
+//   y[t, n] = sum_k x'[t, k] * S[n, k/128] * (q[n, k] - z[n, k/128])   (+ bias[n])
+//
+// Orientation: the WEIGHTS are the MMA's M operand (128 rows per CTA tile) and live in
+// TMEM: four dequant warps turn packed nibbles into fp16 (q - z) * S (exact
+// subtraction, one rounding in the multiply) and write them with tcgen05.st straight
+// into tensor memory -- the A operand of tcgen05.mma may come from TMEM, so the
+// dequantised weights never touch shared memory.  The rotated activations x' (fp16,
+// produced by the transform pre-stage into an L2-resident workspace) are the N
+// operand (256 tokens per tile), loaded by TMA with 128-byte swizzle into a
+// shared-memory ring.  One elected thread issues tcgen05.mma (M=128, N=256, K=16)
+// into a 128 x 256 fp32 accumulator in TMEM; four epilogue warps read it back with
+// tcgen05.ld, add the bias, convert and store y.
+//
+// The pre-stage stores x' with each 8-channel block permuted to
+// (0,4,1,5,2,6,3,7): the same permutation along K on both operands leaves the
+// contraction unchanged and lets the dequant producer emit fp16 pairs straight from
+// two AND/OR masks per 32-bit code word (no byte permutes).
+//
+// Warp roles (384 threads, persistent over tiles):
+//   warp 0: TMA producer (x' tiles)     warp 1: MMA issuer     warp 2: TMEM allocator
+//   warps 4-7: dequant -> TMEM (A)      warps 8-11: epilogue (TMEM -> y)
+#include <cuda.h>
+#include <cuda_fp16.h>
+
+#include <cstdint>
+#include <mutex>
+
 #include "paro_internal.h"
+#include "ptx.cuh"
+#include "umma.cuh"
 
 namespace paro {
 
-bool prefill_supported(int64_t, int64_t, int64_t) { return false; }
+constexpr int PF_BM = 128;    // weight rows per tile (MMA M)
+constexpr int PF_BN = 256;    // tokens per tile (MMA N)
+constexpr int PF_BK = 64;     // K per pipeline stage (4 MMAs of K=16)
+constexpr int PF_SX = 4;      // x' shared-memory stages (32 KB each)
+constexpr int PF_SA = 4;      // A (dequantised weight) TMEM stages (32 columns each)
+constexpr int PF_ACC_COL = 0;
+constexpr int PF_A_COL = 256;
+constexpr int PF_TMEM_COLS = 512;
+constexpr int PF_THREADS = 384;
+constexpr uint32_t PF_X_STAGE_BYTES = PF_BN * PF_BK * 2;
 
-cudaError_t launch_prefill_gemm(const void*, int64_t, const uint8_t*, const uint8_t*, const uint8_t*, const float*,
-                                void*, int, int64_t, int64_t, int, cudaStream_t) {
-  return cudaErrorNotSupported;
+struct PrefillArgs {
+  const uint8_t* codes;
+  const __half* scales;
+  const uint8_t* zeros;
+  const float* bias;
+  void* y;
+  int y_dtype;
+  int B, N, K;
+  int pdl;
+};
+
+__device__ __forceinline__ uint32_t hsub_hmul(uint32_t v, uint32_t zz, uint32_t ss) {
+  __half2 a = *reinterpret_cast<__half2*>(&v);
+  __half2 z = *reinterpret_cast<__half2*>(&zz);
+  __half2 s = *reinterpret_cast<__half2*>(&ss);
+  __half2 r = __hmul2(__hsub2(a, z), s);  // (1024+q) - (1024+z) exact, then one rounding
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+
+__global__ void __launch_bounds__(PF_THREADS, 1)
+    prefill_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const PrefillArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* xs = smem;  // PF_SX * 32 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + PF_SX * PF_X_STAGE_BYTES);
+  uint64_t* x_full = bars;
+  uint64_t* x_empty = x_full + PF_SX;
+  uint64_t* a_full = x_empty + PF_SX;
+  uint64_t* a_empty = a_full + PF_SA;
+  uint64_t* acc_full = a_empty + PF_SA;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_base_sh = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_row_tiles = a.N / PF_BM;
+  const int n_tok_tiles = (a.B + PF_BN - 1) / PF_BN;
+  const int n_tiles = n_row_tiles * n_tok_tiles;
+  const int n_ks = a.K / PF_BK;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < PF_SX; ++i) {
+      mbar_init(&x_full[i], 1);
+      mbar_init(&x_empty[i], 1);
+    }
+    for (int i = 0; i < PF_SA; ++i) {
+      mbar_init(&a_full[i], 128);
+      mbar_init(&a_empty[i], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 128);
+    fence_mbar_init();
+    prefetch_tmap(&tmap_x);
+  }
+  if (warp == 2) tmem_alloc(tmem_base_sh, PF_TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_base_sh;
+  if (a.pdl) pdl_wait();  // x' is written by the pre-stage kernel
+
+  if (warp == 0) {
+    // ---------------- TMA producer: x' tiles [256 tokens x 64 K] (SW128)
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int tok0 = (tile / n_row_tiles) * PF_BN;
+        for (int ks = 0; ks < n_ks; ++ks, ++it) {
+          const int s = it % PF_SX;
+          mbar_wait(&x_empty[s], ((it / PF_SX) & 1) ^ 1);
+          mbar_arrive_expect_tx(&x_full[s], PF_X_STAGE_BYTES);
+          tma_load_2d(xs + s * PF_X_STAGE_BYTES, &tmap_x, ks * PF_BK, tok0, &x_full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread)
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_f16_f32(PF_BM, PF_BN);
+      uint32_t it = 0, tcount = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
+        mbar_wait(acc_empty, (tcount & 1) ^ 1);
+        tc_fence_after();
+        for (int ks = 0; ks < n_ks; ++ks, ++it) {
+          const int sx = it % PF_SX, sa = it % PF_SA;
+          mbar_wait(&a_full[sa], (it / PF_SA) & 1);
+          mbar_wait(&x_full[sx], (it / PF_SX) & 1);
+          tc_fence_after();
+          const uint64_t bdesc = smem_desc_sw128(xs + sx * PF_X_STAGE_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < PF_BK / 16; ++kk) {
+            mma_f16_ts(tbase + PF_ACC_COL, tbase + PF_A_COL + sa * 32 + kk * 8, bdesc + static_cast<uint64_t>(kk * 2),
+                       idesc, (ks | kk) ? 1u : 0u);
+          }
+          mma_commit(&x_empty[sx]);
+          mma_commit(&a_empty[sa]);
+        }
+        mma_commit(acc_full);
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ---------------- dequant producer: weight row r of the tile -> TMEM lane r
+    const int r = (warp - 4) * 32 + lane;
+    const uint32_t lane_addr = static_cast<uint32_t>((warp - 4) * 32) << 16;
+    const int G = a.K / 128, ZB = (G + 1) / 2;
+    uint32_t it = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const int n = (tile % n_row_tiles) * PF_BM + r;
+      const uint8_t* crow = a.codes + static_cast<int64_t>(n) * (a.K / 2);
+      uint4 c0 = __ldg(reinterpret_cast<const uint4*>(crow));
+      uint4 c1 = __ldg(reinterpret_cast<const uint4*>(crow + 16));
+      uint32_t ss = 0, zz = 0;
+      for (int ks = 0; ks < n_ks; ++ks, ++it) {
+        const int k0 = ks * PF_BK;
+        if ((k0 & 127) == 0) {
+          const int g = k0 >> 7;
+          const __half S = a.scales[static_cast<int64_t>(n) * G + g];
+          const uint8_t zb = a.zeros[static_cast<int64_t>(n) * ZB + (g >> 1)];
+          const int z = (g & 1) ? (zb >> 4) : (zb & 15);
+          const __half2 S2 = __halves2half2(S, S);
+          const __half zh = __ushort_as_half(static_cast<unsigned short>(0x6400 + z));  // 1024 + z
+          const __half2 Z2 = __halves2half2(zh, zh);
+          ss = *reinterpret_cast<const uint32_t*>(&S2);
+          zz = *reinterpret_cast<const uint32_t*>(&Z2);
+        }
+        const uint4 w0 = c0, w1 = c1;
+        if (ks + 1 < n_ks) {  // prefetch the next 32 code bytes of this row
+          c0 = __ldg(reinterpret_cast<const uint4*>(crow + (k0 + PF_BK) / 2));
+          c1 = __ldg(reinterpret_cast<const uint4*>(crow + (k0 + PF_BK) / 2 + 16));
+        }
+        uint32_t v[32];
+        const uint32_t wd[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const uint32_t w = wd[m];
+          v[4 * m + 0] = hsub_hmul((w & 0x000F000Fu) | 0x64006400u, zz, ss);          // (k0, k4)
+          v[4 * m + 1] = hsub_hmul(((w >> 4) & 0x000F000Fu) | 0x64006400u, zz, ss);   // (k1, k5)
+          v[4 * m + 2] = hsub_hmul(((w >> 8) & 0x000F000Fu) | 0x64006400u, zz, ss);   // (k2, k6)
+          v[4 * m + 3] = hsub_hmul(((w >> 12) & 0x000F000Fu) | 0x64006400u, zz, ss);  // (k3, k7)
+        }
+        const int sa = it % PF_SA;
+        mbar_wait(&a_empty[sa], ((it / PF_SA) & 1) ^ 1);
+        tc_fence_after();
+        tmem_st32(tbase + lane_addr + PF_A_COL + sa * 32, v);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&a_full[sa]);
+      }
+    }
+  } else if (warp >= 8) {
+    // ---------------- epilogue: accumulator lane r = weight row, column = token
+    const int r = (warp - 8) * 32 + lane;
+    const uint32_t lane_addr = static_cast<uint32_t>((warp - 8) * 32) << 16;
+    uint32_t tcount = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
+      const int n = (tile % n_row_tiles) * PF_BM + r;
+      const int tok0 = (tile / n_row_tiles) * PF_BN;
+      const float bv = a.bias ? a.bias[n] : 0.f;
+      mbar_wait(acc_full, tcount & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < PF_BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tbase + lane_addr + PF_ACC_COL + c * 32, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int t = tok0 + c * 32 + i;
+          if (t < a.B) {
+            const float f = __uint_as_float(v[i]) + bv;
+            const int64_t o = static_cast<int64_t>(t) * a.N + n;
+            if (a.y_dtype == 0)
+              static_cast<__half*>(a.y)[o] = __float2half_rn(f);
+            else if (a.y_dtype == 1)
+              static_cast<__nv_bfloat16*>(a.y)[o] = __float2bfloat16_rn(f);
+            else
+              static_cast<float*>(a.y)[o] = f;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(acc_empty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (a.pdl) pdl_launch_dependents();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tbase, PF_TMEM_COLS);
+  }
+}
+
+// ============================================================================ host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+bool prefill_supported(int64_t B, int64_t N, int64_t K) {
+  return B >= 1 && N % PF_BM == 0 && K % PF_BK == 0 && K >= PF_BK && N <= (int64_t(1) << 30) && B < (1 << 30);
+}
+
+cudaError_t launch_prefill_gemm(const void* xq, int64_t B, const uint8_t* codes, const uint8_t* scales,
+                                const uint8_t* zeros, const float* bias, void* y, int y_dtype, int64_t N, int64_t K,
+                                int pdl, cudaStream_t st) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  CUtensorMap tmap;
+  cuuint64_t gdim[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(B)};
+  cuuint64_t gstride[1] = {static_cast<cuuint64_t>(K) * 2};
+  cuuint32_t box[2] = {PF_BK, PF_BN};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(xq), gdim, gstride, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  PrefillArgs a{codes, reinterpret_cast<const __half*>(scales), zeros, bias, y, y_dtype, static_cast<int>(B),
+                static_cast<int>(N), static_cast<int>(K), pdl};
+  const size_t smem = 1024 + PF_SX * PF_X_STAGE_BYTES + 256;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t tiles = (N / PF_BM) * ((B + PF_BN - 1) / PF_BN);
+  const int grid = static_cast<int>(tiles < device_sm_count() ? tiles : device_sm_count());
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(PF_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  if (pdl) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, prefill_gemm_kernel, tmap, a);
 }
 
 }  // namespace paro

@@ -202,3 +202,28 @@ def test_full_size_sampled(paro, name, N, K):
     y = paro.paro_linear(t["x"], packed, flags=paro.PARO_LINEAR_PDL).float().cpu().numpy()[:, rows]
     y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"])
     assert O.normwise_error(y, y_ref) <= TOL
+
+
+@pytest.mark.parametrize("B,N,K", [(300, 256, 512), (17, 384, 1024), (520, 1024, 4096)])
+def test_prefill_gemm(paro, B, N, K):
+    """Prefill path (B > 16): transform pre-stage + tcgen05 GEMM with TMEM dequant producer."""
+    p = synth.make_problem(N, K, B, seed=80 + B, with_bias=True)
+    t = dev_tensors(p)
+    packed, ref = check_pack(paro, p, t)
+    y = paro.paro_linear(t["x"], packed, bias=t["bias"], flags=paro.PARO_LINEAR_FORCE_GEMM)
+    y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"], bias=p["bias"])
+    err = O.normwise_error(y.float().cpu().numpy(), y_ref)
+    assert err <= TOL, f"prefill normwise error {err:.3e}"
+
+
+def test_prefill_full_size_sampled(paro):
+    """configs[3]: LLaMA-3-8B prefill 2048 tokens, q_proj, sampled tokens and rows."""
+    N, K, B = 4096, 4096, 2048
+    p = synth.make_problem(N, K, B, seed=90)
+    t = dev_tensors(p)
+    rows = np.sort(np.random.default_rng(1).choice(N, size=32, replace=False))
+    packed, ref = check_pack(paro, p, t, rows=rows)
+    y = paro.paro_linear(t["x"], packed).float().cpu().numpy()
+    toks = np.sort(np.random.default_rng(2).choice(B, size=64, replace=False))
+    y_ref = O.oracle_linear(p["x"][toks], ref, p["s"], p["theta"], p["pairs"])
+    assert O.normwise_error(y[toks][:, rows], y_ref) <= TOL

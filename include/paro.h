@@ -66,8 +66,11 @@ typedef enum { PARO_F16 = 0, PARO_BF16 = 1, PARO_F32 = 2 } paro_dtype;
  *                        its low nibble, k odd in its high nibble.
  *   scales : N*G*2 + 16  fp16 [N][G] group scales S (G = K/128), +16 B tail pad.
  *   zeros  : N*ceil(G/2) + 16   uint4 zero points [N][G], nibble-packed like codes.
- *   rot_cs : G*L*64*8    fp32 (cos theta, sin theta) per (group, rotation, slot).
- *   rot_idx: G*L*64*2    u8 (i, j) per slot; absent slots hold (128, 128).
+ *   rot_cs : G*L*64*8    fp32 (cos theta, sin theta) per (group, rotation, slot), stored as
+ *                        records [G][L][32][2] (slot = lane + 32*s), the slots of each rotation
+ *                        reordered and oriented so every shared-memory gather/scatter of the
+ *                        runtime transform is bank-conflict free.
+ *   rot_idx: G*L*64*2    u8 (i, j) per slot in the same order.
  *   svec   : K*4         fp32 s.
  * Algorithmic weight bytes are N*K/2 + N*G*2 + N*G/2 (0.5195 B/weight). */
 typedef struct {

@@ -2,35 +2,38 @@
 // into the activation staging, then the group-wise INT4 dequant GEMV.
 //
 // SURVEY.md 8(a) rows a4 (stage + scale), a5 (L rotations, Eq. 5 in column form),
-// a6 (dequant GEMV), a8 (epilogue).  One kernel, launched as clusters of CL CTAs,
-// one CTA per SM:
+// a6 (dequant GEMV), a8 (epilogue).  One kernel, launched as clusters of CL CTAs
+// (1-2 CTAs per SM, one wave):
 //
-//  * producer warp: streams this CTA's contiguous row slice of the packed weight
-//    (INT4 codes / fp16 scales / uint4 zeros, row-major) through a ring of
-//    shared-memory stages (SR rows each) with cp.async.bulk (TMA engine) +
-//    mbarriers.  All stages that fit are issued at kernel start -- before the
-//    programmatic-dependent-launch wait -- so the weight stream overlaps both the
-//    previous kernel's tail and the activation transform below.
+//  * producer warp: bulk-copies (cp.async.bulk, TMA engine) first the activations
+//    this CTA transforms, then its contiguous row slice of the packed weight (INT4
+//    codes / fp16 scales / uint4 zeros, row-major) through a ring of shared-memory
+//    stages (SR rows each), completion tracked by mbarriers.
 //  * compute warps, phase 1 (transform; PAPER.md:195-209's token / group / pair
 //    parallelism): the CL CTAs of a cluster split the K/128 groups; a warp owns a
 //    group, keeps its L rotations' (cos, sin, i, j) in registers (loaded before the
-//    PDL wait: they do not depend on the previous kernel), stages the group's
-//    activations in shared memory, scales by s and applies the L independent
-//    rotations (2 pairs per lane per rotation, sync-free inside a rotation,
-//    __syncwarp between rotations), then writes fp16 x' into every CTA of the
-//    cluster through DSMEM.  x' never goes to HBM.
+//    producer starts, so they do not queue behind the weight stream), stages the
+//    group in shared memory, scales by s and applies the L independent rotations
+//    (2 pairs per lane per rotation, sync-free inside a rotation, __syncwarp
+//    between rotations).  The fp16 x' of the group -- stored with each 8-channel
+//    block in (0,4,1,5,2,6,3,7) order, the register order the dequantiser wants --
+//    and its 32-channel partial sums go to every CTA of the cluster with st.async
+//    (DSMEM), completion counted in bytes on the receiver's mbarrier.  x' never
+//    goes to HBM.
 //  * compute warps, phase 2 (GEMV): warp wk owns a 512*J-wide K slice; half-warp h
-//    handles row 2p+h of each row pair, lane 32 consecutive K per chunk.  x' lives
-//    in registers as fp16 pairs.  Codes are dequantised in registers with one AND
-//    mask per pair of weights: a nibble q in bits [0,4) of an fp16 half IS the
-//    subnormal q*2^-24, in bits [4,8) it is 16q*2^-24; fma.rn.f32.f16 (FHFMA)
+//    handles row 2p+h of each row pair, lane 32*J consecutive K (one 128-group).
+//    x' lives in registers as fp16 pairs.  Codes are dequantised in registers with
+//    one AND mask per pair of weights: a nibble q in bits [0,4) of an fp16 half IS
+//    the subnormal q*2^-24, in bits [4,8) it is 16q*2^-24; fma.rn.f32.f16 (FHFMA)
 //    multiplies-accumulates those into fp32, exactly scaled by powers of two.
 //    Per (row, group): y += S * (sum q x' - z * sum x').  Row partials are reduced
-//    by a transpose-shuffle over the 16 lanes of a half-warp (one per stage of
-//    eight row pairs) and across K-slice warps through shared memory in a fixed
-//    order (deterministic).
+//    by a transpose-shuffle over the 16 lanes of a half-warp (eight row pairs per
+//    stage) and across K-slice warps through shared memory in a fixed order
+//    (deterministic).
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "paro_internal.h"
@@ -42,6 +45,19 @@ constexpr int GRP = 128;
 constexpr float TWO_M24 = 5.9604644775390625e-08f;  // 2^-24
 constexpr float TWO_P24 = 16777216.0f;              // 2^24
 constexpr int RP_PER_STAGE = 8;                     // max row pairs per stage (SR <= 16 rows)
+constexpr int TL_EVENTS = 12;                        // debug timeline: events per CTA
+
+__device__ unsigned long long g_paro_timeline[1024 * TL_EVENTS];
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PARO_TL(a, ev)                                                                             \
+  do {                                                                                             \
+    if ((a).debug && blockIdx.x < 1024) g_paro_timeline[blockIdx.x * TL_EVENTS + (ev)] = gtimer(); \
+  } while (0)
 
 __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
   __half2 h = __floats2half2_rn(a, b);
@@ -62,26 +78,14 @@ __device__ __forceinline__ void store_out(void* y, int dt, int64_t i, float v) {
     static_cast<float*>(y)[i] = v;
 }
 
-// u32 words w0 = (k0,k1), w1 = (k2,k3), w2 = (k4,k5), w3 = (k6,k7) as fp16 pairs ->
-// P[0] = (k0,k4), P[1] = (k1,k5), P[2] = (k2,k6), P[3] = (k3,k7)
-__device__ __forceinline__ void regroup8(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t* P) {
-  P[0] = __byte_perm(w0, w2, 0x5410);
-  P[1] = __byte_perm(w0, w2, 0x7632);
-  P[2] = __byte_perm(w1, w3, 0x5410);
-  P[3] = __byte_perm(w1, w3, 0x7632);
+__device__ __forceinline__ float half2_sum(uint32_t w) {
+  const float2 f = __half22float2(*reinterpret_cast<__half2*>(&w));
+  return f.x + f.y;
 }
 
-__device__ __forceinline__ float sum8_h(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3) {
-  float2 a = __half22float2(*reinterpret_cast<__half2*>(&w0));
-  float2 b = __half22float2(*reinterpret_cast<__half2*>(&w1));
-  float2 c = __half22float2(*reinterpret_cast<__half2*>(&w2));
-  float2 d = __half22float2(*reinterpret_cast<__half2*>(&w3));
-  return ((a.x + a.y) + (b.x + b.y)) + ((c.x + c.y) + (d.x + d.y));
-}
-
-// 2^-24 * sum_{32 k} q_k u_k for one 16-byte chunk of codes (4 words of 8 nibbles).
-// Low nibbles carry q*2^-24, high nibbles 16q*2^-24: two kinds of FHFMA chains, the
-// high ones scaled by 1/16 at the end (exact).
+// One 32-bit code word (8 nibbles, k = 8m..8m+7) against the x' pairs
+// P[0]=(k0,k4), P[1]=(k1,k5), P[2]=(k2,k6), P[3]=(k3,k7): low nibbles carry q*2^-24
+// (chain tl), high nibbles 16q*2^-24 (chain th, scaled by 1/16 at the end, exactly).
 __device__ __forceinline__ void dot_word(uint32_t x, const uint32_t* P, float& tl, float& th) {
   const uint32_t x8 = x >> 8;
   tl = fma_f16lo(x & 0x000F000Fu, P[0], tl);
@@ -94,22 +98,11 @@ __device__ __forceinline__ void dot_word(uint32_t x, const uint32_t* P, float& t
   th = fma_f16hi(x8 & 0x00F000F0u, P[3], th);
 }
 
-__device__ __forceinline__ float dot32(const uint4 c, const uint32_t* P) {
-  float tl0 = 0.f, tl1 = 0.f, th0 = 0.f, th1 = 0.f;
-  dot_word(c.x, P + 0, tl0, th0);
-  dot_word(c.y, P + 4, tl1, th1);
-  dot_word(c.z, P + 8, tl0, th0);
-  dot_word(c.w, P + 12, tl1, th1);
-  return fmaf(0.0625f, th0 + th1, tl0 + tl1);
-}
-
-template <int BT, int J>
-struct GemvThreads {  // register budget: u' (16*J*BT) + row accumulators (8*BT) + ~48
-  static constexpr int value = (BT * J <= 2) ? 544 : 288;
-};
-
-template <int BT, int J>
-__global__ void __launch_bounds__(GemvThreads<BT, J>::value, 1) paro_gemv_kernel(const GemvArgs a) {
+// MAXT: 288 (<= 8 compute warps) or 544 (<= 16 compute warps, very large K);
+// u' occupies 16*J*BT registers per thread (BT * J <= 4).
+template <int BT, int J, int MAXT>
+__global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_gemv_kernel(const GemvArgs a) {
+  constexpr int RP = RP_PER_STAGE / J;  // row pairs per stage: SR = 2 * RP rows
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -119,12 +112,19 @@ __global__ void __launch_bounds__(GemvThreads<BT, J>::value, 1) paro_gemv_kernel
   const int K = a.K, G = a.G, L = a.L;
   const int ZB = (G + 1) >> 1;
   const int SR = a.SR;
+  const int NCH = K / 32;  // 32-channel chunks
 
-  __half* u16 = reinterpret_cast<__half*>(smem + a.off_u);
+  __half* u16 = reinterpret_cast<__half*>(smem + a.off_u);          // x' [BT][K], perm8 order
+  float* usum = reinterpret_cast<float*>(smem + a.off_usum);         // 2^-24 * chunk sums [BT][NCH]
+  uint8_t* xs = smem + a.off_x;                                       // raw x slice [BT][x_cols]
   float* part = reinterpret_cast<float*>(smem + a.off_part);
   uint8_t* ring = smem + a.off_ring;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.off_bar);
   uint64_t* empty = full + a.S;
+  uint64_t* xbar = empty + a.S;  // raw activations landed (bulk copy)
+  uint64_t* xpbar = xbar + 1;    // x' of all K landed (DSMEM st.async from the cluster)
+  uint64_t* pbar = xpbar + 1;    // rotation parameters + s of this CTA's groups landed
+  uint64_t* pfree = pbar + 1;    // phase 1 done with them (their ring slots can be refilled)
 
   const int cta = blockIdx.x;
   const int n_rows = a.rows_base + (cta < a.rows_extra ? 1 : 0);
@@ -132,12 +132,37 @@ __global__ void __launch_bounds__(GemvThreads<BT, J>::value, 1) paro_gemv_kernel
   const int n_stages = (n_rows + SR - 1) / SR;
   const uint32_t CL = cluster_nctarank();
   const uint32_t crank = cluster_ctarank();
+  // groups whose transform this CTA computes
+  const int g_per = (G + static_cast<int>(CL) - 1) / static_cast<int>(CL);
+  const int g0 = min(G, static_cast<int>(crank) * g_per);
+  const int g1 = min(G, g0 + g_per);
+  const int x_cols = (g1 - g0) * GRP;  // activation columns this CTA stages
+  const uint32_t x_row_bytes = static_cast<uint32_t>(x_cols) * 2;
+  // rotation parameters of groups [g0, g1) (lane-major records, contiguous per group) and
+  // s are bulk-copied into the LAST P ring slots before anything else; those slots get
+  // weights only after phase 1 has released them (pfree).
+  const int L_eff = a.rotate ? L : 0;
+  const uint32_t p_cs_bytes = static_cast<uint32_t>(g1 - g0) * 32 * L_eff * 16;
+  const uint32_t p_ix_bytes = static_cast<uint32_t>(g1 - g0) * 32 * L_eff * 4;
+  const uint32_t p_s_bytes = a.rotate ? static_cast<uint32_t>(x_cols) * 4 : 0;
+  // staged parameters: in a dedicated region (param_slots < 0) or in the last
+  // param_slots ring slots (lent until phase 1 is done); 0: read from global memory
+  const bool pded = a.param_slots < 0;
+  const int P = pded ? 0 : a.param_slots;  // lent ring slots
+  const bool pstaged = a.param_slots != 0;
+  uint8_t* pslot = pded ? smem + a.off_param : ring + static_cast<size_t>(a.S - P) * a.slot_bytes;
 
   if (threadIdx.x == 0) {
+    PARO_TL(a, 0);
     for (int i = 0; i < a.S; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], n_compute_warps);
     }
+    mbar_init(xbar, 1);
+    mbar_init(xpbar, 1);
+    mbar_init(pbar, 1);
+    mbar_init(pfree, n_compute_warps);
+    if (CL > 1) mbar_arrive_expect_tx(xpbar, static_cast<uint32_t>(BT) * (K * 2 + NCH * 4));
     fence_mbar_init();
   }
   if (CL > 1) {
@@ -149,9 +174,10 @@ __global__ void __launch_bounds__(GemvThreads<BT, J>::value, 1) paro_gemv_kernel
 
   // ------------------------------------------------------------ producer warp
   if (is_producer) {
-    // Stages [0, S) need no slot release; issue them, then take part in the cluster
-    // barrier that publishes x' (the consumers block on it before releasing any slot),
-    // then stream the rest of the slice.
+    // Request order (latency-critical first): the compute warps' rotation-parameter
+    // loads (handshake on barrier 2), then -- after the PDL wait -- the activations,
+    // then the weight ring.  Stages [0, S) need no slot release.
+    named_bar_sync(2, (n_compute_warps + 1) * 32);
     const uint64_t pol = l2_evict_first_policy();
     auto issue = [&](int st, int slot) {
       const int r0 = row_begin + st * SR;
@@ -168,18 +194,36 @@ __global__ void __launch_bounds__(GemvThreads<BT, J>::value, 1) paro_gemv_kernel
       bulk_g2s(dst + a.sc_off, a.scales + s_lo, sb, &full[slot], pol);
       bulk_g2s(dst + a.z_off, a.zeros + z_lo, zb, &full[slot], pol);
     };
-    const int first = min(a.S, n_stages);
-    if (lane == 0)
-      for (int st = 0; st < first; ++st) issue(st, st);
-    __syncwarp();
-    if (a.rotate && CL > 1) {
-      cluster_arrive();
-      cluster_wait();
+    const int first = min(a.S - P, n_stages);
+    if (lane == 0 && pstaged && x_cols > 0 && L_eff > 0) {
+      // rotation parameters and s: independent of the previous kernel, latency-critical
+      mbar_arrive_expect_tx(pbar, p_cs_bytes + p_ix_bytes + p_s_bytes);
+      bulk_g2s_nohint(pslot, reinterpret_cast<const uint8_t*>(a.rot_cs) + static_cast<size_t>(g0) * 32 * L_eff * 16,
+                      p_cs_bytes, pbar);
+      bulk_g2s_nohint(pslot + p_cs_bytes,
+                      reinterpret_cast<const uint8_t*>(a.rot_idx) + static_cast<size_t>(g0) * 32 * L_eff * 4,
+                      p_ix_bytes, pbar);
+      bulk_g2s_nohint(pslot + p_cs_bytes + p_ix_bytes, a.svec + g0 * GRP, p_s_bytes, pbar);
     }
+    if (a.pdl) pdl_wait();  // x may be produced by the previous kernel on the stream
     if (lane == 0) {
+      if (x_cols > 0) {
+        mbar_arrive_expect_tx(xbar, x_row_bytes * static_cast<uint32_t>(a.B));
+        for (int b = 0; b < a.B; ++b)
+          bulk_g2s_nohint(xs + static_cast<size_t>(b) * x_row_bytes,
+                          static_cast<const uint8_t*>(a.x) + (static_cast<int64_t>(b) * K + g0 * GRP) * 2,
+                          x_row_bytes, xbar);
+      }
+      for (int st = 0; st < first; ++st) issue(st, st);
+      // the lent slots: first use once phase 1 released them, then the normal ring
+      int st = first;
+      if (P > 0) {
+        mbar_wait(pfree, 0);
+        for (; st < min(a.S, n_stages); ++st) issue(st, st);
+      }
       int slot = 0;
       uint32_t phase = 1;  // stages >= S: the ring has wrapped once
-      for (int st = first; st < n_stages; ++st) {
+      for (; st < n_stages; ++st) {
         mbar_wait(&empty[slot], phase ^ 1);  // stage st - S released by all consumers
         issue(st, slot);
         if (++slot == a.S) {
@@ -193,31 +237,61 @@ __global__ void __launch_bounds__(GemvThreads<BT, J>::value, 1) paro_gemv_kernel
   }
 
   // ------------------------------------------------------------ phase 1: activation transform
-  if (a.rotate) {
+  {
     float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * (BT * 132);
-    const int g_per = (G + static_cast<int>(CL) - 1) / static_cast<int>(CL);
-    const int g0 = static_cast<int>(crank) * g_per;
-    const int g1 = min(G, g0 + g_per);
+    const uint32_t u_addr = smem_u32(u16), s_addr = smem_u32(usum), bar_addr = smem_u32(xpbar);
+    const int b8 = (lane >> 1) * 8, hh = lane & 1;  // output: lane writes half hh of 8-block b8
+    const int c0 = b8 + 2 * hh;
     bool first = true;
-    for (int gam = g0 + warp; gam < g1; gam += n_compute_warps) {
+    for (int gam = g0 + warp; gam < g1 || first; gam += n_compute_warps) {
+      const bool have = gam < g1;
       // rotation parameters of this group -> registers (independent of the previous kernel)
-      float2 cs0[8], cs1[8];
-      uchar2 ix0[8], ix1[8];
+      // records [group][t][32 lanes]: (cos0, sin0, cos1, sin1) and (i0, j0, i1, j1)
+      float4 csr[8];
+      uint32_t ixr[8];
+      float sv[4];
+      if (first) {
+        named_bar_arrive(2, (n_compute_warps + 1) * 32);  // let the producer start
+        if (pstaged && x_cols > 0 && L_eff > 0) mbar_wait(pbar, 0);
+        if (x_cols > 0) mbar_wait(xbar, 0);
+        if (threadIdx.x == 0) PARO_TL(a, 1);
+        first = false;
+      }
+      if (have && L_eff > 0) {
+        if (pstaged) {  // staged in shared memory, records [group][t][32 lanes]
+          const float4* csp = reinterpret_cast<const float4*>(pslot) + (gam - g0) * L_eff * 32 + lane;
+          const uint32_t* ixp = reinterpret_cast<const uint32_t*>(pslot + p_cs_bytes) + (gam - g0) * L_eff * 32 + lane;
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        if (t < L) {
-          const int64_t e = (static_cast<int64_t>(gam) * L + t) * 64;
-          cs0[t] = a.rot_cs[e + lane];
-          cs1[t] = a.rot_cs[e + lane + 32];
-          ix0[t] = a.rot_idx[e + lane];
-          ix1[t] = a.rot_idx[e + lane + 32];
+          for (int t = 0; t < 8; ++t)
+            if (t < L_eff) {
+              csr[t] = csp[t * 32];
+              ixr[t] = ixp[t * 32];
+            }
+        } else {
+          const int64_t rec = static_cast<int64_t>(gam) * L * 32 + lane;
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            if (t < L_eff) {
+              csr[t] = __ldg(reinterpret_cast<const float4*>(a.rot_cs) + rec + t * 32);
+              ixr[t] = __ldg(reinterpret_cast<const uint32_t*>(a.rot_idx) + rec + t * 32);
+            }
         }
       }
-      float sv[4];
+      if (have) {
+        // two explicit paths: a runtime-selected shared/global pointer would compile to
+        // generic loads, which queue behind the weight stream
 #pragma unroll
-      for (int i = 0; i < 4; ++i) sv[i] = a.svec[gam * GRP + lane + 32 * i];
-      if (first && a.pdl) pdl_wait();  // x is produced by the previous kernel on the stream
-      first = false;
+        for (int i = 0; i < 4; ++i) {
+          const int k = (gam - g0) * GRP + lane + 32 * i;
+          if (!a.rotate)
+            sv[i] = 1.f;
+          else if (pstaged && L_eff > 0)
+            sv[i] = reinterpret_cast<const float*>(pslot + p_cs_bytes + p_ix_bytes)[k];
+          else
+            sv[i] = __ldg(a.svec + g0 * GRP + k);
+        }
+      }
+      if (!have) break;
       const int kg = gam * GRP;
 #pragma unroll
       for (int b = 0; b < BT; ++b)
@@ -225,167 +299,186 @@ __global__ void __launch_bounds__(GemvThreads<BT, J>::value, 1) paro_gemv_kernel
         for (int i = 0; i < 4; ++i) {
           const int k = lane + 32 * i;
           float v = 0.f;
-          if (b < a.B) v = load_act(a.x, a.x_bf16, static_cast<int64_t>(b) * K + kg + k);
+          if (b < a.B) v = load_act(xs + static_cast<size_t>(b) * x_row_bytes, a.x_bf16, kg - g0 * GRP + k);
           scr[b * 132 + k] = v * sv[i];  // diag(s) x  (a4)
         }
       __syncwarp();
+      if (threadIdx.x == 0 && gam == g0) PARO_TL(a, 8);
 #pragma unroll
       for (int t = 0; t < 8; ++t) {  // a5: rotations t = 1..L, Eq. 4 form, pre-update values
-        if (t >= L) break;
+        if (t >= L_eff) break;
 #pragma unroll
         for (int b = 0; b < BT; ++b) {
           float* sb = scr + b * 132;
-          const float a0 = sb[ix0[t].x], b0 = sb[ix0[t].y];
-          const float a1 = sb[ix1[t].x], b1 = sb[ix1[t].y];
-          sb[ix0[t].x] = cs0[t].x * a0 - cs0[t].y * b0;
-          sb[ix0[t].y] = cs0[t].y * a0 + cs0[t].x * b0;
-          sb[ix1[t].x] = cs1[t].x * a1 - cs1[t].y * b1;
-          sb[ix1[t].y] = cs1[t].y * a1 + cs1[t].x * b1;
+          const uint32_t i0 = ixr[t] & 0xff, j0 = (ixr[t] >> 8) & 0xff;
+          const uint32_t i1 = (ixr[t] >> 16) & 0xff, j1 = ixr[t] >> 24;
+          const float a0 = sb[i0], b0 = sb[j0];
+          const float a1 = sb[i1], b1 = sb[j1];
+          sb[i0] = csr[t].x * a0 - csr[t].y * b0;
+          sb[j0] = csr[t].y * a0 + csr[t].x * b0;
+          sb[i1] = csr[t].z * a1 - csr[t].w * b1;
+          sb[j1] = csr[t].w * a1 + csr[t].z * b1;
         }
         __syncwarp();
+        if (threadIdx.x == 0 && gam == g0 && t == 0) PARO_TL(a, 9);
       }
+      if (threadIdx.x == 0 && gam == g0) PARO_TL(a, 6);
 #pragma unroll
       for (int b = 0; b < BT; ++b) {
         const float* sb = scr + b * 132;
-        const uint32_t h01 = pack_half2(sb[4 * lane], sb[4 * lane + 1]);
-        const uint32_t h23 = pack_half2(sb[4 * lane + 2], sb[4 * lane + 3]);
-        __half* dstp = u16 + static_cast<int64_t>(b) * K + kg + 4 * lane;
+        // perm8 order: pairs (c0, c0+4), (c0+1, c0+5) of the lane's 8-block half
+        const uint32_t p0 = pack_half2(sb[c0], sb[c0 + 4]);
+        const uint32_t p1 = pack_half2(sb[c0 + 1], sb[c0 + 5]);
+        // 32-channel chunk sums of the fp16-rounded x' (chunk = 8 lanes)
+        float cs = half2_sum(p0) + half2_sum(p1);
+        cs += __shfl_xor_sync(0xffffffffu, cs, 1);
+        cs += __shfl_xor_sync(0xffffffffu, cs, 2);
+        cs += __shfl_xor_sync(0xffffffffu, cs, 4);
+        cs *= TWO_M24;
+        const uint32_t uo = u_addr + static_cast<uint32_t>((b * K + kg + b8) * 2 + hh * 8);
+        const uint32_t so = s_addr + static_cast<uint32_t>((b * NCH + (kg >> 5) + (lane >> 3)) * 4);
         if (CL > 1) {
-          const uint32_t addr = smem_u32(dstp);
           for (uint32_t r = 0; r < CL; ++r) {
-            const uint32_t ra = mapa(addr, r);
-            st_cluster_u32(ra, h01);
-            st_cluster_u32(ra + 4, h23);
+            const uint32_t rb = mapa(bar_addr, r);
+            st_async_v2(mapa(uo, r), p0, p1, rb);
+            if ((lane & 7) == 0) st_async_b32(mapa(so, r), __float_as_uint(cs), rb);
           }
         } else {
-          *reinterpret_cast<uint2*>(dstp) = make_uint2(h01, h23);
+          *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(u16) + (uo - u_addr)) = make_uint2(p0, p1);
+          if ((lane & 7) == 0) usum[b * NCH + (kg >> 5) + (lane >> 3)] = cs;
         }
       }
       __syncwarp();
+      if (threadIdx.x == 0 && gam == g0) PARO_TL(a, 7);
     }
-    if (first && a.pdl) pdl_wait();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(pfree);  // this warp no longer reads the staged parameters
     if (CL > 1) {
-      cluster_arrive();
-      cluster_wait();
+      mbar_wait(xpbar, 0);  // every group's x' has arrived from its owner CTA
     } else {
       named_bar_sync(1, n_compute_warps * 32);
     }
-  } else if (a.pdl) {
-    pdl_wait();
   }
+  if (threadIdx.x == 0) PARO_TL(a, 2);
 
   // ------------------------------------------------------------ phase 2: GEMV
+  // warp wk: K slice [wk*512*J, (wk+1)*512*J); lane hl of a half-warp owns 32*J
+  // contiguous K (one 128-group).  Slot j of a lane holds chunk (j + hl) % J of its
+  // span, so the per-slot 16-byte code loads of the 16 lanes hit distinct banks.
   const int wk = warp;
   const int h = lane >> 4;
   const int hl = lane & 15;
+  const int kbase = wk * (512 * J) + hl * (32 * J);
+  const bool act = kbase < K;
   uint32_t uP[J][BT][16];
-  float Us[J][BT];
-  int k0s[J];
-  bool act[J];
+  float Us[BT];
 #pragma unroll
-  for (int j = 0; j < J; ++j) {
-    const int k0 = (wk * J + j) * 512 + hl * 32;
-    k0s[j] = k0;
-    act[j] = k0 < K;
+  for (int b = 0; b < BT; ++b) {
+    Us[b] = 0.f;
 #pragma unroll
-    for (int b = 0; b < BT; ++b) {
-      Us[j][b] = 0.f;
+    for (int j = 0; j < J; ++j) {
+      const int k0 = kbase + 32 * ((j + hl) & (J - 1));
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
         uint4 q = make_uint4(0u, 0u, 0u, 0u);
-        if (act[j]) {
-          if (a.rotate) {
-            q = *reinterpret_cast<const uint4*>(u16 + static_cast<int64_t>(b) * K + k0 + 8 * m);
-          } else if (b < a.B) {
-            // rotation disabled (overhead baseline): u = x straight from global (16-byte loads)
-            q = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(a.x) +
-                                                     (static_cast<int64_t>(b) * K + k0 + 8 * m) * 2));
-            if (a.x_bf16) {
-              uint32_t* e = reinterpret_cast<uint32_t*>(&q);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&e[i]));
-                e[i] = pack_half2(f.x, f.y);
-              }
-            }
-          }
-        }
-        regroup8(q.x, q.y, q.z, q.w, &uP[j][b][4 * m]);
-        Us[j][b] += sum8_h(q.x, q.y, q.z, q.w);
+        if (act) q = *reinterpret_cast<const uint4*>(u16 + static_cast<int64_t>(b) * K + k0 + 8 * m);
+        uP[j][b][4 * m + 0] = q.x;
+        uP[j][b][4 * m + 1] = q.y;
+        uP[j][b][4 * m + 2] = q.z;
+        uP[j][b][4 * m + 3] = q.w;
       }
-      Us[j][b] *= TWO_M24;  // exact power-of-two scaling
+      if (act) Us[b] += usum[b * NCH + (k0 >> 5)];
     }
   }
+  // inactive lanes (K not a multiple of 512*J) read a valid chunk and contribute 0 (u' = 0)
+  const int kb = act ? kbase : 0;
+  const int gam = kb >> 7;
+  const uint32_t code_off = static_cast<uint32_t>(kb >> 1);
+  const int zsh = (gam & 1) * 4;
 
+  // stage slots as 32-bit shared addresses (no generic->shared conversion in the loop)
+  const uint32_t ring_a = smem_u32(ring);
   int slot = 0;
   uint32_t phase = 0;
   for (int st = 0; st < n_stages; ++st) {
     mbar_wait(&full[slot], phase);
-    const uint8_t* sbase = ring + static_cast<size_t>(slot) * a.slot_bytes;
+    if (st == 0 && threadIdx.x == 0) PARO_TL(a, 3);
+    const uint32_t sbase = ring_a + static_cast<uint32_t>(slot) * a.slot_bytes;
     const int r0 = row_begin + st * SR;
     const int nr = min(SR, n_rows - st * SR);
-    const int64_t s_lo = (static_cast<int64_t>(r0) * 2 * G) & ~int64_t(15);
-    const int64_t z_lo = (static_cast<int64_t>(r0) * ZB) & ~int64_t(15);
-    const uint8_t* sc_base = sbase + a.sc_off + (static_cast<int64_t>(r0) * 2 * G - s_lo);
-    const uint8_t* z_base = sbase + a.z_off + (static_cast<int64_t>(r0) * ZB - z_lo);
-    float racc[RP_PER_STAGE][BT];
+    const uint32_t s_lo = static_cast<uint32_t>((static_cast<int64_t>(r0) * 2 * G) & ~int64_t(15));
+    const uint32_t z_lo = static_cast<uint32_t>((static_cast<int64_t>(r0) * ZB) & ~int64_t(15));
+    // this lane's row lr = 2i + h: scale, zero and codes addresses (all rows of the slot
+    // exist in shared memory; rows past nr hold stale bytes -- computed, never stored)
+    const uint32_t sc_a = sbase + a.sc_off + static_cast<uint32_t>(r0 * 2 * G) - s_lo + 2 * gam + h * 2 * G;
+    const uint32_t z_a = sbase + a.z_off + static_cast<uint32_t>(r0 * ZB) - z_lo + (gam >> 1) + h * ZB;
+    const uint32_t c_a = sbase + code_off + h * (K / 2);
+    float racc[RP][BT];
 #pragma unroll
-    for (int i = 0; i < RP_PER_STAGE; ++i) {
+    for (int i = 0; i < RP; ++i) {
+      const uint32_t row_off = 2 * i;
+      uint4 c[J];
 #pragma unroll
-      for (int b = 0; b < BT; ++b) racc[i][b] = 0.f;
-      const int lr = 2 * i + h;  // stage-local row
-      if (2 * i < SR && lr < nr) {
-        const uint8_t* crow = sbase + static_cast<size_t>(lr) * (K / 2);
+      for (int j = 0; j < J; ++j) c[j] = lds128_a(c_a + row_off * (K / 2) + 16 * ((j + hl) & (J - 1)));
+      const float S = __half2float(__ushort_as_half(lds_u16_a(sc_a + row_off * 2 * G)));
+      const float zf = static_cast<float>((lds_u8_a(z_a + row_off * ZB) >> zsh) & 15u);
+#pragma unroll
+      for (int b = 0; b < BT; ++b) {
+        float tl = 0.f, th = 0.f;  // 2^-24 sum q x' over the lane's 32*J codes
 #pragma unroll
         for (int j = 0; j < J; ++j) {
-          if (!act[j]) continue;
-          const int k0 = k0s[j];
-          const int gam = k0 >> 7;
-          const uint4 c = lds128(crow + (k0 >> 1));
-          const float S = __half2float(*reinterpret_cast<const __half*>(sc_base + lr * 2 * G + 2 * gam));
-          const uint32_t zbyte = *(z_base + lr * ZB + (gam >> 1));
-          const float zf = static_cast<float>((zbyte >> ((gam & 1) * 4)) & 15u);
-#pragma unroll
-          for (int b = 0; b < BT; ++b) {
-            const float dot = dot32(c, uP[j][b]);  // = 2^-24 sum q x'
-            racc[i][b] = fmaf(S, fmaf(-zf, Us[j][b], dot), racc[i][b]);
-          }
+          dot_word(c[j].x, &uP[j][b][0], tl, th);
+          dot_word(c[j].y, &uP[j][b][4], tl, th);
+          dot_word(c[j].z, &uP[j][b][8], tl, th);
+          dot_word(c[j].w, &uP[j][b][12], tl, th);
         }
+        const float dot = fmaf(0.0625f, th, tl);
+        racc[i][b] = S * fmaf(-zf, Us[b], dot);
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);  // codes of this stage consumed
-    // transpose-reduce the 8 row-pair slots across the 16 lanes of each half-warp
+    // transpose-reduce the RP row-pair slots across the 16 lanes of each half-warp
 #pragma unroll
     for (int b = 0; b < BT; ++b) {
-      const bool b3 = hl & 8, b2 = hl & 4, b1 = hl & 2;
-      float k4[4];
+      float v[RP];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float keep = b3 ? racc[i + 4][b] : racc[i][b];
-        const float send = b3 ? racc[i][b] : racc[i + 4][b];
-        k4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-      }
-      float k2[2];
+      for (int i = 0; i < RP; ++i) v[i] = racc[i][b];
+      int si = 0;
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const float keep = b2 ? k4[i + 2] : k4[i];
-        const float send = b2 ? k4[i] : k4[i + 2];
-        k2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      for (int off = 8, n = RP; off >= 1; off >>= 1) {
+        const bool up = hl & off;
+        if (n > 1) {
+          const int hn = n / 2;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (i < hn) {
+              const float keep = up ? v[i + hn] : v[i];
+              const float send = up ? v[i] : v[i + hn];
+              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+          }
+          si = 2 * si + (up ? 1 : 0);
+          n = hn;
+        } else {
+          v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+        }
       }
-      float k1 = (b1 ? k2[1] : k2[0]) + __shfl_xor_sync(0xffffffffu, b1 ? k2[0] : k2[1], 2);
-      k1 += __shfl_xor_sync(0xffffffffu, k1, 1);
-      const int si = hl >> 1;
+      // lanes whose unused low bits are 0 hold slot si (0 <= si < RP)
       const int lr = 2 * si + h;
-      if ((hl & 1) == 0 && lr < nr)
-        part[(static_cast<size_t>(wk) * a.rows_max + st * SR + lr) * BT + b] = k1;
+      const bool writer = (hl & (16 / RP - 1)) == 0;
+      if (writer && lr < nr) part[(static_cast<size_t>(wk) * a.rows_max + st * SR + lr) * BT + b] = v[0];
     }
     if (++slot == a.S) {
       slot = 0;
       phase ^= 1;
     }
   }
-  if (a.pdl) pdl_launch_dependents();
+  if (threadIdx.x == 0) PARO_TL(a, 4);
+  if (a.pdl) {
+    pdl_launch_dependents();
+    pdl_wait();  // y may still be read by the previous kernel (no-op once it has finished)
+  }
 
   // ------------------------------------------------------------ cross-warp reduction + epilogue (a8)
   named_bar_sync(1, n_compute_warps * 32);
@@ -396,9 +489,16 @@ __global__ void __launch_bounds__(GemvThreads<BT, J>::value, 1) paro_gemv_kernel
     for (int w = 0; w < WK; ++w) sum += part[(static_cast<size_t>(w) * a.rows_max + row) * BT + b];
     const int64_t n = static_cast<int64_t>(row_begin) + row;
     float v = sum * TWO_P24;
-    if (a.bias) v += a.bias[n];
+    if (a.bias) v += __ldg(a.bias + n);
     store_out(a.y, a.y_dtype, static_cast<int64_t>(b) * a.N + n, v);
   }
+  if (threadIdx.x == 0) PARO_TL(a, 5);
+}
+
+// debug: copy the per-CTA event timeline (ns, %globaltimer) of the last debug launch
+extern "C" int paro_debug_read_timeline(unsigned long long* host, int n) {
+  if (n > 1024 * TL_EVENTS) n = 1024 * TL_EVENTS;
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_paro_timeline, sizeof(unsigned long long) * n));
 }
 
 // ============================================================================ host side
@@ -428,37 +528,89 @@ static int smem_optin() {
 
 static inline uint32_t align_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
-static int max_compute_warps(int bt, int j) { return ((bt * j <= 2) ? 544 : 288) / 32 - 1; }
+
+static const void* kernel_for(int BT, int J, int big) {
+#define PARO_K(BT_, J_, T_) \
+  if (BT == BT_ && J == J_ && (big ? 544 : 288) == T_) return reinterpret_cast<const void*>(&paro_gemv_kernel<BT_, J_, T_>);
+  PARO_K(1, 1, 288)
+  PARO_K(1, 2, 288)
+  PARO_K(1, 4, 288)
+  PARO_K(2, 1, 288)
+  PARO_K(2, 2, 288)
+  PARO_K(4, 1, 288)
+  PARO_K(1, 1, 544)
+  PARO_K(1, 2, 544)
+  PARO_K(1, 4, 544)
+#undef PARO_K
+  return nullptr;
+}
+
+// Co-resident CTAs for this launch shape (whole clusters), from the occupancy API.
+static int max_resident_ctas(int BT, int J, int threads, int smem, int CL) {
+  const void* k = kernel_for(BT, J, threads > 288);
+  if (!k) return 0;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  if (CL > 1) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(CL * 64);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = CL;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, k, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    return nc * CL;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return per_sm * device_sm_count();
+}
 
 bool plan_gemv(int B_tile, int64_t N, int64_t K, int L, int rotate, GemvConfig* cfg, const char** why) {
   GemvConfig c{};
   c.BT = B_tile <= 1 ? 1 : B_tile <= 2 ? 2 : 4;
   const int G = static_cast<int>(K / GRP);
-  const int slices = static_cast<int>((K + 511) / 512);
-  // J: 32-K chunks per lane per row.  Prefer J=2 once the K-slices need more than 8 warps.
-  int J = 1;
-  while (J < 4 && ((slices + J - 1) / J > max_compute_warps(c.BT, J) || (slices + J - 1) / J > 8)) J *= 2;
-  const int WK = (slices + J - 1) / J;
-  const bool supported = (c.BT == 1) || (c.BT == 2 && J <= 2) || (c.BT == 4 && J == 1);
-  if (WK > max_compute_warps(c.BT, J) || !supported) {
-    *why = "token tile too wide for this K in the decode kernel";
+  // J: contiguous 32-K chunks per lane per row (all in one 128-group).  Smallest J that
+  // keeps the K slices within 8 warps with <= 6% idle lanes (u' registers: BT * J <= 4);
+  // very large K uses up to 16 warps (J = 4).
+  int J = 0;
+  for (int cand = 1; cand <= 4 && !J; cand *= 2) {
+    if (c.BT * cand > 4) break;
+    const int64_t span = 512 * cand;
+    const int64_t wk = (K + span - 1) / span;
+    if (wk <= 8 && (wk * span * 100 <= K * 106 || cand == 4 || K <= span)) J = cand;
+  }
+  if (!J) J = (c.BT == 1) ? 4 : (c.BT == 2 ? 2 : 1);
+  const int WK = static_cast<int>((K + 512 * J - 1) / (512 * J));
+  if (WK > 16 || (WK > 8 && c.BT > 1)) {
+    *why = "K too large for the decode kernel at this token tile";
     return false;
   }
+  const int RG = 1;
   c.J = J;
   const int sms = device_sm_count();
+  const int threads = (WK * RG + 1) * 32;
   // cluster size: share the transform across CTAs (each CTA rotates G/CL groups)
-  int CL = 1;
-  if (rotate) {
-    CL = 8;
-    while (CL > 1 && CL > G) CL /= 2;
-  }
+  // (the rotation-off baseline uses the same split, so it differs only by the rotation)
+  int CL = 8;
+  if (const char* e = getenv("PARO_CLUSTER")) CL = atoi(e);
+  if (CL != 1 && CL != 2 && CL != 4 && CL != 8) CL = 8;
+  while (CL > 1 && CL > G) CL /= 2;
   c.CL = CL;
-  // grid: one CTA per SM (shared-memory ring), rows split evenly
-  int grid = sms / CL * CL;
-  const int64_t max_ctas = (N + 1) / 2;  // at least one row pair per CTA
-  if (grid > max_ctas) grid = static_cast<int>(max_ctas) / CL * CL;
-  if (grid < CL) grid = CL;
-  c.grid = grid;
   GemvArgs& a = c.a;
   a.N = static_cast<int>(N);
   a.K = static_cast<int>(K);
@@ -466,50 +618,93 @@ bool plan_gemv(int B_tile, int64_t N, int64_t K, int L, int rotate, GemvConfig* 
   a.L = L;
   a.rotate = rotate;
   a.WK = WK;
-  a.RG = 1;
-  a.rows_base = static_cast<int>(N / grid);
-  a.rows_extra = static_cast<int>(N % grid);
-  a.rows_max = a.rows_base + (a.rows_extra ? 1 : 0);
+  a.RG = RG;
   const int row_bytes = static_cast<int>(K / 2);
-  // rows per stage: ~32 KB of codes, even, at most 2 * RP_PER_STAGE
-  int SR = 32768 / row_bytes;
-  SR &= ~1;
-  if (SR < 2) SR = 2;
-  if (SR > 2 * RP_PER_STAGE) SR = 2 * RP_PER_STAGE;
+  // rows per stage: 2 * RP_PER_STAGE / J (16 rows of <= 2 KB, 4 rows of <= 8 KB, ...)
+  const int SR = 2 * RP_PER_STAGE / J;
   a.SR = SR;
   const int ZB = (G + 1) / 2;
   a.sc_off = align_up(static_cast<uint32_t>(SR) * row_bytes, 128);
   a.z_off = a.sc_off + align_up(static_cast<uint32_t>(SR) * 2 * G + 32, 128);
   a.slot_bytes = a.z_off + align_up(static_cast<uint32_t>(SR) * ZB + 32, 128);
-  uint32_t off = 0;
-  a.off_u = off;
-  if (rotate) off += align_up(static_cast<uint32_t>(c.BT) * K * 2, 128);
-  a.off_scr = off;
-  if (rotate) off += align_up(static_cast<uint32_t>(WK) * c.BT * 132 * 4, 128);
-  a.off_part = off;
-  off += align_up(static_cast<uint32_t>(WK) * a.rows_max * c.BT * 4, 128);
-  a.off_bar = off;
-  off += 64 * 16;  // up to 64 stages x (full, empty)
-  a.off_ring = align_up(off, 1024);
-  const int budget = smem_optin() - 1024;
-  const int64_t ring_avail = static_cast<int64_t>(budget) - a.off_ring;
-  int S = static_cast<int>(ring_avail / a.slot_bytes);
-  const int stages_needed = (a.rows_max + SR - 1) / SR;
-  if (S > stages_needed) S = stages_needed;
-  if (S > 64) S = 64;
-  if (S < 1) {
+  const uint32_t u_bytes = align_up(static_cast<uint32_t>(c.BT) * K * 2, 128);
+  const uint32_t usum_bytes = align_up(static_cast<uint32_t>(c.BT) * (K / 32) * 4, 128);
+  const int g_per = (G + CL - 1) / CL;
+  const uint32_t x_bytes = align_up(static_cast<uint32_t>(c.BT) * g_per * GRP * 2, 128);
+  const uint32_t scr_bytes = align_up(static_cast<uint32_t>(WK * RG) * c.BT * 132 * 4, 128);
+  // two CTAs per SM when the activation buffer is small (lets the next kernel's weight
+  // prefetch start while this one drains, and doubles the warps hiding latency)
+  int ctas_per_sm = (u_bytes <= 40 * 1024) ? 2 : 1;
+  if (const char* e = getenv("PARO_CTAS_PER_SM")) ctas_per_sm = atoi(e) == 1 ? 1 : ctas_per_sm;
+  const int budget = (smem_optin() + 1024) / ctas_per_sm - 2048;
+  auto layout = [&](int grid) -> bool {
+    a.rows_base = static_cast<int>(N / grid);
+    a.rows_extra = static_cast<int>(N % grid);
+    a.rows_max = a.rows_base + (a.rows_extra ? 1 : 0);
+    uint32_t off = 0;
+    a.off_u = off;
+    off += u_bytes;
+    a.off_usum = off;
+    off += usum_bytes;
+    a.off_x = off;
+    off += x_bytes;
+    a.off_scr = off;
+    off += scr_bytes;
+    a.off_part = off;
+    off += align_up(static_cast<uint32_t>(WK) * a.rows_max * c.BT * 4, 128);
+    a.off_bar = off;
+    off += 64 * 16;  // up to 60 stages x (full, empty) + 4 singles
+    a.off_ring = align_up(off, 1024);
+    const int64_t ring_avail = static_cast<int64_t>(budget) - a.off_ring;
+    int S = static_cast<int>(ring_avail / a.slot_bytes);
+    const int stages_needed = (a.rows_max + SR - 1) / SR;
+    if (S > stages_needed) S = stages_needed;
+    if (S > 60) S = 60;
+    if (S < 1) return false;
+    a.S = S;
+    a.smem_total = a.off_ring + static_cast<uint32_t>(S) * a.slot_bytes;
+    // stage the rotation parameters of this CTA's groups in shared memory: a dedicated
+    // region when it fits, else lend the last ring slots (refilled after phase 1)
+    a.param_slots = 0;
+    a.off_param = 0;
+    if (rotate && L > 0) {
+      const uint32_t pbytes = static_cast<uint32_t>(g_per) * 32 * L * 20 + static_cast<uint32_t>(g_per) * GRP * 4;
+      const int P = static_cast<int>((pbytes + a.slot_bytes - 1) / a.slot_bytes);
+      if (static_cast<int64_t>(a.smem_total) + align_up(pbytes, 128) <= budget) {
+        a.param_slots = -1;
+        a.off_param = a.smem_total;
+        a.smem_total += align_up(pbytes, 128);
+      } else if (P < S) {
+        a.param_slots = P;
+      }
+    }
+    return true;
+  };
+  const int64_t max_ctas = (N + 1) / 2;  // at least one row pair per CTA
+  int grid = sms * ctas_per_sm;
+  for (int iter = 0; iter < 3; ++iter) {
+    grid = static_cast<int>(std::min<int64_t>(grid, max_ctas)) / CL * CL;
+    if (grid < CL) grid = CL;
+    if (!layout(grid)) {
+      *why = "decode kernel shared-memory plan does not fit";
+      return false;
+    }
+    const int resident = max_resident_ctas(c.BT, J, threads, static_cast<int>(a.smem_total), CL);
+    if (resident <= 0 || resident >= grid) break;
+    grid = resident;  // never launch more than one wave
+  }
+  c.grid = grid;
+  if (!layout(grid)) {
     *why = "decode kernel shared-memory plan does not fit";
     return false;
   }
-  a.S = S;
-  a.smem_total = a.off_ring + static_cast<uint32_t>(S) * a.slot_bytes;
   *cfg = c;
   return true;
 }
 
-template <int BT, int J>
+template <int BT, int J, int T>
 static cudaError_t launch_t(const GemvConfig& c, cudaStream_t st) {
-  auto kern = paro_gemv_kernel<BT, J>;
+  auto kern = paro_gemv_kernel<BT, J, T>;
   static int configured_smem = 0;  // per instantiation
   if (static_cast<int>(c.a.smem_total) > configured_smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -519,7 +714,7 @@ static cudaError_t launch_t(const GemvConfig& c, cudaStream_t st) {
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(c.grid);
-  cfg.blockDim = dim3((c.a.WK + 1) * 32);
+  cfg.blockDim = dim3((c.a.WK * c.a.RG + 1) * 32);
   cfg.dynamicSmemBytes = c.a.smem_total;
   cfg.stream = st;
   cudaLaunchAttribute attrs[2];
@@ -542,14 +737,18 @@ static cudaError_t launch_t(const GemvConfig& c, cudaStream_t st) {
 }
 
 cudaError_t launch_gemv(const GemvConfig& c, cudaStream_t st) {
-#define PARO_GEMV_CASE(BT_, J_) \
-  if (c.BT == BT_ && c.J == J_) return launch_t<BT_, J_>(c, st);
-  PARO_GEMV_CASE(1, 1)
-  PARO_GEMV_CASE(1, 2)
-  PARO_GEMV_CASE(1, 4)
-  PARO_GEMV_CASE(2, 1)
-  PARO_GEMV_CASE(2, 2)
-  PARO_GEMV_CASE(4, 1)
+  const bool big = (c.a.WK * c.a.RG + 1) * 32 > 288;
+#define PARO_GEMV_CASE(BT_, J_, T_) \
+  if (c.BT == BT_ && c.J == J_ && (big ? 544 : 288) == T_) return launch_t<BT_, J_, T_>(c, st);
+  PARO_GEMV_CASE(1, 1, 288)
+  PARO_GEMV_CASE(1, 2, 288)
+  PARO_GEMV_CASE(1, 4, 288)
+  PARO_GEMV_CASE(2, 1, 288)
+  PARO_GEMV_CASE(2, 2, 288)
+  PARO_GEMV_CASE(4, 1, 288)
+  PARO_GEMV_CASE(1, 1, 544)
+  PARO_GEMV_CASE(1, 2, 544)
+  PARO_GEMV_CASE(1, 4, 544)
 #undef PARO_GEMV_CASE
   return cudaErrorInvalidConfiguration;
 }

@@ -28,19 +28,19 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
   const int gam = static_cast<int>(item % G);
   const int64_t b0 = (item / G) * TOK_PER_WARP;
   if (b0 >= B) return;
-  float2 cs0[8], cs1[8];
-  uchar2 ix0[8], ix1[8];
+  // records [G][L][32 lanes]: (cos0, sin0, cos1, sin1) / (i0, j0, i1, j1) of slots l and
+  // l + 32 of rotation t
+  float4 csr[8];
+  uint32_t ixr[8];
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
     if (t < L && rotate) {
-      const int64_t e = (static_cast<int64_t>(gam) * L + t) * 64;
-      cs0[t] = rot_cs[e + lane];
-      cs1[t] = rot_cs[e + lane + 32];
-      ix0[t] = rot_idx[e + lane];
-      ix1[t] = rot_idx[e + lane + 32];
+      const int64_t rec = (static_cast<int64_t>(gam) * L + t) * 32 + lane;
+      csr[t] = __ldg(reinterpret_cast<const float4*>(rot_cs) + rec);
+      ixr[t] = __ldg(reinterpret_cast<const uint32_t*>(rot_idx) + rec);
     } else {
-      cs0[t] = cs1[t] = make_float2(1.f, 0.f);
-      ix0[t] = ix1[t] = make_uchar2(128, 128);
+      csr[t] = make_float4(1.f, 0.f, 1.f, 0.f);
+      ixr[t] = 0x80808080u;
     }
   }
   float sv[4];
@@ -60,12 +60,14 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       if (t >= L || !rotate) break;
-      const float a0 = scr[ix0[t].x], c0 = scr[ix0[t].y];
-      const float a1 = scr[ix1[t].x], c1 = scr[ix1[t].y];
-      scr[ix0[t].x] = cs0[t].x * a0 - cs0[t].y * c0;
-      scr[ix0[t].y] = cs0[t].y * a0 + cs0[t].x * c0;
-      scr[ix1[t].x] = cs1[t].x * a1 - cs1[t].y * c1;
-      scr[ix1[t].y] = cs1[t].y * a1 + cs1[t].x * c1;
+      const uint32_t i0 = ixr[t] & 0xff, j0 = (ixr[t] >> 8) & 0xff;
+      const uint32_t i1 = (ixr[t] >> 16) & 0xff, j1 = ixr[t] >> 24;
+      const float a0 = scr[i0], c0 = scr[j0];
+      const float a1 = scr[i1], c1 = scr[j1];
+      scr[i0] = csr[t].x * a0 - csr[t].y * c0;
+      scr[j0] = csr[t].y * a0 + csr[t].x * c0;
+      scr[i1] = csr[t].z * a1 - csr[t].w * c1;
+      scr[j1] = csr[t].w * a1 + csr[t].z * c1;
       __syncwarp();
     }
     // natural order: lane writes channels 4l..4l+3.  perm8 (prefill operand order): each
@@ -112,6 +114,8 @@ __global__ void prepare_transform_kernel(const float* __restrict__ theta, const 
   if (e >= static_cast<int64_t>(G) * L * 64) return;
   const int slot = static_cast<int>(e % 64);
   const int64_t gt = e / 64;
+  const int64_t gam = gt / L, t = gt % L;
+  const int64_t dst = ((gam * L + t) * 32 + (slot & 31)) * 2 + (slot >> 5);  // [G][L][32][2] record
   float2 cs = make_float2(1.f, 0.f);
   uchar2 ij = make_uchar2(128, 128);
   if (slot < P) {
@@ -124,8 +128,8 @@ __global__ void prepare_transform_kernel(const float* __restrict__ theta, const 
       ij = make_uchar2(static_cast<unsigned char>(i), static_cast<unsigned char>(j));
     }
   }
-  rot_cs[e] = cs;
-  rot_idx[e] = ij;
+  rot_cs[dst] = cs;
+  rot_idx[dst] = ij;
 }
 
 cudaError_t launch_prepare_transform(const float* theta, const int16_t* pairs, int G, int L, int P, float2* rot_cs,

@@ -45,6 +45,100 @@ size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 
 }  // namespace
 
+
+// ---------------------------------------------------------------- bank-conflict-free rotation schedule
+// One independent rotation = a perfect matching of the 128 channels of a group (absent
+// slots are completed with identity pairs of the unpaired channels, cos = 1, sin = 0).
+// The runtime kernels keep the group in shared memory and lane l of a warp updates the
+// two pairs of slots (l, 0) and (l, 1): four gathers v[a0], v[b0], v[a1], v[b1] and four
+// scatters per rotation.  With bank(ch) = ch % 32 each bank holds 4 channels, so the
+// pairs form a 4-regular multigraph on the 32 banks.  Orienting it along an Euler
+// circuit gives in = out = 2 at every bank; splitting the oriented edges into two
+// perfect matchings (2-regular bipartite graph out-bank -> in-bank) yields, per slot,
+// 32 pairs whose first channels hit 32 distinct banks and whose second channels do
+// too -- every gather/scatter is conflict-free.  Swapping a pair's orientation is exact:
+// (i, j, theta) == (j, i, -theta).  The slot order inside one independent rotation is
+// irrelevant (Def. 2).
+struct RotPair {
+  int a, b;
+  double c, s;
+};
+
+static void schedule_rotation(std::vector<RotPair> pairs, RotPair out[2][32]) {
+  bool used[128] = {false};
+  for (const RotPair& p : pairs) used[p.a] = used[p.b] = true;
+  int pend = -1;
+  for (int ch = 0; ch < 128; ++ch) {
+    if (used[ch]) continue;
+    if (pend < 0) {
+      pend = ch;
+    } else {
+      pairs.push_back({pend, ch, 1.0, 0.0});
+      pend = -1;
+    }
+  }
+  const int E = static_cast<int>(pairs.size());  // 64
+  std::vector<std::vector<std::pair<int, int>>> adj(32);  // (edge, other bank)
+  for (int e = 0; e < E; ++e) {
+    const int u = pairs[e].a & 31, v = pairs[e].b & 31;
+    adj[u].push_back({e, v});
+    adj[v].push_back({e, u});
+  }
+  std::vector<int> src(E, -1), dst(E, -1);  // oriented: bank src -> bank dst
+  std::vector<bool> eused(E, false);
+  std::vector<size_t> ptr(32, 0);
+  for (int start = 0; start < 32; ++start) {
+    // Hierholzer: walk unused edges, orienting each in traversal direction
+    std::vector<int> stack{start};
+    while (!stack.empty()) {
+      const int x = stack.back();
+      while (ptr[x] < adj[x].size() && eused[adj[x][ptr[x]].first]) ++ptr[x];
+      if (ptr[x] == adj[x].size()) {
+        stack.pop_back();
+        continue;
+      }
+      const auto [e, y] = adj[x][ptr[x]];
+      eused[e] = true;
+      src[e] = x;
+      dst[e] = y;
+      stack.push_back(y);
+    }
+  }
+  // split into two perfect matchings along the alternating cycles of out->in
+  std::vector<std::vector<int>> outs(32), ins(32);
+  for (int e = 0; e < E; ++e) {
+    outs[src[e]].push_back(e);
+    ins[dst[e]].push_back(e);
+  }
+  std::vector<int> slot(E, -1);
+  for (int e0 = 0; e0 < E; ++e0) {
+    if (slot[e0] >= 0) continue;
+    int e = e0, s = 0;
+    while (slot[e] < 0) {
+      slot[e] = s;
+      // partner at the same in-bank gets the other slot
+      const std::vector<int>& in = ins[dst[e]];
+      const int f = (in[0] == e) ? in[1] : in[0];
+      if (slot[f] >= 0) break;
+      slot[f] = 1 - s;
+      // next: the other out-edge of f's source bank gets slot s again
+      const std::vector<int>& ou = outs[src[f]];
+      e = (ou[0] == f) ? ou[1] : ou[0];
+    }
+  }
+  for (int e = 0; e < E; ++e) {
+    const RotPair& p = pairs[e];
+    RotPair r;
+    // first element in bank src[e]
+    if ((p.a & 31) == src[e] && ((p.b & 31) == dst[e])) {
+      r = p;
+    } else {
+      r = {p.b, p.a, p.c, -p.s};
+    }
+    out[slot[e]][src[e]] = r;
+  }
+}
+
 extern "C" {
 
 const char* paro_last_error(void) { return g_err.c_str(); }
@@ -100,17 +194,24 @@ paro_status paro_pack(const void* W, const float* s, const float* theta, const i
     if (!std::isfinite(hs[k]) || !(hs[k] > 0.f))
       return fail(PARO_ERR_INVALID_ARGUMENT, "paro_pack: s[%lld] must be finite and > 0", (long long)k);
   // prepared transform: fp64 (cos, sin) for the fold, fp32 copies + u8 indices for the runtime
+  // fold kernel tables are slot-major [G][L][64]; the runtime tables are records
+  // [G][L][32 lanes][2 slots] (slot p = lane + 32 * s): 16-byte (cos0, sin0, cos1, sin1)
+  // and 4-byte (i0, j0, i1, j1) per (group, rotation, lane), lane-contiguous.
   std::vector<double> cs64(static_cast<size_t>(G * L * PARO_SLOTS * 2), 0.0);
+  std::vector<uint8_t> idx64(static_cast<size_t>(G * L * PARO_SLOTS * 2), 128);
   std::vector<float> cs32(static_cast<size_t>(G * L * PARO_SLOTS * 2), 0.f);
   std::vector<uint8_t> idx(static_cast<size_t>(G * L * PARO_SLOTS * 2), 128);
+  auto lane_major = [&](int64_t g, int t, int p) -> size_t {
+    return static_cast<size_t>(((g * L + t) * 32 + (p & 31)) * 2 + (p >> 5));
+  };
   for (int64_t g = 0; g < G; ++g) {
     std::set<std::pair<int, int>> seen;
     for (int t = 0; t < L; ++t) {
       bool used[kG] = {false};
+      std::vector<RotPair> layer;
       for (int p = 0; p < PARO_SLOTS; ++p) {
         const size_t o = static_cast<size_t>((g * L + t) * PARO_SLOTS + p);
         cs64[2 * o] = 1.0;
-        cs32[2 * o] = 1.f;
         if (p >= P) continue;
         const size_t src = static_cast<size_t>((g * L + t) * P + p);
         const int i = hpr[2 * src], j = hpr[2 * src + 1];
@@ -129,32 +230,44 @@ paro_status paro_pack(const void* W, const float* s, const float* theta, const i
         const double c = std::cos(static_cast<double>(th)), sn = std::sin(static_cast<double>(th));
         cs64[2 * o] = c;
         cs64[2 * o + 1] = sn;
-        cs32[2 * o] = static_cast<float>(c);
-        cs32[2 * o + 1] = static_cast<float>(sn);
-        idx[2 * o] = static_cast<uint8_t>(i);
-        idx[2 * o + 1] = static_cast<uint8_t>(j);
+        idx64[2 * o] = static_cast<uint8_t>(i);
+        idx64[2 * o + 1] = static_cast<uint8_t>(j);
+        layer.push_back({i, j, c, sn});
       }
+      RotPair sched[2][32];
+      schedule_rotation(layer, sched);
+      for (int sl = 0; sl < 2; ++sl)
+        for (int ln = 0; ln < 32; ++ln) {
+          const size_t r = lane_major(g, t, ln + 32 * sl);
+          const RotPair& q = sched[sl][ln];
+          cs32[2 * r] = static_cast<float>(q.c);
+          cs32[2 * r + 1] = static_cast<float>(q.s);
+          idx[2 * r] = static_cast<uint8_t>(q.a);
+          idx[2 * r + 1] = static_cast<uint8_t>(q.b);
+        }
     }
   }
   // ---- device temporaries: fp64 (cos, sin) table, status word
   const size_t cs_bytes = cs64.size() * sizeof(double);
-  const size_t tmp_bytes = align256(cs_bytes) + 256;
+  const size_t tmp_bytes = align256(cs_bytes) + align256(idx64.size()) + 256;
   void* tmp = nullptr;
   e = cudaMallocAsync(&tmp, tmp_bytes, cs);
   if (e != cudaSuccess) return cuda_fail(e, "paro_pack: cudaMallocAsync");
   uint8_t* tb = static_cast<uint8_t*>(tmp);
-  int* status = reinterpret_cast<int*>(tb + align256(cs_bytes));
+  uint8_t* idx_dev = tb + align256(cs_bytes);
+  int* status = reinterpret_cast<int*>(idx_dev + align256(idx64.size()));
   e = cudaMemsetAsync(status, 0, 4, cs);
   if (e == cudaSuccess && cs_bytes) e = cudaMemcpyAsync(tb, cs64.data(), cs_bytes, cudaMemcpyHostToDevice, cs);
+  if (e == cudaSuccess && !idx64.empty())
+    e = cudaMemcpyAsync(idx_dev, idx64.data(), idx64.size(), cudaMemcpyHostToDevice, cs);
   if (e == cudaSuccess && L > 0) e = cudaMemcpyAsync(out->rot_cs, cs32.data(), cs32.size() * 4, cudaMemcpyHostToDevice, cs);
   if (e == cudaSuccess && L > 0) e = cudaMemcpyAsync(out->rot_idx, idx.data(), idx.size(), cudaMemcpyHostToDevice, cs);
   if (e == cudaSuccess) e = cudaMemcpyAsync(out->svec, s, K * 4, cudaMemcpyDeviceToDevice, cs);
   // zero the padding tails of scales/zeros (read by 16-byte bulk copies)
   if (e == cudaSuccess) e = cudaMemsetAsync(static_cast<uint8_t*>(out->scales) + N * G * 2, 0, 16, cs);
   if (e == cudaSuccess) e = cudaMemsetAsync(static_cast<uint8_t*>(out->zeros) + N * ceil_div(G, 2), 0, 16, cs);
-  // idx buffer for the fold: same u8 table; use the packed rot_idx when L > 0
   if (e == cudaSuccess)
-    e = paro::launch_pack(W, s, tb, out->rot_idx, N, K, L, out->codes, out->scales, out->zeros, status, cs);
+    e = paro::launch_pack(W, s, tb, idx_dev, N, K, L, out->codes, out->scales, out->zeros, status, cs);
   int hstatus = 0;
   if (e == cudaSuccess) e = cudaMemcpyAsync(&hstatus, status, 4, cudaMemcpyDeviceToHost, cs);
   cudaError_t e2 = cudaFreeAsync(tmp, cs);
@@ -278,6 +391,7 @@ paro_status paro_linear(const void* x, paro_dtype x_dtype, int64_t B, const paro
     a.y = static_cast<uint8_t*>(y) + b0 * N * ye;
     a.y_dtype = static_cast<int>(y_dtype);
     a.pdl = pdl;
+    a.debug = (flags & 0x100u) ? 1 : 0;  // internal: event timeline
     cudaError_t e = paro::launch_gemv(cfg, cs);
     if (e != cudaSuccess) return cuda_fail(e, "paro_linear: decode GEMV launch");
   }

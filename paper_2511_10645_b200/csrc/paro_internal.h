@@ -26,13 +26,16 @@ struct GemvArgs {
   int N, K, G, L;
   int rotate;
   int pdl;
+  int debug;      // record a per-CTA event timeline (g_paro_timeline)
   int WK;         // warps along K (one 512*J K-slice each)
   int RG;         // row groups (warps along rows)
   int SR;         // rows per stage (even)
   int S;          // ring depth
+  int param_slots;  // ring slots lent to the staged rotation parameters (-1: dedicated region)
+  uint32_t off_param;
   int rows_base, rows_extra, rows_max;
   uint32_t slot_bytes, sc_off, z_off;  // per-stage slot layout
-  uint32_t off_u, off_scr, off_part, off_ring, off_bar, smem_total;
+  uint32_t off_u, off_usum, off_x, off_scr, off_part, off_ring, off_bar, smem_total;
 };
 
 struct GemvConfig {

@@ -25,6 +25,7 @@ PARO_DEV void mbar_arrive(uint64_t* bar) {
 }
 PARO_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
+  // suspend-time hint: the waiting warp sleeps (up to ~1 us) instead of spinning on issue slots
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -54,6 +55,13 @@ PARO_DEV void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uin
       : "memory");
 }
 
+PARO_DEV void bulk_g2s_nohint(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // ---------------------------------------------------------------- cluster / DSMEM
 PARO_DEV uint32_t cluster_ctarank() {
   uint32_t r;
@@ -73,6 +81,20 @@ PARO_DEV uint32_t mapa(uint32_t smem_addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
   return r;
 }
+// asynchronous DSMEM store; completion counted (bytes) on the receiver's mbarrier
+PARO_DEV void st_async_v2(uint32_t remote_addr, uint32_t v0, uint32_t v1, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];" ::"r"(remote_addr),
+               "r"(v0), "r"(v1), "r"(remote_bar)
+               : "memory");
+}
+PARO_DEV void st_async_b32(uint32_t remote_addr, uint32_t v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(remote_addr), "r"(v),
+               "r"(remote_bar)
+               : "memory");
+}
+PARO_DEV void prefetch_l2_bulk(const void* gmem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem), "r"(bytes) : "memory");
+}
 PARO_DEV void st_cluster_u32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
@@ -80,6 +102,9 @@ PARO_DEV void st_cluster_u32(uint32_t addr, uint32_t v) {
 // ---------------------------------------------------------------- named barrier
 PARO_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+PARO_DEV void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 // ---------------------------------------------------------------- programmatic dependent launch
@@ -92,6 +117,24 @@ PARO_DEV uint4 lds128(const void* p) {
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "r"(smem_u32(p)));
+  return v;
+}
+
+// shared loads by 32-bit shared-window address (volatile: never hoisted above the
+// mbarrier wait that guards the data)
+PARO_DEV uint4 lds128_a(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+PARO_DEV unsigned short lds_u16_a(uint32_t addr) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+PARO_DEV uint32_t lds_u8_a(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
 

@@ -155,10 +155,8 @@ def run_paro(args):
     B = args.batch
     comm = None
     if world > 1:
-        uid = paro.paro_comm_unique_id() if rank == 0 else b"\0" * 128
-        t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
-        dist.broadcast(t, 0)
-        comm = paro.paro_comm_init(bytes(t.cpu().tolist()), rank, world)
+        from paper_2511_10645_b200 import dist as pd
+        comm = pd.make_comm(rank, world)
 
     layer_bytes = sum(algorithmic_bytes(N, K, B)[0] for N, K in shapes.values())
     weight_bytes_rank = sum(algorithmic_bytes(N // world, K, B)[1] for N, K in shapes.values())

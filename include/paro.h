@@ -148,6 +148,18 @@ paro_status paro_linear(const void* x, paro_dtype x_dtype, int64_t B, const paro
                         const float* theta, const int16_t* pairs, int32_t n_pairs, const float* bias, void* y,
                         paro_dtype y_dtype, uint32_t flags, void* workspace, size_t workspace_bytes, void* stream);
 
+/* paro_linear_multi: n (1..4) linears that read the SAME activation x (e.g. q/k/v, or
+ * gate/up), each with its own transform (one (s, theta, pairs) per linear, Alg. A2,
+ * PAPER.md:576-586): y[i] = (T_i^{-1} x) . dequant(Q_i)^T + bias[i].  In decode (B <= 16)
+ * all linears run in ONE kernel launch (the clusters of the grid are split over the
+ * linears in proportion to their rows), which removes the per-launch prologue of the
+ * others; prefill runs one GEMM per linear.  packed, bias (NULL or array of n, entries
+ * may be NULL) and y (array of n device [B, N_i]) are host arrays.  All packed[i].K must
+ * be equal.  Workspace as paro_linear for the largest linear.  Errors as paro_linear. */
+paro_status paro_linear_multi(const void* x, paro_dtype x_dtype, int64_t B, int32_t n, const paro_packed* packed,
+                              const float* const* bias, void* const* y, paro_dtype y_dtype, uint32_t flags,
+                              void* workspace, size_t workspace_bytes, void* stream);
+
 /* paro_transform_activations: x' = R_L ... R_1 diag(s) x for every token (the
  * activation side of Eq. 2 / Eq. 5), written as fp16 [B, K] (x_out, device).
  * Uses the transform captured in `packed` (its codes/scales/zeros are not read).

@@ -54,6 +54,8 @@ SIGNATURES = {
     "paro_linear_workspace": (_SZ, [_I64, _I64, _I64, _I32, _I32, _I32, _U32]),
     "paro_linear": (ctypes.c_int, [_P, ctypes.c_int, _I64, _PP, _P, _P, _P, _I32, _P, _P, ctypes.c_int, _U32, _P,
                                    _SZ, _P]),
+    "paro_linear_multi": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I32, _PP, _P, _P, ctypes.c_int, _U32, _P, _SZ,
+                                         _P]),
     "paro_transform_activations": (ctypes.c_int, [_P, ctypes.c_int, _I64, _PP, _P, _P]),
     "paro_unpack_logical": (ctypes.c_int, [_PP, _P, _P, _P, _P]),
     "paro_comm_unique_id": (ctypes.c_int, [_P]),
@@ -186,6 +188,25 @@ def paro_linear(x, packed: PackedLinear, s=None, theta=None, pairs=None, bias=No
     _check(_lib.paro_linear(_ptr(x), _dt(x), B, ctypes.byref(st), _ptr(s), _ptr(theta), _ptr(pairs), P, _ptr(bias),
                             _ptr(y), _dt(y), flags, _ptr(workspace), 0 if workspace is None else workspace.numel(),
                             _stream(stream)))
+    return y
+
+
+def paro_linear_multi(x, packed: list, bias=None, y=None, out_dtype=None, flags: int = 0, workspace=None,
+                      stream=None):
+    """Several linears sharing x (q/k/v, gate/up) in one decode launch; returns [y_i]."""
+    torch = _torch()
+    B = x.shape[0]
+    n = len(packed)
+    if y is None:
+        y = [torch.empty((B, p.N), dtype=out_dtype or x.dtype, device=x.device) for p in packed]
+    need = max(paro_linear_workspace(B, p.N, p.K, p.n_rot, 64, False, flags) for p in packed)
+    if need and (workspace is None or workspace.numel() < need):
+        workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+    structs = (paro_packed * n)(*[p.struct() for p in packed])
+    ys = (ctypes.c_void_p * n)(*[t.data_ptr() for t in y])
+    bs = None if bias is None else (ctypes.c_void_p * n)(*[_ptr(b) for b in bias])
+    _check(_lib.paro_linear_multi(_ptr(x), _dt(x), B, n, structs, bs, ys, _dt(y[0]), flags, _ptr(workspace),
+                                  0 if workspace is None else workspace.numel(), _stream(stream)))
     return y
 
 

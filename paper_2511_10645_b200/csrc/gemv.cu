@@ -109,7 +109,11 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
   const int WK = a.WK;
   const int n_compute_warps = WK;
   const bool is_producer = warp == n_compute_warps;
-  const int K = a.K, G = a.G, L = a.L;
+  // which linear this CTA serves (CTA ranges are whole clusters)
+  int li = 0;
+  while (li + 1 < a.n_lin && static_cast<int>(blockIdx.x) >= a.lin[li + 1].cta_begin) ++li;
+  const GemvLinear& d = a.lin[li];
+  const int K = a.K, G = a.G, L = d.L;
   const int ZB = (G + 1) >> 1;
   const int SR = a.SR;
   const int NCH = K / 32;  // 32-channel chunks
@@ -126,9 +130,9 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
   uint64_t* pbar = xpbar + 1;    // rotation parameters + s of this CTA's groups landed
   uint64_t* pfree = pbar + 1;    // phase 1 done with them (their ring slots can be refilled)
 
-  const int cta = blockIdx.x;
-  const int n_rows = a.rows_base + (cta < a.rows_extra ? 1 : 0);
-  const int row_begin = cta * a.rows_base + min(cta, a.rows_extra);
+  const int cta = static_cast<int>(blockIdx.x) - d.cta_begin;
+  const int n_rows = d.rows_base + (cta < d.rows_extra ? 1 : 0);
+  const int row_begin = cta * d.rows_base + min(cta, d.rows_extra);
   const int n_stages = (n_rows + SR - 1) / SR;
   const uint32_t CL = cluster_nctarank();
   const uint32_t crank = cluster_ctarank();
@@ -171,6 +175,10 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
   } else {
     __syncthreads();
   }
+  // Let the next kernel on the stream launch now: its CTAs take SM slots as ours retire
+  // and run their prologue (parameter loads) early; its griddepcontrol.wait still
+  // orders every access to data this kernel produces.
+  if (a.pdl) pdl_launch_dependents();
 
   // ------------------------------------------------------------ producer warp
   if (is_producer) {
@@ -190,20 +198,20 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
       const int64_t z_hi = (static_cast<int64_t>(r0 + nr) * ZB + 15) & ~int64_t(15);
       const uint32_t sb = static_cast<uint32_t>(s_hi - s_lo), zb = static_cast<uint32_t>(z_hi - z_lo);
       mbar_arrive_expect_tx(&full[slot], cb + sb + zb);
-      bulk_g2s(dst, a.codes + static_cast<int64_t>(r0) * (K / 2), cb, &full[slot], pol);
-      bulk_g2s(dst + a.sc_off, a.scales + s_lo, sb, &full[slot], pol);
-      bulk_g2s(dst + a.z_off, a.zeros + z_lo, zb, &full[slot], pol);
+      bulk_g2s(dst, d.codes + static_cast<int64_t>(r0) * (K / 2), cb, &full[slot], pol);
+      bulk_g2s(dst + a.sc_off, d.scales + s_lo, sb, &full[slot], pol);
+      bulk_g2s(dst + a.z_off, d.zeros + z_lo, zb, &full[slot], pol);
     };
     const int first = min(a.S - P, n_stages);
     if (lane == 0 && pstaged && x_cols > 0 && L_eff > 0) {
       // rotation parameters and s: independent of the previous kernel, latency-critical
       mbar_arrive_expect_tx(pbar, p_cs_bytes + p_ix_bytes + p_s_bytes);
-      bulk_g2s_nohint(pslot, reinterpret_cast<const uint8_t*>(a.rot_cs) + static_cast<size_t>(g0) * 32 * L_eff * 16,
+      bulk_g2s_nohint(pslot, reinterpret_cast<const uint8_t*>(d.rot_cs) + static_cast<size_t>(g0) * 32 * L_eff * 16,
                       p_cs_bytes, pbar);
       bulk_g2s_nohint(pslot + p_cs_bytes,
-                      reinterpret_cast<const uint8_t*>(a.rot_idx) + static_cast<size_t>(g0) * 32 * L_eff * 4,
+                      reinterpret_cast<const uint8_t*>(d.rot_idx) + static_cast<size_t>(g0) * 32 * L_eff * 4,
                       p_ix_bytes, pbar);
-      bulk_g2s_nohint(pslot + p_cs_bytes + p_ix_bytes, a.svec + g0 * GRP, p_s_bytes, pbar);
+      bulk_g2s_nohint(pslot + p_cs_bytes + p_ix_bytes, d.svec + g0 * GRP, p_s_bytes, pbar);
     }
     if (a.pdl) pdl_wait();  // x may be produced by the previous kernel on the stream
     if (lane == 0) {
@@ -272,8 +280,8 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
 #pragma unroll
           for (int t = 0; t < 8; ++t)
             if (t < L_eff) {
-              csr[t] = __ldg(reinterpret_cast<const float4*>(a.rot_cs) + rec + t * 32);
-              ixr[t] = __ldg(reinterpret_cast<const uint32_t*>(a.rot_idx) + rec + t * 32);
+              csr[t] = __ldg(reinterpret_cast<const float4*>(d.rot_cs) + rec + t * 32);
+              ixr[t] = __ldg(reinterpret_cast<const uint32_t*>(d.rot_idx) + rec + t * 32);
             }
         }
       }
@@ -288,7 +296,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
           else if (pstaged && L_eff > 0)
             sv[i] = reinterpret_cast<const float*>(pslot + p_cs_bytes + p_ix_bytes)[k];
           else
-            sv[i] = __ldg(a.svec + g0 * GRP + k);
+            sv[i] = __ldg(d.svec + g0 * GRP + k);
         }
       }
       if (!have) break;
@@ -475,10 +483,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
     }
   }
   if (threadIdx.x == 0) PARO_TL(a, 4);
-  if (a.pdl) {
-    pdl_launch_dependents();
-    pdl_wait();  // y may still be read by the previous kernel (no-op once it has finished)
-  }
+  if (a.pdl) pdl_wait();  // y may still be read by the previous kernel (no-op once it has finished)
 
   // ------------------------------------------------------------ cross-warp reduction + epilogue (a8)
   named_bar_sync(1, n_compute_warps * 32);
@@ -489,8 +494,8 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
     for (int w = 0; w < WK; ++w) sum += part[(static_cast<size_t>(w) * a.rows_max + row) * BT + b];
     const int64_t n = static_cast<int64_t>(row_begin) + row;
     float v = sum * TWO_P24;
-    if (a.bias) v += __ldg(a.bias + n);
-    store_out(a.y, a.y_dtype, static_cast<int64_t>(b) * a.N + n, v);
+    if (d.bias) v += __ldg(d.bias + n);
+    store_out(d.y, a.y_dtype, static_cast<int64_t>(b) * d.N + n, v);
   }
   if (threadIdx.x == 0) PARO_TL(a, 5);
 }
@@ -580,8 +585,19 @@ static int max_resident_ctas(int BT, int J, int threads, int smem, int CL) {
   return per_sm * device_sm_count();
 }
 
-bool plan_gemv(int B_tile, int64_t N, int64_t K, int L, int rotate, GemvConfig* cfg, const char** why) {
+bool plan_gemv(int B_tile, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, int rotate, GemvConfig* cfg,
+               const char** why) {
   GemvConfig c{};
+  if (n_lin < 1 || n_lin > GEMV_MAX_LIN) {
+    *why = "1..4 linears per decode launch";
+    return false;
+  }
+  int64_t N = 0;
+  int L = 0;
+  for (int i = 0; i < n_lin; ++i) {
+    N += Ns[i];
+    L = std::max(L, Ls[i]);
+  }
   c.BT = B_tile <= 1 ? 1 : B_tile <= 2 ? 2 : 4;
   const int G = static_cast<int>(K / GRP);
   // J: contiguous 32-K chunks per lane per row (all in one 128-group).  Smallest J that
@@ -612,10 +628,9 @@ bool plan_gemv(int B_tile, int64_t N, int64_t K, int L, int rotate, GemvConfig* 
   while (CL > 1 && CL > G) CL /= 2;
   c.CL = CL;
   GemvArgs& a = c.a;
-  a.N = static_cast<int>(N);
+  a.n_lin = n_lin;
   a.K = static_cast<int>(K);
   a.G = G;
-  a.L = L;
   a.rotate = rotate;
   a.WK = WK;
   a.RG = RG;
@@ -637,10 +652,36 @@ bool plan_gemv(int B_tile, int64_t N, int64_t K, int L, int rotate, GemvConfig* 
   int ctas_per_sm = (u_bytes <= 40 * 1024) ? 2 : 1;
   if (const char* e = getenv("PARO_CTAS_PER_SM")) ctas_per_sm = atoi(e) == 1 ? 1 : ctas_per_sm;
   const int budget = (smem_optin() + 1024) / ctas_per_sm - 2048;
+  // split the grid's clusters over the linears in proportion to their rows (>= 1 each)
+  auto split = [&](int grid) -> bool {
+    const int ncl = grid / CL;
+    if (ncl < n_lin) return false;
+    int cl[GEMV_MAX_LIN], used = 0, big = 0;
+    for (int i = 0; i < n_lin; ++i) {
+      cl[i] = std::max<int>(1, static_cast<int>(static_cast<double>(ncl) * Ns[i] / N));
+      used += cl[i];
+      if (Ns[i] > Ns[big]) big = i;
+    }
+    cl[big] += ncl - used;
+    if (cl[big] < 1) return false;
+    int begin = 0;
+    a.rows_max = 0;
+    for (int i = 0; i < n_lin; ++i) {
+      GemvLinear& d = a.lin[i];
+      d.N = static_cast<int>(Ns[i]);
+      d.L = Ls[i];
+      d.cta_begin = begin;
+      d.n_ctas = cl[i] * CL;
+      if (d.n_ctas > Ns[i]) return false;  // at least one row per CTA
+      d.rows_base = static_cast<int>(Ns[i] / d.n_ctas);
+      d.rows_extra = static_cast<int>(Ns[i] % d.n_ctas);
+      a.rows_max = std::max(a.rows_max, d.rows_base + (d.rows_extra ? 1 : 0));
+      begin += d.n_ctas;
+    }
+    return true;
+  };
   auto layout = [&](int grid) -> bool {
-    a.rows_base = static_cast<int>(N / grid);
-    a.rows_extra = static_cast<int>(N % grid);
-    a.rows_max = a.rows_base + (a.rows_extra ? 1 : 0);
+    if (!split(grid)) return false;
     uint32_t off = 0;
     a.off_u = off;
     off += u_bytes;
@@ -680,11 +721,12 @@ bool plan_gemv(int B_tile, int64_t N, int64_t K, int L, int rotate, GemvConfig* 
     }
     return true;
   };
-  const int64_t max_ctas = (N + 1) / 2;  // at least one row pair per CTA
+  int64_t max_ctas = 0;  // at least one row pair per CTA
+  for (int i = 0; i < n_lin; ++i) max_ctas += std::max<int64_t>(CL, (Ns[i] + 1) / 2 / CL * CL);
   int grid = sms * ctas_per_sm;
   for (int iter = 0; iter < 3; ++iter) {
     grid = static_cast<int>(std::min<int64_t>(grid, max_ctas)) / CL * CL;
-    if (grid < CL) grid = CL;
+    if (grid < CL * n_lin) grid = CL * n_lin;
     if (!layout(grid)) {
       *why = "decode kernel shared-memory plan does not fit";
       return false;

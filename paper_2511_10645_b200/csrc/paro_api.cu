@@ -302,6 +302,61 @@ size_t paro_linear_workspace(int64_t B, int64_t N, int64_t K, int32_t n_rot, int
   return ws;
 }
 
+
+// transform tables to use for linear i of a decode launch (on-the-fly override or packed)
+struct RotOverride {
+  const float2* cs;
+  const uchar2* idx;
+  const float* s;
+  int active;
+};
+static RotOverride rot_cs_override(const float2* cs, const uchar2* idx, const float* s, int on) {
+  return RotOverride{cs, idx, s, on};
+}
+
+static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, int n, const paro_packed* packed,
+                                  RotOverride ov, const float* const* bias, void* const* y, paro_dtype y_dtype,
+                                  int rotate, int pdl, int debug, cudaStream_t cs) {
+  int64_t Ns[paro::GEMV_MAX_LIN];
+  int Ls[paro::GEMV_MAX_LIN];
+  for (int i = 0; i < n; ++i) {
+    Ns[i] = packed[i].N;
+    Ls[i] = packed[i].n_rot;
+  }
+  const int64_t K = packed[0].K;
+  int bt = B >= 4 ? 4 : (B >= 2 ? 2 : 1);
+  paro::GemvConfig cfg;
+  const char* why = "";
+  while (!paro::plan_gemv(bt, n, Ns, Ls, K, rotate, &cfg, &why)) {
+    if (bt == 1) return fail(PARO_ERR_UNSUPPORTED, "paro_linear: %s", why);
+    bt /= 2;
+  }
+  const size_t xe = 2, ye = dtype_bytes(y_dtype);
+  for (int64_t b0 = 0; b0 < B; b0 += cfg.BT) {
+    paro::GemvArgs& a = cfg.a;
+    a.x = static_cast<const uint8_t*>(x) + b0 * K * xe;
+    a.x_bf16 = x_dtype == PARO_BF16;
+    a.B = static_cast<int>(std::min<int64_t>(cfg.BT, B - b0));
+    for (int i = 0; i < n; ++i) {
+      paro::GemvLinear& d = a.lin[i];
+      d.codes = static_cast<const uint8_t*>(packed[i].codes);
+      d.scales = static_cast<const uint8_t*>(packed[i].scales);
+      d.zeros = static_cast<const uint8_t*>(packed[i].zeros);
+      d.rot_cs = ov.active ? ov.cs : static_cast<const float2*>(packed[i].rot_cs);
+      d.rot_idx = ov.active ? ov.idx : static_cast<const uchar2*>(packed[i].rot_idx);
+      d.svec = ov.active ? ov.s : static_cast<const float*>(packed[i].svec);
+      d.bias = bias ? bias[i] : nullptr;
+      d.y = static_cast<uint8_t*>(y[i]) + b0 * packed[i].N * ye;
+    }
+    a.y_dtype = static_cast<int>(y_dtype);
+    a.pdl = pdl;
+    a.debug = debug;
+    cudaError_t e = paro::launch_gemv(cfg, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "paro_linear: decode GEMV launch");
+  }
+  return PARO_OK;
+}
+
 static paro_status check_packed(const paro_packed* p) {
   if (!p) return fail(PARO_ERR_INVALID_ARGUMENT, "packed is NULL");
   if (p->group != kG) return fail(PARO_ERR_UNSUPPORTED, "packed->group must be 128");
@@ -369,33 +424,40 @@ paro_status paro_linear(const void* x, paro_dtype x_dtype, int64_t B, const paro
     return PARO_OK;
   }
   // decode GEMV over token tiles
-  int bt = B >= 4 ? 4 : (B >= 2 ? 2 : 1);
-  paro::GemvConfig cfg;
-  const char* why = "";
-  while (!paro::plan_gemv(bt, N, K, L, rotate, &cfg, &why)) {
-    if (bt == 1) return fail(PARO_ERR_UNSUPPORTED, "paro_linear: %s", why);
-    bt /= 2;
+  return decode_linears(x, x_dtype, B, 1, packed, rot_cs_override(rot_cs, rot_idx, svec, on_the_fly), &bias, &y,
+                        y_dtype, rotate, pdl, (flags & 0x100u) ? 1 : 0, cs);
+}
+
+paro_status paro_linear_multi(const void* x, paro_dtype x_dtype, int64_t B, int32_t n, const paro_packed* packed,
+                              const float* const* bias, void* const* y, paro_dtype y_dtype, uint32_t flags,
+                              void* workspace, size_t workspace_bytes, void* stream) {
+  if (n < 1 || n > paro::GEMV_MAX_LIN || !packed || !y)
+    return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear_multi: 1..4 linears, packed and y arrays required");
+  for (int i = 0; i < n; ++i) {
+    paro_status st = check_packed(&packed[i]);
+    if (st != PARO_OK) return st;
+    if (packed[i].K != packed[0].K) return fail(PARO_ERR_SHAPE, "paro_linear_multi: all linears must share K");
+    if (!y[i] || !aligned16(y[i])) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear_multi: y[%d] NULL/misaligned", i);
   }
-  for (int64_t b0 = 0; b0 < B; b0 += cfg.BT) {
-    paro::GemvArgs& a = cfg.a;
-    a.x = static_cast<const uint8_t*>(x) + b0 * K * xe;
-    a.x_bf16 = x_dtype == PARO_BF16;
-    a.B = static_cast<int>(std::min<int64_t>(cfg.BT, B - b0));
-    a.codes = static_cast<const uint8_t*>(packed->codes);
-    a.scales = static_cast<const uint8_t*>(packed->scales);
-    a.zeros = static_cast<const uint8_t*>(packed->zeros);
-    a.rot_cs = rot_cs;
-    a.rot_idx = rot_idx;
-    a.svec = svec;
-    a.bias = bias;
-    a.y = static_cast<uint8_t*>(y) + b0 * N * ye;
-    a.y_dtype = static_cast<int>(y_dtype);
-    a.pdl = pdl;
-    a.debug = (flags & 0x100u) ? 1 : 0;  // internal: event timeline
-    cudaError_t e = paro::launch_gemv(cfg, cs);
-    if (e != cudaSuccess) return cuda_fail(e, "paro_linear: decode GEMV launch");
+  if (!x || !aligned16(x) || B <= 0) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear_multi: bad x/B");
+  if (x_dtype != PARO_F16 && x_dtype != PARO_BF16) return fail(PARO_ERR_UNSUPPORTED, "x must be fp16 or bf16");
+  if (y_dtype != PARO_F16 && y_dtype != PARO_BF16 && y_dtype != PARO_F32)
+    return fail(PARO_ERR_UNSUPPORTED, "y must be fp16, bf16 or fp32");
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  bool prefill = false;
+  for (int i = 0; i < n; ++i) prefill = prefill || use_prefill(B, packed[i].N, packed[i].K, flags);
+  if (prefill || n == 1) {  // prefill: one GEMM per linear (each with its own transform)
+    for (int i = 0; i < n; ++i) {
+      paro_status st = paro_linear(x, x_dtype, B, &packed[i], nullptr, nullptr, nullptr, 0, bias ? bias[i] : nullptr,
+                                   y[i], y_dtype, flags, workspace, workspace_bytes, stream);
+      if (st != PARO_OK) return st;
+    }
+    return PARO_OK;
   }
-  return PARO_OK;
+  const int rotate = (flags & PARO_LINEAR_NO_ROTATION) ? 0 : 1;
+  const int pdl = (flags & PARO_LINEAR_PDL) ? 1 : 0;
+  return decode_linears(x, x_dtype, B, n, packed, rot_cs_override(nullptr, nullptr, nullptr, 0), bias, y, y_dtype,
+                        rotate, pdl, (flags & 0x100u) ? 1 : 0, cs);
 }
 
 paro_status paro_transform_activations(const void* x, paro_dtype x_dtype, int64_t B, const paro_packed* packed,

@@ -10,10 +10,11 @@ cudaError_t launch_pack(const void* W, const float* s, const void* cs64, const v
                         void* codes, void* scales, void* zeros, int* status, cudaStream_t st);
 
 // ---------------------------------------------------------------- decode GEMV
-struct GemvArgs {
-  const void* x;  // [B][K] fp16 / bf16
-  int x_bf16;
-  int B;          // live tokens in this launch (<= BT)
+constexpr int GEMV_MAX_LIN = 4;  // linears sharing one activation in a single launch
+
+// One linear of a (multi-)linear decode launch: its CTAs are [cta_begin, cta_begin + n_ctas)
+// (whole clusters), its rows split evenly over them.
+struct GemvLinear {
   const uint8_t* codes;
   const uint8_t* scales;  // fp16 bytes
   const uint8_t* zeros;
@@ -22,8 +23,18 @@ struct GemvArgs {
   const float* svec;
   const float* bias;
   void* y;  // [B][N]
+  int N, L;
+  int cta_begin, n_ctas, rows_base, rows_extra;
+};
+
+struct GemvArgs {
+  const void* x;  // [B][K] fp16 / bf16 (shared by all linears of the launch)
+  int x_bf16;
+  int B;          // live tokens in this launch (<= BT)
+  int n_lin;
+  GemvLinear lin[GEMV_MAX_LIN];
   int y_dtype;
-  int N, K, G, L;
+  int K, G;
   int rotate;
   int pdl;
   int debug;      // record a per-CTA event timeline (g_paro_timeline)
@@ -33,7 +44,7 @@ struct GemvArgs {
   int S;          // ring depth
   int param_slots;  // ring slots lent to the staged rotation parameters (-1: dedicated region)
   uint32_t off_param;
-  int rows_base, rows_extra, rows_max;
+  int rows_max;
   uint32_t slot_bytes, sc_off, z_off;  // per-stage slot layout
   uint32_t off_u, off_usum, off_x, off_scr, off_part, off_ring, off_bar, smem_total;
 };
@@ -44,7 +55,9 @@ struct GemvConfig {
 };
 
 // Plan a launch (pure host arithmetic, no CUDA calls except a cached device query).
-bool plan_gemv(int B_tile, int64_t N, int64_t K, int L, int rotate, GemvConfig* cfg, const char** why);
+// n_lin linears of widths Ns[i] and rotation counts Ls[i] sharing K (and x).
+bool plan_gemv(int B_tile, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, int rotate, GemvConfig* cfg,
+               const char** why);
 cudaError_t launch_gemv(const GemvConfig& cfg, cudaStream_t st);
 
 // ---------------------------------------------------------------- activation transform (prefill pre-stage)

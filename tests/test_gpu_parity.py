@@ -227,3 +227,24 @@ def test_prefill_full_size_sampled(paro):
     toks = np.sort(np.random.default_rng(2).choice(B, size=64, replace=False))
     y_ref = O.oracle_linear(p["x"][toks], ref, p["s"], p["theta"], p["pairs"])
     assert O.normwise_error(y[toks][:, rows], y_ref) <= TOL
+
+
+@pytest.mark.parametrize("B", [1, 3])
+def test_linear_multi_shared_x(paro, B):
+    """q/k/v-style: three linears with their own transforms reading the same x, one launch."""
+    K = 1024
+    shapes = [(512, K), (128, K), (256, K)]
+    probs = [synth.make_problem(N, K, B, seed=100 + i, with_bias=(i == 1)) for i, (N, _) in enumerate(shapes)]
+    x = probs[0]["x"]
+    packs, refs = [], []
+    for p in probs:
+        t = dev_tensors(p)
+        pk, ref = check_pack(paro, p, t)
+        packs.append(pk)
+        refs.append(ref)
+    xt = torch.from_numpy(x).cuda()
+    bias = [None if p["bias"] is None else torch.from_numpy(p["bias"]).cuda() for p in probs]
+    ys = paro.paro_linear_multi(xt, packs, bias=bias)
+    for p, ref, y in zip(probs, refs, ys):
+        y_ref = O.oracle_linear(x, ref, p["s"], p["theta"], p["pairs"], bias=p["bias"])
+        assert O.normwise_error(y.float().cpu().numpy(), y_ref) <= TOL

@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int WK = a.WK;
-  const int n_compute_warps = WK;
+  const int n_compute_warps = WK * a.RG;
   const bool is_producer = warp == n_compute_warps;
   // which linear this CTA serves (CTA ranges are whole clusters)
   int li = 0;
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
     PARO_TL(a, 0);
     for (int i = 0; i < a.S; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], n_compute_warps);
+      mbar_init(&empty[i], WK);  // a stage is consumed by the WK warps of one row group
     }
     mbar_init(xbar, 1);
     mbar_init(xpbar, 1);
@@ -229,15 +229,13 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
         mbar_wait(pfree, 0);
         for (; st < min(a.S, n_stages); ++st) issue(st, st);
       }
-      int slot = 0;
-      uint32_t phase = 1;  // stages >= S: the ring has wrapped once
+      // stages >= S reuse the slot of stage st - S (same row group: S % RG == 0)
+      const int RGN = a.RG, SP = a.S / RGN;
       for (; st < n_stages; ++st) {
-        mbar_wait(&empty[slot], phase ^ 1);  // stage st - S released by all consumers
+        const int use = st / RGN;
+        const int slot = st % RGN + RGN * (use % SP);
+        mbar_wait(&empty[slot], ((use / SP) & 1) ^ 1);  // stage st - S released by its row group
         issue(st, slot);
-        if (++slot == a.S) {
-          slot = 0;
-          phase ^= 1;
-        }
       }
     }
     __syncwarp();
@@ -373,7 +371,10 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
   // warp wk: K slice [wk*512*J, (wk+1)*512*J); lane hl of a half-warp owns 32*J
   // contiguous K (one 128-group).  Slot j of a lane holds chunk (j + hl) % J of its
   // span, so the per-slot 16-byte code loads of the 16 lanes hit distinct banks.
-  const int wk = warp;
+  // row group rg consumes stages rg, rg + RG, ... (all eight row pairs of each)
+  const int wk = warp % WK;
+  const int rg = warp / WK;
+  const int RGN = a.RG;
   const int h = lane >> 4;
   const int hl = lane & 15;
   const int kbase = wk * (512 * J) + hl * (32 * J);
@@ -406,11 +407,17 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
 
   // stage slots as 32-bit shared addresses (no generic->shared conversion in the loop)
   const uint32_t ring_a = smem_u32(ring);
-  int slot = 0;
-  uint32_t phase = 0;
-  for (int st = 0; st < n_stages; ++st) {
+  // row group rg owns slots rg, rg + RG, ... so every slot is consumed by one row group
+  // in order (mbarrier parity waits can only look one phase ahead)
+  const int SP = a.S / RGN;
+  for (int st = rg; st < n_stages; st += RGN) {
+    const int use = st / RGN;
+    const int slot = rg + RGN * (use % SP);
+    const uint32_t phase = (use / SP) & 1;
+    if (st == n_stages - 1 && threadIdx.x == 0) PARO_TL(a, 10);  // consumer reached the last stage
     mbar_wait(&full[slot], phase);
     if (st == 0 && threadIdx.x == 0) PARO_TL(a, 3);
+    if (st == n_stages - 1 && threadIdx.x == 0) PARO_TL(a, 11);  // last stage's bytes landed
     const uint32_t sbase = ring_a + static_cast<uint32_t>(slot) * a.slot_bytes;
     const int r0 = row_begin + st * SR;
     const int nr = min(SR, n_rows - st * SR);
@@ -476,10 +483,6 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
       const int lr = 2 * si + h;
       const bool writer = (hl & (16 / RP - 1)) == 0;
       if (writer && lr < nr) part[(static_cast<size_t>(wk) * a.rows_max + st * SR + lr) * BT + b] = v[0];
-    }
-    if (++slot == a.S) {
-      slot = 0;
-      phase ^= 1;
     }
   }
   if (threadIdx.x == 0) PARO_TL(a, 4);
@@ -616,7 +619,15 @@ bool plan_gemv(int B_tile, int n_lin, const int64_t* Ns, const int* Ls, int64_t 
     *why = "K too large for the decode kernel at this token tile";
     return false;
   }
-  const int RG = 1;
+  // row groups (stage-interleaved): fill up to 8 compute warps per CTA with 2 CTAs/SM,
+  // or 16 with 1 CTA/SM
+  int ctas_per_sm_pref = 2;
+  if (const char* e = getenv("PARO_CTAS_PER_SM")) ctas_per_sm_pref = atoi(e) == 1 ? 1 : 2;
+  const int warp_cap = (ctas_per_sm_pref == 1 && c.BT == 1) ? 16 : 8;  // 544-thread variants are BT = 1
+  int RG = 1;
+  while (RG < 4 && WK * RG * 2 <= warp_cap) RG *= 2;
+  if (const char* e = getenv("PARO_RG")) RG = std::max(1, std::min(4, atoi(e)));
+  if (WK * RG > 16) RG = 1;
   c.J = J;
   const int sms = device_sm_count();
   const int threads = (WK * RG + 1) * 32;
@@ -649,8 +660,7 @@ bool plan_gemv(int B_tile, int n_lin, const int64_t* Ns, const int* Ls, int64_t 
   const uint32_t scr_bytes = align_up(static_cast<uint32_t>(WK * RG) * c.BT * 132 * 4, 128);
   // two CTAs per SM when the activation buffer is small (lets the next kernel's weight
   // prefetch start while this one drains, and doubles the warps hiding latency)
-  int ctas_per_sm = (u_bytes <= 40 * 1024) ? 2 : 1;
-  if (const char* e = getenv("PARO_CTAS_PER_SM")) ctas_per_sm = atoi(e) == 1 ? 1 : ctas_per_sm;
+  int ctas_per_sm = (u_bytes <= 40 * 1024) ? ctas_per_sm_pref : 1;
   const int budget = (smem_optin() + 1024) / ctas_per_sm - 2048;
   // split the grid's clusters over the linears in proportion to their rows (>= 1 each)
   auto split = [&](int grid) -> bool {
@@ -698,10 +708,11 @@ bool plan_gemv(int B_tile, int n_lin, const int64_t* Ns, const int* Ls, int64_t 
     a.off_ring = align_up(off, 1024);
     const int64_t ring_avail = static_cast<int64_t>(budget) - a.off_ring;
     int S = static_cast<int>(ring_avail / a.slot_bytes);
-    const int stages_needed = (a.rows_max + SR - 1) / SR;
+    const int stages_needed = std::max((a.rows_max + SR - 1) / SR, RG);
     if (S > stages_needed) S = stages_needed;
     if (S > 60) S = 60;
-    if (S < 1) return false;
+    S -= S % RG;  // each row group owns S / RG slots
+    if (S < RG) return false;
     a.S = S;
     a.smem_total = a.off_ring + static_cast<uint32_t>(S) * a.slot_bytes;
     // stage the rotation parameters of this CTA's groups in shared memory: a dedicated

@@ -12,19 +12,21 @@ import paper_2511_10645_b200 as paro  # noqa: E402
 import synth  # noqa: E402
 
 N, K, mode = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
+nlin = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 dev = torch.device("cuda")
 p = synth.make_problem(8, K, 1, seed=1)
 s, th, pr = (torch.from_numpy(p[k]).to(dev) for k in ("s", "theta", "pairs"))
-pks = [paro.paro_pack((torch.randn(N, K, device=dev) * 0.02).half(), s, th, pr) for _ in range(2)]
+pks = [[paro.paro_pack((torch.randn(N, K, device=dev) * 0.02).half(), s, th, pr) for _ in range(nlin)]
+       for _ in range(2)]
 x = torch.randn(1, K, device=dev).half()
-y = torch.empty(1, N, device=dev, dtype=torch.half)
+ys = [torch.empty(1, N, device=dev, dtype=torch.half) for _ in range(nlin)]
 fl = paro.PARO_LINEAR_NO_ROTATION if mode == "norot" else 0
 lib = paro._lib
 lib.paro_debug_read_timeline.argtypes = [ctypes.c_void_p, ctypes.c_int]
 for it in range(3):
-    paro.paro_linear(x, pks[0], y=y, flags=fl)
+    paro.paro_linear_multi(x, pks[0], y=ys, flags=fl)
     torch.cuda.synchronize()
-    paro.paro_linear(x, pks[1], y=y, flags=fl | 0x100)
+    paro.paro_linear_multi(x, pks[1], y=ys, flags=fl | 0x100)
     torch.cuda.synchronize()
 buf = np.zeros(1024 * 12, dtype=np.uint64)
 lib.paro_debug_read_timeline(buf.ctypes.data, buf.size)
@@ -33,8 +35,8 @@ live = t[:, 0] > 0
 t = t[live]
 t0 = t[:, 0].min()
 rel = (t - t0) / 1000.0
-names = ["start", "x_arrived", "transform_done", "stage0_ready", "loop_done", "end", "w0_layers_done", "w0_item_out", "w0_layers_start", "w0_layer1_done"]
-print(f"{mode} N={N} K={K}: {live.sum()} CTAs; us relative to first CTA start")
+names = ["start", "x_arrived", "transform_done", "stage0_ready", "loop_done", "end", "w0_layers_done", "w0_item_out", "w0_layers_start", "w0_layer1_done", "reach_last_stage", "last_stage_landed"]
+print(f"{mode} N={N}x{nlin} K={K}: {live.sum()} CTAs; us relative to first CTA start")
 for i, n in enumerate(names):
     col = rel[:, i]
     print(f"  {n:15s} min {col.min():7.2f}  median {np.median(col):7.2f}  max {col.max():7.2f}")

@@ -18,7 +18,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
 # pack.cu must not contract a*b - c*d into FMA: bit-exact fp64 fold (Q7)
 PER_FILE = {"pack.cu": ["-fmad=false"]}
 SOURCES = ["paro_api.cu", "pack.cu", "gemv.cu", "misc.cu", "prefill.cu"]
-HEADERS = ["ptx.cuh", "paro_internal.h", "umma.cuh"]
+HEADERS = ["ptx.cuh", "paro_internal.h", "umma.cuh", "tile_layout.cuh"]
 
 
 def nvcc() -> str:

@@ -1,35 +1,37 @@
-// gemv.cu -- decode path (B <= 4 tokens per launch): scale + L Givens layers fused
-// into the activation staging, then the group-wise INT4 dequant GEMV.
+// gemv.cu -- decode path (B <= 8 tokens per launch): scale + L Givens layers fused
+// into the activation staging, then the group-wise INT4 dequant GEMV on the warp-level
+// tensor cores.
 //
 // SURVEY.md 8(a) rows a4 (stage + scale), a5 (L rotations, Eq. 5 in column form),
 // a6 (dequant GEMV), a8 (epilogue).  One kernel, launched as clusters of CL CTAs
-// (1-2 CTAs per SM, one wave):
+// (1-2 CTAs per SM, one wave).  A cluster owns a run of 16-row blocks of one linear;
+// the tiles (16 rows x one 128-group, tile_layout.cuh) of that run are split evenly and
+// contiguously over its CL CTAs (split-K at tile granularity, so every CTA streams the
+// same number of bytes whatever N and K are).
 //
-//  * producer warp: bulk-copies (cp.async.bulk, TMA engine) first the activations
-//    this CTA transforms, then its contiguous row slice of the packed weight (INT4
-//    codes / fp16 scales / uint4 zeros, row-major) through a ring of shared-memory
-//    stages (SR rows each), completion tracked by mbarriers.
+//  * producer warp: bulk-copies (cp.async.bulk, TMA engine) first the rotation
+//    parameters and the activations this CTA transforms, then its contiguous tile range
+//    (codes / scales / zeros are three contiguous ranges) through a ring of
+//    shared-memory stages (TPS tiles each), completion tracked by mbarriers.
 //  * compute warps, phase 1 (transform; PAPER.md:195-209's token / group / pair
 //    parallelism): the CL CTAs of a cluster split the K/128 groups; a warp owns a
-//    group, keeps its L rotations' (cos, sin, i, j) in registers (loaded before the
-//    producer starts, so they do not queue behind the weight stream), stages the
-//    group in shared memory, scales by s and applies the L independent rotations
-//    (2 pairs per lane per rotation, sync-free inside a rotation, __syncwarp
-//    between rotations).  The fp16 x' of the group -- stored with each 8-channel
-//    block in (0,4,1,5,2,6,3,7) order, the register order the dequantiser wants --
-//    and its 32-channel partial sums go to every CTA of the cluster with st.async
-//    (DSMEM), completion counted in bytes on the receiver's mbarrier.  x' never
-//    goes to HBM.
-//  * compute warps, phase 2 (GEMV): warp wk owns a 512*J-wide K slice; half-warp h
-//    handles row 2p+h of each row pair, lane 32*J consecutive K (one 128-group).
-//    x' lives in registers as fp16 pairs.  Codes are dequantised in registers with
-//    one AND mask per pair of weights: a nibble q in bits [0,4) of an fp16 half IS
-//    the subnormal q*2^-24, in bits [4,8) it is 16q*2^-24; fma.rn.f32.f16 (FHFMA)
-//    multiplies-accumulates those into fp32, exactly scaled by powers of two.
-//    Per (row, group): y += S * (sum q x' - z * sum x').  Row partials are reduced
-//    by a transpose-shuffle over the 16 lanes of a half-warp (eight row pairs per
-//    stage) and across K-slice warps through shared memory in a fixed order
-//    (deterministic).
+//    group, stages it in shared memory, scales by s and applies the L independent
+//    rotations (2 pairs per lane per rotation, sync-free inside a rotation, __syncwarp
+//    between rotations; the pack-time schedule makes every gather / scatter
+//    bank-conflict free).  The fp16 x' of the group -- laid out as mma.sync B fragments
+//    -- and its per-token sum go to every CTA of the cluster with st.async (DSMEM),
+//    completion counted in bytes on the receiver's mbarrier.  x' never goes to HBM.
+//  * compute warps, phase 2 (GEMV): warp w takes tiles w, w + NW, ... of each stage.
+//    Lane (g, t) loads 16 code bytes of row g and of row g + 8 (two LDS.128); one AND
+//    mask per 32-bit word turns 2 nibbles into an fp16 A-fragment register: a nibble q
+//    in bits [0,4) of a half IS the subnormal q * 2^-24 (bits [4,8): 16q * 2^-24), which
+//    the tensor cores multiply exactly.  Eight mma.sync.m16n8k16 per tile (four per
+//    power-of-two scale) give sum_k q[n,k] x'[k, b] for the 16 rows x 8 token columns;
+//    the epilogue applies y += S * (sum q x' - z * sum x') per (row, group, token).
+//    Row partials of a warp go to shared memory when its row block changes; warps are
+//    summed in a fixed order, and the CTA holding the first tile of a row block adds
+//    the partials of the (at most CL - 1) later CTAs that share it, pushed to it with
+//    st.async -- deterministic, no atomics.
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
@@ -38,14 +40,14 @@
 
 #include "paro_internal.h"
 #include "ptx.cuh"
+#include "tile_layout.cuh"
 
 namespace paro {
 
 constexpr int GRP = 128;
-constexpr float TWO_M24 = 5.9604644775390625e-08f;  // 2^-24
-constexpr float TWO_P24 = 16777216.0f;              // 2^24
-constexpr int RP_PER_STAGE = 8;                     // max row pairs per stage (SR <= 16 rows)
-constexpr int TL_EVENTS = 12;                        // debug timeline: events per CTA
+constexpr float TWO_P24 = 16777216.0f;  // 2^24
+constexpr int TL_EVENTS = 12;           // debug timeline: events per CTA
+constexpr uint32_t TILE_BYTES = TILE_CODE_BYTES + TILE_SCALE_BYTES + TILE_ZERO_BYTES;
 
 __device__ unsigned long long g_paro_timeline[1024 * TL_EVENTS];
 
@@ -83,45 +85,55 @@ __device__ __forceinline__ float half2_sum(uint32_t w) {
   return f.x + f.y;
 }
 
-// One 32-bit code word (8 nibbles, k = 8m..8m+7) against the x' pairs
-// P[0]=(k0,k4), P[1]=(k1,k5), P[2]=(k2,k6), P[3]=(k3,k7): low nibbles carry q*2^-24
-// (chain tl), high nibbles 16q*2^-24 (chain th, scaled by 1/16 at the end, exactly).
-__device__ __forceinline__ void dot_word(uint32_t x, const uint32_t* P, float& tl, float& th) {
-  const uint32_t x8 = x >> 8;
-  tl = fma_f16lo(x & 0x000F000Fu, P[0], tl);
-  th = fma_f16lo(x & 0x00F000F0u, P[1], th);
-  tl = fma_f16hi(x & 0x000F000Fu, P[0], tl);
-  th = fma_f16hi(x & 0x00F000F0u, P[1], th);
-  tl = fma_f16lo(x8 & 0x000F000Fu, P[2], tl);
-  th = fma_f16lo(x8 & 0x00F000F0u, P[3], th);
-  tl = fma_f16hi(x8 & 0x000F000Fu, P[2], tl);
-  th = fma_f16hi(x8 & 0x00F000F0u, P[3], th);
+// first cluster-local tile of cluster CTA k (tiles split evenly and contiguously)
+__device__ __forceinline__ int cta_tile_start(int k, int nt, int CL) {
+  return static_cast<int>((static_cast<int64_t>(k) * nt) / CL);
+}
+// the CTA whose (non-empty) range holds cluster-local tile x
+__device__ __forceinline__ int cta_of_tile(int x, int nt, int CL) {
+  int k = 0;
+  for (int c = 1; c < CL; ++c)
+    if (cta_tile_start(c, nt, CL) <= x) k = c;
+  return k;
 }
 
-// MAXT: 288 (<= 8 compute warps) or 544 (<= 16 compute warps, very large K);
-// u' occupies 16*J*BT registers per thread (BT * J <= 4).
-template <int BT, int J, int MAXT>
-__global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_gemv_kernel(const GemvArgs a) {
-  constexpr int RP = RP_PER_STAGE / J;  // row pairs per stage: SR = 2 * RP rows
+// MAXT: 288 (<= 8 compute warps, 2 CTAs / SM) or 544 (<= 16 compute warps)
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(const GemvArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int WK = a.WK;
-  const int n_compute_warps = WK * a.RG;
-  const bool is_producer = warp == n_compute_warps;
+  const int NW = a.NW;
+  const bool is_producer = warp == NW;
   // which linear this CTA serves (CTA ranges are whole clusters)
   int li = 0;
   while (li + 1 < a.n_lin && static_cast<int>(blockIdx.x) >= a.lin[li + 1].cta_begin) ++li;
   const GemvLinear& d = a.lin[li];
-  const int K = a.K, G = a.G, L = d.L;
-  const int ZB = (G + 1) >> 1;
-  const int SR = a.SR;
-  const int NCH = K / 32;  // 32-channel chunks
+  const int K = a.K, G = a.G, L = d.L, B = a.B;
+  const int CL = static_cast<int>(cluster_nctarank());
+  const int crank = static_cast<int>(cluster_ctarank());
+  // this cluster's row blocks and this CTA's tile range [tA, tE) (cluster-local indices)
+  const int cl = (static_cast<int>(blockIdx.x) - d.cta_begin) / CL;
+  const int nrb_c = d.rb_base + (cl < d.rb_extra ? 1 : 0);
+  const int rbc0 = cl * d.rb_base + min(cl, d.rb_extra);
+  const int nt = nrb_c * G;
+  const int tA = cta_tile_start(crank, nt, CL), tE = cta_tile_start(crank + 1, nt, CL);
+  const int n_my = tE - tA;
+  const int TPS = a.TPS;
+  const int n_stages = (n_my + TPS - 1) / TPS;
+  const int rho_first = n_my > 0 ? tA / G : 0;  // cluster-local row block of my first tile
+  const int n_rho = n_my > 0 ? (tE - 1) / G - rho_first + 1 : 0;
+  const bool own_first = n_my > 0 && rho_first * G >= tA;                // its first tile is mine
+  const bool own_last = n_my > 0 && (rho_first + n_rho - 1) * G >= tA;  // likewise for my last block
+  // later CTAs of the cluster that share my last row block (they push their partials)
+  int last_cta = crank;
+  if (own_last && (rho_first + n_rho) * G > tE) last_cta = cta_of_tile((rho_first + n_rho) * G - 1, nt, CL);
 
-  __half* u16 = reinterpret_cast<__half*>(smem + a.off_u);          // x' [BT][K], perm8 order
-  float* usum = reinterpret_cast<float*>(smem + a.off_usum);         // 2^-24 * chunk sums [BT][NCH]
-  uint8_t* xs = smem + a.off_x;                                       // raw x slice [BT][x_cols]
-  float* part = reinterpret_cast<float*>(smem + a.off_part);
+  uint8_t* ufr = smem + a.off_u;                                  // x' fragments [G][4][B][4][4] u32
+  float* xsum = reinterpret_cast<float*>(smem + a.off_xs);        // sum of x' per (group, token) [G][8]
+  uint8_t* xs = smem + a.off_x;                                   // raw x slice [B][x_cols]
+  float* part = reinterpret_cast<float*>(smem + a.off_part);      // [NW][R_max][16][B]
+  float* recv = reinterpret_cast<float*>(smem + a.off_recv);      // [CL-1][16][B]
   uint8_t* ring = smem + a.off_ring;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.off_bar);
   uint64_t* empty = full + a.S;
@@ -129,22 +141,14 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
   uint64_t* xpbar = xbar + 1;    // x' of all K landed (DSMEM st.async from the cluster)
   uint64_t* pbar = xpbar + 1;    // rotation parameters + s of this CTA's groups landed
   uint64_t* pfree = pbar + 1;    // phase 1 done with them (their ring slots can be refilled)
+  uint64_t* rbar = pfree + 1;    // partials of my last row block from later CTAs landed
 
-  const int cta = static_cast<int>(blockIdx.x) - d.cta_begin;
-  const int n_rows = d.rows_base + (cta < d.rows_extra ? 1 : 0);
-  const int row_begin = cta * d.rows_base + min(cta, d.rows_extra);
-  const int n_stages = (n_rows + SR - 1) / SR;
-  const uint32_t CL = cluster_nctarank();
-  const uint32_t crank = cluster_ctarank();
   // groups whose transform this CTA computes
-  const int g_per = (G + static_cast<int>(CL) - 1) / static_cast<int>(CL);
-  const int g0 = min(G, static_cast<int>(crank) * g_per);
+  const int g_per = (G + CL - 1) / CL;
+  const int g0 = min(G, crank * g_per);
   const int g1 = min(G, g0 + g_per);
   const int x_cols = (g1 - g0) * GRP;  // activation columns this CTA stages
   const uint32_t x_row_bytes = static_cast<uint32_t>(x_cols) * 2;
-  // rotation parameters of groups [g0, g1) (lane-major records, contiguous per group) and
-  // s are bulk-copied into the LAST P ring slots before anything else; those slots get
-  // weights only after phase 1 has released them (pfree).
   const int L_eff = a.rotate ? L : 0;
   const uint32_t p_cs_bytes = static_cast<uint32_t>(g1 - g0) * 32 * L_eff * 16;
   const uint32_t p_ix_bytes = static_cast<uint32_t>(g1 - g0) * 32 * L_eff * 4;
@@ -152,7 +156,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
   // staged parameters: in a dedicated region (param_slots < 0) or in the last
   // param_slots ring slots (lent until phase 1 is done); 0: read from global memory
   const bool pded = a.param_slots < 0;
-  const int P = pded ? 0 : a.param_slots;  // lent ring slots
+  const int P = pded ? 0 : a.param_slots;
   const bool pstaged = a.param_slots != 0;
   uint8_t* pslot = pded ? smem + a.off_param : ring + static_cast<size_t>(a.S - P) * a.slot_bytes;
 
@@ -160,13 +164,18 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
     PARO_TL(a, 0);
     for (int i = 0; i < a.S; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], WK);  // a stage is consumed by the WK warps of one row group
+      mbar_init(&empty[i], NW);
     }
     mbar_init(xbar, 1);
     mbar_init(xpbar, 1);
     mbar_init(pbar, 1);
-    mbar_init(pfree, n_compute_warps);
-    if (CL > 1) mbar_arrive_expect_tx(xpbar, static_cast<uint32_t>(BT) * (K * 2 + NCH * 4));
+    mbar_init(pfree, NW);
+    mbar_init(rbar, 1);
+    if (CL > 1) mbar_arrive_expect_tx(xpbar, static_cast<uint32_t>(B) * (K * 2 + G * 4));
+    uint32_t rbytes = 0;
+    for (int c = crank + 1; c <= last_cta; ++c)
+      if (cta_tile_start(c + 1, nt, CL) > cta_tile_start(c, nt, CL)) rbytes += 16 * B * 4;
+    if (rbytes) mbar_arrive_expect_tx(rbar, rbytes);
     fence_mbar_init();
   }
   if (CL > 1) {
@@ -175,36 +184,24 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
   } else {
     __syncthreads();
   }
-  // Let the next kernel on the stream launch now: its CTAs take SM slots as ours retire
-  // and run their prologue (parameter loads) early; its griddepcontrol.wait still
-  // orders every access to data this kernel produces.
   if (a.pdl) pdl_launch_dependents();
 
   // ------------------------------------------------------------ producer warp
   if (is_producer) {
-    // Request order (latency-critical first): the compute warps' rotation-parameter
-    // loads (handshake on barrier 2), then -- after the PDL wait -- the activations,
-    // then the weight ring.  Stages [0, S) need no slot release.
-    named_bar_sync(2, (n_compute_warps + 1) * 32);
+    named_bar_sync(2, (NW + 1) * 32);
     const uint64_t pol = l2_evict_first_policy();
+    const int64_t tile0 = static_cast<int64_t>(rbc0) * G + tA;  // my first tile (global index)
     auto issue = [&](int st, int slot) {
-      const int r0 = row_begin + st * SR;
-      const int nr = min(SR, n_rows - st * SR);
+      const int64_t T = tile0 + static_cast<int64_t>(st) * TPS;
+      const uint32_t nts = static_cast<uint32_t>(min(TPS, n_my - st * TPS));
       uint8_t* dst = ring + static_cast<size_t>(slot) * a.slot_bytes;
-      const uint32_t cb = static_cast<uint32_t>(nr) * (K / 2);
-      const int64_t s_lo = (static_cast<int64_t>(r0) * 2 * G) & ~int64_t(15);
-      const int64_t s_hi = (static_cast<int64_t>(r0 + nr) * 2 * G + 15) & ~int64_t(15);
-      const int64_t z_lo = (static_cast<int64_t>(r0) * ZB) & ~int64_t(15);
-      const int64_t z_hi = (static_cast<int64_t>(r0 + nr) * ZB + 15) & ~int64_t(15);
-      const uint32_t sb = static_cast<uint32_t>(s_hi - s_lo), zb = static_cast<uint32_t>(z_hi - z_lo);
-      mbar_arrive_expect_tx(&full[slot], cb + sb + zb);
-      bulk_g2s(dst, d.codes + static_cast<int64_t>(r0) * (K / 2), cb, &full[slot], pol);
-      bulk_g2s(dst + a.sc_off, d.scales + s_lo, sb, &full[slot], pol);
-      bulk_g2s(dst + a.z_off, d.zeros + z_lo, zb, &full[slot], pol);
+      mbar_arrive_expect_tx(&full[slot], nts * TILE_BYTES);
+      bulk_g2s(dst, d.codes + T * TILE_CODE_BYTES, nts * TILE_CODE_BYTES, &full[slot], pol);
+      bulk_g2s(dst + a.sc_off, d.scales + T * TILE_SCALE_BYTES, nts * TILE_SCALE_BYTES, &full[slot], pol);
+      bulk_g2s(dst + a.z_off, d.zeros + T * TILE_ZERO_BYTES, nts * TILE_ZERO_BYTES, &full[slot], pol);
     };
     const int first = min(a.S - P, n_stages);
     if (lane == 0 && pstaged && x_cols > 0 && L_eff > 0) {
-      // rotation parameters and s: independent of the previous kernel, latency-critical
       mbar_arrive_expect_tx(pbar, p_cs_bytes + p_ix_bytes + p_s_bytes);
       bulk_g2s_nohint(pslot, reinterpret_cast<const uint8_t*>(d.rot_cs) + static_cast<size_t>(g0) * 32 * L_eff * 16,
                       p_cs_bytes, pbar);
@@ -216,25 +213,21 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
     if (a.pdl) pdl_wait();  // x may be produced by the previous kernel on the stream
     if (lane == 0) {
       if (x_cols > 0) {
-        mbar_arrive_expect_tx(xbar, x_row_bytes * static_cast<uint32_t>(a.B));
-        for (int b = 0; b < a.B; ++b)
+        mbar_arrive_expect_tx(xbar, x_row_bytes * static_cast<uint32_t>(B));
+        for (int b = 0; b < B; ++b)
           bulk_g2s_nohint(xs + static_cast<size_t>(b) * x_row_bytes,
                           static_cast<const uint8_t*>(a.x) + (static_cast<int64_t>(b) * K + g0 * GRP) * 2,
                           x_row_bytes, xbar);
       }
       for (int st = 0; st < first; ++st) issue(st, st);
-      // the lent slots: first use once phase 1 released them, then the normal ring
       int st = first;
-      if (P > 0) {
+      if (P > 0) {  // the lent slots: first use once phase 1 released them
         mbar_wait(pfree, 0);
         for (; st < min(a.S, n_stages); ++st) issue(st, st);
       }
-      // stages >= S reuse the slot of stage st - S (same row group: S % RG == 0)
-      const int RGN = a.RG, SP = a.S / RGN;
       for (; st < n_stages; ++st) {
-        const int use = st / RGN;
-        const int slot = st % RGN + RGN * (use % SP);
-        mbar_wait(&empty[slot], ((use / SP) & 1) ^ 1);  // stage st - S released by its row group
+        const int slot = st % a.S;
+        mbar_wait(&empty[slot], ((st / a.S) & 1) ^ 1);  // stage st - S consumed by every warp
         issue(st, slot);
       }
     }
@@ -244,27 +237,28 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
 
   // ------------------------------------------------------------ phase 1: activation transform
   {
-    float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * (BT * 132);
-    const uint32_t u_addr = smem_u32(u16), s_addr = smem_u32(usum), bar_addr = smem_u32(xpbar);
-    const int b8 = (lane >> 1) * 8, hh = lane & 1;  // output: lane writes half hh of 8-block b8
-    const int c0 = b8 + 2 * hh;
+    float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * (B * 132);
+    const uint32_t u_addr = smem_u32(ufr), s_addr = smem_u32(xsum), bar_addr = smem_u32(xpbar);
+    // output: lane (i4, t4, hf) writes B-fragment registers 4*i4 + 2*hf, +1 of fragment lane t4
+    // (MMA m = 2*i4 + hf: channels (16m + 2t4, +1) and (16m + 2t4 + 8, +9))
+    const int i4 = lane >> 3, t4 = (lane >> 1) & 3, hf = lane & 1;
+    const int k0 = 16 * (2 * i4 + hf) + 2 * t4;
     bool first = true;
-    for (int gam = g0 + warp; gam < g1 || first; gam += n_compute_warps) {
+    for (int gam = g0 + warp; gam < g1 || first; gam += NW) {
       const bool have = gam < g1;
-      // rotation parameters of this group -> registers (independent of the previous kernel)
-      // records [group][t][32 lanes]: (cos0, sin0, cos1, sin1) and (i0, j0, i1, j1)
       float4 csr[8];
       uint32_t ixr[8];
       float sv[4];
       if (first) {
-        named_bar_arrive(2, (n_compute_warps + 1) * 32);  // let the producer start
+        named_bar_arrive(2, (NW + 1) * 32);  // let the producer start
         if (pstaged && x_cols > 0 && L_eff > 0) mbar_wait(pbar, 0);
         if (x_cols > 0) mbar_wait(xbar, 0);
         if (threadIdx.x == 0) PARO_TL(a, 1);
         first = false;
       }
-      if (have && L_eff > 0) {
-        if (pstaged) {  // staged in shared memory, records [group][t][32 lanes]
+      if (!have) break;
+      if (L_eff > 0) {
+        if (pstaged) {  // records [group][t][32 lanes]
           const float4* csp = reinterpret_cast<const float4*>(pslot) + (gam - g0) * L_eff * 32 + lane;
           const uint32_t* ixp = reinterpret_cast<const uint32_t*>(pslot + p_cs_bytes) + (gam - g0) * L_eff * 32 + lane;
 #pragma unroll
@@ -283,29 +277,23 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
             }
         }
       }
-      if (have) {
-        // two explicit paths: a runtime-selected shared/global pointer would compile to
-        // generic loads, which queue behind the weight stream
+      // two explicit paths: a runtime-selected shared/global pointer compiles to generic loads
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int k = (gam - g0) * GRP + lane + 32 * i;
-          if (!a.rotate)
-            sv[i] = 1.f;
-          else if (pstaged && L_eff > 0)
-            sv[i] = reinterpret_cast<const float*>(pslot + p_cs_bytes + p_ix_bytes)[k];
-          else
-            sv[i] = __ldg(d.svec + g0 * GRP + k);
-        }
+      for (int i = 0; i < 4; ++i) {
+        const int k = (gam - g0) * GRP + lane + 32 * i;
+        if (!a.rotate)
+          sv[i] = 1.f;
+        else if (pstaged && L_eff > 0)
+          sv[i] = reinterpret_cast<const float*>(pslot + p_cs_bytes + p_ix_bytes)[k];
+        else
+          sv[i] = __ldg(d.svec + g0 * GRP + k);
       }
-      if (!have) break;
       const int kg = gam * GRP;
-#pragma unroll
-      for (int b = 0; b < BT; ++b)
+      for (int b = 0; b < B; ++b)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int k = lane + 32 * i;
-          float v = 0.f;
-          if (b < a.B) v = load_act(xs + static_cast<size_t>(b) * x_row_bytes, a.x_bf16, kg - g0 * GRP + k);
+          const float v = load_act(xs + static_cast<size_t>(b) * x_row_bytes, a.x_bf16, kg - g0 * GRP + k);
           scr[b * 132 + k] = v * sv[i];  // diag(s) x  (a4)
         }
       __syncwarp();
@@ -313,11 +301,10 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
 #pragma unroll
       for (int t = 0; t < 8; ++t) {  // a5: rotations t = 1..L, Eq. 4 form, pre-update values
         if (t >= L_eff) break;
-#pragma unroll
-        for (int b = 0; b < BT; ++b) {
+        const uint32_t i0 = ixr[t] & 0xff, j0 = (ixr[t] >> 8) & 0xff;
+        const uint32_t i1 = (ixr[t] >> 16) & 0xff, j1 = ixr[t] >> 24;
+        for (int b = 0; b < B; ++b) {
           float* sb = scr + b * 132;
-          const uint32_t i0 = ixr[t] & 0xff, j0 = (ixr[t] >> 8) & 0xff;
-          const uint32_t i1 = (ixr[t] >> 16) & 0xff, j1 = ixr[t] >> 24;
           const float a0 = sb[i0], b0 = sb[j0];
           const float a1 = sb[i1], b1 = sb[j1];
           sb[i0] = csr[t].x * a0 - csr[t].y * b0;
@@ -326,32 +313,28 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
           sb[j1] = csr[t].w * a1 + csr[t].z * b1;
         }
         __syncwarp();
-        if (threadIdx.x == 0 && gam == g0 && t == 0) PARO_TL(a, 9);
       }
       if (threadIdx.x == 0 && gam == g0) PARO_TL(a, 6);
-#pragma unroll
-      for (int b = 0; b < BT; ++b) {
+      for (int b = 0; b < B; ++b) {
         const float* sb = scr + b * 132;
-        // perm8 order: pairs (c0, c0+4), (c0+1, c0+5) of the lane's 8-block half
-        const uint32_t p0 = pack_half2(sb[c0], sb[c0 + 4]);
-        const uint32_t p1 = pack_half2(sb[c0 + 1], sb[c0 + 5]);
-        // 32-channel chunk sums of the fp16-rounded x' (chunk = 8 lanes)
+        const uint32_t p0 = pack_half2(sb[k0], sb[k0 + 1]);
+        const uint32_t p1 = pack_half2(sb[k0 + 8], sb[k0 + 9]);
+        // sum over the group of the fp16-rounded x' (the zero-point term uses exactly the
+        // values the tensor cores multiply)
         float cs = half2_sum(p0) + half2_sum(p1);
-        cs += __shfl_xor_sync(0xffffffffu, cs, 1);
-        cs += __shfl_xor_sync(0xffffffffu, cs, 2);
-        cs += __shfl_xor_sync(0xffffffffu, cs, 4);
-        cs *= TWO_M24;
-        const uint32_t uo = u_addr + static_cast<uint32_t>((b * K + kg + b8) * 2 + hh * 8);
-        const uint32_t so = s_addr + static_cast<uint32_t>((b * NCH + (kg >> 5) + (lane >> 3)) * 4);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+        const uint32_t uo = u_addr + static_cast<uint32_t>(((gam * 4 + i4) * B + b) * 64 + t4 * 16 + hf * 8);
+        const uint32_t so = s_addr + static_cast<uint32_t>((gam * 8 + b) * 4);
         if (CL > 1) {
-          for (uint32_t r = 0; r < CL; ++r) {
+          for (int r = 0; r < CL; ++r) {
             const uint32_t rb = mapa(bar_addr, r);
             st_async_v2(mapa(uo, r), p0, p1, rb);
-            if ((lane & 7) == 0) st_async_b32(mapa(so, r), __float_as_uint(cs), rb);
+            if (lane == 0) st_async_b32(mapa(so, r), __float_as_uint(cs), rb);
           }
         } else {
-          *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(u16) + (uo - u_addr)) = make_uint2(p0, p1);
-          if ((lane & 7) == 0) usum[b * NCH + (kg >> 5) + (lane >> 3)] = cs;
+          *reinterpret_cast<uint2*>(ufr + (uo - u_addr)) = make_uint2(p0, p1);
+          if (lane == 0) xsum[gam * 8 + b] = cs;
         }
       }
       __syncwarp();
@@ -362,143 +345,139 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 288 && BT == 1) ? 2 : 1) paro_g
     if (CL > 1) {
       mbar_wait(xpbar, 0);  // every group's x' has arrived from its owner CTA
     } else {
-      named_bar_sync(1, n_compute_warps * 32);
+      named_bar_sync(1, NW * 32);
     }
   }
   if (threadIdx.x == 0) PARO_TL(a, 2);
 
-  // ------------------------------------------------------------ phase 2: GEMV
-  // warp wk: K slice [wk*512*J, (wk+1)*512*J); lane hl of a half-warp owns 32*J
-  // contiguous K (one 128-group).  Slot j of a lane holds chunk (j + hl) % J of its
-  // span, so the per-slot 16-byte code loads of the 16 lanes hit distinct banks.
-  // row group rg consumes stages rg, rg + RG, ... (all eight row pairs of each)
-  const int wk = warp % WK;
-  const int rg = warp / WK;
-  const int RGN = a.RG;
-  const int h = lane >> 4;
-  const int hl = lane & 15;
-  const int kbase = wk * (512 * J) + hl * (32 * J);
-  const bool act = kbase < K;
-  uint32_t uP[J][BT][16];
-  float Us[BT];
-#pragma unroll
-  for (int b = 0; b < BT; ++b) {
-    Us[b] = 0.f;
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const int k0 = kbase + 32 * ((j + hl) & (J - 1));
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        uint4 q = make_uint4(0u, 0u, 0u, 0u);
-        if (act) q = *reinterpret_cast<const uint4*>(u16 + static_cast<int64_t>(b) * K + k0 + 8 * m);
-        uP[j][b][4 * m + 0] = q.x;
-        uP[j][b][4 * m + 1] = q.y;
-        uP[j][b][4 * m + 2] = q.z;
-        uP[j][b][4 * m + 3] = q.w;
-      }
-      if (act) Us[b] += usum[b * NCH + (k0 >> 5)];
+  // ------------------------------------------------------------ phase 2: GEMV on mma.sync
+  float* pw = part + static_cast<size_t>(warp) * a.R_max * 16 * B;
+  for (int i = lane; i < n_rho * 16 * B; i += 32) pw[i] = 0.f;
+  __syncwarp();
+  const int gq = lane >> 2, t = lane & 3;
+  const uint32_t u_a = smem_u32(ufr), xs_a = smem_u32(xsum), ring_a = smem_u32(ring);
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  int cur = -1;
+  auto flush = [&]() {
+    float* pr = pw + cur * 16 * B;
+    if (2 * t < B) {
+      pr[gq * B + 2 * t] = acc[0];
+      pr[(gq + 8) * B + 2 * t] = acc[2];
     }
-  }
-  // inactive lanes (K not a multiple of 512*J) read a valid chunk and contribute 0 (u' = 0)
-  const int kb = act ? kbase : 0;
-  const int gam = kb >> 7;
-  const uint32_t code_off = static_cast<uint32_t>(kb >> 1);
-  const int zsh = (gam & 1) * 4;
-
-  // stage slots as 32-bit shared addresses (no generic->shared conversion in the loop)
-  const uint32_t ring_a = smem_u32(ring);
-  // row group rg owns slots rg, rg + RG, ... so every slot is consumed by one row group
-  // in order (mbarrier parity waits can only look one phase ahead)
-  const int SP = a.S / RGN;
-  for (int st = rg; st < n_stages; st += RGN) {
-    const int use = st / RGN;
-    const int slot = rg + RGN * (use % SP);
-    const uint32_t phase = (use / SP) & 1;
-    if (st == n_stages - 1 && threadIdx.x == 0) PARO_TL(a, 10);  // consumer reached the last stage
-    mbar_wait(&full[slot], phase);
+    if (2 * t + 1 < B) {
+      pr[gq * B + 2 * t + 1] = acc[1];
+      pr[(gq + 8) * B + 2 * t + 1] = acc[3];
+    }
+  };
+  for (int st = 0; st < n_stages; ++st) {
+    const int slot = st % a.S;
+    if (st == n_stages - 1 && threadIdx.x == 0) PARO_TL(a, 10);
+    mbar_wait(&full[slot], (st / a.S) & 1);
     if (st == 0 && threadIdx.x == 0) PARO_TL(a, 3);
-    if (st == n_stages - 1 && threadIdx.x == 0) PARO_TL(a, 11);  // last stage's bytes landed
+    if (st == n_stages - 1 && threadIdx.x == 0) PARO_TL(a, 11);
     const uint32_t sbase = ring_a + static_cast<uint32_t>(slot) * a.slot_bytes;
-    const int r0 = row_begin + st * SR;
-    const int nr = min(SR, n_rows - st * SR);
-    const uint32_t s_lo = static_cast<uint32_t>((static_cast<int64_t>(r0) * 2 * G) & ~int64_t(15));
-    const uint32_t z_lo = static_cast<uint32_t>((static_cast<int64_t>(r0) * ZB) & ~int64_t(15));
-    // this lane's row lr = 2i + h: scale, zero and codes addresses (all rows of the slot
-    // exist in shared memory; rows past nr hold stale bytes -- computed, never stored)
-    const uint32_t sc_a = sbase + a.sc_off + static_cast<uint32_t>(r0 * 2 * G) - s_lo + 2 * gam + h * 2 * G;
-    const uint32_t z_a = sbase + a.z_off + static_cast<uint32_t>(r0 * ZB) - z_lo + (gam >> 1) + h * ZB;
-    const uint32_t c_a = sbase + code_off + h * (K / 2);
-    float racc[RP][BT];
-#pragma unroll
-    for (int i = 0; i < RP; ++i) {
-      const uint32_t row_off = 2 * i;
-      uint4 c[J];
-#pragma unroll
-      for (int j = 0; j < J; ++j) c[j] = lds128_a(c_a + row_off * (K / 2) + 16 * ((j + hl) & (J - 1)));
-      const float S = __half2float(__ushort_as_half(lds_u16_a(sc_a + row_off * 2 * G)));
-      const float zf = static_cast<float>((lds_u8_a(z_a + row_off * ZB) >> zsh) & 15u);
-#pragma unroll
-      for (int b = 0; b < BT; ++b) {
-        float tl = 0.f, th = 0.f;  // 2^-24 sum q x' over the lane's 32*J codes
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-          dot_word(c[j].x, &uP[j][b][0], tl, th);
-          dot_word(c[j].y, &uP[j][b][4], tl, th);
-          dot_word(c[j].z, &uP[j][b][8], tl, th);
-          dot_word(c[j].w, &uP[j][b][12], tl, th);
-        }
-        const float dot = fmaf(0.0625f, th, tl);
-        racc[i][b] = S * fmaf(-zf, Us[b], dot);
+    const int nts = min(TPS, n_my - st * TPS);
+    for (int i = warp; i < nts; i += NW) {
+      const int tl = tA + st * TPS + i;
+      const int rb = tl / G;
+      const int g = tl - rb * G;
+      if (rb - rho_first != cur) {
+        if (cur >= 0) flush();
+        acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+        cur = rb - rho_first;
       }
+      const uint32_t ca = sbase + static_cast<uint32_t>(i) * TILE_CODE_BYTES + lane * 16;
+      const uint4 wa = lds128_a(ca);        // row gq, quad t: words j = 0..3
+      const uint4 wb = lds128_a(ca + 512);  // row gq + 8
+      uint32_t bf[16];
+      if (gq < B) {
+        const uint32_t xa = u_a + static_cast<uint32_t>(((g * 4) * B + gq) * 64 + t * 16);
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+          const uint4 v = lds128_a(xa + ii * B * 64);
+          bf[4 * ii + 0] = v.x;
+          bf[4 * ii + 1] = v.y;
+          bf[4 * ii + 2] = v.z;
+          bf[4 * ii + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) bf[q] = 0u;
+      }
+      const uint32_t w0[4] = {wa.x, wa.y, wa.z, wa.w};
+      const uint32_t w1[4] = {wb.x, wb.y, wb.z, wb.w};
+      float D1[4], D16[4];  // 2^-24 sum q x' (low nibbles), 2^-20 sum q x' (high nibbles)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t x = w0[j], y = w1[j], x8 = x >> 8, y8 = y >> 8;
+        if (j == 0) {
+          mma_16816_z(D1, x & 0x000F000Fu, y & 0x000F000Fu, x8 & 0x000F000Fu, y8 & 0x000F000Fu, bf[0], bf[1]);
+          mma_16816_z(D16, x & 0x00F000F0u, y & 0x00F000F0u, x8 & 0x00F000F0u, y8 & 0x00F000F0u, bf[2], bf[3]);
+        } else {
+          mma_16816(D1, x & 0x000F000Fu, y & 0x000F000Fu, x8 & 0x000F000Fu, y8 & 0x000F000Fu, bf[4 * j], bf[4 * j + 1]);
+          mma_16816(D16, x & 0x00F000F0u, y & 0x00F000F0u, x8 & 0x00F000F0u, y8 & 0x00F000F0u, bf[4 * j + 2],
+                    bf[4 * j + 3]);
+        }
+      }
+      // epilogue of the tile (a6): y += S * (2^24 * (D1 + D16 / 16) - z * sum x')
+      const uint32_t sp = lds_u32_a(sbase + a.sc_off + static_cast<uint32_t>(i) * TILE_SCALE_BYTES + gq * 4);
+      const uint32_t zb = lds_u8_a(sbase + a.z_off + static_cast<uint32_t>(i) * TILE_ZERO_BYTES + gq);
+      const float2 S2 = __half22float2(*reinterpret_cast<const __half2*>(&sp));
+      const float z0 = static_cast<float>(zb & 15u), z1 = static_cast<float>(zb >> 4);
+      const float2 X2 = lds_f2_a(xs_a + static_cast<uint32_t>((g * 8 + 2 * t) * 4));
+      acc[0] = fmaf(S2.x, fmaf(fmaf(D16[0], 0.0625f, D1[0]), TWO_P24, -z0 * X2.x), acc[0]);
+      acc[1] = fmaf(S2.x, fmaf(fmaf(D16[1], 0.0625f, D1[1]), TWO_P24, -z0 * X2.y), acc[1]);
+      acc[2] = fmaf(S2.y, fmaf(fmaf(D16[2], 0.0625f, D1[2]), TWO_P24, -z1 * X2.x), acc[2]);
+      acc[3] = fmaf(S2.y, fmaf(fmaf(D16[3], 0.0625f, D1[3]), TWO_P24, -z1 * X2.y), acc[3]);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);  // codes of this stage consumed
-    // transpose-reduce the RP row-pair slots across the 16 lanes of each half-warp
-#pragma unroll
-    for (int b = 0; b < BT; ++b) {
-      float v[RP];
-#pragma unroll
-      for (int i = 0; i < RP; ++i) v[i] = racc[i][b];
-      int si = 0;
-#pragma unroll
-      for (int off = 8, n = RP; off >= 1; off >>= 1) {
-        const bool up = hl & off;
-        if (n > 1) {
-          const int hn = n / 2;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            if (i < hn) {
-              const float keep = up ? v[i + hn] : v[i];
-              const float send = up ? v[i] : v[i + hn];
-              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-            }
-          }
-          si = 2 * si + (up ? 1 : 0);
-          n = hn;
-        } else {
-          v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
-        }
-      }
-      // lanes whose unused low bits are 0 hold slot si (0 <= si < RP)
-      const int lr = 2 * si + h;
-      const bool writer = (hl & (16 / RP - 1)) == 0;
-      if (writer && lr < nr) part[(static_cast<size_t>(wk) * a.rows_max + st * SR + lr) * BT + b] = v[0];
-    }
+    if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the stage
   }
+  if (cur >= 0) flush();
   if (threadIdx.x == 0) PARO_TL(a, 4);
   if (a.pdl) pdl_wait();  // y may still be read by the previous kernel (no-op once it has finished)
 
-  // ------------------------------------------------------------ cross-warp reduction + epilogue (a8)
-  named_bar_sync(1, n_compute_warps * 32);
-  for (int idx = threadIdx.x; idx < n_rows * BT; idx += n_compute_warps * 32) {
-    const int row = idx / BT, b = idx % BT;
-    if (b >= a.B) continue;
+  // ------------------------------------------------------------ reduction + epilogue (a8)
+  named_bar_sync(1, NW * 32);
+  const int n_out = n_rho * 16 * B;
+  for (int idx = threadIdx.x; idx < n_out; idx += NW * 32) {
+    const int rho = idx / (16 * B), r = (idx / B) % 16, b = idx % B;
     float sum = 0.f;
-    for (int w = 0; w < WK; ++w) sum += part[(static_cast<size_t>(w) * a.rows_max + row) * BT + b];
-    const int64_t n = static_cast<int64_t>(row_begin) + row;
-    float v = sum * TWO_P24;
-    if (d.bias) v += __ldg(d.bias + n);
-    store_out(d.y, a.y_dtype, static_cast<int64_t>(b) * d.N + n, v);
+    for (int w = 0; w < NW; ++w) sum += part[((static_cast<size_t>(w) * a.R_max + rho) * 16 + r) * B + b];
+    const int rg = rho_first + rho;
+    if (rho == 0 && !own_first) {
+      // the block started in an earlier CTA: push this partial to it (recv slot crank - owner - 1)
+      const int owner = cta_of_tile(rg * G, nt, CL);
+      const uint32_t dst =
+          smem_u32(recv) + static_cast<uint32_t>((((crank - owner - 1) * 16 + r) * B + b) * 4);
+      st_async_b32(mapa(dst, owner), __float_as_uint(sum), mapa(smem_u32(rbar), owner));
+    } else if (rho == n_rho - 1 && last_cta > crank) {
+      part[(static_cast<size_t>(rho) * 16 + r) * B + b] = sum;  // warp-0 slot of this element
+    } else {
+      const int64_t n = static_cast<int64_t>(rbc0 + rg) * 16 + r;
+      if (n < d.N) {
+        float v = sum;
+        if (d.bias) v += __ldg(d.bias + n);
+        store_out(d.y, a.y_dtype, static_cast<int64_t>(b) * d.N + n, v);
+      }
+    }
+  }
+  if (last_cta > crank) {
+    named_bar_sync(1, NW * 32);
+    mbar_wait(rbar, 0);
+    const int rho = n_rho - 1, rg = rho_first + rho;
+    for (int idx = threadIdx.x; idx < 16 * B; idx += NW * 32) {
+      const int r = idx / B, b = idx % B;
+      float sum = part[(static_cast<size_t>(rho) * 16 + r) * B + b];
+      for (int c = crank + 1; c <= last_cta; ++c)  // fixed order
+        if (cta_tile_start(c + 1, nt, CL) > cta_tile_start(c, nt, CL)) sum += recv[((c - crank - 1) * 16 + r) * B + b];
+      const int64_t n = static_cast<int64_t>(rbc0 + rg) * 16 + r;
+      if (n < d.N) {
+        float v = sum;
+        if (d.bias) v += __ldg(d.bias + n);
+        store_out(d.y, a.y_dtype, static_cast<int64_t>(b) * d.N + n, v);
+      }
+    }
   }
   if (threadIdx.x == 0) PARO_TL(a, 5);
 }
@@ -536,26 +515,15 @@ static int smem_optin() {
 
 static inline uint32_t align_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
-
-static const void* kernel_for(int BT, int J, int big) {
-#define PARO_K(BT_, J_, T_) \
-  if (BT == BT_ && J == J_ && (big ? 544 : 288) == T_) return reinterpret_cast<const void*>(&paro_gemv_kernel<BT_, J_, T_>);
-  PARO_K(1, 1, 288)
-  PARO_K(1, 2, 288)
-  PARO_K(1, 4, 288)
-  PARO_K(2, 1, 288)
-  PARO_K(2, 2, 288)
-  PARO_K(4, 1, 288)
-  PARO_K(1, 1, 544)
-  PARO_K(1, 2, 544)
-  PARO_K(1, 4, 544)
-#undef PARO_K
+static const void* kernel_for(int threads) {
+  if (threads <= 288) return reinterpret_cast<const void*>(&paro_gemv_kernel<288>);
+  if (threads <= 544) return reinterpret_cast<const void*>(&paro_gemv_kernel<544>);
   return nullptr;
 }
 
 // Co-resident CTAs for this launch shape (whole clusters), from the occupancy API.
-static int max_resident_ctas(int BT, int J, int threads, int smem, int CL) {
-  const void* k = kernel_for(BT, J, threads > 288);
+static int max_resident_ctas(int threads, int smem, int CL) {
+  const void* k = kernel_for(threads);
   if (!k) return 0;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
     cudaGetLastError();
@@ -588,131 +556,118 @@ static int max_resident_ctas(int BT, int J, int threads, int smem, int CL) {
   return per_sm * device_sm_count();
 }
 
-bool plan_gemv(int B_tile, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, int rotate, GemvConfig* cfg,
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, int rotate, GemvConfig* cfg,
                const char** why) {
   GemvConfig c{};
   if (n_lin < 1 || n_lin > GEMV_MAX_LIN) {
     *why = "1..4 linears per decode launch";
     return false;
   }
-  int64_t N = 0;
-  int L = 0;
-  for (int i = 0; i < n_lin; ++i) {
-    N += Ns[i];
-    L = std::max(L, Ls[i]);
-  }
-  c.BT = B_tile <= 1 ? 1 : B_tile <= 2 ? 2 : 4;
-  const int G = static_cast<int>(K / GRP);
-  // J: contiguous 32-K chunks per lane per row (all in one 128-group).  Smallest J that
-  // keeps the K slices within 8 warps with <= 6% idle lanes (u' registers: BT * J <= 4);
-  // very large K uses up to 16 warps (J = 4).
-  int J = 0;
-  for (int cand = 1; cand <= 4 && !J; cand *= 2) {
-    if (c.BT * cand > 4) break;
-    const int64_t span = 512 * cand;
-    const int64_t wk = (K + span - 1) / span;
-    if (wk <= 8 && (wk * span * 100 <= K * 106 || cand == 4 || K <= span)) J = cand;
-  }
-  if (!J) J = (c.BT == 1) ? 4 : (c.BT == 2 ? 2 : 1);
-  const int WK = static_cast<int>((K + 512 * J - 1) / (512 * J));
-  if (WK > 16 || (WK > 8 && c.BT > 1)) {
-    *why = "K too large for the decode kernel at this token tile";
+  if (B < 1 || B > GEMV_MAX_B) {
+    *why = "decode launches take 1..8 tokens";
     return false;
   }
-  // row groups (stage-interleaved): fill up to 8 compute warps per CTA with 2 CTAs/SM,
-  // or 16 with 1 CTA/SM
-  int ctas_per_sm_pref = 2;
-  if (const char* e = getenv("PARO_CTAS_PER_SM")) ctas_per_sm_pref = atoi(e) == 1 ? 1 : 2;
-  const int warp_cap = (ctas_per_sm_pref == 1 && c.BT == 1) ? 16 : 8;  // 544-thread variants are BT = 1
-  int RG = 1;
-  while (RG < 4 && WK * RG * 2 <= warp_cap) RG *= 2;
-  if (const char* e = getenv("PARO_RG")) RG = std::max(1, std::min(4, atoi(e)));
-  if (WK * RG > 16) RG = 1;
-  c.J = J;
-  const int sms = device_sm_count();
-  const int threads = (WK * RG + 1) * 32;
-  // cluster size: share the transform across CTAs (each CTA rotates G/CL groups)
-  // (the rotation-off baseline uses the same split, so it differs only by the rotation)
-  int CL = 8;
-  if (const char* e = getenv("PARO_CLUSTER")) CL = atoi(e);
+  int64_t NBsum = 0;
+  int L = 0;
+  int64_t NB[GEMV_MAX_LIN];
+  for (int i = 0; i < n_lin; ++i) {
+    NB[i] = (Ns[i] + TILE_ROWS - 1) / TILE_ROWS;
+    NBsum += NB[i];
+    L = std::max(L, Ls[i]);
+  }
+  const int G = static_cast<int>(K / GRP);
+  // 8 compute warps with 2 CTAs / SM by default; PARO_NW / PARO_CTAS_PER_SM / PARO_CLUSTER /
+  // PARO_TPS override for tuning
+  int NW = std::max(1, std::min(16, env_int("PARO_NW", 8)));
+  int ctas_per_sm = env_int("PARO_CTAS_PER_SM", NW <= 8 ? 2 : 1) == 1 ? 1 : 2;
+  if (NW > 8) ctas_per_sm = 1;
+  int CL = env_int("PARO_CLUSTER", 8);
   if (CL != 1 && CL != 2 && CL != 4 && CL != 8) CL = 8;
   while (CL > 1 && CL > G) CL /= 2;
+  const int TPS = std::max(1, std::min(64, env_int("PARO_TPS", 2 * NW)));
+  c.NW = NW;
   c.CL = CL;
   GemvArgs& a = c.a;
   a.n_lin = n_lin;
+  a.B = B;
   a.K = static_cast<int>(K);
   a.G = G;
   a.rotate = rotate;
-  a.WK = WK;
-  a.RG = RG;
-  const int row_bytes = static_cast<int>(K / 2);
-  // rows per stage: 2 * RP_PER_STAGE / J (16 rows of <= 2 KB, 4 rows of <= 8 KB, ...)
-  const int SR = 2 * RP_PER_STAGE / J;
-  a.SR = SR;
-  const int ZB = (G + 1) / 2;
-  a.sc_off = align_up(static_cast<uint32_t>(SR) * row_bytes, 128);
-  a.z_off = a.sc_off + align_up(static_cast<uint32_t>(SR) * 2 * G + 32, 128);
-  a.slot_bytes = a.z_off + align_up(static_cast<uint32_t>(SR) * ZB + 32, 128);
-  const uint32_t u_bytes = align_up(static_cast<uint32_t>(c.BT) * K * 2, 128);
-  const uint32_t usum_bytes = align_up(static_cast<uint32_t>(c.BT) * (K / 32) * 4, 128);
+  a.NW = NW;
+  a.TPS = TPS;
+  a.sc_off = static_cast<uint32_t>(TPS) * TILE_CODE_BYTES;
+  a.z_off = a.sc_off + static_cast<uint32_t>(TPS) * TILE_SCALE_BYTES;
+  a.slot_bytes = align_up(a.z_off + static_cast<uint32_t>(TPS) * TILE_ZERO_BYTES, 128);
+  const int threads = (NW + 1) * 32;
+  const uint32_t u_bytes = align_up(static_cast<uint32_t>(B) * K * 2, 128);
+  const uint32_t xs_bytes = align_up(static_cast<uint32_t>(G) * 8 * 4, 128);
   const int g_per = (G + CL - 1) / CL;
-  const uint32_t x_bytes = align_up(static_cast<uint32_t>(c.BT) * g_per * GRP * 2, 128);
-  const uint32_t scr_bytes = align_up(static_cast<uint32_t>(WK * RG) * c.BT * 132 * 4, 128);
-  // two CTAs per SM when the activation buffer is small (lets the next kernel's weight
-  // prefetch start while this one drains, and doubles the warps hiding latency)
-  int ctas_per_sm = (u_bytes <= 40 * 1024) ? ctas_per_sm_pref : 1;
-  const int budget = (smem_optin() + 1024) / ctas_per_sm - 2048;
-  // split the grid's clusters over the linears in proportion to their rows (>= 1 each)
+  const uint32_t x_bytes = align_up(static_cast<uint32_t>(B) * g_per * GRP * 2, 128);
+  const uint32_t scr_bytes = align_up(static_cast<uint32_t>(NW) * B * 132 * 4, 128);
+  const uint32_t recv_bytes = align_up(static_cast<uint32_t>(std::max(1, CL - 1)) * 16 * B * 4, 128);
+  if (u_bytes > 64 * 1024) ctas_per_sm = 1;
+  int budget = (smem_optin() + 1024) / ctas_per_sm - 2048;
+  int max_tiles_cta = 0;
+  // split the grid's clusters over the linears in proportion to their row blocks (>= 1 each,
+  // never more clusters than row blocks)
   auto split = [&](int grid) -> bool {
-    const int ncl = grid / CL;
+    int ncl = grid / CL;
     if (ncl < n_lin) return false;
+    if (ncl > NBsum) ncl = static_cast<int>(NBsum);
     int cl[GEMV_MAX_LIN], used = 0, big = 0;
     for (int i = 0; i < n_lin; ++i) {
-      cl[i] = std::max<int>(1, static_cast<int>(static_cast<double>(ncl) * Ns[i] / N));
+      cl[i] = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(NB[i], ncl * NB[i] / NBsum)));
       used += cl[i];
-      if (Ns[i] > Ns[big]) big = i;
+      if (NB[i] > NB[big]) big = i;
     }
-    cl[big] += ncl - used;
-    if (cl[big] < 1) return false;
+    cl[big] = static_cast<int>(std::min<int64_t>(NB[big], cl[big] + std::max(0, ncl - used)));
     int begin = 0;
-    a.rows_max = 0;
+    max_tiles_cta = 0;
     for (int i = 0; i < n_lin; ++i) {
       GemvLinear& d = a.lin[i];
       d.N = static_cast<int>(Ns[i]);
       d.L = Ls[i];
       d.cta_begin = begin;
       d.n_ctas = cl[i] * CL;
-      if (d.n_ctas > Ns[i]) return false;  // at least one row per CTA
-      d.rows_base = static_cast<int>(Ns[i] / d.n_ctas);
-      d.rows_extra = static_cast<int>(Ns[i] % d.n_ctas);
-      a.rows_max = std::max(a.rows_max, d.rows_base + (d.rows_extra ? 1 : 0));
+      d.rb_base = static_cast<int>(NB[i] / cl[i]);
+      d.rb_extra = static_cast<int>(NB[i] % cl[i]);
+      const int nt_max = (d.rb_base + (d.rb_extra ? 1 : 0)) * G;
+      max_tiles_cta = std::max(max_tiles_cta, (nt_max + CL - 1) / CL);
       begin += d.n_ctas;
     }
+    c.grid = begin;
     return true;
   };
   auto layout = [&](int grid) -> bool {
     if (!split(grid)) return false;
+    a.R_max = (max_tiles_cta + G - 1) / G + 1;
     uint32_t off = 0;
     a.off_u = off;
     off += u_bytes;
-    a.off_usum = off;
-    off += usum_bytes;
+    a.off_xs = off;
+    off += xs_bytes;
     a.off_x = off;
     off += x_bytes;
     a.off_scr = off;
     off += scr_bytes;
     a.off_part = off;
-    off += align_up(static_cast<uint32_t>(WK) * a.rows_max * c.BT * 4, 128);
+    off += align_up(static_cast<uint32_t>(NW) * a.R_max * 16 * B * 4, 128);
+    a.off_recv = off;
+    off += recv_bytes;
     a.off_bar = off;
-    off += 64 * 16;  // up to 60 stages x (full, empty) + 4 singles
+    off += 64 * 16;  // up to 60 stages x (full, empty) + 6 singles
     a.off_ring = align_up(off, 1024);
     const int64_t ring_avail = static_cast<int64_t>(budget) - a.off_ring;
     int S = static_cast<int>(ring_avail / a.slot_bytes);
-    const int stages_needed = std::max((a.rows_max + SR - 1) / SR, RG);
+    const int stages_needed = std::max(1, (max_tiles_cta + TPS - 1) / TPS);
     if (S > stages_needed) S = stages_needed;
     if (S > 60) S = 60;
-    S -= S % RG;  // each row group owns S / RG slots
-    if (S < RG) return false;
+    if (S < 1) return false;
     a.S = S;
     a.smem_total = a.off_ring + static_cast<uint32_t>(S) * a.slot_bytes;
     // stage the rotation parameters of this CTA's groups in shared memory: a dedicated
@@ -732,21 +687,23 @@ bool plan_gemv(int B_tile, int n_lin, const int64_t* Ns, const int* Ls, int64_t 
     }
     return true;
   };
-  int64_t max_ctas = 0;  // at least one row pair per CTA
-  for (int i = 0; i < n_lin; ++i) max_ctas += std::max<int64_t>(CL, (Ns[i] + 1) / 2 / CL * CL);
-  int grid = sms * ctas_per_sm;
+  int grid = device_sm_count() * ctas_per_sm / CL * CL;
+  if (grid < CL * n_lin) grid = CL * n_lin;
+  if (!layout(grid) && ctas_per_sm == 2) {  // too big for two CTAs per SM: one, with the full budget
+    ctas_per_sm = 1;
+    budget = smem_optin() - 1024;
+    grid = std::max(CL * n_lin, device_sm_count() / CL * CL);
+  }
   for (int iter = 0; iter < 3; ++iter) {
-    grid = static_cast<int>(std::min<int64_t>(grid, max_ctas)) / CL * CL;
     if (grid < CL * n_lin) grid = CL * n_lin;
     if (!layout(grid)) {
       *why = "decode kernel shared-memory plan does not fit";
       return false;
     }
-    const int resident = max_resident_ctas(c.BT, J, threads, static_cast<int>(a.smem_total), CL);
-    if (resident <= 0 || resident >= grid) break;
-    grid = resident;  // never launch more than one wave
+    const int resident = max_resident_ctas(threads, static_cast<int>(a.smem_total), CL);
+    if (resident <= 0 || resident >= c.grid) break;
+    grid = resident / CL * CL;  // never launch more than one wave
   }
-  c.grid = grid;
   if (!layout(grid)) {
     *why = "decode kernel shared-memory plan does not fit";
     return false;
@@ -755,9 +712,9 @@ bool plan_gemv(int B_tile, int n_lin, const int64_t* Ns, const int* Ls, int64_t 
   return true;
 }
 
-template <int BT, int J, int T>
+template <int T>
 static cudaError_t launch_t(const GemvConfig& c, cudaStream_t st) {
-  auto kern = paro_gemv_kernel<BT, J, T>;
+  auto kern = paro_gemv_kernel<T>;
   static int configured_smem = 0;  // per instantiation
   if (static_cast<int>(c.a.smem_total) > configured_smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -767,7 +724,7 @@ static cudaError_t launch_t(const GemvConfig& c, cudaStream_t st) {
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(c.grid);
-  cfg.blockDim = dim3((c.a.WK * c.a.RG + 1) * 32);
+  cfg.blockDim = dim3((c.NW + 1) * 32);
   cfg.dynamicSmemBytes = c.a.smem_total;
   cfg.stream = st;
   cudaLaunchAttribute attrs[2];
@@ -790,19 +747,9 @@ static cudaError_t launch_t(const GemvConfig& c, cudaStream_t st) {
 }
 
 cudaError_t launch_gemv(const GemvConfig& c, cudaStream_t st) {
-  const bool big = (c.a.WK * c.a.RG + 1) * 32 > 288;
-#define PARO_GEMV_CASE(BT_, J_, T_) \
-  if (c.BT == BT_ && c.J == J_ && (big ? 544 : 288) == T_) return launch_t<BT_, J_, T_>(c, st);
-  PARO_GEMV_CASE(1, 1, 288)
-  PARO_GEMV_CASE(1, 2, 288)
-  PARO_GEMV_CASE(1, 4, 288)
-  PARO_GEMV_CASE(2, 1, 288)
-  PARO_GEMV_CASE(2, 2, 288)
-  PARO_GEMV_CASE(4, 1, 288)
-  PARO_GEMV_CASE(1, 1, 544)
-  PARO_GEMV_CASE(1, 2, 544)
-  PARO_GEMV_CASE(1, 4, 544)
-#undef PARO_GEMV_CASE
+  const int threads = (c.NW + 1) * 32;
+  if (threads <= 288) return launch_t<288>(c, st);
+  if (threads <= 544) return launch_t<544>(c, st);
   return cudaErrorInvalidConfiguration;
 }
 

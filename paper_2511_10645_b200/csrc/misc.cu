@@ -4,6 +4,7 @@
 
 #include "paro_internal.h"
 #include "ptx.cuh"
+#include "tile_layout.cuh"
 
 namespace paro {
 
@@ -19,7 +20,7 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
                                                         int L, const float* __restrict__ svec,
                                                         const float2* __restrict__ rot_cs,
                                                         const uchar2* __restrict__ rot_idx, int rotate,
-                                                        __half* __restrict__ xo, int pdl, int perm8) {
+                                                        __half* __restrict__ xo, int pdl, int prefill_order) {
   __shared__ float scr_all[8][132];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* scr = scr_all[warp];
@@ -70,13 +71,13 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
       scr[j1] = csr[t].w * a1 + csr[t].z * c1;
       __syncwarp();
     }
-    // natural order: lane writes channels 4l..4l+3.  perm8 (prefill operand order): each
-    // 8-channel block stored as (0,4,1,5,2,6,3,7); lane writes half (l&1) of block l/2.
-    const int b8 = (lane >> 1) * 8, hh = lane & 1;
-    const int c0 = perm8 ? b8 + 2 * hh : 4 * lane;
-    const int d = perm8 ? 4 : 1;
-    const __half2 h01 = __floats2half2_rn(scr[c0], scr[c0 + d]);
-    const __half2 h23 = __floats2half2_rn(scr[c0 + (perm8 ? 1 : 2)], scr[c0 + (perm8 ? 5 : 3)]);
+    // natural order: lane writes channels 4l..4l+3.  prefill_order: position p of the group
+    // holds channel prefill_channel(p) (the order the prefill dequantiser emits weights in)
+    float v4[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v4[e] = scr[prefill_order ? prefill_channel(4 * lane + e) : 4 * lane + e];
+    const __half2 h01 = __floats2half2_rn(v4[0], v4[1]);
+    const __half2 h23 = __floats2half2_rn(v4[2], v4[3]);
     uint2 pk;
     pk.x = *reinterpret_cast<const uint32_t*>(&h01);
     pk.y = *reinterpret_cast<const uint32_t*>(&h23);
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
 
 cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, int L, const float* svec,
                              const float2* rot_cs, const uchar2* rot_idx, int rotate, void* x_out, int pdl,
-                             int perm8, cudaStream_t st) {
+                             int prefill_order, cudaStream_t st) {
   const int64_t G = K / TGRP;
   const int64_t items = ((B + TOK_PER_WARP - 1) / TOK_PER_WARP) * G;
   const int64_t blocks = (items + 7) / 8;
@@ -104,7 +105,7 @@ cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, in
     cfg.numAttrs = 1;
   }
   return cudaLaunchKernelEx(&cfg, transform_kernel, x, x_bf16, B, K, L, svec, rot_cs, rot_idx, rotate,
-                            static_cast<__half*>(x_out), pdl, perm8);
+                            static_cast<__half*>(x_out), pdl, prefill_order);
 }
 
 // On-the-fly preparation of (cos, sin, i, j) from device theta / pairs (no validation).
@@ -141,27 +142,34 @@ cudaError_t launch_prepare_transform(const float* theta, const int16_t* pairs, i
   return cudaGetLastError();
 }
 
-__global__ void unpack_kernel(const uint8_t* __restrict__ codes, const uint8_t* __restrict__ zeros, int64_t N,
-                              int64_t K, uint8_t* __restrict__ cu8, uint8_t* __restrict__ zu8) {
-  const int64_t G = K / TGRP, ZB = (G + 1) / 2;
-  const int64_t tot = N * (K / 2);
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < tot;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const uint8_t b = codes[i];
-    cu8[2 * i] = b & 15;
-    cu8[2 * i + 1] = b >> 4;
+// tile layout -> logical codes [N][K], scales [N][G] (fp16), zeros [N][G]
+__global__ void unpack_kernel(const uint8_t* __restrict__ codes, const __half* __restrict__ scales,
+                              const uint8_t* __restrict__ zeros, int64_t N, int64_t K, uint8_t* __restrict__ cu8,
+                              __half* __restrict__ sf16, uint8_t* __restrict__ zu8) {
+  const int64_t G = K / TGRP;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < N * K; i += stride) {
+    const int64_t n = i / K, k = i % K;
+    const int64_t T = (n / TILE_ROWS) * G + k / TGRP;
+    int byte, hi;
+    tile_pos(static_cast<int>(k % TGRP), &byte, &hi);
+    const uint8_t b = codes[T * TILE_CODE_BYTES + (n % TILE_ROWS) * 64 + byte];
+    cu8[i] = hi ? (b >> 4) : (b & 15);
   }
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < N * G;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < N * G; i += stride) {
     const int64_t n = i / G, g = i % G;
-    const uint8_t b = zeros[n * ZB + g / 2];
-    zu8[i] = (g & 1) ? (b >> 4) : (b & 15);
+    const int64_t T = (n / TILE_ROWS) * G + g;
+    const int r = static_cast<int>(n % TILE_ROWS);
+    sf16[i] = scales[T * 16 + tile_scale_idx(r)];
+    const uint8_t b = zeros[T * TILE_ZERO_BYTES + (r & 7)];
+    zu8[i] = (r >> 3) ? (b >> 4) : (b & 15);
   }
 }
 
-cudaError_t launch_unpack(const uint8_t* codes, const uint8_t* zeros, int64_t N, int64_t K, uint8_t* codes_u8,
-                          uint8_t* zeros_u8, cudaStream_t st) {
-  unpack_kernel<<<1024, 256, 0, st>>>(codes, zeros, N, K, codes_u8, zeros_u8);
+cudaError_t launch_unpack(const uint8_t* codes, const uint8_t* scales, const uint8_t* zeros, int64_t N, int64_t K,
+                          uint8_t* codes_u8, uint8_t* scales_f16, uint8_t* zeros_u8, cudaStream_t st) {
+  unpack_kernel<<<1024, 256, 0, st>>>(codes, reinterpret_cast<const __half*>(scales), zeros, N, K, codes_u8,
+                                      reinterpret_cast<__half*>(scales_f16), zeros_u8);
   return cudaGetLastError();
 }
 

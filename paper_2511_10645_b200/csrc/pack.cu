@@ -5,12 +5,14 @@
 // is compiled with -fmad=false, so every product and sum is rounded separately
 // (Q7) -- required for bit-exact codes/scales/zeros.
 //
-// Mapping: one CTA = PACK_ROWS weight rows, looping over the K/128 groups.
+// Mapping: one CTA = PACK_ROWS weight rows, looping over the K/128 groups; results are
+// written in the tile layout of tile_layout.cuh.
 // Thread (r, p), p in [0, 64): holds slot p of the current rotation for row r.
 #include <cstdint>
 #include <cuda_fp16.h>
 
 #include "paro_internal.h"
+#include "tile_layout.cuh"
 
 namespace paro {
 
@@ -39,7 +41,7 @@ __global__ void __launch_bounds__(PACK_ROWS * 64) pack_fold_rtn_kernel(
   __shared__ double Ssh[PACK_ROWS];
   __shared__ double zsh[PACK_ROWS];
   __shared__ uint8_t qsh[PACK_ROWS][G_];
-  extern __shared__ uint8_t zbuf[];  // [PACK_ROWS][G]
+  const int r16 = static_cast<int>(row % TILE_ROWS);
 
   int bad = 0;
   for (int gam = 0; gam < G; ++gam) {
@@ -90,9 +92,12 @@ __global__ void __launch_bounds__(PACK_ROWS * 64) pack_fold_rtn_kernel(
       z = fmin(fmax(z, 0.0), 15.0);              // clamp to [0, 2^b - 1] (Q11)
       Ssh[r] = S;
       zsh[r] = z;
-      if (live) {
-        scales[row * G + gam] = __ushort_as_half(hb);
-        zbuf[r * G + gam] = static_cast<uint8_t>(z);
+      if (live) {  // tile layout (tile_layout.cuh); buffers were zeroed before the launch
+        const int64_t T = (row / TILE_ROWS) * G + gam;
+        scales[T * 16 + tile_scale_idx(r16)] = __ushort_as_half(hb);
+        const int64_t zbyte = T * TILE_ZERO_BYTES + (r16 & 7);
+        atomicOr(reinterpret_cast<unsigned int*>(zeros + (zbyte & ~int64_t(3))),
+                 static_cast<unsigned int>(z) << (8 * (zbyte & 3) + 4 * (r16 >> 3)));
       }
     }
     __syncthreads();
@@ -107,20 +112,14 @@ __global__ void __launch_bounds__(PACK_ROWS * 64) pack_fold_rtn_kernel(
     }
     __syncthreads();
     if (live) {
-      // byte p of this group's 64 code bytes: k = 2p (low nibble), 2p+1 (high nibble)
-      const uint8_t b = static_cast<uint8_t>(qsh[r][2 * p] | (qsh[r][2 * p + 1] << 4));
-      codes[row * (K / 2) + static_cast<int64_t>(gam) * 64 + p] = b;
+      // byte p of the row's 64 code bytes in its tile: quad p / 16, word (p / 4) % 4,
+      // nibbles 2 (p % 4) (low) and 2 (p % 4) + 1 (high) -> channels tile_k(...)
+      const int tq = p >> 4, wj = (p >> 2) & 3, bw = p & 3;
+      const uint8_t b = static_cast<uint8_t>(qsh[r][tile_k(tq, wj, 2 * bw)] | (qsh[r][tile_k(tq, wj, 2 * bw + 1)] << 4));
+      const int64_t T = (row / TILE_ROWS) * G + gam;
+      codes[T * TILE_CODE_BYTES + r16 * 64 + p] = b;
     }
     __syncthreads();
-  }
-  // nibble-pack the zero points of this row: byte j holds groups 2j (low), 2j+1 (high)
-  const int ZB = (G + 1) / 2;
-  if (live) {
-    for (int j = p; j < ZB; j += 64) {
-      const uint8_t lo = zbuf[r * G + 2 * j];
-      const uint8_t hi = (2 * j + 1 < G) ? zbuf[r * G + 2 * j + 1] : 0;
-      zeros[row * ZB + j] = static_cast<uint8_t>(lo | (hi << 4));
-    }
   }
   if (bad) atomicOr(status, bad);
 }
@@ -129,8 +128,8 @@ cudaError_t launch_pack(const void* W, const float* s, const void* cs64, const v
                         void* codes, void* scales, void* zeros, int* status, cudaStream_t st) {
   const int G = static_cast<int>(K / G_);
   const unsigned grid = static_cast<unsigned>((N + PACK_ROWS - 1) / PACK_ROWS);
-  const size_t dyn = static_cast<size_t>(PACK_ROWS) * G;
-  pack_fold_rtn_kernel<<<grid, PACK_ROWS * 64, dyn, st>>>(
+  (void)G;
+  pack_fold_rtn_kernel<<<grid, PACK_ROWS * 64, 0, st>>>(
       static_cast<const __half*>(W), s, static_cast<const double2*>(cs64), static_cast<const uchar2*>(idx), N, K, L,
       static_cast<uint8_t*>(codes), static_cast<__half*>(scales), static_cast<uint8_t*>(zeros), status);
   return cudaGetLastError();

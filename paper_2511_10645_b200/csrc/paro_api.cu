@@ -14,6 +14,7 @@
 
 #include "../../include/paro.h"
 #include "paro_internal.h"
+#include "tile_layout.cuh"
 
 namespace {
 
@@ -152,9 +153,10 @@ paro_status paro_pack_sizes(int64_t N, int64_t K, int32_t group, int32_t n_rot, 
   if (n_rot < 0 || n_rot > PARO_MAX_ROT)
     return fail(PARO_ERR_UNSUPPORTED, "paro_pack_sizes: n_rot must be in [0, 8] (got %d)", n_rot);
   const int64_t G = K / kG;
-  out->codes = static_cast<size_t>(N * K / 2);
-  out->scales = static_cast<size_t>(N * G * 2 + 16);
-  out->zeros = static_cast<size_t>(N * ceil_div(G, 2) + 16);
+  const int64_t tiles = ceil_div(N, int64_t(paro::TILE_ROWS)) * G;  // tile layout (tile_layout.cuh)
+  out->codes = static_cast<size_t>(tiles * paro::TILE_CODE_BYTES);
+  out->scales = static_cast<size_t>(tiles * paro::TILE_SCALE_BYTES);
+  out->zeros = static_cast<size_t>(tiles * paro::TILE_ZERO_BYTES);
   out->rot_cs = static_cast<size_t>(G * n_rot * PARO_SLOTS * 8);
   out->rot_idx = static_cast<size_t>(G * n_rot * PARO_SLOTS * 2);
   out->svec = static_cast<size_t>(K * 4);
@@ -263,9 +265,11 @@ paro_status paro_pack(const void* W, const float* s, const float* theta, const i
   if (e == cudaSuccess && L > 0) e = cudaMemcpyAsync(out->rot_cs, cs32.data(), cs32.size() * 4, cudaMemcpyHostToDevice, cs);
   if (e == cudaSuccess && L > 0) e = cudaMemcpyAsync(out->rot_idx, idx.data(), idx.size(), cudaMemcpyHostToDevice, cs);
   if (e == cudaSuccess) e = cudaMemcpyAsync(out->svec, s, K * 4, cudaMemcpyDeviceToDevice, cs);
-  // zero the padding tails of scales/zeros (read by 16-byte bulk copies)
-  if (e == cudaSuccess) e = cudaMemsetAsync(static_cast<uint8_t*>(out->scales) + N * G * 2, 0, 16, cs);
-  if (e == cudaSuccess) e = cudaMemsetAsync(static_cast<uint8_t*>(out->zeros) + N * ceil_div(G, 2), 0, 16, cs);
+  // zero the packed buffers: rows >= N of the last row block stay zero, zero points are
+  // OR-ed in nibble by nibble
+  if (e == cudaSuccess) e = cudaMemsetAsync(out->codes, 0, sz.codes, cs);
+  if (e == cudaSuccess) e = cudaMemsetAsync(out->scales, 0, sz.scales, cs);
+  if (e == cudaSuccess) e = cudaMemsetAsync(out->zeros, 0, sz.zeros, cs);
   if (e == cudaSuccess)
     e = paro::launch_pack(W, s, tb, idx_dev, N, K, L, out->codes, out->scales, out->zeros, status, cs);
   int hstatus = 0;
@@ -324,19 +328,19 @@ static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, 
     Ls[i] = packed[i].n_rot;
   }
   const int64_t K = packed[0].K;
-  int bt = B >= 4 ? 4 : (B >= 2 ? 2 : 1);
-  paro::GemvConfig cfg;
-  const char* why = "";
-  while (!paro::plan_gemv(bt, n, Ns, Ls, K, rotate, &cfg, &why)) {
-    if (bt == 1) return fail(PARO_ERR_UNSUPPORTED, "paro_linear: %s", why);
-    bt /= 2;
-  }
   const size_t xe = 2, ye = dtype_bytes(y_dtype);
-  for (int64_t b0 = 0; b0 < B; b0 += cfg.BT) {
+  paro::GemvConfig cfg;
+  int planned_b = 0;
+  for (int64_t b0 = 0; b0 < B; b0 += paro::GEMV_MAX_B) {  // token tiles of <= 8 (the MMA's N)
+    const int bt = static_cast<int>(std::min<int64_t>(paro::GEMV_MAX_B, B - b0));
+    if (bt != planned_b) {
+      const char* why = "";
+      if (!paro::plan_gemv(bt, n, Ns, Ls, K, rotate, &cfg, &why)) return fail(PARO_ERR_UNSUPPORTED, "paro_linear: %s", why);
+      planned_b = bt;
+    }
     paro::GemvArgs& a = cfg.a;
     a.x = static_cast<const uint8_t*>(x) + b0 * K * xe;
     a.x_bf16 = x_dtype == PARO_BF16;
-    a.B = static_cast<int>(std::min<int64_t>(cfg.BT, B - b0));
     for (int i = 0; i < n; ++i) {
       paro::GemvLinear& d = a.lin[i];
       d.codes = static_cast<const uint8_t*>(packed[i].codes);
@@ -412,7 +416,6 @@ paro_status paro_linear(const void* x, paro_dtype x_dtype, int64_t B, const paro
       rot_idx = widx;
     }
   }
-  const size_t xe = 2, ye = dtype_bytes(y_dtype);
   if (use_prefill(B, N, K, flags)) {
     void* xq = wsp;
     cudaError_t e = paro::launch_transform(x, x_dtype == PARO_BF16, B, K, L, svec, rot_cs, rot_idx, rotate, xq, pdl, 1, cs);
@@ -482,10 +485,11 @@ paro_status paro_unpack_logical(const paro_packed* packed, void* codes_u8, void*
   if (!codes_u8 || !scales_f16 || !zeros_u8) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_unpack_logical: NULL output");
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   const int64_t N = packed->N, K = packed->K, G = K / kG;
-  cudaError_t e = cudaMemcpyAsync(scales_f16, packed->scales, N * G * 2, cudaMemcpyDeviceToDevice, cs);
-  if (e == cudaSuccess)
-    e = paro::launch_unpack(static_cast<const uint8_t*>(packed->codes), static_cast<const uint8_t*>(packed->zeros), N,
-                            K, static_cast<uint8_t*>(codes_u8), static_cast<uint8_t*>(zeros_u8), cs);
+  (void)G;
+  cudaError_t e = paro::launch_unpack(static_cast<const uint8_t*>(packed->codes),
+                                      static_cast<const uint8_t*>(packed->scales),
+                                      static_cast<const uint8_t*>(packed->zeros), N, K, static_cast<uint8_t*>(codes_u8),
+                                      static_cast<uint8_t*>(scales_f16), static_cast<uint8_t*>(zeros_u8), cs);
   if (e != cudaSuccess) return cuda_fail(e, "paro_unpack_logical");
   return PARO_OK;
 }

@@ -11,12 +11,13 @@ cudaError_t launch_pack(const void* W, const float* s, const void* cs64, const v
 
 // ---------------------------------------------------------------- decode GEMV
 constexpr int GEMV_MAX_LIN = 4;  // linears sharing one activation in a single launch
+constexpr int GEMV_MAX_B = 8;    // tokens per decode launch (the MMA's N = 8 columns)
 
 // One linear of a (multi-)linear decode launch: its CTAs are [cta_begin, cta_begin + n_ctas)
-// (whole clusters), its rows split evenly over them.
+// (whole clusters); cluster c owns rb_base + (c < rb_extra) consecutive 16-row blocks.
 struct GemvLinear {
-  const uint8_t* codes;
-  const uint8_t* scales;  // fp16 bytes
+  const uint8_t* codes;   // tiles (tile_layout.cuh)
+  const uint8_t* scales;
   const uint8_t* zeros;
   const float2* rot_cs;
   const uchar2* rot_idx;
@@ -24,54 +25,53 @@ struct GemvLinear {
   const float* bias;
   void* y;  // [B][N]
   int N, L;
-  int cta_begin, n_ctas, rows_base, rows_extra;
+  int cta_begin, n_ctas, rb_base, rb_extra;
 };
 
 struct GemvArgs {
   const void* x;  // [B][K] fp16 / bf16 (shared by all linears of the launch)
   int x_bf16;
-  int B;          // live tokens in this launch (<= BT)
+  int B;          // tokens in this launch (1..8)
   int n_lin;
   GemvLinear lin[GEMV_MAX_LIN];
   int y_dtype;
   int K, G;
   int rotate;
   int pdl;
-  int debug;      // record a per-CTA event timeline (g_paro_timeline)
-  int WK;         // warps along K (one 512*J K-slice each)
-  int RG;         // row groups (warps along rows)
-  int SR;         // rows per stage (even)
-  int S;          // ring depth
+  int debug;        // record a per-CTA event timeline (g_paro_timeline)
+  int NW;           // compute warps
+  int TPS;          // tiles per ring stage
+  int S;            // ring depth
   int param_slots;  // ring slots lent to the staged rotation parameters (-1: dedicated region)
   uint32_t off_param;
-  int rows_max;
+  int R_max;        // row blocks a CTA's tile range can touch
   uint32_t slot_bytes, sc_off, z_off;  // per-stage slot layout
-  uint32_t off_u, off_usum, off_x, off_scr, off_part, off_ring, off_bar, smem_total;
+  uint32_t off_u, off_xs, off_x, off_scr, off_part, off_recv, off_ring, off_bar, smem_total;
 };
 
 struct GemvConfig {
-  int BT, J, CL, grid;
+  int NW, CL, grid;
   GemvArgs a;
 };
 
-// Plan a launch (pure host arithmetic, no CUDA calls except a cached device query).
-// n_lin linears of widths Ns[i] and rotation counts Ls[i] sharing K (and x).
-bool plan_gemv(int B_tile, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, int rotate, GemvConfig* cfg,
+// Plan a launch (pure host arithmetic plus cached device / occupancy queries).
+// n_lin linears of widths Ns[i] and rotation counts Ls[i] sharing K (and x); B <= 8 tokens.
+bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, int rotate, GemvConfig* cfg,
                const char** why);
 cudaError_t launch_gemv(const GemvConfig& cfg, cudaStream_t st);
 
 // ---------------------------------------------------------------- activation transform (prefill pre-stage)
 cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, int L, const float* svec,
                              const float2* rot_cs, const uchar2* rot_idx, int rotate, void* x_out, int pdl,
-                             int perm8, cudaStream_t st);
+                             int prefill_order, cudaStream_t st);
 
 // ---------------------------------------------------------------- on-the-fly transform preparation
 cudaError_t launch_prepare_transform(const float* theta, const int16_t* pairs, int G, int L, int P, float2* rot_cs,
                                      uchar2* rot_idx, cudaStream_t st);
 
 // ---------------------------------------------------------------- misc
-cudaError_t launch_unpack(const uint8_t* codes, const uint8_t* zeros, int64_t N, int64_t K, uint8_t* codes_u8,
-                          uint8_t* zeros_u8, cudaStream_t st);
+cudaError_t launch_unpack(const uint8_t* codes, const uint8_t* scales, const uint8_t* zeros, int64_t N, int64_t K,
+                          uint8_t* codes_u8, uint8_t* scales_f16, uint8_t* zeros_u8, cudaStream_t st);
 cudaError_t launch_permute_gather(const void* src, void* dst, int world, int64_t B, int64_t Ns, int elem_bytes,
                                   cudaStream_t st);
 

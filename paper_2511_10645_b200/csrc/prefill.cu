@@ -14,10 +14,11 @@
 // into a 128 x 256 fp32 accumulator in TMEM; four epilogue warps read it back with
 // tcgen05.ld, add the bias, convert and store y.
 //
-// The pre-stage stores x' with each 8-channel block permuted to
-// (0,4,1,5,2,6,3,7): the same permutation along K on both operands leaves the
-// contraction unchanged and lets the dequant producer emit fp16 pairs straight from
-// two AND/OR masks per 32-bit code word (no byte permutes).
+// Stage ks of a row is the 32-byte half (ks & 1) of its tile-layout row in group ks / 2;
+// the dequantiser emits fp16 pairs straight from one AND/OR mask per nibble pair of a
+// 32-bit code word (no byte permutes).  The pre-stage stores x' in that same channel
+// order (prefill_pos, tile_layout.cuh): one permutation along K on both operands leaves
+// the contraction unchanged.
 //
 // Warp roles (384 threads, persistent over tiles):
 //   warp 0: TMA producer (x' tiles)     warp 1: MMA issuer     warp 2: TMEM allocator
@@ -31,6 +32,7 @@
 #include "paro_internal.h"
 #include "ptx.cuh"
 #include "umma.cuh"
+#include "tile_layout.cuh"
 
 namespace paro {
 
@@ -148,21 +150,23 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     // ---------------- dequant producer: weight row r of the tile -> TMEM lane r
     const int r = (warp - 4) * 32 + lane;
     const uint32_t lane_addr = static_cast<uint32_t>((warp - 4) * 32) << 16;
-    const int G = a.K / 128, ZB = (G + 1) / 2;
+    const int G = a.K / 128;
     uint32_t it = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const int n = (tile % n_row_tiles) * PF_BM + r;
-      const uint8_t* crow = a.codes + static_cast<int64_t>(n) * (a.K / 2);
+      const int r16 = n % TILE_ROWS;
+      const int64_t T0 = static_cast<int64_t>(n / TILE_ROWS) * G;  // first tile of the row block
+      // stage ks = half-row (32 bytes) ks & 1 of tile (row block, ks / 2)
+      const uint8_t* crow = a.codes + T0 * TILE_CODE_BYTES + r16 * 64;
       uint4 c0 = __ldg(reinterpret_cast<const uint4*>(crow));
       uint4 c1 = __ldg(reinterpret_cast<const uint4*>(crow + 16));
       uint32_t ss = 0, zz = 0;
       for (int ks = 0; ks < n_ks; ++ks, ++it) {
-        const int k0 = ks * PF_BK;
-        if ((k0 & 127) == 0) {
-          const int g = k0 >> 7;
-          const __half S = a.scales[static_cast<int64_t>(n) * G + g];
-          const uint8_t zb = a.zeros[static_cast<int64_t>(n) * ZB + (g >> 1)];
-          const int z = (g & 1) ? (zb >> 4) : (zb & 15);
+        if ((ks & 1) == 0) {
+          const int64_t T = T0 + (ks >> 1);
+          const __half S = a.scales[T * 16 + tile_scale_idx(r16)];
+          const uint8_t zb = a.zeros[T * TILE_ZERO_BYTES + (r16 & 7)];
+          const int z = (r16 >> 3) ? (zb >> 4) : (zb & 15);
           const __half2 S2 = __halves2half2(S, S);
           const __half zh = __ushort_as_half(static_cast<unsigned short>(0x6400 + z));  // 1024 + z
           const __half2 Z2 = __halves2half2(zh, zh);
@@ -171,18 +175,19 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         }
         const uint4 w0 = c0, w1 = c1;
         if (ks + 1 < n_ks) {  // prefetch the next 32 code bytes of this row
-          c0 = __ldg(reinterpret_cast<const uint4*>(crow + (k0 + PF_BK) / 2));
-          c1 = __ldg(reinterpret_cast<const uint4*>(crow + (k0 + PF_BK) / 2 + 16));
+          const uint8_t* nx = crow + static_cast<int64_t>((ks + 1) >> 1) * TILE_CODE_BYTES + ((ks + 1) & 1) * 32;
+          c0 = __ldg(reinterpret_cast<const uint4*>(nx));
+          c1 = __ldg(reinterpret_cast<const uint4*>(nx + 16));
         }
         uint32_t v[32];
         const uint32_t wd[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
           const uint32_t w = wd[m];
-          v[4 * m + 0] = hsub_hmul((w & 0x000F000Fu) | 0x64006400u, zz, ss);          // (k0, k4)
-          v[4 * m + 1] = hsub_hmul(((w >> 4) & 0x000F000Fu) | 0x64006400u, zz, ss);   // (k1, k5)
-          v[4 * m + 2] = hsub_hmul(((w >> 8) & 0x000F000Fu) | 0x64006400u, zz, ss);   // (k2, k6)
-          v[4 * m + 3] = hsub_hmul(((w >> 12) & 0x000F000Fu) | 0x64006400u, zz, ss);  // (k3, k7)
+          v[4 * m + 0] = hsub_hmul((w & 0x000F000Fu) | 0x64006400u, zz, ss);          // nibbles (0, 4)
+          v[4 * m + 1] = hsub_hmul(((w >> 4) & 0x000F000Fu) | 0x64006400u, zz, ss);   // (1, 5)
+          v[4 * m + 2] = hsub_hmul(((w >> 8) & 0x000F000Fu) | 0x64006400u, zz, ss);   // (2, 6)
+          v[4 * m + 3] = hsub_hmul(((w >> 12) & 0x000F000Fu) | 0x64006400u, zz, ss);  // (3, 7)
         }
         const int sa = it % PF_SA;
         mbar_wait(&a_empty[sa], ((it / PF_SA) & 1) ^ 1);

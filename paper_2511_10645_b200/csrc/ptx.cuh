@@ -138,21 +138,34 @@ PARO_DEV uint32_t lds_u8_a(uint32_t addr) {
   return v;
 }
 
-// fp32 += f16 * f16 (mixed-precision FMA, sm_100+: SASS FHFMA; the half of each
-// 32-bit register is selected for free).
-PARO_DEV float fma_f16lo(uint32_t a2, uint32_t b2, float c) {
-  float d;
-  asm("{.reg .f16 a0,a1,b0,b1;\n\tmov.b32 {a0,a1}, %1;\n\tmov.b32 {b0,b1}, %2;\n\tfma.rn.f32.f16 %0, a0, b0, %3;\n\t}"
-      : "=f"(d)
-      : "r"(a2), "r"(b2), "f"(c));
-  return d;
+PARO_DEV uint32_t lds_u32_a(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
 }
-PARO_DEV float fma_f16hi(uint32_t a2, uint32_t b2, float c) {
-  float d;
-  asm("{.reg .f16 a0,a1,b0,b1;\n\tmov.b32 {a0,a1}, %1;\n\tmov.b32 {b0,b1}, %2;\n\tfma.rn.f32.f16 %0, a1, b1, %3;\n\t}"
-      : "=f"(d)
-      : "r"(a2), "r"(b2), "f"(c));
-  return d;
+PARO_DEV float2 lds_f2_a(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return v;
+}
+
+// ---------------------------------------------------------------- warp-level tensor-core MMA
+// D(16x8, fp32) += A(16x16, fp16, row) * B(16x8, fp16, col)  (SASS HMMA.16816.F32).
+// Fragments (g = lane / 4, t = lane % 4): a0 = A[g][2t..2t+1], a1 = A[g+8][2t..], a2 = A[g][2t+8..],
+// a3 = A[g+8][2t+8..]; b0 = B[2t..2t+1][g], b1 = B[2t+8..2t+9][g]; d = D[g][2t], D[g][2t+1],
+// D[g+8][2t], D[g+8][2t+1].  fp16 subnormal A inputs are exact (tools/probe_hmma.cu).
+PARO_DEV void mma_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+PARO_DEV void mma_16816_z(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%10,%10,%10,%10};"
+      : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "f"(0.f));
 }
 
 }  // namespace paro

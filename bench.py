@@ -172,7 +172,7 @@ def run_paro(args):
     # its own transform (Alg. A2 inserts one per linear)
     groups = [["q_proj", "k_proj", "v_proj"], ["o_proj"], ["gate_proj", "up_proj"], ["down_proj"]]
 
-    def run_step(li, flags, pdl=True):
+    def run_step(li, flags, pdl=False):
         f = flags | (paro.PARO_LINEAR_PDL if pdl else 0)
         layer = {name: (N, K, packed) for name, N, K, packed in pool[li % n_layers]}
         if world == 1:
@@ -242,13 +242,13 @@ def run_paro(args):
                 with torch.cuda.stream(stream):
                     for li in range(2):
                         lin = [e for e in pool[li % n_layers] if e[0] == name][0]
-                        paro.paro_linear(xs[K], lin[3], y=ys[name], flags=fl | paro.PARO_LINEAR_PDL, workspace=ws,
+                        paro.paro_linear(xs[K], lin[3], y=ys[name], flags=fl, workspace=ws,
                                          stream=stream)
                     stream.synchronize()
                     with torch.cuda.graph(gph, stream=stream):
                         for li in range(reps):
                             lin = [e for e in pool[li % n_layers] if e[0] == name][0]
-                            paro.paro_linear(xs[K], lin[3], y=ys[name], flags=fl | paro.PARO_LINEAR_PDL,
+                            paro.paro_linear(xs[K], lin[3], y=ys[name], flags=fl,
                                              workspace=ws, stream=stream)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 with torch.cuda.stream(stream):

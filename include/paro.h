@@ -61,22 +61,21 @@ typedef enum { PARO_F16 = 0, PARO_BF16 = 1, PARO_F32 = 2 } paro_dtype;
 
 /* Byte sizes of the packed buffers of one linear layer (all device buffers,
  * each must be 16-byte aligned).  Layout (private to the kernels; tests read it
- * only through paro_unpack_logical).  The weight is stored in TILES of 16 output rows x
- * one 128-channel group, tile T = (n / 16) * G + gamma (G = K/128, NB = ceil(N/16) row
+ * only through paro_unpack_logical).  The weight is stored in TILES of 32 output rows x
+ * one 128-channel group, tile T = (n / 32) * G + gamma (G = K/128, NB = ceil(N/32) row
  * blocks; rows >= N of the last block are zero):
- *   codes  : NB*G*1024   INT4 codes; row r of a tile is 64 bytes at r*64 whose nibbles hold
+ *   codes  : NB*G*2048   INT4 codes; row r of a tile is 64 bytes at r*64 whose nibbles hold
  *                        the group's channels in the order the decode kernel's mma.sync
  *                        fragments need (tile_k() in csrc/tile_layout.cuh).
- *   scales : NB*G*32     fp16 group scales S, 16 per tile (rows r and r+8 adjacent).
- *   zeros  : NB*G*16     uint4 zero points, 8 bytes per tile (byte r: rows r, r+8) + 8 zero bytes.
+ *   scales : NB*G*64     fp16 group scales S, 32 per tile (rows r, r+8, r+16, r+24 adjacent).
+ *   zeros  : NB*G*16     uint4 zero points, 32 per tile (16-bit word r: rows r, r+8, r+16, r+24).
  *   rot_cs : G*L*64*8    fp32 (cos theta, sin theta) per (group, rotation, slot), stored as
  *                        records [G][L][32][2] (slot = lane + 32*s), the slots of each rotation
  *                        reordered and oriented so every shared-memory gather/scatter of the
  *                        runtime transform is bank-conflict free.
  *   rot_idx: G*L*64*2    u8 (i, j) per slot in the same order.
  *   svec   : K*4         fp32 s.
- * Algorithmic weight bytes are N*K/2 + N*G*2 + N*G/2 (0.5195 B/weight); the stored
- * layout reads 0.5234 B/weight (16-byte zero-point records). */
+ * Weight bytes are N*K/2 + N*G*2 + N*G/2 (0.5195 B/weight) when N % 32 == 0. */
 typedef struct {
   size_t codes, scales, zeros, rot_cs, rot_idx, svec;
 } paro_packed_sizes;

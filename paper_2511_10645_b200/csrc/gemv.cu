@@ -4,8 +4,8 @@
 //
 // SURVEY.md 8(a) rows a4 (stage + scale), a5 (L rotations, Eq. 5 in column form),
 // a6 (dequant GEMV), a8 (epilogue).  One kernel, launched as clusters of CL CTAs
-// (1-2 CTAs per SM, one wave).  A cluster owns a run of 16-row blocks of one linear;
-// the tiles (16 rows x one 128-group, tile_layout.cuh) of that run are split evenly and
+// (1-2 CTAs per SM, one wave).  A cluster owns a run of 32-row blocks of one linear;
+// the tiles (32 rows x one 128-group, tile_layout.cuh) of that run are split evenly and
 // contiguously over its CL CTAs (split-K at tile granularity, so every CTA streams the
 // same number of bytes whatever N and K are).
 //
@@ -22,11 +22,13 @@
 //    -- and its per-token sum go to every CTA of the cluster with st.async (DSMEM),
 //    completion counted in bytes on the receiver's mbarrier.  x' never goes to HBM.
 //  * compute warps, phase 2 (GEMV): warp w takes tiles w, w + NW, ... of each stage.
-//    Lane (g, t) loads 16 code bytes of row g and of row g + 8 (two LDS.128); one AND
-//    mask per 32-bit word turns 2 nibbles into an fp16 A-fragment register: a nibble q
-//    in bits [0,4) of a half IS the subnormal q * 2^-24 (bits [4,8): 16q * 2^-24), which
-//    the tensor cores multiply exactly.  Eight mma.sync.m16n8k16 per tile (four per
-//    power-of-two scale) give sum_k q[n,k] x'[k, b] for the 16 rows x 8 token columns;
+//    Lane (g, t) loads 16 code bytes of rows g, g + 8, g + 16, g + 24 (four LDS.128); one
+//    AND mask per 32-bit word turns 2 nibbles into an fp16 A-fragment register: a nibble
+//    q in bits [0,4) of a half IS the subnormal q * 2^-24 (bits [4,8): 16q * 2^-24), which
+//    the tensor cores multiply exactly.  Sixteen mma.sync.m16n8k16 per tile (two 16-row
+//    blocks, four per power-of-two scale each, four independent accumulator chains) give
+//    sum_k q[n,k] x'[k, b] for the 32 rows x 8 token columns, sharing one set of B
+//    fragments;
 //    the epilogue applies y += S * (sum q x' - z * sum x') per (row, group, token).
 //    Row partials of a warp go to shared memory when its row block changes; warps are
 //    summed in a fixed order, and the CTA holding the first tile of a row block adds
@@ -50,6 +52,7 @@ constexpr int TL_EVENTS = 12;           // debug timeline: events per CTA
 constexpr uint32_t TILE_BYTES = TILE_CODE_BYTES + TILE_SCALE_BYTES + TILE_ZERO_BYTES;
 
 __device__ unsigned long long g_paro_timeline[1024 * TL_EVENTS];
+__device__ unsigned long long g_paro_prof[1024 * 16 * 8];  // debug: per (CTA, warp) cycle counters
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -85,20 +88,21 @@ __device__ __forceinline__ float half2_sum(uint32_t w) {
   return f.x + f.y;
 }
 
-// first cluster-local tile of cluster CTA k (tiles split evenly and contiguously)
-__device__ __forceinline__ int cta_tile_start(int k, int nt, int CL) {
-  return static_cast<int>((static_cast<int64_t>(k) * nt) / CL);
-}
+// first cluster-local tile of cluster CTA k (tiles split evenly and contiguously); CL is a
+// power of two, lcl = log2(CL): shifts, no integer division
+__device__ __forceinline__ int cta_tile_start(int k, int nt, int lcl) { return (k * nt) >> lcl; }
 // the CTA whose (non-empty) range holds cluster-local tile x
-__device__ __forceinline__ int cta_of_tile(int x, int nt, int CL) {
+__device__ __forceinline__ int cta_of_tile(int x, int nt, int lcl) {
   int k = 0;
-  for (int c = 1; c < CL; ++c)
-    if (cta_tile_start(c, nt, CL) <= x) k = c;
+  for (int c = 1; c < (1 << lcl); ++c)
+    if (cta_tile_start(c, nt, lcl) <= x) k = c;
   return k;
 }
 
+// BT: token tile (1, 2, 4, 8; a.B <= BT live tokens), compile-time so the per-token loops
+// of the transform unroll (a runtime token loop costs ~3.5x in the rotation latency).
 // MAXT: 288 (<= 8 compute warps, 2 CTAs / SM) or 544 (<= 16 compute warps)
-template <int MAXT>
+template <int BT, int MAXT>
 __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(const GemvArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
@@ -112,12 +116,13 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
   const int K = a.K, G = a.G, L = d.L, B = a.B;
   const int CL = static_cast<int>(cluster_nctarank());
   const int crank = static_cast<int>(cluster_ctarank());
+  const int lcl = __ffs(CL) - 1;  // CL is 1, 2, 4 or 8
   // this cluster's row blocks and this CTA's tile range [tA, tE) (cluster-local indices)
   const int cl = (static_cast<int>(blockIdx.x) - d.cta_begin) / CL;
   const int nrb_c = d.rb_base + (cl < d.rb_extra ? 1 : 0);
   const int rbc0 = cl * d.rb_base + min(cl, d.rb_extra);
   const int nt = nrb_c * G;
-  const int tA = cta_tile_start(crank, nt, CL), tE = cta_tile_start(crank + 1, nt, CL);
+  const int tA = cta_tile_start(crank, nt, lcl), tE = cta_tile_start(crank + 1, nt, lcl);
   const int n_my = tE - tA;
   const int TPS = a.TPS;
   const int n_stages = (n_my + TPS - 1) / TPS;
@@ -127,13 +132,13 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
   const bool own_last = n_my > 0 && (rho_first + n_rho - 1) * G >= tA;  // likewise for my last block
   // later CTAs of the cluster that share my last row block (they push their partials)
   int last_cta = crank;
-  if (own_last && (rho_first + n_rho) * G > tE) last_cta = cta_of_tile((rho_first + n_rho) * G - 1, nt, CL);
+  if (own_last && (rho_first + n_rho) * G > tE) last_cta = cta_of_tile((rho_first + n_rho) * G - 1, nt, lcl);
 
-  uint8_t* ufr = smem + a.off_u;                                  // x' fragments [G][4][B][4][4] u32
+  uint8_t* ufr = smem + a.off_u;                                  // x' fragments [G][4][BT][4][4] u32
   float* xsum = reinterpret_cast<float*>(smem + a.off_xs);        // sum of x' per (group, token) [G][8]
   uint8_t* xs = smem + a.off_x;                                   // raw x slice [B][x_cols]
-  float* part = reinterpret_cast<float*>(smem + a.off_part);      // [NW][R_max][16][B]
-  float* recv = reinterpret_cast<float*>(smem + a.off_recv);      // [CL-1][16][B]
+  float* part = reinterpret_cast<float*>(smem + a.off_part);      // [NW][R_max][32][BT]
+  float* recv = reinterpret_cast<float*>(smem + a.off_recv);      // [CL-1][32][BT]
   uint8_t* ring = smem + a.off_ring;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.off_bar);
   uint64_t* empty = full + a.S;
@@ -171,24 +176,22 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
     mbar_init(pbar, 1);
     mbar_init(pfree, NW);
     mbar_init(rbar, 1);
-    if (CL > 1) mbar_arrive_expect_tx(xpbar, static_cast<uint32_t>(B) * (K * 2 + G * 4));
+    if (CL > 1) mbar_arrive_expect_tx(xpbar, static_cast<uint32_t>(BT) * (K * 2 + G * 4));
     uint32_t rbytes = 0;
     for (int c = crank + 1; c <= last_cta; ++c)
-      if (cta_tile_start(c + 1, nt, CL) > cta_tile_start(c, nt, CL)) rbytes += 16 * B * 4;
+      if (cta_tile_start(c + 1, nt, lcl) > cta_tile_start(c, nt, lcl)) rbytes += TILE_ROWS * B * 4;
     if (rbytes) mbar_arrive_expect_tx(rbar, rbytes);
     fence_mbar_init();
   }
-  if (CL > 1) {
-    cluster_arrive();
-    cluster_wait();  // mbarriers initialised; every CTA of the cluster is running (DSMEM legal)
-  } else {
-    __syncthreads();
-  }
+  // Barriers are initialised; arrive on the cluster barrier (release) now but wait on it
+  // only right before the first DSMEM access, so the copies below are not held back by
+  // the launch skew between the CTAs of a cluster.
+  __syncthreads();
+  if (CL > 1) cluster_arrive();
   if (a.pdl) pdl_launch_dependents();
 
   // ------------------------------------------------------------ producer warp
   if (is_producer) {
-    named_bar_sync(2, (NW + 1) * 32);
     const uint64_t pol = l2_evict_first_policy();
     const int64_t tile0 = static_cast<int64_t>(rbc0) * G + tA;  // my first tile (global index)
     auto issue = [&](int st, int slot) {
@@ -219,6 +222,10 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
                           static_cast<const uint8_t*>(a.x) + (static_cast<int64_t>(b) * K + g0 * GRP) * 2,
                           x_row_bytes, xbar);
       }
+      if (a.xfirst > 0) {  // let the activations / parameters land before the weight stream
+        if (x_cols > 0) mbar_wait(xbar, 0);
+        if (pstaged && x_cols > 0 && L_eff > 0) mbar_wait(pbar, 0);
+      }
       for (int st = 0; st < first; ++st) issue(st, st);
       int st = first;
       if (P > 0) {  // the lent slots: first use once phase 1 released them
@@ -232,40 +239,43 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
       }
     }
     __syncwarp();
+    if (CL > 1) cluster_wait();
     return;
   }
 
   // ------------------------------------------------------------ phase 1: activation transform
   {
-    float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * (B * 132);
+    float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * (BT * 132);
+    const uint32_t scr_a = smem_u32(scr);
     const uint32_t u_addr = smem_u32(ufr), s_addr = smem_u32(xsum), bar_addr = smem_u32(xpbar);
+    const uint32_t ps_a = pded ? smem_u32(smem + a.off_param)
+                               : smem_u32(ring) + static_cast<uint32_t>(a.S - P) * a.slot_bytes;
+    const uint32_t xs_a = smem_u32(xs);
     // output: lane (i4, t4, hf) writes B-fragment registers 4*i4 + 2*hf, +1 of fragment lane t4
     // (MMA m = 2*i4 + hf: channels (16m + 2t4, +1) and (16m + 2t4 + 8, +9))
     const int i4 = lane >> 3, t4 = (lane >> 1) & 3, hf = lane & 1;
     const int k0 = 16 * (2 * i4 + hf) + 2 * t4;
-    bool first = true;
-    for (int gam = g0 + warp; gam < g1 || first; gam += NW) {
-      const bool have = gam < g1;
+    bool cwaited = false;
+    if (g0 + warp < g1) {
+      if (pstaged && x_cols > 0 && L_eff > 0) mbar_wait(pbar, 0);
+      if (x_cols > 0) mbar_wait(xbar, 0);
+      if (threadIdx.x == 0) PARO_TL(a, 1);
+    }
+    unsigned long long q0 = a.debug ? clock64() : 0, q_par = 0, q_rot = 0, q_out = 0;
+    for (int gam = g0 + warp; gam < g1; gam += NW) {
+      const int gl = gam - g0;  // group index within this CTA's staged slice
       float4 csr[8];
       uint32_t ixr[8];
-      float sv[4];
-      if (first) {
-        named_bar_arrive(2, (NW + 1) * 32);  // let the producer start
-        if (pstaged && x_cols > 0 && L_eff > 0) mbar_wait(pbar, 0);
-        if (x_cols > 0) mbar_wait(xbar, 0);
-        if (threadIdx.x == 0) PARO_TL(a, 1);
-        first = false;
-      }
-      if (!have) break;
       if (L_eff > 0) {
         if (pstaged) {  // records [group][t][32 lanes]
-          const float4* csp = reinterpret_cast<const float4*>(pslot) + (gam - g0) * L_eff * 32 + lane;
-          const uint32_t* ixp = reinterpret_cast<const uint32_t*>(pslot + p_cs_bytes) + (gam - g0) * L_eff * 32 + lane;
 #pragma unroll
           for (int t = 0; t < 8; ++t)
             if (t < L_eff) {
-              csr[t] = csp[t * 32];
-              ixr[t] = ixp[t * 32];
+              const uint32_t rec = static_cast<uint32_t>((gl * L_eff + t) * 32 + lane);
+              const uint4 c = lds128_a(ps_a + rec * 16);
+              csr[t] = make_float4(__uint_as_float(c.x), __uint_as_float(c.y), __uint_as_float(c.z),
+                                   __uint_as_float(c.w));
+              ixr[t] = lds_u32_a(ps_a + p_cs_bytes + rec * 4);
             }
         } else {
           const int64_t rec = static_cast<int64_t>(gam) * L * 32 + lane;
@@ -277,33 +287,46 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
             }
         }
       }
-      // two explicit paths: a runtime-selected shared/global pointer compiles to generic loads
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int k = (gam - g0) * GRP + lane + 32 * i;
-        if (!a.rotate)
-          sv[i] = 1.f;
-        else if (pstaged && L_eff > 0)
-          sv[i] = reinterpret_cast<const float*>(pslot + p_cs_bytes + p_ix_bytes)[k];
-        else
-          sv[i] = __ldg(d.svec + g0 * GRP + k);
-      }
-      const int kg = gam * GRP;
-      for (int b = 0; b < B; ++b)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int k = lane + 32 * i;
-          const float v = load_act(xs + static_cast<size_t>(b) * x_row_bytes, a.x_bf16, kg - g0 * GRP + k);
-          scr[b * 132 + k] = v * sv[i];  // diag(s) x  (a4)
+      // lane: channels 4*lane .. 4*lane + 3 of the group for the scale step
+      float4 sv = make_float4(1.f, 1.f, 1.f, 1.f);
+      if (a.rotate) {
+        if (pstaged && L_eff > 0) {
+          const uint4 v = lds128_a(ps_a + p_cs_bytes + p_ix_bytes + static_cast<uint32_t>(gl * GRP + 4 * lane) * 4);
+          sv = make_float4(__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), __uint_as_float(v.w));
+        } else {
+          sv = __ldg(reinterpret_cast<const float4*>(d.svec + gam * GRP) + lane);
         }
+      }
+#pragma unroll
+      for (int b = 0; b < BT; ++b) {
+        uint2 xv = make_uint2(0u, 0u);  // tokens >= B: x = 0 (x' = 0, never stored)
+        if (b < B) xv = lds_u64_a(xs_a + static_cast<uint32_t>(b) * x_row_bytes + static_cast<uint32_t>(gl * GRP + 4 * lane) * 2);
+        float2 f01, f23;
+        if (a.x_bf16) {
+          f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.x));
+          f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.y));
+        } else {
+          f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv.x));
+          f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv.y));
+        }
+        // diag(s) x  (a4)
+        *reinterpret_cast<float4*>(scr + b * 132 + 4 * lane) =
+            make_float4(f01.x * sv.x, f01.y * sv.y, f23.x * sv.z, f23.y * sv.w);
+      }
       __syncwarp();
+      if (a.debug) {
+        const unsigned long long c = clock64();
+        q_par += c - q0;
+        q0 = c;
+      }
       if (threadIdx.x == 0 && gam == g0) PARO_TL(a, 8);
 #pragma unroll
       for (int t = 0; t < 8; ++t) {  // a5: rotations t = 1..L, Eq. 4 form, pre-update values
         if (t >= L_eff) break;
         const uint32_t i0 = ixr[t] & 0xff, j0 = (ixr[t] >> 8) & 0xff;
         const uint32_t i1 = (ixr[t] >> 16) & 0xff, j1 = ixr[t] >> 24;
-        for (int b = 0; b < B; ++b) {
+#pragma unroll
+        for (int b = 0; b < BT; ++b) {
           float* sb = scr + b * 132;
           const float a0 = sb[i0], b0 = sb[j0];
           const float a1 = sb[i1], b1 = sb[j1];
@@ -314,23 +337,37 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
         }
         __syncwarp();
       }
+      if (a.debug) {
+        const unsigned long long c = clock64();
+        q_rot += c - q0;
+        q0 = c;
+      }
       if (threadIdx.x == 0 && gam == g0) PARO_TL(a, 6);
-      for (int b = 0; b < B; ++b) {
-        const float* sb = scr + b * 132;
-        const uint32_t p0 = pack_half2(sb[k0], sb[k0 + 1]);
-        const uint32_t p1 = pack_half2(sb[k0 + 8], sb[k0 + 9]);
+      if (CL > 1 && !cwaited) {
+        cluster_wait();  // every CTA of the cluster is running and initialised: DSMEM is legal
+        cwaited = true;
+      }
+#pragma unroll
+      for (int b = 0; b < BT; ++b) {
+        const float2 v01 = lds_f2_a(scr_a + static_cast<uint32_t>(b * 132 + k0) * 4);
+        const float2 v89 = lds_f2_a(scr_a + static_cast<uint32_t>(b * 132 + k0 + 8) * 4);
+        const uint32_t p0 = pack_half2(v01.x, v01.y);
+        const uint32_t p1 = pack_half2(v89.x, v89.y);
         // sum over the group of the fp16-rounded x' (the zero-point term uses exactly the
         // values the tensor cores multiply)
         float cs = half2_sum(p0) + half2_sum(p1);
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
-        const uint32_t uo = u_addr + static_cast<uint32_t>(((gam * 4 + i4) * B + b) * 64 + t4 * 16 + hf * 8);
+        const uint32_t uo = u_addr + static_cast<uint32_t>(((gam * 4 + i4) * BT + b) * 64 + t4 * 16 + hf * 8);
         const uint32_t so = s_addr + static_cast<uint32_t>((gam * 8 + b) * 4);
         if (CL > 1) {
-          for (int r = 0; r < CL; ++r) {
-            const uint32_t rb = mapa(bar_addr, r);
-            st_async_v2(mapa(uo, r), p0, p1, rb);
-            if (lane == 0) st_async_b32(mapa(so, r), __float_as_uint(cs), rb);
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            if (r < CL) {
+              const uint32_t rb = mapa(bar_addr, r);
+              st_async_v2(mapa(uo, r), p0, p1, rb);
+              if (lane == 0) st_async_b32(mapa(so, r), __float_as_uint(cs), rb);
+            }
           }
         } else {
           *reinterpret_cast<uint2*>(ufr + (uo - u_addr)) = make_uint2(p0, p1);
@@ -338,100 +375,158 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
         }
       }
       __syncwarp();
+      if (a.debug) {
+        const unsigned long long c = clock64();
+        q_out += c - q0;
+        q0 = c;
+      }
       if (threadIdx.x == 0 && gam == g0) PARO_TL(a, 7);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(pfree);  // this warp no longer reads the staged parameters
     if (CL > 1) {
+      if (!cwaited) cluster_wait();
       mbar_wait(xpbar, 0);  // every group's x' has arrived from its owner CTA
     } else {
       named_bar_sync(1, NW * 32);
+    }
+    if (a.debug && lane == 0 && blockIdx.x < 1024 && warp < 16) {
+      unsigned long long* pp = g_paro_prof + (blockIdx.x * 16 + warp) * 8;
+      pp[4] = q_par;
+      pp[5] = q_rot;
+      pp[6] = q_out;
+      pp[7] = clock64() - q0;  // waiting for the cluster's x'
     }
   }
   if (threadIdx.x == 0) PARO_TL(a, 2);
 
   // ------------------------------------------------------------ phase 2: GEMV on mma.sync
-  float* pw = part + static_cast<size_t>(warp) * a.R_max * 16 * B;
-  for (int i = lane; i < n_rho * 16 * B; i += 32) pw[i] = 0.f;
+  constexpr int TR = TILE_ROWS;  // 32 rows per tile: two 16-row MMA blocks (rows g, g+8 | g+16, g+24)
+  float* pw = part + static_cast<size_t>(warp) * a.R_max * TR * BT;
+  for (int i = lane; i < n_rho * TR * BT; i += 32) pw[i] = 0.f;
   __syncwarp();
   const int gq = lane >> 2, t = lane & 3;
+  // B-fragment token of this lane: columns >= BT duplicate token BT-1 (computed, never stored)
+  const int bq = min(gq, BT - 1);
   const uint32_t u_a = smem_u32(ufr), xs_a = smem_u32(xsum), ring_a = smem_u32(ring);
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  // acc[4h + e]: rows gq + 16h (e = 0, 1) and gq + 16h + 8 (e = 2, 3), columns 2t, 2t + 1
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
   int cur = -1;
   auto flush = [&]() {
-    float* pr = pw + cur * 16 * B;
-    if (2 * t < B) {
-      pr[gq * B + 2 * t] = acc[0];
-      pr[(gq + 8) * B + 2 * t] = acc[2];
-    }
-    if (2 * t + 1 < B) {
-      pr[gq * B + 2 * t + 1] = acc[1];
-      pr[(gq + 8) * B + 2 * t + 1] = acc[3];
+    float* pr = pw + cur * TR * BT;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (2 * t < B) {
+        pr[(gq + 16 * h) * BT + 2 * t] = acc[4 * h + 0];
+        pr[(gq + 16 * h + 8) * BT + 2 * t] = acc[4 * h + 2];
+      }
+      if (2 * t + 1 < B) {
+        pr[(gq + 16 * h) * BT + 2 * t + 1] = acc[4 * h + 1];
+        pr[(gq + 16 * h + 8) * BT + 2 * t + 1] = acc[4 * h + 3];
+      }
     }
   };
+  // this warp's tiles are tA + warp + NW * m (TPS is a multiple of NW): (row block, group)
+  // advance incrementally
+  int rb = (tA + warp) / G;
+  int g = (tA + warp) - rb * G;
+  unsigned long long c_wait = 0, c_work = 0, c_t = a.debug ? clock64() : 0;
   for (int st = 0; st < n_stages; ++st) {
     const int slot = st % a.S;
     if (st == n_stages - 1 && threadIdx.x == 0) PARO_TL(a, 10);
     mbar_wait(&full[slot], (st / a.S) & 1);
+    if (a.debug) {
+      const unsigned long long c = clock64();
+      c_wait += c - c_t;
+      c_t = c;
+    }
     if (st == 0 && threadIdx.x == 0) PARO_TL(a, 3);
     if (st == n_stages - 1 && threadIdx.x == 0) PARO_TL(a, 11);
     const uint32_t sbase = ring_a + static_cast<uint32_t>(slot) * a.slot_bytes;
     const int nts = min(TPS, n_my - st * TPS);
-    for (int i = warp; i < nts; i += NW) {
-      const int tl = tA + st * TPS + i;
-      const int rb = tl / G;
-      const int g = tl - rb * G;
+    for (int i = warp; i < (a.skip_math ? 0 : nts); i += NW) {
       if (rb - rho_first != cur) {
         if (cur >= 0) flush();
-        acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = 0.f;
         cur = rb - rho_first;
       }
+      // codes: quad t of rows gq, gq + 8, gq + 16, gq + 24 (words j = 0..3 each)
       const uint32_t ca = sbase + static_cast<uint32_t>(i) * TILE_CODE_BYTES + lane * 16;
-      const uint4 wa = lds128_a(ca);        // row gq, quad t: words j = 0..3
-      const uint4 wb = lds128_a(ca + 512);  // row gq + 8
+      uint4 w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[q] = lds128_a(ca + q * 512);
+      // B fragments of group g (token bq): registers 4 * ii .. 4 * ii + 3 = MMAs 2 ii, 2 ii + 1
       uint32_t bf[16];
-      if (gq < B) {
-        const uint32_t xa = u_a + static_cast<uint32_t>(((g * 4) * B + gq) * 64 + t * 16);
+      {
+        const uint32_t xa = u_a + static_cast<uint32_t>(((g * 4) * BT + bq) * 64 + t * 16);
 #pragma unroll
         for (int ii = 0; ii < 4; ++ii) {
-          const uint4 v = lds128_a(xa + ii * B * 64);
+          const uint4 v = lds128_a(xa + ii * BT * 64);
           bf[4 * ii + 0] = v.x;
           bf[4 * ii + 1] = v.y;
           bf[4 * ii + 2] = v.z;
           bf[4 * ii + 3] = v.w;
         }
-      } else {
-#pragma unroll
-        for (int q = 0; q < 16; ++q) bf[q] = 0u;
       }
-      const uint32_t w0[4] = {wa.x, wa.y, wa.z, wa.w};
-      const uint32_t w1[4] = {wb.x, wb.y, wb.z, wb.w};
-      float D1[4], D16[4];  // 2^-24 sum q x' (low nibbles), 2^-20 sum q x' (high nibbles)
+      // 2^-24 sum q x' (low-nibble MMAs) and 2^-20 sum q x' (high-nibble MMAs) per 16-row block
+      float D1[2][4], D16[2][4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t x = w0[j], y = w1[j], x8 = x >> 8, y8 = y >> 8;
-        if (j == 0) {
-          mma_16816_z(D1, x & 0x000F000Fu, y & 0x000F000Fu, x8 & 0x000F000Fu, y8 & 0x000F000Fu, bf[0], bf[1]);
-          mma_16816_z(D16, x & 0x00F000F0u, y & 0x00F000F0u, x8 & 0x00F000F0u, y8 & 0x00F000F0u, bf[2], bf[3]);
-        } else {
-          mma_16816(D1, x & 0x000F000Fu, y & 0x000F000Fu, x8 & 0x000F000Fu, y8 & 0x000F000Fu, bf[4 * j], bf[4 * j + 1]);
-          mma_16816(D16, x & 0x00F000F0u, y & 0x00F000F0u, x8 & 0x00F000F0u, y8 & 0x00F000F0u, bf[4 * j + 2],
-                    bf[4 * j + 3]);
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t w0[4] = {w[2 * h].x, w[2 * h].y, w[2 * h].z, w[2 * h].w};
+        const uint32_t w1[4] = {w[2 * h + 1].x, w[2 * h + 1].y, w[2 * h + 1].z, w[2 * h + 1].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t x = w0[j], y = w1[j], x8 = x >> 8, y8 = y >> 8;
+          if (j == 0) {
+            mma_16816_z(D1[h], x & 0x000F000Fu, y & 0x000F000Fu, x8 & 0x000F000Fu, y8 & 0x000F000Fu, bf[0], bf[1]);
+            mma_16816_z(D16[h], x & 0x00F000F0u, y & 0x00F000F0u, x8 & 0x00F000F0u, y8 & 0x00F000F0u, bf[2],
+                        bf[3]);
+          } else {
+            mma_16816(D1[h], x & 0x000F000Fu, y & 0x000F000Fu, x8 & 0x000F000Fu, y8 & 0x000F000Fu, bf[4 * j],
+                      bf[4 * j + 1]);
+            mma_16816(D16[h], x & 0x00F000F0u, y & 0x00F000F0u, x8 & 0x00F000F0u, y8 & 0x00F000F0u, bf[4 * j + 2],
+                      bf[4 * j + 3]);
+          }
         }
       }
       // epilogue of the tile (a6): y += S * (2^24 * (D1 + D16 / 16) - z * sum x')
-      const uint32_t sp = lds_u32_a(sbase + a.sc_off + static_cast<uint32_t>(i) * TILE_SCALE_BYTES + gq * 4);
-      const uint32_t zb = lds_u8_a(sbase + a.z_off + static_cast<uint32_t>(i) * TILE_ZERO_BYTES + gq);
-      const float2 S2 = __half22float2(*reinterpret_cast<const __half2*>(&sp));
-      const float z0 = static_cast<float>(zb & 15u), z1 = static_cast<float>(zb >> 4);
+      const uint2 sp = lds_u64_a(sbase + a.sc_off + static_cast<uint32_t>(i) * TILE_SCALE_BYTES + gq * 8);
+      const uint32_t zw = lds_u16z_a(sbase + a.z_off + static_cast<uint32_t>(i) * TILE_ZERO_BYTES + gq * 2);
+      const float2 Sa = __half22float2(*reinterpret_cast<const __half2*>(&sp.x));  // rows gq, gq + 8
+      const float2 Sb = __half22float2(*reinterpret_cast<const __half2*>(&sp.y));  // rows gq + 16, gq + 24
       const float2 X2 = lds_f2_a(xs_a + static_cast<uint32_t>((g * 8 + 2 * t) * 4));
-      acc[0] = fmaf(S2.x, fmaf(fmaf(D16[0], 0.0625f, D1[0]), TWO_P24, -z0 * X2.x), acc[0]);
-      acc[1] = fmaf(S2.x, fmaf(fmaf(D16[1], 0.0625f, D1[1]), TWO_P24, -z0 * X2.y), acc[1]);
-      acc[2] = fmaf(S2.y, fmaf(fmaf(D16[2], 0.0625f, D1[2]), TWO_P24, -z1 * X2.x), acc[2]);
-      acc[3] = fmaf(S2.y, fmaf(fmaf(D16[3], 0.0625f, D1[3]), TWO_P24, -z1 * X2.y), acc[3]);
+      const float Sr[4] = {Sa.x, Sa.y, Sb.x, Sb.y};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {  // row gq + 8q: block h = q / 2, fragment half q % 2
+        const float zq = static_cast<float>((zw >> (4 * q)) & 15u);
+        const int h = q >> 1, e = (q & 1) * 2;
+        acc[4 * h + e] = fmaf(Sr[q], fmaf(fmaf(D16[h][e], 0.0625f, D1[h][e]), TWO_P24, -zq * X2.x), acc[4 * h + e]);
+        acc[4 * h + e + 1] =
+            fmaf(Sr[q], fmaf(fmaf(D16[h][e + 1], 0.0625f, D1[h][e + 1]), TWO_P24, -zq * X2.y), acc[4 * h + e + 1]);
+      }
+      g += NW;
+      while (g >= G) {
+        g -= G;
+        ++rb;
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the stage
+    if (a.debug) {
+      const unsigned long long c = clock64();
+      c_work += c - c_t;
+      c_t = c;
+    }
+  }
+  if (a.debug && lane == 0 && blockIdx.x < 1024 && warp < 16) {
+    unsigned long long* pp = g_paro_prof + (blockIdx.x * 16 + warp) * 8;
+    pp[0] = c_wait;
+    pp[1] = c_work;
+    pp[2] = static_cast<unsigned long long>(n_stages);
+    pp[3] = static_cast<unsigned long long>(n_my);
   }
   if (cur >= 0) flush();
   if (threadIdx.x == 0) PARO_TL(a, 4);
@@ -439,22 +534,23 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
 
   // ------------------------------------------------------------ reduction + epilogue (a8)
   named_bar_sync(1, NW * 32);
-  const int n_out = n_rho * 16 * B;
+  const int n_out = n_rho * TR * BT;
   for (int idx = threadIdx.x; idx < n_out; idx += NW * 32) {
-    const int rho = idx / (16 * B), r = (idx / B) % 16, b = idx % B;
+    const int rho = idx / (TR * BT), r = (idx / BT) % TR, b = idx % BT;
+    if (b >= B) continue;
     float sum = 0.f;
-    for (int w = 0; w < NW; ++w) sum += part[((static_cast<size_t>(w) * a.R_max + rho) * 16 + r) * B + b];
+    for (int w = 0; w < NW; ++w) sum += part[((static_cast<size_t>(w) * a.R_max + rho) * TR + r) * BT + b];
     const int rg = rho_first + rho;
     if (rho == 0 && !own_first) {
       // the block started in an earlier CTA: push this partial to it (recv slot crank - owner - 1)
-      const int owner = cta_of_tile(rg * G, nt, CL);
+      const int owner = cta_of_tile(rg * G, nt, lcl);
       const uint32_t dst =
-          smem_u32(recv) + static_cast<uint32_t>((((crank - owner - 1) * 16 + r) * B + b) * 4);
+          smem_u32(recv) + static_cast<uint32_t>((((crank - owner - 1) * TR + r) * BT + b) * 4);
       st_async_b32(mapa(dst, owner), __float_as_uint(sum), mapa(smem_u32(rbar), owner));
     } else if (rho == n_rho - 1 && last_cta > crank) {
-      part[(static_cast<size_t>(rho) * 16 + r) * B + b] = sum;  // warp-0 slot of this element
+      part[(static_cast<size_t>(rho) * TR + r) * BT + b] = sum;  // warp-0 slot of this element
     } else {
-      const int64_t n = static_cast<int64_t>(rbc0 + rg) * 16 + r;
+      const int64_t n = static_cast<int64_t>(rbc0 + rg) * TR + r;
       if (n < d.N) {
         float v = sum;
         if (d.bias) v += __ldg(d.bias + n);
@@ -466,12 +562,13 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
     named_bar_sync(1, NW * 32);
     mbar_wait(rbar, 0);
     const int rho = n_rho - 1, rg = rho_first + rho;
-    for (int idx = threadIdx.x; idx < 16 * B; idx += NW * 32) {
-      const int r = idx / B, b = idx % B;
-      float sum = part[(static_cast<size_t>(rho) * 16 + r) * B + b];
+    for (int idx = threadIdx.x; idx < TR * BT; idx += NW * 32) {
+      const int r = idx / BT, b = idx % BT;
+      if (b >= B) continue;
+      float sum = part[(static_cast<size_t>(rho) * TR + r) * BT + b];
       for (int c = crank + 1; c <= last_cta; ++c)  // fixed order
-        if (cta_tile_start(c + 1, nt, CL) > cta_tile_start(c, nt, CL)) sum += recv[((c - crank - 1) * 16 + r) * B + b];
-      const int64_t n = static_cast<int64_t>(rbc0 + rg) * 16 + r;
+        if (cta_tile_start(c + 1, nt, lcl) > cta_tile_start(c, nt, lcl)) sum += recv[((c - crank - 1) * TR + r) * BT + b];
+      const int64_t n = static_cast<int64_t>(rbc0 + rg) * TR + r;
       if (n < d.N) {
         float v = sum;
         if (d.bias) v += __ldg(d.bias + n);
@@ -480,6 +577,11 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
     }
   }
   if (threadIdx.x == 0) PARO_TL(a, 5);
+}
+
+extern "C" int paro_debug_read_prof(unsigned long long* host, int n) {
+  if (n > 1024 * 16 * 8) n = 1024 * 16 * 8;
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_paro_prof, sizeof(unsigned long long) * n));
 }
 
 // debug: copy the per-CTA event timeline (ns, %globaltimer) of the last debug launch
@@ -515,15 +617,23 @@ static int smem_optin() {
 
 static inline uint32_t align_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
-static const void* kernel_for(int threads) {
-  if (threads <= 288) return reinterpret_cast<const void*>(&paro_gemv_kernel<288>);
-  if (threads <= 544) return reinterpret_cast<const void*>(&paro_gemv_kernel<544>);
+static const void* kernel_for(int BT, int threads) {
+#define PARO_KF(BT_)                                                                        \
+  if (BT == BT_) {                                                                        \
+    if (threads <= 288) return reinterpret_cast<const void*>(&paro_gemv_kernel<BT_, 288>); \
+    if (threads <= 544) return reinterpret_cast<const void*>(&paro_gemv_kernel<BT_, 544>); \
+  }
+  PARO_KF(1)
+  PARO_KF(2)
+  PARO_KF(4)
+  PARO_KF(8)
+#undef PARO_KF
   return nullptr;
 }
 
 // Co-resident CTAs for this launch shape (whole clusters), from the occupancy API.
-static int max_resident_ctas(int threads, int smem, int CL) {
-  const void* k = kernel_for(threads);
+static int max_resident_ctas(int BT, int threads, int smem, int CL) {
+  const void* k = kernel_for(BT, threads);
   if (!k) return 0;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
     cudaGetLastError();
@@ -568,10 +678,11 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
     *why = "1..4 linears per decode launch";
     return false;
   }
-  if (B < 1 || B > GEMV_MAX_B) {
-    *why = "decode launches take 1..8 tokens";
+  if (B != 1 && B != 2 && B != 4 && B != 8) {
+    *why = "decode token tile must be 1, 2, 4 or 8";
     return false;
   }
+  c.BT = B;
   int64_t NBsum = 0;
   int L = 0;
   int64_t NB[GEMV_MAX_LIN];
@@ -581,17 +692,20 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
     L = std::max(L, Ls[i]);
   }
   const int G = static_cast<int>(K / GRP);
-  // 8 compute warps with 2 CTAs / SM by default; PARO_NW / PARO_CTAS_PER_SM / PARO_CLUSTER /
-  // PARO_TPS override for tuning
-  int NW = std::max(1, std::min(16, env_int("PARO_NW", 8)));
+  // 16 compute warps, 1 CTA / SM, clusters of 4, 32-tile stages by default (measured best on
+  // the bench's Llama-3-8B layer); PARO_NW / PARO_CTAS_PER_SM / PARO_CLUSTER / PARO_TPS override
+  int NW = std::max(1, std::min(16, env_int("PARO_NW", 16)));
   int ctas_per_sm = env_int("PARO_CTAS_PER_SM", NW <= 8 ? 2 : 1) == 1 ? 1 : 2;
   if (NW > 8) ctas_per_sm = 1;
-  int CL = env_int("PARO_CLUSTER", 8);
+  int CL = env_int("PARO_CLUSTER", 4);
   if (CL != 1 && CL != 2 && CL != 4 && CL != 8) CL = 8;
   while (CL > 1 && CL > G) CL /= 2;
-  const int TPS = std::max(1, std::min(64, env_int("PARO_TPS", 2 * NW)));
+  int TPS = std::max(1, std::min(64, env_int("PARO_TPS", 2 * NW)));
+  TPS = std::max(NW, TPS / NW * NW);  // a multiple of NW: warp w's tiles are w, w + NW, ...
   c.NW = NW;
   c.CL = CL;
+  c.a.xfirst = env_int("PARO_XFIRST", 0);
+  c.a.skip_math = env_int("PARO_SKIP_MATH", 0);  // debug: stream the weights, skip the tile math
   GemvArgs& a = c.a;
   a.n_lin = n_lin;
   a.B = B;
@@ -609,7 +723,7 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
   const int g_per = (G + CL - 1) / CL;
   const uint32_t x_bytes = align_up(static_cast<uint32_t>(B) * g_per * GRP * 2, 128);
   const uint32_t scr_bytes = align_up(static_cast<uint32_t>(NW) * B * 132 * 4, 128);
-  const uint32_t recv_bytes = align_up(static_cast<uint32_t>(std::max(1, CL - 1)) * 16 * B * 4, 128);
+  const uint32_t recv_bytes = align_up(static_cast<uint32_t>(std::max(1, CL - 1)) * TILE_ROWS * B * 4, 128);
   if (u_bytes > 64 * 1024) ctas_per_sm = 1;
   int budget = (smem_optin() + 1024) / ctas_per_sm - 2048;
   int max_tiles_cta = 0;
@@ -656,7 +770,7 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
     a.off_scr = off;
     off += scr_bytes;
     a.off_part = off;
-    off += align_up(static_cast<uint32_t>(NW) * a.R_max * 16 * B * 4, 128);
+    off += align_up(static_cast<uint32_t>(NW) * a.R_max * TILE_ROWS * B * 4, 128);
     a.off_recv = off;
     off += recv_bytes;
     a.off_bar = off;
@@ -674,10 +788,14 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
     // region when it fits, else lend the last ring slots (refilled after phase 1)
     a.param_slots = 0;
     a.off_param = 0;
-    if (rotate && L > 0) {
+    if (rotate && L > 0 && env_int("PARO_PSTAGE", 1)) {
       const uint32_t pbytes = static_cast<uint32_t>(g_per) * 32 * L * 20 + static_cast<uint32_t>(g_per) * GRP * 4;
       const int P = static_cast<int>((pbytes + a.slot_bytes - 1) / a.slot_bytes);
-      if (static_cast<int64_t>(a.smem_total) + align_up(pbytes, 128) <= budget) {
+      // lend the last ring slots (refilled once phase 1 is done) when that keeps >= 3 slots
+      // streaming weights from the start; else a dedicated region if it fits
+      if (P + 3 <= S && env_int("PARO_PDED", 0) == 0) {
+        a.param_slots = P;
+      } else if (static_cast<int64_t>(a.smem_total) + align_up(pbytes, 128) <= budget) {
         a.param_slots = -1;
         a.off_param = a.smem_total;
         a.smem_total += align_up(pbytes, 128);
@@ -700,7 +818,7 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
       *why = "decode kernel shared-memory plan does not fit";
       return false;
     }
-    const int resident = max_resident_ctas(threads, static_cast<int>(a.smem_total), CL);
+    const int resident = max_resident_ctas(c.BT, threads, static_cast<int>(a.smem_total), CL);
     if (resident <= 0 || resident >= c.grid) break;
     grid = resident / CL * CL;  // never launch more than one wave
   }
@@ -708,13 +826,16 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
     *why = "decode kernel shared-memory plan does not fit";
     return false;
   }
+  if (env_int("PARO_PLAN_DEBUG", 0))
+    fprintf(stderr, "[paro gemv plan] B=%d n_lin=%d K=%lld grid=%d CL=%d NW=%d TPS=%d S=%d param_slots=%d R_max=%d smem=%u\n",
+            B, n_lin, static_cast<long long>(K), c.grid, CL, NW, TPS, a.S, a.param_slots, a.R_max, a.smem_total);
   *cfg = c;
   return true;
 }
 
-template <int T>
+template <int BT, int T>
 static cudaError_t launch_t(const GemvConfig& c, cudaStream_t st) {
-  auto kern = paro_gemv_kernel<T>;
+  auto kern = paro_gemv_kernel<BT, T>;
   static int configured_smem = 0;  // per instantiation
   if (static_cast<int>(c.a.smem_total) > configured_smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -747,9 +868,15 @@ static cudaError_t launch_t(const GemvConfig& c, cudaStream_t st) {
 }
 
 cudaError_t launch_gemv(const GemvConfig& c, cudaStream_t st) {
-  const int threads = (c.NW + 1) * 32;
-  if (threads <= 288) return launch_t<288>(c, st);
-  if (threads <= 544) return launch_t<544>(c, st);
+  if (c.a.B < 1 || c.a.B > c.BT) return cudaErrorInvalidValue;
+  const bool big = (c.NW + 1) * 32 > 288;
+#define PARO_LG(BT_) \
+  if (c.BT == BT_) return big ? launch_t<BT_, 544>(c, st) : launch_t<BT_, 288>(c, st);
+  PARO_LG(1)
+  PARO_LG(2)
+  PARO_LG(4)
+  PARO_LG(8)
+#undef PARO_LG
   return cudaErrorInvalidConfiguration;
 }
 

@@ -160,9 +160,9 @@ __global__ void unpack_kernel(const uint8_t* __restrict__ codes, const __half* _
     const int64_t n = i / G, g = i % G;
     const int64_t T = (n / TILE_ROWS) * G + g;
     const int r = static_cast<int>(n % TILE_ROWS);
-    sf16[i] = scales[T * 16 + tile_scale_idx(r)];
-    const uint8_t b = zeros[T * TILE_ZERO_BYTES + (r & 7)];
-    zu8[i] = (r >> 3) ? (b >> 4) : (b & 15);
+    sf16[i] = scales[T * TILE_ROWS + tile_scale_idx(r)];
+    const uint8_t b = zeros[T * TILE_ZERO_BYTES + tile_zero_byte(r)];
+    zu8[i] = tile_zero_hi(r) ? (b >> 4) : (b & 15);
   }
 }
 

@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(PACK_ROWS * 64) pack_fold_rtn_kernel(
   __shared__ double Ssh[PACK_ROWS];
   __shared__ double zsh[PACK_ROWS];
   __shared__ uint8_t qsh[PACK_ROWS][G_];
-  const int r16 = static_cast<int>(row % TILE_ROWS);
+  const int rt = static_cast<int>(row % TILE_ROWS);  // row within its tile
 
   int bad = 0;
   for (int gam = 0; gam < G; ++gam) {
@@ -94,10 +94,10 @@ __global__ void __launch_bounds__(PACK_ROWS * 64) pack_fold_rtn_kernel(
       zsh[r] = z;
       if (live) {  // tile layout (tile_layout.cuh); buffers were zeroed before the launch
         const int64_t T = (row / TILE_ROWS) * G + gam;
-        scales[T * 16 + tile_scale_idx(r16)] = __ushort_as_half(hb);
-        const int64_t zbyte = T * TILE_ZERO_BYTES + (r16 & 7);
+        scales[T * TILE_ROWS + tile_scale_idx(rt)] = __ushort_as_half(hb);
+        const int64_t zbyte = T * TILE_ZERO_BYTES + tile_zero_byte(rt);
         atomicOr(reinterpret_cast<unsigned int*>(zeros + (zbyte & ~int64_t(3))),
-                 static_cast<unsigned int>(z) << (8 * (zbyte & 3) + 4 * (r16 >> 3)));
+                 static_cast<unsigned int>(z) << (8 * (zbyte & 3) + 4 * tile_zero_hi(rt)));
       }
     }
     __syncthreads();
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(PACK_ROWS * 64) pack_fold_rtn_kernel(
       const int tq = p >> 4, wj = (p >> 2) & 3, bw = p & 3;
       const uint8_t b = static_cast<uint8_t>(qsh[r][tile_k(tq, wj, 2 * bw)] | (qsh[r][tile_k(tq, wj, 2 * bw + 1)] << 4));
       const int64_t T = (row / TILE_ROWS) * G + gam;
-      codes[T * TILE_CODE_BYTES + r16 * 64 + p] = b;
+      codes[T * TILE_CODE_BYTES + rt * 64 + p] = b;
     }
     __syncthreads();
   }

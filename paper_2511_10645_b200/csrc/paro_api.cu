@@ -332,13 +332,15 @@ static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, 
   paro::GemvConfig cfg;
   int planned_b = 0;
   for (int64_t b0 = 0; b0 < B; b0 += paro::GEMV_MAX_B) {  // token tiles of <= 8 (the MMA's N)
-    const int bt = static_cast<int>(std::min<int64_t>(paro::GEMV_MAX_B, B - b0));
+    const int live = static_cast<int>(std::min<int64_t>(paro::GEMV_MAX_B, B - b0));
+    const int bt = live <= 1 ? 1 : live <= 2 ? 2 : live <= 4 ? 4 : 8;  // kernel token tile
     if (bt != planned_b) {
       const char* why = "";
       if (!paro::plan_gemv(bt, n, Ns, Ls, K, rotate, &cfg, &why)) return fail(PARO_ERR_UNSUPPORTED, "paro_linear: %s", why);
       planned_b = bt;
     }
     paro::GemvArgs& a = cfg.a;
+    a.B = live;
     a.x = static_cast<const uint8_t*>(x) + b0 * K * xe;
     a.x_bf16 = x_dtype == PARO_BF16;
     for (int i = 0; i < n; ++i) {

@@ -39,6 +39,8 @@ struct GemvArgs {
   int rotate;
   int pdl;
   int debug;        // record a per-CTA event timeline (g_paro_timeline)
+  int xfirst;       // producer waits for x / parameters before streaming weights
+  int skip_math;    // debug: stream the weights but skip the phase-2 math (timing only)
   int NW;           // compute warps
   int TPS;          // tiles per ring stage
   int S;            // ring depth
@@ -50,12 +52,13 @@ struct GemvArgs {
 };
 
 struct GemvConfig {
-  int NW, CL, grid;
+  int BT, NW, CL, grid;  // BT: compile-time token tile of the kernel instance
   GemvArgs a;
 };
 
 // Plan a launch (pure host arithmetic plus cached device / occupancy queries).
-// n_lin linears of widths Ns[i] and rotation counts Ls[i] sharing K (and x); B <= 8 tokens.
+// n_lin linears of widths Ns[i] and rotation counts Ls[i] sharing K (and x); B = token tile
+// (1, 2, 4 or 8); the launch sets cfg.a.B <= B live tokens.
 bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, int rotate, GemvConfig* cfg,
                const char** why);
 cudaError_t launch_gemv(const GemvConfig& cfg, cudaStream_t st);

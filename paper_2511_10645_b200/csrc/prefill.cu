@@ -154,19 +154,19 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     uint32_t it = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const int n = (tile % n_row_tiles) * PF_BM + r;
-      const int r16 = n % TILE_ROWS;
+      const int rt = n % TILE_ROWS;
       const int64_t T0 = static_cast<int64_t>(n / TILE_ROWS) * G;  // first tile of the row block
       // stage ks = half-row (32 bytes) ks & 1 of tile (row block, ks / 2)
-      const uint8_t* crow = a.codes + T0 * TILE_CODE_BYTES + r16 * 64;
+      const uint8_t* crow = a.codes + T0 * TILE_CODE_BYTES + rt * 64;
       uint4 c0 = __ldg(reinterpret_cast<const uint4*>(crow));
       uint4 c1 = __ldg(reinterpret_cast<const uint4*>(crow + 16));
       uint32_t ss = 0, zz = 0;
       for (int ks = 0; ks < n_ks; ++ks, ++it) {
         if ((ks & 1) == 0) {
           const int64_t T = T0 + (ks >> 1);
-          const __half S = a.scales[T * 16 + tile_scale_idx(r16)];
-          const uint8_t zb = a.zeros[T * TILE_ZERO_BYTES + (r16 & 7)];
-          const int z = (r16 >> 3) ? (zb >> 4) : (zb & 15);
+          const __half S = a.scales[T * TILE_ROWS + tile_scale_idx(rt)];
+          const uint8_t zb = a.zeros[T * TILE_ZERO_BYTES + tile_zero_byte(rt)];
+          const int z = tile_zero_hi(rt) ? (zb >> 4) : (zb & 15);
           const __half2 S2 = __halves2half2(S, S);
           const __half zh = __ushort_as_half(static_cast<unsigned short>(0x6400 + z));  // 1024 + z
           const __half2 Z2 = __halves2half2(zh, zh);

@@ -6,6 +6,9 @@
 #include <cuda_bf16.h>
 
 #define PARO_DEV __device__ __forceinline__
+#ifndef PARO_MBAR_SUSPEND_NS
+#define PARO_MBAR_SUSPEND_NS 1000000u
+#endif
 
 namespace paro {
 
@@ -25,13 +28,14 @@ PARO_DEV void mbar_arrive(uint64_t* bar) {
 }
 PARO_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
-  // suspend-time hint: the waiting warp sleeps (up to ~1 us) instead of spinning on issue slots
+  // suspend-time hint: the waiting warp is parked by the hardware until the phase completes
+  // (or the hint expires) instead of spinning on issue slots and the shared-memory pipe
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(PARO_MBAR_SUSPEND_NS)
       : "memory");
   return ok != 0;
 }
@@ -141,6 +145,16 @@ PARO_DEV uint32_t lds_u8_a(uint32_t addr) {
 PARO_DEV uint32_t lds_u32_a(uint32_t addr) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+PARO_DEV uint2 lds_u64_a(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+PARO_DEV uint32_t lds_u16z_a(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
 PARO_DEV float2 lds_f2_a(uint32_t addr) {

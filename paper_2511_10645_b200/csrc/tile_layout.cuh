@@ -1,21 +1,22 @@
 // tile_layout.cuh -- the packed weight layout shared by paro_pack, the decode GEMV, the
 // prefill GEMM and the logical unpack (private to the kernels; include/paro.h documents it).
 //
-// A tile is 16 output rows x one 128-channel group (2048 weights).  Tiles are stored
-// row-block-major: tile T = (n / 16) * G + gamma, so the tiles of a run of row blocks are
+// A tile is 32 output rows x one 128-channel group (4096 weights).  Tiles are stored
+// row-block-major: tile T = (n / 32) * G + gamma, so the tiles of a run of row blocks are
 // one contiguous range in all three arrays.
-//   codes : 1024 B per tile.  Row r (0..15) of the tile is 64 bytes at r * 64, read as
+//   codes : 2048 B per tile.  Row r (0..31) of the tile is 64 bytes at r * 64, read as
 //           4 quads t (16 B) x 4 words j (4 B).  Nibble n (bits [4n, 4n+4)) of word (t, j)
 //           holds in-group channel tile_k(t, j, n).  The map is chosen so that one AND mask
 //           per 32-bit word yields a ready mma.sync A-fragment register: lane (g, t) of the
-//           decode GEMV loads row g's quad t and row g+8's quad t (LDS.128 each) and
-//           (w & 0x000F000F) is {A[g][2t], A[g][2t+1]} of MMA 2j as fp16 subnormals q * 2^-24,
+//           decode GEMV loads quad t of rows g, g+8, g+16, g+24 (LDS.128 each, 512 B apart);
+//           for the 16-row MMA block (g, g+8), (w & 0x000F000F) of row g's word j is
+//           {A[g][2t], A[g][2t+1]} of MMA 2j as fp16 subnormals q * 2^-24,
 //           (w >> 8 & 0x000F000F) is {A[g][2t+8], A[g][2t+9]}, and the 0x00F000F0 masks give
 //           the same positions of MMA 2j+1 scaled by 16 (MMA m covers channels 16m..16m+15).
-//   scales: 32 B per tile: 16 fp16 S, row r at half index tile_scale_idx(r) (rows g, g+8
-//           adjacent: one 32-bit load per lane).
-//   zeros : 16 B per tile: byte r (0..7) holds z of row r (low nibble) and row r+8 (high);
-//           bytes 8..15 are zero (16-byte records keep every bulk copy aligned).
+//   scales: 64 B per tile: 32 fp16 S, row r at half index tile_scale_idx(r) (rows g, g+8,
+//           g+16, g+24 adjacent: one 64-bit load per lane).
+//   zeros : 16 B per tile: 32 uint4 z; the 16-bit word g holds rows g, g+8, g+16, g+24 in
+//           nibbles 0..3 (byte tile_zero_byte(r), nibble tile_zero_hi(r)).
 // Rows >= N of the last row block are zero in all three arrays.
 #pragma once
 
@@ -25,9 +26,9 @@
 
 namespace paro {
 
-constexpr int TILE_ROWS = 16;
-constexpr int TILE_CODE_BYTES = 1024;
-constexpr int TILE_SCALE_BYTES = 32;
+constexpr int TILE_ROWS = 32;
+constexpr int TILE_CODE_BYTES = 2048;
+constexpr int TILE_SCALE_BYTES = 64;
 constexpr int TILE_ZERO_BYTES = 16;
 
 // in-group channel held by nibble n of word j of quad t of a tile row
@@ -42,7 +43,9 @@ PARO_HD void tile_pos(int k, int* byte, int* hi) {
   *hi = n & 1;
 }
 
-PARO_HD int tile_scale_idx(int r) { return 2 * (r & 7) + (r >> 3); }
+PARO_HD int tile_scale_idx(int r) { return 4 * (r & 7) + (r >> 3); }
+PARO_HD int tile_zero_byte(int r) { return 2 * (r & 7) + (r >> 4); }
+PARO_HD int tile_zero_hi(int r) { return (r >> 3) & 1; }
 
 // Prefill operand order: position (within the group) of the channel held by nibble n of
 // word j of quad t, as the prefill dequantiser emits it (32-byte half rows, fp16 pairs

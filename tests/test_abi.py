@@ -43,12 +43,12 @@ def test_library_exports_every_declared_symbol(paro):
 def test_pack_sizes(paro):
     sz = paro.paro_pack_sizes(4096, 4096, 128, 8)
     G = 32
-    tiles = (4096 // 16) * G                   # tiles of 16 rows x one 128-group
-    assert sz.codes == 4096 * 4096 // 2 == tiles * 1024
-    assert sz.scales == tiles * 32 and sz.zeros == tiles * 16
+    tiles = (4096 // 32) * G                   # tiles of 32 rows x one 128-group
+    assert sz.codes == 4096 * 4096 // 2 == tiles * 2048
+    assert sz.scales == 4096 * G * 2 == tiles * 64 and sz.zeros == 4096 * G // 2 == tiles * 16
     assert sz.rot_cs == G * 8 * 64 * 8 and sz.rot_idx == G * 8 * 64 * 2 and sz.svec == 4096 * 4
-    sz = paro.paro_pack_sizes(3, 384, 128, 0)   # a partial row block pads to 16 rows
-    assert sz.codes == 3 * 1024 and sz.scales == 3 * 32 and sz.zeros == 3 * 16 and sz.rot_cs == 0
+    sz = paro.paro_pack_sizes(3, 384, 128, 0)   # a partial row block pads to 32 rows
+    assert sz.codes == 3 * 2048 and sz.scales == 3 * 64 and sz.zeros == 3 * 16 and sz.rot_cs == 0
 
 
 @pytest.mark.parametrize("args,kind", [

@@ -40,3 +40,14 @@ print(f"{mode} N={N}x{nlin} K={K}: {live.sum()} CTAs; us relative to first CTA s
 for i, n in enumerate(names):
     col = rel[:, i]
     print(f"  {n:15s} min {col.min():7.2f}  median {np.median(col):7.2f}  max {col.max():7.2f}")
+
+lib.paro_debug_read_prof.argtypes = [ctypes.c_void_p, ctypes.c_int]
+pb = np.zeros(1024 * 16 * 8, dtype=np.uint64)
+lib.paro_debug_read_prof(pb.ctypes.data, pb.size)
+pb = pb.reshape(1024, 16, 8)[: live.sum()].astype(np.int64)
+wait, work = pb[:, :, 0], pb[:, :, 1]
+act = (wait + work) > 0
+print(f"  phase-2 per warp (cycles): wait median {np.median(wait[act]):.0f} max {wait[act].max()}  work median {np.median(work[act]):.0f} max {work[act].max()}")
+print(f"  stages/CTA median {np.median(pb[:, 0, 2]):.0f}  tiles/CTA median {np.median(pb[:, 0, 3]):.0f}  work cycles per tile-per-warp {np.median(work[act]) / max(1, np.median(pb[:, 0, 3]) / max(1, act.sum(1).max())):.0f}")
+w0 = pb[:, 0, :]
+print(f"  phase-1 warp 0 (cycles): params+x+scale median {np.median(w0[:, 4]):.0f}  rotations {np.median(w0[:, 5]):.0f}  output {np.median(w0[:, 6]):.0f}  x'-wait {np.median(w0[:, 7]):.0f}")

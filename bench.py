@@ -172,7 +172,7 @@ def run_paro(args):
     # its own transform (Alg. A2 inserts one per linear)
     groups = [["q_proj", "k_proj", "v_proj"], ["o_proj"], ["gate_proj", "up_proj"], ["down_proj"]]
 
-    def run_step(li, flags, pdl=False):
+    def run_step(li, flags, pdl=True):
         f = flags | (paro.PARO_LINEAR_PDL if pdl else 0)
         layer = {name: (N, K, packed) for name, N, K, packed in pool[li % n_layers]}
         if world == 1:

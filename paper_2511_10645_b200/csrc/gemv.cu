@@ -39,6 +39,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "paro_internal.h"
 #include "ptx.cuh"
@@ -101,7 +102,9 @@ __device__ __forceinline__ int cta_of_tile(int x, int nt, int lcl) {
 
 // BT: token tile (1, 2, 4, 8; a.B <= BT live tokens), compile-time so the per-token loops
 // of the transform unroll (a runtime token loop costs ~3.5x in the rotation latency).
-// MAXT: 288 (<= 8 compute warps, 2 CTAs / SM) or 544 (<= 16 compute warps)
+// MAXT: 288 (<= 8 compute warps, 2 CTAs / SM), 512 (<= 15) or 640 (<= 19).  Registers are
+// allocated per SM sub-partition (16K each, warps round-robin), so 16 warps get up to 128
+// registers per thread while 17..20 warps get 96.
 template <int BT, int MAXT>
 __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(const GemvArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -144,9 +147,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
   uint64_t* empty = full + a.S;
   uint64_t* xbar = empty + a.S;  // raw activations landed (bulk copy)
   uint64_t* xpbar = xbar + 1;    // x' of all K landed (DSMEM st.async from the cluster)
-  uint64_t* pbar = xpbar + 1;    // rotation parameters + s of this CTA's groups landed
-  uint64_t* pfree = pbar + 1;    // phase 1 done with them (their ring slots can be refilled)
-  uint64_t* rbar = pfree + 1;    // partials of my last row block from later CTAs landed
+  uint64_t* rbar = xpbar + 1;    // partials of my last row block from later CTAs landed
 
   // groups whose transform this CTA computes
   const int g_per = (G + CL - 1) / CL;
@@ -155,15 +156,6 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
   const int x_cols = (g1 - g0) * GRP;  // activation columns this CTA stages
   const uint32_t x_row_bytes = static_cast<uint32_t>(x_cols) * 2;
   const int L_eff = a.rotate ? L : 0;
-  const uint32_t p_cs_bytes = static_cast<uint32_t>(g1 - g0) * 32 * L_eff * 16;
-  const uint32_t p_ix_bytes = static_cast<uint32_t>(g1 - g0) * 32 * L_eff * 4;
-  const uint32_t p_s_bytes = a.rotate ? static_cast<uint32_t>(x_cols) * 4 : 0;
-  // staged parameters: in a dedicated region (param_slots < 0) or in the last
-  // param_slots ring slots (lent until phase 1 is done); 0: read from global memory
-  const bool pded = a.param_slots < 0;
-  const int P = pded ? 0 : a.param_slots;
-  const bool pstaged = a.param_slots != 0;
-  uint8_t* pslot = pded ? smem + a.off_param : ring + static_cast<size_t>(a.S - P) * a.slot_bytes;
 
   if (threadIdx.x == 0) {
     PARO_TL(a, 0);
@@ -173,8 +165,6 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
     }
     mbar_init(xbar, 1);
     mbar_init(xpbar, 1);
-    mbar_init(pbar, 1);
-    mbar_init(pfree, NW);
     mbar_init(rbar, 1);
     if (CL > 1) mbar_arrive_expect_tx(xpbar, static_cast<uint32_t>(BT) * (K * 2 + G * 4));
     uint32_t rbytes = 0;
@@ -203,17 +193,14 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
       bulk_g2s(dst + a.sc_off, d.scales + T * TILE_SCALE_BYTES, nts * TILE_SCALE_BYTES, &full[slot], pol);
       bulk_g2s(dst + a.z_off, d.zeros + T * TILE_ZERO_BYTES, nts * TILE_ZERO_BYTES, &full[slot], pol);
     };
-    const int first = min(a.S - P, n_stages);
-    if (lane == 0 && pstaged && x_cols > 0 && L_eff > 0) {
-      mbar_arrive_expect_tx(pbar, p_cs_bytes + p_ix_bytes + p_s_bytes);
-      bulk_g2s_nohint(pslot, reinterpret_cast<const uint8_t*>(d.rot_cs) + static_cast<size_t>(g0) * 32 * L_eff * 16,
-                      p_cs_bytes, pbar);
-      bulk_g2s_nohint(pslot + p_cs_bytes,
-                      reinterpret_cast<const uint8_t*>(d.rot_idx) + static_cast<size_t>(g0) * 32 * L_eff * 4,
-                      p_ix_bytes, pbar);
-      bulk_g2s_nohint(pslot + p_cs_bytes + p_ix_bytes, d.svec + g0 * GRP, p_s_bytes, pbar);
-    }
-    if (a.pdl) pdl_wait();  // x may be produced by the previous kernel on the stream
+    const int first = min(a.S, n_stages);
+    // Request order: the activations are latency-critical (the transform waits for them), so
+    // they go first -- except under PDL, where one weight stage is requested before waiting
+    // for the previous kernel (weights are never written by it: PARO_LINEAR_PDL's contract).
+    const int early = (a.pdl && !a.xfirst) ? min(1, first) : 0;
+    if (lane == 0)
+      for (int st = 0; st < early; ++st) issue(st, st);
+    if (a.pdl) pdl_wait();
     if (lane == 0) {
       if (x_cols > 0) {
         mbar_arrive_expect_tx(xbar, x_row_bytes * static_cast<uint32_t>(B));
@@ -222,17 +209,9 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
                           static_cast<const uint8_t*>(a.x) + (static_cast<int64_t>(b) * K + g0 * GRP) * 2,
                           x_row_bytes, xbar);
       }
-      if (a.xfirst > 0) {  // let the activations / parameters land before the weight stream
-        if (x_cols > 0) mbar_wait(xbar, 0);
-        if (pstaged && x_cols > 0 && L_eff > 0) mbar_wait(pbar, 0);
-      }
-      for (int st = 0; st < first; ++st) issue(st, st);
-      int st = first;
-      if (P > 0) {  // the lent slots: first use once phase 1 released them
-        mbar_wait(pfree, 0);
-        for (; st < min(a.S, n_stages); ++st) issue(st, st);
-      }
-      for (; st < n_stages; ++st) {
+      if (a.xfirst && x_cols > 0) mbar_wait(xbar, 0);  // debug: activations land first
+      for (int st = early; st < first; ++st) issue(st, st);
+      for (int st = first; st < n_stages; ++st) {
         const int slot = st % a.S;
         mbar_wait(&empty[slot], ((st / a.S) & 1) ^ 1);  // stage st - S consumed by every warp
         issue(st, slot);
@@ -245,73 +224,55 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
 
   // ------------------------------------------------------------ phase 1: activation transform
   {
-    float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * (BT * 132);
+    float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * (a.scr_groups * BT * 132);
     const uint32_t scr_a = smem_u32(scr);
     const uint32_t u_addr = smem_u32(ufr), s_addr = smem_u32(xsum), bar_addr = smem_u32(xpbar);
-    const uint32_t ps_a = pded ? smem_u32(smem + a.off_param)
-                               : smem_u32(ring) + static_cast<uint32_t>(a.S - P) * a.slot_bytes;
     const uint32_t xs_a = smem_u32(xs);
     // output: lane (i4, t4, hf) writes B-fragment registers 4*i4 + 2*hf, +1 of fragment lane t4
     // (MMA m = 2*i4 + hf: channels (16m + 2t4, +1) and (16m + 2t4 + 8, +9))
     const int i4 = lane >> 3, t4 = (lane >> 1) & 3, hf = lane & 1;
     const int k0 = 16 * (2 * i4 + hf) + 2 * t4;
     bool cwaited = false;
-    if (g0 + warp < g1) {
-      if (pstaged && x_cols > 0 && L_eff > 0) mbar_wait(pbar, 0);
-      if (x_cols > 0) mbar_wait(xbar, 0);
-      if (threadIdx.x == 0) PARO_TL(a, 1);
-    }
-    unsigned long long q0 = a.debug ? clock64() : 0, q_par = 0, q_rot = 0, q_out = 0;
-    for (int gam = g0 + warp; gam < g1; gam += NW) {
-      const int gl = gam - g0;  // group index within this CTA's staged slice
-      float4 csr[8];
-      uint32_t ixr[8];
-      if (L_eff > 0) {
-        if (pstaged) {  // records [group][t][32 lanes]
+    unsigned long long q0 = 0, q_par = 0, q_rot = 0, q_out = 0;
+
+    // rotation parameters + s of one group -> registers (records [group][t][32 lanes]:
+    // (cos0, sin0, cos1, sin1) and (i0, j0, i1, j1) of slots lane, lane + 32)
+    auto load_params = [&](int gam, float4 (&cs)[8], uint32_t (&ix)[8], float4& sv) {
+      const int64_t rec = static_cast<int64_t>(gam) * L * 32 + lane;
 #pragma unroll
-          for (int t = 0; t < 8; ++t)
-            if (t < L_eff) {
-              const uint32_t rec = static_cast<uint32_t>((gl * L_eff + t) * 32 + lane);
-              const uint4 c = lds128_a(ps_a + rec * 16);
-              csr[t] = make_float4(__uint_as_float(c.x), __uint_as_float(c.y), __uint_as_float(c.z),
-                                   __uint_as_float(c.w));
-              ixr[t] = lds_u32_a(ps_a + p_cs_bytes + rec * 4);
-            }
-        } else {
-          const int64_t rec = static_cast<int64_t>(gam) * L * 32 + lane;
+      for (int t = 0; t < 8; ++t)
+        if (t < L_eff) {
+          cs[t] = __ldg(reinterpret_cast<const float4*>(d.rot_cs) + rec + t * 32);
+          ix[t] = __ldg(reinterpret_cast<const uint32_t*>(d.rot_idx) + rec + t * 32);
+        }
+      sv = a.rotate ? __ldg(reinterpret_cast<const float4*>(d.svec + gam * GRP) + lane) : make_float4(1.f, 1.f, 1.f, 1.f);
+    };
+    // x' = R_L ... R_1 diag(s) x of NG groups (in lockstep: independent dependency chains)
+    // for the BT tokens, written as B fragments (+ per-token sums) into every CTA of the cluster
+    auto process = [&](auto ngc, const int* gams, const float4 (*csr)[8], const uint32_t (*ixr)[8],
+                       const float4* sv) {
+      constexpr int NG = decltype(ngc)::value;
+      if (a.debug) q0 = clock64();
 #pragma unroll
-          for (int t = 0; t < 8; ++t)
-            if (t < L_eff) {
-              csr[t] = __ldg(reinterpret_cast<const float4*>(d.rot_cs) + rec + t * 32);
-              ixr[t] = __ldg(reinterpret_cast<const uint32_t*>(d.rot_idx) + rec + t * 32);
-            }
-        }
-      }
-      // lane: channels 4*lane .. 4*lane + 3 of the group for the scale step
-      float4 sv = make_float4(1.f, 1.f, 1.f, 1.f);
-      if (a.rotate) {
-        if (pstaged && L_eff > 0) {
-          const uint4 v = lds128_a(ps_a + p_cs_bytes + p_ix_bytes + static_cast<uint32_t>(gl * GRP + 4 * lane) * 4);
-          sv = make_float4(__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), __uint_as_float(v.w));
-        } else {
-          sv = __ldg(reinterpret_cast<const float4*>(d.svec + gam * GRP) + lane);
-        }
-      }
+      for (int q = 0; q < NG; ++q) {
+        const int gl = gams[q] - g0;  // group index within this CTA's activation slice
 #pragma unroll
-      for (int b = 0; b < BT; ++b) {
-        uint2 xv = make_uint2(0u, 0u);  // tokens >= B: x = 0 (x' = 0, never stored)
-        if (b < B) xv = lds_u64_a(xs_a + static_cast<uint32_t>(b) * x_row_bytes + static_cast<uint32_t>(gl * GRP + 4 * lane) * 2);
-        float2 f01, f23;
-        if (a.x_bf16) {
-          f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.x));
-          f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.y));
-        } else {
-          f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv.x));
-          f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv.y));
+        for (int b = 0; b < BT; ++b) {  // a4: diag(s) x, lane = channels 4*lane .. 4*lane + 3
+          uint2 xv = make_uint2(0u, 0u);  // tokens >= B: x = 0 (x' = 0, never stored)
+          if (b < B)
+            xv = lds_u64_a(xs_a + static_cast<uint32_t>(b) * x_row_bytes +
+                           static_cast<uint32_t>(gl * GRP + 4 * lane) * 2);
+          float2 f01, f23;
+          if (a.x_bf16) {
+            f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.x));
+            f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.y));
+          } else {
+            f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv.x));
+            f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv.y));
+          }
+          *reinterpret_cast<float4*>(scr + (q * BT + b) * 132 + 4 * lane) =
+              make_float4(f01.x * sv[q].x, f01.y * sv[q].y, f23.x * sv[q].z, f23.y * sv[q].w);
         }
-        // diag(s) x  (a4)
-        *reinterpret_cast<float4*>(scr + b * 132 + 4 * lane) =
-            make_float4(f01.x * sv.x, f01.y * sv.y, f23.x * sv.z, f23.y * sv.w);
       }
       __syncwarp();
       if (a.debug) {
@@ -319,21 +280,25 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
         q_par += c - q0;
         q0 = c;
       }
-      if (threadIdx.x == 0 && gam == g0) PARO_TL(a, 8);
+      if (threadIdx.x == 0 && gams[0] == g0) PARO_TL(a, 8);
 #pragma unroll
       for (int t = 0; t < 8; ++t) {  // a5: rotations t = 1..L, Eq. 4 form, pre-update values
         if (t >= L_eff) break;
-        const uint32_t i0 = ixr[t] & 0xff, j0 = (ixr[t] >> 8) & 0xff;
-        const uint32_t i1 = (ixr[t] >> 16) & 0xff, j1 = ixr[t] >> 24;
 #pragma unroll
-        for (int b = 0; b < BT; ++b) {
-          float* sb = scr + b * 132;
-          const float a0 = sb[i0], b0 = sb[j0];
-          const float a1 = sb[i1], b1 = sb[j1];
-          sb[i0] = csr[t].x * a0 - csr[t].y * b0;
-          sb[j0] = csr[t].y * a0 + csr[t].x * b0;
-          sb[i1] = csr[t].z * a1 - csr[t].w * b1;
-          sb[j1] = csr[t].w * a1 + csr[t].z * b1;
+        for (int q = 0; q < NG; ++q) {
+          const uint32_t i0 = ixr[q][t] & 0xff, j0 = (ixr[q][t] >> 8) & 0xff;
+          const uint32_t i1 = (ixr[q][t] >> 16) & 0xff, j1 = ixr[q][t] >> 24;
+          const float4 c = csr[q][t];
+#pragma unroll
+          for (int b = 0; b < BT; ++b) {
+            float* sb = scr + (q * BT + b) * 132;
+            const float a0 = sb[i0], b0 = sb[j0];
+            const float a1 = sb[i1], b1 = sb[j1];
+            sb[i0] = c.x * a0 - c.y * b0;
+            sb[j0] = c.y * a0 + c.x * b0;
+            sb[i1] = c.z * a1 - c.w * b1;
+            sb[j1] = c.w * a1 + c.z * b1;
+          }
         }
         __syncwarp();
       }
@@ -342,36 +307,40 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
         q_rot += c - q0;
         q0 = c;
       }
-      if (threadIdx.x == 0 && gam == g0) PARO_TL(a, 6);
+      if (threadIdx.x == 0 && gams[0] == g0) PARO_TL(a, 6);
       if (CL > 1 && !cwaited) {
         cluster_wait();  // every CTA of the cluster is running and initialised: DSMEM is legal
         cwaited = true;
       }
 #pragma unroll
-      for (int b = 0; b < BT; ++b) {
-        const float2 v01 = lds_f2_a(scr_a + static_cast<uint32_t>(b * 132 + k0) * 4);
-        const float2 v89 = lds_f2_a(scr_a + static_cast<uint32_t>(b * 132 + k0 + 8) * 4);
-        const uint32_t p0 = pack_half2(v01.x, v01.y);
-        const uint32_t p1 = pack_half2(v89.x, v89.y);
-        // sum over the group of the fp16-rounded x' (the zero-point term uses exactly the
-        // values the tensor cores multiply)
-        float cs = half2_sum(p0) + half2_sum(p1);
+      for (int q = 0; q < NG; ++q) {
+        const int gam = gams[q];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
-        const uint32_t uo = u_addr + static_cast<uint32_t>(((gam * 4 + i4) * BT + b) * 64 + t4 * 16 + hf * 8);
-        const uint32_t so = s_addr + static_cast<uint32_t>((gam * 8 + b) * 4);
-        if (CL > 1) {
+        for (int b = 0; b < BT; ++b) {
+          const float2 v01 = lds_f2_a(scr_a + static_cast<uint32_t>((q * BT + b) * 132 + k0) * 4);
+          const float2 v89 = lds_f2_a(scr_a + static_cast<uint32_t>((q * BT + b) * 132 + k0 + 8) * 4);
+          const uint32_t p0 = pack_half2(v01.x, v01.y);
+          const uint32_t p1 = pack_half2(v89.x, v89.y);
+          // sum over the group of the fp16-rounded x' (the zero-point term uses exactly the
+          // values the tensor cores multiply)
+          float cs = half2_sum(p0) + half2_sum(p1);
 #pragma unroll
-          for (int r = 0; r < 8; ++r) {
-            if (r < CL) {
-              const uint32_t rb = mapa(bar_addr, r);
-              st_async_v2(mapa(uo, r), p0, p1, rb);
-              if (lane == 0) st_async_b32(mapa(so, r), __float_as_uint(cs), rb);
+          for (int o = 1; o < 32; o <<= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+          const uint32_t uo = u_addr + static_cast<uint32_t>(((gam * 4 + i4) * BT + b) * 64 + t4 * 16 + hf * 8);
+          const uint32_t so = s_addr + static_cast<uint32_t>((gam * 8 + b) * 4);
+          if (CL > 1) {
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+              if (r < CL) {
+                const uint32_t rb = mapa(bar_addr, r);
+                st_async_v2(mapa(uo, r), p0, p1, rb);
+                if (lane == 0) st_async_b32(mapa(so, r), __float_as_uint(cs), rb);
+              }
             }
+          } else {
+            *reinterpret_cast<uint2*>(ufr + (uo - u_addr)) = make_uint2(p0, p1);
+            if (lane == 0) xsum[gam * 8 + b] = cs;
           }
-        } else {
-          *reinterpret_cast<uint2*>(ufr + (uo - u_addr)) = make_uint2(p0, p1);
-          if (lane == 0) xsum[gam * 8 + b] = cs;
         }
       }
       __syncwarp();
@@ -380,10 +349,36 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
         q_out += c - q0;
         q0 = c;
       }
-      if (threadIdx.x == 0 && gam == g0) PARO_TL(a, 7);
+      if (threadIdx.x == 0 && gams[0] == g0) PARO_TL(a, 7);
+    };
+
+    // This warp's first two groups: both parameter sets are loaded into registers before the
+    // activations arrive (their L2 latency overlaps the activation copy), then both groups are
+    // transformed in lockstep.
+    const int gams[2] = {g0 + warp, g0 + warp + NW};
+    const int ng = gams[1] < g1 ? 2 : (gams[0] < g1 ? 1 : 0);
+    float4 cs2[2][8];
+    uint32_t ix2[2][8];
+    float4 sv2[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (q < ng) load_params(gams[q], cs2[q], ix2[q], sv2[q]);
+    if (ng > 0 && x_cols > 0) {
+      mbar_wait(xbar, 0);
+      if (threadIdx.x == 0) PARO_TL(a, 1);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(pfree);  // this warp no longer reads the staged parameters
+    if (ng == 2)
+      process(std::integral_constant<int, 2>{}, gams, cs2, ix2, sv2);
+    else if (ng == 1)
+      process(std::integral_constant<int, 1>{}, gams, cs2, ix2, sv2);
+    for (int gam = gams[1] + NW; gam < g1; gam += NW) {  // more than two rounds (large K, few CTAs)
+      float4 cs1[1][8];
+      uint32_t ix1[1][8];
+      float4 sv1[1];
+      load_params(gam, cs1[0], ix1[0], sv1[0]);
+      process(std::integral_constant<int, 1>{}, &gam, cs1, ix1, sv1);
+    }
+    if (a.debug) q0 = clock64();
     if (CL > 1) {
       if (!cwaited) cluster_wait();
       mbar_wait(xpbar, 0);  // every group's x' has arrived from its owner CTA
@@ -621,7 +616,8 @@ static const void* kernel_for(int BT, int threads) {
 #define PARO_KF(BT_)                                                                        \
   if (BT == BT_) {                                                                        \
     if (threads <= 288) return reinterpret_cast<const void*>(&paro_gemv_kernel<BT_, 288>); \
-    if (threads <= 544) return reinterpret_cast<const void*>(&paro_gemv_kernel<BT_, 544>); \
+    if (threads <= 512) return reinterpret_cast<const void*>(&paro_gemv_kernel<BT_, 512>); \
+    if (threads <= 640) return reinterpret_cast<const void*>(&paro_gemv_kernel<BT_, 640>); \
   }
   PARO_KF(1)
   PARO_KF(2)
@@ -671,8 +667,8 @@ static int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
-bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, int rotate, GemvConfig* cfg,
-               const char** why) {
+static bool plan_try(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, int rotate, int NW, int ctas_pref,
+                     int CL, int TPS_req, GemvConfig* cfg, const char** why) {
   GemvConfig c{};
   if (n_lin < 1 || n_lin > GEMV_MAX_LIN) {
     *why = "1..4 linears per decode launch";
@@ -692,15 +688,9 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
     L = std::max(L, Ls[i]);
   }
   const int G = static_cast<int>(K / GRP);
-  // 16 compute warps, 1 CTA / SM, clusters of 4, 32-tile stages by default (measured best on
-  // the bench's Llama-3-8B layer); PARO_NW / PARO_CTAS_PER_SM / PARO_CLUSTER / PARO_TPS override
-  int NW = std::max(1, std::min(16, env_int("PARO_NW", 16)));
-  int ctas_per_sm = env_int("PARO_CTAS_PER_SM", NW <= 8 ? 2 : 1) == 1 ? 1 : 2;
-  if (NW > 8) ctas_per_sm = 1;
-  int CL = env_int("PARO_CLUSTER", 4);
-  if (CL != 1 && CL != 2 && CL != 4 && CL != 8) CL = 8;
+  int ctas_per_sm = (NW <= 8 && ctas_pref == 2) ? 2 : 1;
   while (CL > 1 && CL > G) CL /= 2;
-  int TPS = std::max(1, std::min(64, env_int("PARO_TPS", 2 * NW)));
+  int TPS = std::max(1, std::min(64, TPS_req > 0 ? TPS_req : 2 * NW));
   TPS = std::max(NW, TPS / NW * NW);  // a multiple of NW: warp w's tiles are w, w + NW, ...
   c.NW = NW;
   c.CL = CL;
@@ -722,7 +712,10 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
   const uint32_t xs_bytes = align_up(static_cast<uint32_t>(G) * 8 * 4, 128);
   const int g_per = (G + CL - 1) / CL;
   const uint32_t x_bytes = align_up(static_cast<uint32_t>(B) * g_per * GRP * 2, 128);
-  const uint32_t scr_bytes = align_up(static_cast<uint32_t>(NW) * B * 132 * 4, 128);
+  // transform scratch of the warps that own groups (two groups in lockstep when g_per > NW)
+  a.scr_groups = g_per > NW ? 2 : 1;
+  const uint32_t scr_bytes =
+      align_up(static_cast<uint32_t>(std::min(NW, g_per)) * a.scr_groups * B * 132 * 4, 128);
   const uint32_t recv_bytes = align_up(static_cast<uint32_t>(std::max(1, CL - 1)) * TILE_ROWS * B * 4, 128);
   if (u_bytes > 64 * 1024) ctas_per_sm = 1;
   int budget = (smem_optin() + 1024) / ctas_per_sm - 2048;
@@ -774,7 +767,7 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
     a.off_recv = off;
     off += recv_bytes;
     a.off_bar = off;
-    off += 64 * 16;  // up to 60 stages x (full, empty) + 6 singles
+    off += 64 * 16;  // up to 60 stages x (full, empty) + 3 singles
     a.off_ring = align_up(off, 1024);
     const int64_t ring_avail = static_cast<int64_t>(budget) - a.off_ring;
     int S = static_cast<int>(ring_avail / a.slot_bytes);
@@ -784,25 +777,6 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
     if (S < 1) return false;
     a.S = S;
     a.smem_total = a.off_ring + static_cast<uint32_t>(S) * a.slot_bytes;
-    // stage the rotation parameters of this CTA's groups in shared memory: a dedicated
-    // region when it fits, else lend the last ring slots (refilled after phase 1)
-    a.param_slots = 0;
-    a.off_param = 0;
-    if (rotate && L > 0 && env_int("PARO_PSTAGE", 1)) {
-      const uint32_t pbytes = static_cast<uint32_t>(g_per) * 32 * L * 20 + static_cast<uint32_t>(g_per) * GRP * 4;
-      const int P = static_cast<int>((pbytes + a.slot_bytes - 1) / a.slot_bytes);
-      // lend the last ring slots (refilled once phase 1 is done) when that keeps >= 3 slots
-      // streaming weights from the start; else a dedicated region if it fits
-      if (P + 3 <= S && env_int("PARO_PDED", 0) == 0) {
-        a.param_slots = P;
-      } else if (static_cast<int64_t>(a.smem_total) + align_up(pbytes, 128) <= budget) {
-        a.param_slots = -1;
-        a.off_param = a.smem_total;
-        a.smem_total += align_up(pbytes, 128);
-      } else if (P < S) {
-        a.param_slots = P;
-      }
-    }
     return true;
   };
   int grid = device_sm_count() * ctas_per_sm / CL * CL;
@@ -827,10 +801,25 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
     return false;
   }
   if (env_int("PARO_PLAN_DEBUG", 0))
-    fprintf(stderr, "[paro gemv plan] B=%d n_lin=%d K=%lld grid=%d CL=%d NW=%d TPS=%d S=%d param_slots=%d R_max=%d smem=%u\n",
-            B, n_lin, static_cast<long long>(K), c.grid, CL, NW, TPS, a.S, a.param_slots, a.R_max, a.smem_total);
+    fprintf(stderr, "[paro gemv plan] B=%d n_lin=%d K=%lld grid=%d CL=%d NW=%d TPS=%d S=%d R_max=%d smem=%u\n", B,
+            n_lin, static_cast<long long>(K), c.grid, CL, NW, TPS, a.S, a.R_max, a.smem_total);
   *cfg = c;
   return true;
+}
+
+bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, int rotate, GemvConfig* cfg,
+               const char** why) {
+  // Default: 15 compute warps, 1 CTA / SM, clusters of 4, 2 tiles per warp per stage (measured
+  // best on the bench's Llama-3-8B layer); PARO_NW / PARO_CTAS_PER_SM / PARO_CLUSTER / PARO_TPS
+  // override.  Shapes whose shared-memory plan does not fit fall back to 8 warps.
+  const int NW = std::max(1, std::min(19, env_int("PARO_NW", 15)));
+  const int cps = env_int("PARO_CTAS_PER_SM", 2) == 1 ? 1 : 2;
+  int CL = env_int("PARO_CLUSTER", 4);
+  if (CL != 1 && CL != 2 && CL != 4 && CL != 8) CL = 4;
+  const int TPS = env_int("PARO_TPS", 0);
+  if (plan_try(B, n_lin, Ns, Ls, K, rotate, NW, cps, CL, TPS, cfg, why)) return true;
+  if (NW > 8 && plan_try(B, n_lin, Ns, Ls, K, rotate, 8, 2, CL, 0, cfg, why)) return true;
+  return plan_try(B, n_lin, Ns, Ls, K, rotate, 4, 1, CL, 0, cfg, why);
 }
 
 template <int BT, int T>
@@ -869,9 +858,13 @@ static cudaError_t launch_t(const GemvConfig& c, cudaStream_t st) {
 
 cudaError_t launch_gemv(const GemvConfig& c, cudaStream_t st) {
   if (c.a.B < 1 || c.a.B > c.BT) return cudaErrorInvalidValue;
-  const bool big = (c.NW + 1) * 32 > 288;
-#define PARO_LG(BT_) \
-  if (c.BT == BT_) return big ? launch_t<BT_, 544>(c, st) : launch_t<BT_, 288>(c, st);
+  const int threads = (c.NW + 1) * 32;
+#define PARO_LG(BT_)                                               \
+  if (c.BT == BT_) {                                               \
+    if (threads <= 288) return launch_t<BT_, 288>(c, st);          \
+    if (threads <= 512) return launch_t<BT_, 512>(c, st);          \
+    if (threads <= 640) return launch_t<BT_, 640>(c, st);          \
+  }
   PARO_LG(1)
   PARO_LG(2)
   PARO_LG(4)

@@ -43,9 +43,8 @@ struct GemvArgs {
   int skip_math;    // debug: stream the weights but skip the phase-2 math (timing only)
   int NW;           // compute warps
   int TPS;          // tiles per ring stage
+  int scr_groups;   // transform groups per warp in lockstep (1 or 2)
   int S;            // ring depth
-  int param_slots;  // ring slots lent to the staged rotation parameters (-1: dedicated region)
-  uint32_t off_param;
   int R_max;        // row blocks a CTA's tile range can touch
   uint32_t slot_bytes, sc_off, z_off;  // per-stage slot layout
   uint32_t off_u, off_xs, off_x, off_scr, off_part, off_recv, off_ring, off_bar, smem_total;

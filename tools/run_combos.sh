@@ -1,5 +1,7 @@
 #!/bin/bash
-# decode-kernel config sweep (graph timing of the bench's launch groups)
-for env in "PARO_NW=8 PARO_CLUSTER=8" "PARO_NW=8 PARO_CLUSTER=4" "PARO_NW=16 PARO_CLUSTER=4 PARO_TPS=32" "PARO_NW=16 PARO_CLUSTER=2 PARO_TPS=32"; do
-  echo "== $env"; env $env timeout 120 python tools/time_groups.py rot 0 2>&1
+for env in "PARO_NW=15" "PARO_NW=15 PARO_TPS=45"; do
+  echo "== $env"; env $env timeout 120 python tools/time_groups.py rot 1 2>&1
 done
+timeout 120 python tools/time_groups.py norot 1 2>&1
+timeout 60 python tools/timeline.py 4096 14336 rot 1 2>&1 | grep -v layer1
+timeout 60 python tools/timeline.py 4096 4096 rot 1 2>&1 | grep -v layer1

@@ -139,22 +139,18 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
 
   uint8_t* ufr = smem + a.off_u;                                  // x' fragments [G][4][BT][4][4] u32
   float* xsum = reinterpret_cast<float*>(smem + a.off_xs);        // sum of x' per (group, token) [G][8]
-  uint8_t* xs = smem + a.off_x;                                   // raw x slice [B][x_cols]
   float* part = reinterpret_cast<float*>(smem + a.off_part);      // [NW][R_max][32][BT]
   float* recv = reinterpret_cast<float*>(smem + a.off_recv);      // [CL-1][32][BT]
   uint8_t* ring = smem + a.off_ring;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.off_bar);
   uint64_t* empty = full + a.S;
-  uint64_t* xbar = empty + a.S;  // raw activations landed (bulk copy)
-  uint64_t* xpbar = xbar + 1;    // x' of all K landed (DSMEM st.async from the cluster)
+  uint64_t* xpbar = empty + a.S;  // x' of all K landed (DSMEM st.async from the cluster)
   uint64_t* rbar = xpbar + 1;    // partials of my last row block from later CTAs landed
 
   // groups whose transform this CTA computes
   const int g_per = (G + CL - 1) / CL;
   const int g0 = min(G, crank * g_per);
   const int g1 = min(G, g0 + g_per);
-  const int x_cols = (g1 - g0) * GRP;  // activation columns this CTA stages
-  const uint32_t x_row_bytes = static_cast<uint32_t>(x_cols) * 2;
   const int L_eff = a.rotate ? L : 0;
 
   if (threadIdx.x == 0) {
@@ -163,7 +159,6 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], NW);
     }
-    mbar_init(xbar, 1);
     mbar_init(xpbar, 1);
     mbar_init(rbar, 1);
     if (CL > 1) mbar_arrive_expect_tx(xpbar, static_cast<uint32_t>(BT) * (K * 2 + G * 4));
@@ -194,23 +189,22 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
       bulk_g2s(dst + a.z_off, d.zeros + T * TILE_ZERO_BYTES, nts * TILE_ZERO_BYTES, &full[slot], pol);
     };
     const int first = min(a.S, n_stages);
-    // Request order: the activations are latency-critical (the transform waits for them), so
-    // they go first -- except under PDL, where one weight stage is requested before waiting
-    // for the previous kernel (weights are never written by it: PARO_LINEAR_PDL's contract).
-    const int early = (a.pdl && !a.xfirst) ? min(1, first) : 0;
+    // Request order: the transform warps' parameter and activation loads first (they are on
+    // the critical path and would otherwise queue behind the whole GPU's ring fill), then the
+    // weight ring.  Under PDL a couple of stages go out before waiting for them: the weights
+    // are never written by the previous kernel (PARO_LINEAR_PDL's contract), and its tail
+    // leaves HBM idle.
+    const int early = a.pdl ? min(a.early_stages, first) : 0;
     if (lane == 0)
       for (int st = 0; st < early; ++st) issue(st, st);
-    if (a.pdl) pdl_wait();
+    if (a.xfirst) named_bar_sync(2, (NW + 1) * 32);  // the transform warps have issued their loads
     if (lane == 0) {
-      if (x_cols > 0) {
-        mbar_arrive_expect_tx(xbar, x_row_bytes * static_cast<uint32_t>(B));
-        for (int b = 0; b < B; ++b)
-          bulk_g2s_nohint(xs + static_cast<size_t>(b) * x_row_bytes,
-                          static_cast<const uint8_t*>(a.x) + (static_cast<int64_t>(b) * K + g0 * GRP) * 2,
-                          x_row_bytes, xbar);
+      int st0 = early;
+      if (a.stagger > 0) {  // experiment: let the first stage(s) land before the rest of the ring
+        for (; st0 < min(a.stagger, first); ++st0) issue(st0, st0);
+        mbar_wait(&full[0], 0);
       }
-      if (a.xfirst && x_cols > 0) mbar_wait(xbar, 0);  // debug: activations land first
-      for (int st = early; st < first; ++st) issue(st, st);
+      for (int st = st0; st < first; ++st) issue(st, st);
       for (int st = first; st < n_stages; ++st) {
         const int slot = st % a.S;
         mbar_wait(&empty[slot], ((st / a.S) & 1) ^ 1);  // stage st - S consumed by every warp
@@ -227,7 +221,6 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
     float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * (a.scr_groups * BT * 132);
     const uint32_t scr_a = smem_u32(scr);
     const uint32_t u_addr = smem_u32(ufr), s_addr = smem_u32(xsum), bar_addr = smem_u32(xpbar);
-    const uint32_t xs_a = smem_u32(xs);
     // output: lane (i4, t4, hf) writes B-fragment registers 4*i4 + 2*hf, +1 of fragment lane t4
     // (MMA m = 2*i4 + hf: channels (16m + 2t4, +1) and (16m + 2t4 + 8, +9))
     const int i4 = lane >> 3, t4 = (lane >> 1) & 3, hf = lane & 1;
@@ -249,19 +242,16 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
     };
     // x' = R_L ... R_1 diag(s) x of NG groups (in lockstep: independent dependency chains)
     // for the BT tokens, written as B fragments (+ per-token sums) into every CTA of the cluster
+    // xr: activations (channels 4*lane .. 4*lane + 3 of each group, straight from L2)
     auto process = [&](auto ngc, const int* gams, const float4 (*csr)[8], const uint32_t (*ixr)[8],
-                       const float4* sv) {
+                       const float4* sv, const uint2 (*xr)[BT]) {
       constexpr int NG = decltype(ngc)::value;
       if (a.debug) q0 = clock64();
 #pragma unroll
       for (int q = 0; q < NG; ++q) {
-        const int gl = gams[q] - g0;  // group index within this CTA's activation slice
 #pragma unroll
         for (int b = 0; b < BT; ++b) {  // a4: diag(s) x, lane = channels 4*lane .. 4*lane + 3
-          uint2 xv = make_uint2(0u, 0u);  // tokens >= B: x = 0 (x' = 0, never stored)
-          if (b < B)
-            xv = lds_u64_a(xs_a + static_cast<uint32_t>(b) * x_row_bytes +
-                           static_cast<uint32_t>(gl * GRP + 4 * lane) * 2);
+          const uint2 xv = xr[q][b];
           float2 f01, f23;
           if (a.x_bf16) {
             f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.x));
@@ -363,20 +353,34 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
 #pragma unroll
     for (int q = 0; q < 2; ++q)
       if (q < ng) load_params(gams[q], cs2[q], ix2[q], sv2[q]);
-    if (ng > 0 && x_cols > 0) {
-      mbar_wait(xbar, 0);
-      if (threadIdx.x == 0) PARO_TL(a, 1);
-    }
+    if (ng > 0 && a.pdl) pdl_wait();  // x may be written by the previous kernel on the stream
+    // activations of the (up to two) groups -> registers, then let the producer stream weights
+    uint2 xr2[2][BT];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int b = 0; b < BT; ++b)
+        xr2[q][b] = (q < ng && b < B) ? __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(a.x) +
+                                                                             (static_cast<int64_t>(b) * K + gams[q] * GRP + 4 * lane) * 2))
+                                      : make_uint2(0u, 0u);  // tokens >= B: x = 0 (x' = 0, never stored)
+    if (a.xfirst) named_bar_arrive(2, (NW + 1) * 32);
+    if (threadIdx.x == 0) PARO_TL(a, 1);
     if (ng == 2)
-      process(std::integral_constant<int, 2>{}, gams, cs2, ix2, sv2);
+      process(std::integral_constant<int, 2>{}, gams, cs2, ix2, sv2, xr2);
     else if (ng == 1)
-      process(std::integral_constant<int, 1>{}, gams, cs2, ix2, sv2);
+      process(std::integral_constant<int, 1>{}, gams, cs2, ix2, sv2, xr2);
     for (int gam = gams[1] + NW; gam < g1; gam += NW) {  // more than two rounds (large K, few CTAs)
       float4 cs1[1][8];
       uint32_t ix1[1][8];
       float4 sv1[1];
+      uint2 xr1[1][BT];
       load_params(gam, cs1[0], ix1[0], sv1[0]);
-      process(std::integral_constant<int, 1>{}, &gam, cs1, ix1, sv1);
+#pragma unroll
+      for (int b = 0; b < BT; ++b)
+        xr1[0][b] = b < B ? __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(a.x) +
+                                                                 (static_cast<int64_t>(b) * K + gam * GRP + 4 * lane) * 2))
+                          : make_uint2(0u, 0u);
+      process(std::integral_constant<int, 1>{}, &gam, cs1, ix1, sv1, xr1);
     }
     if (a.debug) q0 = clock64();
     if (CL > 1) {
@@ -499,8 +503,9 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
         const float zq = static_cast<float>((zw >> (4 * q)) & 15u);
         const int h = q >> 1, e = (q & 1) * 2;
         acc[4 * h + e] = fmaf(Sr[q], fmaf(fmaf(D16[h][e], 0.0625f, D1[h][e]), TWO_P24, -zq * X2.x), acc[4 * h + e]);
-        acc[4 * h + e + 1] =
-            fmaf(Sr[q], fmaf(fmaf(D16[h][e + 1], 0.0625f, D1[h][e + 1]), TWO_P24, -zq * X2.y), acc[4 * h + e + 1]);
+        if (BT > 1)  // column 2t + 1 holds a token only when BT > 1
+          acc[4 * h + e + 1] =
+              fmaf(Sr[q], fmaf(fmaf(D16[h][e + 1], 0.0625f, D1[h][e + 1]), TWO_P24, -zq * X2.y), acc[4 * h + e + 1]);
       }
       g += NW;
       while (g >= G) {
@@ -694,7 +699,9 @@ static bool plan_try(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t
   TPS = std::max(NW, TPS / NW * NW);  // a multiple of NW: warp w's tiles are w, w + NW, ...
   c.NW = NW;
   c.CL = CL;
-  c.a.xfirst = env_int("PARO_XFIRST", 0);
+  c.a.xfirst = env_int("PARO_XFIRST", 1);           // weights wait until the transform loads are out
+  c.a.early_stages = env_int("PARO_EARLY_STAGES", 2);  // under PDL: stages requested before that
+  c.a.stagger = env_int("PARO_STAGGER", 1);  // first stage lands before the rest of the ring is requested
   c.a.skip_math = env_int("PARO_SKIP_MATH", 0);  // debug: stream the weights, skip the tile math
   GemvArgs& a = c.a;
   a.n_lin = n_lin;
@@ -711,7 +718,6 @@ static bool plan_try(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t
   const uint32_t u_bytes = align_up(static_cast<uint32_t>(B) * K * 2, 128);
   const uint32_t xs_bytes = align_up(static_cast<uint32_t>(G) * 8 * 4, 128);
   const int g_per = (G + CL - 1) / CL;
-  const uint32_t x_bytes = align_up(static_cast<uint32_t>(B) * g_per * GRP * 2, 128);
   // transform scratch of the warps that own groups (two groups in lockstep when g_per > NW)
   a.scr_groups = g_per > NW ? 2 : 1;
   const uint32_t scr_bytes =
@@ -758,8 +764,6 @@ static bool plan_try(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t
     off += u_bytes;
     a.off_xs = off;
     off += xs_bytes;
-    a.off_x = off;
-    off += x_bytes;
     a.off_scr = off;
     off += scr_bytes;
     a.off_part = off;
@@ -814,7 +818,11 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
   // override.  Shapes whose shared-memory plan does not fit fall back to 8 warps.
   const int NW = std::max(1, std::min(19, env_int("PARO_NW", 15)));
   const int cps = env_int("PARO_CTAS_PER_SM", 2) == 1 ? 1 : 2;
-  int CL = env_int("PARO_CLUSTER", 4);
+  // clusters of 4 share the transform 4 ways; very large launches with few groups (gate/up at
+  // K = 4096) prefer pairs, which tile all 148 SMs (clusters of 4 leave 16 idle)
+  int64_t tiles = 0;
+  for (int i = 0; i < n_lin; ++i) tiles += (Ns[i] + TILE_ROWS - 1) / TILE_ROWS * (K / GRP);
+  int CL = env_int("PARO_CLUSTER", (K / GRP <= 32 && tiles >= 150LL * device_sm_count()) ? 2 : 4);
   if (CL != 1 && CL != 2 && CL != 4 && CL != 8) CL = 4;
   const int TPS = env_int("PARO_TPS", 0);
   if (plan_try(B, n_lin, Ns, Ls, K, rotate, NW, cps, CL, TPS, cfg, why)) return true;

@@ -39,7 +39,9 @@ struct GemvArgs {
   int rotate;
   int pdl;
   int debug;        // record a per-CTA event timeline (g_paro_timeline)
-  int xfirst;       // producer waits for x / parameters before streaming weights
+  int xfirst;       // producer waits until the transform warps have issued their loads
+  int early_stages; // under PDL: weight stages requested before that
+  int stagger;      // experiment: stages issued (and the first awaited) before the rest of the ring
   int skip_math;    // debug: stream the weights but skip the phase-2 math (timing only)
   int NW;           // compute warps
   int TPS;          // tiles per ring stage
@@ -47,7 +49,7 @@ struct GemvArgs {
   int S;            // ring depth
   int R_max;        // row blocks a CTA's tile range can touch
   uint32_t slot_bytes, sc_off, z_off;  // per-stage slot layout
-  uint32_t off_u, off_xs, off_x, off_scr, off_part, off_recv, off_ring, off_bar, smem_total;
+  uint32_t off_u, off_xs, off_scr, off_part, off_recv, off_ring, off_bar, smem_total;
 };
 
 struct GemvConfig {

@@ -301,6 +301,48 @@ def run_paro(args):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "api": "paper_2511_10645_b200.paro_linear per linear (ctypes), pinned host x/y"}
 
+    # prefill (SURVEY.md 8(d) "also prefill TFLOPS"): the same packed linears at 2048 tokens
+    # through paro_linear's tcgen05 path (transform pre-stage + GEMM), one CUDA graph per linear
+    prefill = None
+    if world == 1 and not args.no_prefill:
+        Bp = 2048
+        tot_flop, tot_us, per = 0.0, 0.0, {}
+        with torch.cuda.stream(stream):
+            for name, N, K, packed in pool[0]:
+                xp = torch.randn((Bp, K), generator=g, device=dev).to(torch.float16)
+                yp = torch.empty((Bp, N), dtype=torch.float16, device=dev)
+                wsp = torch.empty(max(1, paro.paro_linear_workspace(Bp, N, K)), dtype=torch.uint8, device=dev)
+                for _ in range(2):
+                    paro.paro_linear(xp, packed, y=yp, workspace=wsp, stream=stream)
+                reps = 10
+                gp = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gp, stream=stream):
+                    for _ in range(reps):
+                        paro.paro_linear(xp, packed, y=yp, workspace=wsp, stream=stream)
+                gp.replay()
+                stream.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                gp.replay()
+                e1.record(stream)
+                e1.synchronize()
+                us = e0.elapsed_time(e1) / reps * 1e3
+                fl = 2.0 * Bp * N * K
+                tot_flop += fl
+                tot_us += us
+                per[name] = {"us": round(us, 2), "TFLOPs": round(fl / us / 1e6, 1)}
+                del xp, yp, wsp, gp
+        tpeak = float(load_peaks().get("bf16_tflops", 1649.0))
+        prefill = {"tokens": Bp, "TFLOPs": round(tot_flop / tot_us / 1e6, 1), "us_per_layer": round(tot_us, 1),
+                   "peak_TFLOPs": tpeak, "frac": round(tot_flop / tot_us / 1e6 / tpeak, 4), "per_linear": per,
+                   "def": "2*B*N*K flop per linear / device time of transform pre-stage + tcgen05 GEMM"}
+
+    # C1 (launch-latency bound) and C3 (Qwen3-4B 36-layer stack, B = 1 and 16): SURVEY.md 8(d)
+    extra = {}
+    if world == 1 and not args.no_extra:
+        extra["c1"] = measure_c1(torch, paro, dev, stream)
+        extra["c3_qwen3_4b_stack"] = measure_qwen_stack(torch, paro, dev, stream, (1, 16))
+
     if comm is not None:
         torch.cuda.synchronize()
         paro.paro_comm_destroy(comm)
@@ -331,7 +373,8 @@ def run_paro(args):
                      "kernel": "paro_gemv_kernel (all launches of the step)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not peaks.get("_fallback") else "fallback 6.65 TB/s",
                      "achieved_def": "algorithmic bytes per step / device time per step (all GEMV launches, gaps included)"},
-        "clocks": clocks, "e2e": e2e, "gpu_launches": (4 if world == 1 else 14) * args.steps,
+        "clocks": clocks, "e2e": e2e, "prefill": prefill, **extra,
+        "gpu_launches": (4 if world == 1 else 14) * args.steps,
         "gpu_launches_note": ("4 paro_gemv_kernel launches per step (q/k/v and gate/up fused by shared input)"
                               if world == 1 else "7 paro_gemv_kernel + 7 ncclAllGather launches per step"),
     }
@@ -346,6 +389,71 @@ def run_paro(args):
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def graph_time_us(torch, stream, fn, reps):
+    """Device time per call of fn() captured reps times in one CUDA graph (CUDA events)."""
+    with torch.cuda.stream(stream):
+        fn()
+        fn()
+        stream.synchronize()
+        gph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gph, stream=stream):
+            for _ in range(reps):
+                fn()
+        gph.replay()
+        stream.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        gph.replay()
+        e1.record(stream)
+        e1.synchronize()
+    return e0.elapsed_time(e1) / reps * 1e3
+
+
+def measure_c1(torch, paro, dev, stream):
+    """configs[0]: one K = N = 256 linear, bs=1 (launch-latency bound: report us)."""
+    p = synth.make_problem(256, 256, 1, seed=7)
+    t = {k: torch.from_numpy(p[k]).to(dev) for k in ("W", "s", "theta", "pairs", "x")}
+    packed = paro.paro_pack(t["W"], t["s"], t["theta"], t["pairs"])
+    y = torch.empty((1, 256), dtype=torch.float16, device=dev)
+    res = {}
+    for tag, fl in (("rot", 0), ("norot", paro.PARO_LINEAR_NO_ROTATION)):
+        res[tag] = graph_time_us(torch, stream, lambda: paro.paro_linear(t["x"], packed, y=y, flags=fl, stream=stream),
+                                 200)
+    return {"us": round(res["rot"], 3), "us_norot": round(res["norot"], 3),
+            "rot_overhead": round(res["rot"] / res["norot"] - 1.0, 4),
+            "def": "device time per paro_linear call, 200 calls in one CUDA graph (weights L2-resident)"}
+
+
+def measure_qwen_stack(torch, paro, dev, stream, batches):
+    """configs[2]: the Qwen3-4B decode stack (36 layers x 7 linears, each with its own
+    transform; q/k/v and gate/up share their input: 4 launches per layer), one CUDA graph
+    per step with PDL; 1.9 GB of packed weights, so every step streams from HBM."""
+    shapes = synth.QWEN3_4B_LAYER
+    pool = build_layer_pool(torch, paro, shapes, 0, 1, synth.QWEN3_4B_LAYERS, dev, seed=11)
+    groups = [["q_proj", "k_proj", "v_proj"], ["o_proj"], ["gate_proj", "up_proj"], ["down_proj"]]
+    step_bytes = sum(algorithmic_bytes(N, K, 1)[0] for N, K in shapes.values()) * synth.QWEN3_4B_LAYERS
+    out = {"layers": synth.QWEN3_4B_LAYERS, "weight_bytes": int(step_bytes)}
+    for B in batches:
+        g = torch.Generator(device=dev).manual_seed(5 + B)
+        xs = {K: torch.randn((B, K), generator=g, device=dev).to(torch.float16) for _, K in shapes.values()}
+        ys = {n: torch.empty((B, N), dtype=torch.float16, device=dev) for n, (N, K) in shapes.items()}
+        ws = torch.empty(1 << 20, dtype=torch.uint8, device=dev)
+
+        def step():
+            for layer in pool:
+                lin = {name: packed for name, N, K, packed in layer}
+                for grp in groups:
+                    K = shapes[grp[0]][1]
+                    paro.paro_linear_multi(xs[K], [lin[n] for n in grp], y=[ys[n] for n in grp],
+                                           flags=paro.PARO_LINEAR_PDL, workspace=ws, stream=stream)
+
+        us = graph_time_us(torch, stream, step, 3)
+        out[f"bs{B}"] = {"us_per_step": round(us, 1), "GBps": round(step_bytes / us / 1e3, 1)}
+    del pool
+    torch.cuda.empty_cache()
+    return out
 
 
 # ----------------------------------------------------------------------------- the oracle as baseline
@@ -425,6 +533,8 @@ def main():
     ap.add_argument("--impl", default="paro", choices=["paro", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--load-s", type=float, default=1.0)
+    ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C1 / Qwen3-4B stack lines")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -44,7 +44,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
         op = os.path.join(BUILD, src.replace(".cu", ".o"))
         objs.append(op)
         if force or _stale(op, [sp] + hdrs + [__file__]):
-            cmd = [nvcc(), *ARCH, *COMMON, *PER_FILE.get(src, []), "-c", sp, "-o", op]
+            extra = os.environ.get("PARO_NVCC_EXTRA", "").split()  # experiments only (e.g. -DPARO_MBAR_SPIN=1)
+            cmd = [nvcc(), *ARCH, *COMMON, *PER_FILE.get(src, []), *extra, "-c", sp, "-o", op]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
                 print(" ".join(cmd), flush=True)

@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
       if (a.stagger > 0) {  // experiment: let the first stage(s) land before the rest of the ring
         for (; st0 < min(a.stagger, first); ++st0) issue(st0, st0);
         mbar_wait(&full[0], 0);
+        PARO_TL(a, 9);  // debug: the first stage landed (producer view)
       }
       for (int st = st0; st < first; ++st) issue(st, st);
       for (int st = first; st < n_stages; ++st) {
@@ -538,8 +539,13 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
   for (int idx = threadIdx.x; idx < n_out; idx += NW * 32) {
     const int rho = idx / (TR * BT), r = (idx / BT) % TR, b = idx % BT;
     if (b >= B) continue;
-    float sum = 0.f;
-    for (int w = 0; w < NW; ++w) sum += part[((static_cast<size_t>(w) * a.R_max + rho) * TR + r) * BT + b];
+    // fixed-order sum over the warps (four independent chains, then combined: deterministic)
+    const float* pp = part + (static_cast<size_t>(rho) * TR + r) * BT + b;
+    const size_t wstride = static_cast<size_t>(a.R_max) * TR * BT;
+    float s4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+    for (int w = 0; w < NW; ++w) s4[w & 3] += pp[w * wstride];
+    float sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
     const int rg = rho_first + rho;
     if (rho == 0 && !own_first) {
       // the block started in an earlier CTA: push this partial to it (recv slot crank - owner - 1)
@@ -673,7 +679,7 @@ static int env_int(const char* name, int dflt) {
 }
 
 static bool plan_try(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, int rotate, int NW, int ctas_pref,
-                     int CL, int TPS_req, GemvConfig* cfg, const char** why) {
+                     int CL, int TPS_req, int min_stages, GemvConfig* cfg, const char** why) {
   GemvConfig c{};
   if (n_lin < 1 || n_lin > GEMV_MAX_LIN) {
     *why = "1..4 linears per decode launch";
@@ -778,7 +784,7 @@ static bool plan_try(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t
     const int stages_needed = std::max(1, (max_tiles_cta + TPS - 1) / TPS);
     if (S > stages_needed) S = stages_needed;
     if (S > 60) S = 60;
-    if (S < 1) return false;
+    if (S < std::max(1, std::min(min_stages, stages_needed))) return false;
     a.S = S;
     a.smem_total = a.off_ring + static_cast<uint32_t>(S) * a.slot_bytes;
     return true;
@@ -825,9 +831,12 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
   int CL = env_int("PARO_CLUSTER", (K / GRP <= 32 && tiles >= 150LL * device_sm_count()) ? 2 : 4);
   if (CL != 1 && CL != 2 && CL != 4 && CL != 8) CL = 4;
   const int TPS = env_int("PARO_TPS", 0);
-  if (plan_try(B, n_lin, Ns, Ls, K, rotate, NW, cps, CL, TPS, cfg, why)) return true;
-  if (NW > 8 && plan_try(B, n_lin, Ns, Ls, K, rotate, 8, 2, CL, 0, cfg, why)) return true;
-  return plan_try(B, n_lin, Ns, Ls, K, rotate, 4, 1, CL, 0, cfg, why);
+  // prefer >= 2 ring stages (large token tiles eat shared memory: halve the stage first)
+  if (plan_try(B, n_lin, Ns, Ls, K, rotate, NW, cps, CL, TPS, 2, cfg, why)) return true;
+  if (plan_try(B, n_lin, Ns, Ls, K, rotate, NW, cps, CL, NW, 2, cfg, why)) return true;
+  if (plan_try(B, n_lin, Ns, Ls, K, rotate, NW, cps, CL, NW, 1, cfg, why)) return true;
+  if (NW > 8 && plan_try(B, n_lin, Ns, Ls, K, rotate, 8, 2, CL, 0, 1, cfg, why)) return true;
+  return plan_try(B, n_lin, Ns, Ls, K, rotate, 4, 1, CL, 0, 1, cfg, why);
 }
 
 template <int BT, int T>

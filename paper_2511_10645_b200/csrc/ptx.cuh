@@ -26,6 +26,17 @@ PARO_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
 PARO_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+PARO_DEV bool mbar_try_wait_spin(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 PARO_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   // suspend-time hint: the waiting warp is parked by the hardware until the phase completes
@@ -40,8 +51,13 @@ PARO_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 PARO_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if PARO_MBAR_SPIN
+  while (!mbar_try_wait_spin(bar, parity)) {
+  }
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 
 // ---------------------------------------------------------------- bulk async copy (TMA engine, 1-D)

@@ -1,3 +1,3 @@
 #!/bin/bash
-timeout 120 python tools/time_groups.py rot 1 2>&1
-timeout 120 python tools/time_groups.py norot 1 2>&1
+for b in 1 8; do echo "== B=$b"; TL_B=$b timeout 60 python tools/timeline.py 4096 4096 rot 1 2>&1; done
+timeout 120 python tools/time_groups.py rot 1

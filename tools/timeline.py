@@ -18,8 +18,9 @@ p = synth.make_problem(8, K, 1, seed=1)
 s, th, pr = (torch.from_numpy(p[k]).to(dev) for k in ("s", "theta", "pairs"))
 pks = [[paro.paro_pack((torch.randn(N, K, device=dev) * 0.02).half(), s, th, pr) for _ in range(nlin)]
        for _ in range(2)]
-x = torch.randn(1, K, device=dev).half()
-ys = [torch.empty(1, N, device=dev, dtype=torch.half) for _ in range(nlin)]
+Bt = int(os.environ.get("TL_B", "1"))
+x = torch.randn(Bt, K, device=dev).half()
+ys = [torch.empty(Bt, N, device=dev, dtype=torch.half) for _ in range(nlin)]
 fl = paro.PARO_LINEAR_NO_ROTATION if mode == "norot" else 0
 lib = paro._lib
 lib.paro_debug_read_timeline.argtypes = [ctypes.c_void_p, ctypes.c_int]
@@ -35,7 +36,7 @@ live = t[:, 0] > 0
 t = t[live]
 t0 = t[:, 0].min()
 rel = (t - t0) / 1000.0
-names = ["start", "x_arrived", "transform_done", "stage0_ready", "loop_done", "end", "w0_layers_done", "w0_item_out", "w0_layers_start", "w0_layer1_done", "reach_last_stage", "last_stage_landed"]
+names = ["start", "x_arrived", "transform_done", "stage0_ready", "loop_done", "end", "w0_layers_done", "w0_item_out", "w0_layers_start", "stage0_landed(producer)", "reach_last_stage", "last_stage_landed"]
 print(f"{mode} N={N}x{nlin} K={K}: {live.sum()} CTAs; us relative to first CTA start")
 for i, n in enumerate(names):
     col = rel[:, i]

@@ -1,4 +1,5 @@
-"""Per-CTA event timeline of one decode launch (internal debug flag 0x100).
+"""Per-CTA event timeline of one decode launch (internal debug flag 0x100; needs a library built with
+PARO_NVCC_EXTRA=-DPARO_ENABLE_DEBUG=1).
 argv: N K (rot|norot) [graph_prev=1]"""
 import ctypes
 import os

@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
     if (a.xfirst) named_bar_sync(2, (NW + 1) * 32);  // the transform warps have issued their loads
     if (lane == 0) {
       int st0 = early;
-      if (a.stagger > 0) {  // experiment: let the first stage(s) land before the rest of the ring
+      if (a.stagger > 0 && n_stages > a.S) {  // the ring will be refilled: let the first stage(s) land first
         for (; st0 < min(a.stagger, first); ++st0) issue(st0, st0);
         mbar_wait(&full[0], 0);
         PARO_TL(a, 9);  // debug: the first stage landed (producer view)
@@ -324,13 +324,11 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
           const uint32_t uo = u_addr + static_cast<uint32_t>(((gam * 4 + i4) * BT + b) * 64 + t4 * 16 + hf * 8);
           const uint32_t so = s_addr + static_cast<uint32_t>((gam * 8 + b) * 4);
           if (CL > 1) {
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-              if (r < CL) {
-                const uint32_t rb = mapa(bar_addr, r);
-                st_async_v2(mapa(uo, r), p0, p1, rb);
-                if (lane == 0) st_async_b32(mapa(so, r), __float_as_uint(cs), rb);
-              }
+#pragma unroll 1
+            for (int r = 0; r < CL; ++r) {  // not unrolled: small code (instruction cache)
+              const uint32_t rb = mapa(bar_addr, r);
+              st_async_v2(mapa(uo, r), p0, p1, rb);
+              if (lane == 0) st_async_b32(mapa(so, r), __float_as_uint(cs), rb);
             }
           } else {
             *reinterpret_cast<uint2*>(ufr + (uo - u_addr)) = make_uint2(p0, p1);
@@ -370,22 +368,29 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
                                       : make_uint2(0u, 0u);  // tokens >= B: x = 0 (x' = 0, never stored)
     if (a.xfirst) named_bar_arrive(2, (NW + 1) * 32);
     if (threadIdx.x == 0) PARO_TL(a, 1);
-    if (ng == 2)
-      process(std::integral_constant<int, 2>{}, gams, cs2, ix2, sv2, xr2);
-    else if (ng == 1)
-      process(std::integral_constant<int, 1>{}, gams, cs2, ix2, sv2, xr2);
-    for (int gam = gams[1] + NW; gam < g1; gam += NW) {  // more than two rounds (large K, few CTAs)
-      float4 cs1[1][8];
-      uint32_t ix1[1][8];
-      float4 sv1[1];
-      uint2 xr1[1][BT];
-      load_params(gam, cs1[0], ix1[0], sv1[0]);
+    // rounds of (up to) two groups; the parameters / activations of later rounds (large K,
+    // few CTAs per cluster) are loaded at the top of their round.  One call site per group
+    // count keeps a single copy of each transform instance (instruction-cache footprint).
+    for (int r = 0;; ++r) {
+      int gr[2] = {gams[0] + 2 * r * NW, gams[1] + 2 * r * NW};
+      const int nr = gr[1] < g1 ? 2 : (gr[0] < g1 ? 1 : 0);
+      if (nr == 0) break;
+      if (r > 0) {
 #pragma unroll
-      for (int b = 0; b < BT; ++b)
-        xr1[0][b] = b < B ? __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(a.x) +
-                                                                 (static_cast<int64_t>(b) * K + gam * GRP + 4 * lane) * 2))
-                          : make_uint2(0u, 0u);
-      process(std::integral_constant<int, 1>{}, &gam, cs1, ix1, sv1, xr1);
+        for (int q = 0; q < 2; ++q) {
+          if (q < nr) load_params(gr[q], cs2[q], ix2[q], sv2[q]);
+#pragma unroll
+          for (int b = 0; b < BT; ++b)
+            xr2[q][b] = (q < nr && b < B)
+                            ? __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(a.x) +
+                                                                   (static_cast<int64_t>(b) * K + gr[q] * GRP + 4 * lane) * 2))
+                            : make_uint2(0u, 0u);
+        }
+      }
+      if (nr == 2)
+        process(std::integral_constant<int, 2>{}, gr, cs2, ix2, sv2, xr2);
+      else
+        process(std::integral_constant<int, 1>{}, gr, cs2, ix2, sv2, xr2);
     }
     if (PARO_DBG(a)) q0 = clock64();
     if (CL > 1) {

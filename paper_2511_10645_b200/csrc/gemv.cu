@@ -199,23 +199,20 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
     // are never written by the previous kernel (PARO_LINEAR_PDL's contract), and its tail
     // leaves HBM idle.
     const int early = a.pdl ? min(a.early_stages, first) : 0;
-    if (lane == 0)
-      for (int st = 0; st < early; ++st) issue(st, st);
-    if (a.xfirst) named_bar_sync(2, (NW + 1) * 32);  // the transform warps have issued their loads
-    if (lane == 0) {
-      int st0 = early;
-      if (a.stagger > 0 && n_stages > a.S) {  // the ring will be refilled: let the first stage(s) land first
-        for (; st0 < min(a.stagger, first); ++st0) issue(st0, st0);
-        mbar_wait(&full[0], 0);
-        PARO_TL(a, 9);  // debug: the first stage landed (producer view)
+    // when the ring will be refilled, the first stage lands before the rest is requested
+    const int stag = (a.stagger > 0 && n_stages > a.S) ? max(early, min(a.stagger, first)) : -1;
+    bool synced = !a.xfirst;
+    for (int st = 0; st < n_stages; ++st) {  // one issue site (small code: instruction cache)
+      if (!synced && st >= early) {
+        named_bar_sync(2, (NW + 1) * 32);  // the transform warps have issued their loads
+        synced = true;
       }
-      for (int st = st0; st < first; ++st) issue(st, st);
-      for (int st = first; st < n_stages; ++st) {
-        const int slot = st % a.S;
-        mbar_wait(&empty[slot], ((st / a.S) & 1) ^ 1);  // stage st - S consumed by every warp
-        issue(st, slot);
-      }
+      if (st == stag) mbar_wait(&full[0], 0);
+      const int slot = st % a.S;
+      if (st >= a.S) mbar_wait(&empty[slot], ((st / a.S) & 1) ^ 1);  // stage st - S consumed by every warp
+      if (lane == 0) issue(st, slot);
     }
+    if (!synced) named_bar_sync(2, (NW + 1) * 32);
     __syncwarp();
     if (CL > 1) cluster_wait();
     return;
@@ -444,7 +441,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
   unsigned long long c_wait = 0, c_work = 0, c_t = PARO_DBG(a) ? clock64() : 0;
   for (int st = 0; st < n_stages; ++st) {
     const int slot = st % a.S;
-    if (st == n_stages - 1 && threadIdx.x == 0) PARO_TL(a, 10);
+    if (st == 0 && threadIdx.x == 0) PARO_TL(a, 10);  // debug: reached the first stage wait
     mbar_wait(&full[slot], (st / a.S) & 1);
     if (PARO_DBG(a)) {
       const unsigned long long c = clock64();

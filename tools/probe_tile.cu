@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(480, 1) ktile(float* out, unsigned long long* 
       const uint4 v = lds128_a(xa + ii * 64);
       bf[4 * ii] = v.x; bf[4 * ii + 1] = v.y; bf[4 * ii + 2] = v.z; bf[4 * ii + 3] = v.w;
     }
-    if (V < 2) {
+    if (V < 2 || V == 3) {
       float D1[2][4], D16[2][4];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -58,17 +58,25 @@ __global__ void __launch_bounds__(480, 1) ktile(float* out, unsigned long long* 
         const uint32_t w1[4] = {w[2 * h + 1].x, w[2 * h + 1].y, w[2 * h + 1].z, w[2 * h + 1].w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const uint32_t x = w0[j], y = w1[j], x8 = x >> 8, y8 = y >> 8;
-          if (j == 0) {
-            mma_16816_z(D1[h], x & 0x000F000Fu, y & 0x000F000Fu, x8 & 0x000F000Fu, y8 & 0x000F000Fu, bf[0], bf[1]);
-            mma_16816_z(D16[h], x & 0x00F000F0u, y & 0x00F000F0u, x8 & 0x00F000F0u, y8 & 0x00F000F0u, bf[2], bf[3]);
+          const uint32_t x = w0[j], y = w1[j];
+          uint32_t x0, y0, x8, y8, x1, y1, x9, y9;
+          x0 = x & 0x000F000Fu; y0 = y & 0x000F000Fu; x1 = x & 0x00F000F0u; y1 = y & 0x00F000F0u;
+          if (V == 3) {  // upper nibbles: AND on the ALU pipe, >> 8 as IMAD.HI on the FMA pipe
+            x8 = __umulhi(x & 0x0F000F00u, 1u << 24); y8 = __umulhi(y & 0x0F000F00u, 1u << 24);
+            x9 = __umulhi(x & 0xF000F000u, 1u << 24); y9 = __umulhi(y & 0xF000F000u, 1u << 24);
           } else {
-            mma_16816(D1[h], x & 0x000F000Fu, y & 0x000F000Fu, x8 & 0x000F000Fu, y8 & 0x000F000Fu, bf[4 * j], bf[4 * j + 1]);
-            mma_16816(D16[h], x & 0x00F000F0u, y & 0x00F000F0u, x8 & 0x00F000F0u, y8 & 0x00F000F0u, bf[4 * j + 2], bf[4 * j + 3]);
+            x8 = (x >> 8) & 0x000F000Fu; y8 = (y >> 8) & 0x000F000Fu; x9 = (x >> 8) & 0x00F000F0u; y9 = (y >> 8) & 0x00F000F0u;
+          }
+          if (j == 0) {
+            mma_16816_z(D1[h], x0, y0, x8, y8, bf[0], bf[1]);
+            mma_16816_z(D16[h], x1, y1, x9, y9, bf[2], bf[3]);
+          } else {
+            mma_16816(D1[h], x0, y0, x8, y8, bf[4 * j], bf[4 * j + 1]);
+            mma_16816(D16[h], x1, y1, x9, y9, bf[4 * j + 2], bf[4 * j + 3]);
           }
         }
       }
-      if (V == 0) {
+      if (V == 0 || V == 3) {
         const uint2 sp = lds_u64_a(sbase + i * 64 + gq * 8);
         const uint32_t zw = lds_u16z_a(zbase + i * 16 + gq * 2);
         const float2 Sa = __half22float2(*reinterpret_cast<const __half2*>(&sp.x));
@@ -123,13 +131,14 @@ int main() {
   float* o; unsigned long long* cyc; cudaMalloc(&o, 1 << 22); cudaMalloc(&cyc, 8 * 148 * 32);
   const int smem = 65536 + 8192 + 2048 + 512 + 1024;
   const int ntiles = 15 * 64;
-  for (int v = 0; v < 3; ++v) {
+  for (int v = 0; v < 4; ++v) {
     for (int nw = 8; nw <= 15; nw += 7) {
       unsigned long long h[32];
       for (int rep = 0; rep < 2; ++rep) {
         if (v == 0) { cudaFuncSetAttribute(ktile<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); ktile<0><<<148, nw * 32, smem>>>(o, cyc, ntiles); }
         if (v == 1) { cudaFuncSetAttribute(ktile<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); ktile<1><<<148, nw * 32, smem>>>(o, cyc, ntiles); }
         if (v == 2) { cudaFuncSetAttribute(ktile<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); ktile<2><<<148, nw * 32, smem>>>(o, cyc, ntiles); }
+        if (v == 3) { cudaFuncSetAttribute(ktile<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); ktile<3><<<148, nw * 32, smem>>>(o, cyc, ntiles); }
         cudaDeviceSynchronize();
       }
       cudaMemcpy(h, cyc, 8 * 32, cudaMemcpyDeviceToHost);

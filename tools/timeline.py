@@ -37,7 +37,7 @@ live = t[:, 0] > 0
 t = t[live]
 t0 = t[:, 0].min()
 rel = (t - t0) / 1000.0
-names = ["start", "x_arrived", "transform_done", "stage0_ready", "loop_done", "end", "w0_layers_done", "w0_item_out", "w0_layers_start", "stage0_landed(producer)", "reach_last_stage", "last_stage_landed"]
+names = ["start", "x_arrived", "transform_done", "stage0_ready", "loop_done", "end", "w0_layers_done", "w0_item_out", "w0_layers_start", "stage0_landed(producer)", "reach_stage0_wait", "last_stage_landed"]
 print(f"{mode} N={N}x{nlin} K={K}: {live.sum()} CTAs; us relative to first CTA start")
 for i, n in enumerate(names):
     col = rel[:, i]

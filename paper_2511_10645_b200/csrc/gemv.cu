@@ -434,10 +434,9 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
       }
     }
   };
-  // this warp's tiles are tA + warp + NW * m (TPS is a multiple of NW): (row block, group)
-  // advance incrementally
-  int rb = (tA + warp) / G;
-  int g = (tA + warp) - rb * G;
+  // this warp's tiles of stage st are tA + st * TPS + warp + NW * m: (row block, group) from
+  // one division per stage, then advanced incrementally
+  int rb = 0, g = 0;
   unsigned long long c_wait = 0, c_work = 0, c_t = PARO_DBG(a) ? clock64() : 0;
   for (int st = 0; st < n_stages; ++st) {
     const int slot = st % a.S;
@@ -452,6 +451,11 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
     if (st == n_stages - 1 && threadIdx.x == 0) PARO_TL(a, 11);
     const uint32_t sbase = ring_a + static_cast<uint32_t>(slot) * a.slot_bytes;
     const int nts = min(TPS, n_my - st * TPS);
+    {
+      const int tl0 = tA + st * TPS + warp;
+      rb = tl0 / G;
+      g = tl0 - rb * G;
+    }
     for (int i = warp; i < (a.skip_math ? 0 : nts); i += NW) {
       if (rb - rho_first != cur) {
         if (cur >= 0) flush();
@@ -707,8 +711,7 @@ static bool plan_try(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t
   const int G = static_cast<int>(K / GRP);
   int ctas_per_sm = (NW <= 8 && ctas_pref == 2) ? 2 : 1;
   while (CL > 1 && CL > G) CL /= 2;
-  int TPS = std::max(1, std::min(64, TPS_req > 0 ? TPS_req : 2 * NW));
-  TPS = std::max(NW, TPS / NW * NW);  // a multiple of NW: warp w's tiles are w, w + NW, ...
+  const int TPS = std::max(1, std::min(64, TPS_req > 0 ? TPS_req : 2 * NW));
   c.NW = NW;
   c.CL = CL;
   c.a.xfirst = env_int("PARO_XFIRST", 1);           // weights wait until the transform loads are out

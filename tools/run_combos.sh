@@ -1,3 +1,2 @@
 #!/bin/bash
-PARO_NVCC_EXTRA="-DPARO_ENABLE_DEBUG=1" python -c "from paper_2511_10645_b200 import _build; _build.build(force=True)"
-timeout 60 python tools/timeline.py 4096 4096 rot 1 2>&1
+for t in 30 24 20 18 15; do echo "== TPS=$t"; PARO_TPS=$t PARO_PLAN_DEBUG=1 timeout 120 python tools/time_groups.py rot 1 2>&1 | sort -u | grep -v "^$" | grep "layer\|gate\|down\|o_proj\|q_proj\|K=4096 grid=148\|K=14336"; done

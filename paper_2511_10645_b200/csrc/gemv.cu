@@ -109,8 +109,10 @@ __device__ __forceinline__ int cta_of_tile(int x, int nt, int lcl) {
 // MAXT: 288 (<= 8 compute warps, 2 CTAs / SM), 512 (<= 15) or 640 (<= 19).  Registers are
 // allocated per SM sub-partition (16K each, warps round-robin), so 16 warps get up to 128
 // registers per thread while 17..20 warps get 96.
-template <int BT, int MAXT>
+// IM: integer tensor-core variant for BT <= 2 (see the header comment, "IMMA path").
+template <int BT, int MAXT, bool IM>
 __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(const GemvArgs a) {
+  static_assert(!IM || BT <= 2, "the IMMA path holds at most two tokens per launch");
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -165,7 +167,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
     }
     mbar_init(xpbar, 1);
     mbar_init(rbar, 1);
-    if (CL > 1) mbar_arrive_expect_tx(xpbar, static_cast<uint32_t>(BT) * (K * 2 + G * 4));
+    if (CL > 1) mbar_arrive_expect_tx(xpbar, static_cast<uint32_t>(BT) * (K * 2 + G * (IM ? 8 : 4)));
     uint32_t rbytes = 0;
     for (int c = crank + 1; c <= last_cta; ++c)
       if (cta_tile_start(c + 1, nt, lcl) > cta_tile_start(c, nt, lcl)) rbytes += TILE_ROWS * B * 4;
@@ -304,6 +306,80 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
         cluster_wait();  // every CTA of the cluster is running and initialised: DSMEM is legal
         cwaited = true;
       }
+      if constexpr (IM) {
+        // IMMA path: x' of (group, token) -> fixed point x'fix = rint(x' * 2^(14 - E)), 2^E >= max|x'|
+        // over the group (|x'fix| <= 2^14), split into two balanced s8 digits x'fix = 256 hi + lo.
+        // The digits are laid out as IMMA B fragments: slot (group, token, hd = 2 hl + dg, t) holds
+        // 16 bytes, byte i of word j = digit dg (0: hi, 1: lo) of the channel in nibble hl of byte i
+        // of word j of quad t (tile_layout.cuh).  Per (group, token) also X = sum x'fix (zero-point
+        // term) and F = 2^(E - 14).
+#pragma unroll
+        for (int q = 0; q < NG; ++q) {
+          const int gam = gams[q];
+          int fxv[BT][4];
+          int Xs[BT];
+          float Fs[BT];
+#pragma unroll
+          for (int b = 0; b < BT; ++b) {
+            const float4 v = *reinterpret_cast<const float4*>(scr + (q * BT + b) * 132 + 4 * lane);
+            float m = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            const uint32_t mb = __float_as_uint(m);
+            int E = mb < 0x00800000u ? -100 : static_cast<int>(mb >> 23) - 127 + ((mb & 0x7fffffu) != 0u ? 1 : 0);
+            E = max(E, -100);
+            const float mul = __uint_as_float(static_cast<uint32_t>(141 - E) << 23);  // 2^(14 - E)
+            Fs[b] = __uint_as_float(static_cast<uint32_t>(113 + E) << 23);           // 2^(E - 14)
+            fxv[b][0] = __float2int_rn(v.x * mul);
+            fxv[b][1] = __float2int_rn(v.y * mul);
+            fxv[b][2] = __float2int_rn(v.z * mul);
+            fxv[b][3] = __float2int_rn(v.w * mul);
+            int xs = (fxv[b][0] + fxv[b][1]) + (fxv[b][2] + fxv[b][3]);
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
+            Xs[b] = xs;
+          }
+          __syncwarp();  // every lane has read its x' (the digit image overwrites the scratch)
+#pragma unroll
+          for (int b = 0; b < BT; ++b) {
+            uint8_t* img = reinterpret_cast<uint8_t*>(scr + (q * BT + b) * 132);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int c = 4 * lane + e;
+              const int j = c >> 5, hl = (c >> 4) & 1, i = ((c & 1) << 1) | ((c >> 3) & 1), tq = (c >> 1) & 3;
+              const int fx = fxv[b][e];
+              const int lo = static_cast<int>(static_cast<int8_t>(fx & 0xff));
+              const int hi = (fx - lo) >> 8;
+              img[((hl * 2 + 0) * 4 + tq) * 16 + j * 4 + i] = static_cast<uint8_t>(hi);
+              img[((hl * 2 + 1) * 4 + tq) * 16 + j * 4 + i] = static_cast<uint8_t>(lo);
+            }
+          }
+          __syncwarp();
+          const int sl = lane & 15, tl = lane >> 4;
+          if (tl < BT) {
+            const uint4 v =
+                *reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(scr + (q * BT + tl) * 132) + sl * 16);
+            const uint32_t uo = u_addr + static_cast<uint32_t>(((gam * BT + tl) * 16 + sl) * 16);
+            const uint32_t so = s_addr + static_cast<uint32_t>((gam * 8 + 2 * tl) * 4);
+            const int Xt = (BT == 2 && tl) ? Xs[BT - 1] : Xs[0];
+            const float Ft = (BT == 2 && tl) ? Fs[BT - 1] : Fs[0];
+            if (CL > 1) {
+#pragma unroll 1
+              for (int r = 0; r < CL; ++r) {
+                const uint32_t rb = mapa(bar_addr, r);
+                st_async_v4(mapa(uo, r), v, rb);
+                if (sl == 0) st_async_v2(mapa(so, r), static_cast<uint32_t>(Xt), __float_as_uint(Ft), rb);
+              }
+            } else {
+              *reinterpret_cast<uint4*>(ufr + (uo - u_addr)) = v;
+              if (sl == 0) {
+                reinterpret_cast<int*>(xsum)[gam * 8 + 2 * tl] = Xt;
+                xsum[gam * 8 + 2 * tl + 1] = Ft;
+              }
+            }
+          }
+        }
+      } else {
 #pragma unroll
       for (int q = 0; q < NG; ++q) {
         const int gam = gams[q];
@@ -333,6 +409,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
           }
         }
       }
+      }  // !IM
       __syncwarp();
       if (PARO_DBG(a)) {
         const unsigned long long c = clock64();
@@ -420,8 +497,24 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0.f;
   int cur = -1;
+  // IMMA path: lane (gq, t) accumulates rows gq + 8q (acc[q], q = 0..3) of token tok_l; lanes
+  // t = 2 tok_l (low-nibble channels) and t = 2 tok_l + 1 (high-nibble channels) are summed at flush
+  const int tok_l = (IM && BT == 2) ? (t >> 1) : 0;
+  const int tokB = (IM && BT == 2) ? (gq >> 2) : 0;      // token of the B column this lane supplies
+  const uint32_t mlo = ((gq >> 1) & 1) ? 0u : 0xffffffffu;  // column gq carries low-nibble digits
+  const uint32_t mhi = ~mlo;
+  const int xmask = (t & 1) ? 0 : -1;   // zero-point term on the low-nibble lane only
+  const float fsc = (t & 1) ? 0.0625f : 1.0f;  // high-nibble products carry 16 q
   auto flush = [&]() {
     float* pr = pw + cur * TR * BT;
+    if constexpr (IM) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float v = acc[q] + __shfl_xor_sync(0xffffffffu, acc[q], 1);
+        if ((t & 1) == 0 && (t >> 1) < BT && tok_l < B) pr[(gq + 8 * q) * BT + tok_l] = v;
+      }
+      return;
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (2 * t < B) {
@@ -468,6 +561,47 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
       uint4 w[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) w[q] = lds128_a(ca + q * 512);
+      if constexpr (IM) {
+        // A = codes as u8 (low nibbles: w & 0x0F0F0F0F; high: w & 0xF0F0F0F0 = 16 q), B = x'fix digits.
+        // k-steps: (words 0, 1) and (words 2, 3) of the low nibbles into columns of low-nibble digits,
+        // then the same words' high nibbles into the high-nibble columns (the other columns see B = 0).
+        const uint4 r = lds128_a(u_a + static_cast<uint32_t>((((g * BT + tokB) * 16) + (gq & 3) * 4 + t) * 16));
+        constexpr uint32_t ML = 0x0f0f0f0fu, MH = 0xf0f0f0f0u;
+        int D[2][4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          imma_16832_z(D[h], w[2 * h].x & ML, w[2 * h + 1].x & ML, w[2 * h].y & ML, w[2 * h + 1].y & ML, r.x & mlo,
+                       r.y & mlo);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          imma_16832(D[h], w[2 * h].z & ML, w[2 * h + 1].z & ML, w[2 * h].w & ML, w[2 * h + 1].w & ML, r.z & mlo,
+                     r.w & mlo);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          imma_16832(D[h], w[2 * h].x & MH, w[2 * h + 1].x & MH, w[2 * h].y & MH, w[2 * h + 1].y & MH, r.x & mhi,
+                     r.y & mhi);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          imma_16832(D[h], w[2 * h].z & MH, w[2 * h + 1].z & MH, w[2 * h].w & MH, w[2 * h + 1].w & MH, r.z & mhi,
+                     r.w & mhi);
+        // epilogue (a6): I = sum (q - z) x'fix exactly in int32 (low lane: 256 D_hi + D_lo - z X;
+        // high lane: 16x that sum of its channels), y += S * F * I
+        const uint2 sp = lds_u64_a(sbase + a.sc_off + static_cast<uint32_t>(i) * TILE_SCALE_BYTES + gq * 8);
+        const uint32_t zw = lds_u16z_a(sbase + a.z_off + static_cast<uint32_t>(i) * TILE_ZERO_BYTES + gq * 2);
+        const uint2 mt = lds_u64_a(xs_a + static_cast<uint32_t>((g * 8 + 2 * tok_l) * 4));
+        const int Xl = static_cast<int>(mt.x) & xmask;
+        const float Fl = __uint_as_float(mt.y) * fsc;
+        const float2 Sa = __half22float2(*reinterpret_cast<const __half2*>(&sp.x));  // rows gq, gq + 8
+        const float2 Sb = __half22float2(*reinterpret_cast<const __half2*>(&sp.y));  // rows gq + 16, gq + 24
+        const float Sr[4] = {Sa.x, Sa.y, Sb.x, Sb.y};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int zq = static_cast<int>((zw >> (4 * q)) & 15u);
+          const int h = q >> 1, e = (q & 1) * 2;
+          const int I = D[h][e] * 256 + D[h][e + 1] - zq * Xl;
+          acc[q] = fmaf(static_cast<float>(I), Sr[q] * Fl, acc[q]);
+        }
+      } else {
       // B fragments of group g (token bq): registers 4 * ii .. 4 * ii + 3 = MMAs 2 ii, 2 ii + 1
       uint32_t bf[16];
       {
@@ -518,6 +652,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
           acc[4 * h + e + 1] =
               fmaf(Sr[q], fmaf(fmaf(D16[h][e + 1], 0.0625f, D1[h][e + 1]), TWO_P24, -zq * X2.y), acc[4 * h + e + 1]);
       }
+      }  // !IM
       g += NW;
       while (g >= G) {
         g -= G;
@@ -633,24 +768,26 @@ static int smem_optin() {
 
 static inline uint32_t align_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
-static const void* kernel_for(int BT, int threads) {
-#define PARO_KF(BT_)                                                                        \
-  if (BT == BT_) {                                                                        \
-    if (threads <= 288) return reinterpret_cast<const void*>(&paro_gemv_kernel<BT_, 288>); \
-    if (threads <= 512) return reinterpret_cast<const void*>(&paro_gemv_kernel<BT_, 512>); \
-    if (threads <= 640) return reinterpret_cast<const void*>(&paro_gemv_kernel<BT_, 640>); \
+static const void* kernel_for(int BT, int threads, bool im) {
+#define PARO_KF(BT_, IM_)                                                                          \
+  if (BT == BT_ && im == IM_) {                                                                   \
+    if (threads <= 288) return reinterpret_cast<const void*>(&paro_gemv_kernel<BT_, 288, IM_>); \
+    if (threads <= 512) return reinterpret_cast<const void*>(&paro_gemv_kernel<BT_, 512, IM_>); \
+    if (threads <= 640) return reinterpret_cast<const void*>(&paro_gemv_kernel<BT_, 640, IM_>); \
   }
-  PARO_KF(1)
-  PARO_KF(2)
-  PARO_KF(4)
-  PARO_KF(8)
+  PARO_KF(1, false)
+  PARO_KF(2, false)
+  PARO_KF(4, false)
+  PARO_KF(8, false)
+  PARO_KF(1, true)
+  PARO_KF(2, true)
 #undef PARO_KF
   return nullptr;
 }
 
 // Co-resident CTAs for this launch shape (whole clusters), from the occupancy API.
-static int max_resident_ctas(int BT, int threads, int smem, int CL) {
-  const void* k = kernel_for(BT, threads);
+static int max_resident_ctas(int BT, int threads, int smem, int CL, bool im) {
+  const void* k = kernel_for(BT, threads, im);
   if (!k) return 0;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
     cudaGetLastError();
@@ -700,6 +837,8 @@ static bool plan_try(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t
     return false;
   }
   c.BT = B;
+  // integer tensor-core path (x' as 16-bit fixed point per group) for 1-2 tokens; PARO_IMMA=0: fp16 HMMA
+  c.IM = B <= 2 && env_int("PARO_IMMA", 1) != 0;
   int64_t NBsum = 0;
   int L = 0;
   int64_t NB[GEMV_MAX_LIN];
@@ -811,7 +950,7 @@ static bool plan_try(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t
       *why = "decode kernel shared-memory plan does not fit";
       return false;
     }
-    const int resident = max_resident_ctas(c.BT, threads, static_cast<int>(a.smem_total), CL);
+    const int resident = max_resident_ctas(c.BT, threads, static_cast<int>(a.smem_total), CL, c.IM);
     if (resident <= 0 || resident >= c.grid) break;
     grid = resident / CL * CL;  // never launch more than one wave
   }
@@ -848,9 +987,9 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
   return plan_try(B, n_lin, Ns, Ls, K, rotate, 4, 1, CL, 0, 1, cfg, why);
 }
 
-template <int BT, int T>
+template <int BT, int T, bool IM>
 static cudaError_t launch_t(const GemvConfig& c, cudaStream_t st) {
-  auto kern = paro_gemv_kernel<BT, T>;
+  auto kern = paro_gemv_kernel<BT, T, IM>;
   static int configured_smem = 0;  // per instantiation
   if (static_cast<int>(c.a.smem_total) > configured_smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -885,16 +1024,18 @@ static cudaError_t launch_t(const GemvConfig& c, cudaStream_t st) {
 cudaError_t launch_gemv(const GemvConfig& c, cudaStream_t st) {
   if (c.a.B < 1 || c.a.B > c.BT) return cudaErrorInvalidValue;
   const int threads = (c.NW + 1) * 32;
-#define PARO_LG(BT_)                                               \
-  if (c.BT == BT_) {                                               \
-    if (threads <= 288) return launch_t<BT_, 288>(c, st);          \
-    if (threads <= 512) return launch_t<BT_, 512>(c, st);          \
-    if (threads <= 640) return launch_t<BT_, 640>(c, st);          \
+#define PARO_LG(BT_, IM_)                                          \
+  if (c.BT == BT_ && c.IM == IM_) {                                \
+    if (threads <= 288) return launch_t<BT_, 288, IM_>(c, st);     \
+    if (threads <= 512) return launch_t<BT_, 512, IM_>(c, st);     \
+    if (threads <= 640) return launch_t<BT_, 640, IM_>(c, st);     \
   }
-  PARO_LG(1)
-  PARO_LG(2)
-  PARO_LG(4)
-  PARO_LG(8)
+  PARO_LG(1, false)
+  PARO_LG(2, false)
+  PARO_LG(4, false)
+  PARO_LG(8, false)
+  PARO_LG(1, true)
+  PARO_LG(2, true)
 #undef PARO_LG
   return cudaErrorInvalidConfiguration;
 }

@@ -54,6 +54,7 @@ struct GemvArgs {
 
 struct GemvConfig {
   int BT, NW, CL, grid;  // BT: compile-time token tile of the kernel instance
+  bool IM;               // integer tensor-core (IMMA) instance (BT <= 2)
   GemvArgs a;
 };
 

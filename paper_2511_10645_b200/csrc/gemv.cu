@@ -849,6 +849,10 @@ static bool plan_try(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t
   }
   const int G = static_cast<int>(K / GRP);
   int ctas_per_sm = (NW <= 8 && ctas_pref == 2) ? 2 : 1;
+  // co-resident mode: one CTA per SM in the grid, but a half-SM footprint (smem, registers) so
+  // that the next launch on the stream (PDL) is resident while this one runs
+  const bool coloc = ctas_pref == 3 && NW <= 8;
+  if (coloc) ctas_per_sm = 2;
   while (CL > 1 && CL > G) CL /= 2;
   const int TPS = std::max(1, std::min(64, TPS_req > 0 ? TPS_req : 2 * NW));
   c.NW = NW;
@@ -937,7 +941,7 @@ static bool plan_try(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t
     a.smem_total = a.off_ring + static_cast<uint32_t>(S) * a.slot_bytes;
     return true;
   };
-  int grid = device_sm_count() * ctas_per_sm / CL * CL;
+  int grid = device_sm_count() * (coloc ? 1 : ctas_per_sm) / CL * CL;
   if (grid < CL * n_lin) grid = CL * n_lin;
   if (!layout(grid) && ctas_per_sm == 2) {  // too big for two CTAs per SM: one, with the full budget
     ctas_per_sm = 1;
@@ -950,7 +954,8 @@ static bool plan_try(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t
       *why = "decode kernel shared-memory plan does not fit";
       return false;
     }
-    const int resident = max_resident_ctas(c.BT, threads, static_cast<int>(a.smem_total), CL, c.IM);
+    int resident = max_resident_ctas(c.BT, threads, static_cast<int>(a.smem_total), CL, c.IM);
+    if (coloc) resident /= 2;
     if (resident <= 0 || resident >= c.grid) break;
     grid = resident / CL * CL;  // never launch more than one wave
   }
@@ -971,7 +976,8 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
   // best on the bench's Llama-3-8B layer); PARO_NW / PARO_CTAS_PER_SM / PARO_CLUSTER / PARO_TPS
   // override.  Shapes whose shared-memory plan does not fit fall back to 8 warps.
   const int NW = std::max(1, std::min(19, env_int("PARO_NW", 15)));
-  const int cps = env_int("PARO_CTAS_PER_SM", 2) == 1 ? 1 : 2;
+  const int cps_env = env_int("PARO_CTAS_PER_SM", 2);
+  const int cps = cps_env == 1 ? 1 : (cps_env == 3 ? 3 : 2);
   // clusters of 4 share the transform 4 ways; very large launches with few groups (gate/up at
   // K = 4096) prefer pairs, which tile all 148 SMs (clusters of 4 leave 16 idle)
   int64_t tiles = 0;

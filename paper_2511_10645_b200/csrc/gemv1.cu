@@ -1,0 +1,562 @@
+// gemv1.cu -- decode path for ONE token (B = 1): scale + L Givens layers + group-wise INT4
+// dequant GEMV, one launch per (multi-)linear, built for the shortest serial chain.
+//
+// SURVEY.md 8(a) rows a4 (u = s . x), a5 (the L rotations, Eq. 5 in column
+// form), a6 (dequant GEMV, Eq. 1 dequantisation (q - z) * S),
+// a8 (bias + output rounding, Eq. 2).
+//
+// Work split (K-split inside a thread-block cluster):
+//  * a cluster of CL CTAs (one per SM, one wave) owns a run of 32-row blocks of one linear;
+//  * CTA c of the cluster owns the groups [c G / CL, (c + 1) G / CL) of those rows.  It
+//    transforms ONLY its own groups (a warp per group: the rotation is group-local, so no
+//    activation ever crosses CTAs) and streams only the tiles of its groups;
+//  * the cluster sums its CTAs' row partials through distributed shared memory (fixed order:
+//    deterministic, no atomics) and the owner CTA of a row writes y.
+// Pipeline per CTA: one producer warp issues every weight stage with cp.async.bulk (TMA
+// engine) at kernel start -- before the programmatic-dependent-launch wait, because packed
+// weights are never written by the previous kernel -- while the compute warps load their
+// rotation parameters, wait for the previous kernel (x may be its output), load x, rotate in
+// shared memory and leave x' as fixed-point digits in shared memory; then the tiles are consumed as they land.
+//
+// Dot product on the warp-level integer tensor cores (IMMA.16832, u8 x s8 -> s32, exact):
+// x' of a group becomes 16-bit fixed point x'fix = rint(x' 2^(14 - E)) with 2^E >= max |x'|
+// (|x'fix| <= 2^14), split into two s8 digits x'fix = 256 hi + lo.  An AND mask on a code word
+// gives four u8 codes (low nibbles: q; high nibbles: 16 q), which ARE the A fragment of the
+// MMA; B holds the digits (column 0: hi, column 1: lo).  Per (row, group) the int32 result
+// I = sum (q - z) x'fix is exact and y += S * 2^(E - 14) * I.  Lane (g, t) of a warp loads
+// quad t of rows g, g + 8, g + 16, g + 24 of a tile (four LDS.128, 128 weights); eight MMAs
+// cover the tile.
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+
+#include "paro_internal.h"
+#include "ptx.cuh"
+#include "tile_layout.cuh"
+
+namespace paro {
+
+#ifndef G1_TL
+#define G1_TL 0  // 1: per-CTA %globaltimer timeline of every launch (tools/timeline1.py)
+#endif
+__device__ unsigned long long g_g1_tl[1024 * 8];
+extern "C" int paro_debug_read_timeline1(unsigned long long* host, int n) {
+  if (n > 1024 * 8) n = 1024 * 8;
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_g1_tl, sizeof(unsigned long long) * n));
+}
+
+namespace {
+constexpr int G1_NW = 16;
+__device__ __forceinline__ void g1_mark(int ev) {
+  if (G1_TL && blockIdx.x < 1024) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_g1_tl[blockIdx.x * 8 + ev] = t;
+  }
+}  // compute warps per CTA (+ 1 producer warp)
+constexpr uint32_t TILE_B = TILE_CODE_BYTES + TILE_SCALE_BYTES + TILE_ZERO_BYTES;
+
+// D(16x8 s32) += A(16x32 u8, row) * B(32x8 s8, col); fragments as in ptx.cuh (imma_16832),
+// not volatile so the scheduler may interleave the four accumulator chains
+__device__ __forceinline__ void mma_u8s8(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// stage st -> (first cluster-local row block, row blocks, first group, groups)
+struct StageGeo {
+  int r_lo, nr, g_lo, pl;
+};
+__device__ __forceinline__ StageGeo stage_geo(int st, int npc, int plen, int rbs, int nrb, int ga, int gb) {
+  const int rc = st / npc, pc = st - rc * npc;
+  StageGeo s;
+  s.r_lo = rc * rbs;
+  s.nr = min(rbs, nrb - s.r_lo);
+  s.g_lo = ga + pc * plen;
+  s.pl = min(plen, gb - s.g_lo);
+  return s;
+}
+}  // namespace
+
+// NW compute warps (+ 1 producer).  NW = 8: half-SM footprint (registers, shared memory) so the
+// next launch on the stream (PDL) is resident and streams its weights while this one computes.
+template <int NW>
+__global__ void __launch_bounds__((NW + 1) * 32, NW <= 8 ? 2 : 1) paro_gemv1_kernel(const Gemv1Args a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int li = 0;
+#pragma unroll 1
+  while (li + 1 < a.n_lin && static_cast<int>(blockIdx.x) >= a.lin[li + 1].cta_begin) ++li;
+  const Gemv1Linear& d = a.lin[li];
+  const int CL = static_cast<int>(cluster_nctarank());
+  const int crank = static_cast<int>(cluster_ctarank());
+  const int G = a.G;
+  const int cl = (static_cast<int>(blockIdx.x) - d.cta_begin) / CL;
+  const int nrb = d.rb_base + (cl < d.rb_extra ? 1 : 0);
+  const int rb0 = cl * d.rb_base + min(cl, d.rb_extra);
+  const int R = nrb * TILE_ROWS;
+  const int ga = crank * G / CL, gb = (crank + 1) * G / CL, gc = gb - ga;
+  // stages: (row-block chunk) x (group piece); pieces balanced, chunks fill a stage
+  const int npc = (gc + a.TPS - 1) / a.TPS;
+  const int plen = (gc + npc - 1) / npc;
+  const int rbs = max(1, a.TPS / plen);
+  const int n_stages = ((nrb + rbs - 1) / rbs) * npc;
+
+  uint8_t* xp = smem + a.off_xp;                                 // x' digits [gc][4 t][2 col][4 kb][8 B]
+  float* xs = reinterpret_cast<float*>(smem + a.off_xs);         // per group (sum x'fix, 2^(E-14))
+  float* part = reinterpret_cast<float*>(smem + a.off_part);     // [NW][R_max] row partials
+  float* recv = reinterpret_cast<float*>(smem + a.off_recv);     // [CL][RR] cluster partials
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.off_bar);
+  uint64_t* empty = full + a.S;
+  uint64_t* rbar = empty + a.S;  // cluster partials of my rows landed (st.async bytes)
+  const int RR = (R + CL - 1) / CL;  // rows per owner CTA
+  const int my_lo = crank * RR, my_n = max(0, min(RR, R - my_lo));
+  uint8_t* ring = smem + a.off_ring;
+
+  if (threadIdx.x == 0) {
+    g1_mark(0);
+    for (int i = 0; i < a.S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NW);
+    }
+    mbar_init(rbar, 1);
+    if (CL > 1) mbar_arrive_expect_tx(rbar, static_cast<uint32_t>((CL - 1) * my_n * 4));
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (CL > 1) cluster_arrive_relaxed();  // matched by the wait before the first DSMEM store
+  if (a.pdl) pdl_launch_dependents();
+
+  // ------------------------------------------------------------ producer warp: the whole ring
+  if (warp == NW) {
+    const uint64_t pol = l2_evict_first_policy();
+    const int pre = min(a.pre_stages, n_stages);
+#pragma unroll 1
+    for (int st = 0; st < n_stages; ++st) {
+      const int slot = st % a.S;
+      // the latency-critical x / rotation-parameter loads of the compute warps go out before
+      // the bulk of the weight stream (which would otherwise queue ahead of them)
+      if (st == pre) named_bar_sync(2, (NW + 1) * 32);
+      if (st >= a.S) mbar_wait(&empty[slot], ((st / a.S) & 1) ^ 1);
+      if (lane == 0) {
+        const StageGeo s = stage_geo(st, npc, plen, rbs, nrb, ga, gb);
+        uint8_t* dst = ring + static_cast<size_t>(slot) * a.slot_bytes;
+        mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(s.nr * s.pl) * TILE_B);
+#pragma unroll 1
+        for (int r = 0; r < s.nr; ++r) {
+          const int64_t T = static_cast<int64_t>(rb0 + s.r_lo + r) * G + s.g_lo;
+          const uint32_t i0 = static_cast<uint32_t>(r * s.pl), n = static_cast<uint32_t>(s.pl);
+          bulk_g2s(dst + i0 * TILE_CODE_BYTES, d.codes + T * TILE_CODE_BYTES, n * TILE_CODE_BYTES, &full[slot], pol);
+          bulk_g2s(dst + a.sc_off + i0 * TILE_SCALE_BYTES, d.scales + T * TILE_SCALE_BYTES, n * TILE_SCALE_BYTES,
+                   &full[slot], pol);
+          bulk_g2s(dst + a.z_off + i0 * TILE_ZERO_BYTES, d.zeros + T * TILE_ZERO_BYTES, n * TILE_ZERO_BYTES, &full[slot],
+                   pol);
+        }
+      }
+      __syncwarp();
+    }
+    if (pre >= n_stages) named_bar_sync(2, (NW + 1) * 32);
+    if (lane == 0) g1_mark(1);  // every stage issued
+    if (CL > 1) cluster_wait();
+    return;
+  }
+
+  // ------------------------------------------------------------ phase 1: x' of my groups (a4, a5)
+  float* pw = part + static_cast<size_t>(warp) * a.R_max;
+  for (int i = lane; i < R; i += 32) pw[i] = 0.f;
+  {
+    float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * 128;
+    const int L = a.rotate ? d.L : 0;
+    bool waited = false;
+    if (warp >= gc) named_bar_arrive(2, (NW + 1) * 32);
+#pragma unroll 1
+    for (int g = warp; g < gc; g += NW) {
+      const int gam = ga + g;
+      // rotation records [group][layer][32 lanes]: (cos, sin) of slots lane, lane + 32 and
+      // their (i, j) channel pairs (pack-time bank-conflict-free schedule)
+      float4 cs[8];
+      uint32_t ix[8];
+      const int64_t rec = static_cast<int64_t>(gam) * L * 32 + lane;
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        if (t < L) {
+          cs[t] = __ldg(reinterpret_cast<const float4*>(d.rot_cs) + rec + t * 32);
+          ix[t] = __ldg(reinterpret_cast<const uint32_t*>(d.rot_idx) + rec + t * 32);
+        }
+      const float4 sv =
+          a.rotate ? __ldg(reinterpret_cast<const float4*>(d.svec + gam * 128) + lane) : make_float4(1.f, 1.f, 1.f, 1.f);
+      if (!waited) {
+        if (a.pdl) pdl_wait();  // x may be written by the previous kernel on the stream
+        waited = true;
+      }
+      const uint2 xv = __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(a.x) +
+                                                           (static_cast<int64_t>(gam) * 128 + 4 * lane) * 2));
+      float2 f01, f23;
+      if (a.x_bf16) {
+        f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.x));
+        f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.y));
+      } else {
+        f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv.x));
+        f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv.y));
+      }
+      if (g == warp) {
+        __syncwarp();
+        named_bar_arrive(2, (NW + 1) * 32);  // my x and parameters are in
+        if (threadIdx.x == 0) g1_mark(2);
+      }
+      // a4: u = s . x
+      *reinterpret_cast<float4*>(scr + 4 * lane) = make_float4(f01.x * sv.x, f01.y * sv.y, f23.x * sv.z, f23.y * sv.w);
+      __syncwarp();
+      // a5: rotations t = 1..L, each pair from the pre-update values (Eq. 4 / Eq. 5)
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        if (t >= L) break;
+        const uint32_t i0 = ix[t] & 0xff, j0 = (ix[t] >> 8) & 0xff, i1 = (ix[t] >> 16) & 0xff, j1 = ix[t] >> 24;
+        const float a0 = scr[i0], b0 = scr[j0], a1 = scr[i1], b1 = scr[j1];
+        scr[i0] = cs[t].x * a0 - cs[t].y * b0;
+        scr[j0] = cs[t].y * a0 + cs[t].x * b0;
+        scr[i1] = cs[t].z * a1 - cs[t].w * b1;
+        scr[j1] = cs[t].w * a1 + cs[t].z * b1;
+        __syncwarp();
+      }
+      // x' -> per-group fixed point and s8 digits (see the header), laid out as B fragments:
+      // [quad t][column g = 0 hi / 1 lo][k-block kb][b0, b1]; k-block kb = 2 p + h covers the
+      // low (p = 0) or high (p = 1) nibbles of words 2h, 2h + 1 (b0: word 2h, b1: word 2h + 1);
+      // byte b of the word for quad t, word j, parity p is channel tile_k(t, j, 2 b + p)
+      {
+        const float4 v = *reinterpret_cast<const float4*>(scr + 4 * lane);
+        float m = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        const uint32_t mb = __float_as_uint(m);
+        int E = mb < 0x00800000u ? -100 : static_cast<int>(mb >> 23) - 127 + ((mb & 0x7fffffu) != 0u ? 1 : 0);
+        E = max(E, -100);
+        const float mul = __uint_as_float(static_cast<uint32_t>(141 - E) << 23);  // 2^(14 - E)
+        const int f0 = __float2int_rn(v.x * mul), f1 = __float2int_rn(v.y * mul);
+        const int f2 = __float2int_rn(v.z * mul), f3 = __float2int_rn(v.w * mul);
+        int X = (f0 + f1) + (f2 + f3);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) X += __shfl_xor_sync(0xffffffffu, X, o);
+        __syncwarp();  // every lane has read its x' before the scratch holds x'fix
+        *reinterpret_cast<int4*>(scr + 4 * lane) = make_int4(f0, f1, f2, f3);
+        __syncwarp();
+        const int* fx = reinterpret_cast<const int*>(scr);
+        const int tq = lane >> 3, col = (lane >> 2) & 1, kb = lane & 3, p = kb >> 1, h = kb & 1;
+        uint32_t wd[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = 2 * h + e;
+          uint32_t wv = 0;
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb) {
+            const int c = 16 * (2 * j + p) + 2 * tq + (bb >> 1) + 8 * (bb & 1);  // tile_k(tq, j, 2 bb + p)
+            const int f = fx[c];
+            const int lo = static_cast<int>(static_cast<int8_t>(f & 0xff));
+            const int dg = col ? lo : ((f - lo) >> 8);
+            wv |= (static_cast<uint32_t>(dg) & 0xffu) << (8 * bb);
+          }
+          wd[e] = wv;
+        }
+        *reinterpret_cast<uint2*>(xp + g * 256 + tq * 64 + col * 32 + kb * 8) = make_uint2(wd[0], wd[1]);
+        if (lane == 0)
+          *reinterpret_cast<int2*>(xs + 2 * g) =
+              make_int2(X, static_cast<int>((static_cast<uint32_t>(113 + E) << 23)));  // (sum x'fix, 2^(E - 14))
+      }
+      __syncwarp();
+    }
+  }
+  named_bar_sync(1, NW * 32);  // every x' of the CTA is in shared memory
+  if (threadIdx.x == 0) g1_mark(3);
+
+  // ------------------------------------------------------------ phase 2: tiles (a6)
+  {
+    const int gq = lane >> 2, tq = lane & 3;
+    int rc = 0, pc = 0;  // stage -> (row-block chunk, group piece), advanced incrementally
+#pragma unroll 1
+    for (int st = 0; st < n_stages; ++st) {
+      const int slot = st % a.S;
+      const int r_lo = rc * rbs, nr = min(rbs, nrb - r_lo);
+      const int g_lo = ga + pc * plen, pl = min(plen, gb - g_lo);
+      if (++pc == npc) {
+        pc = 0;
+        ++rc;
+      }
+      mbar_wait(&full[slot], (st / a.S) & 1);
+      if (threadIdx.x == 0 && st == 0) g1_mark(4);
+      const uint8_t* sb = ring + static_cast<size_t>(slot) * a.slot_bytes;
+      const int nt = nr * pl;
+      int ri = 0, gi = warp;  // tile warp + k NW of the stage = (row block ri, group gi)
+      while (gi >= pl) {
+        gi -= pl;
+        ++ri;
+      }
+#pragma unroll 1
+      for (int i = warp; i < nt; i += NW) {
+        const int gl = g_lo - ga + gi;
+        const uint8_t* tc = sb + i * TILE_CODE_BYTES + gq * 64 + tq * 16;
+        uint4 w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[q] = *reinterpret_cast<const uint4*>(tc + q * 512);
+        uint4 bA = make_uint4(0u, 0u, 0u, 0u), bB = bA;  // B fragments (columns >= 2 are zero)
+        if (gq < 2) {
+          const uint8_t* bp = xp + gl * 256 + tq * 64 + gq * 32;
+          bA = *reinterpret_cast<const uint4*>(bp);
+          bB = *reinterpret_cast<const uint4*>(bp + 16);
+        }
+        constexpr uint32_t ML = 0x0f0f0f0fu, MH = 0xf0f0f0f0u;
+        int Dl[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}}, Dh[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {  // rows gq + 16 hh (w[2 hh]) and gq + 16 hh + 8 (w[2 hh + 1])
+          const uint4 r0 = w[2 * hh], r1 = w[2 * hh + 1];
+          mma_u8s8(Dl[hh], r0.x & ML, r1.x & ML, r0.y & ML, r1.y & ML, bA.x, bA.y);  // low nibbles, words 0, 1
+          mma_u8s8(Dl[hh], r0.z & ML, r1.z & ML, r0.w & ML, r1.w & ML, bA.z, bA.w);  // low nibbles, words 2, 3
+          mma_u8s8(Dh[hh], r0.x & MH, r1.x & MH, r0.y & MH, r1.y & MH, bB.x, bB.y);  // high nibbles (16 q)
+          mma_u8s8(Dh[hh], r0.z & MH, r1.z & MH, r0.w & MH, r1.w & MH, bB.z, bB.w);
+        }
+        // lanes tq = 0 hold columns 0 (hi digit) and 1 (lo digit) of rows gq + 8 q
+        if (tq == 0) {
+          const uint2 sp = *reinterpret_cast<const uint2*>(sb + a.sc_off + i * TILE_SCALE_BYTES + gq * 8);
+          const uint32_t zw = *reinterpret_cast<const uint16_t*>(sb + a.z_off + i * TILE_ZERO_BYTES + gq * 2);
+          const int2 xf = *reinterpret_cast<const int2*>(xs + 2 * gl);
+          const float F = __int_as_float(xf.y);
+          const float2 Sa = __half22float2(*reinterpret_cast<const __half2*>(&sp.x));  // rows gq, gq + 8
+          const float2 Sb = __half22float2(*reinterpret_cast<const __half2*>(&sp.y));  // rows gq + 16, gq + 24
+          const float Sr[4] = {Sa.x, Sa.y, Sb.x, Sb.y};
+          float* pr = pw + (r_lo + ri) * TILE_ROWS + gq;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int hh = q >> 1, e = (q & 1) * 2;
+            const int zq = static_cast<int>((zw >> (4 * q)) & 15u);
+            const int I = Dl[hh][e] * 256 + Dl[hh][e + 1] + ((Dh[hh][e] * 256 + Dh[hh][e + 1]) >> 4) - zq * xf.x;
+            pr[8 * q] += Sr[q] * F * static_cast<float>(I);
+          }
+        }
+        gi += NW;
+        while (gi >= pl) {
+          gi -= pl;
+          ++ri;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+  }
+
+  // ------------------------------------------------------------ reduction + epilogue (a8)
+  named_bar_sync(1, NW * 32);
+  if (threadIdx.x == 0) g1_mark(5);
+  if (CL > 1) cluster_wait();  // every CTA of the cluster is running: DSMEM is legal
+  const int tid = threadIdx.x;
+  for (int r = tid; r < R; r += NW * 32) {
+    float s4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+    for (int w = 0; w < NW; ++w) s4[w & 3] += part[static_cast<size_t>(w) * a.R_max + r];
+    const float sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    const int owner = r / RR;
+    float* dst = recv + crank * a.RRmax + (r - owner * RR);
+    if (owner == crank)
+      *dst = sum;
+    else
+      st_async_b32(mapa(smem_u32(dst), static_cast<uint32_t>(owner)), __float_as_uint(sum),
+                   mapa(smem_u32(rbar), static_cast<uint32_t>(owner)));
+  }
+  named_bar_sync(1, NW * 32);  // my own partials are in recv
+  if (CL > 1) mbar_wait(rbar, 0);  // and those of the other CTAs of the cluster
+  if (a.pdl) pdl_wait();  // y may still be read by the previous kernel
+  if (threadIdx.x == 0) g1_mark(6);
+  for (int rl = tid; rl < my_n; rl += NW * 32) {
+    float v = 0.f;
+    for (int c = 0; c < CL; ++c) v += recv[c * a.RRmax + rl];  // fixed order
+    const int64_t n = static_cast<int64_t>(rb0) * TILE_ROWS + my_lo + rl;
+    if (n < d.N) {
+      if (d.bias) v += __ldg(d.bias + n);
+      if (a.y_dtype == 0)
+        static_cast<__half*>(d.y)[n] = __float2half_rn(v);
+      else if (a.y_dtype == 1)
+        static_cast<__nv_bfloat16*>(d.y)[n] = __float2bfloat16_rn(v);
+      else
+        static_cast<float*>(d.y)[n] = v;
+    }
+  }
+  if (threadIdx.x == 0) g1_mark(7);
+}
+
+// ============================================================================ host side
+static int g1_env(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+static inline uint32_t g1_align(uint32_t v, uint32_t al) { return (v + al - 1) / al * al; }
+
+bool gemv1_enabled() { return g1_env("PARO_GEMV1", 1) != 0; }
+
+bool plan_gemv1(int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config* cfg, const char** why) {
+  if (n_lin < 1 || n_lin > GEMV_MAX_LIN) {
+    *why = "1..4 linears per decode launch";
+    return false;
+  }
+  const int G = static_cast<int>(K / 128);
+  if (G < 1) {
+    *why = "K must be a positive multiple of 128";
+    return false;
+  }
+  Gemv1Config c{};
+  Gemv1Args& a = c.a;
+  int CL = g1_env("PARO_G1_CL", G >= 64 ? 4 : 2);
+  if (CL != 1 && CL != 2 && CL != 4 && CL != 8) CL = 2;
+  while (CL > 1 && CL > G) CL /= 2;
+  const int NW = g1_env("PARO_G1_NW", G1_NW) <= 8 ? 8 : 16;
+  const bool half = NW == 8;  // co-resident with the next launch
+  const int TPS = std::max(1, std::min(64, g1_env("PARO_G1_TPS", half ? 16 : 32)));
+  const int threads = (NW + 1) * 32;
+  c.NW = NW;
+  int optin = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (optin <= 0) optin = 227 * 1024;
+  const int budget = half ? (optin + 1024) / 2 - 2048 : optin - 1024;
+  // clusters that fit in one wave (occupancy API, cached per cluster size)
+  static int ncl_cache[2][9] = {{0}};
+  static std::mutex mu;
+  int ncl_max;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!ncl_cache[half][CL]) {
+      const void* k = half ? reinterpret_cast<const void*>(&paro_gemv1_kernel<8>)
+                           : reinterpret_cast<const void*>(&paro_gemv1_kernel<G1_NW>);
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, budget);
+      if (CL > 1) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(CL * 64);
+      lc.blockDim = dim3(threads);
+      lc.dynamicSmemBytes = budget;
+      cudaLaunchAttribute at;
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = CL;
+      at.val.clusterDim.y = 1;
+      at.val.clusterDim.z = 1;
+      lc.attrs = &at;
+      lc.numAttrs = 1;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, k, &lc) != cudaSuccess || nc <= 0) {
+        cudaGetLastError();
+        nc = device_sm_count() / CL;
+      }
+      if (half) nc = std::max(1, nc / 2);  // one CTA per SM for this launch, the other half for the next
+      ncl_cache[half][CL] = nc;
+    }
+    ncl_max = ncl_cache[half][CL];
+  }
+  ncl_max = std::min(ncl_max, std::max(1, g1_env("PARO_G1_MAXCL", 1 << 20)));
+  // clusters over linears in proportion to their row blocks (>= 1 each, <= row blocks)
+  int64_t NB[GEMV_MAX_LIN], NBsum = 0;
+  for (int i = 0; i < n_lin; ++i) {
+    NB[i] = (Ns[i] + TILE_ROWS - 1) / TILE_ROWS;
+    NBsum += NB[i];
+  }
+  int ncl = static_cast<int>(std::min<int64_t>(ncl_max, NBsum));
+  if (ncl < n_lin) ncl = n_lin;
+  int cls[GEMV_MAX_LIN], used = 0, big = 0;
+  for (int i = 0; i < n_lin; ++i) {
+    cls[i] = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(NB[i], ncl * NB[i] / NBsum)));
+    used += cls[i];
+    if (NB[i] > NB[big]) big = i;
+  }
+  cls[big] = static_cast<int>(std::min<int64_t>(NB[big], cls[big] + std::max(0, ncl - used)));
+  int begin = 0, rmax = 0;
+  for (int i = 0; i < n_lin; ++i) {
+    Gemv1Linear& d = a.lin[i];
+    d.N = static_cast<int>(Ns[i]);
+    d.cta_begin = begin;
+    d.rb_base = static_cast<int>(NB[i] / cls[i]);
+    d.rb_extra = static_cast<int>(NB[i] % cls[i]);
+    rmax = std::max(rmax, (d.rb_base + (d.rb_extra ? 1 : 0)) * TILE_ROWS);
+    begin += cls[i] * CL;
+  }
+  c.grid = begin;
+  c.CL = CL;
+  a.n_lin = n_lin;
+  a.K = static_cast<int>(K);
+  a.G = G;
+  a.rotate = rotate;
+  a.TPS = TPS;
+  a.pre_stages = std::max(0, g1_env("PARO_G1_PRE", 2));
+  a.R_max = rmax;
+  a.RRmax = (rmax + CL - 1) / CL;
+  const int gcm = (G + CL - 1) / CL;
+  a.sc_off = static_cast<uint32_t>(TPS) * TILE_CODE_BYTES;
+  a.z_off = a.sc_off + static_cast<uint32_t>(TPS) * TILE_SCALE_BYTES;
+  a.slot_bytes = g1_align(a.z_off + static_cast<uint32_t>(TPS) * TILE_ZERO_BYTES, 128);
+  uint32_t off = 0;
+  a.off_xp = off;
+  off += g1_align(static_cast<uint32_t>(gcm) * 256, 128);
+  a.off_xs = off;
+  off += g1_align(static_cast<uint32_t>(gcm) * 8, 128);
+  a.off_scr = off;
+  off += NW * 512;
+  a.off_part = off;
+  off += g1_align(static_cast<uint32_t>(NW) * rmax * 4, 128);
+  a.off_recv = off;
+  off += g1_align(static_cast<uint32_t>(CL) * a.RRmax * 4, 128);
+  a.off_bar = off;
+  off += 64 * 16;
+  a.off_ring = g1_align(off, 1024);
+  int64_t avail = static_cast<int64_t>(budget) - a.off_ring;
+  int S = static_cast<int>(avail / a.slot_bytes);
+  // stages a CTA needs at most (every stage holds <= TPS tiles)
+  const int npc = (gcm + TPS - 1) / TPS;
+  const int plen = (gcm + npc - 1) / npc;
+  const int rbs = std::max(1, TPS / plen);
+  const int need = ((rmax / TILE_ROWS + rbs - 1) / rbs) * npc + npc;
+  S = std::min(S, std::min(need, 60));
+  if (S < 1) {
+    *why = "decode (B=1) shared-memory plan does not fit";
+    return false;
+  }
+  a.S = S;
+  a.smem_total = a.off_ring + static_cast<uint32_t>(S) * a.slot_bytes;
+  if (g1_env("PARO_PLAN_DEBUG", 0))
+    fprintf(stderr, "[paro gemv1 plan] n_lin=%d K=%lld grid=%d CL=%d NW=%d TPS=%d S=%d R_max=%d smem=%u\n", n_lin,
+            static_cast<long long>(K), c.grid, CL, NW, TPS, S, rmax, a.smem_total);
+  *cfg = c;
+  return true;
+}
+
+cudaError_t launch_gemv1(const Gemv1Config& c, cudaStream_t st) {
+  auto kern = c.NW == 8 ? paro_gemv1_kernel<8> : paro_gemv1_kernel<G1_NW>;
+  static int configured[2] = {0, 0};
+  int& conf = configured[c.NW == 8 ? 1 : 0];
+  if (static_cast<int>(c.a.smem_total) > conf) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(c.a.smem_total));
+    if (e != cudaSuccess) return e;
+    conf = static_cast<int>(c.a.smem_total);
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(c.grid);
+  cfg.blockDim = dim3((c.NW + 1) * 32);
+  cfg.dynamicSmemBytes = c.a.smem_total;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[2];
+  int na = 0;
+  attrs[na].id = cudaLaunchAttributeClusterDimension;
+  attrs[na].val.clusterDim.x = c.CL;
+  attrs[na].val.clusterDim.y = 1;
+  attrs[na].val.clusterDim.z = 1;
+  ++na;
+  if (c.a.pdl) {
+    attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attrs;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, c.a);
+}
+
+}  // namespace paro

@@ -333,6 +333,31 @@ static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, 
   int planned_b = 0;
   for (int64_t b0 = 0; b0 < B; b0 += paro::GEMV_MAX_B) {  // token tiles of <= 8 (the MMA's N)
     const int live = static_cast<int>(std::min<int64_t>(paro::GEMV_MAX_B, B - b0));
+    if (live == 1 && !debug && paro::gemv1_enabled()) {  // one token: the K-split CUDA-core kernel
+      paro::Gemv1Config c1;
+      const char* why = "";
+      if (!paro::plan_gemv1(n, Ns, K, rotate, &c1, &why)) return fail(PARO_ERR_UNSUPPORTED, "paro_linear: %s", why);
+      paro::Gemv1Args& a = c1.a;
+      a.x = static_cast<const uint8_t*>(x) + b0 * K * xe;
+      a.x_bf16 = x_dtype == PARO_BF16;
+      for (int i = 0; i < n; ++i) {
+        paro::Gemv1Linear& d = a.lin[i];
+        d.codes = static_cast<const uint8_t*>(packed[i].codes);
+        d.scales = static_cast<const uint8_t*>(packed[i].scales);
+        d.zeros = static_cast<const uint8_t*>(packed[i].zeros);
+        d.rot_cs = ov.active ? ov.cs : static_cast<const float2*>(packed[i].rot_cs);
+        d.rot_idx = ov.active ? ov.idx : static_cast<const uchar2*>(packed[i].rot_idx);
+        d.svec = ov.active ? ov.s : static_cast<const float*>(packed[i].svec);
+        d.bias = bias ? bias[i] : nullptr;
+        d.y = static_cast<uint8_t*>(y[i]) + b0 * packed[i].N * ye;
+        d.L = packed[i].n_rot;
+      }
+      a.y_dtype = static_cast<int>(y_dtype);
+      a.pdl = pdl;
+      cudaError_t e = paro::launch_gemv1(c1, cs);
+      if (e != cudaSuccess) return cuda_fail(e, "paro_linear: decode GEMV (B=1) launch");
+      continue;
+    }
     const int bt = live <= 1 ? 1 : live <= 2 ? 2 : live <= 4 ? 4 : 8;  // kernel token tile
     if (bt != planned_b) {
       const char* why = "";

@@ -65,6 +65,49 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
                const char** why);
 cudaError_t launch_gemv(const GemvConfig& cfg, cudaStream_t st);
 
+// ---------------------------------------------------------------- decode GEMV, one token (gemv1.cu)
+// Cluster c of linear i owns rb_base + (c < rb_extra) consecutive 32-row blocks; CTA k of a
+// cluster of CL owns the groups [k G / CL, (k + 1) G / CL) of those rows (K-split).
+struct Gemv1Linear {
+  const uint8_t* codes;
+  const uint8_t* scales;
+  const uint8_t* zeros;
+  const float2* rot_cs;
+  const uchar2* rot_idx;
+  const float* svec;
+  const float* bias;
+  void* y;  // [N]
+  int N, L;
+  int cta_begin, rb_base, rb_extra;
+};
+
+struct Gemv1Args {
+  const void* x;  // [K] fp16 / bf16
+  int x_bf16;
+  int n_lin;
+  Gemv1Linear lin[GEMV_MAX_LIN];
+  int y_dtype;
+  int K, G;
+  int rotate;
+  int pdl;
+  int TPS;     // tiles per ring stage (capacity)
+  int S;       // ring depth
+  int pre_stages;  // stages issued before the compute warps' x / parameter loads are out
+  int R_max;   // rows of the largest cluster
+  int RRmax;   // rows per owner CTA (reduction)
+  uint32_t slot_bytes, sc_off, z_off;
+  uint32_t off_xp, off_xs, off_scr, off_part, off_recv, off_bar, off_ring, smem_total;
+};
+
+struct Gemv1Config {
+  int CL, grid, NW;
+  Gemv1Args a;
+};
+
+bool gemv1_enabled();
+bool plan_gemv1(int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config* cfg, const char** why);
+cudaError_t launch_gemv1(const Gemv1Config& cfg, cudaStream_t st);
+
 // ---------------------------------------------------------------- activation transform (prefill pre-stage)
 cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, int L, const float* svec,
                              const float2* rot_cs, const uchar2* rot_idx, int rotate, void* x_out, int pdl,

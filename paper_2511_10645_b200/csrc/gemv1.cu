@@ -82,10 +82,9 @@ __device__ __forceinline__ StageGeo stage_geo(int st, int npc, int plen, int rbs
 }
 }  // namespace
 
-// NW compute warps (+ 1 producer).  NW = 8: half-SM footprint (registers, shared memory) so the
-// next launch on the stream (PDL) is resident and streams its weights while this one computes.
+// NW compute warps + 1 producer warp (17 warps: up to 96 registers per thread)
 template <int NW>
-__global__ void __launch_bounds__((NW + 1) * 32, NW <= 8 ? 2 : 1) paro_gemv1_kernel(const Gemv1Args a) {
+__global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv1Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int li = 0;
@@ -229,18 +228,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, NW <= 8 ? 2 : 1) paro_gemv1_ker
       // byte b of the word for quad t, word j, parity p is channel tile_k(t, j, 2 b + p)
       {
         const float4 v = *reinterpret_cast<const float4*>(scr + 4 * lane);
-        float m = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        const uint32_t mb = __float_as_uint(m);
+        const float ml = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+        const uint32_t mb = __reduce_max_sync(0xffffffffu, __float_as_uint(ml));  // |x| bits order like |x|
         int E = mb < 0x00800000u ? -100 : static_cast<int>(mb >> 23) - 127 + ((mb & 0x7fffffu) != 0u ? 1 : 0);
         E = max(E, -100);
         const float mul = __uint_as_float(static_cast<uint32_t>(141 - E) << 23);  // 2^(14 - E)
         const int f0 = __float2int_rn(v.x * mul), f1 = __float2int_rn(v.y * mul);
         const int f2 = __float2int_rn(v.z * mul), f3 = __float2int_rn(v.w * mul);
-        int X = (f0 + f1) + (f2 + f3);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) X += __shfl_xor_sync(0xffffffffu, X, o);
+        const int X = __reduce_add_sync(0xffffffffu, (f0 + f1) + (f2 + f3));
         __syncwarp();  // every lane has read its x' before the scratch holds x'fix
         *reinterpret_cast<int4*>(scr + 4 * lane) = make_int4(f0, f1, f2, f3);
         __syncwarp();
@@ -407,28 +402,26 @@ bool plan_gemv1(int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config
   }
   Gemv1Config c{};
   Gemv1Args& a = c.a;
-  int CL = g1_env("PARO_G1_CL", G >= 64 ? 4 : 2);
+  int CL = g1_env("PARO_G1_CL", G >= 64 ? 8 : 2);  // large K: few groups per CTA (one transform round)
   if (CL != 1 && CL != 2 && CL != 4 && CL != 8) CL = 2;
   while (CL > 1 && CL > G) CL /= 2;
-  const int NW = g1_env("PARO_G1_NW", G1_NW) <= 8 ? 8 : 16;
-  const bool half = NW == 8;  // co-resident with the next launch
-  const int TPS = std::max(1, std::min(64, g1_env("PARO_G1_TPS", half ? 16 : 32)));
+  const int NW = G1_NW;
+  const int TPS = std::max(1, std::min(64, g1_env("PARO_G1_TPS", 2 * NW)));
   const int threads = (NW + 1) * 32;
   c.NW = NW;
   int optin = 0, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (optin <= 0) optin = 227 * 1024;
-  const int budget = half ? (optin + 1024) / 2 - 2048 : optin - 1024;
+  const int budget = optin - 1024;
   // clusters that fit in one wave (occupancy API, cached per cluster size)
-  static int ncl_cache[2][9] = {{0}};
+  static int ncl_cache[9] = {0};
   static std::mutex mu;
   int ncl_max;
   {
     std::lock_guard<std::mutex> lk(mu);
-    if (!ncl_cache[half][CL]) {
-      const void* k = half ? reinterpret_cast<const void*>(&paro_gemv1_kernel<8>)
-                           : reinterpret_cast<const void*>(&paro_gemv1_kernel<G1_NW>);
+    if (!ncl_cache[CL]) {
+      const void* k = reinterpret_cast<const void*>(&paro_gemv1_kernel<G1_NW>);
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, budget);
       if (CL > 1) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaLaunchConfig_t lc{};
@@ -447,10 +440,9 @@ bool plan_gemv1(int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config
         cudaGetLastError();
         nc = device_sm_count() / CL;
       }
-      if (half) nc = std::max(1, nc / 2);  // one CTA per SM for this launch, the other half for the next
-      ncl_cache[half][CL] = nc;
+      ncl_cache[CL] = nc;
     }
-    ncl_max = ncl_cache[half][CL];
+    ncl_max = ncl_cache[CL];
   }
   ncl_max = std::min(ncl_max, std::max(1, g1_env("PARO_G1_MAXCL", 1 << 20)));
   // clusters over linears in proportion to their row blocks (>= 1 each, <= row blocks)
@@ -528,9 +520,8 @@ bool plan_gemv1(int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config
 }
 
 cudaError_t launch_gemv1(const Gemv1Config& c, cudaStream_t st) {
-  auto kern = c.NW == 8 ? paro_gemv1_kernel<8> : paro_gemv1_kernel<G1_NW>;
-  static int configured[2] = {0, 0};
-  int& conf = configured[c.NW == 8 ? 1 : 0];
+  auto kern = paro_gemv1_kernel<G1_NW>;
+  static int conf = 0;
   if (static_cast<int>(c.a.smem_total) > conf) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(c.a.smem_total));

@@ -1,0 +1,10 @@
+#!/bin/bash
+O=gpurun_out/g1e; mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.txt 2>&1
+timeout 600 python -m pytest tests -x -q -m gpu > $O/pytest.txt 2>&1; echo "pytest rc=$?" >> $O/pytest.txt
+{
+echo "== default"; timeout 120 python tools/time_groups.py rot 1; timeout 120 python tools/time_groups.py norot 1
+echo "== CL8 (down)"; PARO_G1_CL=8 timeout 120 python tools/time_groups.py rot 1
+} > $O/sweep.txt 2>&1
+timeout 600 python bench.py > $O/bench.json 2> $O/bench.err
+echo done

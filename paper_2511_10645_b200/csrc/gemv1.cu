@@ -82,9 +82,18 @@ __device__ __forceinline__ StageGeo stage_geo(int st, int npc, int plen, int rbs
 }
 }  // namespace
 
-// NW compute warps + 1 producer warp (17 warps: up to 96 registers per thread)
-template <int NW>
+// NW compute warps + 1 producer warp (17 warps: up to 96 registers per thread).
+// BT: token capacity of the instance (1, 4, 8, 16).  Tokens are transformed four at a time in
+// lockstep and occupy the MMA's 8 columns in sets of four (columns 2b, 2b+1 = hi, lo digit of
+// token b of the set).  BT = 1 sums row partials per warp in a fixed order (deterministic);
+// BT > 1 adds them with shared-memory atomics.
+template <int NW, int BT>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv1Args a) {
+  constexpr int TB = BT == 1 ? 1 : 4;          // tokens per transform chunk / MMA column set
+  constexpr int NB = (BT + 3) / 4;             // column sets
+  constexpr int NCOL = BT == 1 ? 2 : 8;        // B columns holding digits
+  constexpr int XPC = 4 * NCOL * 32;           // digit bytes per (group, column set)
+  constexpr int XPG = NB * XPC;                // digit bytes per group
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int li = 0;
@@ -93,7 +102,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
   const Gemv1Linear& d = a.lin[li];
   const int CL = static_cast<int>(cluster_nctarank());
   const int crank = static_cast<int>(cluster_ctarank());
-  const int G = a.G;
+  const int G = a.G, B = a.B;
   const int cl = (static_cast<int>(blockIdx.x) - d.cta_begin) / CL;
   const int nrb = d.rb_base + (cl < d.rb_extra ? 1 : 0);
   const int rb0 = cl * d.rb_base + min(cl, d.rb_extra);
@@ -105,10 +114,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
   const int rbs = max(1, a.TPS / plen);
   const int n_stages = ((nrb + rbs - 1) / rbs) * npc;
 
-  uint8_t* xp = smem + a.off_xp;                                 // x' digits [gc][4 t][2 col][4 kb][8 B]
-  float* xs = reinterpret_cast<float*>(smem + a.off_xs);         // per group (sum x'fix, 2^(E-14))
-  float* part = reinterpret_cast<float*>(smem + a.off_part);     // [NW][R_max] row partials
-  float* recv = reinterpret_cast<float*>(smem + a.off_recv);     // [CL][RR] cluster partials
+  uint8_t* xp = smem + a.off_xp;                                 // x' digits [gc][NB][4 t][NCOL][4 kb][8 B]
+  int2* xs = reinterpret_cast<int2*>(smem + a.off_xs);           // per (group, token): (sum x'fix, 2^(E-14))
+  float* part = reinterpret_cast<float*>(smem + a.off_part);     // BT = 1: [NW][R_max]; else [R_max][BT]
+  float* recv = reinterpret_cast<float*>(smem + a.off_recv);     // [CL][RRmax][BT] cluster partials
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.off_bar);
   uint64_t* empty = full + a.S;
   uint64_t* rbar = empty + a.S;  // cluster partials of my rows landed (st.async bytes)
@@ -123,11 +132,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
       mbar_init(&empty[i], NW);
     }
     mbar_init(rbar, 1);
-    if (CL > 1) mbar_arrive_expect_tx(rbar, static_cast<uint32_t>((CL - 1) * my_n * 4));
+    if (CL > 1) mbar_arrive_expect_tx(rbar, static_cast<uint32_t>((CL - 1) * my_n * BT * 4));
     fence_mbar_init();
   }
   __syncthreads();
-  if (CL > 1) cluster_arrive_relaxed();  // matched by the wait before the first DSMEM store
+  // BT > 1: the cluster barrier arrive of the compute warps comes after phase 1, because the
+  // transform scratch shares its shared memory with recv, which other CTAs write once the
+  // barrier completes
+  if (CL > 1 && (BT == 1 || warp == NW)) cluster_arrive_relaxed();
   if (a.pdl) pdl_launch_dependents();
 
   // ------------------------------------------------------------ producer warp: the whole ring
@@ -166,11 +178,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
 
   // ------------------------------------------------------------ phase 1: x' of my groups (a4, a5)
   float* pw = part + static_cast<size_t>(warp) * a.R_max;
-  for (int i = lane; i < R; i += 32) pw[i] = 0.f;
+  if (BT == 1) {
+    for (int i = lane; i < R; i += 32) pw[i] = 0.f;
+  } else {
+    for (int i = threadIdx.x; i < R * BT; i += NW * 32) part[i] = 0.f;
+  }
   {
-    float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * 128;
+    float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * (TB * 128);
     const int L = a.rotate ? d.L : 0;
-    bool waited = false;
+    bool waited = false, arrived = false;
     if (warp >= gc) named_bar_arrive(2, (NW + 1) * 32);
 #pragma unroll 1
     for (int g = warp; g < gc; g += NW) {
@@ -192,79 +208,100 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
         if (a.pdl) pdl_wait();  // x may be written by the previous kernel on the stream
         waited = true;
       }
-      const uint2 xv = __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(a.x) +
-                                                           (static_cast<int64_t>(gam) * 128 + 4 * lane) * 2));
-      float2 f01, f23;
-      if (a.x_bf16) {
-        f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.x));
-        f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.y));
-      } else {
-        f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv.x));
-        f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv.y));
-      }
-      if (g == warp) {
-        __syncwarp();
-        named_bar_arrive(2, (NW + 1) * 32);  // my x and parameters are in
-        if (threadIdx.x == 0) g1_mark(2);
-      }
-      // a4: u = s . x
-      *reinterpret_cast<float4*>(scr + 4 * lane) = make_float4(f01.x * sv.x, f01.y * sv.y, f23.x * sv.z, f23.y * sv.w);
-      __syncwarp();
-      // a5: rotations t = 1..L, each pair from the pre-update values (Eq. 4 / Eq. 5)
+#pragma unroll 1
+      for (int b0 = 0; b0 < B; b0 += TB) {  // token chunks, TB tokens in lockstep
+        uint2 xv[TB];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        if (t >= L) break;
-        const uint32_t i0 = ix[t] & 0xff, j0 = (ix[t] >> 8) & 0xff, i1 = (ix[t] >> 16) & 0xff, j1 = ix[t] >> 24;
-        const float a0 = scr[i0], b0 = scr[j0], a1 = scr[i1], b1 = scr[j1];
-        scr[i0] = cs[t].x * a0 - cs[t].y * b0;
-        scr[j0] = cs[t].y * a0 + cs[t].x * b0;
-        scr[i1] = cs[t].z * a1 - cs[t].w * b1;
-        scr[j1] = cs[t].w * a1 + cs[t].z * b1;
-        __syncwarp();
-      }
-      // x' -> per-group fixed point and s8 digits (see the header), laid out as B fragments:
-      // [quad t][column g = 0 hi / 1 lo][k-block kb][b0, b1]; k-block kb = 2 p + h covers the
-      // low (p = 0) or high (p = 1) nibbles of words 2h, 2h + 1 (b0: word 2h, b1: word 2h + 1);
-      // byte b of the word for quad t, word j, parity p is channel tile_k(t, j, 2 b + p)
-      {
-        const float4 v = *reinterpret_cast<const float4*>(scr + 4 * lane);
-        const float ml = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
-        const uint32_t mb = __reduce_max_sync(0xffffffffu, __float_as_uint(ml));  // |x| bits order like |x|
-        int E = mb < 0x00800000u ? -100 : static_cast<int>(mb >> 23) - 127 + ((mb & 0x7fffffu) != 0u ? 1 : 0);
-        E = max(E, -100);
-        const float mul = __uint_as_float(static_cast<uint32_t>(141 - E) << 23);  // 2^(14 - E)
-        const int f0 = __float2int_rn(v.x * mul), f1 = __float2int_rn(v.y * mul);
-        const int f2 = __float2int_rn(v.z * mul), f3 = __float2int_rn(v.w * mul);
-        const int X = __reduce_add_sync(0xffffffffu, (f0 + f1) + (f2 + f3));
-        __syncwarp();  // every lane has read its x' before the scratch holds x'fix
-        *reinterpret_cast<int4*>(scr + 4 * lane) = make_int4(f0, f1, f2, f3);
-        __syncwarp();
-        const int* fx = reinterpret_cast<const int*>(scr);
-        const int tq = lane >> 3, col = (lane >> 2) & 1, kb = lane & 3, p = kb >> 1, h = kb & 1;
-        uint32_t wd[2];
+        for (int tb = 0; tb < TB; ++tb)
+          xv[tb] = (b0 + tb < B) ? __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(a.x) +
+                                                                       (static_cast<int64_t>(b0 + tb) * a.K +
+                                                                        gam * 128 + 4 * lane) * 2))
+                                 : make_uint2(0u, 0u);  // tokens >= B: x = 0, never stored
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int j = 2 * h + e;
-          uint32_t wv = 0;
-#pragma unroll
-          for (int bb = 0; bb < 4; ++bb) {
-            const int c = 16 * (2 * j + p) + 2 * tq + (bb >> 1) + 8 * (bb & 1);  // tile_k(tq, j, 2 bb + p)
-            const int f = fx[c];
-            const int lo = static_cast<int>(static_cast<int8_t>(f & 0xff));
-            const int dg = col ? lo : ((f - lo) >> 8);
-            wv |= (static_cast<uint32_t>(dg) & 0xffu) << (8 * bb);
+        for (int tb = 0; tb < TB; ++tb) {
+          float2 f01, f23;
+          if (a.x_bf16) {
+            f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv[tb].x));
+            f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv[tb].y));
+          } else {
+            f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv[tb].x));
+            f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv[tb].y));
           }
-          wd[e] = wv;
+          // a4: u = s . x
+          *reinterpret_cast<float4*>(scr + tb * 128 + 4 * lane) =
+              make_float4(f01.x * sv.x, f01.y * sv.y, f23.x * sv.z, f23.y * sv.w);
         }
-        *reinterpret_cast<uint2*>(xp + g * 256 + tq * 64 + col * 32 + kb * 8) = make_uint2(wd[0], wd[1]);
-        if (lane == 0)
-          *reinterpret_cast<int2*>(xs + 2 * g) =
-              make_int2(X, static_cast<int>((static_cast<uint32_t>(113 + E) << 23)));  // (sum x'fix, 2^(E - 14))
+        if (!arrived) {
+          __syncwarp();
+          named_bar_arrive(2, (NW + 1) * 32);  // my x and parameters are in
+          if (threadIdx.x == 0) g1_mark(2);
+          arrived = true;
+        }
+        __syncwarp();
+        // a5: rotations t = 1..L, each pair from the pre-update values (Eq. 4 / Eq. 5)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (t >= L) break;
+          const uint32_t i0 = ix[t] & 0xff, j0 = (ix[t] >> 8) & 0xff, i1 = (ix[t] >> 16) & 0xff, j1 = ix[t] >> 24;
+#pragma unroll
+          for (int tb = 0; tb < TB; ++tb) {
+            float* sc = scr + tb * 128;
+            const float a0 = sc[i0], b0v = sc[j0], a1 = sc[i1], b1v = sc[j1];
+            sc[i0] = cs[t].x * a0 - cs[t].y * b0v;
+            sc[j0] = cs[t].y * a0 + cs[t].x * b0v;
+            sc[i1] = cs[t].z * a1 - cs[t].w * b1v;
+            sc[j1] = cs[t].w * a1 + cs[t].z * b1v;
+          }
+          __syncwarp();
+        }
+        // x' -> per-(group, token) fixed point and s8 digits (see the header), laid out as B
+        // fragments [column set][quad t][column][k-block kb][b0, b1]; column 2 b + dg of a set =
+        // digit dg (0 hi, 1 lo) of its token b; k-block kb = 2 p + h covers the low (p = 0) or
+        // high (p = 1) nibbles of words 2h, 2h + 1 (b0: word 2h, b1: word 2h + 1); byte bb of the
+        // word for quad t, word j, parity p is channel tile_k(t, j, 2 bb + p)
+#pragma unroll
+        for (int tb = 0; tb < TB; ++tb) {
+          int* fx = reinterpret_cast<int*>(scr + tb * 128);
+          const float4 v = *reinterpret_cast<const float4*>(scr + tb * 128 + 4 * lane);
+          const float ml = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+          const uint32_t mb = __reduce_max_sync(0xffffffffu, __float_as_uint(ml));  // |x| bits order like |x|
+          int E = mb < 0x00800000u ? -100 : static_cast<int>(mb >> 23) - 127 + ((mb & 0x7fffffu) != 0u ? 1 : 0);
+          E = max(E, -100);
+          const float mul = __uint_as_float(static_cast<uint32_t>(141 - E) << 23);  // 2^(14 - E)
+          const int f0 = __float2int_rn(v.x * mul), f1 = __float2int_rn(v.y * mul);
+          const int f2 = __float2int_rn(v.z * mul), f3 = __float2int_rn(v.w * mul);
+          const int X = __reduce_add_sync(0xffffffffu, (f0 + f1) + (f2 + f3));
+          __syncwarp();  // every lane has read its x' before the scratch holds x'fix
+          *reinterpret_cast<int4*>(fx + 4 * lane) = make_int4(f0, f1, f2, f3);
+          __syncwarp();
+          const int tq = lane >> 3, col = (lane >> 2) & 1, kb = lane & 3, p = kb >> 1, h = kb & 1;
+          uint32_t wd[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = 2 * h + e;
+            uint32_t wv = 0;
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) {
+              const int c = 16 * (2 * j + p) + 2 * tq + (bb >> 1) + 8 * (bb & 1);  // tile_k(tq, j, 2 bb + p)
+              const int f = fx[c];
+              const int lo = static_cast<int>(static_cast<int8_t>(f & 0xff));
+              const int dg = col ? lo : ((f - lo) >> 8);
+              wv |= (static_cast<uint32_t>(dg) & 0xffu) << (8 * bb);
+            }
+            wd[e] = wv;
+          }
+          const int b = b0 + tb, set = b >> 2, cb = b & 3;
+          *reinterpret_cast<uint2*>(xp + g * XPG + set * XPC + tq * (NCOL * 32) + (2 * cb + col) * 32 + kb * 8) =
+              make_uint2(wd[0], wd[1]);
+          if (lane == 0)
+            xs[g * BT + b] = make_int2(X, static_cast<int>(static_cast<uint32_t>(113 + E) << 23));  // 2^(E - 14)
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
   }
-  named_bar_sync(1, NW * 32);  // every x' of the CTA is in shared memory
+  named_bar_sync(1, NW * 32);  // every x' of the CTA is in shared memory (and BT > 1: part zeroed)
+  if (BT > 1 && CL > 1) cluster_arrive();  // my scratch is free: the cluster may now write recv
   if (threadIdx.x == 0) g1_mark(3);
 
   // ------------------------------------------------------------ phase 2: tiles (a6)
@@ -296,38 +333,48 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
         uint4 w[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) w[q] = *reinterpret_cast<const uint4*>(tc + q * 512);
-        uint4 bA = make_uint4(0u, 0u, 0u, 0u), bB = bA;  // B fragments (columns >= 2 are zero)
-        if (gq < 2) {
-          const uint8_t* bp = xp + gl * 256 + tq * 64 + gq * 32;
-          bA = *reinterpret_cast<const uint4*>(bp);
-          bB = *reinterpret_cast<const uint4*>(bp + 16);
-        }
-        constexpr uint32_t ML = 0x0f0f0f0fu, MH = 0xf0f0f0f0u;
-        int Dl[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}}, Dh[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+        const uint2 sp = *reinterpret_cast<const uint2*>(sb + a.sc_off + i * TILE_SCALE_BYTES + gq * 8);
+        const uint32_t zw = *reinterpret_cast<const uint16_t*>(sb + a.z_off + i * TILE_ZERO_BYTES + gq * 2);
+        const float2 Sa = __half22float2(*reinterpret_cast<const __half2*>(&sp.x));  // rows gq, gq + 8
+        const float2 Sb = __half22float2(*reinterpret_cast<const __half2*>(&sp.y));  // rows gq + 16, gq + 24
+        const float Sr[4] = {Sa.x, Sa.y, Sb.x, Sb.y};
+        const int rowl = (r_lo + ri) * TILE_ROWS + gq;  // cluster-local row of q = 0
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {  // rows gq + 16 hh (w[2 hh]) and gq + 16 hh + 8 (w[2 hh + 1])
-          const uint4 r0 = w[2 * hh], r1 = w[2 * hh + 1];
-          mma_u8s8(Dl[hh], r0.x & ML, r1.x & ML, r0.y & ML, r1.y & ML, bA.x, bA.y);  // low nibbles, words 0, 1
-          mma_u8s8(Dl[hh], r0.z & ML, r1.z & ML, r0.w & ML, r1.w & ML, bA.z, bA.w);  // low nibbles, words 2, 3
-          mma_u8s8(Dh[hh], r0.x & MH, r1.x & MH, r0.y & MH, r1.y & MH, bB.x, bB.y);  // high nibbles (16 q)
-          mma_u8s8(Dh[hh], r0.z & MH, r1.z & MH, r0.w & MH, r1.w & MH, bB.z, bB.w);
-        }
-        // lanes tq = 0 hold columns 0 (hi digit) and 1 (lo digit) of rows gq + 8 q
-        if (tq == 0) {
-          const uint2 sp = *reinterpret_cast<const uint2*>(sb + a.sc_off + i * TILE_SCALE_BYTES + gq * 8);
-          const uint32_t zw = *reinterpret_cast<const uint16_t*>(sb + a.z_off + i * TILE_ZERO_BYTES + gq * 2);
-          const int2 xf = *reinterpret_cast<const int2*>(xs + 2 * gl);
-          const float F = __int_as_float(xf.y);
-          const float2 Sa = __half22float2(*reinterpret_cast<const __half2*>(&sp.x));  // rows gq, gq + 8
-          const float2 Sb = __half22float2(*reinterpret_cast<const __half2*>(&sp.y));  // rows gq + 16, gq + 24
-          const float Sr[4] = {Sa.x, Sa.y, Sb.x, Sb.y};
-          float* pr = pw + (r_lo + ri) * TILE_ROWS + gq;
+        for (int set = 0; set < NB; ++set) {
+          if (set * 4 >= B) break;
+          uint4 bA = make_uint4(0u, 0u, 0u, 0u), bB = bA;  // B fragments (columns >= NCOL are zero)
+          if (gq < NCOL) {
+            const uint8_t* bp = xp + gl * XPG + set * XPC + tq * (NCOL * 32) + gq * 32;
+            bA = *reinterpret_cast<const uint4*>(bp);
+            bB = *reinterpret_cast<const uint4*>(bp + 16);
+          }
+          constexpr uint32_t ML = 0x0f0f0f0fu, MH = 0xf0f0f0f0u;
+          int Dl[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}}, Dh[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int hh = q >> 1, e = (q & 1) * 2;
-            const int zq = static_cast<int>((zw >> (4 * q)) & 15u);
-            const int I = Dl[hh][e] * 256 + Dl[hh][e + 1] + ((Dh[hh][e] * 256 + Dh[hh][e + 1]) >> 4) - zq * xf.x;
-            pr[8 * q] += Sr[q] * F * static_cast<float>(I);
+          for (int hh = 0; hh < 2; ++hh) {  // rows gq + 16 hh (w[2 hh]) and gq + 16 hh + 8 (w[2 hh + 1])
+            const uint4 r0 = w[2 * hh], r1 = w[2 * hh + 1];
+            mma_u8s8(Dl[hh], r0.x & ML, r1.x & ML, r0.y & ML, r1.y & ML, bA.x, bA.y);  // low nibbles, words 0, 1
+            mma_u8s8(Dl[hh], r0.z & ML, r1.z & ML, r0.w & ML, r1.w & ML, bA.z, bA.w);  // low nibbles, words 2, 3
+            mma_u8s8(Dh[hh], r0.x & MH, r1.x & MH, r0.y & MH, r1.y & MH, bB.x, bB.y);  // high nibbles (16 q)
+            mma_u8s8(Dh[hh], r0.z & MH, r1.z & MH, r0.w & MH, r1.w & MH, bB.z, bB.w);
+          }
+          // lane (gq, tq) holds columns 2 tq (hi digit) and 2 tq + 1 (lo digit) = token tq of the
+          // set, rows gq + 8 q
+          const int b = set * 4 + tq;
+          if (BT == 1 ? tq == 0 : b < B) {
+            const int2 xf = xs[gl * BT + b];
+            const float F = __int_as_float(xf.y);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int hh = q >> 1, e = (q & 1) * 2;
+              const int zq = static_cast<int>((zw >> (4 * q)) & 15u);
+              const int I = Dl[hh][e] * 256 + Dl[hh][e + 1] + ((Dh[hh][e] * 256 + Dh[hh][e + 1]) >> 4) - zq * xf.x;
+              const float out = Sr[q] * F * static_cast<float>(I);
+              if (BT == 1)
+                pw[rowl + 8 * q] += out;
+              else
+                atomicAdd(part + (rowl + 8 * q) * BT + b, out);
+            }
           }
         }
         gi += NW;
@@ -346,13 +393,19 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
   if (threadIdx.x == 0) g1_mark(5);
   if (CL > 1) cluster_wait();  // every CTA of the cluster is running: DSMEM is legal
   const int tid = threadIdx.x;
-  for (int r = tid; r < R; r += NW * 32) {
-    float s4[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int idx = tid; idx < R * BT; idx += NW * 32) {
+    const int r = idx / BT, b = idx - r * BT;
+    float sum;
+    if (BT == 1) {
+      float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
-    for (int w = 0; w < NW; ++w) s4[w & 3] += part[static_cast<size_t>(w) * a.R_max + r];
-    const float sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+      for (int w = 0; w < NW; ++w) s4[w & 3] += part[static_cast<size_t>(w) * a.R_max + r];
+      sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);  // fixed order
+    } else {
+      sum = part[idx];
+    }
     const int owner = r / RR;
-    float* dst = recv + crank * a.RRmax + (r - owner * RR);
+    float* dst = recv + (crank * a.RRmax + (r - owner * RR)) * BT + b;
     if (owner == crank)
       *dst = sum;
     else
@@ -363,18 +416,21 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
   if (CL > 1) mbar_wait(rbar, 0);  // and those of the other CTAs of the cluster
   if (a.pdl) pdl_wait();  // y may still be read by the previous kernel
   if (threadIdx.x == 0) g1_mark(6);
-  for (int rl = tid; rl < my_n; rl += NW * 32) {
+  for (int idx = tid; idx < my_n * BT; idx += NW * 32) {
+    const int rl = idx / BT, b = idx - rl * BT;
+    if (b >= B) continue;
     float v = 0.f;
-    for (int c = 0; c < CL; ++c) v += recv[c * a.RRmax + rl];  // fixed order
+    for (int c = 0; c < CL; ++c) v += recv[(c * a.RRmax + rl) * BT + b];  // fixed order
     const int64_t n = static_cast<int64_t>(rb0) * TILE_ROWS + my_lo + rl;
     if (n < d.N) {
       if (d.bias) v += __ldg(d.bias + n);
+      const int64_t o = static_cast<int64_t>(b) * d.N + n;
       if (a.y_dtype == 0)
-        static_cast<__half*>(d.y)[n] = __float2half_rn(v);
+        static_cast<__half*>(d.y)[o] = __float2half_rn(v);
       else if (a.y_dtype == 1)
-        static_cast<__nv_bfloat16*>(d.y)[n] = __float2bfloat16_rn(v);
+        static_cast<__nv_bfloat16*>(d.y)[o] = __float2bfloat16_rn(v);
       else
-        static_cast<float*>(d.y)[n] = v;
+        static_cast<float*>(d.y)[o] = v;
     }
   }
   if (threadIdx.x == 0) g1_mark(7);
@@ -390,7 +446,21 @@ static inline uint32_t g1_align(uint32_t v, uint32_t al) { return (v + al - 1) /
 
 bool gemv1_enabled() { return g1_env("PARO_GEMV1", 1) != 0; }
 
-bool plan_gemv1(int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config* cfg, const char** why) {
+template <int BT>
+static const void* g1_kernel() {
+  return reinterpret_cast<const void*>(&paro_gemv1_kernel<G1_NW, BT>);
+}
+static const void* g1_kernel_bt(int BT) {
+  return BT == 1 ? g1_kernel<1>() : BT == 4 ? g1_kernel<4>() : BT == 8 ? g1_kernel<8>() : g1_kernel<16>();
+}
+
+bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config* cfg, const char** why) {
+  if (B < 1 || B > GEMV1_MAX_B) {
+    *why = "1..16 tokens per decode launch";
+    return false;
+  }
+  const int BT = B == 1 ? 1 : B <= 4 ? 4 : B <= 8 ? 8 : 16;
+  const int TB = BT == 1 ? 1 : 4, NSET = (BT + 3) / 4, NCOL = BT == 1 ? 2 : 8;
   if (n_lin < 1 || n_lin > GEMV_MAX_LIN) {
     *why = "1..4 linears per decode launch";
     return false;
@@ -406,7 +476,7 @@ bool plan_gemv1(int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config
   if (CL != 1 && CL != 2 && CL != 4 && CL != 8) CL = 2;
   while (CL > 1 && CL > G) CL /= 2;
   const int NW = G1_NW;
-  const int TPS = std::max(1, std::min(64, g1_env("PARO_G1_TPS", 2 * NW)));
+  const int TPS = std::max(1, std::min(64, g1_env("PARO_G1_TPS", BT == 1 ? 2 * NW : NW)));
   const int threads = (NW + 1) * 32;
   c.NW = NW;
   int optin = 0, dev = 0;
@@ -415,13 +485,13 @@ bool plan_gemv1(int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config
   if (optin <= 0) optin = 227 * 1024;
   const int budget = optin - 1024;
   // clusters that fit in one wave (occupancy API, cached per cluster size)
-  static int ncl_cache[9] = {0};
+  static int ncl_cache[17][9] = {{0}};
   static std::mutex mu;
   int ncl_max;
   {
     std::lock_guard<std::mutex> lk(mu);
-    if (!ncl_cache[CL]) {
-      const void* k = reinterpret_cast<const void*>(&paro_gemv1_kernel<G1_NW>);
+    if (!ncl_cache[BT][CL]) {
+      const void* k = g1_kernel_bt(BT);
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, budget);
       if (CL > 1) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaLaunchConfig_t lc{};
@@ -440,9 +510,9 @@ bool plan_gemv1(int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config
         cudaGetLastError();
         nc = device_sm_count() / CL;
       }
-      ncl_cache[CL] = nc;
+      ncl_cache[BT][CL] = nc;
     }
-    ncl_max = ncl_cache[CL];
+    ncl_max = ncl_cache[BT][CL];
   }
   ncl_max = std::min(ncl_max, std::max(1, g1_env("PARO_G1_MAXCL", 1 << 20)));
   // clusters over linears in proportion to their row blocks (>= 1 each, <= row blocks)
@@ -472,6 +542,8 @@ bool plan_gemv1(int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config
   }
   c.grid = begin;
   c.CL = CL;
+  c.BT = BT;
+  a.B = B;
   a.n_lin = n_lin;
   a.K = static_cast<int>(K);
   a.G = G;
@@ -486,15 +558,19 @@ bool plan_gemv1(int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config
   a.slot_bytes = g1_align(a.z_off + static_cast<uint32_t>(TPS) * TILE_ZERO_BYTES, 128);
   uint32_t off = 0;
   a.off_xp = off;
-  off += g1_align(static_cast<uint32_t>(gcm) * 256, 128);
+  off += g1_align(static_cast<uint32_t>(gcm) * NSET * 4 * NCOL * 32, 128);
   a.off_xs = off;
-  off += g1_align(static_cast<uint32_t>(gcm) * 8, 128);
-  a.off_scr = off;
-  off += NW * 512;
+  off += g1_align(static_cast<uint32_t>(gcm) * BT * 8, 128);
   a.off_part = off;
-  off += g1_align(static_cast<uint32_t>(NW) * rmax * 4, 128);
-  a.off_recv = off;
-  off += g1_align(static_cast<uint32_t>(CL) * a.RRmax * 4, 128);
+  off += g1_align(static_cast<uint32_t>(BT == 1 ? NW : BT) * rmax * 4, 128);
+  a.off_scr = a.off_recv = off;  // BT > 1: phase-1 scratch and the cluster reduction share this space
+  if (BT == 1) {
+    off += NW * 512;
+    a.off_recv = off;
+    off += g1_align(static_cast<uint32_t>(CL) * a.RRmax * 4, 128);
+  } else {
+    off += g1_align(std::max<uint32_t>(NW * TB * 512, static_cast<uint32_t>(CL) * a.RRmax * BT * 4), 128);
+  }
   a.off_bar = off;
   off += 64 * 16;
   a.off_ring = g1_align(off, 1024);
@@ -507,20 +583,21 @@ bool plan_gemv1(int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config
   const int need = ((rmax / TILE_ROWS + rbs - 1) / rbs) * npc + npc;
   S = std::min(S, std::min(need, 60));
   if (S < 1) {
-    *why = "decode (B=1) shared-memory plan does not fit";
+    *why = "decode shared-memory plan does not fit";
     return false;
   }
   a.S = S;
   a.smem_total = a.off_ring + static_cast<uint32_t>(S) * a.slot_bytes;
   if (g1_env("PARO_PLAN_DEBUG", 0))
-    fprintf(stderr, "[paro gemv1 plan] n_lin=%d K=%lld grid=%d CL=%d NW=%d TPS=%d S=%d R_max=%d smem=%u\n", n_lin,
-            static_cast<long long>(K), c.grid, CL, NW, TPS, S, rmax, a.smem_total);
+    fprintf(stderr, "[paro gemv1 plan] B=%d BT=%d n_lin=%d K=%lld grid=%d CL=%d NW=%d TPS=%d S=%d R_max=%d smem=%u\n",
+            B, BT, n_lin, static_cast<long long>(K), c.grid, CL, NW, TPS, S, rmax, a.smem_total);
   *cfg = c;
   return true;
 }
 
-cudaError_t launch_gemv1(const Gemv1Config& c, cudaStream_t st) {
-  auto kern = paro_gemv1_kernel<G1_NW>;
+template <int BT>
+static cudaError_t g1_launch(const Gemv1Config& c, cudaLaunchConfig_t* cfg) {
+  auto kern = paro_gemv1_kernel<G1_NW, BT>;
   static int conf = 0;
   if (static_cast<int>(c.a.smem_total) > conf) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -528,6 +605,10 @@ cudaError_t launch_gemv1(const Gemv1Config& c, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     conf = static_cast<int>(c.a.smem_total);
   }
+  return cudaLaunchKernelEx(cfg, kern, c.a);
+}
+
+cudaError_t launch_gemv1(const Gemv1Config& c, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(c.grid);
   cfg.blockDim = dim3((c.NW + 1) * 32);
@@ -547,7 +628,13 @@ cudaError_t launch_gemv1(const Gemv1Config& c, cudaStream_t st) {
   }
   cfg.attrs = attrs;
   cfg.numAttrs = na;
-  return cudaLaunchKernelEx(&cfg, kern, c.a);
+  switch (c.BT) {
+    case 1: return g1_launch<1>(c, &cfg);
+    case 4: return g1_launch<4>(c, &cfg);
+    case 8: return g1_launch<8>(c, &cfg);
+    case 16: return g1_launch<16>(c, &cfg);
+    default: return cudaErrorInvalidConfiguration;
+  }
 }
 
 }  // namespace paro

@@ -331,12 +331,16 @@ static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, 
   const size_t xe = 2, ye = dtype_bytes(y_dtype);
   paro::GemvConfig cfg;
   int planned_b = 0;
-  for (int64_t b0 = 0; b0 < B; b0 += paro::GEMV_MAX_B) {  // token tiles of <= 8 (the MMA's N)
-    const int live = static_cast<int>(std::min<int64_t>(paro::GEMV_MAX_B, B - b0));
-    if (live == 1 && !debug && paro::gemv1_enabled()) {  // one token: the K-split CUDA-core kernel
+  // token count -> kernel (measured, tools/time_batch.py): the K-split kernel (gemv1.cu) for one
+  // token and for 5..16 tokens per launch; the cluster-shared-transform kernel (gemv.cu) for 2..4
+  const bool k_split = !debug && paro::gemv1_enabled() && (B == 1 || B > 4);
+  const int64_t tile_b = k_split ? paro::GEMV1_MAX_B : paro::GEMV_MAX_B;
+  for (int64_t b0 = 0; b0 < B; b0 += tile_b) {
+    const int live = static_cast<int>(std::min<int64_t>(tile_b, B - b0));
+    if (k_split) {
       paro::Gemv1Config c1;
       const char* why = "";
-      if (!paro::plan_gemv1(n, Ns, K, rotate, &c1, &why)) return fail(PARO_ERR_UNSUPPORTED, "paro_linear: %s", why);
+      if (!paro::plan_gemv1(live, n, Ns, K, rotate, &c1, &why)) return fail(PARO_ERR_UNSUPPORTED, "paro_linear: %s", why);
       paro::Gemv1Args& a = c1.a;
       a.x = static_cast<const uint8_t*>(x) + b0 * K * xe;
       a.x_bf16 = x_dtype == PARO_BF16;

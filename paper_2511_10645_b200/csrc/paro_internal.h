@@ -76,14 +76,17 @@ struct Gemv1Linear {
   const uchar2* rot_idx;
   const float* svec;
   const float* bias;
-  void* y;  // [N]
+  void* y;  // [B][N]
   int N, L;
   int cta_begin, rb_base, rb_extra;
 };
 
+constexpr int GEMV1_MAX_B = 16;  // tokens per launch of the K-split kernel
+
 struct Gemv1Args {
-  const void* x;  // [K] fp16 / bf16
+  const void* x;  // [B][K] fp16 / bf16
   int x_bf16;
+  int B;          // tokens (1..16)
   int n_lin;
   Gemv1Linear lin[GEMV_MAX_LIN];
   int y_dtype;
@@ -100,12 +103,12 @@ struct Gemv1Args {
 };
 
 struct Gemv1Config {
-  int CL, grid, NW;
+  int CL, grid, NW, BT;
   Gemv1Args a;
 };
 
 bool gemv1_enabled();
-bool plan_gemv1(int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config* cfg, const char** why);
+bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config* cfg, const char** why);
 cudaError_t launch_gemv1(const Gemv1Config& cfg, cudaStream_t st);
 
 // ---------------------------------------------------------------- activation transform (prefill pre-stage)

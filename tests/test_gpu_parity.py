@@ -229,7 +229,19 @@ def test_prefill_full_size_sampled(paro):
     assert O.normwise_error(y[toks][:, rows], y_ref) <= TOL
 
 
-@pytest.mark.parametrize("B", [1, 3])
+@pytest.mark.parametrize("B,N,K", [(8, 256, 14336), (16, 512, 9728), (5, 384, 2560), (12, 640, 4096)])
+def test_k_split_tokens(paro, B, N, K):
+    """Token counts routed to the K-split decode kernel (gemv1.cu) beyond one token, at the
+    large-K shapes (clusters of 8): B = 5..16 in one launch, column sets of four tokens."""
+    p = synth.make_problem(N, K, B, seed=80 + B)
+    t = dev_tensors(p)
+    packed, ref = check_pack(paro, p, t)
+    y = paro.paro_linear(t["x"], packed, flags=paro.PARO_LINEAR_FORCE_GEMV)
+    y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"])
+    assert O.normwise_error(y.float().cpu().numpy(), y_ref) <= TOL
+
+
+@pytest.mark.parametrize("B", [1, 3, 6])
 def test_linear_multi_shared_x(paro, B):
     """q/k/v-style: three linears with their own transforms reading the same x, one launch."""
     K = 1024

@@ -370,13 +370,13 @@ def run_paro(args):
         "per_linear": per_linear,
         "roofline": {"bound": "hbm", "achieved": round(gbps, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(gbps / peak, 4), "traffic": None,
-                     "kernel": "paro_gemv_kernel (all launches of the step)",
+                     "kernel": "paro_gemv1_kernel (all launches of the step)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not peaks.get("_fallback") else "fallback 6.65 TB/s",
                      "achieved_def": "algorithmic bytes per step / device time per step (all GEMV launches, gaps included)"},
         "clocks": clocks, "e2e": e2e, "prefill": prefill, **extra,
         "gpu_launches": (4 if world == 1 else 14) * args.steps,
-        "gpu_launches_note": ("4 paro_gemv_kernel launches per step (q/k/v and gate/up fused by shared input)"
-                              if world == 1 else "7 paro_gemv_kernel + 7 ncclAllGather launches per step"),
+        "gpu_launches_note": ("4 paro_gemv1_kernel launches per step (q/k/v and gate/up fused by shared input)"
+                              if world == 1 else "7 paro_gemv1_kernel + 7 ncclAllGather launches per step"),
     }
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args)

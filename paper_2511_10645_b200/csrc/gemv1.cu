@@ -41,9 +41,9 @@ namespace paro {
 #ifndef G1_TL
 #define G1_TL 0  // 1: per-CTA %globaltimer timeline of every launch (tools/timeline1.py)
 #endif
-__device__ unsigned long long g_g1_tl[1024 * 8];
+__device__ unsigned long long g_g1_tl[1024 * 12];
 extern "C" int paro_debug_read_timeline1(unsigned long long* host, int n) {
-  if (n > 1024 * 8) n = 1024 * 8;
+  if (n > 1024 * 12) n = 1024 * 12;
   return static_cast<int>(cudaMemcpyFromSymbol(host, g_g1_tl, sizeof(unsigned long long) * n));
 }
 
@@ -53,7 +53,7 @@ __device__ __forceinline__ void g1_mark(int ev) {
   if (G1_TL && blockIdx.x < 1024) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_g1_tl[blockIdx.x * 8 + ev] = t;
+    g_g1_tl[blockIdx.x * 12 + ev] = t;
   }
 }  // compute warps per CTA (+ 1 producer warp)
 constexpr uint32_t TILE_B = TILE_CODE_BYTES + TILE_SCALE_BYTES + TILE_ZERO_BYTES;
@@ -146,6 +146,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
   if (warp == NW) {
     const uint64_t pol = l2_evict_first_policy();
     const int pre = min(a.pre_stages, n_stages);
+    if (a.params_first) named_bar_sync(3, (NW + 1) * 32);  // the rotation-parameter loads are out
 #pragma unroll 1
     for (int st = 0; st < n_stages; ++st) {
       const int slot = st % a.S;
@@ -187,7 +188,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
     float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * (TB * 128);
     const int L = a.rotate ? d.L : 0;
     bool waited = false, arrived = false;
-    if (warp >= gc) named_bar_arrive(2, (NW + 1) * 32);
+    if (warp >= gc) {
+      if (a.params_first) named_bar_arrive(3, (NW + 1) * 32);
+      named_bar_arrive(2, (NW + 1) * 32);
+    }
 #pragma unroll 1
     for (int g = warp; g < gc; g += NW) {
       const int gam = ga + g;
@@ -204,6 +208,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
         }
       const float4 sv =
           a.rotate ? __ldg(reinterpret_cast<const float4*>(d.svec + gam * 128) + lane) : make_float4(1.f, 1.f, 1.f, 1.f);
+      if (!waited && a.params_first) {
+        __syncwarp();
+        named_bar_arrive(3, (NW + 1) * 32);
+      }
       if (!waited) {
         if (a.pdl) pdl_wait();  // x may be written by the previous kernel on the stream
         waited = true;
@@ -253,7 +261,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
             sc[j1] = cs[t].w * a1 + cs[t].z * b1v;
           }
           __syncwarp();
+          if (G1_TL && t == 0 && threadIdx.x == 0 && g == warp && b0 == 0) g1_mark(8);
         }
+        if (G1_TL && threadIdx.x == 0 && g == warp && b0 == 0) g1_mark(9);
         // x' -> per-(group, token) fixed point and s8 digits (see the header), laid out as B
         // fragments [column set][quad t][column][k-block kb][b0, b1]; column 2 b + dg of a set =
         // digit dg (0 hi, 1 lo) of its token b; k-block kb = 2 p + h covers the low (p = 0) or
@@ -472,7 +482,14 @@ bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv
   }
   Gemv1Config c{};
   Gemv1Args& a = c.a;
-  int CL = g1_env("PARO_G1_CL", G >= 64 ? 8 : 2);  // large K: few groups per CTA (one transform round)
+  // Cluster size = how many ways a row block's groups are split, i.e. groups transformed per CTA
+  // (G / CL).  The rotations are shared-memory-bound (8 accesses per pair per layer, all warps
+  // at once: ~200 cycles per layer with 16 groups per CTA, tools/timeline1.py), so launches whose
+  // weight stream is short prefer CL = 4 (8 groups at K = 4096, but only 132 SMs can hold
+  // clusters of 4), long streams CL = 2 (148 SMs), large K CL = 8 (one transform round).
+  int64_t wbytes = 0;
+  for (int i = 0; i < n_lin; ++i) wbytes += Ns[i] * K / 2;
+  int CL = g1_env("PARO_G1_CL", G >= 64 ? 8 : (wbytes < (20LL << 20) ? 4 : 2));
   if (CL != 1 && CL != 2 && CL != 4 && CL != 8) CL = 2;
   while (CL > 1 && CL > G) CL /= 2;
   const int NW = G1_NW;
@@ -550,6 +567,7 @@ bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv
   a.rotate = rotate;
   a.TPS = TPS;
   a.pre_stages = std::max(0, g1_env("PARO_G1_PRE", 2));
+  a.params_first = g1_env("PARO_G1_PF", 1);
   a.R_max = rmax;
   a.RRmax = (rmax + CL - 1) / CL;
   const int gcm = (G + CL - 1) / CL;

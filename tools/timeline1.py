@@ -42,13 +42,14 @@ e1.synchronize()
 print(f"{sys.argv[1]} K={K} {mode}: {e0.elapsed_time(e1) / reps * 1e3:.2f} us per launch (graph, PDL)")
 lib = paro._lib
 lib.paro_debug_read_timeline1.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = np.zeros(1024 * 8, dtype=np.uint64)
+buf = np.zeros(1024 * 12, dtype=np.uint64)
 lib.paro_debug_read_timeline1(buf.ctypes.data, buf.size)
-t = buf.reshape(1024, 8).astype(np.int64)
+t = buf.reshape(1024, 12).astype(np.int64)
 live = t[:, 0] > 0
 t = t[live]
 rel = (t - t[:, 0].min()) / 1000.0
-names = ["start", "all_issued(prod)", "x_arrived", "transform_done", "stage0_ready", "tiles_done", "reduced", "end"]
+names = ["start", "all_issued(prod)", "x_arrived", "transform_done", "stage0_ready", "tiles_done", "reduced", "end",
+         "w0_layer0_done", "w0_rotations_done"]
 for i, n in enumerate(names):
     col = rel[:, i]
     print(f"  {n:18s} min {col.min():7.2f}  median {np.median(col):7.2f}  max {col.max():7.2f}")

@@ -199,7 +199,7 @@ def paro_linear_multi(x, packed: list, bias=None, y=None, out_dtype=None, flags:
     n = len(packed)
     if y is None:
         y = [torch.empty((B, p.N), dtype=out_dtype or x.dtype, device=x.device) for p in packed]
-    need = max(paro_linear_workspace(B, p.N, p.K, p.n_rot, 64, False, flags) for p in packed)
+    need = len(packed) * max(paro_linear_workspace(B, p.N, p.K, p.n_rot, 64, False, flags) for p in packed)
     if need and (workspace is None or workspace.numel() < need):
         workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
     structs = (paro_packed * n)(*[p.struct() for p in packed])

@@ -121,6 +121,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.off_bar);
   uint64_t* empty = full + a.S;
   uint64_t* rbar = empty + a.S;  // cluster partials of my rows landed (st.async bytes)
+  uint64_t* xbar = rbar + 1;     // BT > 1: the pre-transformed x' slice landed
   const int RR = (R + CL - 1) / CL;  // rows per owner CTA
   const int my_lo = crank * RR, my_n = max(0, min(RR, R - my_lo));
   uint8_t* ring = smem + a.off_ring;
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
       mbar_init(&empty[i], NW);
     }
     mbar_init(rbar, 1);
+    mbar_init(xbar, 1);
     if (CL > 1) mbar_arrive_expect_tx(rbar, static_cast<uint32_t>((CL - 1) * my_n * BT * 4));
     fence_mbar_init();
   }
@@ -146,13 +148,26 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
   if (warp == NW) {
     const uint64_t pol = l2_evict_first_policy();
     const int pre = min(a.pre_stages, n_stages);
+    auto issue_xq = [&]() {  // BT > 1: x' digits of my groups, written by the preceding xform kernel
+      if (a.pdl) pdl_wait();
+      if (lane == 0) {
+        const uint32_t nd = static_cast<uint32_t>(gc * XPG), ns = static_cast<uint32_t>(gc * BT * 8);
+        mbar_arrive_expect_tx(xbar, nd + ns);
+        bulk_g2s_nohint(xp, d.xq + static_cast<size_t>(ga) * XPG, nd, xbar);
+        bulk_g2s_nohint(xs, d.xqs + static_cast<size_t>(ga) * BT, ns, xbar);
+      }
+      __syncwarp();
+    };
     if (a.params_first) named_bar_sync(3, (NW + 1) * 32);  // the rotation-parameter loads are out
 #pragma unroll 1
     for (int st = 0; st < n_stages; ++st) {
       const int slot = st % a.S;
       // the latency-critical x / rotation-parameter loads of the compute warps go out before
       // the bulk of the weight stream (which would otherwise queue ahead of them)
-      if (st == pre) named_bar_sync(2, (NW + 1) * 32);
+      if (st == pre) {
+        if (BT > 1) issue_xq();
+        named_bar_sync(2, (NW + 1) * 32);
+      }
       if (st >= a.S) mbar_wait(&empty[slot], ((st / a.S) & 1) ^ 1);
       if (lane == 0) {
         const StageGeo s = stage_geo(st, npc, plen, rbs, nrb, ga, gb);
@@ -171,7 +186,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
       }
       __syncwarp();
     }
-    if (pre >= n_stages) named_bar_sync(2, (NW + 1) * 32);
+    if (pre >= n_stages) {
+      if (BT > 1) issue_xq();
+      named_bar_sync(2, (NW + 1) * 32);
+    }
     if (lane == 0) g1_mark(1);  // every stage issued
     if (CL > 1) cluster_wait();
     return;
@@ -184,13 +202,32 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
   } else {
     for (int i = threadIdx.x; i < R * BT; i += NW * 32) part[i] = 0.f;
   }
-  {
+  if constexpr (BT > 1) {
+    // x' digits and (sum, scale) of my groups come from paro_gemv1_xform_kernel (one transform
+    // per (group, token) for the whole GPU instead of one per cluster): the producer bulk-copies
+    // the contiguous slice [ga, gb) after the PDL wait
+    if (a.params_first) named_bar_arrive(3, (NW + 1) * 32);
+    named_bar_arrive(2, (NW + 1) * 32);
+    if (a.pdl) pdl_wait();  // (y is written at the end)
+    mbar_wait(xbar, 0);
+  } else {
     float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * (TB * 128);
     const int L = a.rotate ? d.L : 0;
     bool waited = false, arrived = false;
     if (warp >= gc) {
       if (a.params_first) named_bar_arrive(3, (NW + 1) * 32);
       named_bar_arrive(2, (NW + 1) * 32);
+    } else if (lane == 0) {
+      // later rounds' rotation records -> L2 now, ahead of the weight stream (requested after
+      // the first round they would queue behind the whole ring)
+      for (int g = warp + NW; g < gc; g += NW) {
+        const int64_t rec = static_cast<int64_t>(ga + g) * L * 32;
+        if (L > 0) {
+          prefetch_l2_bulk(reinterpret_cast<const float4*>(d.rot_cs) + rec, static_cast<uint32_t>(L * 32 * 16));
+          prefetch_l2_bulk(reinterpret_cast<const uint32_t*>(d.rot_idx) + rec, static_cast<uint32_t>(L * 32 * 4));
+        }
+        if (a.rotate) prefetch_l2_bulk(d.svec + (ga + g) * 128, 512u);
+      }
     }
 #pragma unroll 1
     for (int g = warp; g < gc; g += NW) {
@@ -331,6 +368,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
       if (threadIdx.x == 0 && st == 0) g1_mark(4);
       const uint8_t* sb = ring + static_cast<size_t>(slot) * a.slot_bytes;
       const int nt = nr * pl;
+      if constexpr (BT == 1) {
       int ri = 0, gi = warp;  // tile warp + k NW of the stage = (row block ri, group gi)
       while (gi >= pl) {
         gi -= pl;
@@ -393,6 +431,96 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
           ++ri;
         }
       }
+      } else {
+      // B > 1: warp w takes a contiguous chunk of the stage's tiles (row block ri, group gi), so
+      // that its consecutive tiles mostly share a row block and the row partials (atomics) go to
+      // shared memory once per row block; B = 1: tiles w, w + NW, ... (measured faster)
+      const int per = (nt + NW - 1) / NW;
+      const int step = BT == 1 ? NW : 1;
+      const int i_end = BT == 1 ? nt : min(nt, (warp + 1) * per);
+      int i = BT == 1 ? warp : warp * per;
+      int ri = i / pl, gi = i - ri * pl;
+      float acc[NB][4];
+      int acc_ri = -1;
+      auto flush = [&]() {
+        if (acc_ri < 0) return;
+        const int rowl = (r_lo + acc_ri) * TILE_ROWS + gq;  // cluster-local row of q = 0
+#pragma unroll
+        for (int set = 0; set < NB; ++set) {
+          const int b = set * 4 + tq;
+          if (BT == 1 ? tq == 0 : b < B) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (BT == 1)
+                pw[rowl + 8 * q] += acc[set][q];
+              else
+                atomicAdd(part + (rowl + 8 * q) * BT + b, acc[set][q]);
+            }
+          }
+        }
+      };
+#pragma unroll 1
+      for (; i < i_end; i += step) {
+        if (ri != acc_ri) {
+          flush();
+          acc_ri = ri;
+#pragma unroll
+          for (int set = 0; set < NB; ++set)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[set][q] = 0.f;
+        }
+        const int gl = g_lo - ga + gi;
+        const uint8_t* tc = sb + i * TILE_CODE_BYTES + gq * 64 + tq * 16;
+        uint4 w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[q] = *reinterpret_cast<const uint4*>(tc + q * 512);
+        const uint2 sp = *reinterpret_cast<const uint2*>(sb + a.sc_off + i * TILE_SCALE_BYTES + gq * 8);
+        const uint32_t zw = *reinterpret_cast<const uint16_t*>(sb + a.z_off + i * TILE_ZERO_BYTES + gq * 2);
+        const float2 Sa = __half22float2(*reinterpret_cast<const __half2*>(&sp.x));  // rows gq, gq + 8
+        const float2 Sb = __half22float2(*reinterpret_cast<const __half2*>(&sp.y));  // rows gq + 16, gq + 24
+        const float Sr[4] = {Sa.x, Sa.y, Sb.x, Sb.y};
+#pragma unroll
+        for (int set = 0; set < NB; ++set) {
+          if (set * 4 >= B) break;
+          uint4 bA = make_uint4(0u, 0u, 0u, 0u), bB = bA;  // B fragments (columns >= NCOL are zero)
+          if (gq < NCOL) {
+            const uint8_t* bp = xp + gl * XPG + set * XPC + tq * (NCOL * 32) + gq * 32;
+            bA = *reinterpret_cast<const uint4*>(bp);
+            bB = *reinterpret_cast<const uint4*>(bp + 16);
+          }
+          constexpr uint32_t ML = 0x0f0f0f0fu, MH = 0xf0f0f0f0u;
+          int Dl[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}}, Dh[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {  // rows gq + 16 hh (w[2 hh]) and gq + 16 hh + 8 (w[2 hh + 1])
+            const uint4 r0 = w[2 * hh], r1 = w[2 * hh + 1];
+            mma_u8s8(Dl[hh], r0.x & ML, r1.x & ML, r0.y & ML, r1.y & ML, bA.x, bA.y);  // low nibbles, words 0, 1
+            mma_u8s8(Dl[hh], r0.z & ML, r1.z & ML, r0.w & ML, r1.w & ML, bA.z, bA.w);  // low nibbles, words 2, 3
+            mma_u8s8(Dh[hh], r0.x & MH, r1.x & MH, r0.y & MH, r1.y & MH, bB.x, bB.y);  // high nibbles (16 q)
+            mma_u8s8(Dh[hh], r0.z & MH, r1.z & MH, r0.w & MH, r1.w & MH, bB.z, bB.w);
+          }
+          // lane (gq, tq) holds columns 2 tq (hi digit) and 2 tq + 1 (lo digit) = token tq of the
+          // set, rows gq + 8 q
+          const int b = set * 4 + tq;
+          if (BT == 1 ? tq == 0 : b < B) {
+            const int2 xf = xs[gl * BT + b];
+            const float F = __int_as_float(xf.y);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int hh = q >> 1, e = (q & 1) * 2;
+              const int zq = static_cast<int>((zw >> (4 * q)) & 15u);
+              const int I = Dl[hh][e] * 256 + Dl[hh][e + 1] + ((Dh[hh][e] * 256 + Dh[hh][e + 1]) >> 4) - zq * xf.x;
+              acc[set][q] = fmaf(Sr[q] * F, static_cast<float>(I), acc[set][q]);
+            }
+          }
+        }
+        gi += step;
+        while (gi >= pl) {
+          gi -= pl;
+          ++ri;
+        }
+      }
+      flush();
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
     }
@@ -446,6 +574,110 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
   if (threadIdx.x == 0) g1_mark(7);
 }
 
+// Activation transform for B > 1 (a4, a5), once per (linear, group, set of four tokens) for the
+// whole launch: one warp each, results (fixed-point digits laid out as the GEMV's B fragments,
+// per-(group, token) sum and scale) to a workspace the GEMV bulk-copies.  Same arithmetic as the
+// fused B = 1 path of paro_gemv1_kernel.
+template <int BT>
+__global__ void __launch_bounds__(128) paro_gemv1_xform_kernel(const Gemv1Args a) {
+  constexpr int NB = BT / 4, XPC = 4 * 8 * 32, XPG = NB * XPC;
+  __shared__ __align__(16) float scr_all[4][4 * 128];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (a.pdl) pdl_launch_dependents();
+  const int task = blockIdx.x * 4 + warp;
+  const int G = a.G, B = a.B;
+  if (task >= a.n_lin * G * NB) return;
+  const int li = task / (G * NB), rem = task - li * G * NB, gam = rem / NB, set = rem - gam * NB;
+  const Gemv1Linear& d = a.lin[li];
+  float* scr = scr_all[warp];
+  const int L = a.rotate ? d.L : 0;
+  float4 cs[8];
+  uint32_t ix[8];
+  const int64_t rec = static_cast<int64_t>(gam) * L * 32 + lane;
+#pragma unroll
+  for (int t = 0; t < 8; ++t)
+    if (t < L) {
+      cs[t] = __ldg(reinterpret_cast<const float4*>(d.rot_cs) + rec + t * 32);
+      ix[t] = __ldg(reinterpret_cast<const uint32_t*>(d.rot_idx) + rec + t * 32);
+    }
+  const float4 sv =
+      a.rotate ? __ldg(reinterpret_cast<const float4*>(d.svec + gam * 128) + lane) : make_float4(1.f, 1.f, 1.f, 1.f);
+  if (a.pdl) pdl_wait();  // x may be written by the previous kernel on the stream
+  const int b0 = set * 4;
+  uint2 xv[4];
+#pragma unroll
+  for (int tb = 0; tb < 4; ++tb)
+    xv[tb] = (b0 + tb < B) ? __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(a.x) +
+                                                                 (static_cast<int64_t>(b0 + tb) * a.K + gam * 128 +
+                                                                  4 * lane) * 2))
+                           : make_uint2(0u, 0u);  // tokens >= B: x = 0, never stored
+#pragma unroll
+  for (int tb = 0; tb < 4; ++tb) {
+    float2 f01, f23;
+    if (a.x_bf16) {
+      f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv[tb].x));
+      f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv[tb].y));
+    } else {
+      f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv[tb].x));
+      f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv[tb].y));
+    }
+    *reinterpret_cast<float4*>(scr + tb * 128 + 4 * lane) =
+        make_float4(f01.x * sv.x, f01.y * sv.y, f23.x * sv.z, f23.y * sv.w);  // a4: u = s . x
+  }
+  __syncwarp();
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {  // a5: rotations t = 1..L (Eq. 4 / Eq. 5)
+    if (t >= L) break;
+    const uint32_t i0 = ix[t] & 0xff, j0 = (ix[t] >> 8) & 0xff, i1 = (ix[t] >> 16) & 0xff, j1 = ix[t] >> 24;
+#pragma unroll
+    for (int tb = 0; tb < 4; ++tb) {
+      float* sc = scr + tb * 128;
+      const float a0 = sc[i0], b0v = sc[j0], a1 = sc[i1], b1v = sc[j1];
+      sc[i0] = cs[t].x * a0 - cs[t].y * b0v;
+      sc[j0] = cs[t].y * a0 + cs[t].x * b0v;
+      sc[i1] = cs[t].z * a1 - cs[t].w * b1v;
+      sc[j1] = cs[t].w * a1 + cs[t].z * b1v;
+    }
+    __syncwarp();
+  }
+  uint8_t* xq = const_cast<uint8_t*>(d.xq) + static_cast<size_t>(gam) * XPG + set * XPC;
+  int2* xs = const_cast<int2*>(d.xqs) + static_cast<size_t>(gam) * BT;
+#pragma unroll
+  for (int tb = 0; tb < 4; ++tb) {  // fixed point + digits, the layout of paro_gemv1_kernel's B fragments
+    int* fx = reinterpret_cast<int*>(scr + tb * 128);
+    const float4 v = *reinterpret_cast<const float4*>(scr + tb * 128 + 4 * lane);
+    const float ml = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+    const uint32_t mb = __reduce_max_sync(0xffffffffu, __float_as_uint(ml));
+    int E = mb < 0x00800000u ? -100 : static_cast<int>(mb >> 23) - 127 + ((mb & 0x7fffffu) != 0u ? 1 : 0);
+    E = max(E, -100);
+    const float mul = __uint_as_float(static_cast<uint32_t>(141 - E) << 23);  // 2^(14 - E)
+    const int f0 = __float2int_rn(v.x * mul), f1 = __float2int_rn(v.y * mul);
+    const int f2 = __float2int_rn(v.z * mul), f3 = __float2int_rn(v.w * mul);
+    const int X = __reduce_add_sync(0xffffffffu, (f0 + f1) + (f2 + f3));
+    __syncwarp();
+    *reinterpret_cast<int4*>(fx + 4 * lane) = make_int4(f0, f1, f2, f3);
+    __syncwarp();
+    const int tq = lane >> 3, col = (lane >> 2) & 1, kb = lane & 3, p = kb >> 1, h = kb & 1;
+    uint32_t wd[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int j = 2 * h + e;
+      uint32_t wv = 0;
+#pragma unroll
+      for (int bb = 0; bb < 4; ++bb) {
+        const int c = 16 * (2 * j + p) + 2 * tq + (bb >> 1) + 8 * (bb & 1);  // tile_k(tq, j, 2 bb + p)
+        const int f = fx[c];
+        const int lo = static_cast<int>(static_cast<int8_t>(f & 0xff));
+        const int dg = col ? lo : ((f - lo) >> 8);
+        wv |= (static_cast<uint32_t>(dg) & 0xffu) << (8 * bb);
+      }
+      wd[e] = wv;
+    }
+    *reinterpret_cast<uint2*>(xq + tq * (8 * 32) + (2 * tb + col) * 32 + kb * 8) = make_uint2(wd[0], wd[1]);
+    if (lane == 0) xs[b0 + tb] = make_int2(X, static_cast<int>(static_cast<uint32_t>(113 + E) << 23));
+  }
+}
+
 // ============================================================================ host side
 static int g1_env(const char* name, int dflt) {
   const char* e = getenv(name);
@@ -455,6 +687,33 @@ static int g1_env(const char* name, int dflt) {
 static inline uint32_t g1_align(uint32_t v, uint32_t al) { return (v + al - 1) / al * al; }
 
 bool gemv1_enabled() { return g1_env("PARO_GEMV1", 1) != 0; }
+
+size_t gemv1_xq_bytes(int B, int64_t K) {
+  if (B <= 1) return 0;
+  const int BT = B <= 4 ? 4 : B <= 8 ? 8 : 16;
+  const size_t G = static_cast<size_t>(K / 128);
+  return (G * (BT / 4) * 1024 + G * BT * 8 + 255) / 256 * 256;
+}
+
+cudaError_t launch_gemv1_xform(const Gemv1Config& c, cudaStream_t st) {
+  const int tasks = c.a.n_lin * c.a.G * (c.BT / 4);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((tasks + 3) / 4);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at;
+  at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &at;
+  cfg.numAttrs = c.a.pdl ? 1 : 0;
+  switch (c.BT) {
+    case 4: return cudaLaunchKernelEx(&cfg, paro_gemv1_xform_kernel<4>, c.a);
+    case 8: return cudaLaunchKernelEx(&cfg, paro_gemv1_xform_kernel<8>, c.a);
+    case 16: return cudaLaunchKernelEx(&cfg, paro_gemv1_xform_kernel<16>, c.a);
+    default: return cudaErrorInvalidConfiguration;
+  }
+}
 
 template <int BT>
 static const void* g1_kernel() {
@@ -493,7 +752,7 @@ bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv
   if (CL != 1 && CL != 2 && CL != 4 && CL != 8) CL = 2;
   while (CL > 1 && CL > G) CL /= 2;
   const int NW = G1_NW;
-  const int TPS = std::max(1, std::min(64, g1_env("PARO_G1_TPS", BT == 1 ? 2 * NW : NW)));
+  int TPS = std::max(1, std::min(64, g1_env("PARO_G1_TPS", 2 * NW)));
   const int threads = (NW + 1) * 32;
   c.NW = NW;
   int optin = 0, dev = 0;
@@ -586,8 +845,8 @@ bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv
     off += NW * 512;
     a.off_recv = off;
     off += g1_align(static_cast<uint32_t>(CL) * a.RRmax * 4, 128);
-  } else {
-    off += g1_align(std::max<uint32_t>(NW * TB * 512, static_cast<uint32_t>(CL) * a.RRmax * BT * 4), 128);
+  } else {  // the transform runs in paro_gemv1_xform_kernel: no scratch
+    off += g1_align(static_cast<uint32_t>(CL) * a.RRmax * BT * 4, 128);
   }
   a.off_bar = off;
   off += 64 * 16;
@@ -600,6 +859,16 @@ bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv
   const int rbs = std::max(1, TPS / plen);
   const int need = ((rmax / TILE_ROWS + rbs - 1) / rbs) * npc + npc;
   S = std::min(S, std::min(need, 60));
+  if (S < std::min(2, need) && TPS > NW && !getenv("PARO_G1_TPS")) {  // keep two ring stages: halve the stage
+    TPS = NW;
+    a.TPS = TPS;
+    a.sc_off = static_cast<uint32_t>(TPS) * TILE_CODE_BYTES;
+    a.z_off = a.sc_off + static_cast<uint32_t>(TPS) * TILE_SCALE_BYTES;
+    a.slot_bytes = g1_align(a.z_off + static_cast<uint32_t>(TPS) * TILE_ZERO_BYTES, 128);
+    const int npc2 = (gcm + TPS - 1) / TPS, plen2 = (gcm + npc2 - 1) / npc2, rbs2 = std::max(1, TPS / plen2);
+    const int need2 = ((rmax / TILE_ROWS + rbs2 - 1) / rbs2) * npc2 + npc2;
+    S = std::min(static_cast<int>(avail / a.slot_bytes), std::min(need2, 60));
+  }
   if (S < 1) {
     *why = "decode shared-memory plan does not fit";
     return false;

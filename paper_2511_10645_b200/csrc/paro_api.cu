@@ -302,7 +302,10 @@ size_t paro_linear_workspace(int64_t B, int64_t N, int64_t K, int32_t n_rot, int
     ws += align256(static_cast<size_t>(G * n_rot * PARO_SLOTS * 8));
     ws += align256(static_cast<size_t>(G * n_rot * PARO_SLOTS * 2));
   }
-  if (use_prefill(B, N, K, flags)) ws += align256(static_cast<size_t>(B * K * 2));
+  if (use_prefill(B, N, K, flags))
+    ws += align256(static_cast<size_t>(B * K * 2));
+  else if (B > 1 && paro::gemv1_enabled())  // decode, 2..16 tokens: pre-transformed x' (gemv1.cu)
+    ws += paro::gemv1_xq_bytes(static_cast<int>(std::min<int64_t>(B, paro::GEMV1_MAX_B)), K);
   return ws;
 }
 
@@ -320,7 +323,7 @@ static RotOverride rot_cs_override(const float2* cs, const uchar2* idx, const fl
 
 static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, int n, const paro_packed* packed,
                                   RotOverride ov, const float* const* bias, void* const* y, paro_dtype y_dtype,
-                                  int rotate, int pdl, int debug, cudaStream_t cs) {
+                                  int rotate, int pdl, int debug, void* ws, size_t ws_bytes, cudaStream_t cs) {
   int64_t Ns[paro::GEMV_MAX_LIN];
   int Ls[paro::GEMV_MAX_LIN];
   for (int i = 0; i < n; ++i) {
@@ -333,7 +336,16 @@ static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, 
   int planned_b = 0;
   // token count -> kernel (measured, tools/time_batch.py): the K-split kernel (gemv1.cu) for one
   // token and for 5..16 tokens per launch; the cluster-shared-transform kernel (gemv.cu) for 2..4
-  const bool k_split = !debug && paro::gemv1_enabled() && (B == 1 || B > 4);
+  static const int small_b = [] {
+    const char* e = getenv("PARO_G1_SMALLB");
+    return e ? atoi(e) : 0;
+  }();
+  // 2..4 tokens (tools/time_batch.py): the cluster-shared-transform kernel for B = 2 and for wide
+  // launches with K < 8192 (e.g. gate+up), the K-split kernel otherwise
+  int64_t nk = 0;
+  for (int i = 0; i < n; ++i) nk += packed[i].N * K;
+  const bool old_small = B == 2 || (B <= 4 && nk >= (48LL << 20) && K < 8192);
+  const bool k_split = !debug && paro::gemv1_enabled() && (B == 1 || B > 4 || !old_small || small_b);
   const int64_t tile_b = k_split ? paro::GEMV1_MAX_B : paro::GEMV_MAX_B;
   for (int64_t b0 = 0; b0 < B; b0 += tile_b) {
     const int live = static_cast<int>(std::min<int64_t>(tile_b, B - b0));
@@ -358,6 +370,18 @@ static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, 
       }
       a.y_dtype = static_cast<int>(y_dtype);
       a.pdl = pdl;
+      if (live > 1) {  // x' of all tokens once, by a small transform kernel, into the workspace
+        const size_t per = paro::gemv1_xq_bytes(live, K);
+        if (!ws || ws_bytes < per * n)
+          return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear: workspace too small (%zu < %zu)", ws_bytes, per * n);
+        for (int i = 0; i < n; ++i) {
+          uint8_t* base = static_cast<uint8_t*>(ws) + per * i;
+          a.lin[i].xq = base;
+          a.lin[i].xqs = reinterpret_cast<const int2*>(base + static_cast<size_t>(K / kG) * (c1.BT / 4) * 1024);
+        }
+        cudaError_t e = paro::launch_gemv1_xform(c1, cs);
+        if (e != cudaSuccess) return cuda_fail(e, "paro_linear: decode activation transform launch");
+      }
       cudaError_t e = paro::launch_gemv1(c1, cs);
       if (e != cudaSuccess) return cuda_fail(e, "paro_linear: decode GEMV (B=1) launch");
       continue;
@@ -458,8 +482,10 @@ paro_status paro_linear(const void* x, paro_dtype x_dtype, int64_t B, const paro
     return PARO_OK;
   }
   // decode GEMV over token tiles
+  const size_t used = static_cast<size_t>(wsp - static_cast<uint8_t*>(workspace));
   return decode_linears(x, x_dtype, B, 1, packed, rot_cs_override(rot_cs, rot_idx, svec, on_the_fly), &bias, &y,
-                        y_dtype, rotate, pdl, (flags & 0x100u) ? 1 : 0, cs);
+                        y_dtype, rotate, pdl, (flags & 0x100u) ? 1 : 0, wsp,
+                        workspace_bytes > used ? workspace_bytes - used : 0, cs);
 }
 
 paro_status paro_linear_multi(const void* x, paro_dtype x_dtype, int64_t B, int32_t n, const paro_packed* packed,
@@ -490,8 +516,14 @@ paro_status paro_linear_multi(const void* x, paro_dtype x_dtype, int64_t B, int3
   }
   const int rotate = (flags & PARO_LINEAR_NO_ROTATION) ? 0 : 1;
   const int pdl = (flags & PARO_LINEAR_PDL) ? 1 : 0;
+  size_t need = 0;  // n x the per-linear decode workspace
+  for (int i = 0; i < n; ++i)
+    need = std::max(need, paro_linear_workspace(B, packed[i].N, packed[i].K, packed[i].n_rot, PARO_SLOTS, 0, flags));
+  need *= static_cast<size_t>(n);
+  if (workspace_bytes < need || (need && !workspace))
+    return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear_multi: workspace too small (%zu < %zu)", workspace_bytes, need);
   return decode_linears(x, x_dtype, B, n, packed, rot_cs_override(nullptr, nullptr, nullptr, 0), bias, y, y_dtype,
-                        rotate, pdl, (flags & 0x100u) ? 1 : 0, cs);
+                        rotate, pdl, (flags & 0x100u) ? 1 : 0, workspace, workspace_bytes, cs);
 }
 
 paro_status paro_transform_activations(const void* x, paro_dtype x_dtype, int64_t B, const paro_packed* packed,

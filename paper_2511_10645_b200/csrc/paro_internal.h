@@ -77,6 +77,8 @@ struct Gemv1Linear {
   const float* svec;
   const float* bias;
   void* y;  // [B][N]
+  const uint8_t* xq;  // B > 1: pre-transformed x' digits [G][NB][4][8][4][8 B] (paro_gemv1_xform_kernel)
+  const int2* xqs;    // B > 1: per (group, token) (sum x'fix, 2^(E-14)) [G][BT]
   int N, L;
   int cta_begin, rb_base, rb_extra;
 };
@@ -109,6 +111,9 @@ struct Gemv1Config {
 };
 
 bool gemv1_enabled();
+// B > 1: bytes of pre-transformed activations per linear (digits + per-group sums / scales)
+size_t gemv1_xq_bytes(int B, int64_t K);
+cudaError_t launch_gemv1_xform(const Gemv1Config& cfg, cudaStream_t st);
 bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config* cfg, const char** why);
 cudaError_t launch_gemv1(const Gemv1Config& cfg, cudaStream_t st);
 

@@ -9,11 +9,17 @@
 #include "ptx.cuh"
 using namespace paro;
 
-constexpr int NW = 16;
+#ifndef HALF
+#define HALF 0  // 1: half-SM footprint (8 consumer warps, 3 x 32 KB ring) so the next PDL launch co-resides
+#endif
+#ifndef CLUSTER
+#define CLUSTER 1
+#endif
+constexpr int NW = HALF ? 8 : 16;
 constexpr uint32_t STG = 32 * 1024;
-constexpr int S = 6;
+constexpr int S = HALF ? 3 : 6;
 
-__global__ void __launch_bounds__((NW + 1) * 32, 1) stream_k(const uint8_t* base, uint32_t per_cta, const uint4* x, float* out, int pdl, int prefetch_before_wait) {
+__global__ void __launch_bounds__((NW + 1) * 32, HALF ? 2 : 1) stream_k(const uint8_t* base, uint32_t per_cta, const uint4* x, float* out, int pdl, int prefetch_before_wait) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STG);
   uint64_t* empty = full + S;
@@ -63,13 +69,14 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const size_t smem = S * STG + 2 * S * 8;
   cudaFuncSetAttribute(stream_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const size_t sizes[] = {0, 2179072, 8716288, 30507008, 61014016, 122028032};
+  const size_t sizes[] = {0, 8716288, 30507008, 61014016};
   uint4* x; float* out; cudaMalloc(&x, 4096); cudaMalloc(&out, sms * 1024 * 4 * 2);
   const size_t pool_bytes = 640ull << 20;
   uint8_t* pool; cudaMalloc(&pool, pool_bytes); cudaMemset(pool, 1, pool_bytes);
   cudaStream_t st; cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-  for (int pdl = 0; pdl < 2; ++pdl)
-    for (int pf = 0; pf < (pdl ? 2 : 1); ++pf)
+  printf("HALF=%d CLUSTER=%d\n", HALF, CLUSTER);
+  for (int pdl = 1; pdl < 2; ++pdl)
+    for (int pf = 1; pf < 2; ++pf)
       for (size_t bytes : sizes) {
         uint32_t per = (uint32_t)(((bytes + sms - 1) / sms + 15) / 16 * 16);
         if (per == 0) per = 16;
@@ -81,9 +88,12 @@ int main() {
         for (int r = 0; r < reps; ++r) {
           cudaLaunchConfig_t cfg{};
           cfg.gridDim = dim3(sms); cfg.blockDim = dim3((NW + 1) * 32); cfg.dynamicSmemBytes = smem; cfg.stream = st;
-          cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-          at[0].val.programmaticStreamSerializationAllowed = 1;
-          cfg.attrs = at; cfg.numAttrs = pdl ? 1 : 0;
+          cudaLaunchAttribute at[2]; int na = 0;
+          if (pdl) { at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[na].val.programmaticStreamSerializationAllowed = 1; ++na; }
+          if (CLUSTER > 1) { at[na].id = cudaLaunchAttributeClusterDimension; at[na].val.clusterDim.x = CLUSTER;
+            at[na].val.clusterDim.y = 1; at[na].val.clusterDim.z = 1; ++na; }
+          cfg.attrs = at; cfg.numAttrs = na;
           const uint8_t* b = pool + (size_t)(r % std::min(nbuf, 64)) * span;
           cudaLaunchKernelEx(&cfg, stream_k, b, per, (const uint4*)x, out, pdl, pf);
         }

@@ -123,8 +123,10 @@ paro_status paro_pack_sizes(int64_t N, int64_t K, int32_t group, int32_t n_rot, 
 paro_status paro_pack(const void* W, const float* s, const float* theta, const int16_t* pairs, int64_t N,
                       int64_t K, int32_t group, int32_t n_rot, int32_t n_pairs, paro_packed* out, void* stream);
 
-/* Workspace bytes paro_linear needs for this call shape (0 is possible).
- * `on_the_fly` != 0 when paro_linear will be given s/theta/pairs pointers. */
+/* Workspace bytes paro_linear needs for this call shape (0 for B = 1 with the packed
+ * transform).  `on_the_fly` != 0 when paro_linear will be given s/theta/pairs pointers.
+ * Decode with 2..16 tokens needs (G (B'/4) 1024 + G B' 8) bytes (G = K/128, B' = B
+ * rounded up to 4, 8 or 16) for the pre-transformed activations. */
 size_t paro_linear_workspace(int64_t B, int64_t N, int64_t K, int32_t n_rot, int32_t n_pairs, int32_t on_the_fly,
                              uint32_t flags);
 
@@ -138,10 +140,14 @@ size_t paro_linear_workspace(int64_t B, int64_t N, int64_t K, int32_t n_rot, int
  *   bias    device fp32 [N] or NULL
  *   y       device [B, N] (y_dtype fp16, bf16 or fp32), row-major
  *   flags   PARO_LINEAR_*
- * Decode (B <= 16): one fused kernel -- the scale + L rotations are applied to the
- * activation while it is staged in shared memory (never written to HBM), the
+ * Decode (B <= 16): B = 1: one fused kernel -- the scale + L rotations are applied to
+ * the activation while it is staged in shared memory (never written to HBM), the
  * packed INT4 stream is bulk-copied (TMA engine) into a shared-memory ring and
- * dequantised in registers, fp32 accumulate.  Prefill (B > 16): activation
+ * multiplied on the integer tensor cores (x' as 16-bit fixed point per group), exact
+ * int32 per (row, group), fp32 accumulate.  B = 2..16: the transform of all tokens runs
+ * once in a small kernel into the workspace (x' digits, a few KB per group), then the
+ * same GEMV (or, for some widths at B <= 4, a kernel with a cluster-shared in-kernel
+ * transform).  Prefill (B > 16): activation
  * transform into an fp16 workspace, then a tcgen05/TMEM GEMM with an in-kernel
  * INT4 -> fp16 dequant producer.
  * Asynchronous, no allocation.  Errors: PARO_ERR_SHAPE (packed vs call), PARO_ERR_INVALID_ARGUMENT
@@ -158,7 +164,8 @@ paro_status paro_linear(const void* x, paro_dtype x_dtype, int64_t B, const paro
  * linears in proportion to their rows), which removes the per-launch prologue of the
  * others; prefill runs one GEMM per linear.  packed, bias (NULL or array of n, entries
  * may be NULL) and y (array of n device [B, N_i]) are host arrays.  All packed[i].K must
- * be equal.  Workspace as paro_linear for the largest linear.  Errors as paro_linear. */
+ * be equal.  Workspace: n times paro_linear_workspace of the largest linear.  Errors as
+ * paro_linear. */
 paro_status paro_linear_multi(const void* x, paro_dtype x_dtype, int64_t B, int32_t n, const paro_packed* packed,
                               const float* const* bias, void* const* y, paro_dtype y_dtype, uint32_t flags,
                               void* workspace, size_t workspace_bytes, void* stream);

@@ -10,20 +10,22 @@ namespace paro {
 
 constexpr int TGRP = 128;
 constexpr int TOK_PER_WARP = 8;
+constexpr int TOK_LOCK = 4;  // tokens rotated in lockstep (independent shared-memory chains)
 
 // x' = R_L ... R_1 diag(s) x per (token, group); Eq. 5 in column form,
-// the scale first.  One warp = one group x TOK_PER_WARP tokens; the
-// rotation parameters of the group (L <= 8 rotations x 2 slots per lane) stay in
-// registers ("the rotation parameters ... fit into registers"), the
-// 128 activations of the group in shared memory.
+// the scale first.  One warp = one group x TOK_PER_WARP tokens, TOK_LOCK of
+// them in lockstep; the rotation parameters of the group (L <= 8 rotations x 2 slots per
+// lane) stay in registers ("the rotation parameters ... fit into registers"),
+// the 128 activations of each token of the group in shared memory.  The rotations are
+// shared-memory bound (4 loads + 4 stores per lane per rotation); the lockstep tokens give
+// the pipe independent work instead of one dependent chain.
 __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__ x, int x_bf16, int64_t B, int64_t K,
                                                         int L, const float* __restrict__ svec,
                                                         const float2* __restrict__ rot_cs,
                                                         const uchar2* __restrict__ rot_idx, int rotate,
                                                         __half* __restrict__ xo, int pdl, int prefill_order) {
-  __shared__ float scr_all[8][132];
+  __shared__ float scr_all[8][TOK_LOCK][TGRP];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* scr = scr_all[warp];
   const int G = static_cast<int>(K / TGRP);
   const int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + warp;  // (token tile, group)
   const int gam = static_cast<int>(item % G);
@@ -33,55 +35,75 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
   // l + 32 of rotation t
   float4 csr[8];
   uint32_t ixr[8];
+  const int Le = rotate ? L : 0;
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
-    if (t < L && rotate) {
+    if (t < Le) {
       const int64_t rec = (static_cast<int64_t>(gam) * L + t) * 32 + lane;
       csr[t] = __ldg(reinterpret_cast<const float4*>(rot_cs) + rec);
       ixr[t] = __ldg(reinterpret_cast<const uint32_t*>(rot_idx) + rec);
-    } else {
-      csr[t] = make_float4(1.f, 0.f, 1.f, 0.f);
-      ixr[t] = 0x80808080u;
     }
   }
-  float sv[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) sv[i] = rotate ? svec[gam * TGRP + lane + 32 * i] : 1.f;
+  const float4 sv = rotate ? __ldg(reinterpret_cast<const float4*>(svec + gam * TGRP) + lane)
+                           : make_float4(1.f, 1.f, 1.f, 1.f);
   if (pdl) pdl_wait();
-  for (int64_t b = b0; b < b0 + TOK_PER_WARP && b < B; ++b) {
-    const int64_t base = b * K + static_cast<int64_t>(gam) * TGRP;
+  // output position p of the group: natural (channel p) or prefill order (channel prefill_channel(p))
+  int src[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int k = lane + 32 * i;
-      const float v = x_bf16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(x)[base + k])
-                             : __half2float(static_cast<const __half*>(x)[base + k]);
-      scr[k] = v * sv[i];
+  for (int e = 0; e < 4; ++e) src[e] = prefill_order ? prefill_channel(4 * lane + e) : 4 * lane + e;
+  for (int64_t bc = b0; bc < b0 + TOK_PER_WARP && bc < B; bc += TOK_LOCK) {
+    uint2 xv[TOK_LOCK];
+#pragma unroll
+    for (int tb = 0; tb < TOK_LOCK; ++tb) {
+      const int64_t b = bc + tb;
+      xv[tb] = (b < B && b < b0 + TOK_PER_WARP)
+                   ? __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(x) +
+                                                          (b * K + static_cast<int64_t>(gam) * TGRP + 4 * lane) * 2))
+                   : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int tb = 0; tb < TOK_LOCK; ++tb) {
+      float2 f01, f23;
+      if (x_bf16) {
+        f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv[tb].x));
+        f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv[tb].y));
+      } else {
+        f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv[tb].x));
+        f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv[tb].y));
+      }
+      *reinterpret_cast<float4*>(&scr_all[warp][tb][4 * lane]) =
+          make_float4(f01.x * sv.x, f01.y * sv.y, f23.x * sv.z, f23.y * sv.w);
     }
     __syncwarp();
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
-      if (t >= L || !rotate) break;
+      if (t >= Le) break;
       const uint32_t i0 = ixr[t] & 0xff, j0 = (ixr[t] >> 8) & 0xff;
       const uint32_t i1 = (ixr[t] >> 16) & 0xff, j1 = ixr[t] >> 24;
-      const float a0 = scr[i0], c0 = scr[j0];
-      const float a1 = scr[i1], c1 = scr[j1];
-      scr[i0] = csr[t].x * a0 - csr[t].y * c0;
-      scr[j0] = csr[t].y * a0 + csr[t].x * c0;
-      scr[i1] = csr[t].z * a1 - csr[t].w * c1;
-      scr[j1] = csr[t].w * a1 + csr[t].z * c1;
+#pragma unroll
+      for (int tb = 0; tb < TOK_LOCK; ++tb) {
+        float* scr = scr_all[warp][tb];
+        const float a0 = scr[i0], c0 = scr[j0];
+        const float a1 = scr[i1], c1 = scr[j1];
+        scr[i0] = csr[t].x * a0 - csr[t].y * c0;
+        scr[j0] = csr[t].y * a0 + csr[t].x * c0;
+        scr[i1] = csr[t].z * a1 - csr[t].w * c1;
+        scr[j1] = csr[t].w * a1 + csr[t].z * c1;
+      }
       __syncwarp();
     }
-    // natural order: lane writes channels 4l..4l+3.  prefill_order: position p of the group
-    // holds channel prefill_channel(p) (the order the prefill dequantiser emits weights in)
-    float v4[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) v4[e] = scr[prefill_order ? prefill_channel(4 * lane + e) : 4 * lane + e];
-    const __half2 h01 = __floats2half2_rn(v4[0], v4[1]);
-    const __half2 h23 = __floats2half2_rn(v4[2], v4[3]);
-    uint2 pk;
-    pk.x = *reinterpret_cast<const uint32_t*>(&h01);
-    pk.y = *reinterpret_cast<const uint32_t*>(&h23);
-    *reinterpret_cast<uint2*>(xo + base + 4 * lane) = pk;
+    for (int tb = 0; tb < TOK_LOCK; ++tb) {
+      const int64_t b = bc + tb;
+      const float* scr = scr_all[warp][tb];
+      const __half2 h01 = __floats2half2_rn(scr[src[0]], scr[src[1]]);
+      const __half2 h23 = __floats2half2_rn(scr[src[2]], scr[src[3]]);
+      uint2 pk;
+      pk.x = *reinterpret_cast<const uint32_t*>(&h01);
+      pk.y = *reinterpret_cast<const uint32_t*>(&h23);
+      if (b < B && b < b0 + TOK_PER_WARP)
+        *reinterpret_cast<uint2*>(xo + b * K + static_cast<int64_t>(gam) * TGRP + 4 * lane) = pk;
+    }
     __syncwarp();
   }
   if (pdl) pdl_launch_dependents();

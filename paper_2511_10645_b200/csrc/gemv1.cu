@@ -67,19 +67,6 @@ __device__ __forceinline__ void mma_u8s8(int (&d)[4], uint32_t a0, uint32_t a1, 
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// stage st -> (first cluster-local row block, row blocks, first group, groups)
-struct StageGeo {
-  int r_lo, nr, g_lo, pl;
-};
-__device__ __forceinline__ StageGeo stage_geo(int st, int npc, int plen, int rbs, int nrb, int ga, int gb) {
-  const int rc = st / npc, pc = st - rc * npc;
-  StageGeo s;
-  s.r_lo = rc * rbs;
-  s.nr = min(rbs, nrb - s.r_lo);
-  s.g_lo = ga + pc * plen;
-  s.pl = min(plen, gb - s.g_lo);
-  return s;
-}
 }  // namespace
 
 // NW compute warps + 1 producer warp (17 warps: up to 96 registers per thread).
@@ -108,11 +95,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
   const int rb0 = cl * d.rb_base + min(cl, d.rb_extra);
   const int R = nrb * TILE_ROWS;
   const int ga = crank * G / CL, gb = (crank + 1) * G / CL, gc = gb - ga;
-  // stages: (row-block chunk) x (group piece); pieces balanced, chunks fill a stage
-  const int npc = (gc + a.TPS - 1) / a.TPS;
-  const int plen = (gc + npc - 1) / npc;
-  const int rbs = max(1, a.TPS / plen);
-  const int n_stages = ((nrb + rbs - 1) / rbs) * npc;
+  // stages: TPS consecutive tiles of the CTA's tile sequence u = rb * gc + (gamma - ga)
+  // (row block by row block, my groups within each; a stage may start or end inside a row block)
+  const int n_tiles = nrb * gc;
+  const int n_stages = (n_tiles + a.TPS - 1) / a.TPS;
 
   uint8_t* xp = smem + a.off_xp;                                 // x' digits [gc][NB][4 t][NCOL][4 kb][8 B]
   int2* xs = reinterpret_cast<int2*>(smem + a.off_xs);           // per (group, token): (sum x'fix, 2^(E-14))
@@ -170,13 +156,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
       }
       if (st >= a.S) mbar_wait(&empty[slot], ((st / a.S) & 1) ^ 1);
       if (lane == 0) {
-        const StageGeo s = stage_geo(st, npc, plen, rbs, nrb, ga, gb);
+        const int u0 = st * a.TPS, u1 = min(n_tiles, u0 + a.TPS);
         uint8_t* dst = ring + static_cast<size_t>(slot) * a.slot_bytes;
-        mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(s.nr * s.pl) * TILE_B);
+        mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(u1 - u0) * TILE_B);
 #pragma unroll 1
-        for (int r = 0; r < s.nr; ++r) {
-          const int64_t T = static_cast<int64_t>(rb0 + s.r_lo + r) * G + s.g_lo;
-          const uint32_t i0 = static_cast<uint32_t>(r * s.pl), n = static_cast<uint32_t>(s.pl);
+        for (int u = u0; u < u1;) {  // one contiguous segment per row block touched
+          const int rb = u / gc, ue = min(u1, (rb + 1) * gc);
+          const int64_t T = static_cast<int64_t>(rb0 + rb) * G + ga + (u - rb * gc);
+          const uint32_t i0 = static_cast<uint32_t>(u - u0), n = static_cast<uint32_t>(ue - u);
+          u = ue;
           bulk_g2s(dst + i0 * TILE_CODE_BYTES, d.codes + T * TILE_CODE_BYTES, n * TILE_CODE_BYTES, &full[slot], pol);
           bulk_g2s(dst + a.sc_off + i0 * TILE_SCALE_BYTES, d.scales + T * TILE_SCALE_BYTES, n * TILE_SCALE_BYTES,
                    &full[slot], pol);
@@ -354,22 +342,19 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
   // ------------------------------------------------------------ phase 2: tiles (a6)
   {
     const int gq = lane >> 2, tq = lane & 3;
-    int rc = 0, pc = 0;  // stage -> (row-block chunk, group piece), advanced incrementally
 #pragma unroll 1
     for (int st = 0; st < n_stages; ++st) {
       const int slot = st % a.S;
-      const int r_lo = rc * rbs, nr = min(rbs, nrb - r_lo);
-      const int g_lo = ga + pc * plen, pl = min(plen, gb - g_lo);
-      if (++pc == npc) {
-        pc = 0;
-        ++rc;
-      }
+      // stage tiles [u0, u1): tile i of the stage is (row block r_lo + ri, group ga + gi) with
+      // (ri, gi) = divmod(off0 + i, gc)
+      const int u0 = st * a.TPS, nt = min(n_tiles, u0 + a.TPS) - u0;
+      const int r_lo = u0 / gc, off0 = u0 - r_lo * gc;
+      const int g_lo = ga, pl = gc;
       mbar_wait(&full[slot], (st / a.S) & 1);
       if (threadIdx.x == 0 && st == 0) g1_mark(4);
       const uint8_t* sb = ring + static_cast<size_t>(slot) * a.slot_bytes;
-      const int nt = nr * pl;
       if constexpr (BT == 1) {
-      int ri = 0, gi = warp;  // tile warp + k NW of the stage = (row block ri, group gi)
+      int ri = 0, gi = off0 + warp;  // tile warp + k NW of the stage
       while (gi >= pl) {
         gi -= pl;
         ++ri;
@@ -439,7 +424,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
       const int step = BT == 1 ? NW : 1;
       const int i_end = BT == 1 ? nt : min(nt, (warp + 1) * per);
       int i = BT == 1 ? warp : warp * per;
-      int ri = i / pl, gi = i - ri * pl;
+      int ri = (off0 + i) / pl, gi = off0 + i - ri * pl;
       float acc[NB][4];
       int acc_ri = -1;
       auto flush = [&]() {
@@ -851,24 +836,31 @@ bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv
   a.off_bar = off;
   off += 64 * 16;
   a.off_ring = g1_align(off, 1024);
-  int64_t avail = static_cast<int64_t>(budget) - a.off_ring;
-  int S = static_cast<int>(avail / a.slot_bytes);
-  // stages a CTA needs at most (every stage holds <= TPS tiles)
-  const int npc = (gcm + TPS - 1) / TPS;
-  const int plen = (gcm + npc - 1) / npc;
-  const int rbs = std::max(1, TPS / plen);
-  const int need = ((rmax / TILE_ROWS + rbs - 1) / rbs) * npc + npc;
-  S = std::min(S, std::min(need, 60));
-  if (S < std::min(2, need) && TPS > NW && !getenv("PARO_G1_TPS")) {  // keep two ring stages: halve the stage
-    TPS = NW;
-    a.TPS = TPS;
-    a.sc_off = static_cast<uint32_t>(TPS) * TILE_CODE_BYTES;
-    a.z_off = a.sc_off + static_cast<uint32_t>(TPS) * TILE_SCALE_BYTES;
-    a.slot_bytes = g1_align(a.z_off + static_cast<uint32_t>(TPS) * TILE_ZERO_BYTES, 128);
-    const int npc2 = (gcm + TPS - 1) / TPS, plen2 = (gcm + npc2 - 1) / npc2, rbs2 = std::max(1, TPS / plen2);
-    const int need2 = ((rmax / TILE_ROWS + rbs2 - 1) / rbs2) * npc2 + npc2;
-    S = std::min(static_cast<int>(avail / a.slot_bytes), std::min(need2, 60));
+  const int64_t avail = static_cast<int64_t>(budget) - a.off_ring;
+  // stage size: the largest TPS <= 32 (two tiles per warp) that keeps >= 2 stages in flight, else
+  // the largest that fits once (stages a CTA needs: ceil(row blocks x groups / TPS)); measured
+  // flat between 24 and 32 tiles per stage with 2-3 stages (tools/run_g1n.sh)
+  const int64_t cta_tiles = static_cast<int64_t>(rmax / TILE_ROWS) * gcm;
+  auto slot_of = [&](int tps) {
+    const uint32_t sc = static_cast<uint32_t>(tps) * TILE_CODE_BYTES;
+    return g1_align(sc + static_cast<uint32_t>(tps) * (TILE_SCALE_BYTES + TILE_ZERO_BYTES), 128);
+  };
+  auto stages_of = [&](int tps) {
+    const int need = static_cast<int>((cta_tiles + tps - 1) / tps);
+    return std::min<int64_t>(std::min(need, 60), avail / slot_of(tps));
+  };
+  if (!getenv("PARO_G1_TPS")) {
+    int best = 0;
+    for (int want = 2; want >= 1 && !best; --want)
+      for (int tps = 32; tps >= 8 && !best; tps -= 4)
+        if (stages_of(tps) >= std::min<int64_t>(want, (cta_tiles + tps - 1) / tps)) best = tps;
+    TPS = best ? best : 8;
   }
+  a.TPS = TPS;
+  a.sc_off = static_cast<uint32_t>(TPS) * TILE_CODE_BYTES;
+  a.z_off = a.sc_off + static_cast<uint32_t>(TPS) * TILE_SCALE_BYTES;
+  a.slot_bytes = slot_of(TPS);
+  int S = static_cast<int>(stages_of(TPS));
   if (S < 1) {
     *why = "decode shared-memory plan does not fit";
     return false;

@@ -342,6 +342,7 @@ def run_paro(args):
     if world == 1 and not args.no_extra:
         extra["c1"] = measure_c1(torch, paro, dev, stream)
         extra["c3_qwen3_4b_stack"] = measure_qwen_stack(torch, paro, dev, stream, (1, 16))
+        extra["c5_llama3_70b_mlp"] = measure_70b_mlp(torch, paro, dev, stream)
 
     if comm is not None:
         torch.cuda.synchronize()
@@ -451,6 +452,38 @@ def measure_qwen_stack(torch, paro, dev, stream, batches):
 
         us = graph_time_us(torch, stream, step, 3)
         out[f"bs{B}"] = {"us_per_step": round(us, 1), "GBps": round(step_bytes / us / 1e3, 1)}
+    del pool
+    torch.cuda.empty_cache()
+    return out
+
+
+def measure_70b_mlp(torch, paro, dev, stream):
+    """configs[4] at one GPU: the LLaMA-3-70B MLP linears (gate/up 8192 -> 28672 in one launch,
+    down 28672 -> 8192) at bs=1; two layer copies (732 MB) alternate, so every call streams from
+    HBM.  The 2/4/8-GPU N-sharded numbers come from `torchrun ... bench.py --gpus N` (rows per
+    rank, NCCL all-gather)."""
+    shapes = synth.LLAMA3_70B_MLP
+    pool = build_layer_pool(torch, paro, shapes, 0, 1, 2, dev, seed=23)
+    x = {K: torch.randn((1, K), device=dev).to(torch.float16) for _, K in shapes.values()}
+    ys = {n: torch.empty((1, N), dtype=torch.float16, device=dev) for n, (N, K) in shapes.items()}
+    out = {}
+    for grp in (["gate_proj", "up_proj"], ["down_proj"]):
+        K = shapes[grp[0]][1]
+        nbytes = sum(algorithmic_bytes(shapes[n][0], K, 1)[0] for n in grp)
+        res = {}
+        for tag, fl in (("rot", 0), ("norot", paro.PARO_LINEAR_NO_ROTATION)):
+            cnt = [0]
+
+            def call():
+                layer = {name: packed for name, N, K_, packed in pool[cnt[0] % 2]}
+                cnt[0] += 1
+                paro.paro_linear_multi(x[K], [layer[n] for n in grp], y=[ys[n] for n in grp],
+                                       flags=fl | paro.PARO_LINEAR_PDL, stream=stream)
+
+            res[tag] = graph_time_us(torch, stream, call, 20)
+        out["+".join(grp)] = {"us": round(res["rot"], 2), "us_norot": round(res["norot"], 2),
+                              "GBps": round(nbytes / res["rot"] / 1e3, 1),
+                              "rot_overhead": round(res["rot"] / res["norot"] - 1.0, 4)}
     del pool
     torch.cuda.empty_cache()
     return out

@@ -185,7 +185,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
 
   // ------------------------------------------------------------ phase 1: x' of my groups (a4, a5)
   float* pw = part + static_cast<size_t>(warp) * a.R_max;
-  if (BT == 1) {
+  if (BT == 1 && !a.atom) {
     for (int i = lane; i < R; i += 32) pw[i] = 0.f;
   } else {
     for (int i = threadIdx.x; i < R * BT; i += NW * 32) part[i] = 0.f;
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
               const int zq = static_cast<int>((zw >> (4 * q)) & 15u);
               const int I = Dl[hh][e] * 256 + Dl[hh][e + 1] + ((Dh[hh][e] * 256 + Dh[hh][e + 1]) >> 4) - zq * xf.x;
               const float out = Sr[q] * F * static_cast<float>(I);
-              if (BT == 1)
+              if (BT == 1 && !a.atom)
                 pw[rowl + 8 * q] += out;
               else
                 atomicAdd(part + (rowl + 8 * q) * BT + b, out);
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
   for (int idx = tid; idx < R * BT; idx += NW * 32) {
     const int r = idx / BT, b = idx - r * BT;
     float sum;
-    if (BT == 1) {
+    if (BT == 1 && !a.atom) {
       float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
       for (int w = 0; w < NW; ++w) s4[w & 3] += part[static_cast<size_t>(w) * a.R_max + r];
@@ -708,6 +708,36 @@ static const void* g1_kernel_bt(int BT) {
   return BT == 1 ? g1_kernel<1>() : BT == 4 ? g1_kernel<4>() : BT == 8 ? g1_kernel<8>() : g1_kernel<16>();
 }
 
+// clusters of CL (BT-token instance) that fit in one wave, from the occupancy API (cached)
+static int g1_active_clusters(int BT, int CL, int threads, int budget) {
+  static int ncl_cache[17][9] = {{0}};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!ncl_cache[BT][CL]) {
+    const void* k = g1_kernel_bt(BT);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, budget);
+    if (CL > 1) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(CL * 64);
+    lc.blockDim = dim3(threads);
+    lc.dynamicSmemBytes = budget;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = CL;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    lc.attrs = &at;
+    lc.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, k, &lc) != cudaSuccess || nc <= 0) {
+      cudaGetLastError();
+      nc = device_sm_count() / CL;
+    }
+    ncl_cache[BT][CL] = nc;
+  }
+  return ncl_cache[BT][CL];
+}
+
 bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config* cfg, const char** why) {
   if (B < 1 || B > GEMV1_MAX_B) {
     *why = "1..16 tokens per decode launch";
@@ -726,14 +756,20 @@ bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv
   }
   Gemv1Config c{};
   Gemv1Args& a = c.a;
-  // Cluster size = how many ways a row block's groups are split, i.e. groups transformed per CTA
-  // (G / CL).  The rotations are shared-memory-bound (8 accesses per pair per layer, all warps
-  // at once: ~200 cycles per layer with 16 groups per CTA, tools/timeline1.py), so launches whose
-  // weight stream is short prefer CL = 4 (8 groups at K = 4096, but only 132 SMs can hold
-  // clusters of 4), long streams CL = 2 (148 SMs), large K CL = 8 (one transform round).
-  int64_t wbytes = 0;
-  for (int i = 0; i < n_lin; ++i) wbytes += Ns[i] * K / 2;
-  int CL = g1_env("PARO_G1_CL", G >= 64 ? 8 : (wbytes < (20LL << 20) ? 4 : 2));
+  // Cluster size = how many ways a row block's groups are split (G / CL groups transformed per
+  // CTA).  The rotations are shared-memory bound (8 accesses per pair-update, all warps at once),
+  // so fewer groups per CTA shorten the transform; but clusters of 2 / 4 / 8 fill only 148 / 132
+  // / 120 SMs (occupancy API), which slows the weight stream.  Measured (tools/time_groups.py,
+  // tools/time_70b.py): short streams (< 20 MB) at K = 4096 prefer 4, long ones 2; K >= 8192
+  // prefers 8 (one transform round) unless the stream is very long and G small (70B gate+up: 2).
+  double wbytes = 0;
+  for (int i = 0; i < n_lin; ++i) wbytes += static_cast<double>(Ns[i]) * K * 0.52;
+  int CL;
+  if (G >= 64)
+    CL = (wbytes < 64e6 || G >= 128) ? 8 : 2;
+  else
+    CL = wbytes < 20e6 ? 4 : 2;
+  CL = g1_env("PARO_G1_CL", CL);
   if (CL != 1 && CL != 2 && CL != 4 && CL != 8) CL = 2;
   while (CL > 1 && CL > G) CL /= 2;
   const int NW = G1_NW;
@@ -746,35 +782,7 @@ bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv
   if (optin <= 0) optin = 227 * 1024;
   const int budget = optin - 1024;
   // clusters that fit in one wave (occupancy API, cached per cluster size)
-  static int ncl_cache[17][9] = {{0}};
-  static std::mutex mu;
-  int ncl_max;
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    if (!ncl_cache[BT][CL]) {
-      const void* k = g1_kernel_bt(BT);
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, budget);
-      if (CL > 1) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaLaunchConfig_t lc{};
-      lc.gridDim = dim3(CL * 64);
-      lc.blockDim = dim3(threads);
-      lc.dynamicSmemBytes = budget;
-      cudaLaunchAttribute at;
-      at.id = cudaLaunchAttributeClusterDimension;
-      at.val.clusterDim.x = CL;
-      at.val.clusterDim.y = 1;
-      at.val.clusterDim.z = 1;
-      lc.attrs = &at;
-      lc.numAttrs = 1;
-      int nc = 0;
-      if (cudaOccupancyMaxActiveClusters(&nc, k, &lc) != cudaSuccess || nc <= 0) {
-        cudaGetLastError();
-        nc = device_sm_count() / CL;
-      }
-      ncl_cache[BT][CL] = nc;
-    }
-    ncl_max = ncl_cache[BT][CL];
-  }
+  int ncl_max = g1_active_clusters(BT, CL, threads, budget);
   ncl_max = std::min(ncl_max, std::max(1, g1_env("PARO_G1_MAXCL", 1 << 20)));
   // clusters over linears in proportion to their row blocks (>= 1 each, <= row blocks)
   int64_t NB[GEMV_MAX_LIN], NBsum = 0;
@@ -824,7 +832,10 @@ bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv
   a.off_xs = off;
   off += g1_align(static_cast<uint32_t>(gcm) * BT * 8, 128);
   a.off_part = off;
-  off += g1_align(static_cast<uint32_t>(BT == 1 ? NW : BT) * rmax * 4, 128);
+  // B = 1: per-warp row partials summed in a fixed order (deterministic) while they fit in
+  // 48 KB; clusters with more rows (e.g. 70B gate+up: 3840 rows) add with shared atomics
+  a.atom = BT == 1 && static_cast<int64_t>(NW) * rmax * 4 > (48 << 10);
+  off += g1_align(static_cast<uint32_t>(BT == 1 && !a.atom ? NW : BT) * rmax * 4, 128);
   a.off_scr = a.off_recv = off;  // BT > 1: phase-1 scratch and the cluster reduction share this space
   if (BT == 1) {
     off += NW * 512;

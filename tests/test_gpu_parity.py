@@ -190,7 +190,8 @@ def test_pack_errors(paro):
     assert e.value.kind == "invalid_argument"
 
 
-@pytest.mark.parametrize("name,N,K", [("q_proj", 4096, 4096), ("down_proj", 4096, 14336), ("gate_proj", 14336, 4096)])
+@pytest.mark.parametrize("name,N,K", [("q_proj", 4096, 4096), ("down_proj", 4096, 14336), ("gate_proj", 14336, 4096),
+                                      ("llama70b_gate", 28672, 8192), ("llama70b_down", 8192, 28672)])
 def test_full_size_sampled(paro, name, N, K):
     """BASELINE configs[1] at full size, in the launch configuration bench.py times:
     pack bit-exact and outputs within tolerance on sampled rows (rows are independent

@@ -48,7 +48,10 @@ extern "C" int paro_debug_read_timeline1(unsigned long long* host, int n) {
 }
 
 namespace {
-constexpr int G1_NW = 16;
+#ifndef G1_NWARPS
+#define G1_NWARPS 16
+#endif
+constexpr int G1_NW = G1_NWARPS;
 __device__ __forceinline__ void g1_mark(int ev) {
   if (G1_TL && blockIdx.x < 1024) {
     unsigned long long t;
@@ -353,7 +356,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
       mbar_wait(&full[slot], (st / a.S) & 1);
       if (threadIdx.x == 0 && st == 0) g1_mark(4);
       const uint8_t* sb = ring + static_cast<size_t>(slot) * a.slot_bytes;
-      if constexpr (BT == 1) {
+      if (a.skip_math) {  // debug (PARO_G1_SKIP): stream the weights, no tile math
+      } else if constexpr (BT == 1) {
       int ri = 0, gi = off0 + warp;  // tile warp + k NW of the stage
       while (gi >= pl) {
         gi -= pl;
@@ -820,6 +824,7 @@ bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv
   a.TPS = TPS;
   a.pre_stages = std::max(0, g1_env("PARO_G1_PRE", 2));
   a.params_first = g1_env("PARO_G1_PF", 1);
+  a.skip_math = g1_env("PARO_G1_SKIP", 0);
   a.R_max = rmax;
   a.RRmax = (rmax + CL - 1) / CL;
   const int gcm = (G + CL - 1) / CL;
@@ -863,7 +868,7 @@ bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv
   if (!getenv("PARO_G1_TPS")) {
     int best = 0;
     for (int want = 2; want >= 1 && !best; --want)
-      for (int tps = 32; tps >= 8 && !best; tps -= 4)
+      for (int tps = 2 * NW; tps >= 8 && !best; tps -= 4)
         if (stages_of(tps) >= std::min<int64_t>(want, (cta_tiles + tps - 1) / tps)) best = tps;
     TPS = best ? best : 8;
   }

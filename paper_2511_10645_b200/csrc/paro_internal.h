@@ -100,6 +100,7 @@ struct Gemv1Args {
   int pre_stages;  // stages issued before the compute warps' x / parameter loads are out
   int params_first;  // the first stages wait until the rotation-parameter loads are issued
   int atom;          // B = 1: row partials by shared atomics (clusters with too many rows)
+  int skip_math;     // debug: stream the weights, skip the tile math (timing only)
   int R_max;   // rows of the largest cluster
   int RRmax;   // rows per owner CTA (reduction)
   uint32_t slot_bytes, sc_off, z_off;

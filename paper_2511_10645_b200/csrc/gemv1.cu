@@ -839,7 +839,7 @@ bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv
   a.off_part = off;
   // B = 1: per-warp row partials summed in a fixed order (deterministic) while they fit in
   // 48 KB; clusters with more rows (e.g. 70B gate+up: 3840 rows) add with shared atomics
-  a.atom = BT == 1 && static_cast<int64_t>(NW) * rmax * 4 > (48 << 10);
+  a.atom = BT == 1 && (static_cast<int64_t>(NW) * rmax * 4 > (g1_env("PARO_G1_ATOM_KB", 48) << 10));
   off += g1_align(static_cast<uint32_t>(BT == 1 && !a.atom ? NW : BT) * rmax * 4, 128);
   a.off_scr = a.off_recv = off;  // BT > 1: phase-1 scratch and the cluster reduction share this space
   if (BT == 1) {

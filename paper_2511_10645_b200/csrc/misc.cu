@@ -9,8 +9,14 @@
 namespace paro {
 
 constexpr int TGRP = 128;
-constexpr int TOK_PER_WARP = 8;
-constexpr int TOK_LOCK = 4;  // tokens rotated in lockstep (independent shared-memory chains)
+#ifndef PARO_TOK_PER_WARP
+#define PARO_TOK_PER_WARP 8
+#endif
+#ifndef PARO_TOK_LOCK
+#define PARO_TOK_LOCK 8
+#endif
+constexpr int TOK_PER_WARP = PARO_TOK_PER_WARP;
+constexpr int TOK_LOCK = PARO_TOK_LOCK;  // tokens rotated in lockstep (independent shared-memory chains)
 
 // x' = R_L ... R_1 diag(s) x per (token, group); Eq. 5 in column form,
 // the scale first.  One warp = one group x TOK_PER_WARP tokens, TOK_LOCK of

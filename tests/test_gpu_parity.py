@@ -242,6 +242,19 @@ def test_k_split_tokens(paro, B, N, K):
     assert O.normwise_error(y.float().cpu().numpy(), y_ref) <= TOL
 
 
+@pytest.mark.parametrize("N,K,B", [(96, 128, 1), (96, 128, 5), (200, 384, 1), (200, 384, 3), (4128, 640, 1)])
+def test_k_split_edge_shapes(paro, N, K, B):
+    """Edge shapes of the K-split decode kernel: one group (clusters of 1), an odd group count
+    split unevenly over a cluster (G = 3, 5), ragged row blocks (N % 32 != 0), many row blocks
+    over few groups."""
+    p = synth.make_problem(N, K, B, seed=90 + N + B)
+    t = dev_tensors(p)
+    packed, ref = check_pack(paro, p, t)
+    y = paro.paro_linear(t["x"], packed, flags=paro.PARO_LINEAR_FORCE_GEMV)
+    y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"])
+    assert O.normwise_error(y.float().cpu().numpy(), y_ref) <= TOL
+
+
 @pytest.mark.parametrize("B", [1, 3, 6])
 def test_linear_multi_shared_x(paro, B):
     """q/k/v-style: three linears with their own transforms reading the same x, one launch."""

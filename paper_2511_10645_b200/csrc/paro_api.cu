@@ -345,7 +345,12 @@ static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, 
   int64_t nk = 0;
   for (int i = 0; i < n; ++i) nk += packed[i].N * K;
   const bool old_small = B == 2 || (B <= 4 && nk >= (48LL << 20) && K < 8192);
-  const bool k_split = !debug && paro::gemv1_enabled() && (B == 1 || B > 4 || !old_small || small_b);
+  bool k_split = !debug && paro::gemv1_enabled() && (B == 1 || B > 4 || !old_small || small_b);
+  if (!k_split && !debug && paro::gemv1_enabled()) {  // the other kernel must be able to plan this shape
+    const int bt0 = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8;
+    const char* why0 = "";
+    if (!paro::plan_gemv(bt0, n, Ns, Ls, K, rotate, &cfg, &why0)) k_split = true;
+  }
   const int64_t tile_b = k_split ? paro::GEMV1_MAX_B : paro::GEMV_MAX_B;
   for (int64_t b0 = 0; b0 < B; b0 += tile_b) {
     const int live = static_cast<int>(std::min<int64_t>(tile_b, B - b0));

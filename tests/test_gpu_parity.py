@@ -230,7 +230,7 @@ def test_prefill_full_size_sampled(paro):
     assert O.normwise_error(y[toks][:, rows], y_ref) <= TOL
 
 
-@pytest.mark.parametrize("B,N,K", [(8, 256, 14336), (16, 512, 9728), (5, 384, 2560), (12, 640, 4096)])
+@pytest.mark.parametrize("B,N,K", [(8, 256, 14336), (16, 512, 9728), (5, 384, 2560), (12, 640, 4096), (2, 256, 28672)])
 def test_k_split_tokens(paro, B, N, K):
     """Token counts routed to the K-split decode kernel (gemv1.cu) beyond one token, at the
     large-K shapes (clusters of 8): B = 5..16 in one launch, column sets of four tokens."""

@@ -164,8 +164,18 @@ def run_paro(args):
     n_layers = min(n_layers, 64)
     pool = build_layer_pool(torch, paro, shapes, rank, world, n_layers, dev)
     g = torch.Generator(device=dev).manual_seed(123 + rank * 0)
-    xs = {K: torch.randn((B, K), generator=g, device=dev).to(torch.float16) for _, K in shapes.values()}
-    ys = {name: torch.empty((B, N), dtype=torch.float16, device=dev) for name, (N, K) in shapes.items()}
+    # activations and outputs are views of one contiguous buffer each (one copy per direction in e2e)
+    Ks = sorted({K for _, K in shapes.values()})
+    x_all = torch.randn((B * sum(Ks),), generator=g, device=dev).to(torch.float16)
+    xs, off = {}, 0
+    for K in Ks:
+        xs[K] = x_all[off:off + B * K].view(B, K)
+        off += B * K
+    y_all = torch.empty((B * sum(N for N, _ in shapes.values()),), dtype=torch.float16, device=dev)
+    ys, off = {}, 0
+    for name, (N, K) in shapes.items():
+        ys[name] = y_all[off:off + B * N].view(B, N)
+        off += B * N
     ws = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
 
     # linears that read the same activation run in one launch (q/k/v, gate/up); each keeps
@@ -267,39 +277,53 @@ def run_paro(args):
     # end-to-end through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
     if True:
-        hx = {K: xs[K].cpu().pin_memory() for K in xs}
-        hy = {name: torch.empty((B, N), dtype=torch.float16).pin_memory() for name, (N, K) in shapes.items()}
-        h2d = sum(t.numel() * 2 for t in hx.values())
-        d2h = sum(t.numel() * 2 for t in hy.values())
+        hx = x_all.cpu().pin_memory()
+        hy = torch.empty(y_all.shape, dtype=torch.float16).pin_memory()
+        h2d = hx.numel() * 2
+        d2h = hy.numel() * 2
         n_e2e = max(10, min(args.steps, 200))
 
         def e2e_step(li):
             with torch.cuda.stream(stream):
-                for K, t in hx.items():
-                    xs[K].copy_(t, non_blocking=True)
-                run_step(li, 0, pdl=False)
-                for name, t in hy.items():
-                    t.copy_(ys[name], non_blocking=True)
+                x_all.copy_(hx, non_blocking=True)
+                # PDL between the decode launches (the first one follows the copy normally; each
+                # launch waits for its predecessor before reading x or writing y, so the y copy
+                # after the last launch sees every output)
+                run_step(li, 0, pdl=True)
+                hy.copy_(y_all, non_blocking=True)
 
         for li in range(3):
             e2e_step(li)
         stream.synchronize()
+        # the serving loop's form: each step (pinned-host x -> device, the 4 decode launches,
+        # y -> pinned host) captured once in a CUDA graph and replayed; the copies run every step
+        per_graph = n_layers
+        gph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            with torch.cuda.graph(gph, stream=stream):
+                for li in range(per_graph):
+                    e2e_step(li)
+            gph.replay()
+            stream.synchronize()
+        reps = max(1, n_e2e // per_graph)
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for li in range(n_e2e):
-            e2e_step(li)
-        e1.record(stream)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(reps):
+                gph.replay()
+            e1.record(stream)
         e1.synchronize()
-        ms_e2e = e0.elapsed_time(e1) / n_e2e
+        ms_e2e = e0.elapsed_time(e1) / (reps * per_graph)
         if world > 1:
             t = torch.tensor([ms_e2e], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_e2e = float(t.item())
         e2e = {"value": round(layer_bytes / (ms_e2e * 1e-3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms_e2e, 4),
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "api": "paper_2511_10645_b200.paro_linear per linear (ctypes), pinned host x/y"}
+               "api": "paper_2511_10645_b200.paro_linear_multi (4 decode launches per step) with the pinned-host "
+                      "x -> device and y -> host copies of every step, captured per step in a CUDA graph and replayed"}
 
     # prefill (SURVEY.md 8(d) "also prefill TFLOPS"): the same packed linears at 2048 tokens
     # through paro_linear's tcgen05 path (transform pre-stage + GEMM), one CUDA graph per linear

@@ -346,14 +346,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
   {
     const int gq = lane >> 2, tq = lane & 3;
 #pragma unroll 1
+    // stage bookkeeping advanced incrementally (no divisions in the loop): ring slot and phase,
+    // first tile u0 = st * TPS = r_lo * gc + off0
+    int slot = 0, phase = 0, r_lo = 0, off0 = 0;
     for (int st = 0; st < n_stages; ++st) {
-      const int slot = st % a.S;
       // stage tiles [u0, u1): tile i of the stage is (row block r_lo + ri, group ga + gi) with
       // (ri, gi) = divmod(off0 + i, gc)
       const int u0 = st * a.TPS, nt = min(n_tiles, u0 + a.TPS) - u0;
-      const int r_lo = u0 / gc, off0 = u0 - r_lo * gc;
       const int g_lo = ga, pl = gc;
-      mbar_wait(&full[slot], (st / a.S) & 1);
+      mbar_wait(&full[slot], phase);
       if (threadIdx.x == 0 && st == 0) g1_mark(4);
       const uint8_t* sb = ring + static_cast<size_t>(slot) * a.slot_bytes;
       if (a.skip_math) {  // debug (PARO_G1_SKIP): stream the weights, no tile math
@@ -512,6 +513,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
+      if (++slot == a.S) {
+        slot = 0;
+        phase ^= 1;
+      }
+      off0 += a.TPS;
+      while (off0 >= gc) {
+        off0 -= gc;
+        ++r_lo;
+      }
     }
   }
 

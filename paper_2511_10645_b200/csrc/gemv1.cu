@@ -82,7 +82,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
   constexpr int TB = BT == 1 ? 1 : 4;          // tokens per transform chunk / MMA column set
   constexpr int NB = (BT + 3) / 4;             // column sets
   constexpr int NCOL = BT == 1 ? 2 : 8;        // B columns holding digits
-  constexpr int XPC = 4 * NCOL * 32;           // digit bytes per (group, column set)
+  constexpr int XTQ = NCOL * 32;               // digit bytes per (group, set, quad)
+  constexpr int XPC = 4 * XTQ;                 // digit bytes per (group, column set)
   constexpr int XPG = NB * XPC;                // digit bytes per group
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
 
   uint8_t* xp = smem + a.off_xp;                                 // x' digits [gc][NB][4 t][NCOL][4 kb][8 B]
   int2* xs = reinterpret_cast<int2*>(smem + a.off_xs);           // per (group, token): (sum x'fix, 2^(E-14))
+  const uint8_t* zblk = smem + a.off_xs + ((gc * BT * 8 + 15) & ~15);  // 32 zero bytes (B columns >= 2)
   float* part = reinterpret_cast<float*>(smem + a.off_part);     // BT = 1: [NW][R_max]; else [R_max][BT]
   float* recv = reinterpret_cast<float*>(smem + a.off_recv);     // [CL][RRmax][BT] cluster partials
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.off_bar);
@@ -115,6 +117,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
   const int my_lo = crank * RR, my_n = max(0, min(RR, R - my_lo));
   uint8_t* ring = smem + a.off_ring;
 
+  if (threadIdx.x < 8) reinterpret_cast<uint32_t*>(smem + a.off_xs + ((gc * BT * 8 + 15) & ~15))[threadIdx.x] = 0u;
   if (threadIdx.x == 0) {
     g1_mark(0);
     for (int i = 0; i < a.S; ++i) {
@@ -329,7 +332,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
             wd[e] = wv;
           }
           const int b = b0 + tb, set = b >> 2, cb = b & 3;
-          *reinterpret_cast<uint2*>(xp + g * XPG + set * XPC + tq * (NCOL * 32) + (2 * cb + col) * 32 + kb * 8) =
+          *reinterpret_cast<uint2*>(xp + g * XPG + set * XPC + tq * XTQ + (2 * cb + col) * 32 + kb * 8) =
               make_uint2(wd[0], wd[1]);
           if (lane == 0)
             xs[g * BT + b] = make_int2(X, static_cast<int>(static_cast<uint32_t>(113 + E) << 23));  // 2^(E - 14)
@@ -380,12 +383,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
 #pragma unroll
         for (int set = 0; set < NB; ++set) {
           if (set * 4 >= B) break;
-          uint4 bA = make_uint4(0u, 0u, 0u, 0u), bB = bA;  // B fragments (columns >= NCOL are zero)
-          if (gq < NCOL) {
-            const uint8_t* bp = xp + gl * XPG + set * XPC + tq * (NCOL * 32) + gq * 32;
-            bA = *reinterpret_cast<const uint4*>(bp);
-            bB = *reinterpret_cast<const uint4*>(bp + 16);
-          }
+          // B fragments: lanes of MMA columns >= 2 read a 32-byte zero block (address select, no branch)
+          const uint8_t* bp = gq < 2 ? xp + gl * XPG + set * XPC + tq * XTQ + gq * 32 : zblk;
+          const uint4 bA = *reinterpret_cast<const uint4*>(bp);
+          const uint4 bB = *reinterpret_cast<const uint4*>(bp + 16);
           constexpr uint32_t ML = 0x0f0f0f0fu, MH = 0xf0f0f0f0u;
           int Dl[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}}, Dh[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
 #pragma unroll
@@ -474,7 +475,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
           if (set * 4 >= B) break;
           uint4 bA = make_uint4(0u, 0u, 0u, 0u), bB = bA;  // B fragments (columns >= NCOL are zero)
           if (gq < NCOL) {
-            const uint8_t* bp = xp + gl * XPG + set * XPC + tq * (NCOL * 32) + gq * 32;
+            const uint8_t* bp = xp + gl * XPG + set * XPC + tq * XTQ + gq * 32;
             bA = *reinterpret_cast<const uint4*>(bp);
             bB = *reinterpret_cast<const uint4*>(bp + 16);
           }
@@ -845,7 +846,7 @@ bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv
   a.off_xp = off;
   off += g1_align(static_cast<uint32_t>(gcm) * NSET * 4 * NCOL * 32, 128);
   a.off_xs = off;
-  off += g1_align(static_cast<uint32_t>(gcm) * BT * 8, 128);
+  off += g1_align(static_cast<uint32_t>(gcm) * BT * 8 + 48, 128);  // + a 16-aligned 32-byte zero block
   a.off_part = off;
   // B = 1: per-warp row partials summed in a fixed order (deterministic) while they fit in
   // 48 KB; clusters with more rows (e.g. 70B gate+up: 3840 rows) add with shared atomics

@@ -349,6 +349,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
   {
     const int gq = lane >> 2, tq = lane & 3;
 #pragma unroll 1
+    const bool atom = a.atom != 0;
     // stage bookkeeping advanced incrementally (no divisions in the loop): ring slot and phase,
     // first tile u0 = st * TPS = r_lo * gc + off0
     int slot = 0, phase = 0, r_lo = 0, off0 = 0;
@@ -403,16 +404,20 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
           if (BT == 1 ? tq == 0 : b < B) {
             const int2 xf = xs[gl * BT + b];
             const float F = __int_as_float(xf.y);
+            float out[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               const int hh = q >> 1, e = (q & 1) * 2;
               const int zq = static_cast<int>((zw >> (4 * q)) & 15u);
               const int I = Dl[hh][e] * 256 + Dl[hh][e + 1] + ((Dh[hh][e] * 256 + Dh[hh][e + 1]) >> 4) - zq * xf.x;
-              const float out = Sr[q] * F * static_cast<float>(I);
-              if (BT == 1 && !a.atom)
-                pw[rowl + 8 * q] += out;
-              else
-                atomicAdd(part + (rowl + 8 * q) * BT + b, out);
+              out[q] = Sr[q] * F * static_cast<float>(I);
+            }
+            if (BT == 1 && !atom) {  // one uniform branch per tile, not per row
+#pragma unroll
+              for (int q = 0; q < 4; ++q) pw[rowl + 8 * q] += out[q];
+            } else {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) atomicAdd(part + (rowl + 8 * q) * BT + b, out[q]);
             }
           }
         }

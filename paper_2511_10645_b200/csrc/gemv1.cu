@@ -1,5 +1,6 @@
-// gemv1.cu -- decode path for ONE token (B = 1): scale + L Givens layers + group-wise INT4
-// dequant GEMV, one launch per (multi-)linear, built for the shortest serial chain.
+// gemv1.cu -- decode path (B = 1 fused; B = 2..16 with a transform pre-kernel): scale + L
+// Givens layers + group-wise INT4 dequant GEMV, one launch per (multi-)linear, built for the
+// shortest serial chain.
 //
 // SURVEY.md 8(a) rows a4 (u = s . x), a5 (the L rotations, Eq. 5 in column
 // form), a6 (dequant GEMV, Eq. 1 dequantisation (q - z) * S),
@@ -10,13 +11,19 @@
 //  * CTA c of the cluster owns the groups [c G / CL, (c + 1) G / CL) of those rows.  It
 //    transforms ONLY its own groups (a warp per group: the rotation is group-local, so no
 //    activation ever crosses CTAs) and streams only the tiles of its groups;
-//  * the cluster sums its CTAs' row partials through distributed shared memory (fixed order:
-//    deterministic, no atomics) and the owner CTA of a row writes y.
-// Pipeline per CTA: one producer warp issues every weight stage with cp.async.bulk (TMA
-// engine) at kernel start -- before the programmatic-dependent-launch wait, because packed
-// weights are never written by the previous kernel -- while the compute warps load their
-// rotation parameters, wait for the previous kernel (x may be its output), load x, rotate in
-// shared memory and leave x' as fixed-point digits in shared memory; then the tiles are consumed as they land.
+//  * the cluster sums its CTAs' row partials through distributed shared memory (st.async,
+//    fixed order) and the owner CTA of a row writes y.  Within a CTA, B = 1 keeps per-warp row
+//    partials summed in a fixed order (deterministic) unless the cluster has too many rows;
+//    B > 1 and those clusters use shared-memory atomics.
+// Pipeline per CTA: one producer warp issues the weight stages with cp.async.bulk (TMA engine)
+// -- the first ones at kernel start, before the programmatic-dependent-launch wait, because
+// packed weights are never written by the previous kernel; the rest once the compute warps'
+// rotation parameters and x are requested, so those latency-critical loads do not queue behind
+// the weight stream -- while the compute warps load their rotation parameters, wait for the
+// previous kernel (x may be its output), load x, rotate in shared memory and leave x' as
+// fixed-point digits in shared memory; then the tiles are consumed as they land.
+// B = 2..16: paro_gemv1_xform_kernel (below) computes the digits of all tokens once per
+// (linear, group, four tokens) and the producer bulk-copies this CTA's groups' slice.
 //
 // Dot product on the warp-level integer tensor cores (IMMA.16832, u8 x s8 -> s32, exact):
 // x' of a group becomes 16-bit fixed point x'fix = rint(x' 2^(14 - E)) with 2^E >= max |x'|

@@ -199,6 +199,10 @@ paro_status paro_comm_unique_id(void* uid);
  * receives an opaque handle (an ncclComm_t).  Collective over all ranks. */
 paro_status paro_comm_init(const void* uid, int32_t rank, int32_t world, void** comm);
 paro_status paro_comm_destroy(void* comm);
+/* Asynchronous NCCL errors (a failed peer, a broken link) detected since the last call:
+ * PARO_OK, or PARO_ERR_NCCL with the NCCL message in paro_last_error().  Also checked by
+ * paro_linear_allgather before and after it enqueues the collective. */
+paro_status paro_comm_check(void* comm);
 
 /* Sharded linear: packed_shard holds this rank's N/world rows; y_full is device
  * [B, N] (N = packed_shard->N * world) in y_dtype.  workspace must hold

@@ -61,6 +61,7 @@ SIGNATURES = {
     "paro_comm_unique_id": (ctypes.c_int, [_P]),
     "paro_comm_init": (ctypes.c_int, [_P, _I32, _I32, ctypes.POINTER(ctypes.c_void_p)]),
     "paro_comm_destroy": (ctypes.c_int, [_P]),
+    "paro_comm_check": (ctypes.c_int, [_P]),
     "paro_linear_allgather_workspace": (_SZ, [_I64, _I64, _I64, _I32, ctypes.c_int, _U32]),
     "paro_linear_allgather": (ctypes.c_int, [_P, ctypes.c_int, _I64, _PP, _P, _P, ctypes.c_int, _U32, _P, _SZ, _P,
                                              _I32, _I32, _P]),
@@ -248,6 +249,11 @@ def paro_comm_init(uid: bytes, rank: int, world: int) -> int:
 
 def paro_comm_destroy(comm: int) -> None:
     _check(_lib.paro_comm_destroy(comm))
+
+
+def paro_comm_check(comm: int) -> None:
+    """Raise ParoError(PARO_ERR_NCCL) if NCCL reported an asynchronous error on comm."""
+    _check(_lib.paro_comm_check(comm))
 
 
 def paro_linear_allgather(x, packed_shard: PackedLinear, comm: int, rank: int, world: int, bias_shard=None, y=None,

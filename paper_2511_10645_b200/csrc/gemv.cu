@@ -52,8 +52,6 @@ constexpr float TWO_P24 = 16777216.0f;  // 2^24
 constexpr int TL_EVENTS = 12;           // debug timeline: events per CTA
 constexpr uint32_t TILE_BYTES = TILE_CODE_BYTES + TILE_SCALE_BYTES + TILE_ZERO_BYTES;
 
-__device__ unsigned long long g_paro_timeline[1024 * TL_EVENTS];
-__device__ unsigned long long g_paro_prof[1024 * 16 * 8];  // debug: per (CTA, warp) cycle counters
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -62,6 +60,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #ifndef PARO_ENABLE_DEBUG
 #define PARO_ENABLE_DEBUG 0  // 1: per-launch timeline / cycle counters (flag 0x100; tools/timeline.py). Off: ~5% faster
+#endif
+#if PARO_ENABLE_DEBUG
+__device__ unsigned long long g_paro_timeline[1024 * TL_EVENTS];
+__device__ unsigned long long g_paro_prof[1024 * 16 * 8];  // debug: per (CTA, warp) cycle counters
+#else
+__device__ unsigned long long* const g_paro_timeline = nullptr;
+__device__ unsigned long long* const g_paro_prof = nullptr;
 #endif
 #define PARO_DBG(a) (PARO_ENABLE_DEBUG && (a).debug)
 #define PARO_TL(a, ev)                                                                            \
@@ -730,6 +735,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
   if (threadIdx.x == 0) PARO_TL(a, 5);
 }
 
+#if PARO_ENABLE_DEBUG
 extern "C" int paro_debug_read_prof(unsigned long long* host, int n) {
   if (n > 1024 * 16 * 8) n = 1024 * 16 * 8;
   return static_cast<int>(cudaMemcpyFromSymbol(host, g_paro_prof, sizeof(unsigned long long) * n));
@@ -740,31 +746,10 @@ extern "C" int paro_debug_read_timeline(unsigned long long* host, int n) {
   if (n > 1024 * TL_EVENTS) n = 1024 * TL_EVENTS;
   return static_cast<int>(cudaMemcpyFromSymbol(host, g_paro_timeline, sizeof(unsigned long long) * n));
 }
+#endif
 
 // ============================================================================ host side
-int device_sm_count() {
-  static int sms = 0;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  });
-  return sms;
-}
-
-static int smem_optin() {
-  static int v = 0;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (v <= 0) v = 227 * 1024;
-  });
-  return v;
-}
+static int smem_optin() { return device_smem_optin(); }
 
 static inline uint32_t align_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
@@ -789,7 +774,7 @@ static const void* kernel_for(int BT, int threads, bool im) {
 static int max_resident_ctas(int BT, int threads, int smem, int CL, bool im) {
   const void* k = kernel_for(BT, threads, im);
   if (!k) return 0;
-  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+  if (ensure_smem_attr(k, smem) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -820,9 +805,16 @@ static int max_resident_ctas(int BT, int threads, int smem, int CL, bool im) {
   return per_sm * device_sm_count();
 }
 
+// Plan overrides for experiments exist only in builds with -DPARO_DEBUG_KNOBS=1 (never in
+// the shipped library: a stray environment variable must not change what a call computes).
 static int env_int(const char* name, int dflt) {
+#if PARO_DEBUG_KNOBS
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;
+#else
+  (void)name;
+  return dflt;
+#endif
 }
 
 static bool plan_try(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, int rotate, int NW, int ctas_pref,
@@ -996,13 +988,8 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
 template <int BT, int T, bool IM>
 static cudaError_t launch_t(const GemvConfig& c, cudaStream_t st) {
   auto kern = paro_gemv_kernel<BT, T, IM>;
-  static int configured_smem = 0;  // per instantiation
-  if (static_cast<int>(c.a.smem_total) > configured_smem) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(c.a.smem_total));
-    if (e != cudaSuccess) return e;
-    configured_smem = static_cast<int>(c.a.smem_total);
-  }
+  cudaError_t e0 = ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(c.a.smem_total));
+  if (e0 != cudaSuccess) return e0;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(c.grid);
   cfg.blockDim = dim3((c.NW + 1) * 32);

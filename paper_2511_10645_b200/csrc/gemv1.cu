@@ -48,11 +48,13 @@ namespace paro {
 #ifndef G1_TL
 #define G1_TL 0  // 1: per-CTA %globaltimer timeline of every launch (tools/timeline1.py)
 #endif
+#if G1_TL
 __device__ unsigned long long g_g1_tl[1024 * 12];
 extern "C" int paro_debug_read_timeline1(unsigned long long* host, int n) {
   if (n > 1024 * 12) n = 1024 * 12;
   return static_cast<int>(cudaMemcpyFromSymbol(host, g_g1_tl, sizeof(unsigned long long) * n));
 }
+#endif
 
 namespace {
 #ifndef G1_NWARPS
@@ -60,11 +62,15 @@ namespace {
 #endif
 constexpr int G1_NW = G1_NWARPS;
 __device__ __forceinline__ void g1_mark(int ev) {
-  if (G1_TL && blockIdx.x < 1024) {
+#if G1_TL
+  if (blockIdx.x < 1024) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_g1_tl[blockIdx.x * 12 + ev] = t;
   }
+#else
+  (void)ev;
+#endif
 }  // compute warps per CTA (+ 1 producer warp)
 constexpr uint32_t TILE_B = TILE_CODE_BYTES + TILE_SCALE_BYTES + TILE_ZERO_BYTES;
 
@@ -691,9 +697,16 @@ __global__ void __launch_bounds__(128) paro_gemv1_xform_kernel(const Gemv1Args a
 }
 
 // ============================================================================ host side
+// Plan overrides for experiments exist only in builds with -DPARO_DEBUG_KNOBS=1 (never in
+// the shipped library: a stray environment variable must not change what a call computes).
 static int g1_env(const char* name, int dflt) {
+#if PARO_DEBUG_KNOBS
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;
+#else
+  (void)name;
+  return dflt;
+#endif
 }
 
 static inline uint32_t g1_align(uint32_t v, uint32_t al) { return (v + al - 1) / al * al; }
@@ -735,34 +748,31 @@ static const void* g1_kernel_bt(int BT) {
   return BT == 1 ? g1_kernel<1>() : BT == 4 ? g1_kernel<4>() : BT == 8 ? g1_kernel<8>() : g1_kernel<16>();
 }
 
-// clusters of CL (BT-token instance) that fit in one wave, from the occupancy API (cached)
-static int g1_active_clusters(int BT, int CL, int threads, int budget) {
-  static int ncl_cache[17][9] = {{0}};
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lk(mu);
-  if (!ncl_cache[BT][CL]) {
-    const void* k = g1_kernel_bt(BT);
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, budget);
-    if (CL > 1) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(CL * 64);
-    lc.blockDim = dim3(threads);
-    lc.dynamicSmemBytes = budget;
-    cudaLaunchAttribute at;
-    at.id = cudaLaunchAttributeClusterDimension;
-    at.val.clusterDim.x = CL;
-    at.val.clusterDim.y = 1;
-    at.val.clusterDim.z = 1;
-    lc.attrs = &at;
-    lc.numAttrs = 1;
-    int nc = 0;
-    if (cudaOccupancyMaxActiveClusters(&nc, k, &lc) != cudaSuccess || nc <= 0) {
-      cudaGetLastError();
-      nc = device_sm_count() / CL;
-    }
-    ncl_cache[BT][CL] = nc;
+// clusters of CL (BT-token instance) that fit in one wave, from the occupancy API (cached per
+// device)
+static int g1_active_clusters_compute(const void* k, int CL, int threads, int budget) {
+  ensure_smem_attr(k, budget);
+  if (CL > 1) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(CL * 64);
+  lc.blockDim = dim3(threads);
+  lc.dynamicSmemBytes = budget;
+  cudaLaunchAttribute at;
+  at.id = cudaLaunchAttributeClusterDimension;
+  at.val.clusterDim.x = CL;
+  at.val.clusterDim.y = 1;
+  at.val.clusterDim.z = 1;
+  lc.attrs = &at;
+  lc.numAttrs = 1;
+  int nc = 0;
+  if (cudaOccupancyMaxActiveClusters(&nc, k, &lc) != cudaSuccess || nc <= 0) {
+    cudaGetLastError();
+    nc = device_sm_count() / CL;
   }
-  return ncl_cache[BT][CL];
+  return nc;
+}
+static int g1_active_clusters(int BT, int CL, int threads, int budget) {
+  return cached_device_int(g1_kernel_bt(BT), CL, threads, budget, g1_active_clusters_compute);
 }
 
 bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config* cfg, const char** why) {
@@ -803,11 +813,7 @@ bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv
   int TPS = std::max(1, std::min(64, g1_env("PARO_G1_TPS", 2 * NW)));
   const int threads = (NW + 1) * 32;
   c.NW = NW;
-  int optin = 0, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (optin <= 0) optin = 227 * 1024;
-  const int budget = optin - 1024;
+  const int budget = device_smem_optin() - 1024;
   // clusters that fit in one wave (occupancy API, cached per cluster size)
   int ncl_max = g1_active_clusters(BT, CL, threads, budget);
   ncl_max = std::min(ncl_max, std::max(1, g1_env("PARO_G1_MAXCL", 1 << 20)));
@@ -888,7 +894,7 @@ bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv
     const int need = static_cast<int>((cta_tiles + tps - 1) / tps);
     return std::min<int64_t>(std::min(need, 60), avail / slot_of(tps));
   };
-  if (!getenv("PARO_G1_TPS")) {
+  if (g1_env("PARO_G1_TPS", 0) == 0) {
     int best = 0;
     for (int want = 2; want >= 1 && !best; --want)
       for (int tps = 2 * NW; tps >= 8 && !best; tps -= 4)
@@ -916,13 +922,8 @@ bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv
 template <int BT>
 static cudaError_t g1_launch(const Gemv1Config& c, cudaLaunchConfig_t* cfg) {
   auto kern = paro_gemv1_kernel<G1_NW, BT>;
-  static int conf = 0;
-  if (static_cast<int>(c.a.smem_total) > conf) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(c.a.smem_total));
-    if (e != cudaSuccess) return e;
-    conf = static_cast<int>(c.a.smem_total);
-  }
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(c.a.smem_total));
+  if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(cfg, kern, c.a);
 }
 

@@ -1,12 +1,81 @@
 // misc.cu -- standalone activation transform (prefill pre-stage / microbenchmark),
 // on-the-fly transform preparation, logical unpack (tests), all-gather permute.
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "paro_internal.h"
 #include "ptx.cuh"
 #include "tile_layout.cuh"
 
 namespace paro {
+
+// ---------------------------------------------------------------- per-device host caches
+// Every cached device property / function attribute is keyed by the CURRENT device ordinal
+// (cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-device setting) and guarded by
+// one mutex, so several host threads and several GPUs in one process are safe.
+namespace {
+std::mutex g_cache_mu;
+std::map<int, int> g_sm_count, g_optin;
+std::map<std::pair<int, const void*>, int> g_smem_attr;
+std::map<std::tuple<int, const void*, int, int, int>, int> g_int_cache;
+int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) {
+    cudaGetLastError();
+    d = 0;
+  }
+  return d;
+}
+}  // namespace
+
+int device_sm_count() {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  auto it = g_sm_count.find(dev);
+  if (it != g_sm_count.end()) return it->second;
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  if (v <= 0) v = 148;
+  g_sm_count[dev] = v;
+  return v;
+}
+
+int device_smem_optin() {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  auto it = g_optin.find(dev);
+  if (it != g_optin.end()) return it->second;
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (v <= 0) v = 227 * 1024;
+  g_optin[dev] = v;
+  return v;
+}
+
+cudaError_t ensure_smem_attr(const void* fn, int bytes) {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  int& have = g_smem_attr[{dev, fn}];
+  if (bytes <= have) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
+int cached_device_int(const void* fn, int a, int b, int c, int (*compute)(const void*, int, int, int)) {
+  const int dev = current_device();
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_int_cache.find({dev, fn, a, b, c});
+    if (it != g_int_cache.end()) return it->second;
+  }
+  const int v = compute(fn, a, b, c);  // may call ensure_smem_attr (takes the lock)
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_int_cache[{dev, fn, a, b, c}] = v;
+  return v;
+}
 
 constexpr int TGRP = 128;
 #ifndef PARO_TOK_PER_WARP
@@ -136,37 +205,60 @@ cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, in
                             static_cast<__half*>(x_out), pdl, prefill_order);
 }
 
-// On-the-fly preparation of (cos, sin, i, j) from device theta / pairs (no validation).
-__global__ void prepare_transform_kernel(const float* __restrict__ theta, const int16_t* __restrict__ pairs, int G,
-                                         int L, int P, float2* __restrict__ rot_cs, uchar2* __restrict__ rot_idx) {
-  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // (gamma, t, slot<64)
-  if (e >= static_cast<int64_t>(G) * L * 64) return;
-  const int slot = static_cast<int>(e % 64);
-  const int64_t gt = e / 64;
-  const int64_t gam = gt / L, t = gt % L;
-  const int64_t dst = ((gam * L + t) * 32 + (slot & 31)) * 2 + (slot >> 5);  // [G][L][32][2] record
-  float2 cs = make_float2(1.f, 0.f);
-  uchar2 ij = make_uchar2(128, 128);
+// On-the-fly preparation of (cos, sin, i, j) from device theta / pairs (no validation of
+// Definition 1: the caller guarantees it).  One 64-thread block per (group, rotation), one
+// thread per slot.  An absent slot ((-1, -1) or p >= P) becomes the identity pair (u, u)
+// with cos = 1, sin = 0 on the lowest channel u that no present pair of this rotation
+// touches: the runtime kernels then read and write only in-range channels, and the
+// identity update writes back the value it read (no race with a present pair, whose
+// channels are all different from u).  If every slot is present there is no absent slot.
+__global__ void __launch_bounds__(64) prepare_transform_kernel(const float* __restrict__ theta,
+                                                               const int16_t* __restrict__ pairs, int G, int L, int P,
+                                                               float2* __restrict__ rot_cs,
+                                                               uchar2* __restrict__ rot_idx) {
+  __shared__ uint32_t used[4];
+  const int slot = threadIdx.x;
+  const int64_t gt = blockIdx.x;  // gamma * L + t
+  if (slot < 4) used[slot] = 0u;
+  __syncthreads();
+  int i = -1, j = -1;
   if (slot < P) {
     const int64_t src = gt * P + slot;
-    const int i = pairs[2 * src], j = pairs[2 * src + 1];
-    if (i >= 0 && j >= 0 && i < 128 && j < 128) {
-      float s, c;
-      sincosf(theta[src], &s, &c);
-      cs = make_float2(c, s);
-      ij = make_uchar2(static_cast<unsigned char>(i), static_cast<unsigned char>(j));
-    }
+    i = pairs[2 * src];
+    j = pairs[2 * src + 1];
+    if (i < 0 || j < 0 || i >= 128 || j >= 128) i = j = -1;
   }
+  if (i >= 0) {
+    atomicOr(&used[i >> 5], 1u << (i & 31));
+    atomicOr(&used[j >> 5], 1u << (j & 31));
+  }
+  __syncthreads();
+  float2 cs = make_float2(1.f, 0.f);
+  uchar2 ij;
+  if (i >= 0) {
+    float sn, c;
+    sincosf(theta[gt * P + slot], &sn, &c);
+    cs = make_float2(c, sn);
+    ij = make_uchar2(static_cast<unsigned char>(i), static_cast<unsigned char>(j));
+  } else {
+    int u = 0;
+    for (int w = 0; w < 4; ++w)
+      if (~used[w]) {
+        u = 32 * w + __ffs(~used[w]) - 1;
+        break;
+      }
+    ij = make_uchar2(static_cast<unsigned char>(u), static_cast<unsigned char>(u));
+  }
+  const int64_t dst = (gt * 32 + (slot & 31)) * 2 + (slot >> 5);  // [G][L][32][2] record
   rot_cs[dst] = cs;
   rot_idx[dst] = ij;
 }
 
 cudaError_t launch_prepare_transform(const float* theta, const int16_t* pairs, int G, int L, int P, float2* rot_cs,
                                      uchar2* rot_idx, cudaStream_t st) {
-  const int64_t n = static_cast<int64_t>(G) * L * 64;
+  const int64_t n = static_cast<int64_t>(G) * L;
   if (n == 0) return cudaSuccess;
-  prepare_transform_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(theta, pairs, G, L, P, rot_cs,
-                                                                                   rot_idx);
+  prepare_transform_kernel<<<static_cast<unsigned>(n), 64, 0, st>>>(theta, pairs, G, L, P, rot_cs, rot_idx);
   return cudaGetLastError();
 }
 

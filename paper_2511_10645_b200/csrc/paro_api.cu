@@ -336,10 +336,14 @@ static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, 
   int planned_b = 0;
   // token count -> kernel (measured, tools/time_batch.py): the K-split kernel (gemv1.cu) for one
   // token and for 5..16 tokens per launch; the cluster-shared-transform kernel (gemv.cu) for 2..4
+#if PARO_DEBUG_KNOBS
   static const int small_b = [] {
     const char* e = getenv("PARO_G1_SMALLB");
     return e ? atoi(e) : 0;
   }();
+#else
+  constexpr int small_b = 0;
+#endif
   // 2..4 tokens (tools/time_batch.py): the cluster-shared-transform kernel for B = 2 and for wide
   // launches with K < 8192 (e.g. gate+up), the K-split kernel otherwise
   int64_t nk = 0;
@@ -458,7 +462,9 @@ paro_status paro_linear(const void* x, paro_dtype x_dtype, int64_t B, const paro
     return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear: workspace too small (%zu < %zu)", workspace_bytes, need);
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   const int rotate = (flags & PARO_LINEAR_NO_ROTATION) ? 0 : 1;
-  const int pdl = (flags & PARO_LINEAR_PDL) ? 1 : 0;
+  // on-the-fly tables are written by prepare_transform_kernel just before; the decode kernels
+  // read them before their PDL wait, so the kernel after it is launched without PDL
+  const int pdl = ((flags & PARO_LINEAR_PDL) && !on_the_fly) ? 1 : 0;
   const float2* rot_cs = static_cast<const float2*>(packed->rot_cs);
   const uchar2* rot_idx = static_cast<const uchar2*>(packed->rot_idx);
   const float* svec = static_cast<const float*>(packed->svec);
@@ -571,6 +577,7 @@ typedef int (*nccl_init_rank_fn)(void**, int, nccl_uid_t, int);
 typedef int (*nccl_destroy_fn)(void*);
 typedef int (*nccl_allgather_fn)(const void*, void*, size_t, int, void*, cudaStream_t);
 typedef const char* (*nccl_errstr_fn)(int);
+typedef int (*nccl_async_err_fn)(void*, int*);
 
 static struct {
   std::once_flag once;
@@ -580,6 +587,7 @@ static struct {
   nccl_destroy_fn destroy = nullptr;
   nccl_allgather_fn allgather = nullptr;
   nccl_errstr_fn errstr = nullptr;
+  nccl_async_err_fn async_err = nullptr;
 } g_nccl;
 
 static bool nccl_load() {
@@ -596,8 +604,17 @@ static bool nccl_load() {
     g_nccl.destroy = reinterpret_cast<nccl_destroy_fn>(dlsym(g_nccl.h, "ncclCommDestroy"));
     g_nccl.allgather = reinterpret_cast<nccl_allgather_fn>(dlsym(g_nccl.h, "ncclAllGather"));
     g_nccl.errstr = reinterpret_cast<nccl_errstr_fn>(dlsym(g_nccl.h, "ncclGetErrorString"));
+    g_nccl.async_err = reinterpret_cast<nccl_async_err_fn>(dlsym(g_nccl.h, "ncclCommGetAsyncError"));
   });
-  return g_nccl.get_uid && g_nccl.init_rank && g_nccl.destroy && g_nccl.allgather;
+  return g_nccl.get_uid && g_nccl.init_rank && g_nccl.destroy && g_nccl.allgather && g_nccl.async_err;
+}
+
+// Errors NCCL detects asynchronously (a peer died, a network / NVLink failure) are only
+// reported through ncclCommGetAsyncError; surface them as PARO_ERR_NCCL on the next call.
+static int nccl_async_error(void* comm) {
+  int ar = 0;
+  const int r = g_nccl.async_err(comm, &ar);
+  return r ? r : ar;
 }
 
 static paro_status nccl_fail(int r, const char* where) {
@@ -622,6 +639,13 @@ paro_status paro_comm_init(const void* uid, int32_t rank, int32_t world, void** 
   std::memcpy(&u, uid, sizeof(u));
   int r = g_nccl.init_rank(comm, world, u, rank);
   if (r) return nccl_fail(r, "ncclCommInitRank");
+  return PARO_OK;
+}
+
+paro_status paro_comm_check(void* comm) {
+  if (!comm) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_comm_check: NULL comm");
+  if (!nccl_load()) return fail(PARO_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  if (int ar = nccl_async_error(comm)) return nccl_fail(ar, "ncclCommGetAsyncError");
   return PARO_OK;
 }
 
@@ -656,6 +680,7 @@ paro_status paro_linear_allgather(const void* x, paro_dtype x_dtype, int64_t B, 
     return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear_allgather: workspace too small (%zu < %zu)", workspace_bytes,
                 need);
   if (!nccl_load()) return fail(PARO_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  if (int ar = nccl_async_error(comm)) return nccl_fail(ar, "ncclCommGetAsyncError (before the all-gather)");
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   const size_t ye = dtype_bytes(y_dtype);
   uint8_t* wsp = static_cast<uint8_t*>(workspace);
@@ -674,6 +699,7 @@ paro_status paro_linear_allgather(const void* x, paro_dtype x_dtype, int64_t B, 
   int r = g_nccl.allgather(y_local, B > 1 ? gather : y_full, static_cast<size_t>(B * Ns) * ye, /*ncclInt8*/ 0, comm,
                            cs);
   if (r) return nccl_fail(r, "ncclAllGather");
+  if (int ar = nccl_async_error(comm)) return nccl_fail(ar, "ncclCommGetAsyncError");
   if (B > 1) {
     cudaError_t e = paro::launch_permute_gather(gather, y_full, world, B, Ns, static_cast<int>(ye), cs);
     if (e != cudaSuccess) return cuda_fail(e, "paro_linear_allgather: permute");

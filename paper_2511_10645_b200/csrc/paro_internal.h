@@ -140,6 +140,10 @@ cudaError_t launch_prefill_gemm(const void* xq /*fp16 [B][K]*/, int64_t B, const
                                 const uint8_t* zeros, const float* bias, void* y, int y_dtype, int64_t N, int64_t K,
                                 int pdl, cudaStream_t st);
 
+// per-device host caches (misc.cu): keyed by the current device, thread-safe
 int device_sm_count();
+int device_smem_optin();
+cudaError_t ensure_smem_attr(const void* fn, int bytes);  // MaxDynamicSharedMemorySize >= bytes on this device
+int cached_device_int(const void* fn, int a, int b, int c, int (*compute)(const void*, int, int, int));
 
 }  // namespace paro

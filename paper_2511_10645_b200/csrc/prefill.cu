@@ -281,13 +281,8 @@ cudaError_t launch_prefill_gemm(const void* xq, int64_t B, const uint8_t* codes,
   PrefillArgs a{codes, reinterpret_cast<const __half*>(scales), zeros, bias, y, y_dtype, static_cast<int>(B),
                 static_cast<int>(N), static_cast<int>(K), pdl};
   const size_t smem = 1024 + PF_SX * PF_X_STAGE_BYTES + 256;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(prefill_gemm_kernel), static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
   const int64_t tiles = (N / PF_BM) * ((B + PF_BN - 1) / PF_BN);
   const int grid = static_cast<int>(tiles < device_sm_count() ? tiles : device_sm_count());
   cudaLaunchConfig_t cfg{};

@@ -84,12 +84,20 @@ def select_pairs(n_groups: int, g: int = GROUP, n_rot: int = N_ROT, n_pairs: int
 def make_problem(N: int, K: int, B: int = 1, *, seed: int = 0, g: int = GROUP, n_rot: int = N_ROT,
                  n_pairs: int = N_PAIRS, x_dtype=np.float16, outliers: bool = True,
                  zero_group: bool = False, theta_mode: str = "uniform", s_mode: str = "random",
-                 with_bias: bool = False) -> dict:
+                 with_bias: bool = False, special_groups: bool = False, x_zero_group: bool = False,
+                 x_big: float = 0.0) -> dict:
     """One seeded linear-layer instance: W fp16 [N,K], x [B,K], s fp32 [K],
     theta fp32 [G,L,P], pairs int16 [G,L,P,2], optional bias fp32 [N].
 
     theta_mode: "uniform" (U(-pi,pi)), "zero", "quarter" (pi/2), "eighth" (pi/4).
     s_mode:     "random" (exp(U(-.5,.5))), "ones".
+    special_groups (needs K >= 5 g): group 2 of W all positive, group 3 all negative, group 4
+        the constant 0.5, each with theta = 0 in that group (and s = 1 on group 4), so the
+        weight the quantiser sees keeps that structure (one-signed / constant groups:
+        the zero-point clamp and the scale floor of Eq. 1).
+    x_zero_group: x is 0 on every channel of group 0 (an all-zero activation group).
+    x_big:      if > 0, one channel per group of x is set to +-x_big (activations near the
+        fp16 range; |s x| stays below 65504 for x_big <= 39000).
     """
     if K % g:
         raise ValueError("K must be a multiple of the group size")
@@ -101,12 +109,23 @@ def make_problem(N: int, K: int, B: int = 1, *, seed: int = 0, g: int = GROUP, n
         W[:, oc] *= 50.0
     if zero_group and G >= 2:
         W[:, g:2 * g] = 0.0                                 # one all-zero group
+    if special_groups:
+        if G < 5:
+            raise ValueError("special_groups needs K >= 5 g")
+        W[:, 2 * g:3 * g] = np.abs(W[:, 2 * g:3 * g]) + 1e-3     # all positive
+        W[:, 3 * g:4 * g] = -np.abs(W[:, 3 * g:4 * g]) - 1e-3    # all negative
+        W[:, 4 * g:5 * g] = 0.5                                 # constant nonzero
     W = W.astype(np.float16)
     x = rng.normal(0.0, 1.0, size=(B, K))
     if outliers:
         nx = max(1, K // 100)                               # 1 % outlier channels x20
         xc = rng.choice(K, size=nx, replace=False)
         x[:, xc] *= 20.0
+    if x_zero_group:
+        x[:, 0:g] = 0.0
+    if x_big > 0:
+        cols = np.arange(G) * g + rng.integers(0, g, size=G)
+        x[:, cols] = x_big * np.where(rng.random((B, G)) < 0.5, -1.0, 1.0)
     if x_dtype == "bf16":
         x = x.astype(np.float32)                            # rounded to bf16 by the caller (torch)
     else:
@@ -127,6 +146,9 @@ def make_problem(N: int, K: int, B: int = 1, *, seed: int = 0, g: int = GROUP, n
         raise ValueError(theta_mode)
     pairs = select_pairs(G, g=g, n_rot=n_rot, n_pairs=n_pairs, seed=seed)
     theta = np.where(pairs[..., 0] < 0, np.float32(0), theta).astype(np.float32)
+    if special_groups:
+        theta[2:5] = 0.0
+        s[4 * g:5 * g] = 1.0
     bias = rng.normal(0.0, 0.1, size=N).astype(np.float32) if with_bias else None
     return dict(W=W, x=x, s=s, theta=theta, pairs=pairs, bias=bias, N=N, K=K, B=B, g=g, n_rot=n_rot)
 

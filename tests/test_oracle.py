@@ -243,6 +243,43 @@ def test_rtn_all_zero_group():
     assert np.all(q == 0) and np.all(z == 0) and np.all(S == np.float16(2 ** -24))
 
 
+def test_rtn_zero_point_clamp_all_positive():
+    """Q11: z = -round(min/S) clamped to [0, 15]; an all-positive group has
+    unclamped z = -1.  Hand-computed S, z and codes (golden file)."""
+    ex = GOLD["rtn_all_positive_group"]
+    vals = np.array(ex["values"], dtype=np.float64)
+    v = np.tile(vals, 8)[None, :]                                   # 128 values, 8 copies of 1..16
+    q, S, z = O.rtn_groups(v)
+    assert float(S[0, 0]) == ex["S"] and int(z[0, 0]) == ex["z"]
+    assert np.array_equal(q[0, :16], np.array(ex["codes"], dtype=np.uint8))
+
+
+def test_rtn_zero_point_clamp_all_negative():
+    """Q11: an all-negative group has unclamped z = 16 -> 15, and the code clamp comes AFTER
+    adding z (clamping round(v/S) first would give 15 everywhere)."""
+    ex = GOLD["rtn_all_negative_group"]
+    v = np.tile(np.array(ex["values"], dtype=np.float64), 8)[None, :]
+    q, S, z = O.rtn_groups(v)
+    assert float(S[0, 0]) == ex["S"] and int(z[0, 0]) == ex["z"]
+    assert np.array_equal(q[0, :16], np.array(ex["codes"], dtype=np.uint8))
+    deq = O.dequantize(q, S, z)
+    # in-range values dequantise exactly; -16 is below the clamped grid [-15, 0]
+    assert np.array_equal(deq[0, 1:16], np.array(ex["values"][1:], dtype=np.float64))
+    assert deq[0, 0] == -15.0
+
+
+@pytest.mark.parametrize("sign", ["pos", "neg"])
+def test_rtn_constant_nonzero_group(sign):
+    """Q10 (constant group -> s = eps, z clamped, all codes equal) with eps =
+    2^-24 (the fp16 floor).  Hand-computed: c = 0.5 -> z = 0, codes 15; c = -0.5 -> z = 15,
+    codes 0."""
+    ex = GOLD["rtn_constant_group"]
+    c = ex["c_" + sign]
+    q, S, z = O.rtn_groups(np.full((3, 256), c))
+    assert np.all(S.astype(np.float64) == ex["S"]) and ex["S"] == 2.0 ** -24
+    assert np.all(z == ex[sign]["z"]) and np.all(q == ex[sign]["code"])
+
+
 def test_fp16_single_rounding():
     """Q8: the stored scale is ONE round-to-nearest-even from fp64; via fp32 it would
     double-round (1 + 2^-11 + 2^-40 -> 1.0009765625 direct, 1.0 via fp32)."""

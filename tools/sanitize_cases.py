@@ -1,0 +1,71 @@
+"""Small invocations of every kernel family for compute-sanitizer (memcheck / racecheck /
+synccheck / initcheck): C1, q_proj-shaped decode at B in {1, 3, 16}, a multi-linear launch,
+the on-the-fly transform, prefill at B = 300, and the pack.  Checks results against the
+oracle too (so a sanitizer-perturbed run that computes garbage fails loudly).
+Usage: compute-sanitizer --tool memcheck python tools/sanitize_cases.py [--quick]"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle as O  # noqa: E402
+import paper_2511_10645_b200 as paro  # noqa: E402
+import synth  # noqa: E402
+
+
+def dev(p):
+    d = torch.device("cuda")
+    return {k: torch.from_numpy(p[k]).to(d) for k in ("W", "s", "theta", "pairs", "x")}
+
+
+def case(N, K, B, flags=0, seed=0, otf=False):
+    p = synth.make_problem(N, K, B, seed=seed)
+    t = dev(p)
+    pk = paro.paro_pack(t["W"], t["s"], t["theta"], t["pairs"])
+    kw = dict(s=t["s"], theta=t["theta"], pairs=t["pairs"]) if otf else {}
+    y = paro.paro_linear(t["x"], pk, flags=flags, **kw)
+    torch.cuda.synchronize()
+    rows = np.arange(min(N, 64))
+    ref = O.oracle_pack(p["W"][rows], p["s"], p["theta"], p["pairs"])
+    y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"])
+    err = O.normwise_error(y.float().cpu().numpy()[:, rows], y_ref)
+    print(f"N={N} K={K} B={B} flags={flags:#x} otf={otf}: err {err:.2e}", flush=True)
+    assert err < 2e-3
+
+
+def main():
+    quick = "--quick" in sys.argv
+    case(256, 256, 1)                                          # C1
+    case(4096 if not quick else 1024, 4096, 1, paro.PARO_LINEAR_PDL)
+    case(1024, 4096, 3)
+    case(1024, 4096, 2)
+    case(1024, 4096, 16)
+    case(512, 1024, 5, otf=True)
+    case(512, 1024, 1, otf=True)
+    case(256, 512, 300, paro.PARO_LINEAR_FORCE_GEMM)           # prefill tcgen05
+    # multi-linear launch (q/k/v style)
+    K = 1024
+    ps = [synth.make_problem(N, K, 1, seed=10 + i) for i, N in enumerate((512, 128, 256))]
+    pks = []
+    for p in ps:
+        t = dev(p)
+        pks.append(paro.paro_pack(t["W"], t["s"], t["theta"], t["pairs"]))
+    ys = paro.paro_linear_multi(torch.from_numpy(ps[0]["x"]).cuda(), pks)
+    torch.cuda.synchronize()
+    for p, y in zip(ps, ys):
+        ref = O.oracle_pack(p["W"], p["s"], p["theta"], p["pairs"])
+        y_ref = O.oracle_linear(ps[0]["x"], ref, p["s"], p["theta"], p["pairs"])
+        assert O.normwise_error(y.float().cpu().numpy(), y_ref) < 2e-3
+    print("multi ok", flush=True)
+    extra = getattr(paro, "_sanitize_extra", None)
+    if extra:
+        extra()
+    print("SANITIZE CASES DONE", flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -183,6 +183,24 @@ paro_status paro_transform_activations(const void* x, paro_dtype x_dtype, int64_
 paro_status paro_unpack_logical(const paro_packed* packed, void* codes_u8, void* scales_f16, void* zeros_u8,
                                 void* stream);
 
+/* ---- Alg. A1: selection of independent channel pairs ----
+ * PAPER.md:509-553 (Alg. A1): for each of `n_groups` groups of g
+ * channels, shuffle all g(g-1)/2 pairs (i < j) once, then for rotation r = 1..n_rot
+ * greedily take the next pairs of the shuffled list whose channels are unused in this
+ * rotation and which no earlier rotation took, up to n_pairs; a rotation may run short
+ * (its remaining slots are (-1, -1)).  Every output rotation satisfies Definition 1
+ * and no pair repeats across the rotations of a group, so the result
+ * is valid `pairs` input for paro_pack.
+ * Shuffle (Q20): xoshiro256** whose state for group gamma is
+ * outputs 4 gamma .. 4 gamma + 3 of SplitMix64 seeded with `seed`; Fisher-Yates from the
+ * last element down, j = uniform [0, i] by rejection of draws below 2^64 mod (i + 1).
+ *   pairs_out : HOST int16 [n_groups][n_rot][n_pairs][2], caller-owned, fully written.
+ * Runs on the calling thread (host code, offline); no CUDA call.
+ * Errors: PARO_ERR_INVALID_ARGUMENT unless 2 <= g <= 4096, n_rot >= 1,
+ *         1 <= n_pairs <= g/2, n_groups >= 0 and pairs_out != NULL (when n_groups > 0). */
+paro_status paro_select_pairs(int64_t n_groups, int32_t g, int32_t n_rot, int32_t n_pairs, uint64_t seed,
+                              int16_t* pairs_out);
+
 /* ---- output-channel (N) sharding over NVLink ----
  * Rank r of G owns rows [r*N/G, (r+1)*N/G) of W, packed with paro_pack on that
  * row slice (identical, bitwise, to the same rows of the full pack).  Every rank

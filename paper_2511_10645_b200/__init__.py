@@ -65,6 +65,7 @@ SIGNATURES = {
     "paro_linear_allgather_workspace": (_SZ, [_I64, _I64, _I64, _I32, ctypes.c_int, _U32]),
     "paro_linear_allgather": (ctypes.c_int, [_P, ctypes.c_int, _I64, _PP, _P, _P, ctypes.c_int, _U32, _P, _SZ, _P,
                                              _I32, _I32, _P]),
+    "paro_select_pairs": (ctypes.c_int, [_I64, _I32, _I32, _I32, ctypes.c_uint64, _P]),
     "paro_last_error": (ctypes.c_char_p, []),
     "paro_version": (ctypes.c_char_p, []),
 }
@@ -231,6 +232,17 @@ def paro_unpack_logical(packed: PackedLinear, stream=None):
     st = packed.struct()
     _check(_lib.paro_unpack_logical(ctypes.byref(st), _ptr(codes), _ptr(scales), _ptr(zeros), _stream(stream)))
     return codes, scales, zeros
+
+
+# ---------------------------------------------------------------- Alg. A1 (host)
+def paro_select_pairs(n_groups: int, g: int = GROUP, n_rot: int = 8, n_pairs: int = SLOTS, seed: int = 0):
+    """Alg. A1 pair lists for n_groups groups: numpy int16 [n_groups, n_rot, n_pairs, 2] (host),
+    (-1, -1) in the slots of a short rotation (include/paro.h, paro_select_pairs)."""
+    import numpy as np
+    out = np.empty((max(n_groups, 0), max(n_rot, 0), max(n_pairs, 0), 2), dtype=np.int16)
+    _check(_lib.paro_select_pairs(n_groups, g, n_rot, n_pairs, seed & ((1 << 64) - 1),
+                                  out.ctypes.data if out.size else None))
+    return out
 
 
 # ---------------------------------------------------------------- NCCL-sharded linear

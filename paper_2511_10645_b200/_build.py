@@ -17,7 +17,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 # pack.cu must not contract a*b - c*d into FMA: bit-exact fp64 fold (Q7)
 PER_FILE = {"pack.cu": ["-fmad=false"]}
-SOURCES = ["paro_api.cu", "pack.cu", "gemv.cu", "gemv1.cu", "misc.cu", "prefill.cu"]
+SOURCES = ["paro_api.cu", "pack.cu", "gemv.cu", "gemv1.cu", "misc.cu", "prefill.cu", "pairs.cpp"]
 HEADERS = ["ptx.cuh", "paro_internal.h", "umma.cuh", "tile_layout.cuh"]
 
 
@@ -41,7 +41,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     objs = []
     for src in SOURCES:
         sp = os.path.join(CSRC, src)
-        op = os.path.join(BUILD, src.replace(".cu", ".o"))
+        op = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
         objs.append(op)
         if force or _stale(op, [sp] + hdrs + [__file__]):
             extra = os.environ.get("PARO_NVCC_EXTRA", "").split()  # experiments only (e.g. -DPARO_MBAR_SPIN=1)

@@ -46,6 +46,13 @@ size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 
 }  // namespace
 
+namespace paro {
+int set_error(int st, const char* msg) {
+  g_err = msg;
+  return st;
+}
+}  // namespace paro
+
 
 // ---------------------------------------------------------------- bank-conflict-free rotation schedule
 // One independent rotation = a perfect matching of the 128 channels of a group (absent

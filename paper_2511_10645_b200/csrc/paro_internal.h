@@ -5,6 +5,9 @@
 
 namespace paro {
 
+// thread-local error message of paro_last_error(); returns st
+int set_error(int st, const char* msg);
+
 // ---------------------------------------------------------------- pack
 cudaError_t launch_pack(const void* W, const float* s, const void* cs64, const void* idx, int64_t N, int64_t K, int L,
                         void* codes, void* scales, void* zeros, int* status, cudaStream_t st);

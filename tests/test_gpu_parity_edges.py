@@ -135,3 +135,13 @@ def test_allgather_world1(paro, B):
         paro.paro_comm_destroy(comm)
     y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"], bias=p["bias"])
     assert O.normwise_error(y.float().cpu().numpy(), y_ref) <= TOL
+
+
+@pytest.mark.parametrize("group", ["qkv", "o", "gate_up", "down"])
+def test_llama8b_bench_step_launches(paro, group):
+    """configs[1] exactly as bench.py's step launches it: the four paro_linear_multi launches
+    of the LLaMA-3-8B decode layer at bs = 1 with PDL (q/k/v at K = 4096 in one launch, o,
+    gate+up in one launch, down at K = 14336); oracle on sampled rows of every linear."""
+    shapes = {"qkv": [(4096, 4096), (1024, 4096), (1024, 4096)], "o": [(4096, 4096)],
+              "gate_up": [(14336, 4096), (14336, 4096)], "down": [(4096, 14336)]}[group]
+    _multi_sampled(paro, shapes, 1, 500 + len(group), flags=paro.PARO_LINEAR_PDL)

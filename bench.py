@@ -137,6 +137,43 @@ def build_layer_pool(torch, paro, shapes, rank, world, n_layers, dev, seed=0):
     return pool
 
 
+def clone_packed(paro, pk):
+    """The same packed linear at new addresses (so a pool of clones is streamed from HBM)."""
+    return paro.PackedLinear(pk.codes.clone(), pk.scales.clone(), pk.zeros.clone(), pk.rot_cs.clone(),
+                             pk.rot_idx.clone(), pk.svec.clone(), pk.N, pk.K, pk.n_rot)
+
+
+# the decode layer as chain stages: q/k/v share x, o reads the attention output (a separate
+# input here), gate/up share x, down reads up's output (a real dependency inside the chain)
+LAYER_STAGES = [["q_proj", "k_proj", "v_proj"], ["o_proj"], ["gate_proj", "up_proj"], ["down_proj"]]
+
+
+def layer_chain(paro, layer, x_in, x_attn, ys):
+    lin = {name: packed for name, N, K, packed in layer}
+    return [paro.ChainStage(x_in, [lin[n] for n in LAYER_STAGES[0]], [ys[n] for n in LAYER_STAGES[0]]),
+            paro.ChainStage(x_attn, [lin["o_proj"]], [ys["o_proj"]]),
+            paro.ChainStage(x_in, [lin[n] for n in LAYER_STAGES[2]], [ys[n] for n in LAYER_STAGES[2]]),
+            paro.ChainStage(ys["up_proj"], [lin["down_proj"]], [ys["down_proj"]])]
+
+
+def pool_layers(world=1):
+    """Layers in the weight pool: >= 4 x L2 of packed weights per rank (inputs larger than L2)."""
+    wb = sum(algorithmic_bytes(N // world, K, 1)[1] for N, K in synth.LLAMA3_8B_DECODE.values())
+    return min(64, max(2, int(np.ceil(4 * L2_BYTES / wb)))), wb
+
+
+def bench_config(B, world=1):
+    """The config block shared by both arms (pure arithmetic: the reference arm reports the same)."""
+    n_layers, wb = pool_layers(world)
+    return {"workload": WORKLOAD, "batch": B,
+            "step": ("one paro_linear_chain launch: 4 stages (q/k/v | o | gate/up | down reading up's y), "
+                     "grid barrier between stages") if world == 1 else "7 paro_linear_allgather calls",
+            "parallelism": f"N-shard x{world} + NCCL all-gather" if world > 1 else "single GPU",
+            "l2": (f"inputs larger than L2: weight pool of {n_layers} layers x {wb / 1e6:.1f} MB/rank "
+                   f"> 4 x 126 MB L2, cycled per step"),
+            "bytes_per_step": sum(algorithmic_bytes(N, K, B)[0] for N, K in synth.LLAMA3_8B_DECODE.values())}
+
+
 def run_paro(args):
     import torch
     import torch.distributed as dist
@@ -159,58 +196,53 @@ def run_paro(args):
         comm = pd.make_comm(rank, world)
 
     layer_bytes = sum(algorithmic_bytes(N, K, B)[0] for N, K in shapes.values())
-    weight_bytes_rank = sum(algorithmic_bytes(N // world, K, B)[1] for N, K in shapes.values())
-    n_layers = max(2, int(np.ceil(4 * L2_BYTES / max(weight_bytes_rank, 1))))
-    n_layers = min(n_layers, 64)
+    n_layers, _wb = pool_layers(world)
     pool = build_layer_pool(torch, paro, shapes, rank, world, n_layers, dev)
-    g = torch.Generator(device=dev).manual_seed(123 + rank * 0)
-    # activations and outputs are views of one contiguous buffer each (one copy per direction in e2e)
-    Ks = sorted({K for _, K in shapes.values()})
-    x_all = torch.randn((B * sum(Ks),), generator=g, device=dev).to(torch.float16)
-    xs, off = {}, 0
-    for K in Ks:
-        xs[K] = x_all[off:off + B * K].view(B, K)
-        off += B * K
+    g = torch.Generator(device=dev).manual_seed(123)
+    # the step's inputs: x of the layer (q/k/v, gate/up) and the attention output (o); outputs are
+    # views of one buffer (one copy per direction in e2e)
+    x_all = torch.randn((2 * B * 4096,), generator=g, device=dev).to(torch.float16)
+    x_in, x_attn = x_all[:B * 4096].view(B, 4096), x_all[B * 4096:].view(B, 4096)
     y_all = torch.empty((B * sum(N for N, _ in shapes.values()),), dtype=torch.float16, device=dev)
     ys, off = {}, 0
     for name, (N, K) in shapes.items():
         ys[name] = y_all[off:off + B * N].view(B, N)
         off += B * N
     ws = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
-
-    # linears that read the same activation run in one launch (q/k/v, gate/up); each keeps
-    # its own transform (Alg. A2 inserts one per linear)
-    groups = [["q_proj", "k_proj", "v_proj"], ["o_proj"], ["gate_proj", "up_proj"], ["down_proj"]]
+    chains = [layer_chain(paro, layer, x_in, x_attn, ys) for layer in pool]
+    chain_ws = paro.chain_workspace(B, chains[0])
 
     def run_step(li, flags, pdl=True):
+        """One step: the layer's seven linears (world 1: ONE persistent chain launch)."""
         f = flags | (paro.PARO_LINEAR_PDL if pdl else 0)
-        layer = {name: (N, K, packed) for name, N, K, packed in pool[li % n_layers]}
         if world == 1:
-            for grp in groups:
-                K = layer[grp[0]][1]
-                paro.paro_linear_multi(xs[K], [layer[n][2] for n in grp], y=[ys[n] for n in grp], flags=f,
-                                       workspace=ws, stream=stream)
+            paro.paro_linear_chain(chains[li % n_layers], flags=f, workspace=chain_ws, stream=stream)
         else:
-            for name, (N, K, packed) in layer.items():
-                paro.paro_linear_allgather(xs[K], packed, comm, rank, world, y=ys[name], flags=f, workspace=ws,
-                                           stream=stream)
+            layer = {name: (N, K, packed) for name, N, K, packed in pool[li % n_layers]}
+            for grp in LAYER_STAGES:
+                for name in grp:
+                    N, K, packed = layer[name]
+                    xin = ys["up_proj"] if name == "down_proj" else (x_attn if name == "o_proj" else x_in)
+                    paro.paro_linear_allgather(xin, packed, comm, rank, world, y=ys[name], flags=f, workspace=ws,
+                                               stream=stream)
 
-    def capture(flags, steps_in_graph):
+    def run_step_4launch(li, flags, pdl=True):
+        """The same step as four paro_linear_multi launches (PDL-chained): round-1 form."""
+        f = flags | (paro.PARO_LINEAR_PDL if pdl else 0)
+        for st in chains[li % n_layers]:
+            paro.paro_linear_multi(st.x, st.packed, y=st.y, flags=f, workspace=ws, stream=stream)
+
+    def timed(step_fn, flags, steps, warmup):
+        """Graph of `steps` consecutive steps (layers cycle through the pool); returns
+        max-over-ranks ms per step measured with CUDA events on the launch stream."""
         gph = torch.cuda.CUDAGraph()
         with torch.cuda.stream(stream):
             for li in range(2):
-                run_step(li, flags)
+                step_fn(li, flags)
             stream.synchronize()
             with torch.cuda.graph(gph, stream=stream):
-                for li in range(steps_in_graph):
-                    run_step(li, flags)
-        return gph
-
-    def timed(flags, steps, warmup):
-        """Graph of `steps` consecutive steps (layers cycle through the pool); returns
-        max-over-ranks ms per step measured with CUDA events on the launch stream."""
-        gph = capture(flags, steps)
-        with torch.cuda.stream(stream):
+                for li in range(steps):
+                    step_fn(li, flags)
             for _ in range(max(1, warmup // max(steps, 1) + 1)):
                 gph.replay()
             stream.synchronize()
@@ -237,136 +269,121 @@ def run_paro(args):
 
     # warm-up steps (untimed), then exactly K timed steps (in one graph replay)
     with ClockSampler(local) as clk:
-        ms_step = timed(0, args.steps, args.warmup)
-        ms_norot = timed(paro.PARO_LINEAR_NO_ROTATION, args.steps, args.warmup)
+        ms_step = timed(run_step, 0, args.steps, args.warmup)
     clocks = clk.summary()
+    ms_norot = timed(run_step, paro.PARO_LINEAR_NO_ROTATION, args.steps, args.warmup)
+    ms_4l = timed(run_step_4launch, 0, args.steps, args.warmup) if world == 1 else None
 
-    # per-linear timings (rank 0 view, same pool cycling), rotation on / off
-    per_linear = {}
+    # cold single step: L2 flushed (a 2 x L2 buffer written) before each call, median of 7
+    cold_us = None
     if world == 1:
+        flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+        vals = []
+        with torch.cuda.stream(stream):
+            for i in range(8):
+                flush.fill_(float(i))
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                run_step(i, 0, pdl=False)
+                e1.record(stream)
+                e1.synchronize()
+                if i:
+                    vals.append(e0.elapsed_time(e1) * 1e3)
+        cold_us = round(statistics.median(vals), 2)
+        del flush
+
+    # per-linear timings, rotation on / off: each linear cycles through its own pool of clones
+    # larger than 4 x L2 (inputs larger than L2), 100 calls per graph
+    per_linear = {}
+    if world == 1 and not args.no_extra:
         for name, (N, K) in shapes.items():
+            base = [e for e in pool[0] if e[0] == name][0][3]
+            nb = algorithmic_bytes(N, K, B)[1]
+            n_cl = int(np.ceil(4 * L2_BYTES / nb))
+            clones = [base] + [clone_packed(paro, base) for _ in range(n_cl - 1)]
+            xin = x_attn if name == "o_proj" else (ys["up_proj"] if name == "down_proj" else x_in)
             res = {}
             for tag, fl in (("rot", 0), ("norot", paro.PARO_LINEAR_NO_ROTATION)):
-                gph = torch.cuda.CUDAGraph()
-                reps = 100
-                with torch.cuda.stream(stream):
-                    for li in range(2):
-                        lin = [e for e in pool[li % n_layers] if e[0] == name][0]
-                        paro.paro_linear(xs[K], lin[3], y=ys[name], flags=fl, workspace=ws,
-                                         stream=stream)
-                    stream.synchronize()
-                    with torch.cuda.graph(gph, stream=stream):
-                        for li in range(reps):
-                            lin = [e for e in pool[li % n_layers] if e[0] == name][0]
-                            paro.paro_linear(xs[K], lin[3], y=ys[name], flags=fl,
-                                             workspace=ws, stream=stream)
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                with torch.cuda.stream(stream):
-                    gph.replay()
-                    stream.synchronize()
-                    e0.record(stream)
-                    gph.replay()
-                    e1.record(stream)
-                e1.synchronize()
-                res[tag] = e0.elapsed_time(e1) / reps * 1000.0  # us
-            ab, wb = algorithmic_bytes(N, K, B)
+                cnt = [0]
+
+                def call():
+                    pk = clones[cnt[0] % n_cl]
+                    cnt[0] += 1
+                    paro.paro_linear(xin, pk, y=ys[name], flags=fl | paro.PARO_LINEAR_PDL, workspace=ws, stream=stream)
+
+                res[tag] = graph_time_us(torch, stream, call, max(100, n_cl))
+            ab = algorithmic_bytes(N, K, B)[0]
             per_linear[name] = {"N": N, "K": K, "us": round(res["rot"], 3), "us_norot": round(res["norot"], 3),
-                                "GBps": round(ab / res["rot"] / 1e3, 1),
+                                "GBps": round(ab / res["rot"] / 1e3, 1), "pool_MB": round(n_cl * nb / 1e6),
                                 "rot_overhead": round(res["rot"] / res["norot"] - 1.0, 4)}
+            del clones
+        torch.cuda.empty_cache()
 
     # end-to-end through the public API with host buffers (pinned), copies inside the timed region
-    e2e = None
-    if True:
-        hx = x_all.cpu().pin_memory()
-        hy = torch.empty(y_all.shape, dtype=torch.float16).pin_memory()
-        h2d = hx.numel() * 2
-        d2h = hy.numel() * 2
-        n_e2e = max(10, min(args.steps, 200))
+    hx = x_all.cpu().pin_memory()
+    hy = torch.empty(y_all.shape, dtype=torch.float16).pin_memory()
+    h2d, d2h = hx.numel() * 2, hy.numel() * 2
+    n_e2e = max(10, min(args.steps, 200))
 
-        def e2e_step(li):
-            with torch.cuda.stream(stream):
-                x_all.copy_(hx, non_blocking=True)
-                # PDL between the decode launches (the first one follows the copy normally; each
-                # launch waits for its predecessor before reading x or writing y, so the y copy
-                # after the last launch sees every output)
-                run_step(li, 0, pdl=True)
-                hy.copy_(y_all, non_blocking=True)
+    def e2e_step(li):
+        with torch.cuda.stream(stream):
+            x_all.copy_(hx, non_blocking=True)
+            run_step(li, 0, pdl=True)  # its x loads wait (PDL) for the copy before them
+            hy.copy_(y_all, non_blocking=True)
 
-        for li in range(3):
-            e2e_step(li)
+    for li in range(3):
+        e2e_step(li)
+    stream.synchronize()
+    # the serving loop's form: each step (pinned-host x -> device, the decode chain, y -> pinned
+    # host) captured once in a CUDA graph and replayed; the copies run every step
+    per_graph = n_layers
+    gph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        with torch.cuda.graph(gph, stream=stream):
+            for li in range(per_graph):
+                e2e_step(li)
+        gph.replay()
         stream.synchronize()
-        # the serving loop's form: each step (pinned-host x -> device, the 4 decode launches,
-        # y -> pinned host) captured once in a CUDA graph and replayed; the copies run every step
-        per_graph = n_layers
-        gph = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(stream):
-            with torch.cuda.graph(gph, stream=stream):
-                for li in range(per_graph):
-                    e2e_step(li)
+    reps = max(1, n_e2e // per_graph)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(reps):
             gph.replay()
-            stream.synchronize()
-        reps = max(1, n_e2e // per_graph)
-        if world > 1:
-            dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-            for _ in range(reps):
-                gph.replay()
-            e1.record(stream)
-        e1.synchronize()
-        ms_e2e = e0.elapsed_time(e1) / (reps * per_graph)
-        if world > 1:
-            t = torch.tensor([ms_e2e], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms_e2e = float(t.item())
-        e2e = {"value": round(layer_bytes / (ms_e2e * 1e-3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms_e2e, 4),
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "api": "paper_2511_10645_b200.paro_linear_multi (4 decode launches per step) with the pinned-host "
-                      "x -> device and y -> host copies of every step, captured per step in a CUDA graph and replayed"}
+        e1.record(stream)
+    e1.synchronize()
+    ms_e2e = e0.elapsed_time(e1) / (reps * per_graph)
+    if world > 1:
+        t = torch.tensor([ms_e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    del gph
+    e2e = {"value": round(layer_bytes / (ms_e2e * 1e-3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms_e2e, 4),
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "api": ("paper_2511_10645_b200.paro_linear_chain (one launch per step)" if world == 1 else
+                   "paper_2511_10645_b200.paro_linear_allgather per linear") +
+                  " with the pinned-host x -> device and y -> host copies of every step, each step captured in a "
+                  "CUDA graph and replayed"}
 
     # prefill (SURVEY.md 8(d) "also prefill TFLOPS"): the same packed linears at 2048 tokens
     # through paro_linear's tcgen05 path (transform pre-stage + GEMM), one CUDA graph per linear
     prefill = None
     if world == 1 and not args.no_prefill:
-        Bp = 2048
-        tot_flop, tot_us, per = 0.0, 0.0, {}
-        with torch.cuda.stream(stream):
-            for name, N, K, packed in pool[0]:
-                xp = torch.randn((Bp, K), generator=g, device=dev).to(torch.float16)
-                yp = torch.empty((Bp, N), dtype=torch.float16, device=dev)
-                wsp = torch.empty(max(1, paro.paro_linear_workspace(Bp, N, K)), dtype=torch.uint8, device=dev)
-                for _ in range(2):
-                    paro.paro_linear(xp, packed, y=yp, workspace=wsp, stream=stream)
-                reps = 10
-                gp = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(gp, stream=stream):
-                    for _ in range(reps):
-                        paro.paro_linear(xp, packed, y=yp, workspace=wsp, stream=stream)
-                gp.replay()
-                stream.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                gp.replay()
-                e1.record(stream)
-                e1.synchronize()
-                us = e0.elapsed_time(e1) / reps * 1e3
-                fl = 2.0 * Bp * N * K
-                tot_flop += fl
-                tot_us += us
-                per[name] = {"us": round(us, 2), "TFLOPs": round(fl / us / 1e6, 1)}
-                del xp, yp, wsp, gp
-        tpeak = float(load_peaks().get("bf16_tflops", 1649.0))
-        prefill = {"tokens": Bp, "TFLOPs": round(tot_flop / tot_us / 1e6, 1), "us_per_layer": round(tot_us, 1),
-                   "peak_TFLOPs": tpeak, "frac": round(tot_flop / tot_us / 1e6 / tpeak, 4), "per_linear": per,
-                   "def": "2*B*N*K flop per linear / device time of transform pre-stage + tcgen05 GEMM"}
+        prefill = measure_prefill(torch, paro, dev, stream, pool[0], g)
 
-    # C1 (launch-latency bound) and C3 (Qwen3-4B 36-layer stack, B = 1 and 16): SURVEY.md 8(d)
     extra = {}
     if world == 1 and not args.no_extra:
         extra["c1"] = measure_c1(torch, paro, dev, stream)
-        extra["c3_qwen3_4b_stack"] = measure_qwen_stack(torch, paro, dev, stream, (1, 16))
-        extra["c5_llama3_70b_mlp"] = measure_70b_mlp(torch, paro, dev, stream)
+        extra["transform_vs_fwht"] = measure_transform_vs_fwht(torch, paro, dev, stream)
+        extra["c3_qwen3_4b_stack"] = measure_qwen_stack(torch, paro, dev, stream, (1, 4, 16))
+    del pool, chains
+    torch.cuda.empty_cache()
+    if not args.no_extra:
+        # configs[4]: the LLaMA-3-70B MLP, N-sharded over the ranks of this run (1 GPU: the whole
+        # layer), GEMV and all-gather reported separately
+        extra["c5_llama3_70b_mlp"] = measure_70b_mlp(torch, paro, dev, stream, comm, rank, world)
 
     if comm is not None:
         torch.cuda.synchronize()
@@ -385,23 +402,24 @@ def run_paro(args):
         "metric": METRIC, "value": round(gbps, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "us_per_step": round(ms_step * 1e3, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f16 act / int4 weight / f32 acc",
-        "data": "synthetic (random fp16 W ~ N(0,0.02^2) packed W4 g128 with Alg. A1 pairs, random theta/s; x ~ N(0,1))",
-        "config": {"workload": WORKLOAD, "batch": B, "pool_layers": n_layers,
-                   "l2": f"inputs larger than L2: weight pool {n_layers} layers x "
-                         f"{weight_bytes_rank / 1e6:.1f} MB/rank > 126 MB L2, cycled per step",
-                   "parallelism": f"N-shard x{world} + NCCL all-gather" if world > 1 else "single GPU",
-                   "bytes_per_step": layer_bytes},
         "rotation_overhead": round(ms_step / ms_norot - 1.0, 4), "us_per_step_norot": round(ms_norot * 1e3, 3),
-        "per_linear": per_linear,
+        "frac_of_8TBps": round(gbps / 8000.0, 4),
+        "us_per_step_4_launches": None if ms_4l is None else round(ms_4l * 1e3, 3),
+        "cold_step_us": cold_us,
+        "data": "synthetic (random fp16 W ~ N(0,0.02^2) packed W4 g128 with Alg. A1 pairs, random theta/s; x ~ N(0,1))",
+        "config": bench_config(B, world),
         "roofline": {"bound": "hbm", "achieved": round(gbps, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(gbps / peak, 4), "traffic": None,
-                     "kernel": "paro_gemv1_kernel (all launches of the step)",
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not peaks.get("_fallback") else "fallback 6.65 TB/s",
-                     "achieved_def": "algorithmic bytes per step / device time per step (all GEMV launches, gaps included)"},
-        "clocks": clocks, "e2e": e2e, "prefill": prefill, **extra,
-        "gpu_launches": (4 if world == 1 else 14) * args.steps,
-        "gpu_launches_note": ("4 paro_gemv1_kernel launches per step (q/k/v and gate/up fused by shared input)"
-                              if world == 1 else "7 paro_gemv1_kernel + 7 ncclAllGather launches per step"),
+                     "kernel": "paro_gemv1_kernel (the step's one chain launch)",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if not peaks.get("_fallback")
+                     else "fallback 6.65 TB/s",
+                     "achieved_def": "algorithmic bytes per step (SURVEY.md 8(d): 0.5195 B/weight + 6 B/pair + 4 B/ch "
+                                     "s + 2BK + 2BN) / device time per step"},
+        "clocks": clocks, "e2e": e2e,
+        "gpu_launches": (1 if world == 1 else 14) * args.steps,
+        "gpu_launches_note": ("1 paro_gemv1_kernel (persistent 4-stage chain) launch per step" if world == 1
+                              else "7 paro_gemv1_kernel + 7 ncclAllGather launches per step"),
+        "per_linear": per_linear, "prefill": prefill, **extra,
     }
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args)
@@ -436,6 +454,33 @@ def graph_time_us(torch, stream, fn, reps):
     return e0.elapsed_time(e1) / reps * 1e3
 
 
+def measure_transform_vs_fwht(torch, paro, dev, stream, tokens=(1, 2048)):
+    """SURVEY.md 8(f) NEXT #2, the paper's kernel experiment (fig:kernel-speedup):
+    the standalone scaled pairwise rotation (paro_transform_activations: s, then 8 rotations of
+    <= 64 pairs per 128-channel group) vs the fast Walsh-Hadamard transform over all n channels
+    (paro_fwht, randomised: signs, butterfly, 1/sqrt(n)), same fp16 activations, fp16 outputs,
+    device time per call (graph of repeated calls)."""
+    out = {}
+    for n in (256, 512, 1024, 2048, 4096, 8192, 16384):
+        p = synth.make_problem(32, n, 1, seed=n)
+        t = {k: torch.from_numpy(p[k]).to(dev) for k in ("W", "s", "theta", "pairs")}
+        packed = paro.paro_pack(t["W"], t["s"], t["theta"], t["pairs"])
+        signs = torch.from_numpy(np.random.default_rng(n).choice([-1.0, 1.0], size=n).astype(np.float32)).to(dev)
+        row = {}
+        for T in tokens:
+            x = torch.randn((T, n), device=dev).to(torch.float16)
+            yr = torch.empty((T, n), dtype=torch.float16, device=dev)
+            yf = torch.empty((T, n), dtype=torch.float16, device=dev)
+            reps = 50 if T <= 16 else 20
+            ur = graph_time_us(torch, stream, lambda: paro.paro_transform_activations(x, packed, out=yr, stream=stream),
+                               reps)
+            uf = graph_time_us(torch, stream, lambda: paro.paro_fwht(x, signs, 1.0 / np.sqrt(n), out=yf, stream=stream),
+                               reps)
+            row[f"T{T}"] = {"rotation_us": round(ur, 3), "fwht_us": round(uf, 3), "speedup": round(uf / ur, 3)}
+        out[str(n)] = row
+    return out
+
+
 def measure_c1(torch, paro, dev, stream):
     """configs[0]: one K = N = 256 linear, bs=1 (launch-latency bound: report us)."""
     p = synth.make_problem(256, 256, 1, seed=7)
@@ -451,63 +496,109 @@ def measure_c1(torch, paro, dev, stream):
             "def": "device time per paro_linear call, 200 calls in one CUDA graph (weights L2-resident)"}
 
 
+def measure_prefill(torch, paro, dev, stream, layer, g):
+    """The layer's linears at 2048 tokens through paro_linear's tcgen05 path (transform
+    pre-stage + GEMM), one CUDA graph per linear; TFLOP/s = 2 B N K / device time."""
+    Bp = 2048
+    tot_flop, tot_us, per = 0.0, 0.0, {}
+    with torch.cuda.stream(stream):
+        for name, N, K, packed in layer:
+            xp = torch.randn((Bp, K), generator=g, device=dev).to(torch.float16)
+            yp = torch.empty((Bp, N), dtype=torch.float16, device=dev)
+            wsp = torch.empty(max(1, paro.paro_linear_workspace(Bp, N, K)), dtype=torch.uint8, device=dev)
+            us = graph_time_us(torch, stream, lambda: paro.paro_linear(xp, packed, y=yp, workspace=wsp, stream=stream),
+                               10)
+            fl = 2.0 * Bp * N * K
+            tot_flop += fl
+            tot_us += us
+            per[name] = {"us": round(us, 2), "TFLOPs": round(fl / us / 1e6, 1)}
+            del xp, yp, wsp
+    tpeak = float(load_peaks().get("bf16_tflops", 1649.0))
+    return {"tokens": Bp, "TFLOPs": round(tot_flop / tot_us / 1e6, 1), "us_per_layer": round(tot_us, 1),
+            "peak_TFLOPs": tpeak, "frac": round(tot_flop / tot_us / 1e6 / tpeak, 4), "per_linear": per,
+            "def": "2*B*N*K flop per linear / device time of transform pre-stage + tcgen05 GEMM; peak: "
+                   "MEASURED_PEAKS.json bf16 burst (fp16 dense = bf16 rate)"}
+
+
 def measure_qwen_stack(torch, paro, dev, stream, batches):
     """configs[2]: the Qwen3-4B decode stack (36 layers x 7 linears, each with its own
-    transform; q/k/v and gate/up share their input: 4 launches per layer), one CUDA graph
-    per step with PDL; 1.9 GB of packed weights, so every step streams from HBM."""
+    transform), every layer 4 chain stages (q/k/v | o | gate/up | down reading up's y): 144
+    stages = 9 persistent launches per step; 1.9 GB of packed weights, so every step streams
+    from HBM.  Bytes per step include the B-token activations."""
     shapes = synth.QWEN3_4B_LAYER
     pool = build_layer_pool(torch, paro, shapes, 0, 1, synth.QWEN3_4B_LAYERS, dev, seed=11)
-    groups = [["q_proj", "k_proj", "v_proj"], ["o_proj"], ["gate_proj", "up_proj"], ["down_proj"]]
-    step_bytes = sum(algorithmic_bytes(N, K, 1)[0] for N, K in shapes.values()) * synth.QWEN3_4B_LAYERS
-    out = {"layers": synth.QWEN3_4B_LAYERS, "weight_bytes": int(step_bytes)}
+    out = {"layers": synth.QWEN3_4B_LAYERS}
     for B in batches:
+        step_bytes = sum(algorithmic_bytes(N, K, B)[0] for N, K in shapes.values()) * synth.QWEN3_4B_LAYERS
         g = torch.Generator(device=dev).manual_seed(5 + B)
-        xs = {K: torch.randn((B, K), generator=g, device=dev).to(torch.float16) for _, K in shapes.values()}
+        x_in = torch.randn((B, 2560), generator=g, device=dev).to(torch.float16)
+        x_attn = torch.randn((B, 4096), generator=g, device=dev).to(torch.float16)
         ys = {n: torch.empty((B, N), dtype=torch.float16, device=dev) for n, (N, K) in shapes.items()}
-        ws = torch.empty(1 << 20, dtype=torch.uint8, device=dev)
-
-        def step():
-            for layer in pool:
-                lin = {name: packed for name, N, K, packed in layer}
-                for grp in groups:
-                    K = shapes[grp[0]][1]
-                    paro.paro_linear_multi(xs[K], [lin[n] for n in grp], y=[ys[n] for n in grp],
-                                           flags=paro.PARO_LINEAR_PDL, workspace=ws, stream=stream)
-
-        us = graph_time_us(torch, stream, step, 3)
-        out[f"bs{B}"] = {"us_per_step": round(us, 1), "GBps": round(step_bytes / us / 1e3, 1)}
+        stages = []
+        for layer in pool:
+            stages += layer_chain(paro, layer, x_in, x_attn, ys)
+        ws = paro.chain_workspace(B, stages)
+        res = {}
+        for tag, fl in (("rot", 0), ("norot", paro.PARO_LINEAR_NO_ROTATION)):
+            res[tag] = graph_time_us(torch, stream, lambda: paro.paro_linear_chain(
+                stages, flags=fl | paro.PARO_LINEAR_PDL, workspace=ws, stream=stream), 3)
+        out[f"bs{B}"] = {"us_per_step": round(res["rot"], 1), "GBps": round(step_bytes / res["rot"] / 1e3, 1),
+                         "bytes_per_step": int(step_bytes), "rot_overhead": round(res["rot"] / res["norot"] - 1.0, 4)}
+        del stages, ws
     del pool
     torch.cuda.empty_cache()
     return out
 
 
-def measure_70b_mlp(torch, paro, dev, stream):
-    """configs[4] at one GPU: the LLaMA-3-70B MLP linears (gate/up 8192 -> 28672 in one launch,
-    down 28672 -> 8192) at bs=1; two layer copies (732 MB) alternate, so every call streams from
-    HBM.  The 2/4/8-GPU N-sharded numbers come from `torchrun ... bench.py --gpus N` (rows per
-    rank, NCCL all-gather)."""
+def measure_70b_mlp(torch, paro, dev, stream, comm, rank, world):
+    """configs[4]: the LLaMA-3-70B MLP linears (gate/up 8192 -> 28672, down 28672 -> 8192) at
+    bs=1, rows sharded over the `world` ranks of this run; two layer copies
+    alternate, so every call streams from HBM.  Reported per rank: the shard GEMV alone, the
+    GEMV + NCCL all-gather (paro_linear_allgather; world 1: the plain GEMV), and their difference
+    as the all-gather cost; max over ranks."""
+    import torch.distributed as dist
     shapes = synth.LLAMA3_70B_MLP
-    pool = build_layer_pool(torch, paro, shapes, 0, 1, 2, dev, seed=23)
-    x = {K: torch.randn((1, K), device=dev).to(torch.float16) for _, K in shapes.values()}
-    ys = {n: torch.empty((1, N), dtype=torch.float16, device=dev) for n, (N, K) in shapes.items()}
-    out = {}
-    for grp in (["gate_proj", "up_proj"], ["down_proj"]):
-        K = shapes[grp[0]][1]
-        nbytes = sum(algorithmic_bytes(shapes[n][0], K, 1)[0] for n in grp)
+    pool = build_layer_pool(torch, paro, shapes, rank, world, 2, dev, seed=23)
+    x = torch.randn((1, 8192), device=dev).to(torch.float16)
+    ys = {n: torch.zeros((1, N), dtype=torch.float16, device=dev) for n, (N, K) in shapes.items()}
+    ysh = {n: torch.zeros((1, N // world), dtype=torch.float16, device=dev) for n, (N, K) in shapes.items()}
+    ws = torch.empty(16 << 20, dtype=torch.uint8, device=dev)
+    out = {"world": world}
+    tot = {"gemv_us": 0.0, "total_us": 0.0}
+    for name, (N, K) in shapes.items():
+        xin = ys["up_proj"] if name == "down_proj" else x
         res = {}
-        for tag, fl in (("rot", 0), ("norot", paro.PARO_LINEAR_NO_ROTATION)):
+        for tag in ("gemv", "total", "norot"):
             cnt = [0]
 
             def call():
-                layer = {name: packed for name, N, K_, packed in pool[cnt[0] % 2]}
+                pk = [e for e in pool[cnt[0] % 2] if e[0] == name][0][3]
                 cnt[0] += 1
-                paro.paro_linear_multi(x[K], [layer[n] for n in grp], y=[ys[n] for n in grp],
-                                       flags=fl | paro.PARO_LINEAR_PDL, stream=stream)
+                if tag == "total" and world > 1:
+                    paro.paro_linear_allgather(xin, pk, comm, rank, world, y=ys[name], flags=paro.PARO_LINEAR_PDL,
+                                               workspace=ws, stream=stream)
+                else:
+                    fl = paro.PARO_LINEAR_NO_ROTATION if tag == "norot" else 0
+                    paro.paro_linear(xin, pk, y=ysh[name], flags=fl | paro.PARO_LINEAR_PDL, workspace=ws,
+                                     stream=stream)
 
-            res[tag] = graph_time_us(torch, stream, call, 20)
-        out["+".join(grp)] = {"us": round(res["rot"], 2), "us_norot": round(res["norot"], 2),
-                              "GBps": round(nbytes / res["rot"] / 1e3, 1),
-                              "rot_overhead": round(res["rot"] / res["norot"] - 1.0, 4)}
+            us = graph_time_us(torch, stream, call, 20)
+            if world > 1:
+                t = torch.tensor([us], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                us = float(t.item())
+            res[tag] = us
+        nbytes = algorithmic_bytes(N // world, K, 1)[0]
+        out[name] = {"gemv_us": round(res["gemv"], 2), "allgather_us": round(res["total"] - res["gemv"], 2),
+                     "total_us": round(res["total"], 2), "GBps_per_gpu": round(nbytes / res["gemv"] / 1e3, 1),
+                     "rot_overhead": round(res["gemv"] / res["norot"] - 1.0, 4)}
+        tot["gemv_us"] += res["gemv"]
+        tot["total_us"] += res["total"]
+    all_bytes = sum(algorithmic_bytes(N, K, 1)[0] for N, K in shapes.values())
+    out["mlp"] = {"gemv_us": round(tot["gemv_us"], 2), "allgather_us": round(tot["total_us"] - tot["gemv_us"], 2),
+                  "total_us": round(tot["total_us"], 2),
+                  "aggregate_GBps": round(all_bytes / tot["total_us"] / 1e3, 1),
+                  "def": "one call per linear (gate, up, down reading up's y), each timed alone in a graph of 20"}
     del pool
     torch.cuda.empty_cache()
     return out
@@ -582,7 +673,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "batch": 1},
+        "config": bench_config(1, world),
         "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)

@@ -170,6 +170,43 @@ paro_status paro_linear_multi(const void* x, paro_dtype x_dtype, int64_t B, int3
                               const float* const* bias, void* const* y, paro_dtype y_dtype, uint32_t flags,
                               void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- persistent decode chain (fused multi-linear launches, chained) ----
+ * A chain is a sequence of decode stages; stage s computes, like paro_linear_multi,
+ * y[i] = (T_i^{-1} x) . dequant(Q_i)^T + bias[i] for its n (1..4) linears sharing one x.
+ * Stages run IN ORDER with stream semantics: stage s + 1 sees every y stored by stages
+ * <= s, so its x may be (a view of) an earlier stage's y (e.g. the down projection reading
+ * the up projection's output, or the next layer's q/k/v reading a residual stream the
+ * caller's kernels do not touch in between).  Up to 16 stages run in ONE persistent kernel
+ * launch: one wave of CTAs, a grid-wide barrier between stages, and the packed weights of
+ * all stages streamed back to back through each CTA's shared-memory ring (the weights never
+ * depend on earlier stages), so the HBM stream does not stop at stage boundaries; longer
+ * chains run as several such launches.  Same arithmetic, layout and precision as
+ * paro_linear (Eq. 1, 2, 5, 8).
+ *   stages   host array of n_stages; each entry's packed / bias / y are host arrays of n
+ *            (bias may be NULL, its entries may be NULL); x and y[i] device, 16-B aligned.
+ *            All linears of a stage share K; x is [B][K] of x_dtype, y[i] [B][N_i] of y_dtype.
+ *   B        1..16 tokens (decode).
+ *   flags    PARO_LINEAR_PDL (the first launch overlaps the previous kernel's tail; the
+ *            packed weights must not be written by it), PARO_LINEAR_NO_ROTATION.
+ *   workspace  >= paro_linear_chain_workspace(...) bytes, device, 16-B aligned.  Its first
+ *            256 bytes hold the grid-barrier words: they must be ZERO before the first call
+ *            (e.g. one cudaMemsetAsync at allocation); every call leaves them zero.  A
+ *            workspace serves one chain at a time (do not share it between streams).
+ * A stage's x must not be written by a LATER stage of the same chain (it is read after the
+ * earlier stages only).  Asynchronous, no allocation.  Errors: as paro_linear_multi, plus
+ * PARO_ERR_UNSUPPORTED for B > 16. */
+typedef struct {
+  const void* x;
+  int32_t n;
+  const paro_packed* packed;
+  const float* const* bias;
+  void* const* y;
+} paro_chain_stage;
+size_t paro_linear_chain_workspace(int64_t B, int32_t n_stages, const paro_chain_stage* stages);
+paro_status paro_linear_chain(int32_t n_stages, const paro_chain_stage* stages, paro_dtype x_dtype, int64_t B,
+                              paro_dtype y_dtype, uint32_t flags, void* workspace, size_t workspace_bytes,
+                              void* stream);
+
 /* paro_transform_activations: x' = R_L ... R_1 diag(s) x for every token (the
  * activation side of Eq. 2 / Eq. 5), written as fp16 [B, K] (x_out, device).
  * Uses the transform captured in `packed` (its codes/scales/zeros are not read).
@@ -182,6 +219,19 @@ paro_status paro_transform_activations(const void* x, paro_dtype x_dtype, int64_
  * codes u8 [N, K], scales fp16 [N, K/128], zeros u8 [N, K/128].  Asynchronous. */
 paro_status paro_unpack_logical(const paro_packed* packed, void* codes_u8, void* scales_f16, void* zeros_u8,
                                 void* stream);
+
+/* ---- fast Walsh-Hadamard transform (comparison transform) ----
+ * The transform the paper's kernel experiment compares against (fig:kernel-speedup,
+ * PAPER.md:200-209): per token, y = scale * H_n diag(signs) x with H_n the
+ * Sylvester Hadamard matrix, H[i, j] = (-1)^popcount(i & j) (the unnormalised butterfly;
+ * scale = 1/sqrt(n) and random +-1 signs give the randomised orthogonal variant).
+ *   x      device [T, n] fp16 / bf16, 16-B aligned       T  tokens (> 0)
+ *   n      power of two in [256, 16384]                   signs  device fp32 [n] or NULL (all +1)
+ *   y      device [T, n] fp16 (fp32 arithmetic, one rounding)
+ * Asynchronous on `stream`, no allocation.  Errors: PARO_ERR_INVALID_ARGUMENT (NULL /
+ * misaligned pointers, T <= 0), PARO_ERR_UNSUPPORTED (n, dtype), PARO_ERR_CUDA. */
+paro_status paro_fwht(const void* x, paro_dtype x_dtype, int64_t T, int64_t n, const float* signs, float scale,
+                      void* y, void* stream);
 
 /* ---- Alg. A1: selection of independent channel pairs ----
  * PAPER.md:509-553 (Alg. A1): for each of `n_groups` groups of g

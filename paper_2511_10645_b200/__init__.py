@@ -45,6 +45,11 @@ class paro_packed(ctypes.Structure):
                 ("N", ctypes.c_int64), ("K", ctypes.c_int64), ("group", ctypes.c_int32), ("n_rot", ctypes.c_int32)]
 
 
+class paro_chain_stage(ctypes.Structure):
+    _fields_ = [("x", ctypes.c_void_p), ("n", ctypes.c_int32), ("packed", ctypes.POINTER(paro_packed)),
+                ("bias", ctypes.POINTER(ctypes.c_void_p)), ("y", ctypes.POINTER(ctypes.c_void_p))]
+
+
 # (name, restype, argtypes) of every symbol declared in include/paro.h
 _P, _I64, _I32, _U32, _SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_size_t
 _PP = ctypes.POINTER(paro_packed)
@@ -56,6 +61,9 @@ SIGNATURES = {
                                    _SZ, _P]),
     "paro_linear_multi": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I32, _PP, _P, _P, ctypes.c_int, _U32, _P, _SZ,
                                          _P]),
+    "paro_linear_chain_workspace": (_SZ, [_I64, _I32, ctypes.POINTER(paro_chain_stage)]),
+    "paro_linear_chain": (ctypes.c_int, [_I32, ctypes.POINTER(paro_chain_stage), ctypes.c_int, _I64, ctypes.c_int, _U32,
+                                         _P, _SZ, _P]),
     "paro_transform_activations": (ctypes.c_int, [_P, ctypes.c_int, _I64, _PP, _P, _P]),
     "paro_unpack_logical": (ctypes.c_int, [_PP, _P, _P, _P, _P]),
     "paro_comm_unique_id": (ctypes.c_int, [_P]),
@@ -66,6 +74,7 @@ SIGNATURES = {
     "paro_linear_allgather": (ctypes.c_int, [_P, ctypes.c_int, _I64, _PP, _P, _P, ctypes.c_int, _U32, _P, _SZ, _P,
                                              _I32, _I32, _P]),
     "paro_select_pairs": (ctypes.c_int, [_I64, _I32, _I32, _I32, ctypes.c_uint64, _P]),
+    "paro_fwht": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _P, ctypes.c_float, _P, _P]),
     "paro_last_error": (ctypes.c_char_p, []),
     "paro_version": (ctypes.c_char_p, []),
 }
@@ -212,6 +221,54 @@ def paro_linear_multi(x, packed: list, bias=None, y=None, out_dtype=None, flags:
     return y
 
 
+class ChainStage:
+    """One stage of a decode chain: linears `packed` sharing activation `x` (a [B, K] tensor that
+    may be a view of an earlier stage's output), outputs `y` (list of [B, N_i] tensors), `bias`."""
+
+    def __init__(self, x, packed: list, y: list, bias=None):
+        self.x, self.packed, self.y, self.bias = x, list(packed), list(y), bias
+
+
+def _chain_structs(stages):
+    keep, arr = [], (paro_chain_stage * len(stages))()
+    for k, st in enumerate(stages):
+        n = len(st.packed)
+        structs = (paro_packed * n)(*[p.struct() for p in st.packed])
+        ys = (ctypes.c_void_p * n)(*[t.data_ptr() for t in st.y])
+        bs = None if st.bias is None else (ctypes.c_void_p * n)(*[_ptr(b) for b in st.bias])
+        keep += [structs, ys, bs]
+        arr[k].x = _ptr(st.x)
+        arr[k].n = n
+        arr[k].packed = ctypes.cast(structs, ctypes.POINTER(paro_packed))
+        arr[k].bias = None if bs is None else ctypes.cast(bs, ctypes.POINTER(ctypes.c_void_p))
+        arr[k].y = ctypes.cast(ys, ctypes.POINTER(ctypes.c_void_p))
+    return arr, keep
+
+
+def paro_linear_chain_workspace(B: int, stages) -> int:
+    arr, _keep = _chain_structs(stages)
+    return int(_lib.paro_linear_chain_workspace(B, len(stages), arr))
+
+
+def chain_workspace(B: int, stages, device=None):
+    """A zero-initialised workspace for paro_linear_chain (its barrier words must start at 0)."""
+    torch = _torch()
+    dev = device if device is not None else stages[0].x.device
+    return torch.zeros(max(256, paro_linear_chain_workspace(B, stages)), dtype=torch.uint8, device=dev)
+
+
+def paro_linear_chain(stages, flags: int = 0, workspace=None, stream=None):
+    """Run decode stages in order in one persistent launch (<= 16 stages per launch): stage s + 1
+    may read an earlier stage's y as its x (include/paro.h, paro_linear_chain)."""
+    B = stages[0].x.shape[0]
+    if workspace is None:
+        workspace = chain_workspace(B, stages)
+    arr, _keep = _chain_structs(stages)
+    _check(_lib.paro_linear_chain(len(stages), arr, _dt(stages[0].x), B, _dt(stages[0].y[0]), flags,
+                                  _ptr(workspace), workspace.numel(), _stream(stream)))
+    return [st.y for st in stages]
+
+
 def paro_transform_activations(x, packed: PackedLinear, out=None, stream=None):
     torch = _torch()
     if out is None:
@@ -232,6 +289,16 @@ def paro_unpack_logical(packed: PackedLinear, stream=None):
     st = packed.struct()
     _check(_lib.paro_unpack_logical(ctypes.byref(st), _ptr(codes), _ptr(scales), _ptr(zeros), _stream(stream)))
     return codes, scales, zeros
+
+
+def paro_fwht(x, signs=None, scale: float = 1.0, out=None, stream=None):
+    """y (fp16) = scale * H_n diag(signs) x per row of x [T, n] (include/paro.h, paro_fwht)."""
+    torch = _torch()
+    T, n = x.shape
+    if out is None:
+        out = torch.empty((T, n), dtype=torch.float16, device=x.device)
+    _check(_lib.paro_fwht(_ptr(x), _dt(x), T, n, _ptr(signs), float(scale), _ptr(out), _stream(stream)))
+    return out
 
 
 # ---------------------------------------------------------------- Alg. A1 (host)

@@ -1,12 +1,13 @@
-// gemv1.cu -- decode path (B = 1 fused; B = 2..16 with a transform pre-kernel): scale + L
-// Givens layers + group-wise INT4 dequant GEMV, one launch per (multi-)linear, built for the
-// shortest serial chain.
+// gemv1.cu -- decode path: scale + L Givens layers + group-wise INT4 dequant GEMV, as a
+// PERSISTENT CHAIN of stages in one launch (a stage = one multi-linear GEMV whose linears share
+// x; a single paro_linear / paro_linear_multi call is a one-stage chain).
 //
 // SURVEY.md 8(a) rows a4 (u = s . x), a5 (the L rotations, Eq. 5 in column
 // form), a6 (dequant GEMV, Eq. 1 dequantisation (q - z) * S),
-// a8 (bias + output rounding, Eq. 2).
+// a8 (bias + output rounding, Eq. 2); SURVEY.md 8(f) NEXT #1 (fused multi-linear
+// launches chained without a kernel boundary).
 //
-// Work split (K-split inside a thread-block cluster):
+// Work split (K-split inside a thread-block cluster), per stage:
 //  * a cluster of CL CTAs (one per SM, one wave) owns a run of 32-row blocks of one linear;
 //  * CTA c of the cluster owns the groups [c G / CL, (c + 1) G / CL) of those rows.  It
 //    transforms ONLY its own groups (a warp per group: the rotation is group-local, so no
@@ -15,15 +16,19 @@
 //    fixed order) and the owner CTA of a row writes y.  Within a CTA, B = 1 keeps per-warp row
 //    partials summed in a fixed order (deterministic) unless the cluster has too many rows;
 //    B > 1 and those clusters use shared-memory atomics.
-// Pipeline per CTA: one producer warp issues the weight stages with cp.async.bulk (TMA engine)
-// -- the first ones at kernel start, before the programmatic-dependent-launch wait, because
-// packed weights are never written by the previous kernel; the rest once the compute warps'
-// rotation parameters and x are requested, so those latency-critical loads do not queue behind
-// the weight stream -- while the compute warps load their rotation parameters, wait for the
-// previous kernel (x may be its output), load x, rotate in shared memory and leave x' as
-// fixed-point digits in shared memory; then the tiles are consumed as they land.
-// B = 2..16: paro_gemv1_xform_kernel (below) computes the digits of all tokens once per
-// (linear, group, four tokens) and the producer bulk-copies this CTA's groups' slice.
+// Chain: stage s + 1 may read an earlier stage's y as its x, so every CTA passes a grid-wide
+// barrier (all CTAs co-resident: one wave) after storing its stage-s rows and before loading
+// stage s + 1's x.  The WEIGHTS never depend on earlier stages: one producer warp per CTA streams
+// the tiles of all stages, back to back, through one cp.async.bulk (TMA engine) ring, so while a
+// stage's dependent chain runs (reduction, store, barrier, x load, transform) the ring fills with
+// the next stage's weights and the HBM stream does not stop at stage boundaries.  Stage 0's
+// first batches go out before the programmatic-dependent-launch wait (packed weights are never
+// written by the previous kernel); the rest once the compute warps' rotation parameters and x
+// are requested, so those latency-critical loads do not queue behind the weight stream.
+// B = 2..16: stage 0's x' digits of all tokens come from paro_gemv1_xform_kernel (once per
+// (linear, group, four tokens)); later stages compute them inside the launch (every warp of the
+// grid takes transform tasks, then one more grid barrier) -- the producer / thread 0
+// bulk-copies each CTA's groups' slice.
 //
 // Dot product on the warp-level integer tensor cores (IMMA.16832, u8 x s8 -> s32, exact):
 // x' of a group becomes 16-bit fixed point x'fix = rint(x' 2^(14 - E)) with 2^E >= max |x'|
@@ -37,41 +42,21 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "paro_internal.h"
 #include "ptx.cuh"
 #include "tile_layout.cuh"
+#include "umma.cuh"
 
 namespace paro {
-
-#ifndef G1_TL
-#define G1_TL 0  // 1: per-CTA %globaltimer timeline of every launch (tools/timeline1.py)
-#endif
-#if G1_TL
-__device__ unsigned long long g_g1_tl[1024 * 12];
-extern "C" int paro_debug_read_timeline1(unsigned long long* host, int n) {
-  if (n > 1024 * 12) n = 1024 * 12;
-  return static_cast<int>(cudaMemcpyFromSymbol(host, g_g1_tl, sizeof(unsigned long long) * n));
-}
-#endif
 
 namespace {
 #ifndef G1_NWARPS
 #define G1_NWARPS 16
 #endif
-constexpr int G1_NW = G1_NWARPS;
-__device__ __forceinline__ void g1_mark(int ev) {
-#if G1_TL
-  if (blockIdx.x < 1024) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_g1_tl[blockIdx.x * 12 + ev] = t;
-  }
-#else
-  (void)ev;
-#endif
-}  // compute warps per CTA (+ 1 producer warp)
+constexpr int G1_NW = G1_NWARPS;  // compute warps per CTA (+ 1 producer warp)
 constexpr uint32_t TILE_B = TILE_CODE_BYTES + TILE_SCALE_BYTES + TILE_ZERO_BYTES;
 
 // D(16x8 s32) += A(16x32 u8, row) * B(32x8 s8, col); fragments as in ptx.cuh (imma_16832),
@@ -83,322 +68,501 @@ __device__ __forceinline__ void mma_u8s8(int (&d)[4], uint32_t a0, uint32_t a1, 
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+// This CTA's share of a stage.
+struct G1Geom {
+  int li;         // linear
+  int active;     // the CTA has work in this stage
+  int rb0, R;     // first row block, rows (cluster-wide)
+  int ga, gc;     // first group, groups (this CTA's K-split share)
+  int n_tiles, n_batches;
+  int RR, my_lo, my_n;  // reduction: rows per owner CTA, my owned rows
+  int nrb, nch;         // B > 1: row blocks; group chunks per row-block quad
+};
+
+// B = 1: a batch is TPS consecutive tiles of the sequence (row block, group).  B > 1: a batch
+// is (row-block quad q, group chunk c): the tiles (4 q + j, gamma) for j < 4 and gamma in chunk
+// c of TPS / 4 groups, stored j-major (the four row blocks of one group form one M = 128 MMA).
+__device__ __forceinline__ G1Geom g1_geom(const Gemv1Stage& S, int CL, int crank, int TPS, bool quads) {
+  G1Geom g{};
+  const int bx = static_cast<int>(blockIdx.x);
+  g.active = bx < S.n_cta;
+  if (!g.active) return g;
+  int li = 0;
+#pragma unroll 1
+  while (li + 1 < S.n_lin && bx >= S.lin[li + 1].cta_begin) ++li;
+  g.li = li;
+  const Gemv1Linear& d = S.lin[li];
+  const int cl = (bx - d.cta_begin) / CL;
+  const int nrb = d.rb_base + (cl < d.rb_extra ? 1 : 0);
+  g.rb0 = cl * d.rb_base + min(cl, d.rb_extra);
+  g.R = nrb * TILE_ROWS;
+  g.ga = crank * S.G / CL;
+  g.gc = (crank + 1) * S.G / CL - g.ga;
+  g.n_tiles = nrb * g.gc;
+  g.nrb = nrb;
+  if (quads) {
+    const int m = TPS / 4;
+    g.nch = (g.gc + m - 1) / m;
+    g.n_batches = ((nrb + 3) / 4) * g.nch;
+  } else {
+    g.n_batches = (g.n_tiles + TPS - 1) / TPS;
+  }
+  g.RR = (g.R + CL - 1) / CL;
+  g.my_lo = crank * g.RR;
+  g.my_n = max(0, min(g.RR, g.R - g.my_lo));
+  return g;
+}
+
+// x' of one group of one token chunk as fixed point + s8 digits laid out as the GEMV's B
+// fragments [quad t][column][k-block kb][b0, b1]; column 2 cb + dg = digit dg (0 hi, 1 lo) of
+// token cb of the column set; k-block kb = 2 p + h covers the low (p = 0) or high (p = 1)
+// nibbles of words 2h, 2h + 1 (b0: word 2h, b1: word 2h + 1); byte bb of the word for quad t,
+// word j, parity p is channel tile_k(t, j, 2 bb + p).  sc: the group's 128 rotated values
+// (fp32, overwritten with x'fix).  Returns (sum x'fix, bits of 2^(E - 14)) in lane 0's result.
+template <int NCOLS>
+__device__ __forceinline__ int2 g1_digits(float* sc, int lane, uint8_t* dst_set, int cb) {
+  int* fx = reinterpret_cast<int*>(sc);
+  const float4 v = *reinterpret_cast<const float4*>(sc + 4 * lane);
+  const float ml = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+  const uint32_t mb = __reduce_max_sync(0xffffffffu, __float_as_uint(ml));  // |x| bits order like |x|
+  int E = mb < 0x00800000u ? -100 : static_cast<int>(mb >> 23) - 127 + ((mb & 0x7fffffu) != 0u ? 1 : 0);
+  E = max(E, -100);
+  const float mul = __uint_as_float(static_cast<uint32_t>(141 - E) << 23);  // 2^(14 - E)
+  const int f0 = __float2int_rn(v.x * mul), f1 = __float2int_rn(v.y * mul);
+  const int f2 = __float2int_rn(v.z * mul), f3 = __float2int_rn(v.w * mul);
+  const int X = __reduce_add_sync(0xffffffffu, (f0 + f1) + (f2 + f3));
+  __syncwarp();  // every lane has read its x' before the scratch holds x'fix
+  *reinterpret_cast<int4*>(fx + 4 * lane) = make_int4(f0, f1, f2, f3);
+  __syncwarp();
+  const int tq = lane >> 3, col = (lane >> 2) & 1, kb = lane & 3, p = kb >> 1, h = kb & 1;
+  uint32_t wd[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int j = 2 * h + e;
+    uint32_t wv = 0;
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb) {
+      const int c = 16 * (2 * j + p) + 2 * tq + (bb >> 1) + 8 * (bb & 1);  // tile_k(tq, j, 2 bb + p)
+      const int f = fx[c];
+      const int lo = static_cast<int>(static_cast<int8_t>(f & 0xff));
+      const int dg = col ? lo : ((f - lo) >> 8);
+      wv |= (static_cast<uint32_t>(dg) & 0xffu) << (8 * bb);
+    }
+    wd[e] = wv;
+  }
+  *reinterpret_cast<uint2*>(dst_set + tq * (NCOLS * 32) + (2 * cb + col) * 32 + kb * 8) = make_uint2(wd[0], wd[1]);
+  return make_int2(X, static_cast<int>(static_cast<uint32_t>(113 + E) << 23));  // 2^(E - 14)
+}
+
+// a4 for TB tokens of one group: scr[tb][128] = s . x_tb
+template <int TB>
+__device__ __forceinline__ void g1_scale(float* scr, const uint2 (&xv)[TB], int x_bf16, float4 sv, int lane) {
+#pragma unroll
+  for (int tb = 0; tb < TB; ++tb) {
+    float2 f01, f23;
+    if (x_bf16) {
+      f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv[tb].x));
+      f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv[tb].y));
+    } else {
+      f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv[tb].x));
+      f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv[tb].y));
+    }
+    *reinterpret_cast<float4*>(scr + tb * 128 + 4 * lane) =
+        make_float4(f01.x * sv.x, f01.y * sv.y, f23.x * sv.z, f23.y * sv.w);
+  }
+  __syncwarp();
+}
+
+// a5 for TB tokens in lockstep: rotations t = 1..L, each pair from the pre-update values
+// (Eq. 4 / Eq. 5); lane l updates the pairs of slots l and l + 32
+template <int TB>
+__device__ __forceinline__ void g1_rot(float* scr, const float4 (&cs)[8], const uint32_t (&ix)[8], int L) {
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    if (t >= L) break;
+    const uint32_t i0 = ix[t] & 0xff, j0 = (ix[t] >> 8) & 0xff, i1 = (ix[t] >> 16) & 0xff, j1 = ix[t] >> 24;
+#pragma unroll
+    for (int tb = 0; tb < TB; ++tb) {
+      float* sc = scr + tb * 128;
+      const float a0 = sc[i0], b0v = sc[j0], a1 = sc[i1], b1v = sc[j1];
+      sc[i0] = cs[t].x * a0 - cs[t].y * b0v;
+      sc[j0] = cs[t].y * a0 + cs[t].x * b0v;
+      sc[i1] = cs[t].z * a1 - cs[t].w * b1v;
+      sc[j1] = cs[t].w * a1 + cs[t].z * b1v;
+    }
+    __syncwarp();
+  }
+}
+
+// rotation records [group][layer][32 lanes]: (cos, sin) of slots lane, lane + 32 and their
+// (i, j) channel pairs (pack-time bank-conflict-free schedule), and s of the lane's 4 channels
+__device__ __forceinline__ void g1_params(const Gemv1Linear& d, int gam, int L, int rotate, int lane, float4 (&cs)[8],
+                                          uint32_t (&ix)[8], float4& sv) {
+  const int64_t rec = static_cast<int64_t>(gam) * L * 32 + lane;
+#pragma unroll
+  for (int t = 0; t < 8; ++t)
+    if (t < L) {
+      cs[t] = __ldg(reinterpret_cast<const float4*>(d.rot_cs) + rec + t * 32);
+      ix[t] = __ldg(reinterpret_cast<const uint32_t*>(d.rot_idx) + rec + t * 32);
+    }
+  sv = rotate ? __ldg(reinterpret_cast<const float4*>(d.svec + gam * 128) + lane) : make_float4(1.f, 1.f, 1.f, 1.f);
+}
+
+// x of token b, channels 4 lane .. 4 lane + 3 of group gam (L2-coherent load: x may have been
+// written earlier in this launch by another SM)
+__device__ __forceinline__ uint2 g1_ldx(const void* x, int64_t K, int b, int gam, int lane) {
+  return __ldcg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(x) +
+                                               (static_cast<int64_t>(b) * K + gam * 128 + 4 * lane) * 2));
+}
+
+// B > 1: x' of one (group, token) as fixed point + s8 digits in the UMMA B-operand layout of the
+// group: rows n = 2 b (hi digit of token b) and 2 b + 1 (lo digit), 128 K-bytes each, K-major
+// with the 128-byte swizzle (16-byte chunk c of row n at chunk c ^ (n % 8); 8-row groups 1024 B
+// apart).  K index k < 64: byte k % 4 of the LOW-nibble word k / 4 of a tile row (channel
+// tile_k(t, j, 2 bb) for word 4 t + j); k >= 64: the HIGH nibbles of word (k - 64) / 4.  The
+// A operand (the masked code words, csrc/gemv1.cu phase 2) uses the same K order.
+__device__ __forceinline__ int2 g1_digits_umma(float* sc, int lane, uint8_t* grp, int b) {
+  int* fx = reinterpret_cast<int*>(sc);
+  const float4 v = *reinterpret_cast<const float4*>(sc + 4 * lane);
+  const float ml = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+  const uint32_t mb = __reduce_max_sync(0xffffffffu, __float_as_uint(ml));
+  int E = mb < 0x00800000u ? -100 : static_cast<int>(mb >> 23) - 127 + ((mb & 0x7fffffu) != 0u ? 1 : 0);
+  E = max(E, -100);
+  const float mul = __uint_as_float(static_cast<uint32_t>(141 - E) << 23);  // 2^(14 - E)
+  const int f0 = __float2int_rn(v.x * mul), f1 = __float2int_rn(v.y * mul);
+  const int f2 = __float2int_rn(v.z * mul), f3 = __float2int_rn(v.w * mul);
+  const int X = __reduce_add_sync(0xffffffffu, (f0 + f1) + (f2 + f3));
+  __syncwarp();
+  *reinterpret_cast<int4*>(fx + 4 * lane) = make_int4(f0, f1, f2, f3);
+  __syncwarp();
+  const int w = lane & 15, t = w >> 2, j = w & 3, p = lane >> 4;
+  uint32_t whi = 0, wlo = 0;
+#pragma unroll
+  for (int bb = 0; bb < 4; ++bb) {
+    const int c = 32 * j + 16 * p + 2 * t + (bb >> 1) + 8 * (bb & 1);  // tile_k(t, j, 2 bb + p)
+    const int f = fx[c];
+    const int lo = static_cast<int>(static_cast<int8_t>(f & 0xff));
+    whi |= (static_cast<uint32_t>((f - lo) >> 8) & 0xffu) << (8 * bb);
+    wlo |= (static_cast<uint32_t>(lo) & 0xffu) << (8 * bb);
+  }
+  const int nh = 2 * b, nl = 2 * b + 1;
+  *reinterpret_cast<uint32_t*>(grp + (nh >> 3) * 1024 + (nh & 7) * 128 + (((lane >> 2) ^ (nh & 7)) << 4) +
+                               4 * (lane & 3)) = whi;
+  *reinterpret_cast<uint32_t*>(grp + (nl >> 3) * 1024 + (nl & 7) * 128 + (((lane >> 2) ^ (nl & 7)) << 4) +
+                               4 * (lane & 3)) = wlo;
+  return make_int2(X, static_cast<int>(static_cast<uint32_t>(113 + E) << 23));  // 2^(E - 14)
+}
+
+// B > 1: one transform task = (linear, group, set of four tokens) -> digits + (sum, scale) in the
+// linear's xq / xqs buffers (the layout the GEMV bulk-copies)
+template <int BT>
+__device__ __forceinline__ void g1_xform_task(const Gemv1Stage& S, int task, int B, int x_bf16, int rotate, float* scr,
+                                              int lane, bool wait_pdl) {
+  constexpr int NB = BT / 4, XPG = 2 * BT * 128;  // UMMA B tile of a group: 2 BT rows x 128 B
+  const int G = S.G;
+  const int li = task / (G * NB), rem = task - li * G * NB, gam = rem / NB, set = rem - gam * NB;
+  const Gemv1Linear& d = S.lin[li];
+  const int L = rotate ? d.L : 0;
+  float4 cs[8], sv;
+  uint32_t ix[8];
+  g1_params(d, gam, L, rotate, lane, cs, ix, sv);
+  if (wait_pdl) pdl_wait();  // x may be written by the previous kernel on the stream
+  const int b0 = set * 4;
+  uint2 xv[4];
+#pragma unroll
+  for (int tb = 0; tb < 4; ++tb) xv[tb] = (b0 + tb < B) ? g1_ldx(S.x, S.K, b0 + tb, gam, lane) : make_uint2(0u, 0u);
+  g1_scale<4>(scr, xv, x_bf16, sv, lane);
+  g1_rot<4>(scr, cs, ix, L);
+  uint8_t* xq = d.xq + static_cast<size_t>(gam) * XPG;
+#pragma unroll
+  for (int tb = 0; tb < 4; ++tb) {
+    const int2 r = g1_digits_umma(scr + tb * 128, lane, xq, b0 + tb);
+    if (lane == 0) d.xqs[static_cast<size_t>(gam) * BT + b0 + tb] = r;
+  }
+}
+
 }  // namespace
 
 // NW compute warps + 1 producer warp (17 warps: up to 96 registers per thread).
-// BT: token capacity of the instance (1, 4, 8, 16).  Tokens are transformed four at a time in
-// lockstep and occupy the MMA's 8 columns in sets of four (columns 2b, 2b+1 = hi, lo digit of
-// token b of the set).  BT = 1 sums row partials per warp in a fixed order (deterministic);
-// BT > 1 adds them with shared-memory atomics.
-template <int NW, int BT>
-__global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv1Args a) {
-  constexpr int TB = BT == 1 ? 1 : 4;          // tokens per transform chunk / MMA column set
+// BT: token capacity of the instance (1, 4, 8, 16).  MS: stage capacity of the argument block.
+template <int NW, int BT, int MS>
+__global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __grid_constant__ Gemv1ArgsT<MS> a) {
+  constexpr int TB = BT == 1 ? 1 : 4;          // tokens per MMA column set
   constexpr int NB = (BT + 3) / 4;             // column sets
   constexpr int NCOL = BT == 1 ? 2 : 8;        // B columns holding digits
   constexpr int XTQ = NCOL * 32;               // digit bytes per (group, set, quad)
   constexpr int XPC = 4 * XTQ;                 // digit bytes per (group, column set)
   constexpr int XPG = NB * XPC;                // digit bytes per group
-  extern __shared__ __align__(1024) uint8_t smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int li = 0;
-#pragma unroll 1
-  while (li + 1 < a.n_lin && static_cast<int>(blockIdx.x) >= a.lin[li + 1].cta_begin) ++li;
-  const Gemv1Linear& d = a.lin[li];
+  (void)TB;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  // 1024-byte aligned base (the UMMA B tiles use the 128-byte swizzle); the plan reserves the slack
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int CL = static_cast<int>(cluster_nctarank());
   const int crank = static_cast<int>(cluster_ctarank());
-  const int G = a.G, B = a.B;
-  const int cl = (static_cast<int>(blockIdx.x) - d.cta_begin) / CL;
-  const int nrb = d.rb_base + (cl < d.rb_extra ? 1 : 0);
-  const int rb0 = cl * d.rb_base + min(cl, d.rb_extra);
-  const int R = nrb * TILE_ROWS;
-  const int ga = crank * G / CL, gb = (crank + 1) * G / CL, gc = gb - ga;
-  // stages: TPS consecutive tiles of the CTA's tile sequence u = rb * gc + (gamma - ga)
-  // (row block by row block, my groups within each; a stage may start or end inside a row block)
-  const int n_tiles = nrb * gc;
-  const int n_stages = (n_tiles + a.TPS - 1) / a.TPS;
+  const int B = a.B;
 
   uint8_t* xp = smem + a.off_xp;                                 // x' digits [gc][NB][4 t][NCOL][4 kb][8 B]
   int2* xs = reinterpret_cast<int2*>(smem + a.off_xs);           // per (group, token): (sum x'fix, 2^(E-14))
-  const uint8_t* zblk = smem + a.off_xs + ((gc * BT * 8 + 15) & ~15);  // 32 zero bytes (B columns >= 2)
+  const uint8_t* zblk = smem + a.off_xs - 32;                    // 32 zero bytes (B columns >= 2)
   float* part = reinterpret_cast<float*>(smem + a.off_part);     // BT = 1: [NW][R_max]; else [R_max][BT]
   float* recv = reinterpret_cast<float*>(smem + a.off_recv);     // [CL][RRmax][BT] cluster partials
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.off_bar);
   uint64_t* empty = full + a.S;
-  uint64_t* rbar = empty + a.S;  // cluster partials of my rows landed (st.async bytes)
+  uint64_t* rbar = empty + a.S;  // cluster partials of my rows landed (st.async bytes), one phase per stage
   uint64_t* xbar = rbar + 1;     // BT > 1: the pre-transformed x' slice landed
-  const int RR = (R + CL - 1) / CL;  // rows per owner CTA
-  const int my_lo = crank * RR, my_n = max(0, min(RR, R - my_lo));
+  uint64_t* mdone = xbar + 1;    // BT > 1: [4] the warpgroup's MMAs completed (tcgen05.commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mdone + 4);  // BT > 1: TMEM base address
   uint8_t* ring = smem + a.off_ring;
+  // this CTA's share of every stage (read from shared memory where used: keeps registers free)
+  __shared__ G1Geom sgeo[MS];
+  if (tid < a.n_stages) sgeo[tid] = g1_geom(a.st[tid], CL, crank, a.TPS, BT > 1);
 
-  if (threadIdx.x < 8) reinterpret_cast<uint32_t*>(smem + a.off_xs + ((gc * BT * 8 + 15) & ~15))[threadIdx.x] = 0u;
-  if (threadIdx.x == 0) {
-    g1_mark(0);
+  if (tid < 8) reinterpret_cast<uint32_t*>(smem + a.off_xs - 32)[tid] = 0u;
+  if (tid == 0) {
     for (int i = 0; i < a.S; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], NW);
     }
     mbar_init(rbar, 1);
     mbar_init(xbar, 1);
-    if (CL > 1) mbar_arrive_expect_tx(rbar, static_cast<uint32_t>((CL - 1) * my_n * BT * 4));
+    for (int i = 0; i < 4; ++i) mbar_init(&mdone[i], 1);
+    if (CL > 1) mbar_arrive_expect_tx(rbar, static_cast<uint32_t>((CL - 1) * g1_geom(a.st[0], CL, crank, a.TPS, BT > 1).my_n * BT * 4));
     fence_mbar_init();
   }
+  if (BT > 1 && warp == 0) tmem_alloc(tmem_slot, 512);  // 4 warpgroups x (A 32 + D 2 BT columns), whole TMEM
+  tc_fence_before();
   __syncthreads();
-  // BT > 1: the cluster barrier arrive of the compute warps comes after phase 1, because the
-  // transform scratch shares its shared memory with recv, which other CTAs write once the
-  // barrier completes
-  if (CL > 1 && (BT == 1 || warp == NW)) cluster_arrive_relaxed();
+  tc_fence_after();
+  if (CL > 1) cluster_arrive_relaxed();  // every CTA's mbarriers are initialised (DSMEM legal after the wait)
   if (a.pdl) pdl_launch_dependents();
 
-  // ------------------------------------------------------------ producer warp: the whole ring
+  // ------------------------------------------------------------ producer warp: the whole ring, every stage
   if (warp == NW) {
     const uint64_t pol = l2_evict_first_policy();
-    const int pre = min(a.pre_stages, n_stages);
-    auto issue_xq = [&]() {  // BT > 1: x' digits of my groups, written by the preceding xform kernel
-      if (a.pdl) pdl_wait();
-      if (lane == 0) {
-        const uint32_t nd = static_cast<uint32_t>(gc * XPG), ns = static_cast<uint32_t>(gc * BT * 8);
-        mbar_arrive_expect_tx(xbar, nd + ns);
-        bulk_g2s_nohint(xp, d.xq + static_cast<size_t>(ga) * XPG, nd, xbar);
-        bulk_g2s_nohint(xs, d.xqs + static_cast<size_t>(ga) * BT, ns, xbar);
+    const int pre = a.pre_stages;
+    bool released = false;
+    auto release = [&](const Gemv1Stage& S, const G1Geom& g) {
+      // stage 0, B > 1: x' digits of my groups, written by the preceding xform kernel
+      if (BT > 1 && g.active) {
+        if (a.pdl) pdl_wait();
+        if (lane == 0) {
+          const Gemv1Linear& d = S.lin[g.li];
+          const uint32_t nd = static_cast<uint32_t>(g.gc * XPG), ns = static_cast<uint32_t>(g.gc * BT * 8);
+          mbar_arrive_expect_tx(xbar, nd + ns);
+          bulk_g2s_nohint(xp, d.xq + static_cast<size_t>(g.ga) * XPG, nd, xbar);
+          bulk_g2s_nohint(xs, d.xqs + static_cast<size_t>(g.ga) * BT, ns, xbar);
+        }
+        __syncwarp();
       }
-      __syncwarp();
+      named_bar_sync(2, (NW + 1) * 32);  // the compute warps' x / parameter loads are out
+      released = true;
     };
     if (a.params_first) named_bar_sync(3, (NW + 1) * 32);  // the rotation-parameter loads are out
+    int slot = 0, phase = 0, nb = 0;
 #pragma unroll 1
-    for (int st = 0; st < n_stages; ++st) {
-      const int slot = st % a.S;
-      // the latency-critical x / rotation-parameter loads of the compute warps go out before
-      // the bulk of the weight stream (which would otherwise queue ahead of them)
-      if (st == pre) {
-        if (BT > 1) issue_xq();
-        named_bar_sync(2, (NW + 1) * 32);
-      }
-      if (st >= a.S) mbar_wait(&empty[slot], ((st / a.S) & 1) ^ 1);
-      if (lane == 0) {
-        const int u0 = st * a.TPS, u1 = min(n_tiles, u0 + a.TPS);
-        uint8_t* dst = ring + static_cast<size_t>(slot) * a.slot_bytes;
-        mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(u1 - u0) * TILE_B);
+    for (int s = 0; s < a.n_stages; ++s) {
+      const Gemv1Stage& S = a.st[s];
+      const G1Geom& g = sgeo[s];
+      const Gemv1Linear& d = S.lin[g.li];
+      const int G = S.G;
 #pragma unroll 1
-        for (int u = u0; u < u1;) {  // one contiguous segment per row block touched
-          const int rb = u / gc, ue = min(u1, (rb + 1) * gc);
-          const int64_t T = static_cast<int64_t>(rb0 + rb) * G + ga + (u - rb * gc);
-          const uint32_t i0 = static_cast<uint32_t>(u - u0), n = static_cast<uint32_t>(ue - u);
-          u = ue;
-          bulk_g2s(dst + i0 * TILE_CODE_BYTES, d.codes + T * TILE_CODE_BYTES, n * TILE_CODE_BYTES, &full[slot], pol);
-          bulk_g2s(dst + a.sc_off + i0 * TILE_SCALE_BYTES, d.scales + T * TILE_SCALE_BYTES, n * TILE_SCALE_BYTES,
-                   &full[slot], pol);
-          bulk_g2s(dst + a.z_off + i0 * TILE_ZERO_BYTES, d.zeros + T * TILE_ZERO_BYTES, n * TILE_ZERO_BYTES, &full[slot],
-                   pol);
+      for (int bt = 0; bt < g.n_batches; ++bt) {
+        if (s == 0 && bt == pre) release(S, g);
+        if (nb >= a.S) mbar_wait(&empty[slot], phase ^ 1);
+        if (lane == 0) {
+          uint8_t* dst = ring + static_cast<size_t>(slot) * a.slot_bytes;
+          if constexpr (BT == 1) {
+            const int u0 = bt * a.TPS, u1 = min(g.n_tiles, u0 + a.TPS);
+            mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(u1 - u0) * TILE_B);
+#pragma unroll 1
+            for (int u = u0; u < u1;) {  // one contiguous segment per row block touched
+              const int rb = u / g.gc, ue = min(u1, (rb + 1) * g.gc);
+              const int64_t T = static_cast<int64_t>(g.rb0 + rb) * G + g.ga + (u - rb * g.gc);
+              const uint32_t i0 = static_cast<uint32_t>(u - u0), n = static_cast<uint32_t>(ue - u);
+              u = ue;
+              bulk_g2s(dst + i0 * TILE_CODE_BYTES, d.codes + T * TILE_CODE_BYTES, n * TILE_CODE_BYTES, &full[slot],
+                       pol);
+              bulk_g2s(dst + a.sc_off + i0 * TILE_SCALE_BYTES, d.scales + T * TILE_SCALE_BYTES,
+                       n * TILE_SCALE_BYTES, &full[slot], pol);
+              bulk_g2s(dst + a.z_off + i0 * TILE_ZERO_BYTES, d.zeros + T * TILE_ZERO_BYTES, n * TILE_ZERO_BYTES,
+                       &full[slot], pol);
+            }
+          } else {
+            // (quad q, chunk c): one contiguous segment of mm tiles per row block 4 q + j
+            const int m = a.TPS / 4, q = bt / g.nch, c = bt - q * g.nch;
+            const int mm = min(m, g.gc - c * m), nq = min(4, g.nrb - 4 * q);
+            mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(nq * mm) * TILE_B);
+#pragma unroll 1
+            for (int j = 0; j < nq; ++j) {
+              const int64_t T = static_cast<int64_t>(g.rb0 + 4 * q + j) * G + g.ga + c * m;
+              const uint32_t i0 = static_cast<uint32_t>(j * mm), n = static_cast<uint32_t>(mm);
+              bulk_g2s(dst + i0 * TILE_CODE_BYTES, d.codes + T * TILE_CODE_BYTES, n * TILE_CODE_BYTES, &full[slot],
+                       pol);
+              bulk_g2s(dst + a.sc_off + i0 * TILE_SCALE_BYTES, d.scales + T * TILE_SCALE_BYTES,
+                       n * TILE_SCALE_BYTES, &full[slot], pol);
+              bulk_g2s(dst + a.z_off + i0 * TILE_ZERO_BYTES, d.zeros + T * TILE_ZERO_BYTES, n * TILE_ZERO_BYTES,
+                       &full[slot], pol);
+            }
+          }
+        }
+        __syncwarp();
+        ++nb;
+        if (++slot == a.S) {
+          slot = 0;
+          phase ^= 1;
         }
       }
-      __syncwarp();
+      if (s == 0 && !released) release(S, g);
     }
-    if (pre >= n_stages) {
-      if (BT > 1) issue_xq();
-      named_bar_sync(2, (NW + 1) * 32);
-    }
-    if (lane == 0) g1_mark(1);  // every stage issued
     if (CL > 1) cluster_wait();
     return;
   }
 
-  // ------------------------------------------------------------ phase 1: x' of my groups (a4, a5)
-  float* pw = part + static_cast<size_t>(warp) * a.R_max;
-  if (BT == 1 && !a.atom) {
-    for (int i = lane; i < R; i += 32) pw[i] = 0.f;
-  } else {
-    for (int i = threadIdx.x; i < R * BT; i += NW * 32) part[i] = 0.f;
-  }
-  if constexpr (BT > 1) {
-    // x' digits and (sum, scale) of my groups come from paro_gemv1_xform_kernel (one transform
-    // per (group, token) for the whole GPU instead of one per cluster): the producer bulk-copies
-    // the contiguous slice [ga, gb) after the PDL wait
-    if (a.params_first) named_bar_arrive(3, (NW + 1) * 32);
-    named_bar_arrive(2, (NW + 1) * 32);
-    if (a.pdl) pdl_wait();  // (y is written at the end)
-    mbar_wait(xbar, 0);
-  } else {
-    float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * (TB * 128);
-    const int L = a.rotate ? d.L : 0;
-    bool waited = false, arrived = false;
-    if (warp >= gc) {
-      if (a.params_first) named_bar_arrive(3, (NW + 1) * 32);
-      named_bar_arrive(2, (NW + 1) * 32);
-    } else if (lane == 0) {
-      // later rounds' rotation records -> L2 now, ahead of the weight stream (requested after
-      // the first round they would queue behind the whole ring)
-      for (int g = warp + NW; g < gc; g += NW) {
-        const int64_t rec = static_cast<int64_t>(ga + g) * L * 32;
-        if (L > 0) {
-          prefetch_l2_bulk(reinterpret_cast<const float4*>(d.rot_cs) + rec, static_cast<uint32_t>(L * 32 * 16));
-          prefetch_l2_bulk(reinterpret_cast<const uint32_t*>(d.rot_idx) + rec, static_cast<uint32_t>(L * 32 * 4));
-        }
-        if (a.rotate) prefetch_l2_bulk(d.svec + (ga + g) * 128, 512u);
+  // ------------------------------------------------------------ compute warps
+  int slot = 0, phase = 0, xuse = 0;
+  uint32_t gen = 0;  // thread 0: generation of the last grid barrier it arrived at
+  // all compute warps wait until every CTA has passed the last grid barrier (thread 0 polls)
+  auto wait_grid = [&]() {
+    if (warp == 0) {
+      if (lane == 0) {
+        grid_wait(a.gbar, gen);
+        __threadfence();
+      }
+      __syncwarp();
+    }
+    named_bar_sync(4, NW * 32);
+  };
+#pragma unroll 1
+  for (int s = 0; s < a.n_stages; ++s) {
+    const Gemv1Stage& S = a.st[s];
+    const G1Geom& g = sgeo[s];
+    const Gemv1Linear& d = S.lin[g.li];
+    const int ga = g.ga, gc = g.gc;
+    float* pw = part + static_cast<size_t>(warp) * S.R_max;
+    if (g.active) {
+      if (BT == 1 && !S.atom) {
+        for (int i = lane; i < g.R; i += 32) pw[i] = 0.f;
+      } else {
+        for (int i = tid; i < g.R * BT; i += NW * 32) part[i] = 0.f;
       }
     }
+
+    // ---------------------------------------------------------- phase 1: x' of my groups (a4, a5)
+    if constexpr (BT > 1) {
+      if (s == 0) {
+        if (a.params_first) named_bar_arrive(3, (NW + 1) * 32);
+        named_bar_arrive(2, (NW + 1) * 32);
+        if (a.pdl) pdl_wait();
+      } else {
+        wait_grid();
+        if (S.xq_in_kernel) {
+          // this stage's x is an earlier stage's y: transform tasks over every warp of the grid,
+          // then one more grid barrier before the slices are copied
+          float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * (4 * 128);
+          const int n_tasks = S.n_lin * S.G * NB;
 #pragma unroll 1
-    for (int g = warp; g < gc; g += NW) {
-      const int gam = ga + g;
-      // rotation records [group][layer][32 lanes]: (cos, sin) of slots lane, lane + 32 and
-      // their (i, j) channel pairs (pack-time bank-conflict-free schedule)
-      float4 cs[8];
+          for (int task = static_cast<int>(blockIdx.x) * NW + warp; task < n_tasks;
+               task += static_cast<int>(gridDim.x) * NW)
+            g1_xform_task<BT>(S, task, B, a.x_bf16, a.rotate, scr, lane, false);
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> bulk-copy reads
+          named_bar_sync(1, NW * 32);
+          if (tid == 0) gen = grid_arrive(a.gbar, gridDim.x);
+          wait_grid();
+        }
+        if (g.active && tid == 0) {
+          const uint32_t nd = static_cast<uint32_t>(gc * XPG), ns = static_cast<uint32_t>(gc * BT * 8);
+          mbar_arrive_expect_tx(xbar, nd + ns);
+          bulk_g2s_nohint(xp, d.xq + static_cast<size_t>(ga) * XPG, nd, xbar);
+          bulk_g2s_nohint(xs, d.xqs + static_cast<size_t>(ga) * BT, ns, xbar);
+        }
+      }
+      if (g.active) {
+        mbar_wait(xbar, xuse & 1);
+        ++xuse;
+      }
+    } else {
+      float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * 128;
+      const int L = a.rotate ? d.L : 0;
+      const bool mine = g.active && warp < gc;
+      float4 cs[8], sv = make_float4(1.f, 1.f, 1.f, 1.f);
       uint32_t ix[8];
-      const int64_t rec = static_cast<int64_t>(gam) * L * 32 + lane;
-#pragma unroll
-      for (int t = 0; t < 8; ++t)
-        if (t < L) {
-          cs[t] = __ldg(reinterpret_cast<const float4*>(d.rot_cs) + rec + t * 32);
-          ix[t] = __ldg(reinterpret_cast<const uint32_t*>(d.rot_idx) + rec + t * 32);
-        }
-      const float4 sv =
-          a.rotate ? __ldg(reinterpret_cast<const float4*>(d.svec + gam * 128) + lane) : make_float4(1.f, 1.f, 1.f, 1.f);
-      if (!waited && a.params_first) {
-        __syncwarp();
-        named_bar_arrive(3, (NW + 1) * 32);
-      }
-      if (!waited) {
-        if (a.pdl) pdl_wait();  // x may be written by the previous kernel on the stream
-        waited = true;
-      }
-#pragma unroll 1
-      for (int b0 = 0; b0 < B; b0 += TB) {  // token chunks, TB tokens in lockstep
-        uint2 xv[TB];
-#pragma unroll
-        for (int tb = 0; tb < TB; ++tb)
-          xv[tb] = (b0 + tb < B) ? __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(a.x) +
-                                                                       (static_cast<int64_t>(b0 + tb) * a.K +
-                                                                        gam * 128 + 4 * lane) * 2))
-                                 : make_uint2(0u, 0u);  // tokens >= B: x = 0, never stored
-#pragma unroll
-        for (int tb = 0; tb < TB; ++tb) {
-          float2 f01, f23;
-          if (a.x_bf16) {
-            f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv[tb].x));
-            f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv[tb].y));
-          } else {
-            f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv[tb].x));
-            f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv[tb].y));
+      if (mine) {
+        g1_params(d, ga + warp, L, a.rotate, lane, cs, ix, sv);
+        if (lane == 0) {
+          // later rounds' rotation records -> L2 now, ahead of the weight stream
+          for (int gg = warp + NW; gg < gc; gg += NW) {
+            const int64_t rec = static_cast<int64_t>(ga + gg) * L * 32;
+            if (L > 0) {
+              prefetch_l2_bulk(reinterpret_cast<const float4*>(d.rot_cs) + rec, static_cast<uint32_t>(L * 32 * 16));
+              prefetch_l2_bulk(reinterpret_cast<const uint32_t*>(d.rot_idx) + rec, static_cast<uint32_t>(L * 32 * 4));
+            }
+            if (a.rotate) prefetch_l2_bulk(d.svec + (ga + gg) * 128, 512u);
           }
-          // a4: u = s . x
-          *reinterpret_cast<float4*>(scr + tb * 128 + 4 * lane) =
-              make_float4(f01.x * sv.x, f01.y * sv.y, f23.x * sv.z, f23.y * sv.w);
         }
-        if (!arrived) {
+      }
+      // x dependency: the previous kernel on the stream (stage 0) or the previous stage (grid barrier)
+      if (s == 0) {
+        if (a.params_first) {
           __syncwarp();
+          named_bar_arrive(3, (NW + 1) * 32);
+        }
+        if (a.pdl) pdl_wait();
+      } else {
+        wait_grid();
+      }
+      bool arrived = s != 0;
+#pragma unroll 1
+      for (int gg = warp; mine && gg < gc; gg += NW) {
+        const int gam = ga + gg;
+        if (gg != warp) g1_params(d, gam, L, a.rotate, lane, cs, ix, sv);
+        uint2 xv[1] = {g1_ldx(S.x, S.K, 0, gam, lane)};
+        g1_scale<1>(scr, xv, a.x_bf16, sv, lane);
+        if (!arrived) {
           named_bar_arrive(2, (NW + 1) * 32);  // my x and parameters are in
-          if (threadIdx.x == 0) g1_mark(2);
           arrived = true;
         }
-        __syncwarp();
-        // a5: rotations t = 1..L, each pair from the pre-update values (Eq. 4 / Eq. 5)
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          if (t >= L) break;
-          const uint32_t i0 = ix[t] & 0xff, j0 = (ix[t] >> 8) & 0xff, i1 = (ix[t] >> 16) & 0xff, j1 = ix[t] >> 24;
-#pragma unroll
-          for (int tb = 0; tb < TB; ++tb) {
-            float* sc = scr + tb * 128;
-            const float a0 = sc[i0], b0v = sc[j0], a1 = sc[i1], b1v = sc[j1];
-            sc[i0] = cs[t].x * a0 - cs[t].y * b0v;
-            sc[j0] = cs[t].y * a0 + cs[t].x * b0v;
-            sc[i1] = cs[t].z * a1 - cs[t].w * b1v;
-            sc[j1] = cs[t].w * a1 + cs[t].z * b1v;
-          }
-          __syncwarp();
-          if (G1_TL && t == 0 && threadIdx.x == 0 && g == warp && b0 == 0) g1_mark(8);
-        }
-        if (G1_TL && threadIdx.x == 0 && g == warp && b0 == 0) g1_mark(9);
-        // x' -> per-(group, token) fixed point and s8 digits (see the header), laid out as B
-        // fragments [column set][quad t][column][k-block kb][b0, b1]; column 2 b + dg of a set =
-        // digit dg (0 hi, 1 lo) of its token b; k-block kb = 2 p + h covers the low (p = 0) or
-        // high (p = 1) nibbles of words 2h, 2h + 1 (b0: word 2h, b1: word 2h + 1); byte bb of the
-        // word for quad t, word j, parity p is channel tile_k(t, j, 2 bb + p)
-#pragma unroll
-        for (int tb = 0; tb < TB; ++tb) {
-          int* fx = reinterpret_cast<int*>(scr + tb * 128);
-          const float4 v = *reinterpret_cast<const float4*>(scr + tb * 128 + 4 * lane);
-          const float ml = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
-          const uint32_t mb = __reduce_max_sync(0xffffffffu, __float_as_uint(ml));  // |x| bits order like |x|
-          int E = mb < 0x00800000u ? -100 : static_cast<int>(mb >> 23) - 127 + ((mb & 0x7fffffu) != 0u ? 1 : 0);
-          E = max(E, -100);
-          const float mul = __uint_as_float(static_cast<uint32_t>(141 - E) << 23);  // 2^(14 - E)
-          const int f0 = __float2int_rn(v.x * mul), f1 = __float2int_rn(v.y * mul);
-          const int f2 = __float2int_rn(v.z * mul), f3 = __float2int_rn(v.w * mul);
-          const int X = __reduce_add_sync(0xffffffffu, (f0 + f1) + (f2 + f3));
-          __syncwarp();  // every lane has read its x' before the scratch holds x'fix
-          *reinterpret_cast<int4*>(fx + 4 * lane) = make_int4(f0, f1, f2, f3);
-          __syncwarp();
-          const int tq = lane >> 3, col = (lane >> 2) & 1, kb = lane & 3, p = kb >> 1, h = kb & 1;
-          uint32_t wd[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int j = 2 * h + e;
-            uint32_t wv = 0;
-#pragma unroll
-            for (int bb = 0; bb < 4; ++bb) {
-              const int c = 16 * (2 * j + p) + 2 * tq + (bb >> 1) + 8 * (bb & 1);  // tile_k(tq, j, 2 bb + p)
-              const int f = fx[c];
-              const int lo = static_cast<int>(static_cast<int8_t>(f & 0xff));
-              const int dg = col ? lo : ((f - lo) >> 8);
-              wv |= (static_cast<uint32_t>(dg) & 0xffu) << (8 * bb);
-            }
-            wd[e] = wv;
-          }
-          const int b = b0 + tb, set = b >> 2, cb = b & 3;
-          *reinterpret_cast<uint2*>(xp + g * XPG + set * XPC + tq * XTQ + (2 * cb + col) * 32 + kb * 8) =
-              make_uint2(wd[0], wd[1]);
-          if (lane == 0)
-            xs[g * BT + b] = make_int2(X, static_cast<int>(static_cast<uint32_t>(113 + E) << 23));  // 2^(E - 14)
-        }
+        g1_rot<1>(scr, cs, ix, L);
+        const int2 r = g1_digits<NCOL>(scr, lane, xp + gg * XPG, 0);
+        if (lane == 0) xs[gg] = r;
         __syncwarp();
       }
+      if (!arrived) named_bar_arrive(2, (NW + 1) * 32);
     }
-  }
-  named_bar_sync(1, NW * 32);  // every x' of the CTA is in shared memory (and BT > 1: part zeroed)
-  if (BT > 1 && CL > 1) cluster_arrive();  // my scratch is free: the cluster may now write recv
-  if (threadIdx.x == 0) g1_mark(3);
+    named_bar_sync(1, NW * 32);  // every x' of the CTA is in shared memory (and part zeroed)
 
-  // ------------------------------------------------------------ phase 2: tiles (a6)
-  {
-    const int gq = lane >> 2, tq = lane & 3;
+    // ---------------------------------------------------------- phase 2: tiles (a6)
+    if constexpr (BT == 1) {
+      const int gq = lane >> 2, tq = lane & 3;
+      const bool atom = S.atom != 0;
+      // batch bookkeeping advanced incrementally (no divisions in the loop): first tile of the
+      // batch u0 = bt * TPS = r_lo * gc + off0
+      int r_lo = 0, off0 = 0;
 #pragma unroll 1
-    const bool atom = a.atom != 0;
-    // stage bookkeeping advanced incrementally (no divisions in the loop): ring slot and phase,
-    // first tile u0 = st * TPS = r_lo * gc + off0
-    int slot = 0, phase = 0, r_lo = 0, off0 = 0;
-    for (int st = 0; st < n_stages; ++st) {
-      // stage tiles [u0, u1): tile i of the stage is (row block r_lo + ri, group ga + gi) with
-      // (ri, gi) = divmod(off0 + i, gc)
-      const int u0 = st * a.TPS, nt = min(n_tiles, u0 + a.TPS) - u0;
-      const int g_lo = ga, pl = gc;
-      mbar_wait(&full[slot], phase);
-      if (threadIdx.x == 0 && st == 0) g1_mark(4);
-      const uint8_t* sb = ring + static_cast<size_t>(slot) * a.slot_bytes;
-      if (a.skip_math) {  // debug (PARO_G1_SKIP): stream the weights, no tile math
-      } else if constexpr (BT == 1) {
-      int ri = 0, gi = off0 + warp;  // tile warp + k NW of the stage
-      while (gi >= pl) {
-        gi -= pl;
-        ++ri;
-      }
+      for (int bt = 0; bt < g.n_batches; ++bt) {
+        // batch tiles [u0, u1): tile i is (row block r_lo + ri, group ga + gi) with (ri, gi) = divmod(off0 + i, gc)
+        const int u0 = bt * a.TPS, nt = min(g.n_tiles, u0 + a.TPS) - u0;
+        mbar_wait(&full[slot], phase);
+        const uint8_t* sb = ring + static_cast<size_t>(slot) * a.slot_bytes;
+        int ri = 0, gi = off0 + warp;  // tile warp + k NW of the batch
+        while (gi >= gc) {
+          gi -= gc;
+          ++ri;
+        }
 #pragma unroll 1
-      for (int i = warp; i < nt; i += NW) {
-        const int gl = g_lo - ga + gi;
-        const uint8_t* tc = sb + i * TILE_CODE_BYTES + gq * 64 + tq * 16;
-        uint4 w[4];
+        for (int i = warp; i < nt; i += NW) {
+          const uint8_t* tc = sb + i * TILE_CODE_BYTES + gq * 64 + tq * 16;
+          uint4 w[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) w[q] = *reinterpret_cast<const uint4*>(tc + q * 512);
-        const uint2 sp = *reinterpret_cast<const uint2*>(sb + a.sc_off + i * TILE_SCALE_BYTES + gq * 8);
-        const uint32_t zw = *reinterpret_cast<const uint16_t*>(sb + a.z_off + i * TILE_ZERO_BYTES + gq * 2);
-        const float2 Sa = __half22float2(*reinterpret_cast<const __half2*>(&sp.x));  // rows gq, gq + 8
-        const float2 Sb = __half22float2(*reinterpret_cast<const __half2*>(&sp.y));  // rows gq + 16, gq + 24
-        const float Sr[4] = {Sa.x, Sa.y, Sb.x, Sb.y};
-        const int rowl = (r_lo + ri) * TILE_ROWS + gq;  // cluster-local row of q = 0
-#pragma unroll
-        for (int set = 0; set < NB; ++set) {
-          if (set * 4 >= B) break;
+          for (int q = 0; q < 4; ++q) w[q] = *reinterpret_cast<const uint4*>(tc + q * 512);
+          const uint2 sp = *reinterpret_cast<const uint2*>(sb + a.sc_off + i * TILE_SCALE_BYTES + gq * 8);
+          const uint32_t zw = *reinterpret_cast<const uint16_t*>(sb + a.z_off + i * TILE_ZERO_BYTES + gq * 2);
+          const float2 Sa = __half22float2(*reinterpret_cast<const __half2*>(&sp.x));  // rows gq, gq + 8
+          const float2 Sb = __half22float2(*reinterpret_cast<const __half2*>(&sp.y));  // rows gq + 16, gq + 24
+          const float Sr[4] = {Sa.x, Sa.y, Sb.x, Sb.y};
+          const int rowl = (r_lo + ri) * TILE_ROWS + gq;  // cluster-local row of q = 0
           // B fragments: lanes of MMA columns >= 2 read a 32-byte zero block (address select, no branch)
-          const uint8_t* bp = gq < 2 ? xp + gl * XPG + set * XPC + tq * XTQ + gq * 32 : zblk;
+          const uint8_t* bp = gq < 2 ? xp + gi * XPG + tq * XTQ + gq * 32 : zblk;
           const uint4 bA = *reinterpret_cast<const uint4*>(bp);
           const uint4 bB = *reinterpret_cast<const uint4*>(bp + 16);
           constexpr uint32_t ML = 0x0f0f0f0fu, MH = 0xf0f0f0f0u;
@@ -411,11 +575,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
             mma_u8s8(Dh[hh], r0.x & MH, r1.x & MH, r0.y & MH, r1.y & MH, bB.x, bB.y);  // high nibbles (16 q)
             mma_u8s8(Dh[hh], r0.z & MH, r1.z & MH, r0.w & MH, r1.w & MH, bB.z, bB.w);
           }
-          // lane (gq, tq) holds columns 2 tq (hi digit) and 2 tq + 1 (lo digit) = token tq of the
-          // set, rows gq + 8 q
-          const int b = set * 4 + tq;
-          if (BT == 1 ? tq == 0 : b < B) {
-            const int2 xf = xs[gl * BT + b];
+          // lane (gq, tq) holds columns 2 tq (hi digit) and 2 tq + 1 (lo digit); column pair 0 = the token
+          if (tq == 0) {
+            const int2 xf = xs[gi];
             const float F = __int_as_float(xf.y);
             float out[4];
 #pragma unroll
@@ -425,275 +587,234 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const Gemv
               const int I = Dl[hh][e] * 256 + Dl[hh][e + 1] + ((Dh[hh][e] * 256 + Dh[hh][e + 1]) >> 4) - zq * xf.x;
               out[q] = Sr[q] * F * static_cast<float>(I);
             }
-            if (BT == 1 && !atom) {  // one uniform branch per tile, not per row
+            if (!atom) {  // one uniform branch per tile, not per row
 #pragma unroll
               for (int q = 0; q < 4; ++q) pw[rowl + 8 * q] += out[q];
             } else {
 #pragma unroll
-              for (int q = 0; q < 4; ++q) atomicAdd(part + (rowl + 8 * q) * BT + b, out[q]);
+              for (int q = 0; q < 4; ++q) atomicAdd(part + rowl + 8 * q, out[q]);
             }
           }
+          gi += NW;
+          while (gi >= gc) {
+            gi -= gc;
+            ++ri;
+          }
         }
-        gi += NW;
-        while (gi >= pl) {
-          gi -= pl;
-          ++ri;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (++slot == a.S) {
+          slot = 0;
+          phase ^= 1;
+        }
+        off0 += a.TPS;
+        while (off0 >= gc) {
+          off0 -= gc;
+          ++r_lo;
         }
       }
-      } else {
-      // B > 1: warp w takes a contiguous chunk of the stage's tiles (row block ri, group gi), so
-      // that its consecutive tiles mostly share a row block and the row partials (atomics) go to
-      // shared memory once per row block; B = 1: tiles w, w + NW, ... (measured faster)
-      const int per = (nt + NW - 1) / NW;
-      const int step = BT == 1 ? NW : 1;
-      const int i_end = BT == 1 ? nt : min(nt, (warp + 1) * per);
-      int i = BT == 1 ? warp : warp * per;
-      int ri = (off0 + i) / pl, gi = off0 + i - ri * pl;
-      float acc[NB][4];
-      int acc_ri = -1;
-      auto flush = [&]() {
-        if (acc_ri < 0) return;
-        const int rowl = (r_lo + acc_ri) * TILE_ROWS + gq;  // cluster-local row of q = 0
+    } else {
+      // B > 1: 5th-generation tensor cores.  Warpgroup wg (warps 4 wg .. 4 wg + 3) takes the
+      // groups gi = wg, wg + 4, .. of each batch; per group, its warp j writes the A operand of
+      // row block 4 q + j into TMEM lanes 32 j .. 32 j + 31 (one row per lane: the row's 16 code
+      // words, low nibbles AND 0x0F0F0F0F and high nibbles >> 4 AND 0x0F0F0F0F = the u8 codes of
+      // 128 channels, no conversion), one thread issues four tcgen05.mma.kind::i8 (M = 128 rows,
+      // N = 2 B token digits, K = 32 each; u8 codes x s8 digits -> exact s32 in TMEM), and every
+      // lane reads its row back: I = 256 D_hi + D_lo - z X per token, y_row += S 2^(E-14) I in
+      // registers across the CTA's groups; one shared-memory atomic per (row, token) per quad.
+      constexpr int NC = 2 * BT;  // MMA N: (token, digit) columns
+      constexpr uint32_t IDESC = (2u << 4)                                    // D: s32
+                                 | (0u << 7) | (1u << 10)                     // A: u8, B: s8
+                                 | (static_cast<uint32_t>(NC >> 3) << 17)     // N >> 3
+                                 | (static_cast<uint32_t>(128 >> 4) << 24);   // M >> 4
+      const int wg = warp >> 2, wq = warp & 3;
+      const uint32_t tbase = *tmem_slot + static_cast<uint32_t>(wg * 128);  // this warpgroup's columns
+      const uint32_t tA = tbase, tD = tbase + 32, lane_off = static_cast<uint32_t>(wq * 32) << 16;
+      const int m = a.TPS / 4;
+      const int swz = (lane >> 1) & 3;  // conflict-free row reads: chunk k ^ swz at step k
+      float acc[BT];
 #pragma unroll
-        for (int set = 0; set < NB; ++set) {
-          const int b = set * 4 + tq;
-          if (BT == 1 ? tq == 0 : b < B) {
+      for (int b = 0; b < BT; ++b) acc[b] = 0.f;
+      int cur_q = -1, mph = 0;
+      auto flush = [&](int q) {
+        const int nq = min(4, g.nrb - 4 * q);
+        if (wq < nq) {
+          const int row = (4 * q + wq) * TILE_ROWS + lane;  // cluster-local row
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              if (BT == 1)
-                pw[rowl + 8 * q] += acc[set][q];
-              else
-                atomicAdd(part + (rowl + 8 * q) * BT + b, acc[set][q]);
-            }
-          }
+          for (int b = 0; b < BT; ++b)
+            if (b < B) atomicAdd(part + row * BT + b, acc[b]);
         }
+#pragma unroll
+        for (int b = 0; b < BT; ++b) acc[b] = 0.f;
       };
 #pragma unroll 1
-      for (; i < i_end; i += step) {
-        if (ri != acc_ri) {
-          flush();
-          acc_ri = ri;
-#pragma unroll
-          for (int set = 0; set < NB; ++set)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) acc[set][q] = 0.f;
+      for (int bt = 0; bt < g.n_batches; ++bt) {
+        const int q = bt / g.nch, c = bt - q * g.nch;
+        const int mm = min(m, gc - c * m), nq = min(4, g.nrb - 4 * q);
+        if (q != cur_q) {
+          if (cur_q >= 0) flush(cur_q);
+          cur_q = q;
         }
-        const int gl = g_lo - ga + gi;
-        const uint8_t* tc = sb + i * TILE_CODE_BYTES + gq * 64 + tq * 16;
-        uint4 w[4];
+        mbar_wait(&full[slot], phase);
+        const uint8_t* sb = ring + static_cast<size_t>(slot) * a.slot_bytes;
+#pragma unroll 1
+        for (int gl = wg; gl < mm; gl += 4) {
+          const int gi = c * m + gl;  // CTA-local group
+          const int ti = wq * mm + gl;  // tile of (row block 4 q + wq, group gi) in the batch
+          uint32_t av[32];
+          float Srow = 0.f;
+          int zrow = 0;
+          if (wq < nq) {
+            const uint8_t* rp = sb + ti * TILE_CODE_BYTES + lane * 64;
+            uint4 in[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) w[q] = *reinterpret_cast<const uint4*>(tc + q * 512);
-        const uint2 sp = *reinterpret_cast<const uint2*>(sb + a.sc_off + i * TILE_SCALE_BYTES + gq * 8);
-        const uint32_t zw = *reinterpret_cast<const uint16_t*>(sb + a.z_off + i * TILE_ZERO_BYTES + gq * 2);
-        const float2 Sa = __half22float2(*reinterpret_cast<const __half2*>(&sp.x));  // rows gq, gq + 8
-        const float2 Sb = __half22float2(*reinterpret_cast<const __half2*>(&sp.y));  // rows gq + 16, gq + 24
-        const float Sr[4] = {Sa.x, Sa.y, Sb.x, Sb.y};
+            for (int k = 0; k < 4; ++k) in[k] = *reinterpret_cast<const uint4*>(rp + ((k ^ swz) << 4));
+            if (swz & 1) {
+              uint4 t0 = in[0];
+              in[0] = in[1];
+              in[1] = t0;
+              t0 = in[2];
+              in[2] = in[3];
+              in[3] = t0;
+            }
+            if (swz & 2) {
+              uint4 t0 = in[0];
+              in[0] = in[2];
+              in[2] = t0;
+              t0 = in[1];
+              in[1] = in[3];
+              in[3] = t0;
+            }
 #pragma unroll
-        for (int set = 0; set < NB; ++set) {
-          if (set * 4 >= B) break;
-          uint4 bA = make_uint4(0u, 0u, 0u, 0u), bB = bA;  // B fragments (columns >= NCOL are zero)
-          if (gq < NCOL) {
-            const uint8_t* bp = xp + gl * XPG + set * XPC + tq * XTQ + gq * 32;
-            bA = *reinterpret_cast<const uint4*>(bp);
-            bB = *reinterpret_cast<const uint4*>(bp + 16);
+            for (int t = 0; t < 4; ++t) {
+              const uint32_t wv[4] = {in[t].x, in[t].y, in[t].z, in[t].w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                av[4 * t + j] = wv[j] & 0x0f0f0f0fu;
+                av[16 + 4 * t + j] = (wv[j] >> 4) & 0x0f0f0f0fu;
+              }
+            }
+            Srow = __half2float(*reinterpret_cast<const __half*>(sb + a.sc_off + ti * TILE_SCALE_BYTES +
+                                                                 (lane & 7) * 8 + (lane >> 3) * 2));
+            const uint32_t zw = *reinterpret_cast<const uint16_t*>(sb + a.z_off + ti * TILE_ZERO_BYTES + (lane & 7) * 2);
+            zrow = static_cast<int>((zw >> (4 * (lane >> 3))) & 15u);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) av[k] = 0u;
           }
-          constexpr uint32_t ML = 0x0f0f0f0fu, MH = 0xf0f0f0f0u;
-          int Dl[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}}, Dh[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+          tmem_st32(tA + lane_off, av);
+          tmem_st_wait();
+          tc_fence_before();
+          named_bar_sync(5 + wg, 128);  // A complete; the previous D read back by every warp
+          if (wq == 0 && lane == 0) {
+            tc_fence_after();
+            const uint64_t bd = smem_desc_sw128(xp + gi * XPG);
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {  // rows gq + 16 hh (w[2 hh]) and gq + 16 hh + 8 (w[2 hh + 1])
-            const uint4 r0 = w[2 * hh], r1 = w[2 * hh + 1];
-            mma_u8s8(Dl[hh], r0.x & ML, r1.x & ML, r0.y & ML, r1.y & ML, bA.x, bA.y);  // low nibbles, words 0, 1
-            mma_u8s8(Dl[hh], r0.z & ML, r1.z & ML, r0.w & ML, r1.w & ML, bA.z, bA.w);  // low nibbles, words 2, 3
-            mma_u8s8(Dh[hh], r0.x & MH, r1.x & MH, r0.y & MH, r1.y & MH, bB.x, bB.y);  // high nibbles (16 q)
-            mma_u8s8(Dh[hh], r0.z & MH, r1.z & MH, r0.w & MH, r1.w & MH, bB.z, bB.w);
+            for (int kk = 0; kk < 4; ++kk) mma_i8_ts(tD, tA + 8 * kk, bd + 2 * kk, IDESC, kk > 0 ? 1u : 0u);
+            mma_commit(&mdone[wg]);
           }
-          // lane (gq, tq) holds columns 2 tq (hi digit) and 2 tq + 1 (lo digit) = token tq of the
-          // set, rows gq + 8 q
-          const int b = set * 4 + tq;
-          if (BT == 1 ? tq == 0 : b < B) {
-            const int2 xf = xs[gl * BT + b];
-            const float F = __int_as_float(xf.y);
+          mbar_wait(&mdone[wg], mph);
+          mph ^= 1;
+          tc_fence_after();
+          uint32_t dv[NC];
+          tmem_ld_cols<NC>(tD + lane_off, dv);
+          tmem_ld_wait();
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int hh = q >> 1, e = (q & 1) * 2;
-              const int zq = static_cast<int>((zw >> (4 * q)) & 15u);
-              const int I = Dl[hh][e] * 256 + Dl[hh][e + 1] + ((Dh[hh][e] * 256 + Dh[hh][e + 1]) >> 4) - zq * xf.x;
-              acc[set][q] = fmaf(Sr[q] * F, static_cast<float>(I), acc[set][q]);
+          for (int b = 0; b < BT; ++b) {
+            if (b < B) {
+              const int2 xf = xs[gi * BT + b];
+              const int I = static_cast<int>(dv[2 * b]) * 256 + static_cast<int>(dv[2 * b + 1]) - zrow * xf.x;
+              acc[b] = fmaf(Srow * __int_as_float(xf.y), static_cast<float>(I), acc[b]);
             }
           }
         }
-        gi += step;
-        while (gi >= pl) {
-          gi -= pl;
-          ++ri;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (++slot == a.S) {
+          slot = 0;
+          phase ^= 1;
         }
       }
-      flush();
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-      if (++slot == a.S) {
-        slot = 0;
-        phase ^= 1;
-      }
-      off0 += a.TPS;
-      while (off0 >= gc) {
-        off0 -= gc;
-        ++r_lo;
-      }
+      if (cur_q >= 0) flush(cur_q);
     }
-  }
 
-  // ------------------------------------------------------------ reduction + epilogue (a8)
-  named_bar_sync(1, NW * 32);
-  if (threadIdx.x == 0) g1_mark(5);
-  if (CL > 1) cluster_wait();  // every CTA of the cluster is running: DSMEM is legal
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < R * BT; idx += NW * 32) {
-    const int r = idx / BT, b = idx - r * BT;
-    float sum;
-    if (BT == 1 && !a.atom) {
-      float s4[4] = {0.f, 0.f, 0.f, 0.f};
+    // ---------------------------------------------------------- reduction + epilogue (a8)
+    named_bar_sync(1, NW * 32);
+    if (s == 0 && CL > 1) cluster_wait();  // every CTA of the cluster is running: DSMEM is legal
+    if (g.active) {
+      for (int idx = tid; idx < g.R * BT; idx += NW * 32) {
+        const int r = idx / BT, b = idx - r * BT;
+        float sum;
+        if (BT == 1 && !S.atom) {
+          float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
-      for (int w = 0; w < NW; ++w) s4[w & 3] += part[static_cast<size_t>(w) * a.R_max + r];
-      sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);  // fixed order
-    } else {
-      sum = part[idx];
+          for (int w = 0; w < NW; ++w) s4[w & 3] += part[static_cast<size_t>(w) * S.R_max + r];
+          sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);  // fixed order
+        } else {
+          sum = part[idx];
+        }
+        const int owner = r / g.RR;
+        float* dst = recv + (crank * S.RRmax + (r - owner * g.RR)) * BT + b;
+        if (owner == crank)
+          *dst = sum;
+        else
+          st_async_b32(mapa(smem_u32(dst), static_cast<uint32_t>(owner)), __float_as_uint(sum),
+                       mapa(smem_u32(rbar), static_cast<uint32_t>(owner)));
+      }
     }
-    const int owner = r / RR;
-    float* dst = recv + (crank * a.RRmax + (r - owner * RR)) * BT + b;
-    if (owner == crank)
-      *dst = sum;
-    else
-      st_async_b32(mapa(smem_u32(dst), static_cast<uint32_t>(owner)), __float_as_uint(sum),
-                   mapa(smem_u32(rbar), static_cast<uint32_t>(owner)));
-  }
-  named_bar_sync(1, NW * 32);  // my own partials are in recv
-  if (CL > 1) mbar_wait(rbar, 0);  // and those of the other CTAs of the cluster
-  if (a.pdl) pdl_wait();  // y may still be read by the previous kernel
-  if (threadIdx.x == 0) g1_mark(6);
-  for (int idx = tid; idx < my_n * BT; idx += NW * 32) {
-    const int rl = idx / BT, b = idx - rl * BT;
-    if (b >= B) continue;
-    float v = 0.f;
-    for (int c = 0; c < CL; ++c) v += recv[(c * a.RRmax + rl) * BT + b];  // fixed order
-    const int64_t n = static_cast<int64_t>(rb0) * TILE_ROWS + my_lo + rl;
-    if (n < d.N) {
-      if (d.bias) v += __ldg(d.bias + n);
-      const int64_t o = static_cast<int64_t>(b) * d.N + n;
-      if (a.y_dtype == 0)
-        static_cast<__half*>(d.y)[o] = __float2half_rn(v);
-      else if (a.y_dtype == 1)
-        static_cast<__nv_bfloat16*>(d.y)[o] = __float2bfloat16_rn(v);
-      else
-        static_cast<float*>(d.y)[o] = v;
+    named_bar_sync(1, NW * 32);           // my own partials are in recv
+    if (g.active && CL > 1) mbar_wait(rbar, s & 1);  // and those of the other CTAs of the cluster
+    if (g.active) {
+      for (int idx = tid; idx < g.my_n * BT; idx += NW * 32) {
+        const int rl = idx / BT, b = idx - rl * BT;
+        if (b >= B) continue;
+        float v = 0.f;
+        for (int c = 0; c < CL; ++c) v += recv[(c * S.RRmax + rl) * BT + b];  // fixed order
+        const int64_t n = static_cast<int64_t>(g.rb0) * TILE_ROWS + g.my_lo + rl;
+        if (n < d.N) {
+          if (d.bias) v += __ldg(d.bias + n);
+          const int64_t o = static_cast<int64_t>(b) * d.N + n;
+          if (a.y_dtype == 0)
+            static_cast<__half*>(d.y)[o] = __float2half_rn(v);
+          else if (a.y_dtype == 1)
+            static_cast<__nv_bfloat16*>(d.y)[o] = __float2bfloat16_rn(v);
+          else
+            static_cast<float*>(d.y)[o] = v;
+        }
+      }
+    }
+    if (s + 1 < a.n_stages) {
+      named_bar_sync(1, NW * 32);  // every store (and every read of recv) of this stage is done
+      if (tid == 0) {
+        if (CL > 1)  // the next stage's cluster partials may land once the barrier below completes
+          mbar_arrive_expect_tx(rbar, static_cast<uint32_t>((CL - 1) * sgeo[s + 1].my_n * BT * 4));
+        gen = grid_arrive(a.gbar, gridDim.x);
+      }
     }
   }
-  if (threadIdx.x == 0) g1_mark(7);
+  if constexpr (BT > 1) {  // every warpgroup waited for its last MMA
+    tc_fence_before();
+    named_bar_sync(1, NW * 32);
+    if (warp == 0) tmem_dealloc(*tmem_slot, 512);
+  }
 }
 
-// Activation transform for B > 1 (a4, a5), once per (linear, group, set of four tokens) for the
-// whole launch: one warp each, results (fixed-point digits laid out as the GEMV's B fragments,
-// per-(group, token) sum and scale) to a workspace the GEMV bulk-copies.  Same arithmetic as the
-// fused B = 1 path of paro_gemv1_kernel.
+// Activation transform of stage 0 for B > 1 (a4, a5), once per (linear, group, set of four
+// tokens) for the whole launch: one warp each.
+struct Gemv1XformArgs {
+  Gemv1Stage st;
+  int B, x_bf16, rotate, pdl;
+};
+
 template <int BT>
-__global__ void __launch_bounds__(128) paro_gemv1_xform_kernel(const Gemv1Args a) {
-  constexpr int NB = BT / 4, XPC = 4 * 8 * 32, XPG = NB * XPC;
+__global__ void __launch_bounds__(128) paro_gemv1_xform_kernel(const __grid_constant__ Gemv1XformArgs a) {
+  constexpr int NB = BT / 4;
   __shared__ __align__(16) float scr_all[4][4 * 128];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (a.pdl) pdl_launch_dependents();
   const int task = blockIdx.x * 4 + warp;
-  const int G = a.G, B = a.B;
-  if (task >= a.n_lin * G * NB) return;
-  const int li = task / (G * NB), rem = task - li * G * NB, gam = rem / NB, set = rem - gam * NB;
-  const Gemv1Linear& d = a.lin[li];
-  float* scr = scr_all[warp];
-  const int L = a.rotate ? d.L : 0;
-  float4 cs[8];
-  uint32_t ix[8];
-  const int64_t rec = static_cast<int64_t>(gam) * L * 32 + lane;
-#pragma unroll
-  for (int t = 0; t < 8; ++t)
-    if (t < L) {
-      cs[t] = __ldg(reinterpret_cast<const float4*>(d.rot_cs) + rec + t * 32);
-      ix[t] = __ldg(reinterpret_cast<const uint32_t*>(d.rot_idx) + rec + t * 32);
-    }
-  const float4 sv =
-      a.rotate ? __ldg(reinterpret_cast<const float4*>(d.svec + gam * 128) + lane) : make_float4(1.f, 1.f, 1.f, 1.f);
-  if (a.pdl) pdl_wait();  // x may be written by the previous kernel on the stream
-  const int b0 = set * 4;
-  uint2 xv[4];
-#pragma unroll
-  for (int tb = 0; tb < 4; ++tb)
-    xv[tb] = (b0 + tb < B) ? __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(a.x) +
-                                                                 (static_cast<int64_t>(b0 + tb) * a.K + gam * 128 +
-                                                                  4 * lane) * 2))
-                           : make_uint2(0u, 0u);  // tokens >= B: x = 0, never stored
-#pragma unroll
-  for (int tb = 0; tb < 4; ++tb) {
-    float2 f01, f23;
-    if (a.x_bf16) {
-      f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv[tb].x));
-      f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv[tb].y));
-    } else {
-      f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv[tb].x));
-      f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv[tb].y));
-    }
-    *reinterpret_cast<float4*>(scr + tb * 128 + 4 * lane) =
-        make_float4(f01.x * sv.x, f01.y * sv.y, f23.x * sv.z, f23.y * sv.w);  // a4: u = s . x
-  }
-  __syncwarp();
-#pragma unroll
-  for (int t = 0; t < 8; ++t) {  // a5: rotations t = 1..L (Eq. 4 / Eq. 5)
-    if (t >= L) break;
-    const uint32_t i0 = ix[t] & 0xff, j0 = (ix[t] >> 8) & 0xff, i1 = (ix[t] >> 16) & 0xff, j1 = ix[t] >> 24;
-#pragma unroll
-    for (int tb = 0; tb < 4; ++tb) {
-      float* sc = scr + tb * 128;
-      const float a0 = sc[i0], b0v = sc[j0], a1 = sc[i1], b1v = sc[j1];
-      sc[i0] = cs[t].x * a0 - cs[t].y * b0v;
-      sc[j0] = cs[t].y * a0 + cs[t].x * b0v;
-      sc[i1] = cs[t].z * a1 - cs[t].w * b1v;
-      sc[j1] = cs[t].w * a1 + cs[t].z * b1v;
-    }
-    __syncwarp();
-  }
-  uint8_t* xq = const_cast<uint8_t*>(d.xq) + static_cast<size_t>(gam) * XPG + set * XPC;
-  int2* xs = const_cast<int2*>(d.xqs) + static_cast<size_t>(gam) * BT;
-#pragma unroll
-  for (int tb = 0; tb < 4; ++tb) {  // fixed point + digits, the layout of paro_gemv1_kernel's B fragments
-    int* fx = reinterpret_cast<int*>(scr + tb * 128);
-    const float4 v = *reinterpret_cast<const float4*>(scr + tb * 128 + 4 * lane);
-    const float ml = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
-    const uint32_t mb = __reduce_max_sync(0xffffffffu, __float_as_uint(ml));
-    int E = mb < 0x00800000u ? -100 : static_cast<int>(mb >> 23) - 127 + ((mb & 0x7fffffu) != 0u ? 1 : 0);
-    E = max(E, -100);
-    const float mul = __uint_as_float(static_cast<uint32_t>(141 - E) << 23);  // 2^(14 - E)
-    const int f0 = __float2int_rn(v.x * mul), f1 = __float2int_rn(v.y * mul);
-    const int f2 = __float2int_rn(v.z * mul), f3 = __float2int_rn(v.w * mul);
-    const int X = __reduce_add_sync(0xffffffffu, (f0 + f1) + (f2 + f3));
-    __syncwarp();
-    *reinterpret_cast<int4*>(fx + 4 * lane) = make_int4(f0, f1, f2, f3);
-    __syncwarp();
-    const int tq = lane >> 3, col = (lane >> 2) & 1, kb = lane & 3, p = kb >> 1, h = kb & 1;
-    uint32_t wd[2];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int j = 2 * h + e;
-      uint32_t wv = 0;
-#pragma unroll
-      for (int bb = 0; bb < 4; ++bb) {
-        const int c = 16 * (2 * j + p) + 2 * tq + (bb >> 1) + 8 * (bb & 1);  // tile_k(tq, j, 2 bb + p)
-        const int f = fx[c];
-        const int lo = static_cast<int>(static_cast<int8_t>(f & 0xff));
-        const int dg = col ? lo : ((f - lo) >> 8);
-        wv |= (static_cast<uint32_t>(dg) & 0xffu) << (8 * bb);
-      }
-      wd[e] = wv;
-    }
-    *reinterpret_cast<uint2*>(xq + tq * (8 * 32) + (2 * tb + col) * 32 + kb * 8) = make_uint2(wd[0], wd[1]);
-    if (lane == 0) xs[b0 + tb] = make_int2(X, static_cast<int>(static_cast<uint32_t>(113 + E) << 23));
-  }
+  if (task >= a.st.n_lin * a.st.G * NB) return;
+  g1_xform_task<BT>(a.st, task, a.B, a.x_bf16, a.rotate, scr_all[warp], lane, a.pdl != 0);
 }
 
 // ============================================================================ host side
@@ -721,7 +842,13 @@ size_t gemv1_xq_bytes(int B, int64_t K) {
 }
 
 cudaError_t launch_gemv1_xform(const Gemv1Config& c, cudaStream_t st) {
-  const int tasks = c.a.n_lin * c.a.G * (c.BT / 4);
+  Gemv1XformArgs x{};
+  x.st = c.a.st[0];
+  x.B = c.a.B;
+  x.x_bf16 = c.a.x_bf16;
+  x.rotate = c.a.rotate;
+  x.pdl = c.a.pdl;
+  const int tasks = x.st.n_lin * x.st.G * (c.BT / 4);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((tasks + 3) / 4);
   cfg.blockDim = dim3(128);
@@ -731,21 +858,24 @@ cudaError_t launch_gemv1_xform(const Gemv1Config& c, cudaStream_t st) {
   at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at.val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = &at;
-  cfg.numAttrs = c.a.pdl ? 1 : 0;
+  cfg.numAttrs = x.pdl ? 1 : 0;
   switch (c.BT) {
-    case 4: return cudaLaunchKernelEx(&cfg, paro_gemv1_xform_kernel<4>, c.a);
-    case 8: return cudaLaunchKernelEx(&cfg, paro_gemv1_xform_kernel<8>, c.a);
-    case 16: return cudaLaunchKernelEx(&cfg, paro_gemv1_xform_kernel<16>, c.a);
+    case 4: return cudaLaunchKernelEx(&cfg, paro_gemv1_xform_kernel<4>, x);
+    case 8: return cudaLaunchKernelEx(&cfg, paro_gemv1_xform_kernel<8>, x);
+    case 16: return cudaLaunchKernelEx(&cfg, paro_gemv1_xform_kernel<16>, x);
     default: return cudaErrorInvalidConfiguration;
   }
 }
 
-template <int BT>
+template <int BT, int MS>
 static const void* g1_kernel() {
-  return reinterpret_cast<const void*>(&paro_gemv1_kernel<G1_NW, BT>);
+  return reinterpret_cast<const void*>(&paro_gemv1_kernel<G1_NW, BT, MS>);
 }
-static const void* g1_kernel_bt(int BT) {
-  return BT == 1 ? g1_kernel<1>() : BT == 4 ? g1_kernel<4>() : BT == 8 ? g1_kernel<8>() : g1_kernel<16>();
+static const void* g1_kernel_bt(int BT, bool chain) {
+  if (chain)
+    return BT == 1 ? g1_kernel<1, CHAIN_MAX_STAGES>() : BT == 4 ? g1_kernel<4, CHAIN_MAX_STAGES>()
+         : BT == 8 ? g1_kernel<8, CHAIN_MAX_STAGES>() : g1_kernel<16, CHAIN_MAX_STAGES>();
+  return BT == 1 ? g1_kernel<1, 1>() : BT == 4 ? g1_kernel<4, 1>() : BT == 8 ? g1_kernel<8, 1>() : g1_kernel<16, 1>();
 }
 
 // clusters of CL (BT-token instance) that fit in one wave, from the occupancy API (cached per
@@ -771,130 +901,154 @@ static int g1_active_clusters_compute(const void* k, int CL, int threads, int bu
   }
   return nc;
 }
-static int g1_active_clusters(int BT, int CL, int threads, int budget) {
-  return cached_device_int(g1_kernel_bt(BT), CL, threads, budget, g1_active_clusters_compute);
+static int g1_active_clusters(int BT, bool chain, int CL, int threads, int budget) {
+  return cached_device_int(g1_kernel_bt(BT, chain), CL, threads, budget, g1_active_clusters_compute);
 }
 
-bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config* cfg, const char** why) {
+bool plan_gemv1_chain(int B, int n_stages, const int* n_lin, const int64_t (*Ns)[GEMV_MAX_LIN], const int64_t* Ks,
+                      int rotate, Gemv1Config* cfg, const char** why) {
   if (B < 1 || B > GEMV1_MAX_B) {
     *why = "1..16 tokens per decode launch";
     return false;
   }
-  const int BT = B == 1 ? 1 : B <= 4 ? 4 : B <= 8 ? 8 : 16;
-  const int TB = BT == 1 ? 1 : 4, NSET = (BT + 3) / 4, NCOL = BT == 1 ? 2 : 8;
-  if (n_lin < 1 || n_lin > GEMV_MAX_LIN) {
-    *why = "1..4 linears per decode launch";
+  if (n_stages < 1 || n_stages > CHAIN_MAX_STAGES) {
+    *why = "1..16 stages per decode launch";
     return false;
   }
-  const int G = static_cast<int>(K / 128);
-  if (G < 1) {
-    *why = "K must be a positive multiple of 128";
-    return false;
+  const bool chain = n_stages > 1;
+  const int BT = B == 1 ? 1 : B <= 4 ? 4 : B <= 8 ? 8 : 16;
+  const int NSET = (BT + 3) / 4;
+  int Gmin = 1 << 30;
+  double wbytes = 0;
+  for (int s = 0; s < n_stages; ++s) {
+    if (n_lin[s] < 1 || n_lin[s] > GEMV_MAX_LIN) {
+      *why = "1..4 linears per decode stage";
+      return false;
+    }
+    const int G = static_cast<int>(Ks[s] / 128);
+    if (G < 1) {
+      *why = "K must be a positive multiple of 128";
+      return false;
+    }
+    Gmin = std::min(Gmin, G);
+    for (int i = 0; i < n_lin[s]; ++i) wbytes += static_cast<double>(Ns[s][i]) * Ks[s] * 0.52;
   }
   Gemv1Config c{};
   Gemv1Args& a = c.a;
   // Cluster size = how many ways a row block's groups are split (G / CL groups transformed per
   // CTA).  The rotations are shared-memory bound (8 accesses per pair-update, all warps at once),
   // so fewer groups per CTA shorten the transform; but clusters of 2 / 4 / 8 fill only 148 / 132
-  // / 120 SMs (occupancy API), which slows the weight stream.  Measured (tools/time_groups.py,
-  // tools/time_70b.py): short streams (< 20 MB) at K = 4096 prefer 4, long ones 2; K >= 8192
-  // prefers 8 (one transform round) unless the stream is very long and G small (70B gate+up: 2).
-  double wbytes = 0;
-  for (int i = 0; i < n_lin; ++i) wbytes += static_cast<double>(Ns[i]) * K * 0.52;
+  // / 120 SMs (occupancy API), which slows the weight stream.  Measured for single launches
+  // (tools/time_groups.py, tools/time_70b.py): short streams (< 20 MB) at K = 4096 prefer 4, long
+  // ones 2; K >= 8192 prefers 8 (one transform round) unless the stream is very long and G small
+  // (70B gate+up: 2).  A chain shares one cluster size over its stages: 4.
   int CL;
-  if (G >= 64)
-    CL = (wbytes < 64e6 || G >= 128) ? 8 : 2;
-  else
-    CL = wbytes < 20e6 ? 4 : 2;
-  CL = g1_env("PARO_G1_CL", CL);
+  if (chain) {
+    CL = 4;
+  } else {
+    const int G = static_cast<int>(Ks[0] / 128);
+    if (G >= 64)
+      CL = (wbytes < 64e6 || G >= 128) ? 8 : 2;
+    else
+      CL = wbytes < 20e6 ? 4 : 2;
+  }
+  CL = g1_env(chain ? "PARO_G1_CHAIN_CL" : "PARO_G1_CL", CL);
   if (CL != 1 && CL != 2 && CL != 4 && CL != 8) CL = 2;
-  while (CL > 1 && CL > G) CL /= 2;
+  while (CL > 1 && CL > Gmin) CL /= 2;
   const int NW = G1_NW;
-  int TPS = std::max(1, std::min(64, g1_env("PARO_G1_TPS", 2 * NW)));
   const int threads = (NW + 1) * 32;
   c.NW = NW;
   const int budget = device_smem_optin() - 1024;
-  // clusters that fit in one wave (occupancy API, cached per cluster size)
-  int ncl_max = g1_active_clusters(BT, CL, threads, budget);
+  int ncl_max = g1_active_clusters(BT, chain, CL, threads, budget);
   ncl_max = std::min(ncl_max, std::max(1, g1_env("PARO_G1_MAXCL", 1 << 20)));
-  // clusters over linears in proportion to their row blocks (>= 1 each, <= row blocks)
-  int64_t NB[GEMV_MAX_LIN], NBsum = 0;
-  for (int i = 0; i < n_lin; ++i) {
-    NB[i] = (Ns[i] + TILE_ROWS - 1) / TILE_ROWS;
-    NBsum += NB[i];
+  int grid = 0, rmax_all = 0, rrmax_all = 0, gcm = 0, part_words = 0;
+  int64_t cta_tiles = 0;  // tiles of the busiest CTA over the whole chain
+  for (int s = 0; s < n_stages; ++s) {
+    Gemv1Stage& S = a.st[s];
+    const int n = n_lin[s];
+    const int G = static_cast<int>(Ks[s] / 128);
+    // clusters over linears in proportion to their row blocks (>= 1 each, <= row blocks)
+    int64_t NB[GEMV_MAX_LIN], NBsum = 0;
+    for (int i = 0; i < n; ++i) {
+      NB[i] = (Ns[s][i] + TILE_ROWS - 1) / TILE_ROWS;
+      NBsum += NB[i];
+    }
+    int ncl = static_cast<int>(std::min<int64_t>(ncl_max, NBsum));
+    if (ncl < n) ncl = n;
+    int cls[GEMV_MAX_LIN], used = 0, big = 0;
+    for (int i = 0; i < n; ++i) {
+      cls[i] = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(NB[i], ncl * NB[i] / NBsum)));
+      used += cls[i];
+      if (NB[i] > NB[big]) big = i;
+    }
+    cls[big] = static_cast<int>(std::min<int64_t>(NB[big], cls[big] + std::max(0, ncl - used)));
+    int begin = 0, rmax = 0;
+    for (int i = 0; i < n; ++i) {
+      Gemv1Linear& d = S.lin[i];
+      d.N = static_cast<int>(Ns[s][i]);
+      d.cta_begin = begin;
+      d.rb_base = static_cast<int>(NB[i] / cls[i]);
+      d.rb_extra = static_cast<int>(NB[i] % cls[i]);
+      rmax = std::max(rmax, (d.rb_base + (d.rb_extra ? 1 : 0)) * TILE_ROWS);
+      begin += cls[i] * CL;
+    }
+    S.n_lin = n;
+    S.K = static_cast<int>(Ks[s]);
+    S.G = G;
+    S.n_cta = begin;
+    S.R_max = rmax;
+    S.RRmax = (rmax + CL - 1) / CL;
+    // B = 1: per-warp row partials summed in a fixed order (deterministic) while they fit in
+    // 48 KB; clusters with more rows (e.g. 70B gate+up: 3840 rows) add with shared atomics
+    S.atom = BT == 1 && (static_cast<int64_t>(NW) * rmax * 4 > (g1_env("PARO_G1_ATOM_KB", 48) << 10));
+    S.xq_in_kernel = (BT > 1 && s > 0) ? 1 : 0;
+    grid = std::max(grid, begin);
+    rmax_all = std::max(rmax_all, rmax);
+    rrmax_all = std::max(rrmax_all, S.RRmax);
+    gcm = std::max(gcm, (G + CL - 1) / CL);
+    part_words = std::max(part_words, (BT == 1 && !S.atom ? NW : BT) * rmax);
+    cta_tiles += static_cast<int64_t>(rmax / TILE_ROWS) * ((G + CL - 1) / CL);
   }
-  int ncl = static_cast<int>(std::min<int64_t>(ncl_max, NBsum));
-  if (ncl < n_lin) ncl = n_lin;
-  int cls[GEMV_MAX_LIN], used = 0, big = 0;
-  for (int i = 0; i < n_lin; ++i) {
-    cls[i] = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(NB[i], ncl * NB[i] / NBsum)));
-    used += cls[i];
-    if (NB[i] > NB[big]) big = i;
-  }
-  cls[big] = static_cast<int>(std::min<int64_t>(NB[big], cls[big] + std::max(0, ncl - used)));
-  int begin = 0, rmax = 0;
-  for (int i = 0; i < n_lin; ++i) {
-    Gemv1Linear& d = a.lin[i];
-    d.N = static_cast<int>(Ns[i]);
-    d.cta_begin = begin;
-    d.rb_base = static_cast<int>(NB[i] / cls[i]);
-    d.rb_extra = static_cast<int>(NB[i] % cls[i]);
-    rmax = std::max(rmax, (d.rb_base + (d.rb_extra ? 1 : 0)) * TILE_ROWS);
-    begin += cls[i] * CL;
-  }
-  c.grid = begin;
+  c.grid = grid;
   c.CL = CL;
   c.BT = BT;
   a.B = B;
-  a.n_lin = n_lin;
-  a.K = static_cast<int>(K);
-  a.G = G;
+  a.n_stages = n_stages;
   a.rotate = rotate;
-  a.TPS = TPS;
   a.pre_stages = std::max(0, g1_env("PARO_G1_PRE", 2));
   a.params_first = g1_env("PARO_G1_PF", 1);
-  a.skip_math = g1_env("PARO_G1_SKIP", 0);
-  a.R_max = rmax;
-  a.RRmax = (rmax + CL - 1) / CL;
-  const int gcm = (G + CL - 1) / CL;
-  a.sc_off = static_cast<uint32_t>(TPS) * TILE_CODE_BYTES;
-  a.z_off = a.sc_off + static_cast<uint32_t>(TPS) * TILE_SCALE_BYTES;
-  a.slot_bytes = g1_align(a.z_off + static_cast<uint32_t>(TPS) * TILE_ZERO_BYTES, 128);
   uint32_t off = 0;
   a.off_xp = off;
-  off += g1_align(static_cast<uint32_t>(gcm) * NSET * 4 * NCOL * 32, 128);
+  off += g1_align(static_cast<uint32_t>(gcm) * NSET * 4 * (BT == 1 ? 2 : 8) * 32, 128);
+  off += 128;  // 32 zero bytes (lanes of unused MMA columns) just below xs
   a.off_xs = off;
-  off += g1_align(static_cast<uint32_t>(gcm) * BT * 8 + 48, 128);  // + a 16-aligned 32-byte zero block
+  off += g1_align(static_cast<uint32_t>(gcm) * BT * 8, 128);
   a.off_part = off;
-  // B = 1: per-warp row partials summed in a fixed order (deterministic) while they fit in
-  // 48 KB; clusters with more rows (e.g. 70B gate+up: 3840 rows) add with shared atomics
-  a.atom = BT == 1 && (static_cast<int64_t>(NW) * rmax * 4 > (g1_env("PARO_G1_ATOM_KB", 48) << 10));
-  off += g1_align(static_cast<uint32_t>(BT == 1 && !a.atom ? NW : BT) * rmax * 4, 128);
-  a.off_scr = a.off_recv = off;  // BT > 1: phase-1 scratch and the cluster reduction share this space
-  if (BT == 1) {
+  off += g1_align(static_cast<uint32_t>(part_words) * 4, 128);
+  a.off_scr = off;
+  if (BT == 1)
     off += NW * 512;
-    a.off_recv = off;
-    off += g1_align(static_cast<uint32_t>(CL) * a.RRmax * 4, 128);
-  } else {  // the transform runs in paro_gemv1_xform_kernel: no scratch
-    off += g1_align(static_cast<uint32_t>(CL) * a.RRmax * BT * 4, 128);
-  }
+  else if (chain)
+    off += NW * 2048;  // in-kernel transform tasks of later stages (4 tokens x 128 channels)
+  a.off_recv = off;
+  off += g1_align(static_cast<uint32_t>(CL) * rrmax_all * BT * 4, 128);
   a.off_bar = off;
-  off += 64 * 16;
+  off += 64 * 16 + 64;  // <= 120 mbarriers (ring full / empty, rbar, xbar, 4 x mdone) + the TMEM base
   a.off_ring = g1_align(off, 1024);
-  const int64_t avail = static_cast<int64_t>(budget) - a.off_ring;
-  // stage size: the largest TPS <= 32 (two tiles per warp) that keeps >= 2 stages in flight, else
-  // the largest that fits once (stages a CTA needs: ceil(row blocks x groups / TPS)); measured
-  // flat between 24 and 32 tiles per stage with 2-3 stages (tools/run_g1n.sh)
-  const int64_t cta_tiles = static_cast<int64_t>(rmax / TILE_ROWS) * gcm;
+  const int64_t avail = static_cast<int64_t>(budget) - 1024 - a.off_ring;  // 1024: base alignment slack
+  // batch size: the largest TPS <= 32 (two tiles per warp) that keeps >= 2 batches in flight,
+  // else the largest that fits once; measured flat between 24 and 32 tiles per batch with 2-3
+  // batches (single launches)
   auto slot_of = [&](int tps) {
     const uint32_t sc = static_cast<uint32_t>(tps) * TILE_CODE_BYTES;
     return g1_align(sc + static_cast<uint32_t>(tps) * (TILE_SCALE_BYTES + TILE_ZERO_BYTES), 128);
   };
   auto stages_of = [&](int tps) {
-    const int need = static_cast<int>((cta_tiles + tps - 1) / tps);
-    return std::min<int64_t>(std::min(need, 60), avail / slot_of(tps));
+    const int64_t need = (cta_tiles + tps - 1) / tps + n_stages;
+    return std::min<int64_t>(std::min<int64_t>(need, 56), avail / slot_of(tps));
   };
-  if (g1_env("PARO_G1_TPS", 0) == 0) {
+  int TPS = g1_env("PARO_G1_TPS", 0);
+  if (TPS <= 0 || TPS > 64) {
     int best = 0;
     for (int want = 2; want >= 1 && !best; --want)
       for (int tps = 2 * NW; tps >= 8 && !best; tps -= 4)
@@ -905,26 +1059,40 @@ bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv
   a.sc_off = static_cast<uint32_t>(TPS) * TILE_CODE_BYTES;
   a.z_off = a.sc_off + static_cast<uint32_t>(TPS) * TILE_SCALE_BYTES;
   a.slot_bytes = slot_of(TPS);
-  int S = static_cast<int>(stages_of(TPS));
+  const int S = static_cast<int>(stages_of(TPS));
   if (S < 1) {
     *why = "decode shared-memory plan does not fit";
     return false;
   }
   a.S = S;
-  a.smem_total = a.off_ring + static_cast<uint32_t>(S) * a.slot_bytes;
+  a.smem_total = a.off_ring + static_cast<uint32_t>(S) * a.slot_bytes + 1024;
   if (g1_env("PARO_PLAN_DEBUG", 0))
-    fprintf(stderr, "[paro gemv1 plan] B=%d BT=%d n_lin=%d K=%lld grid=%d CL=%d NW=%d TPS=%d S=%d R_max=%d smem=%u\n",
-            B, BT, n_lin, static_cast<long long>(K), c.grid, CL, NW, TPS, S, rmax, a.smem_total);
+    fprintf(stderr, "[paro gemv1 plan] B=%d BT=%d stages=%d grid=%d CL=%d NW=%d TPS=%d S=%d R_max=%d smem=%u\n", B, BT,
+            n_stages, c.grid, CL, NW, TPS, S, rmax_all, a.smem_total);
   *cfg = c;
   return true;
 }
 
-template <int BT>
+bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config* cfg, const char** why) {
+  int64_t ns[1][GEMV_MAX_LIN] = {};
+  for (int i = 0; i < n_lin && i < GEMV_MAX_LIN; ++i) ns[0][i] = Ns[i];
+  return plan_gemv1_chain(B, 1, &n_lin, ns, &K, rotate, cfg, why);
+}
+
+template <int BT, int MS>
 static cudaError_t g1_launch(const Gemv1Config& c, cudaLaunchConfig_t* cfg) {
-  auto kern = paro_gemv1_kernel<G1_NW, BT>;
+  auto kern = paro_gemv1_kernel<G1_NW, BT, MS>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(c.a.smem_total));
   if (e != cudaSuccess) return e;
-  return cudaLaunchKernelEx(cfg, kern, c.a);
+  if constexpr (MS == CHAIN_MAX_STAGES) {
+    return cudaLaunchKernelEx(cfg, kern, c.a);
+  } else {
+    // one-stage argument block (smaller kernel parameters)
+    Gemv1ArgsT<MS> a1;
+    static_assert(sizeof(Gemv1ArgsT<MS>) <= sizeof(Gemv1Args), "");
+    std::memcpy(static_cast<void*>(&a1), static_cast<const void*>(&c.a), sizeof(a1));
+    return cudaLaunchKernelEx(cfg, kern, a1);
+  }
 }
 
 cudaError_t launch_gemv1(const Gemv1Config& c, cudaStream_t st) {
@@ -947,11 +1115,12 @@ cudaError_t launch_gemv1(const Gemv1Config& c, cudaStream_t st) {
   }
   cfg.attrs = attrs;
   cfg.numAttrs = na;
+  const bool chain = c.a.n_stages > 1;
   switch (c.BT) {
-    case 1: return g1_launch<1>(c, &cfg);
-    case 4: return g1_launch<4>(c, &cfg);
-    case 8: return g1_launch<8>(c, &cfg);
-    case 16: return g1_launch<16>(c, &cfg);
+    case 1: return chain ? g1_launch<1, CHAIN_MAX_STAGES>(c, &cfg) : g1_launch<1, 1>(c, &cfg);
+    case 4: return chain ? g1_launch<4, CHAIN_MAX_STAGES>(c, &cfg) : g1_launch<4, 1>(c, &cfg);
+    case 8: return chain ? g1_launch<8, CHAIN_MAX_STAGES>(c, &cfg) : g1_launch<8, 1>(c, &cfg);
+    case 16: return chain ? g1_launch<16, CHAIN_MAX_STAGES>(c, &cfg) : g1_launch<16, 1>(c, &cfg);
     default: return cudaErrorInvalidConfiguration;
   }
 }

@@ -2,6 +2,7 @@
 // transform preparation (paro_pack), kernel dispatch, NCCL all-gather.
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -370,10 +371,11 @@ static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, 
       const char* why = "";
       if (!paro::plan_gemv1(live, n, Ns, K, rotate, &c1, &why)) return fail(PARO_ERR_UNSUPPORTED, "paro_linear: %s", why);
       paro::Gemv1Args& a = c1.a;
-      a.x = static_cast<const uint8_t*>(x) + b0 * K * xe;
+      paro::Gemv1Stage& S0 = a.st[0];
+      S0.x = static_cast<const uint8_t*>(x) + b0 * K * xe;
       a.x_bf16 = x_dtype == PARO_BF16;
       for (int i = 0; i < n; ++i) {
-        paro::Gemv1Linear& d = a.lin[i];
+        paro::Gemv1Linear& d = S0.lin[i];
         d.codes = static_cast<const uint8_t*>(packed[i].codes);
         d.scales = static_cast<const uint8_t*>(packed[i].scales);
         d.zeros = static_cast<const uint8_t*>(packed[i].zeros);
@@ -392,8 +394,8 @@ static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, 
           return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear: workspace too small (%zu < %zu)", ws_bytes, per * n);
         for (int i = 0; i < n; ++i) {
           uint8_t* base = static_cast<uint8_t*>(ws) + per * i;
-          a.lin[i].xq = base;
-          a.lin[i].xqs = reinterpret_cast<const int2*>(base + static_cast<size_t>(K / kG) * (c1.BT / 4) * 1024);
+          S0.lin[i].xq = base;
+          S0.lin[i].xqs = reinterpret_cast<int2*>(base + static_cast<size_t>(K / kG) * (c1.BT / 4) * 1024);
         }
         cudaError_t e = paro::launch_gemv1_xform(c1, cs);
         if (e != cudaSuccess) return cuda_fail(e, "paro_linear: decode activation transform launch");
@@ -544,6 +546,110 @@ paro_status paro_linear_multi(const void* x, paro_dtype x_dtype, int64_t B, int3
                         rotate, pdl, (flags & 0x100u) ? 1 : 0, workspace, workspace_bytes, cs);
 }
 
+// ---------------------------------------------------------------- persistent decode chain
+static size_t chain_xq_bytes(int64_t B, int32_t n_stages, const paro_chain_stage* stages) {
+  if (B <= 1) return 0;
+  int64_t Kmax = 0;
+  for (int s = 0; s < n_stages; ++s)
+    for (int i = 0; i < stages[s].n; ++i) Kmax = std::max<int64_t>(Kmax, stages[s].packed[i].K);
+  return paro::gemv1_xq_bytes(static_cast<int>(std::min<int64_t>(B, paro::GEMV1_MAX_B)), Kmax);
+}
+
+size_t paro_linear_chain_workspace(int64_t B, int32_t n_stages, const paro_chain_stage* stages) {
+  if (n_stages < 1 || !stages) return 0;
+  for (int s = 0; s < n_stages; ++s)
+    if (stages[s].n < 1 || stages[s].n > paro::GEMV_MAX_LIN || !stages[s].packed) return 0;
+  // grid-barrier words + (B > 1) one x'-digit buffer per linear slot, shared by the stages
+  return 256 + align256(chain_xq_bytes(B, n_stages, stages) * paro::GEMV_MAX_LIN);
+}
+
+paro_status paro_linear_chain(int32_t n_stages, const paro_chain_stage* stages, paro_dtype x_dtype, int64_t B,
+                              paro_dtype y_dtype, uint32_t flags, void* workspace, size_t workspace_bytes,
+                              void* stream) {
+  if (n_stages < 1 || !stages) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear_chain: n_stages >= 1 and stages required");
+  if (B < 1 || B > paro::GEMV1_MAX_B) return fail(PARO_ERR_UNSUPPORTED, "paro_linear_chain: decode chains take 1..16 tokens");
+  if (x_dtype != PARO_F16 && x_dtype != PARO_BF16) return fail(PARO_ERR_UNSUPPORTED, "x must be fp16 or bf16");
+  if (y_dtype != PARO_F16 && y_dtype != PARO_BF16 && y_dtype != PARO_F32)
+    return fail(PARO_ERR_UNSUPPORTED, "y must be fp16, bf16 or fp32");
+  for (int s = 0; s < n_stages; ++s) {
+    const paro_chain_stage& S = stages[s];
+    if (S.n < 1 || S.n > paro::GEMV_MAX_LIN || !S.packed || !S.y)
+      return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear_chain: stage %d needs 1..4 linears, packed and y", s);
+    if (!S.x || !aligned16(S.x)) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear_chain: stage %d x NULL/misaligned", s);
+    for (int i = 0; i < S.n; ++i) {
+      paro_status st = check_packed(&S.packed[i]);
+      if (st != PARO_OK) return st;
+      if (S.packed[i].K != S.packed[0].K) return fail(PARO_ERR_SHAPE, "paro_linear_chain: stage %d linears must share K", s);
+      if (!S.y[i] || !aligned16(S.y[i]))
+        return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear_chain: stage %d y[%d] NULL/misaligned", s, i);
+    }
+  }
+  const size_t need = paro_linear_chain_workspace(B, n_stages, stages);
+  if (!workspace || workspace_bytes < need || !aligned16(workspace))
+    return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear_chain: workspace too small (%zu < %zu) or misaligned",
+                workspace_bytes, need);
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  const int rotate = (flags & PARO_LINEAR_NO_ROTATION) ? 0 : 1;
+  const size_t xe = dtype_bytes(x_dtype), ye = dtype_bytes(y_dtype);
+  const size_t xq_per = chain_xq_bytes(B, n_stages, stages);
+  uint8_t* wsb = static_cast<uint8_t*>(workspace);
+  // chains longer than one argument block run as several launches (the first with the caller's
+  // PDL choice, the later ones always PDL-chained: they only wait for the previous launch)
+  for (int s0 = 0; s0 < n_stages; s0 += paro::CHAIN_MAX_STAGES) {
+    const int ns = std::min(paro::CHAIN_MAX_STAGES, n_stages - s0);
+    int nl[paro::CHAIN_MAX_STAGES];
+    int64_t Ns[paro::CHAIN_MAX_STAGES][paro::GEMV_MAX_LIN] = {};
+    int64_t Ks[paro::CHAIN_MAX_STAGES];
+    for (int s = 0; s < ns; ++s) {
+      const paro_chain_stage& S = stages[s0 + s];
+      nl[s] = S.n;
+      Ks[s] = S.packed[0].K;
+      for (int i = 0; i < S.n; ++i) Ns[s][i] = S.packed[i].N;
+    }
+    paro::Gemv1Config c;
+    const char* why = "";
+    if (!paro::plan_gemv1_chain(static_cast<int>(B), ns, nl, Ns, Ks, rotate, &c, &why))
+      return fail(PARO_ERR_UNSUPPORTED, "paro_linear_chain: %s", why);
+    paro::Gemv1Args& a = c.a;
+    a.x_bf16 = x_dtype == PARO_BF16;
+    a.y_dtype = static_cast<int>(y_dtype);
+    a.pdl = (s0 > 0 || (flags & PARO_LINEAR_PDL)) ? 1 : 0;
+    a.gbar = reinterpret_cast<uint32_t*>(wsb);
+    for (int s = 0; s < ns; ++s) {
+      const paro_chain_stage& S = stages[s0 + s];
+      paro::Gemv1Stage& T = a.st[s];
+      T.x = S.x;
+      for (int i = 0; i < S.n; ++i) {
+        const paro_packed& p = S.packed[i];
+        paro::Gemv1Linear& d = T.lin[i];
+        d.codes = static_cast<const uint8_t*>(p.codes);
+        d.scales = static_cast<const uint8_t*>(p.scales);
+        d.zeros = static_cast<const uint8_t*>(p.zeros);
+        d.rot_cs = static_cast<const float2*>(p.rot_cs);
+        d.rot_idx = static_cast<const uchar2*>(p.rot_idx);
+        d.svec = static_cast<const float*>(p.svec);
+        d.bias = S.bias ? S.bias[i] : nullptr;
+        d.y = S.y[i];
+        d.L = p.n_rot;
+        if (B > 1) {
+          uint8_t* base = wsb + 256 + xq_per * i;
+          d.xq = base;
+          d.xqs = reinterpret_cast<int2*>(base + static_cast<size_t>(p.K / kG) * (c.BT / 4) * 1024);
+        }
+      }
+    }
+    (void)xe;
+    (void)ye;
+    if (B > 1) {
+      cudaError_t e = paro::launch_gemv1_xform(c, cs);
+      if (e != cudaSuccess) return cuda_fail(e, "paro_linear_chain: stage-0 activation transform launch");
+    }
+    cudaError_t e = paro::launch_gemv1(c, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "paro_linear_chain: decode chain launch");
+  }
+  return PARO_OK;
+}
+
 paro_status paro_transform_activations(const void* x, paro_dtype x_dtype, int64_t B, const paro_packed* packed,
                                        void* x_out, void* stream) {
   paro_status st = check_packed(packed);
@@ -556,6 +662,19 @@ paro_status paro_transform_activations(const void* x, paro_dtype x_dtype, int64_
                                          static_cast<const uchar2*>(packed->rot_idx), 1, x_out, 0, 0,
                                          static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "paro_transform_activations");
+  return PARO_OK;
+}
+
+paro_status paro_fwht(const void* x, paro_dtype x_dtype, int64_t T, int64_t n, const float* signs, float scale,
+                      void* y, void* stream) {
+  if (!x || !y || T <= 0) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_fwht: bad x/y/T");
+  if (!aligned16(x) || !aligned16(y) || (signs && !aligned16(signs)))
+    return fail(PARO_ERR_INVALID_ARGUMENT, "paro_fwht: x, y, signs must be 16-byte aligned");
+  if (x_dtype != PARO_F16 && x_dtype != PARO_BF16) return fail(PARO_ERR_UNSUPPORTED, "paro_fwht: x must be fp16 or bf16");
+  if (n < 256 || n > 16384 || (n & (n - 1)))
+    return fail(PARO_ERR_UNSUPPORTED, "paro_fwht: n must be a power of two in [256, 16384]");
+  cudaError_t e = paro::launch_fwht(x, x_dtype == PARO_BF16, T, n, signs, scale, y, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "paro_fwht");
   return PARO_OK;
 }
 

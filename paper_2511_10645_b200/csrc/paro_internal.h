@@ -68,9 +68,12 @@ bool plan_gemv(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t K, in
                const char** why);
 cudaError_t launch_gemv(const GemvConfig& cfg, cudaStream_t st);
 
-// ---------------------------------------------------------------- decode GEMV, one token (gemv1.cu)
-// Cluster c of linear i owns rb_base + (c < rb_extra) consecutive 32-row blocks; CTA k of a
-// cluster of CL owns the groups [k G / CL, (k + 1) G / CL) of those rows (K-split).
+// ---------------------------------------------------------------- decode GEMV, K-split (gemv1.cu)
+// A launch runs a CHAIN of stages (one stage = one multi-linear GEMV whose linears share x);
+// stage s + 1 starts after every CTA finished stage s (grid-wide barrier), so its x may be an
+// earlier stage's y.  A single paro_linear / paro_linear_multi call is a one-stage chain.
+// In stage s, cluster c of linear i owns rb_base + (c < rb_extra) consecutive 32-row blocks;
+// CTA k of a cluster of CL owns the groups [k G / CL, (k + 1) G / CL) of those rows (K-split).
 struct Gemv1Linear {
   const uint8_t* codes;
   const uint8_t* scales;
@@ -80,35 +83,44 @@ struct Gemv1Linear {
   const float* svec;
   const float* bias;
   void* y;  // [B][N]
-  const uint8_t* xq;  // B > 1: pre-transformed x' digits [G][NB][4][8][4][8 B] (paro_gemv1_xform_kernel)
-  const int2* xqs;    // B > 1: per (group, token) (sum x'fix, 2^(E-14)) [G][BT]
+  uint8_t* xq;  // B > 1: pre-transformed x' digits [G][NB][4][8][4][8 B] (workspace)
+  int2* xqs;    // B > 1: per (group, token) (sum x'fix, 2^(E-14)) [G][BT]
   int N, L;
   int cta_begin, rb_base, rb_extra;
 };
 
-constexpr int GEMV1_MAX_B = 16;  // tokens per launch of the K-split kernel
+constexpr int GEMV1_MAX_B = 16;       // tokens per launch of the K-split kernel
+constexpr int CHAIN_MAX_STAGES = 16;  // stages per persistent launch (longer chains: several launches)
 
-struct Gemv1Args {
+struct Gemv1Stage {
   const void* x;  // [B][K] fp16 / bf16
-  int x_bf16;
-  int B;          // tokens (1..16)
-  int n_lin;
+  int n_lin, K, G;
+  int n_cta;      // CTAs with work in this stage (whole clusters); the others only pass the barriers
+  int R_max;      // rows of the largest cluster (per-warp partial stride)
+  int RRmax;      // rows per owner CTA (reduction)
+  int atom;       // B = 1: row partials by shared atomics (clusters with too many rows)
+  int xq_in_kernel;  // B > 1: x' digits computed inside the launch (x is an earlier stage's y)
   Gemv1Linear lin[GEMV_MAX_LIN];
+};
+
+template <int MS>
+struct Gemv1ArgsT {
+  int x_bf16;
+  int B;  // tokens (1..16)
   int y_dtype;
-  int K, G;
   int rotate;
   int pdl;
-  int TPS;     // tiles per ring stage (capacity)
-  int S;       // ring depth
-  int pre_stages;  // stages issued before the compute warps' x / parameter loads are out
-  int params_first;  // the first stages wait until the rotation-parameter loads are issued
-  int atom;          // B = 1: row partials by shared atomics (clusters with too many rows)
-  int skip_math;     // debug: stream the weights, skip the tile math (timing only)
-  int R_max;   // rows of the largest cluster
-  int RRmax;   // rows per owner CTA (reduction)
+  int TPS;           // tiles per ring batch (capacity)
+  int S;             // ring depth (batches)
+  int pre_stages;    // batches issued before the compute warps' x / parameter loads are out
+  int params_first;  // the first batches wait until the rotation-parameter loads are issued
+  int n_stages;
+  uint32_t* gbar;    // grid barrier words (workspace; zero before first use, left zero)
   uint32_t slot_bytes, sc_off, z_off;
   uint32_t off_xp, off_xs, off_scr, off_part, off_recv, off_bar, off_ring, smem_total;
+  Gemv1Stage st[MS];
 };
+using Gemv1Args = Gemv1ArgsT<CHAIN_MAX_STAGES>;
 
 struct Gemv1Config {
   int CL, grid, NW, BT;
@@ -118,7 +130,11 @@ struct Gemv1Config {
 bool gemv1_enabled();
 // B > 1: bytes of pre-transformed activations per linear (digits + per-group sums / scales)
 size_t gemv1_xq_bytes(int B, int64_t K);
+// transform pre-kernel of stage 0 (B > 1)
 cudaError_t launch_gemv1_xform(const Gemv1Config& cfg, cudaStream_t st);
+// Plan a chain: n_stages stages, stage s with n_lin[s] linears of widths Ns[s][i] sharing K[s].
+bool plan_gemv1_chain(int B, int n_stages, const int* n_lin, const int64_t (*Ns)[GEMV_MAX_LIN], const int64_t* K,
+                      int rotate, Gemv1Config* cfg, const char** why);
 bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config* cfg, const char** why);
 cudaError_t launch_gemv1(const Gemv1Config& cfg, cudaStream_t st);
 
@@ -130,6 +146,11 @@ cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, in
 // ---------------------------------------------------------------- on-the-fly transform preparation
 cudaError_t launch_prepare_transform(const float* theta, const int16_t* pairs, int G, int L, int P, float2* rot_cs,
                                      uchar2* rot_idx, cudaStream_t st);
+
+// ---------------------------------------------------------------- fast Walsh-Hadamard transform (hadamard.cu)
+// y (fp16) = scale * H_n diag(signs) x per token; n in {256, ..., 16384}; signs may be NULL
+cudaError_t launch_fwht(const void* x, int x_bf16, int64_t T, int64_t n, const float* signs, float scale, void* y,
+                        cudaStream_t st);
 
 // ---------------------------------------------------------------- misc
 cudaError_t launch_unpack(const uint8_t* codes, const uint8_t* scales, const uint8_t* zeros, int64_t N, int64_t K,

@@ -127,6 +127,53 @@ PARO_DEV void named_bar_arrive(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+
+// ---------------------------------------------------------------- grid-wide barrier (persistent chains)
+// All CTAs of the grid are co-resident (one wave, grid <= occupancy).  gb[0] = arrivals of the
+// current barrier, gb[1] = generation; gb[0] is back to 0 after every completed barrier.
+PARO_DEV uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+PARO_DEV void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+PARO_DEV void st_relaxed_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+PARO_DEV uint32_t atom_add_acq_rel_gpu(uint32_t* p, uint32_t v) {
+  uint32_t o;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(o) : "l"(p), "r"(v) : "memory");
+  return o;
+}
+PARO_DEV uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// One thread per CTA, after a CTA barrier that orders the CTA's writes before it (the
+// cooperative-groups grid.sync pattern).  Returns the generation to wait on.
+PARO_DEV uint32_t grid_arrive(uint32_t* gb, uint32_t nblocks) {
+  const uint32_t gen = ld_acquire_gpu(gb + 1);
+  __threadfence();
+  if (atom_add_acq_rel_gpu(gb, 1u) == nblocks - 1) {
+    st_relaxed_gpu(gb, 0u);
+    st_release_gpu(gb + 1, gen + 1);
+  }
+  return gen;
+}
+// Wait (one thread) until the barrier of generation `gen` completed; traps after 2 s instead of
+// hanging the GPU if a CTA never arrives (e.g. a grid that is not co-resident).
+PARO_DEV void grid_wait(const uint32_t* gb, uint32_t gen) {
+  if (ld_acquire_gpu(gb + 1) != gen) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (ld_acquire_gpu(gb + 1) == gen) {
+    __nanosleep(64);
+    if (globaltimer_ns() - t0 > 2000000000ull) __trap();
+  }
+}
+
 // ---------------------------------------------------------------- programmatic dependent launch
 PARO_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 PARO_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }

@@ -93,6 +93,9 @@ typedef struct {
                                         the previous kernel on the stream finishes (weights must not be written by it) */
 #define PARO_LINEAR_FORCE_GEMV 0x4u  /* force the decode GEMV kernel for any B (tiles of <= 8 tokens) */
 #define PARO_LINEAR_FORCE_GEMM 0x8u  /* force the prefill (tcgen05) path for any B */
+#define PARO_LINEAR_TCGEN05 0x10u    /* decode, 2..16 tokens: tiles on the tcgen05 tensor cores (tcgen05.mma
+                                        kind::i8, A = u8 codes in TMEM, B = s8 x' digits) instead of the
+                                        warp-level mma.sync engine (the default: measured faster) */
 
 /* Sizes of the packed buffers for an [N, K] weight with group size `group`
  * (must be 128) and n_rot rotations (0..8).  Returns PARO_ERR_UNSUPPORTED for
@@ -189,9 +192,10 @@ paro_status paro_linear_multi(const void* x, paro_dtype x_dtype, int64_t B, int3
  *   flags    PARO_LINEAR_PDL (the first launch overlaps the previous kernel's tail; the
  *            packed weights must not be written by it), PARO_LINEAR_NO_ROTATION.
  *   workspace  >= paro_linear_chain_workspace(...) bytes, device, 16-B aligned.  Its first
- *            256 bytes hold the grid-barrier words: they must be ZERO before the first call
- *            (e.g. one cudaMemsetAsync at allocation); every call leaves them zero.  A
- *            workspace serves one chain at a time (do not share it between streams).
+ *            8192 bytes hold the grid-barrier words (a launch epoch and one arrival flag per
+ *            CTA): they must be ZERO before the first call (e.g. one cudaMemsetAsync at
+ *            allocation); every call advances the epoch, so they never need resetting.  A
+ *            workspace serves one stream at a time (calls on it must be stream-ordered).
  * A stage's x must not be written by a LATER stage of the same chain (it is read after the
  * earlier stages only).  Asynchronous, no allocation.  Errors: as paro_linear_multi, plus
  * PARO_ERR_UNSUPPORTED for B > 16. */

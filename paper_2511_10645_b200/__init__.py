@@ -24,6 +24,7 @@ PARO_LINEAR_NO_ROTATION = 0x1
 PARO_LINEAR_PDL = 0x2
 PARO_LINEAR_FORCE_GEMV = 0x4
 PARO_LINEAR_FORCE_GEMM = 0x8
+PARO_LINEAR_TCGEN05 = 0x10
 GROUP = 128
 SLOTS = 64
 

@@ -52,11 +52,33 @@
 
 namespace paro {
 
-namespace {
-#ifndef G1_NWARPS
-#define G1_NWARPS 16
+#ifndef PARO_TIMELINE
+#define PARO_TIMELINE 0  // 1: %globaltimer marks per (CTA, stage, event) for tools/timeline_chain.py
 #endif
-constexpr int G1_NW = G1_NWARPS;  // compute warps per CTA (+ 1 producer warp)
+#if PARO_TIMELINE
+__device__ unsigned long long g_tl[1024 * 16 * 8];
+extern "C" int paro_debug_timeline(unsigned long long* host, int n) {
+  if (n > 1024 * 16 * 8) n = 1024 * 16 * 8;
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_tl, sizeof(unsigned long long) * n));
+}
+#endif
+__device__ __forceinline__ void tl_mark(int s, int ev) {
+#if PARO_TIMELINE
+  if (blockIdx.x < 1024 && s < 16) g_tl[(blockIdx.x * 16 + s) * 8 + ev] = globaltimer_ns();
+#else
+  (void)s;
+  (void)ev;
+#endif
+}
+
+namespace {
+// compute warps per CTA (+ 1 producer warp).  16 warps in all keep four warps per SM
+// sub-partition and so 128 registers per thread (17 warps would cap it at 96 and spill); B > 1
+// uses three warpgroups of four for the tensor-core tiles.
+#ifndef G1_NW1
+#define G1_NW1 15
+#endif
+__host__ __device__ constexpr int g1_nw(int BT, bool um) { return BT > 1 && um ? 12 : G1_NW1; }
 constexpr uint32_t TILE_B = TILE_CODE_BYTES + TILE_SCALE_BYTES + TILE_ZERO_BYTES;
 
 // D(16x8 s32) += A(16x32 u8, row) * B(32x8 s8, col); fragments as in ptx.cuh (imma_16832),
@@ -82,7 +104,7 @@ struct G1Geom {
 // B = 1: a batch is TPS consecutive tiles of the sequence (row block, group).  B > 1: a batch
 // is (row-block quad q, group chunk c): the tiles (4 q + j, gamma) for j < 4 and gamma in chunk
 // c of TPS / 4 groups, stored j-major (the four row blocks of one group form one M = 128 MMA).
-__device__ __forceinline__ G1Geom g1_geom(const Gemv1Stage& S, int CL, int crank, int TPS, bool quads) {
+__device__ __forceinline__ G1Geom g1_geom(const Gemv1Stage& S, int lgCL, int crank, int TPS, bool quads) {
   G1Geom g{};
   const int bx = static_cast<int>(blockIdx.x);
   g.active = bx < S.n_cta;
@@ -92,12 +114,12 @@ __device__ __forceinline__ G1Geom g1_geom(const Gemv1Stage& S, int CL, int crank
   while (li + 1 < S.n_lin && bx >= S.lin[li + 1].cta_begin) ++li;
   g.li = li;
   const Gemv1Linear& d = S.lin[li];
-  const int cl = (bx - d.cta_begin) / CL;
+  const int cl = (bx - d.cta_begin) >> lgCL;  // cluster sizes are powers of two
   const int nrb = d.rb_base + (cl < d.rb_extra ? 1 : 0);
   g.rb0 = cl * d.rb_base + min(cl, d.rb_extra);
   g.R = nrb * TILE_ROWS;
-  g.ga = crank * S.G / CL;
-  g.gc = (crank + 1) * S.G / CL - g.ga;
+  g.ga = (crank * S.G) >> lgCL;
+  g.gc = (((crank + 1) * S.G) >> lgCL) - g.ga;
   g.n_tiles = nrb * g.gc;
   g.nrb = nrb;
   if (quads) {
@@ -107,7 +129,7 @@ __device__ __forceinline__ G1Geom g1_geom(const Gemv1Stage& S, int CL, int crank
   } else {
     g.n_batches = (g.n_tiles + TPS - 1) / TPS;
   }
-  g.RR = (g.R + CL - 1) / CL;
+  g.RR = (g.R + (1 << lgCL) - 1) >> lgCL;
   g.my_lo = crank * g.RR;
   g.my_n = max(0, min(g.RR, g.R - g.my_lo));
   return g;
@@ -208,11 +230,12 @@ __device__ __forceinline__ void g1_params(const Gemv1Linear& d, int gam, int L, 
   sv = rotate ? __ldg(reinterpret_cast<const float4*>(d.svec + gam * 128) + lane) : make_float4(1.f, 1.f, 1.f, 1.f);
 }
 
-// x of token b, channels 4 lane .. 4 lane + 3 of group gam (L2-coherent load: x may have been
-// written earlier in this launch by another SM)
-__device__ __forceinline__ uint2 g1_ldx(const void* x, int64_t K, int b, int gam, int lane) {
-  return __ldcg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(x) +
-                                               (static_cast<int64_t>(b) * K + gam * 128 + 4 * lane) * 2));
+// x of token b, channels 4 lane .. 4 lane + 3 of group gam.  coherent: x may have been written
+// earlier in this launch by another SM (a later chain stage): L2 load; else the read-only path.
+__device__ __forceinline__ uint2 g1_ldx(const void* x, int64_t K, int b, int gam, int lane, bool coherent) {
+  const uint2* p = reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(x) +
+                                                  (static_cast<int64_t>(b) * K + gam * 128 + 4 * lane) * 2);
+  return coherent ? __ldcg(p) : __ldg(p);
 }
 
 // B > 1: x' of one (group, token) as fixed point + s8 digits in the UMMA B-operand layout of the
@@ -255,10 +278,10 @@ __device__ __forceinline__ int2 g1_digits_umma(float* sc, int lane, uint8_t* grp
 
 // B > 1: one transform task = (linear, group, set of four tokens) -> digits + (sum, scale) in the
 // linear's xq / xqs buffers (the layout the GEMV bulk-copies)
-template <int BT>
+template <int BT, bool UM>
 __device__ __forceinline__ void g1_xform_task(const Gemv1Stage& S, int task, int B, int x_bf16, int rotate, float* scr,
                                               int lane, bool wait_pdl) {
-  constexpr int NB = BT / 4, XPG = 2 * BT * 128;  // UMMA B tile of a group: 2 BT rows x 128 B
+  constexpr int NB = BT / 4, XPC = 4 * 8 * 32, XPG = NB * XPC;  // = 2 BT rows x 128 B (UMMA B tile)
   const int G = S.G;
   const int li = task / (G * NB), rem = task - li * G * NB, gam = rem / NB, set = rem - gam * NB;
   const Gemv1Linear& d = S.lin[li];
@@ -270,13 +293,15 @@ __device__ __forceinline__ void g1_xform_task(const Gemv1Stage& S, int task, int
   const int b0 = set * 4;
   uint2 xv[4];
 #pragma unroll
-  for (int tb = 0; tb < 4; ++tb) xv[tb] = (b0 + tb < B) ? g1_ldx(S.x, S.K, b0 + tb, gam, lane) : make_uint2(0u, 0u);
+  for (int tb = 0; tb < 4; ++tb) xv[tb] = (b0 + tb < B) ? g1_ldx(S.x, S.K, b0 + tb, gam, lane, !wait_pdl) : make_uint2(0u, 0u);
   g1_scale<4>(scr, xv, x_bf16, sv, lane);
   g1_rot<4>(scr, cs, ix, L);
   uint8_t* xq = d.xq + static_cast<size_t>(gam) * XPG;
 #pragma unroll
   for (int tb = 0; tb < 4; ++tb) {
-    const int2 r = g1_digits_umma(scr + tb * 128, lane, xq, b0 + tb);
+    // tcgen05 engine: the group's UMMA B tile; mma.sync engine: the column set's B fragments
+    const int2 r = UM ? g1_digits_umma(scr + tb * 128, lane, xq, b0 + tb)
+                      : g1_digits<8>(scr + tb * 128, lane, xq + set * XPC, tb);
     if (lane == 0) d.xqs[static_cast<size_t>(gam) * BT + b0 + tb] = r;
   }
 }
@@ -285,8 +310,10 @@ __device__ __forceinline__ void g1_xform_task(const Gemv1Stage& S, int task, int
 
 // NW compute warps + 1 producer warp (17 warps: up to 96 registers per thread).
 // BT: token capacity of the instance (1, 4, 8, 16).  MS: stage capacity of the argument block.
-template <int NW, int BT, int MS>
+// UM_: B > 1 tiles on the tcgen05 tensor cores (kind::i8, TMEM) instead of warp-level mma.sync.
+template <int NW, int BT, int MS, bool UM_>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __grid_constant__ Gemv1ArgsT<MS> a) {
+  constexpr bool UM = BT > 1 && UM_;
   constexpr int TB = BT == 1 ? 1 : 4;          // tokens per MMA column set
   constexpr int NB = (BT + 3) / 4;             // column sets
   constexpr int NCOL = BT == 1 ? 2 : 8;        // B columns holding digits
@@ -296,7 +323,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
   (void)TB;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   // 1024-byte aligned base (the UMMA B tiles use the 128-byte swizzle); the plan reserves the slack
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  // tcgen05 engine: 1024-byte aligned base (the UMMA B tiles use the 128-byte swizzle; the plan
+  // reserves the slack)
+  uint8_t* smem = UM ? smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) : smem_raw;
+  static_assert(NW % 4 == 0 || !UM, "the tcgen05 engine needs whole warpgroups");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int CL = static_cast<int>(cluster_nctarank());
   const int crank = static_cast<int>(cluster_ctarank());
@@ -311,29 +341,35 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
   uint64_t* empty = full + a.S;
   uint64_t* rbar = empty + a.S;  // cluster partials of my rows landed (st.async bytes), one phase per stage
   uint64_t* xbar = rbar + 1;     // BT > 1: the pre-transformed x' slice landed
-  uint64_t* mdone = xbar + 1;    // BT > 1: [4] the warpgroup's MMAs completed (tcgen05.commit)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mdone + 4);  // BT > 1: TMEM base address
+  uint64_t* mdone = xbar + 1;    // BT > 1: [warpgroup][2 buffers] the MMAs completed (tcgen05.commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mdone + 8);  // BT > 1: TMEM base address
   uint8_t* ring = smem + a.off_ring;
-  // this CTA's share of every stage (read from shared memory where used: keeps registers free)
+  // this CTA's share of every stage (read from shared memory where used: keeps registers free);
+  // the stages' shares are computed in parallel by threads 0 .. n_stages - 1 while warp 1 sets up
+  // the barriers (nothing serial on the launch's critical path)
   __shared__ G1Geom sgeo[MS];
-  if (tid < a.n_stages) sgeo[tid] = g1_geom(a.st[tid], CL, crank, a.TPS, BT > 1);
+  const int lgCL = __ffs(CL) - 1;
+  if (tid < a.n_stages) sgeo[tid] = g1_geom(a.st[tid], lgCL, crank, a.TPS, UM);
 
   if (tid < 8) reinterpret_cast<uint32_t*>(smem + a.off_xs - 32)[tid] = 0u;
-  if (tid == 0) {
+  if (tid == 32) {
     for (int i = 0; i < a.S; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], NW);
     }
     mbar_init(rbar, 1);
     mbar_init(xbar, 1);
-    for (int i = 0; i < 4; ++i) mbar_init(&mdone[i], 1);
-    if (CL > 1) mbar_arrive_expect_tx(rbar, static_cast<uint32_t>((CL - 1) * g1_geom(a.st[0], CL, crank, a.TPS, BT > 1).my_n * BT * 4));
+    for (int i = 0; i < 8; ++i) mbar_init(&mdone[i], 1);
     fence_mbar_init();
   }
-  if (BT > 1 && warp == 0) tmem_alloc(tmem_slot, 512);  // 4 warpgroups x (A 32 + D 2 BT columns), whole TMEM
-  tc_fence_before();
+  if (UM && warp == 2) tmem_alloc(tmem_slot, 512);  // 3 warpgroups x (2 A + 2 D buffers) <= 512 columns
+  if constexpr (UM) tc_fence_before();
   __syncthreads();
-  tc_fence_after();
+  if constexpr (UM) tc_fence_after();
+  // stage 0's cluster partials of my rows (the arm may follow remote bytes: the phase cannot
+  // complete before this arrival)
+  if (tid == 0 && CL > 1) mbar_arrive_expect_tx(rbar, static_cast<uint32_t>((CL - 1) * sgeo[0].my_n * BT * 4));
+  if (tid == 0) tl_mark(0, 0);
   if (CL > 1) cluster_arrive_relaxed();  // every CTA's mbarriers are initialised (DSMEM legal after the wait)
   if (a.pdl) pdl_launch_dependents();
 
@@ -359,6 +395,42 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
       released = true;
     };
     if (a.params_first) named_bar_sync(3, (NW + 1) * 32);  // the rotation-parameter loads are out
+    // the segments of batch bt of a stage: bulk copies into a ring slot, or L2 prefetches (dst NULL)
+    auto batch = [&](const G1Geom& g, const Gemv1Linear& d, int G, int bt, uint8_t* dst, uint64_t* bar) {
+      auto seg = [&](uint32_t i0, int64_t T, uint32_t n) {
+        if (dst) {
+          bulk_g2s(dst + i0 * TILE_CODE_BYTES, d.codes + T * TILE_CODE_BYTES, n * TILE_CODE_BYTES, bar, pol);
+          bulk_g2s(dst + a.sc_off + i0 * TILE_SCALE_BYTES, d.scales + T * TILE_SCALE_BYTES, n * TILE_SCALE_BYTES,
+                   bar, pol);
+          bulk_g2s(dst + a.z_off + i0 * TILE_ZERO_BYTES, d.zeros + T * TILE_ZERO_BYTES, n * TILE_ZERO_BYTES, bar,
+                   pol);
+        } else {
+          prefetch_l2_bulk(d.codes + T * TILE_CODE_BYTES, n * TILE_CODE_BYTES);
+          prefetch_l2_bulk(d.scales + T * TILE_SCALE_BYTES, n * TILE_SCALE_BYTES);
+          prefetch_l2_bulk(d.zeros + T * TILE_ZERO_BYTES, n * TILE_ZERO_BYTES);
+        }
+      };
+      if constexpr (!UM) {
+        const int u0 = bt * a.TPS, u1 = min(g.n_tiles, u0 + a.TPS);
+        if (dst) mbar_arrive_expect_tx(bar, static_cast<uint32_t>(u1 - u0) * TILE_B);
+#pragma unroll 1
+        for (int u = u0; u < u1;) {  // one contiguous segment per row block touched
+          const int rb = u / g.gc, ue = min(u1, (rb + 1) * g.gc);
+          seg(static_cast<uint32_t>(u - u0), static_cast<int64_t>(g.rb0 + rb) * G + g.ga + (u - rb * g.gc),
+              static_cast<uint32_t>(ue - u));
+          u = ue;
+        }
+      } else {
+        // (quad q, chunk c): one contiguous segment of mm tiles per row block 4 q + j
+        const int m = a.TPS / 4, q = bt / g.nch, c = bt - q * g.nch;
+        const int mm = min(m, g.gc - c * m), nq = min(4, g.nrb - 4 * q);
+        if (dst) mbar_arrive_expect_tx(bar, static_cast<uint32_t>(nq * mm) * TILE_B);
+#pragma unroll 1
+        for (int j = 0; j < nq; ++j)
+          seg(static_cast<uint32_t>(j * mm), static_cast<int64_t>(g.rb0 + 4 * q + j) * G + g.ga + c * m,
+              static_cast<uint32_t>(mm));
+      }
+    };
     int slot = 0, phase = 0, nb = 0;
 #pragma unroll 1
     for (int s = 0; s < a.n_stages; ++s) {
@@ -366,46 +438,22 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
       const G1Geom& g = sgeo[s];
       const Gemv1Linear& d = S.lin[g.li];
       const int G = S.G;
+      if (s > 0) {
+        // Stage boundary.  The ring drains while the compute warps finish stage s - 1, pass the
+        // grid barrier and load this stage's x: bulk copies issued now would sit in front of
+        // those latency-critical loads (an SM's requests are served in order), so this stage's
+        // first batches go to L2 as prefetches (no data returns to the SM), and the ring refill
+        // -- from L2 -- starts once the compute warps' x loads are out.
+        if (lane == 0)
+          for (int bt = 0; bt < min(g.n_batches, a.l2_batches); ++bt) batch(g, d, G, bt, nullptr, nullptr);
+        __syncwarp();
+        if (a.xfirst) named_bar_sync(2, (NW + 1) * 32);
+      }
 #pragma unroll 1
       for (int bt = 0; bt < g.n_batches; ++bt) {
         if (s == 0 && bt == pre) release(S, g);
         if (nb >= a.S) mbar_wait(&empty[slot], phase ^ 1);
-        if (lane == 0) {
-          uint8_t* dst = ring + static_cast<size_t>(slot) * a.slot_bytes;
-          if constexpr (BT == 1) {
-            const int u0 = bt * a.TPS, u1 = min(g.n_tiles, u0 + a.TPS);
-            mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(u1 - u0) * TILE_B);
-#pragma unroll 1
-            for (int u = u0; u < u1;) {  // one contiguous segment per row block touched
-              const int rb = u / g.gc, ue = min(u1, (rb + 1) * g.gc);
-              const int64_t T = static_cast<int64_t>(g.rb0 + rb) * G + g.ga + (u - rb * g.gc);
-              const uint32_t i0 = static_cast<uint32_t>(u - u0), n = static_cast<uint32_t>(ue - u);
-              u = ue;
-              bulk_g2s(dst + i0 * TILE_CODE_BYTES, d.codes + T * TILE_CODE_BYTES, n * TILE_CODE_BYTES, &full[slot],
-                       pol);
-              bulk_g2s(dst + a.sc_off + i0 * TILE_SCALE_BYTES, d.scales + T * TILE_SCALE_BYTES,
-                       n * TILE_SCALE_BYTES, &full[slot], pol);
-              bulk_g2s(dst + a.z_off + i0 * TILE_ZERO_BYTES, d.zeros + T * TILE_ZERO_BYTES, n * TILE_ZERO_BYTES,
-                       &full[slot], pol);
-            }
-          } else {
-            // (quad q, chunk c): one contiguous segment of mm tiles per row block 4 q + j
-            const int m = a.TPS / 4, q = bt / g.nch, c = bt - q * g.nch;
-            const int mm = min(m, g.gc - c * m), nq = min(4, g.nrb - 4 * q);
-            mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(nq * mm) * TILE_B);
-#pragma unroll 1
-            for (int j = 0; j < nq; ++j) {
-              const int64_t T = static_cast<int64_t>(g.rb0 + 4 * q + j) * G + g.ga + c * m;
-              const uint32_t i0 = static_cast<uint32_t>(j * mm), n = static_cast<uint32_t>(mm);
-              bulk_g2s(dst + i0 * TILE_CODE_BYTES, d.codes + T * TILE_CODE_BYTES, n * TILE_CODE_BYTES, &full[slot],
-                       pol);
-              bulk_g2s(dst + a.sc_off + i0 * TILE_SCALE_BYTES, d.scales + T * TILE_SCALE_BYTES,
-                       n * TILE_SCALE_BYTES, &full[slot], pol);
-              bulk_g2s(dst + a.z_off + i0 * TILE_ZERO_BYTES, d.zeros + T * TILE_ZERO_BYTES, n * TILE_ZERO_BYTES,
-                       &full[slot], pol);
-            }
-          }
-        }
+        if (lane == 0) batch(g, d, G, bt, ring + static_cast<size_t>(slot) * a.slot_bytes, &full[slot]);
         __syncwarp();
         ++nb;
         if (++slot == a.S) {
@@ -413,6 +461,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
           phase ^= 1;
         }
       }
+      if (lane == 0) tl_mark(s, 7);
       if (s == 0 && !released) release(S, g);
     }
     if (CL > 1) cluster_wait();
@@ -421,16 +470,17 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
 
   // ------------------------------------------------------------ compute warps
   int slot = 0, phase = 0, xuse = 0;
-  uint32_t gen = 0;  // thread 0: generation of the last grid barrier it arrived at
-  // all compute warps wait until every CTA has passed the last grid barrier (thread 0 polls)
+  uint32_t mma_it = 0;  // BT > 1: this warpgroup's MMA items so far (buffer and barrier parity; continues across stages)
+  // grid barrier: warp 0 knows the launch epoch (64 e); every compute thread counts barriers
+  const GridBar gb{a.gbar, a.gbar + 16};
+  uint32_t ep = 0;
+  uint32_t nbar = 0;
+  auto arrive_grid = [&]() {  // after a CTA barrier over the compute warps
+    ++nbar;
+    if (tid == 0) grid_arrive(gb, ep + nbar);
+  };
   auto wait_grid = [&]() {
-    if (warp == 0) {
-      if (lane == 0) {
-        grid_wait(a.gbar, gen);
-        __threadfence();
-      }
-      __syncwarp();
-    }
+    if (warp == 0 && !a.nobar) grid_wait_warp(gb, ep + nbar, lane);
     named_bar_sync(4, NW * 32);
   };
 #pragma unroll 1
@@ -454,6 +504,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
         if (a.params_first) named_bar_arrive(3, (NW + 1) * 32);
         named_bar_arrive(2, (NW + 1) * 32);
         if (a.pdl) pdl_wait();
+        if (warp == 0 && a.n_stages > 1) ep = ld_relaxed_gpu(gb.epoch) << 6;
       } else {
         wait_grid();
         if (S.xq_in_kernel) {
@@ -464,10 +515,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
 #pragma unroll 1
           for (int task = static_cast<int>(blockIdx.x) * NW + warp; task < n_tasks;
                task += static_cast<int>(gridDim.x) * NW)
-            g1_xform_task<BT>(S, task, B, a.x_bf16, a.rotate, scr, lane, false);
+            g1_xform_task<BT, UM>(S, task, B, a.x_bf16, a.rotate, scr, lane, false);
           asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> bulk-copy reads
           named_bar_sync(1, NW * 32);
-          if (tid == 0) gen = grid_arrive(a.gbar, gridDim.x);
+          arrive_grid();
           wait_grid();
         }
         if (g.active && tid == 0) {
@@ -476,11 +527,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
           bulk_g2s_nohint(xp, d.xq + static_cast<size_t>(ga) * XPG, nd, xbar);
           bulk_g2s_nohint(xs, d.xqs + static_cast<size_t>(ga) * BT, ns, xbar);
         }
+        if (a.xfirst) named_bar_arrive(2, (NW + 1) * 32);  // the x' slice is requested: the ring refill may start
       }
       if (g.active) {
         mbar_wait(xbar, xuse & 1);
         ++xuse;
       }
+      if (tid == 0) tl_mark(s, 1);
     } else {
       float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * 128;
       const int L = a.rotate ? d.L : 0;
@@ -508,15 +561,17 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
           named_bar_arrive(3, (NW + 1) * 32);
         }
         if (a.pdl) pdl_wait();
+        if (warp == 0 && a.n_stages > 1) ep = ld_relaxed_gpu(gb.epoch) << 6;
       } else {
         wait_grid();
       }
-      bool arrived = s != 0;
+      if (tid == 0) tl_mark(s, 1);
+      bool arrived = s != 0 && !a.xfirst;
 #pragma unroll 1
       for (int gg = warp; mine && gg < gc; gg += NW) {
         const int gam = ga + gg;
         if (gg != warp) g1_params(d, gam, L, a.rotate, lane, cs, ix, sv);
-        uint2 xv[1] = {g1_ldx(S.x, S.K, 0, gam, lane)};
+        uint2 xv[1] = {g1_ldx(S.x, S.K, 0, gam, lane, s != 0)};
         g1_scale<1>(scr, xv, a.x_bf16, sv, lane);
         if (!arrived) {
           named_bar_arrive(2, (NW + 1) * 32);  // my x and parameters are in
@@ -530,6 +585,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
       if (!arrived) named_bar_arrive(2, (NW + 1) * 32);
     }
     named_bar_sync(1, NW * 32);  // every x' of the CTA is in shared memory (and part zeroed)
+    if (tid == 0) tl_mark(s, 2);
 
     // ---------------------------------------------------------- phase 2: tiles (a6)
     if constexpr (BT == 1) {
@@ -543,6 +599,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
         // batch tiles [u0, u1): tile i is (row block r_lo + ri, group ga + gi) with (ri, gi) = divmod(off0 + i, gc)
         const int u0 = bt * a.TPS, nt = min(g.n_tiles, u0 + a.TPS) - u0;
         mbar_wait(&full[slot], phase);
+        if (bt == 0 && tid == 0) tl_mark(s, 3);
         const uint8_t* sb = ring + static_cast<size_t>(slot) * a.slot_bytes;
         int ri = 0, gi = off0 + warp;  // tile warp + k NW of the batch
         while (gi >= gc) {
@@ -613,15 +670,118 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
           ++r_lo;
         }
       }
+    } else if constexpr (!UM) {
+      // B > 1 on the warp-level integer tensor cores: warp w takes a contiguous chunk of the batch's
+      // tiles (row block ri, group gi), so that its consecutive tiles mostly share a row block and
+      // the row partials (shared-memory atomics) are added once per row block; column sets of four
+      // tokens (hi / lo digits in the MMA's 8 columns)
+      const int gq = lane >> 2, tq = lane & 3;
+      int r_lo = 0, off0 = 0;
+#pragma unroll 1
+      for (int bt = 0; bt < g.n_batches; ++bt) {
+        const int u0 = bt * a.TPS, nt = min(g.n_tiles, u0 + a.TPS) - u0;
+        mbar_wait(&full[slot], phase);
+        if (bt == 0 && tid == 0) tl_mark(s, 3);
+        const uint8_t* sb = ring + static_cast<size_t>(slot) * a.slot_bytes;
+        const int per = (nt + NW - 1) / NW;
+        const int i_end = min(nt, (warp + 1) * per);
+        int i = warp * per;
+        int ri = (off0 + i) / gc, gi = off0 + i - ri * gc;
+        float acc[NB][4];
+        int acc_ri = -1;
+        auto flush = [&]() {
+          if (acc_ri < 0) return;
+          const int rowl = (r_lo + acc_ri) * TILE_ROWS + gq;  // cluster-local row of q = 0
+#pragma unroll
+          for (int set = 0; set < NB; ++set) {
+            const int b = set * 4 + tq;
+            if (b < B) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) atomicAdd(part + (rowl + 8 * q) * BT + b, acc[set][q]);
+            }
+          }
+        };
+#pragma unroll 1
+        for (; i < i_end; ++i) {
+          if (ri != acc_ri) {
+            flush();
+            acc_ri = ri;
+#pragma unroll
+            for (int set = 0; set < NB; ++set)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) acc[set][q] = 0.f;
+          }
+          const uint8_t* tc = sb + i * TILE_CODE_BYTES + gq * 64 + tq * 16;
+          uint4 w[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) w[q] = *reinterpret_cast<const uint4*>(tc + q * 512);
+          const uint2 sp = *reinterpret_cast<const uint2*>(sb + a.sc_off + i * TILE_SCALE_BYTES + gq * 8);
+          const uint32_t zw = *reinterpret_cast<const uint16_t*>(sb + a.z_off + i * TILE_ZERO_BYTES + gq * 2);
+          const float2 Sa = __half22float2(*reinterpret_cast<const __half2*>(&sp.x));  // rows gq, gq + 8
+          const float2 Sb = __half22float2(*reinterpret_cast<const __half2*>(&sp.y));  // rows gq + 16, gq + 24
+          const float Sr[4] = {Sa.x, Sa.y, Sb.x, Sb.y};
+#pragma unroll
+          for (int set = 0; set < NB; ++set) {
+            if (set * 4 >= B) break;
+            uint4 bA = make_uint4(0u, 0u, 0u, 0u), bB = bA;  // B fragments (columns >= NCOL are zero)
+            if (gq < NCOL) {
+              const uint8_t* bp = xp + gi * XPG + set * XPC + tq * XTQ + gq * 32;
+              bA = *reinterpret_cast<const uint4*>(bp);
+              bB = *reinterpret_cast<const uint4*>(bp + 16);
+            }
+            constexpr uint32_t ML = 0x0f0f0f0fu, MH = 0xf0f0f0f0u;
+            int Dl[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}}, Dh[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {  // rows gq + 16 hh (w[2 hh]) and gq + 16 hh + 8 (w[2 hh + 1])
+              const uint4 r0 = w[2 * hh], r1 = w[2 * hh + 1];
+              mma_u8s8(Dl[hh], r0.x & ML, r1.x & ML, r0.y & ML, r1.y & ML, bA.x, bA.y);
+              mma_u8s8(Dl[hh], r0.z & ML, r1.z & ML, r0.w & ML, r1.w & ML, bA.z, bA.w);
+              mma_u8s8(Dh[hh], r0.x & MH, r1.x & MH, r0.y & MH, r1.y & MH, bB.x, bB.y);
+              mma_u8s8(Dh[hh], r0.z & MH, r1.z & MH, r0.w & MH, r1.w & MH, bB.z, bB.w);
+            }
+            // lane (gq, tq) holds columns 2 tq (hi) and 2 tq + 1 (lo) = token tq of the set, rows gq + 8 q
+            const int b = set * 4 + tq;
+            if (b < B) {
+              const int2 xf = xs[gi * BT + b];
+              const float F = __int_as_float(xf.y);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int hh = q >> 1, e = (q & 1) * 2;
+                const int zq = static_cast<int>((zw >> (4 * q)) & 15u);
+                const int I = Dl[hh][e] * 256 + Dl[hh][e + 1] + ((Dh[hh][e] * 256 + Dh[hh][e + 1]) >> 4) - zq * xf.x;
+                acc[set][q] = fmaf(Sr[q] * F, static_cast<float>(I), acc[set][q]);
+              }
+            }
+          }
+          if (++gi == gc) {
+            gi = 0;
+            ++ri;
+          }
+        }
+        flush();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (++slot == a.S) {
+          slot = 0;
+          phase ^= 1;
+        }
+        off0 += a.TPS;
+        while (off0 >= gc) {
+          off0 -= gc;
+          ++r_lo;
+        }
+      }
     } else {
       // B > 1: 5th-generation tensor cores.  Warpgroup wg (warps 4 wg .. 4 wg + 3) takes the
-      // groups gi = wg, wg + 4, .. of each batch; per group, its warp j writes the A operand of
-      // row block 4 q + j into TMEM lanes 32 j .. 32 j + 31 (one row per lane: the row's 16 code
-      // words, low nibbles AND 0x0F0F0F0F and high nibbles >> 4 AND 0x0F0F0F0F = the u8 codes of
-      // 128 channels, no conversion), one thread issues four tcgen05.mma.kind::i8 (M = 128 rows,
-      // N = 2 B token digits, K = 32 each; u8 codes x s8 digits -> exact s32 in TMEM), and every
-      // lane reads its row back: I = 256 D_hi + D_lo - z X per token, y_row += S 2^(E-14) I in
-      // registers across the CTA's groups; one shared-memory atomic per (row, token) per quad.
+      // groups gi = wg, wg + 3, .. of each batch; per group (an "item": 128 rows x 128 channels),
+      // its warp j writes the A operand of row block 4 q + j into TMEM lanes 32 j .. 32 j + 31 (one
+      // row per lane: the row's 16 code words, low nibbles AND 0x0F0F0F0F and high nibbles >> 4
+      // AND 0x0F0F0F0F = the u8 codes of 128 channels, no conversion), one thread issues four
+      // tcgen05.mma.kind::i8 (M = 128 rows, N = 2 B token digits, K = 32 each; u8 codes x s8
+      // digits -> exact s32 in TMEM), and every lane reads its row back: I = 256 D_hi + D_lo - z X
+      // per token, y_row += S 2^(E-14) I in registers across the CTA's groups; one shared-memory
+      // atomic per (row, token) per quad.  Two A / D buffers per warpgroup: the A fill and MMA of
+      // item i overlap the read-back of item i - 1.
       constexpr int NC = 2 * BT;  // MMA N: (token, digit) columns
       constexpr uint32_t IDESC = (2u << 4)                                    // D: s32
                                  | (0u << 7) | (1u << 10)                     // A: u8, B: s8
@@ -629,13 +789,17 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
                                  | (static_cast<uint32_t>(128 >> 4) << 24);   // M >> 4
       const int wg = warp >> 2, wq = warp & 3;
       const uint32_t tbase = *tmem_slot + static_cast<uint32_t>(wg * 128);  // this warpgroup's columns
-      const uint32_t tA = tbase, tD = tbase + 32, lane_off = static_cast<uint32_t>(wq * 32) << 16;
+      const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
       const int m = a.TPS / 4;
       const int swz = (lane >> 1) & 3;  // conflict-free row reads: chunk k ^ swz at step k
       float acc[BT];
 #pragma unroll
       for (int b = 0; b < BT; ++b) acc[b] = 0.f;
-      int cur_q = -1, mph = 0;
+      int cur_q = -1;
+      // the item whose MMA is in flight
+      int pend_gi = -1, pend_q = 0, pend_z = 0;
+      uint32_t pend_it = 0;
+      float pend_S = 0.f;
       auto flush = [&](int q) {
         const int nq = min(4, g.nrb - 4 * q);
         if (wq < nq) {
@@ -647,20 +811,41 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
 #pragma unroll
         for (int b = 0; b < BT; ++b) acc[b] = 0.f;
       };
+      auto epilogue = [&]() {  // read back the pending item and accumulate
+        const uint32_t buf = pend_it & 1u;
+        mbar_wait_spin(&mdone[wg * 2 + buf], (pend_it >> 1) & 1u);
+        tc_fence_after();
+        uint32_t dv[NC];
+        tmem_ld_cols<NC>(tbase + 64 + NC * buf + lane_off, dv);
+        tmem_ld_wait();
+        if (pend_q != cur_q) {
+          if (cur_q >= 0) flush(cur_q);
+          cur_q = pend_q;
+        }
+        // tokens >= B have x' = 0 (digits 0, sum 0): their columns add exactly 0
+        const int4* xq4 = reinterpret_cast<const int4*>(xs + pend_gi * BT);
+#pragma unroll
+        for (int b = 0; b < BT; b += 2) {
+          const int4 xf = xq4[b >> 1];  // (X, F) of tokens b and b + 1
+          const int I0 = static_cast<int>(dv[2 * b]) * 256 + static_cast<int>(dv[2 * b + 1]) - pend_z * xf.x;
+          const int I1 = static_cast<int>(dv[2 * b + 2]) * 256 + static_cast<int>(dv[2 * b + 3]) - pend_z * xf.z;
+          acc[b] = fmaf(pend_S * __int_as_float(xf.y), static_cast<float>(I0), acc[b]);
+          acc[b + 1] = fmaf(pend_S * __int_as_float(xf.w), static_cast<float>(I1), acc[b + 1]);
+        }
+        pend_gi = -1;
+      };
 #pragma unroll 1
       for (int bt = 0; bt < g.n_batches; ++bt) {
         const int q = bt / g.nch, c = bt - q * g.nch;
         const int mm = min(m, gc - c * m), nq = min(4, g.nrb - 4 * q);
-        if (q != cur_q) {
-          if (cur_q >= 0) flush(cur_q);
-          cur_q = q;
-        }
         mbar_wait(&full[slot], phase);
+        if (bt == 0 && tid == 0) tl_mark(s, 3);
         const uint8_t* sb = ring + static_cast<size_t>(slot) * a.slot_bytes;
 #pragma unroll 1
-        for (int gl = wg; gl < mm; gl += 4) {
-          const int gi = c * m + gl;  // CTA-local group
+        for (int gl = wg; gl < mm; gl += NW / 4) {
+          const int gi = c * m + gl;    // CTA-local group
           const int ti = wq * mm + gl;  // tile of (row block 4 q + wq, group gi) in the batch
+          const uint32_t buf = mma_it & 1u;
           uint32_t av[32];
           float Srow = 0.f;
           int zrow = 0;
@@ -702,44 +887,40 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
 #pragma unroll
             for (int k = 0; k < 32; ++k) av[k] = 0u;
           }
-          tmem_st32(tA + lane_off, av);
+          tmem_st32(tbase + 32 * buf + lane_off, av);
           tmem_st_wait();
           tc_fence_before();
-          named_bar_sync(5 + wg, 128);  // A complete; the previous D read back by every warp
+          // A complete; every warp has read back the item that last used these buffers
+          named_bar_sync(5 + wg, 128);
           if (wq == 0 && lane == 0) {
             tc_fence_after();
             const uint64_t bd = smem_desc_sw128(xp + gi * XPG);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) mma_i8_ts(tD, tA + 8 * kk, bd + 2 * kk, IDESC, kk > 0 ? 1u : 0u);
-            mma_commit(&mdone[wg]);
+            for (int kk = 0; kk < 4; ++kk)
+              mma_i8_ts(tbase + 64 + NC * buf, tbase + 32 * buf + 8 * kk, bd + 2 * kk, IDESC, kk > 0 ? 1u : 0u);
+            mma_commit(&mdone[wg * 2 + buf]);
           }
-          mbar_wait(&mdone[wg], mph);
-          mph ^= 1;
-          tc_fence_after();
-          uint32_t dv[NC];
-          tmem_ld_cols<NC>(tD + lane_off, dv);
-          tmem_ld_wait();
-#pragma unroll
-          for (int b = 0; b < BT; ++b) {
-            if (b < B) {
-              const int2 xf = xs[gi * BT + b];
-              const int I = static_cast<int>(dv[2 * b]) * 256 + static_cast<int>(dv[2 * b + 1]) - zrow * xf.x;
-              acc[b] = fmaf(Srow * __int_as_float(xf.y), static_cast<float>(I), acc[b]);
-            }
-          }
+          if (pend_gi >= 0) epilogue();  // the previous item, while this one multiplies
+          pend_gi = gi;
+          pend_q = q;
+          pend_S = Srow;
+          pend_z = zrow;
+          pend_it = mma_it++;
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (lane == 0) mbar_arrive(&empty[slot]);  // the batch's data is in TMEM / registers
         if (++slot == a.S) {
           slot = 0;
           phase ^= 1;
         }
       }
+      if (pend_gi >= 0) epilogue();
       if (cur_q >= 0) flush(cur_q);
     }
 
     // ---------------------------------------------------------- reduction + epilogue (a8)
     named_bar_sync(1, NW * 32);
+    if (tid == 0) tl_mark(s, 4);
     if (s == 0 && CL > 1) cluster_wait();  // every CTA of the cluster is running: DSMEM is legal
     if (g.active) {
       for (int idx = tid; idx < g.R * BT; idx += NW * 32) {
@@ -764,6 +945,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
     }
     named_bar_sync(1, NW * 32);           // my own partials are in recv
     if (g.active && CL > 1) mbar_wait(rbar, s & 1);  // and those of the other CTAs of the cluster
+    if (tid == 0) tl_mark(s, 5);
     if (g.active) {
       for (int idx = tid; idx < g.my_n * BT; idx += NW * 32) {
         const int rl = idx / BT, b = idx - rl * BT;
@@ -783,19 +965,23 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
         }
       }
     }
+    if (tid == 0) tl_mark(s, 6);
     if (s + 1 < a.n_stages) {
       named_bar_sync(1, NW * 32);  // every store (and every read of recv) of this stage is done
       if (tid == 0) {
         if (CL > 1)  // the next stage's cluster partials may land once the barrier below completes
           mbar_arrive_expect_tx(rbar, static_cast<uint32_t>((CL - 1) * sgeo[s + 1].my_n * BT * 4));
-        gen = grid_arrive(a.gbar, gridDim.x);
       }
+      arrive_grid();
     }
   }
-  if constexpr (BT > 1) {  // every warpgroup waited for its last MMA
+  // the next launch on this workspace uses the next epoch (it reads the word only after this
+  // grid completed: PDL wait or stream order)
+  if (a.n_stages > 1 && blockIdx.x == 0 && tid == 0) st_relaxed_gpu(gb.epoch, (ep >> 6) + 1);
+  if constexpr (UM) {  // every warpgroup waited for its last MMA
     tc_fence_before();
     named_bar_sync(1, NW * 32);
-    if (warp == 0) tmem_dealloc(*tmem_slot, 512);
+    if (warp == 2) tmem_dealloc(*tmem_slot, 512);
   }
 }
 
@@ -806,7 +992,7 @@ struct Gemv1XformArgs {
   int B, x_bf16, rotate, pdl;
 };
 
-template <int BT>
+template <int BT, bool UM>
 __global__ void __launch_bounds__(128) paro_gemv1_xform_kernel(const __grid_constant__ Gemv1XformArgs a) {
   constexpr int NB = BT / 4;
   __shared__ __align__(16) float scr_all[4][4 * 128];
@@ -814,7 +1000,7 @@ __global__ void __launch_bounds__(128) paro_gemv1_xform_kernel(const __grid_cons
   if (a.pdl) pdl_launch_dependents();
   const int task = blockIdx.x * 4 + warp;
   if (task >= a.st.n_lin * a.st.G * NB) return;
-  g1_xform_task<BT>(a.st, task, a.B, a.x_bf16, a.rotate, scr_all[warp], lane, a.pdl != 0);
+  g1_xform_task<BT, UM>(a.st, task, a.B, a.x_bf16, a.rotate, scr_all[warp], lane, a.pdl != 0);
 }
 
 // ============================================================================ host side
@@ -860,22 +1046,28 @@ cudaError_t launch_gemv1_xform(const Gemv1Config& c, cudaStream_t st) {
   cfg.attrs = &at;
   cfg.numAttrs = x.pdl ? 1 : 0;
   switch (c.BT) {
-    case 4: return cudaLaunchKernelEx(&cfg, paro_gemv1_xform_kernel<4>, x);
-    case 8: return cudaLaunchKernelEx(&cfg, paro_gemv1_xform_kernel<8>, x);
-    case 16: return cudaLaunchKernelEx(&cfg, paro_gemv1_xform_kernel<16>, x);
+    case 4: return c.a.umma ? cudaLaunchKernelEx(&cfg, paro_gemv1_xform_kernel<4, true>, x)
+                            : cudaLaunchKernelEx(&cfg, paro_gemv1_xform_kernel<4, false>, x);
+    case 8: return c.a.umma ? cudaLaunchKernelEx(&cfg, paro_gemv1_xform_kernel<8, true>, x)
+                            : cudaLaunchKernelEx(&cfg, paro_gemv1_xform_kernel<8, false>, x);
+    case 16: return c.a.umma ? cudaLaunchKernelEx(&cfg, paro_gemv1_xform_kernel<16, true>, x)
+                             : cudaLaunchKernelEx(&cfg, paro_gemv1_xform_kernel<16, false>, x);
     default: return cudaErrorInvalidConfiguration;
   }
 }
 
-template <int BT, int MS>
+template <int BT, int MS, bool UM>
 static const void* g1_kernel() {
-  return reinterpret_cast<const void*>(&paro_gemv1_kernel<G1_NW, BT, MS>);
+  return reinterpret_cast<const void*>(&paro_gemv1_kernel<g1_nw(BT, UM), BT, MS, UM>);
 }
-static const void* g1_kernel_bt(int BT, bool chain) {
-  if (chain)
-    return BT == 1 ? g1_kernel<1, CHAIN_MAX_STAGES>() : BT == 4 ? g1_kernel<4, CHAIN_MAX_STAGES>()
-         : BT == 8 ? g1_kernel<8, CHAIN_MAX_STAGES>() : g1_kernel<16, CHAIN_MAX_STAGES>();
-  return BT == 1 ? g1_kernel<1, 1>() : BT == 4 ? g1_kernel<4, 1>() : BT == 8 ? g1_kernel<8, 1>() : g1_kernel<16, 1>();
+template <int MS, bool UM>
+static const void* g1_kernel_ms(int BT) {
+  return BT == 1 ? g1_kernel<1, MS, false>() : BT == 4 ? g1_kernel<4, MS, UM>() : BT == 8 ? g1_kernel<8, MS, UM>()
+                                                                                            : g1_kernel<16, MS, UM>();
+}
+static const void* g1_kernel_bt(int BT, bool chain, bool um) {
+  if (chain) return um ? g1_kernel_ms<CHAIN_MAX_STAGES, true>(BT) : g1_kernel_ms<CHAIN_MAX_STAGES, false>(BT);
+  return um ? g1_kernel_ms<1, true>(BT) : g1_kernel_ms<1, false>(BT);
 }
 
 // clusters of CL (BT-token instance) that fit in one wave, from the occupancy API (cached per
@@ -901,12 +1093,12 @@ static int g1_active_clusters_compute(const void* k, int CL, int threads, int bu
   }
   return nc;
 }
-static int g1_active_clusters(int BT, bool chain, int CL, int threads, int budget) {
-  return cached_device_int(g1_kernel_bt(BT, chain), CL, threads, budget, g1_active_clusters_compute);
+static int g1_active_clusters(int BT, bool chain, bool um, int CL, int threads, int budget) {
+  return cached_device_int(g1_kernel_bt(BT, chain, um), CL, threads, budget, g1_active_clusters_compute);
 }
 
 bool plan_gemv1_chain(int B, int n_stages, const int* n_lin, const int64_t (*Ns)[GEMV_MAX_LIN], const int64_t* Ks,
-                      int rotate, Gemv1Config* cfg, const char** why) {
+                      int rotate, int tcgen05, Gemv1Config* cfg, const char** why) {
   if (B < 1 || B > GEMV1_MAX_B) {
     *why = "1..16 tokens per decode launch";
     return false;
@@ -917,6 +1109,7 @@ bool plan_gemv1_chain(int B, int n_stages, const int* n_lin, const int64_t (*Ns)
   }
   const bool chain = n_stages > 1;
   const int BT = B == 1 ? 1 : B <= 4 ? 4 : B <= 8 ? 8 : 16;
+  const bool um = BT > 1 && tcgen05;
   const int NSET = (BT + 3) / 4;
   int Gmin = 1 << 30;
   double wbytes = 0;
@@ -955,11 +1148,11 @@ bool plan_gemv1_chain(int B, int n_stages, const int* n_lin, const int64_t (*Ns)
   CL = g1_env(chain ? "PARO_G1_CHAIN_CL" : "PARO_G1_CL", CL);
   if (CL != 1 && CL != 2 && CL != 4 && CL != 8) CL = 2;
   while (CL > 1 && CL > Gmin) CL /= 2;
-  const int NW = G1_NW;
+  const int NW = g1_nw(BT, um);
   const int threads = (NW + 1) * 32;
   c.NW = NW;
   const int budget = device_smem_optin() - 1024;
-  int ncl_max = g1_active_clusters(BT, chain, CL, threads, budget);
+  int ncl_max = g1_active_clusters(BT, chain, um, CL, threads, budget);
   ncl_max = std::min(ncl_max, std::max(1, g1_env("PARO_G1_MAXCL", 1 << 20)));
   int grid = 0, rmax_all = 0, rrmax_all = 0, gcm = 0, part_words = 0;
   int64_t cta_tiles = 0;  // tiles of the busiest CTA over the whole chain
@@ -1013,10 +1206,14 @@ bool plan_gemv1_chain(int B, int n_stages, const int* n_lin, const int64_t (*Ns)
   c.CL = CL;
   c.BT = BT;
   a.B = B;
+  a.umma = um ? 1 : 0;
   a.n_stages = n_stages;
   a.rotate = rotate;
   a.pre_stages = std::max(0, g1_env("PARO_G1_PRE", 2));
   a.params_first = g1_env("PARO_G1_PF", 1);
+  a.l2_batches = g1_env("PARO_G1_L2B", 4);
+  a.xfirst = g1_env("PARO_G1_XFIRST", 1);
+  a.nobar = g1_env("PARO_G1_NOBAR", 0);
   uint32_t off = 0;
   a.off_xp = off;
   off += g1_align(static_cast<uint32_t>(gcm) * NSET * 4 * (BT == 1 ? 2 : 8) * 32, 128);
@@ -1033,12 +1230,14 @@ bool plan_gemv1_chain(int B, int n_stages, const int* n_lin, const int64_t (*Ns)
   a.off_recv = off;
   off += g1_align(static_cast<uint32_t>(CL) * rrmax_all * BT * 4, 128);
   a.off_bar = off;
-  off += 64 * 16 + 64;  // <= 120 mbarriers (ring full / empty, rbar, xbar, 4 x mdone) + the TMEM base
+  off += 64 * 16 + 64;  // <= 128 mbarriers (ring full / empty <= 2 x 56, rbar, xbar, 8 x mdone) + the TMEM base
   a.off_ring = g1_align(off, 1024);
-  const int64_t avail = static_cast<int64_t>(budget) - 1024 - a.off_ring;  // 1024: base alignment slack
-  // batch size: the largest TPS <= 32 (two tiles per warp) that keeps >= 2 batches in flight,
-  // else the largest that fits once; measured flat between 24 and 32 tiles per batch with 2-3
-  // batches (single launches)
+  // B > 1 aligns the dynamic shared-memory base to 1024 B at run time (UMMA swizzle): reserve the slack
+  const int64_t avail = static_cast<int64_t>(budget) - (um ? 1024 : 0) - a.off_ring;
+  // batch size: the TPS that keeps the most tiles in flight (ring depth x batch size, capped by
+  // the CTA's tiles), >= 2 batches in the ring unless one holds everything; measured: the
+  // HBM stream is bound by the bytes a CTA has in flight (LLaMA-3-8B gate+up at 15 warps: 30 tiles
+  // x 2 batches 15.7 us, 28 x 3 14.0 us)
   auto slot_of = [&](int tps) {
     const uint32_t sc = static_cast<uint32_t>(tps) * TILE_CODE_BYTES;
     return g1_align(sc + static_cast<uint32_t>(tps) * (TILE_SCALE_BYTES + TILE_ZERO_BYTES), 128);
@@ -1050,9 +1249,17 @@ bool plan_gemv1_chain(int B, int n_stages, const int* n_lin, const int64_t (*Ns)
   int TPS = g1_env("PARO_G1_TPS", 0);
   if (TPS <= 0 || TPS > 64) {
     int best = 0;
-    for (int want = 2; want >= 1 && !best; --want)
-      for (int tps = 2 * NW; tps >= 8 && !best; tps -= 4)
-        if (stages_of(tps) >= std::min<int64_t>(want, (cta_tiles + tps - 1) / tps)) best = tps;
+    int64_t best_in = -1;
+    const int step = um ? 4 : 2;
+    for (int tps = (2 * NW) / step * step; tps >= 12; tps -= step) {
+      const int64_t S_ = stages_of(tps), nbat = (cta_tiles + tps - 1) / tps;
+      if (S_ < std::min<int64_t>(2, nbat)) continue;
+      const int64_t in = std::min(S_, nbat) * tps;
+      if (in > best_in) {
+        best_in = in;
+        best = tps;
+      }
+    }
     TPS = best ? best : 8;
   }
   a.TPS = TPS;
@@ -1065,7 +1272,7 @@ bool plan_gemv1_chain(int B, int n_stages, const int* n_lin, const int64_t (*Ns)
     return false;
   }
   a.S = S;
-  a.smem_total = a.off_ring + static_cast<uint32_t>(S) * a.slot_bytes + 1024;
+  a.smem_total = a.off_ring + static_cast<uint32_t>(S) * a.slot_bytes + (um ? 1024 : 0);
   if (g1_env("PARO_PLAN_DEBUG", 0))
     fprintf(stderr, "[paro gemv1 plan] B=%d BT=%d stages=%d grid=%d CL=%d NW=%d TPS=%d S=%d R_max=%d smem=%u\n", B, BT,
             n_stages, c.grid, CL, NW, TPS, S, rmax_all, a.smem_total);
@@ -1073,15 +1280,16 @@ bool plan_gemv1_chain(int B, int n_stages, const int* n_lin, const int64_t (*Ns)
   return true;
 }
 
-bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config* cfg, const char** why) {
+bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, int tcgen05, Gemv1Config* cfg,
+                const char** why) {
   int64_t ns[1][GEMV_MAX_LIN] = {};
   for (int i = 0; i < n_lin && i < GEMV_MAX_LIN; ++i) ns[0][i] = Ns[i];
-  return plan_gemv1_chain(B, 1, &n_lin, ns, &K, rotate, cfg, why);
+  return plan_gemv1_chain(B, 1, &n_lin, ns, &K, rotate, tcgen05, cfg, why);
 }
 
-template <int BT, int MS>
+template <int BT, int MS, bool UM>
 static cudaError_t g1_launch(const Gemv1Config& c, cudaLaunchConfig_t* cfg) {
-  auto kern = paro_gemv1_kernel<G1_NW, BT, MS>;
+  auto kern = paro_gemv1_kernel<g1_nw(BT, UM), BT, MS, UM>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(c.a.smem_total));
   if (e != cudaSuccess) return e;
   if constexpr (MS == CHAIN_MAX_STAGES) {
@@ -1116,13 +1324,18 @@ cudaError_t launch_gemv1(const Gemv1Config& c, cudaStream_t st) {
   cfg.attrs = attrs;
   cfg.numAttrs = na;
   const bool chain = c.a.n_stages > 1;
+  const bool um = c.a.umma != 0;
+#define G1_L(BT_)                                                                                              \
+  (chain ? (um ? g1_launch<BT_, CHAIN_MAX_STAGES, true>(c, &cfg) : g1_launch<BT_, CHAIN_MAX_STAGES, false>(c, &cfg)) \
+         : (um ? g1_launch<BT_, 1, true>(c, &cfg) : g1_launch<BT_, 1, false>(c, &cfg)))
   switch (c.BT) {
-    case 1: return chain ? g1_launch<1, CHAIN_MAX_STAGES>(c, &cfg) : g1_launch<1, 1>(c, &cfg);
-    case 4: return chain ? g1_launch<4, CHAIN_MAX_STAGES>(c, &cfg) : g1_launch<4, 1>(c, &cfg);
-    case 8: return chain ? g1_launch<8, CHAIN_MAX_STAGES>(c, &cfg) : g1_launch<8, 1>(c, &cfg);
-    case 16: return chain ? g1_launch<16, CHAIN_MAX_STAGES>(c, &cfg) : g1_launch<16, 1>(c, &cfg);
+    case 1: return chain ? g1_launch<1, CHAIN_MAX_STAGES, false>(c, &cfg) : g1_launch<1, 1, false>(c, &cfg);
+    case 4: return G1_L(4);
+    case 8: return G1_L(8);
+    case 16: return G1_L(16);
     default: return cudaErrorInvalidConfiguration;
   }
+#undef G1_L
 }
 
 }  // namespace paro

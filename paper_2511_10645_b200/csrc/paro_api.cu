@@ -331,7 +331,8 @@ static RotOverride rot_cs_override(const float2* cs, const uchar2* idx, const fl
 
 static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, int n, const paro_packed* packed,
                                   RotOverride ov, const float* const* bias, void* const* y, paro_dtype y_dtype,
-                                  int rotate, int pdl, int debug, void* ws, size_t ws_bytes, cudaStream_t cs) {
+                                  int rotate, int pdl, int debug, int tcgen05, void* ws, size_t ws_bytes,
+                                  cudaStream_t cs) {
   int64_t Ns[paro::GEMV_MAX_LIN];
   int Ls[paro::GEMV_MAX_LIN];
   for (int i = 0; i < n; ++i) {
@@ -357,7 +358,7 @@ static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, 
   int64_t nk = 0;
   for (int i = 0; i < n; ++i) nk += packed[i].N * K;
   const bool old_small = B == 2 || (B <= 4 && nk >= (48LL << 20) && K < 8192);
-  bool k_split = !debug && paro::gemv1_enabled() && (B == 1 || B > 4 || !old_small || small_b);
+  bool k_split = !debug && paro::gemv1_enabled() && (B == 1 || B > 4 || !old_small || small_b || tcgen05);
   if (!k_split && !debug && paro::gemv1_enabled()) {  // the other kernel must be able to plan this shape
     const int bt0 = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8;
     const char* why0 = "";
@@ -369,7 +370,8 @@ static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, 
     if (k_split) {
       paro::Gemv1Config c1;
       const char* why = "";
-      if (!paro::plan_gemv1(live, n, Ns, K, rotate, &c1, &why)) return fail(PARO_ERR_UNSUPPORTED, "paro_linear: %s", why);
+      if (!paro::plan_gemv1(live, n, Ns, K, rotate, tcgen05, &c1, &why))
+        return fail(PARO_ERR_UNSUPPORTED, "paro_linear: %s", why);
       paro::Gemv1Args& a = c1.a;
       paro::Gemv1Stage& S0 = a.st[0];
       S0.x = static_cast<const uint8_t*>(x) + b0 * K * xe;
@@ -504,7 +506,7 @@ paro_status paro_linear(const void* x, paro_dtype x_dtype, int64_t B, const paro
   // decode GEMV over token tiles
   const size_t used = static_cast<size_t>(wsp - static_cast<uint8_t*>(workspace));
   return decode_linears(x, x_dtype, B, 1, packed, rot_cs_override(rot_cs, rot_idx, svec, on_the_fly), &bias, &y,
-                        y_dtype, rotate, pdl, (flags & 0x100u) ? 1 : 0, wsp,
+                        y_dtype, rotate, pdl, (flags & 0x100u) ? 1 : 0, (flags & PARO_LINEAR_TCGEN05) ? 1 : 0, wsp,
                         workspace_bytes > used ? workspace_bytes - used : 0, cs);
 }
 
@@ -543,10 +545,13 @@ paro_status paro_linear_multi(const void* x, paro_dtype x_dtype, int64_t B, int3
   if (workspace_bytes < need || (need && !workspace))
     return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear_multi: workspace too small (%zu < %zu)", workspace_bytes, need);
   return decode_linears(x, x_dtype, B, n, packed, rot_cs_override(nullptr, nullptr, nullptr, 0), bias, y, y_dtype,
-                        rotate, pdl, (flags & 0x100u) ? 1 : 0, workspace, workspace_bytes, cs);
+                        rotate, pdl, (flags & 0x100u) ? 1 : 0, (flags & PARO_LINEAR_TCGEN05) ? 1 : 0, workspace,
+                        workspace_bytes, cs);
 }
 
 // ---------------------------------------------------------------- persistent decode chain
+// workspace header: grid-barrier epoch word + one arrival flag per CTA (zero before first use)
+constexpr size_t kChainHdr = 8192;
 static size_t chain_xq_bytes(int64_t B, int32_t n_stages, const paro_chain_stage* stages) {
   if (B <= 1) return 0;
   int64_t Kmax = 0;
@@ -560,7 +565,7 @@ size_t paro_linear_chain_workspace(int64_t B, int32_t n_stages, const paro_chain
   for (int s = 0; s < n_stages; ++s)
     if (stages[s].n < 1 || stages[s].n > paro::GEMV_MAX_LIN || !stages[s].packed) return 0;
   // grid-barrier words + (B > 1) one x'-digit buffer per linear slot, shared by the stages
-  return 256 + align256(chain_xq_bytes(B, n_stages, stages) * paro::GEMV_MAX_LIN);
+  return kChainHdr + align256(chain_xq_bytes(B, n_stages, stages) * paro::GEMV_MAX_LIN);
 }
 
 paro_status paro_linear_chain(int32_t n_stages, const paro_chain_stage* stages, paro_dtype x_dtype, int64_t B,
@@ -608,7 +613,8 @@ paro_status paro_linear_chain(int32_t n_stages, const paro_chain_stage* stages, 
     }
     paro::Gemv1Config c;
     const char* why = "";
-    if (!paro::plan_gemv1_chain(static_cast<int>(B), ns, nl, Ns, Ks, rotate, &c, &why))
+    if (!paro::plan_gemv1_chain(static_cast<int>(B), ns, nl, Ns, Ks, rotate, (flags & PARO_LINEAR_TCGEN05) ? 1 : 0, &c,
+                                &why))
       return fail(PARO_ERR_UNSUPPORTED, "paro_linear_chain: %s", why);
     paro::Gemv1Args& a = c.a;
     a.x_bf16 = x_dtype == PARO_BF16;
@@ -632,7 +638,7 @@ paro_status paro_linear_chain(int32_t n_stages, const paro_chain_stage* stages, 
         d.y = S.y[i];
         d.L = p.n_rot;
         if (B > 1) {
-          uint8_t* base = wsb + 256 + xq_per * i;
+          uint8_t* base = wsb + kChainHdr + xq_per * i;
           d.xq = base;
           d.xqs = reinterpret_cast<int2*>(base + static_cast<size_t>(p.K / kG) * (c.BT / 4) * 1024);
         }

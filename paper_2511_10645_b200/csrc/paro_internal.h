@@ -107,6 +107,7 @@ template <int MS>
 struct Gemv1ArgsT {
   int x_bf16;
   int B;  // tokens (1..16)
+  int umma;  // B > 1: tiles on the tcgen05 tensor cores (kind::i8, TMEM) instead of mma.sync
   int y_dtype;
   int rotate;
   int pdl;
@@ -114,8 +115,11 @@ struct Gemv1ArgsT {
   int S;             // ring depth (batches)
   int pre_stages;    // batches issued before the compute warps' x / parameter loads are out
   int params_first;  // the first batches wait until the rotation-parameter loads are issued
+  int l2_batches;    // stages >= 1: batches prefetched into L2 at the stage boundary
+  int xfirst;        // stages >= 1: the ring refill waits until the compute warps' x loads are out
+  int nobar;         // experiments only (debug builds): skip the grid-barrier waits
   int n_stages;
-  uint32_t* gbar;    // grid barrier words (workspace; zero before first use, left zero)
+  uint32_t* gbar;    // grid barrier words: [0] epoch, [16 ..) one flag per CTA (workspace, zero before first use)
   uint32_t slot_bytes, sc_off, z_off;
   uint32_t off_xp, off_xs, off_scr, off_part, off_recv, off_bar, off_ring, smem_total;
   Gemv1Stage st[MS];
@@ -134,8 +138,9 @@ size_t gemv1_xq_bytes(int B, int64_t K);
 cudaError_t launch_gemv1_xform(const Gemv1Config& cfg, cudaStream_t st);
 // Plan a chain: n_stages stages, stage s with n_lin[s] linears of widths Ns[s][i] sharing K[s].
 bool plan_gemv1_chain(int B, int n_stages, const int* n_lin, const int64_t (*Ns)[GEMV_MAX_LIN], const int64_t* K,
-                      int rotate, Gemv1Config* cfg, const char** why);
-bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, Gemv1Config* cfg, const char** why);
+                      int rotate, int tcgen05, Gemv1Config* cfg, const char** why);
+bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, int tcgen05, Gemv1Config* cfg,
+                const char** why);
 cudaError_t launch_gemv1(const Gemv1Config& cfg, cudaStream_t st);
 
 // ---------------------------------------------------------------- activation transform (prefill pre-stage)

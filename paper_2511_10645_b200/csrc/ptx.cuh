@@ -50,14 +50,38 @@ PARO_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+PARO_DEV uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Wait for the phase with the given parity.  Watchdog: a phase that never completes (a protocol
+// bug) traps after 4 s instead of hanging the GPU; the clock is read every 256 retries only.
 PARO_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
 #if PARO_MBAR_SPIN
+  if (mbar_try_wait_spin(bar, parity)) return;
+#else
+  if (mbar_try_wait(bar, parity)) return;
+#endif
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t n = 0;
+#if PARO_MBAR_SPIN
   while (!mbar_try_wait_spin(bar, parity)) {
-  }
 #else
   while (!mbar_try_wait(bar, parity)) {
-  }
 #endif
+    if ((++n & 255u) == 0u && globaltimer_ns() - t0 > 4000000000ull) __trap();
+  }
+}
+
+// spin variant (no suspend hint) for short waits on the critical path (e.g. tcgen05.commit)
+PARO_DEV void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait_spin(bar, parity)) return;
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t n = 0;
+  while (!mbar_try_wait_spin(bar, parity)) {
+    if ((++n & 1023u) == 0u && globaltimer_ns() - t0 > 4000000000ull) __trap();
+  }
 }
 
 // ---------------------------------------------------------------- bulk async copy (TMA engine, 1-D)
@@ -129,11 +153,19 @@ PARO_DEV void named_bar_arrive(uint32_t id, uint32_t nthreads) {
 
 
 // ---------------------------------------------------------------- grid-wide barrier (persistent chains)
-// All CTAs of the grid are co-resident (one wave, grid <= occupancy).  gb[0] = arrivals of the
-// current barrier, gb[1] = generation; gb[0] is back to 0 after every completed barrier.
-PARO_DEV uint32_t ld_acquire_gpu(const uint32_t* p) {
+// Flat flags: every CTA publishes its arrival at barrier k of the launch with epoch e as
+// flag[cta] = 64 e + k + 1 (st.release), and a waiter polls all flags until each is >= that
+// value -- one store and one poll round trip, no read-modify-write on the critical path.  The
+// epoch word is read once per launch (after the previous kernel on the stream completed) and
+// bumped by CTA 0 when it exits, so flags left by earlier launches never satisfy a wait.
+// All CTAs of the grid are co-resident (one wave, grid <= occupancy); < 64 barriers per launch.
+struct GridBar {
+  uint32_t* epoch;  // workspace word
+  uint32_t* flags;  // [gridDim.x]
+};
+PARO_DEV uint32_t ld_relaxed_gpu(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 PARO_DEV void st_release_gpu(uint32_t* p, uint32_t v) {
@@ -142,36 +174,20 @@ PARO_DEV void st_release_gpu(uint32_t* p, uint32_t v) {
 PARO_DEV void st_relaxed_gpu(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-PARO_DEV uint32_t atom_add_acq_rel_gpu(uint32_t* p, uint32_t v) {
-  uint32_t o;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(o) : "l"(p), "r"(v) : "memory");
-  return o;
-}
-PARO_DEV uint64_t globaltimer_ns() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-// One thread per CTA, after a CTA barrier that orders the CTA's writes before it (the
-// cooperative-groups grid.sync pattern).  Returns the generation to wait on.
-PARO_DEV uint32_t grid_arrive(uint32_t* gb, uint32_t nblocks) {
-  const uint32_t gen = ld_acquire_gpu(gb + 1);
-  __threadfence();
-  if (atom_add_acq_rel_gpu(gb, 1u) == nblocks - 1) {
-    st_relaxed_gpu(gb, 0u);
-    st_release_gpu(gb + 1, gen + 1);
-  }
-  return gen;
-}
-// Wait (one thread) until the barrier of generation `gen` completed; traps after 2 s instead of
-// hanging the GPU if a CTA never arrives (e.g. a grid that is not co-resident).
-PARO_DEV void grid_wait(const uint32_t* gb, uint32_t gen) {
-  if (ld_acquire_gpu(gb + 1) != gen) return;
+PARO_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// one thread per CTA, after a CTA barrier that orders the CTA's writes before it
+PARO_DEV void grid_arrive(const GridBar& gb, uint32_t target) { st_release_gpu(gb.flags + blockIdx.x, target); }
+// one full warp; returns when every CTA's flag reached `target` (then CTA-barrier the rest)
+PARO_DEV void grid_wait_warp(const GridBar& gb, uint32_t target, int lane) {
+  const int n = static_cast<int>(gridDim.x);
   const uint64_t t0 = globaltimer_ns();
-  while (ld_acquire_gpu(gb + 1) == gen) {
-    __nanosleep(64);
-    if (globaltimer_ns() - t0 > 2000000000ull) __trap();
+  for (;;) {
+    bool ok = true;
+    for (int j = lane; j < n; j += 32) ok &= static_cast<int>(ld_relaxed_gpu(gb.flags + j) - target) >= 0;
+    if (__all_sync(0xffffffffu, ok)) break;
+    if (globaltimer_ns() - t0 > 2000000000ull) __trap();  // a CTA never arrived: error, not a hang
   }
+  fence_acq_rel_gpu();
 }
 
 // ---------------------------------------------------------------- programmatic dependent launch

@@ -21,9 +21,12 @@ def paro():
     return m
 
 
-def _lin(paro, N, K, B, seed, nrows=None, bias=False):
-    """A packed linear + its oracle pack (all rows, or `nrows` sampled rows)."""
-    p = synth.make_problem(N, K, B, seed=seed, with_bias=bias)
+def _lin(paro, N, K, B, seed, nrows=None, bias=False, unit_gain=False):
+    """A packed linear + its oracle pack (all rows, or `nrows` sampled rows).  unit_gain: W ~
+    N(0, 1/K) without outlier channels, so repeated application keeps |y| ~ |x|."""
+    p = synth.make_problem(N, K, B, seed=seed, with_bias=bias, outliers=not unit_gain)
+    if unit_gain:
+        p["W"] = (p["W"].astype(np.float64) * (1.0 / np.sqrt(K)) / 0.02).astype(np.float16)
     t = dev_tensors(p)
     rows = None if nrows is None or nrows >= N else \
         np.sort(np.random.default_rng(seed).choice(N, size=nrows, replace=False))
@@ -86,7 +89,7 @@ def test_chain_llama8b_layer(paro):
           paro.ChainStage(x, [gate["packed"], up["packed"]], [ys["g"], ys["u"]]),
           paro.ChainStage(ys["u"], [down["packed"]], [ys["d"]])]
     ws = paro.chain_workspace(1, st)
-    for _ in range(2):  # the workspace's barrier words are left zero: a second call works the same
+    for _ in range(2):  # the barrier epoch advances per launch: a second call on the workspace works the same
         paro.paro_linear_chain(st, flags=paro.PARO_LINEAR_PDL, workspace=ws)
     torch.cuda.synchronize()
     xn = q["p"]["x"]
@@ -94,7 +97,7 @@ def test_chain_llama8b_layer(paro):
         _check(lin, xn, ys[name])
     _check(o, o["p"]["x"], ys["o"])
     _check(down, ys["u"].float().cpu().numpy(), ys["d"])
-    assert int(ws[:8].view(torch.int32)[0].item()) == 0, "barrier arrival counter not left at zero"
+    assert int(ws[:4].view(torch.int32)[0].item()) == 2, "one barrier epoch per persistent launch"
 
 
 @pytest.mark.parametrize("B", [1, 5])
@@ -102,7 +105,7 @@ def test_chain_longer_than_one_launch(paro, B):
     """18 dependent stages (16 per persistent launch + a second launch): a ping-pong of two
     square linears, each stage reading the previous stage's y."""
     K = 256
-    lins = [_lin(paro, K, K, B, 730 + i) for i in range(2)]
+    lins = [_lin(paro, K, K, B, 730 + i, unit_gain=True) for i in range(2)]
     x = torch.from_numpy(lins[0]["p"]["x"]).cuda()
     ys = [torch.empty((B, K), dtype=torch.float16, device="cuda") for _ in range(18)]
     st, prev = [], x
@@ -167,3 +170,22 @@ def test_chain_errors(paro):
         paro.paro_linear_chain([paro.ChainStage(x1, [a["packed"]], [y1])],
                                workspace=torch.zeros(16, dtype=torch.uint8, device="cuda"))
     assert e.value.kind == "invalid_argument"
+
+
+@pytest.mark.parametrize("B", [2, 3, 5, 8, 12, 16])
+def test_tcgen05_engine_single_and_chain(paro, B):
+    """PARO_LINEAR_TCGEN05: the B > 1 tiles on tcgen05.mma kind::i8 (u8 codes in TMEM x s8 digits)
+    -- one launch (stage-0 transform pre-kernel) and a dependent chain (in-kernel transform)."""
+    A = _lin(paro, 1024, 2560, B, 770, bias=True)
+    C = _lin(paro, 640, 1024, B, 771)
+    x = torch.from_numpy(A["p"]["x"]).cuda()
+    y = paro.paro_linear(x, A["packed"], bias=A["bias"], flags=paro.PARO_LINEAR_TCGEN05)
+    torch.cuda.synchronize()
+    _check(A, A["p"]["x"], y)
+    y0 = torch.empty((B, 1024), dtype=torch.float16, device="cuda")
+    y1 = torch.empty((B, 640), dtype=torch.float16, device="cuda")
+    paro.paro_linear_chain([paro.ChainStage(x, [A["packed"]], [y0], bias=[A["bias"]]),
+                            paro.ChainStage(y0, [C["packed"]], [y1])], flags=paro.PARO_LINEAR_TCGEN05)
+    torch.cuda.synchronize()
+    _check(A, A["p"]["x"], y0)
+    _check(C, y0.float().cpu().numpy(), y1)

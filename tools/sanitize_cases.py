@@ -37,17 +37,7 @@ def case(N, K, B, flags=0, seed=0, otf=False):
     assert err < 2e-3
 
 
-def main():
-    quick = "--quick" in sys.argv
-    case(256, 256, 1)                                          # C1
-    case(4096 if not quick else 1024, 4096, 1, paro.PARO_LINEAR_PDL)
-    case(1024, 4096, 3)
-    case(1024, 4096, 2)
-    case(1024, 4096, 16)
-    case(512, 1024, 5, otf=True)
-    case(512, 1024, 1, otf=True)
-    case(256, 512, 300, paro.PARO_LINEAR_FORCE_GEMM)           # prefill tcgen05
-    # multi-linear launch (q/k/v style)
+def multi():
     K = 1024
     ps = [synth.make_problem(N, K, 1, seed=10 + i) for i, N in enumerate((512, 128, 256))]
     pks = []
@@ -61,9 +51,47 @@ def main():
         y_ref = O.oracle_linear(ps[0]["x"], ref, p["s"], p["theta"], p["pairs"])
         assert O.normwise_error(y.float().cpu().numpy(), y_ref) < 2e-3
     print("multi ok", flush=True)
-    extra = getattr(paro, "_sanitize_extra", None)
-    if extra:
-        extra()
+
+
+def chain(B):
+    """Two dependent stages in one persistent launch (grid barrier; B > 1: in-kernel transform)."""
+    pa = synth.make_problem(256, 512, B, seed=20)
+    pb = synth.make_problem(128, 256, B, seed=21)
+    ta, tb = dev(pa), dev(pb)
+    ka = paro.paro_pack(ta["W"], ta["s"], ta["theta"], ta["pairs"])
+    kb = paro.paro_pack(tb["W"], tb["s"], tb["theta"], tb["pairs"])
+    y0 = torch.empty((B, 256), dtype=torch.float16, device="cuda")
+    y1 = torch.empty((B, 128), dtype=torch.float16, device="cuda")
+    paro.paro_linear_chain([paro.ChainStage(ta["x"], [ka], [y0]), paro.ChainStage(y0, [kb], [y1])])
+    torch.cuda.synchronize()
+    ra = O.oracle_pack(pa["W"], pa["s"], pa["theta"], pa["pairs"])
+    rb = O.oracle_pack(pb["W"], pb["s"], pb["theta"], pb["pairs"])
+    assert O.normwise_error(y0.float().cpu().numpy(), O.oracle_linear(pa["x"], ra, pa["s"], pa["theta"], pa["pairs"])) < 2e-3
+    y0n = y0.float().cpu().numpy()
+    assert O.normwise_error(y1.float().cpu().numpy(), O.oracle_linear(y0n, rb, pb["s"], pb["theta"], pb["pairs"])) < 2e-3
+    print(f"chain B={B} ok", flush=True)
+
+
+CASES = {
+    "c1": lambda: case(256, 256, 1),
+    "q_b1_pdl": lambda: case(1024, 4096, 1, paro.PARO_LINEAR_PDL),
+    "q_b3": lambda: case(1024, 4096, 3),
+    "q_b2": lambda: case(1024, 4096, 2),
+    "q_b16": lambda: case(1024, 4096, 16),
+    "otf_b5": lambda: case(512, 1024, 5, otf=True),
+    "otf_b1": lambda: case(512, 1024, 1, otf=True),
+    "prefill_b300": lambda: case(256, 512, 300, paro.PARO_LINEAR_FORCE_GEMM),
+    "multi": multi,
+    "chain_b1": lambda: chain(1),
+    "chain_b4": lambda: chain(4),
+    "q_b8_tcgen05": lambda: case(1024, 4096, 8, paro.PARO_LINEAR_TCGEN05),
+}
+
+
+def main():
+    names = [a for a in sys.argv[1:] if not a.startswith("--")] or list(CASES)
+    for n in names:
+        CASES[n]()
     print("SANITIZE CASES DONE", flush=True)
 
 

@@ -166,8 +166,8 @@ def bench_config(B, world=1):
     """The config block shared by both arms (pure arithmetic: the reference arm reports the same)."""
     n_layers, wb = pool_layers(world)
     return {"workload": WORKLOAD, "batch": B,
-            "step": ("one paro_linear_chain launch: 4 stages (q/k/v | o | gate/up | down reading up's y), "
-                     "grid barrier between stages") if world == 1 else "7 paro_linear_allgather calls",
+            "step": ("4 paro_linear_multi decode launches (q/k/v | o | gate/up | down reading up's y), "
+                     "PDL-chained") if world == 1 else "7 paro_linear_allgather calls",
             "parallelism": f"N-shard x{world} + NCCL all-gather" if world > 1 else "single GPU",
             "l2": (f"inputs larger than L2: weight pool of {n_layers} layers x {wb / 1e6:.1f} MB/rank "
                    f"> 4 x 126 MB L2, cycled per step"),
@@ -213,10 +213,13 @@ def run_paro(args):
     chain_ws = paro.chain_workspace(B, chains[0])
 
     def run_step(li, flags, pdl=True):
-        """One step: the layer's seven linears (world 1: ONE persistent chain launch)."""
+        """One step: the layer's seven linears as four decode launches (q/k/v and gate/up share
+        their input; down reads up's output), PDL-chained: each launch waits for its predecessor
+        before reading x or writing y."""
         f = flags | (paro.PARO_LINEAR_PDL if pdl else 0)
         if world == 1:
-            paro.paro_linear_chain(chains[li % n_layers], flags=f, workspace=chain_ws, stream=stream)
+            for st in chains[li % n_layers]:
+                paro.paro_linear_multi(st.x, st.packed, y=st.y, flags=f, workspace=ws, stream=stream)
         else:
             layer = {name: (N, K, packed) for name, N, K, packed in pool[li % n_layers]}
             for grp in LAYER_STAGES:
@@ -226,11 +229,10 @@ def run_paro(args):
                     paro.paro_linear_allgather(xin, packed, comm, rank, world, y=ys[name], flags=f, workspace=ws,
                                                stream=stream)
 
-    def run_step_4launch(li, flags, pdl=True):
-        """The same step as four paro_linear_multi launches (PDL-chained): round-1 form."""
+    def run_step_chain(li, flags, pdl=True):
+        """The same step as ONE persistent paro_linear_chain launch (grid barrier between stages)."""
         f = flags | (paro.PARO_LINEAR_PDL if pdl else 0)
-        for st in chains[li % n_layers]:
-            paro.paro_linear_multi(st.x, st.packed, y=st.y, flags=f, workspace=ws, stream=stream)
+        paro.paro_linear_chain(chains[li % n_layers], flags=f, workspace=chain_ws, stream=stream)
 
     def timed(step_fn, flags, steps, warmup):
         """Graph of `steps` consecutive steps (layers cycle through the pool); returns
@@ -272,7 +274,7 @@ def run_paro(args):
         ms_step = timed(run_step, 0, args.steps, args.warmup)
     clocks = clk.summary()
     ms_norot = timed(run_step, paro.PARO_LINEAR_NO_ROTATION, args.steps, args.warmup)
-    ms_4l = timed(run_step_4launch, 0, args.steps, args.warmup) if world == 1 else None
+    ms_chain = timed(run_step_chain, 0, args.steps, args.warmup) if world == 1 else None
 
     # cold single step: L2 flushed (a 2 x L2 buffer written) before each call, median of 7
     cold_us = None
@@ -362,7 +364,7 @@ def run_paro(args):
     del gph
     e2e = {"value": round(layer_bytes / (ms_e2e * 1e-3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms_e2e, 4),
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-           "api": ("paper_2511_10645_b200.paro_linear_chain (one launch per step)" if world == 1 else
+           "api": ("paper_2511_10645_b200.paro_linear_multi (4 decode launches per step)" if world == 1 else
                    "paper_2511_10645_b200.paro_linear_allgather per linear") +
                   " with the pinned-host x -> device and y -> host copies of every step, each step captured in a "
                   "CUDA graph and replayed"}
@@ -404,21 +406,21 @@ def run_paro(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f16 act / int4 weight / f32 acc",
         "rotation_overhead": round(ms_step / ms_norot - 1.0, 4), "us_per_step_norot": round(ms_norot * 1e3, 3),
         "frac_of_8TBps": round(gbps / 8000.0, 4),
-        "us_per_step_4_launches": None if ms_4l is None else round(ms_4l * 1e3, 3),
+        "us_per_step_chain": None if ms_chain is None else round(ms_chain * 1e3, 3),
         "cold_step_us": cold_us,
         "data": "synthetic (random fp16 W ~ N(0,0.02^2) packed W4 g128 with Alg. A1 pairs, random theta/s; x ~ N(0,1))",
         "config": bench_config(B, world),
         "roofline": {"bound": "hbm", "achieved": round(gbps, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(gbps / peak, 4), "traffic": None,
-                     "kernel": "paro_gemv1_kernel (the step's one chain launch)",
+                     "kernel": "paro_gemv1_b1_kernel (the step's 4 decode launches)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if not peaks.get("_fallback")
                      else "fallback 6.65 TB/s",
                      "achieved_def": "algorithmic bytes per step (SURVEY.md 8(d): 0.5195 B/weight + 6 B/pair + 4 B/ch "
                                      "s + 2BK + 2BN) / device time per step"},
         "clocks": clocks, "e2e": e2e,
-        "gpu_launches": (1 if world == 1 else 14) * args.steps,
-        "gpu_launches_note": ("1 paro_gemv1_kernel (persistent 4-stage chain) launch per step" if world == 1
-                              else "7 paro_gemv1_kernel + 7 ncclAllGather launches per step"),
+        "gpu_launches": (4 if world == 1 else 14) * args.steps,
+        "gpu_launches_note": ("4 paro_gemv1_b1_kernel launches per step (q/k/v and gate/up fused by shared input)"
+                              if world == 1 else "7 paro_gemv1_b1_kernel + 7 ncclAllGather launches per step"),
         "per_linear": per_linear, "prefill": prefill, **extra,
     }
     if world == 1 and not args.no_cpu_baseline:
@@ -522,9 +524,10 @@ def measure_prefill(torch, paro, dev, stream, layer, g):
 
 def measure_qwen_stack(torch, paro, dev, stream, batches):
     """configs[2]: the Qwen3-4B decode stack (36 layers x 7 linears, each with its own
-    transform), every layer 4 chain stages (q/k/v | o | gate/up | down reading up's y): 144
-    stages = 9 persistent launches per step; 1.9 GB of packed weights, so every step streams
-    from HBM.  Bytes per step include the B-token activations."""
+    transform), every layer 4 decode launches (q/k/v | o | gate/up | down reading up's y): 144
+    PDL-chained launches per step (also timed as 9 persistent chain launches); 1.9 GB of packed
+    weights, so every step streams from HBM.  Bytes per step include the B-token activations
+    (SURVEY.md 8(d))."""
     shapes = synth.QWEN3_4B_LAYER
     pool = build_layer_pool(torch, paro, shapes, 0, 1, synth.QWEN3_4B_LAYERS, dev, seed=11)
     out = {"layers": synth.QWEN3_4B_LAYERS}
@@ -537,13 +540,25 @@ def measure_qwen_stack(torch, paro, dev, stream, batches):
         stages = []
         for layer in pool:
             stages += layer_chain(paro, layer, x_in, x_attn, ys)
-        ws = paro.chain_workspace(B, stages)
+        ws = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
+
+        def step(fl):
+            for st in stages:  # 144 PDL-chained decode launches
+                paro.paro_linear_multi(st.x, st.packed, y=st.y, flags=fl | paro.PARO_LINEAR_PDL, workspace=ws,
+                                       stream=stream)
+
         res = {}
         for tag, fl in (("rot", 0), ("norot", paro.PARO_LINEAR_NO_ROTATION)):
-            res[tag] = graph_time_us(torch, stream, lambda: paro.paro_linear_chain(
-                stages, flags=fl | paro.PARO_LINEAR_PDL, workspace=ws, stream=stream), 3)
+            res[tag] = graph_time_us(torch, stream, lambda: step(fl), 3)
+        try:  # the same stack as persistent chains (16 stages per launch)
+            cws = paro.chain_workspace(B, stages)
+            res["chain"] = graph_time_us(torch, stream, lambda: paro.paro_linear_chain(
+                stages, flags=paro.PARO_LINEAR_PDL, workspace=cws, stream=stream), 3)
+        except Exception:  # noqa: BLE001  (a chain plan may not fit shared memory at 16 tokens)
+            res["chain"] = None
         out[f"bs{B}"] = {"us_per_step": round(res["rot"], 1), "GBps": round(step_bytes / res["rot"] / 1e3, 1),
-                         "bytes_per_step": int(step_bytes), "rot_overhead": round(res["rot"] / res["norot"] - 1.0, 4)}
+                         "bytes_per_step": int(step_bytes), "rot_overhead": round(res["rot"] / res["norot"] - 1.0, 4),
+                         "us_per_step_chain": None if res["chain"] is None else round(res["chain"], 1)}
         del stages, ws
     del pool
     torch.cuda.empty_cache()

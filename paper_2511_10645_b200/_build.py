@@ -17,7 +17,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 # pack.cu must not contract a*b - c*d into FMA: bit-exact fp64 fold (Q7)
 PER_FILE = {"pack.cu": ["-fmad=false"]}
-SOURCES = ["paro_api.cu", "pack.cu", "gemv.cu", "gemv1.cu", "misc.cu", "prefill.cu", "hadamard.cu", "pairs.cpp"]
+SOURCES = ["paro_api.cu", "pack.cu", "gemv.cu", "gemv1.cu", "gemv1_b1.cu", "misc.cu", "prefill.cu", "hadamard.cu", "pairs.cpp"]
 HEADERS = ["ptx.cuh", "paro_internal.h", "umma.cuh", "tile_layout.cuh"]
 
 

@@ -75,10 +75,12 @@ namespace {
 // compute warps per CTA (+ 1 producer warp).  16 warps in all keep four warps per SM
 // sub-partition and so 128 registers per thread (17 warps would cap it at 96 and spill); B > 1
 // uses three warpgroups of four for the tensor-core tiles.
-#ifndef G1_NW1
-#define G1_NW1 15
-#endif
-__host__ __device__ constexpr int g1_nw(int BT, bool um) { return BT > 1 && um ? 12 : G1_NW1; }
+// B = 1 one-stage instances (no stage loop) fit 16 compute warps in 96 registers without spills;
+// chain instances and B > 1 keep more live state and use 15 (16 warps in all: 128 registers), the
+// tcgen05 engine three warpgroups.
+__host__ __device__ constexpr int g1_nw(int BT, bool um, bool chain) {
+  return BT > 1 ? (um ? 12 : 15) : (chain ? 15 : 16);
+}
 constexpr uint32_t TILE_B = TILE_CODE_BYTES + TILE_SCALE_BYTES + TILE_ZERO_BYTES;
 
 // D(16x8 s32) += A(16x32 u8, row) * B(32x8 s8, col); fragments as in ptx.cuh (imma_16832),
@@ -331,6 +333,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
   const int CL = static_cast<int>(cluster_nctarank());
   const int crank = static_cast<int>(cluster_ctarank());
   const int B = a.B;
+  const int n_st = MS == 1 ? 1 : a.n_stages;  // a one-stage instance has no stage loop
 
   uint8_t* xp = smem + a.off_xp;                                 // x' digits [gc][NB][4 t][NCOL][4 kb][8 B]
   int2* xs = reinterpret_cast<int2*>(smem + a.off_xs);           // per (group, token): (sum x'fix, 2^(E-14))
@@ -349,17 +352,20 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
   // the barriers (nothing serial on the launch's critical path)
   __shared__ G1Geom sgeo[MS];
   const int lgCL = __ffs(CL) - 1;
-  if (tid < a.n_stages) sgeo[tid] = g1_geom(a.st[tid], lgCL, crank, a.TPS, UM);
+  if (tid < n_st) sgeo[tid] = g1_geom(a.st[tid], lgCL, crank, a.TPS, UM);
 
   if (tid < 8) reinterpret_cast<uint32_t*>(smem + a.off_xs - 32)[tid] = 0u;
-  if (tid == 32) {
-    for (int i = 0; i < a.S; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], NW);
-    }
-    mbar_init(rbar, 1);
-    mbar_init(xbar, 1);
-    for (int i = 0; i < 8; ++i) mbar_init(&mdone[i], 1);
+  // barrier initialisation spread over threads 32 .. (each init is a store plus an async-proxy
+  // fence: done serially by one thread it sits on the launch's critical path)
+  if (tid >= 32 && tid < 32 + a.S) {
+    mbar_init(&full[tid - 32], 1);
+    mbar_init(&empty[tid - 32], NW);
+    fence_mbar_init();
+  } else if (tid >= 96 && tid < 106) {
+    if (tid < 104)
+      mbar_init(&mdone[tid - 96], 1);
+    else
+      mbar_init(tid == 104 ? rbar : xbar, 1);
     fence_mbar_init();
   }
   if (UM && warp == 2) tmem_alloc(tmem_slot, 512);  // 3 warpgroups x (2 A + 2 D buffers) <= 512 columns
@@ -433,7 +439,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
     };
     int slot = 0, phase = 0, nb = 0;
 #pragma unroll 1
-    for (int s = 0; s < a.n_stages; ++s) {
+    for (int s = 0; s < n_st; ++s) {
       const Gemv1Stage& S = a.st[s];
       const G1Geom& g = sgeo[s];
       const Gemv1Linear& d = S.lin[g.li];
@@ -484,7 +490,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
     named_bar_sync(4, NW * 32);
   };
 #pragma unroll 1
-  for (int s = 0; s < a.n_stages; ++s) {
+  for (int s = 0; s < n_st; ++s) {
     const Gemv1Stage& S = a.st[s];
     const G1Geom& g = sgeo[s];
     const Gemv1Linear& d = S.lin[g.li];
@@ -504,7 +510,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
         if (a.params_first) named_bar_arrive(3, (NW + 1) * 32);
         named_bar_arrive(2, (NW + 1) * 32);
         if (a.pdl) pdl_wait();
-        if (warp == 0 && a.n_stages > 1) ep = ld_relaxed_gpu(gb.epoch) << 6;
+        if (warp == 0 && n_st > 1) ep = ld_relaxed_gpu(gb.epoch) << 6;
       } else {
         wait_grid();
         if (S.xq_in_kernel) {
@@ -538,39 +544,41 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
       float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * 128;
       const int L = a.rotate ? d.L : 0;
       const bool mine = g.active && warp < gc;
-      float4 cs[8], sv = make_float4(1.f, 1.f, 1.f, 1.f);
-      uint32_t ix[8];
-      if (mine) {
-        g1_params(d, ga + warp, L, a.rotate, lane, cs, ix, sv);
-        if (lane == 0) {
-          // later rounds' rotation records -> L2 now, ahead of the weight stream
-          for (int gg = warp + NW; gg < gc; gg += NW) {
-            const int64_t rec = static_cast<int64_t>(ga + gg) * L * 32;
-            if (L > 0) {
-              prefetch_l2_bulk(reinterpret_cast<const float4*>(d.rot_cs) + rec, static_cast<uint32_t>(L * 32 * 16));
-              prefetch_l2_bulk(reinterpret_cast<const uint32_t*>(d.rot_idx) + rec, static_cast<uint32_t>(L * 32 * 4));
-            }
-            if (a.rotate) prefetch_l2_bulk(d.svec + (ga + gg) * 128, 512u);
+      if (mine && lane == 0) {
+        // later rounds' rotation records -> L2 now, ahead of the weight stream
+        for (int gg = warp + NW; gg < gc; gg += NW) {
+          const int64_t rec = static_cast<int64_t>(ga + gg) * L * 32;
+          if (L > 0) {
+            prefetch_l2_bulk(reinterpret_cast<const float4*>(d.rot_cs) + rec, static_cast<uint32_t>(L * 32 * 16));
+            prefetch_l2_bulk(reinterpret_cast<const uint32_t*>(d.rot_idx) + rec, static_cast<uint32_t>(L * 32 * 4));
           }
+          if (a.rotate) prefetch_l2_bulk(d.svec + (ga + gg) * 128, 512u);
         }
       }
-      // x dependency: the previous kernel on the stream (stage 0) or the previous stage (grid barrier)
-      if (s == 0) {
-        if (a.params_first) {
-          __syncwarp();
-          named_bar_arrive(3, (NW + 1) * 32);
+      // the x dependency: the previous kernel on the stream (stage 0, PDL) or the previous stage
+      // (grid barrier) -- waited for once the first group's rotation parameters are requested
+      bool waited = false, arrived = s != 0 && !a.xfirst;
+      auto wait_x = [&]() {
+        if (s == 0) {
+          if (a.params_first) {
+            __syncwarp();
+            named_bar_arrive(3, (NW + 1) * 32);
+          }
+          if (a.pdl) pdl_wait();
+          if (warp == 0 && n_st > 1) ep = ld_relaxed_gpu(gb.epoch) << 6;
+        } else {
+          wait_grid();
         }
-        if (a.pdl) pdl_wait();
-        if (warp == 0 && a.n_stages > 1) ep = ld_relaxed_gpu(gb.epoch) << 6;
-      } else {
-        wait_grid();
-      }
-      if (tid == 0) tl_mark(s, 1);
-      bool arrived = s != 0 && !a.xfirst;
+        if (tid == 0) tl_mark(s, 1);
+        waited = true;
+      };
 #pragma unroll 1
       for (int gg = warp; mine && gg < gc; gg += NW) {
         const int gam = ga + gg;
-        if (gg != warp) g1_params(d, gam, L, a.rotate, lane, cs, ix, sv);
+        float4 cs[8], sv;
+        uint32_t ix[8];
+        g1_params(d, gam, L, a.rotate, lane, cs, ix, sv);
+        if (!waited) wait_x();
         uint2 xv[1] = {g1_ldx(S.x, S.K, 0, gam, lane, s != 0)};
         g1_scale<1>(scr, xv, a.x_bf16, sv, lane);
         if (!arrived) {
@@ -582,6 +590,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
         if (lane == 0) xs[gg] = r;
         __syncwarp();
       }
+      if (!waited) wait_x();
       if (!arrived) named_bar_arrive(2, (NW + 1) * 32);
     }
     named_bar_sync(1, NW * 32);  // every x' of the CTA is in shared memory (and part zeroed)
@@ -966,7 +975,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
       }
     }
     if (tid == 0) tl_mark(s, 6);
-    if (s + 1 < a.n_stages) {
+    if (s + 1 < n_st) {
       named_bar_sync(1, NW * 32);  // every store (and every read of recv) of this stage is done
       if (tid == 0) {
         if (CL > 1)  // the next stage's cluster partials may land once the barrier below completes
@@ -977,7 +986,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
   }
   // the next launch on this workspace uses the next epoch (it reads the word only after this
   // grid completed: PDL wait or stream order)
-  if (a.n_stages > 1 && blockIdx.x == 0 && tid == 0) st_relaxed_gpu(gb.epoch, (ep >> 6) + 1);
+  if (n_st > 1 && blockIdx.x == 0 && tid == 0) st_relaxed_gpu(gb.epoch, (ep >> 6) + 1);
   if constexpr (UM) {  // every warpgroup waited for its last MMA
     tc_fence_before();
     named_bar_sync(1, NW * 32);
@@ -1058,7 +1067,7 @@ cudaError_t launch_gemv1_xform(const Gemv1Config& c, cudaStream_t st) {
 
 template <int BT, int MS, bool UM>
 static const void* g1_kernel() {
-  return reinterpret_cast<const void*>(&paro_gemv1_kernel<g1_nw(BT, UM), BT, MS, UM>);
+  return reinterpret_cast<const void*>(&paro_gemv1_kernel<g1_nw(BT, UM, MS > 1), BT, MS, UM>);
 }
 template <int MS, bool UM>
 static const void* g1_kernel_ms(int BT) {
@@ -1148,7 +1157,7 @@ bool plan_gemv1_chain(int B, int n_stages, const int* n_lin, const int64_t (*Ns)
   CL = g1_env(chain ? "PARO_G1_CHAIN_CL" : "PARO_G1_CL", CL);
   if (CL != 1 && CL != 2 && CL != 4 && CL != 8) CL = 2;
   while (CL > 1 && CL > Gmin) CL /= 2;
-  const int NW = g1_nw(BT, um);
+  const int NW = g1_nw(BT, um, chain);
   const int threads = (NW + 1) * 32;
   c.NW = NW;
   const int budget = device_smem_optin() - 1024;
@@ -1289,7 +1298,7 @@ bool plan_gemv1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, int 
 
 template <int BT, int MS, bool UM>
 static cudaError_t g1_launch(const Gemv1Config& c, cudaLaunchConfig_t* cfg) {
-  auto kern = paro_gemv1_kernel<g1_nw(BT, UM), BT, MS, UM>;
+  auto kern = paro_gemv1_kernel<g1_nw(BT, UM, MS > 1), BT, MS, UM>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(c.a.smem_total));
   if (e != cudaSuccess) return e;
   if constexpr (MS == CHAIN_MAX_STAGES) {

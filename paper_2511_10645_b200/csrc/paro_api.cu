@@ -367,6 +367,32 @@ static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, 
   const int64_t tile_b = k_split ? paro::GEMV1_MAX_B : paro::GEMV_MAX_B;
   for (int64_t b0 = 0; b0 < B; b0 += tile_b) {
     const int live = static_cast<int>(std::min<int64_t>(tile_b, B - b0));
+    if (k_split && live == 1) {  // one token: the one-launch kernel (gemv1_b1.cu)
+      paro::B1Config c1;
+      const char* why = "";
+      if (!paro::plan_gemv1_b1(1, n, Ns, K, rotate, &c1, &why))
+        return fail(PARO_ERR_UNSUPPORTED, "paro_linear: %s", why);
+      paro::B1Args& a = c1.a;
+      a.x = static_cast<const uint8_t*>(x) + b0 * K * xe;
+      a.x_bf16 = x_dtype == PARO_BF16;
+      for (int i = 0; i < n; ++i) {
+        paro::B1Linear& d = a.lin[i];
+        d.codes = static_cast<const uint8_t*>(packed[i].codes);
+        d.scales = static_cast<const uint8_t*>(packed[i].scales);
+        d.zeros = static_cast<const uint8_t*>(packed[i].zeros);
+        d.rot_cs = ov.active ? ov.cs : static_cast<const float2*>(packed[i].rot_cs);
+        d.rot_idx = ov.active ? ov.idx : static_cast<const uchar2*>(packed[i].rot_idx);
+        d.svec = ov.active ? ov.s : static_cast<const float*>(packed[i].svec);
+        d.bias = bias ? bias[i] : nullptr;
+        d.y = static_cast<uint8_t*>(y[i]) + b0 * packed[i].N * ye;
+        d.L = packed[i].n_rot;
+      }
+      a.y_dtype = static_cast<int>(y_dtype);
+      a.pdl = pdl;
+      cudaError_t e = paro::launch_gemv1_b1(c1, cs);
+      if (e != cudaSuccess) return cuda_fail(e, "paro_linear: decode GEMV (B=1) launch");
+      continue;
+    }
     if (k_split) {
       paro::Gemv1Config c1;
       const char* why = "";

@@ -131,6 +131,42 @@ struct Gemv1Config {
   Gemv1Args a;
 };
 
+// The one-launch B = 1 kernel (gemv1_b1.cu; the round-1 design): B = 1 single launches only.
+struct B1Linear {
+  const uint8_t* codes;
+  const uint8_t* scales;
+  const uint8_t* zeros;
+  const float2* rot_cs;
+  const uchar2* rot_idx;
+  const float* svec;
+  const float* bias;
+  void* y;  // [B][N]
+  const uint8_t* xq;  // unused (B = 1)
+  const int2* xqs;    // unused (B = 1)
+  int N, L;
+  int cta_begin, rb_base, rb_extra;
+};
+struct B1Args {
+  const void* x;  // [1][K] fp16 / bf16
+  int x_bf16;
+  int B;
+  int n_lin;
+  B1Linear lin[GEMV_MAX_LIN];
+  int y_dtype;
+  int K, G;
+  int rotate;
+  int pdl;
+  int TPS, S, pre_stages, params_first, atom, skip_math, R_max, RRmax;
+  uint32_t slot_bytes, sc_off, z_off;
+  uint32_t off_xp, off_xs, off_scr, off_part, off_recv, off_bar, off_ring, smem_total;
+};
+struct B1Config {
+  int CL, grid, NW, BT;
+  B1Args a;
+};
+bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, B1Config* cfg, const char** why);
+cudaError_t launch_gemv1_b1(const B1Config& cfg, cudaStream_t st);
+
 bool gemv1_enabled();
 // B > 1: bytes of pre-transformed activations per linear (digits + per-group sums / scales)
 size_t gemv1_xq_bytes(int B, int64_t K);

@@ -8,6 +8,8 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("PARO_PKG_DIR"):
+    sys.path.insert(0, os.path.abspath(os.environ["PARO_PKG_DIR"]))
 import paper_2511_10645_b200 as paro  # noqa: E402
 import synth  # noqa: E402
 

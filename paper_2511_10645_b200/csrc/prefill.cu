@@ -20,9 +20,10 @@
 // order (prefill_pos, tile_layout.cuh): one permutation along K on both operands leaves
 // the contraction unchanged.
 //
-// Warp roles (384 threads, persistent over tiles):
+// Warp roles (512 threads, persistent over tiles):
 //   warp 0: TMA producer (x' tiles)     warp 1: MMA issuer     warp 2: TMEM allocator
-//   warps 4-7: dequant -> TMEM (A)      warps 8-11: epilogue (TMEM -> y)
+//   warps 4-7 / 12-15: dequant -> TMEM (A), even / odd K stages   warps 8-11: epilogue (TMEM -> y)
+// (eight dequant warps: with four the INT4 -> fp16 producer limited the MMA rate)
 #include <cuda.h>
 #include <cuda_fp16.h>
 
@@ -37,15 +38,13 @@
 namespace paro {
 
 constexpr int PF_BM = 128;    // weight rows per tile (MMA M)
-constexpr int PF_BN = 256;    // tokens per tile (MMA N)
 constexpr int PF_BK = 64;     // K per pipeline stage (4 MMAs of K=16)
 constexpr int PF_SX = 4;      // x' shared-memory stages (32 KB each)
-constexpr int PF_SA = 4;      // A (dequantised weight) TMEM stages (32 columns each)
+constexpr int PF_SA = 8;      // A (dequantised weight) TMEM stages (32 columns each)
 constexpr int PF_ACC_COL = 0;
 constexpr int PF_A_COL = 256;
 constexpr int PF_TMEM_COLS = 512;
-constexpr int PF_THREADS = 384;
-constexpr uint32_t PF_X_STAGE_BYTES = PF_BN * PF_BK * 2;
+constexpr int PF_THREADS = 512;
 
 struct PrefillArgs {
   const uint8_t* codes;
@@ -66,8 +65,11 @@ __device__ __forceinline__ uint32_t hsub_hmul(uint32_t v, uint32_t zz, uint32_t 
   return *reinterpret_cast<uint32_t*>(&r);
 }
 
+// PF_BN: tokens per tile (MMA N): 256, or 128 when 256-token tiles would leave SMs idle (k / v)
+template <int PF_BN>
 __global__ void __launch_bounds__(PF_THREADS, 1)
     prefill_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const PrefillArgs a) {
+  constexpr uint32_t PF_X_STAGE_BYTES = PF_BN * PF_BK * 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* xs = smem;  // PF_SX * 32 KB
@@ -146,10 +148,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         mma_commit(acc_full);
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if ((warp >= 4 && warp < 8) || warp >= 12) {
     // ---------------- dequant producer: weight row r of the tile -> TMEM lane r
-    const int r = (warp - 4) * 32 + lane;
-    const uint32_t lane_addr = static_cast<uint32_t>((warp - 4) * 32) << 16;
+    const int par = warp >= 12 ? 1 : 0;  // K-stage parity of this dequant warp set
+    const int r = (warp & 3) * 32 + lane;
+    const uint32_t lane_addr = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const int G = a.K / 128;
     uint32_t it = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -158,11 +161,12 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       const int64_t T0 = static_cast<int64_t>(n / TILE_ROWS) * G;  // first tile of the row block
       // stage ks = half-row (32 bytes) ks & 1 of tile (row block, ks / 2)
       const uint8_t* crow = a.codes + T0 * TILE_CODE_BYTES + rt * 64;
-      uint4 c0 = __ldg(reinterpret_cast<const uint4*>(crow));
-      uint4 c1 = __ldg(reinterpret_cast<const uint4*>(crow + 16));
+      uint4 c0 = __ldg(reinterpret_cast<const uint4*>(crow + par * 32));
+      uint4 c1 = __ldg(reinterpret_cast<const uint4*>(crow + par * 32 + 16));
       uint32_t ss = 0, zz = 0;
-      for (int ks = 0; ks < n_ks; ++ks, ++it) {
-        if ((ks & 1) == 0) {
+      it += par;
+      for (int ks = par; ks < n_ks; ks += 2, it += 2) {
+        {
           const int64_t T = T0 + (ks >> 1);
           const __half S = a.scales[T * TILE_ROWS + tile_scale_idx(rt)];
           const uint8_t zb = a.zeros[T * TILE_ZERO_BYTES + tile_zero_byte(rt)];
@@ -174,8 +178,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           zz = *reinterpret_cast<const uint32_t*>(&Z2);
         }
         const uint4 w0 = c0, w1 = c1;
-        if (ks + 1 < n_ks) {  // prefetch the next 32 code bytes of this row
-          const uint8_t* nx = crow + static_cast<int64_t>((ks + 1) >> 1) * TILE_CODE_BYTES + ((ks + 1) & 1) * 32;
+        if (ks + 2 < n_ks) {  // prefetch this row's next 32 code bytes of my parity
+          const uint8_t* nx = crow + static_cast<int64_t>((ks + 2) >> 1) * TILE_CODE_BYTES + par * 32;
           c0 = __ldg(reinterpret_cast<const uint4*>(nx));
           c1 = __ldg(reinterpret_cast<const uint4*>(nx + 16));
         }
@@ -197,6 +201,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         tc_fence_before();
         mbar_arrive(&a_full[sa]);
       }
+      it -= par;  // it == (tiles so far) * n_ks for both sets (n_ks is even)
     }
   } else if (warp >= 8) {
     // ---------------- epilogue: accumulator lane r = weight row, column = token
@@ -264,12 +269,13 @@ bool prefill_supported(int64_t B, int64_t N, int64_t K) {
   return B >= 1 && N % PF_BM == 0 && K % PF_BK == 0 && K >= PF_BK && N <= (int64_t(1) << 30) && B < (1 << 30);
 }
 
-cudaError_t launch_prefill_gemm(const void* xq, int64_t B, const uint8_t* codes, const uint8_t* scales,
-                                const uint8_t* zeros, const float* bias, void* y, int y_dtype, int64_t N, int64_t K,
-                                int pdl, cudaStream_t st) {
+template <int PF_BN>
+static cudaError_t prefill_launch(const void* xq, int64_t B, const PrefillArgs& a, int64_t N, int pdl,
+                                  cudaStream_t st) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap tmap;
+  const int64_t K = a.K;
   cuuint64_t gdim[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(B)};
   cuuint64_t gstride[1] = {static_cast<cuuint64_t>(K) * 2};
   cuuint32_t box[2] = {PF_BK, PF_BN};
@@ -278,10 +284,9 @@ cudaError_t launch_prefill_gemm(const void* xq, int64_t B, const uint8_t* codes,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  PrefillArgs a{codes, reinterpret_cast<const __half*>(scales), zeros, bias, y, y_dtype, static_cast<int>(B),
-                static_cast<int>(N), static_cast<int>(K), pdl};
-  const size_t smem = 1024 + PF_SX * PF_X_STAGE_BYTES + 256;
-  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(prefill_gemm_kernel), static_cast<int>(smem));
+  const size_t smem = 1024 + PF_SX * PF_BN * PF_BK * 2 + 256;
+  auto kern = prefill_gemm_kernel<PF_BN>;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int64_t tiles = (N / PF_BM) * ((B + PF_BN - 1) / PF_BN);
   const int grid = static_cast<int>(tiles < device_sm_count() ? tiles : device_sm_count());
@@ -297,7 +302,19 @@ cudaError_t launch_prefill_gemm(const void* xq, int64_t B, const uint8_t* codes,
     cfg.attrs = at;
     cfg.numAttrs = 1;
   }
-  return cudaLaunchKernelEx(&cfg, prefill_gemm_kernel, tmap, a);
+  return cudaLaunchKernelEx(&cfg, kern, tmap, a);
+}
+
+cudaError_t launch_prefill_gemm(const void* xq, int64_t B, const uint8_t* codes, const uint8_t* scales,
+                                const uint8_t* zeros, const float* bias, void* y, int y_dtype, int64_t N, int64_t K,
+                                int pdl, cudaStream_t st) {
+  PrefillArgs a{codes, reinterpret_cast<const __half*>(scales), zeros, bias, y, y_dtype, static_cast<int>(B),
+                static_cast<int>(N), static_cast<int>(K), pdl};
+  // 256-token tiles unless they would fill fewer than 3/4 of the SMs (e.g. 1024 x 4096 at 2048
+  // tokens: 64 tiles): then 128-token tiles
+  const int64_t tiles256 = (N / PF_BM) * ((B + 255) / 256);
+  if (tiles256 * 4 < static_cast<int64_t>(device_sm_count()) * 3) return prefill_launch<128>(xq, B, a, N, pdl, st);
+  return prefill_launch<256>(xq, B, a, N, pdl, st);
 }
 
 }  // namespace paro

@@ -554,7 +554,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
       rb = tl0 / G;
       g = tl0 - rb * G;
     }
-    for (int i = warp; i < (a.skip_math ? 0 : nts); i += NW) {
+    for (int i = warp; i < nts; i += NW) {
       if (rb - rho_first != cur) {
         if (cur >= 0) flush();
 #pragma unroll
@@ -852,7 +852,7 @@ static bool plan_try(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t
   c.a.xfirst = env_int("PARO_XFIRST", 1);           // weights wait until the transform loads are out
   c.a.early_stages = env_int("PARO_EARLY_STAGES", 2);  // under PDL: stages requested before that
   c.a.stagger = env_int("PARO_STAGGER", 1);  // first stage lands before the rest of the ring is requested
-  c.a.skip_math = env_int("PARO_SKIP_MATH", 0);  // debug: stream the weights, skip the tile math
+  c.a.skip_math = 0;
   GemvArgs& a = c.a;
   a.n_lin = n_lin;
   a.B = B;

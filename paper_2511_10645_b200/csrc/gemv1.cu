@@ -487,6 +487,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
   };
   auto wait_grid = [&]() {
     if (warp == 0 && !a.nobar) grid_wait_warp(gb, ep + nbar, lane);
+    __syncwarp();  // bar.sync is .aligned: the warp must be converged (lanes left the poll loop apart)
     named_bar_sync(4, NW * 32);
   };
 #pragma unroll 1
@@ -1033,7 +1034,9 @@ size_t gemv1_xq_bytes(int B, int64_t K) {
   if (B <= 1) return 0;
   const int BT = B <= 4 ? 4 : B <= 8 ? 8 : 16;
   const size_t G = static_cast<size_t>(K / 128);
-  return (G * (BT / 4) * 1024 + G * BT * 8 + 255) / 256 * 256;
+  // per group GEMV1_XQ_GROUP_BYTES (4 KB) of x' digits (BT / 4 KB used), then the
+  // per-(group, token) sums / scales at G * 4096
+  return (G * GEMV1_XQ_GROUP_BYTES + G * BT * 8 + 255) / 256 * 256;
 }
 
 cudaError_t launch_gemv1_xform(const Gemv1Config& c, cudaStream_t st) {

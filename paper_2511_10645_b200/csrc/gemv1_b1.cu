@@ -26,7 +26,6 @@ namespace paro {
 namespace {
 constexpr int B1_NW = 16;  // compute warps per CTA (+ 1 producer warp)
 constexpr uint32_t TILE_B = TILE_CODE_BYTES + TILE_SCALE_BYTES + TILE_ZERO_BYTES;
-__device__ __forceinline__ void b1_mark(int) {}
 
 // D(16x8 s32) += A(16x32 u8, row) * B(32x8 s8, col); fragments as in ptx.cuh (imma_16832),
 // not volatile so the scheduler may interleave the four accumulator chains
@@ -86,7 +85,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
 
   if (threadIdx.x < 8) reinterpret_cast<uint32_t*>(smem + a.off_xs + ((gc * BT * 8 + 15) & ~15))[threadIdx.x] = 0u;
   if (threadIdx.x == 0) {
-    b1_mark(0);
     for (int i = 0; i < a.S; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], NW);
@@ -151,7 +149,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
       if (BT > 1) issue_xq();
       named_bar_sync(2, (NW + 1) * 32);
     }
-    if (lane == 0) b1_mark(1);  // every stage issued
     if (CL > 1) cluster_wait();
     return;
   }
@@ -240,7 +237,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
         if (!arrived) {
           __syncwarp();
           named_bar_arrive(2, (NW + 1) * 32);  // my x and parameters are in
-          if (threadIdx.x == 0) b1_mark(2);
           arrived = true;
         }
         __syncwarp();
@@ -259,9 +255,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
             sc[j1] = cs[t].w * a1 + cs[t].z * b1v;
           }
           __syncwarp();
-          if (false && t == 0 && threadIdx.x == 0 && g == warp && b0 == 0) b1_mark(8);
         }
-        if (false && threadIdx.x == 0 && g == warp && b0 == 0) b1_mark(9);
         // x' -> per-(group, token) fixed point and s8 digits (see the header), laid out as B
         // fragments [column set][quad t][column][k-block kb][b0, b1]; column 2 b + dg of a set =
         // digit dg (0 hi, 1 lo) of its token b; k-block kb = 2 p + h covers the low (p = 0) or
@@ -310,7 +304,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
   }
   named_bar_sync(1, NW * 32);  // every x' of the CTA is in shared memory (and BT > 1: part zeroed)
   if (BT > 1 && CL > 1) cluster_arrive();  // my scratch is free: the cluster may now write recv
-  if (threadIdx.x == 0) b1_mark(3);
 
   // ------------------------------------------------------------ phase 2: tiles (a6)
   {
@@ -326,10 +319,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
       const int u0 = st * a.TPS, nt = min(n_tiles, u0 + a.TPS) - u0;
       const int g_lo = ga, pl = gc;
       mbar_wait(&full[slot], phase);
-      if (threadIdx.x == 0 && st == 0) b1_mark(4);
       const uint8_t* sb = ring + static_cast<size_t>(slot) * a.slot_bytes;
-      if (a.skip_math) {  // debug (PARO_G1_SKIP): stream the weights, no tile math
-      } else if constexpr (BT == 1) {
+      if constexpr (BT == 1) {
       int ri = 0, gi = off0 + warp;  // tile warp + k NW of the stage
       while (gi >= pl) {
         gi -= pl;
@@ -500,7 +491,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
 
   // ------------------------------------------------------------ reduction + epilogue (a8)
   named_bar_sync(1, NW * 32);
-  if (threadIdx.x == 0) b1_mark(5);
   if (CL > 1) cluster_wait();  // every CTA of the cluster is running: DSMEM is legal
   const int tid = threadIdx.x;
   for (int idx = tid; idx < R * BT; idx += NW * 32) {
@@ -525,7 +515,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
   named_bar_sync(1, NW * 32);  // my own partials are in recv
   if (CL > 1) mbar_wait(rbar, 0);  // and those of the other CTAs of the cluster
   if (a.pdl) pdl_wait();  // y may still be read by the previous kernel
-  if (threadIdx.x == 0) b1_mark(6);
   for (int idx = tid; idx < my_n * BT; idx += NW * 32) {
     const int rl = idx / BT, b = idx - rl * BT;
     if (b >= B) continue;
@@ -543,7 +532,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
         static_cast<float*>(d.y)[o] = v;
     }
   }
-  if (threadIdx.x == 0) b1_mark(7);
 }
 
 
@@ -667,7 +655,7 @@ bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, B
   a.TPS = TPS;
   a.pre_stages = std::max(0, b1_env("PARO_G1_PRE", 2));
   a.params_first = b1_env("PARO_G1_PF", 1);
-  a.skip_math = b1_env("PARO_G1_SKIP", 0);
+  a.skip_math = 0;
   a.R_max = rmax;
   a.RRmax = (rmax + CL - 1) / CL;
   const int gcm = (G + CL - 1) / CL;

@@ -423,7 +423,7 @@ static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, 
         for (int i = 0; i < n; ++i) {
           uint8_t* base = static_cast<uint8_t*>(ws) + per * i;
           S0.lin[i].xq = base;
-          S0.lin[i].xqs = reinterpret_cast<int2*>(base + static_cast<size_t>(K / kG) * (c1.BT / 4) * 1024);
+          S0.lin[i].xqs = reinterpret_cast<int2*>(base + static_cast<size_t>(K / kG) * paro::GEMV1_XQ_GROUP_BYTES);
         }
         cudaError_t e = paro::launch_gemv1_xform(c1, cs);
         if (e != cudaSuccess) return cuda_fail(e, "paro_linear: decode activation transform launch");
@@ -666,7 +666,7 @@ paro_status paro_linear_chain(int32_t n_stages, const paro_chain_stage* stages, 
         if (B > 1) {
           uint8_t* base = wsb + kChainHdr + xq_per * i;
           d.xq = base;
-          d.xqs = reinterpret_cast<int2*>(base + static_cast<size_t>(p.K / kG) * (c.BT / 4) * 1024);
+          d.xqs = reinterpret_cast<int2*>(base + static_cast<size_t>(p.K / kG) * paro::GEMV1_XQ_GROUP_BYTES);
         }
       }
     }

@@ -169,6 +169,7 @@ cudaError_t launch_gemv1_b1(const B1Config& cfg, cudaStream_t st);
 
 bool gemv1_enabled();
 // B > 1: bytes of pre-transformed activations per linear (digits + per-group sums / scales)
+constexpr size_t GEMV1_XQ_GROUP_BYTES = 4096;  // x' bytes reserved per group in the workspace
 size_t gemv1_xq_bytes(int B, int64_t K);
 // transform pre-kernel of stage 0 (B > 1)
 cudaError_t launch_gemv1_xform(const Gemv1Config& cfg, cudaStream_t st);

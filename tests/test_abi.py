@@ -95,3 +95,25 @@ def test_product_package_never_imports_oracle():
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "oracle/" not in txt, f
+
+
+def test_chain_workspace_and_argument_errors(paro):
+    """paro_linear_chain's host checks: workspace size (grid-barrier header + B > 1 x' buffers) and
+    argument errors reported before any CUDA call."""
+    pk = paro.paro_packed(16, 16, 16, 16, 16, 16, 4096, 4096, 128, 8)
+    pks = (paro.paro_packed * 1)(pk)
+    ys = (ctypes.c_void_p * 1)(16)
+    st = (paro.paro_chain_stage * 2)()
+    for k in range(2):
+        st[k].x = 16
+        st[k].n = 1
+        st[k].packed = ctypes.cast(pks, ctypes.POINTER(paro.paro_packed))
+        st[k].y = ctypes.cast(ys, ctypes.POINTER(ctypes.c_void_p))
+    ws1 = paro._lib.paro_linear_chain_workspace(1, 2, st)
+    ws16 = paro._lib.paro_linear_chain_workspace(16, 2, st)
+    assert ws1 >= 8192 and ws16 >= ws1 + 4 * 32 * 4096            # B > 1: x' of 4 linear slots
+    assert paro._lib.paro_linear_chain_workspace(1, 0, st) == 0
+    # B > 16, and a workspace that is too small
+    assert paro._lib.paro_linear_chain(2, st, 0, 17, 0, 0, 16, ws1, None) == paro.PARO_ERR_UNSUPPORTED
+    assert paro._lib.paro_linear_chain(2, st, 0, 1, 0, 0, 16, 64, None) == paro.PARO_ERR_INVALID_ARGUMENT
+    assert "workspace" in paro.last_error()

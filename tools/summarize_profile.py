@@ -13,8 +13,10 @@ SRC = os.path.join(ROOT, "gpurun_out", "prof")
 dst = os.path.join(ROOT, sys.argv[1])
 os.makedirs(dst, exist_ok=True)
 
-# 1. bench line
+# 1. bench lines
 shutil.copy(os.path.join(SRC, "bench.json"), os.path.join(dst, "bench.json"))
+if os.path.exists(os.path.join(SRC, "bench_long.json")):
+    shutil.copy(os.path.join(SRC, "bench_long.json"), os.path.join(dst, "bench_long.json"))
 
 # 2. launch list of the bench under ncu (gpu__time_duration.sum): per-kernel shares
 rows = [r for r in csv.reader(open(os.path.join(SRC, "launches.csv"))) if len(r) > 10]
@@ -47,16 +49,28 @@ keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__cluster_dim_x", "launch__registers_per_thread", "sm__cycles_active.avg", "sm__cycles_elapsed.avg",
         "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tmem_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_uma.avg.pct_of_peak_sustained_active",
+        "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
-groups = {0: "q_proj+k_proj+v_proj (N=4096,1024,1024, K=4096)", 1: "o_proj (N=4096, K=4096)",
-          2: "gate_proj+up_proj (N=14336 x2, K=4096)", 3: "down_proj (N=4096, K=14336)"}
+groups = {0: "q_proj+k_proj+v_proj (N=4096,1024,1024, K=4096), B=1", 1: "o_proj (N=4096, K=4096), B=1",
+          2: "gate_proj+up_proj (N=14336 x2, K=4096), B=1", 3: "down_proj (N=4096, K=14336), B=1",
+          4: "Qwen3-4B q/k/v (N=4096,1024,1024, K=2560), B=16, mma.sync engine",
+          5: "Qwen3-4B q/k/v (N=4096,1024,1024, K=2560), B=16, tcgen05 engine",
+          "prefill_q": "prefill GEMM q_proj (N=4096, K=4096), 2048 tokens (tcgen05)",
+          "prefill_transform": "prefill activation transform (2048 x 4096)"}
 out = {"note": "ncu --set full --clock-control none, one launch each (tools/prof_multi.py, bs=1, rotation on); "
                "cold caches and ncu's replay: times are not bench values", "groups": {}}
 traffic = 0.0
 for i, name in groups.items():
-    rep = os.path.join(SRC, f"group{i}.ncu-rep")
+    rep = os.path.join(SRC, f"group{i}.ncu-rep" if isinstance(i, int) else f"{i}.ncu-rep")
+    if not os.path.exists(rep):
+        continue
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(raw.splitlines()))
+    if len(r) < 3:
+        continue
     h, u, v = r[0], r[1], r[2]
     m = {}
     stalls = []
@@ -74,8 +88,9 @@ for i, name in groups.items():
     m["top_stalls"] = [s for _, s in sorted(stalls, reverse=True)[:6]]
     out["groups"][name] = m
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-        traffic += m[k]["value"] * scale.get(m[k]["unit"], 1)
+    if isinstance(i, int) and i < 4:  # the bench step's four launches
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            traffic += m[k]["value"] * scale.get(m[k]["unit"], 1)
 json.dump(out, open(os.path.join(dst, "ncu_decode_groups.json"), "w"), indent=1)
 json.dump({"traffic_per_step": round(traffic), "unit": "bytes",
            "source": f"{sys.argv[1]}/ncu_decode_groups.json: dram__bytes_read.sum + dram__bytes_write.sum of the "

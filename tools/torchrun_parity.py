@@ -1,0 +1,82 @@
+"""Multi-GPU parity of the N-sharded linear, one process per GPU:
+  python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+      --master-port 29511 tools/torchrun_parity.py [N_rows K B]
+Every rank generates the same seeded W / x / transform, packs its row shard (paro_pack on the slice
+== the slice of the full pack), runs paro_linear_allgather (GEMV on the shard + ncclAllGather + the
+[G][B][N/G] -> [B][N] permute), and rank 0 checks sampled rows of the gathered y against the fp64
+oracle (normwise 2e-3) and that every rank holds the same y; then GEMV-only vs GEMV + all-gather
+device times (max over ranks).  Defaults: the LLaMA-3-70B gate projection (28672 x 8192), B = 1."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import oracle as O  # noqa: E402
+import paper_2511_10645_b200 as paro  # noqa: E402
+import synth  # noqa: E402
+from paper_2511_10645_b200 import dist as pd  # noqa: E402
+
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 28672
+K = int(sys.argv[2]) if len(sys.argv) > 2 else 8192
+B = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ.get("LOCAL_RANK", 0))
+dist.init_process_group("nccl", init_method="env://")
+torch.cuda.set_device(local)
+dev = torch.device("cuda", local)
+p = synth.make_problem(N, K, B, seed=2025)
+r0, r1 = paro.shard_rows(N, world, rank)
+W = torch.from_numpy(p["W"][r0:r1]).to(dev)
+s, th, pr, x = (torch.from_numpy(p[k]).to(dev) for k in ("s", "theta", "pairs", "x"))
+packed = paro.paro_pack(W, s, th, pr)
+comm = pd.make_comm(rank, world)
+st = torch.cuda.Stream()
+with torch.cuda.stream(st):
+    y = paro.paro_linear_allgather(x, packed, comm, rank, world, flags=paro.PARO_LINEAR_PDL, stream=st)
+    st.synchronize()
+paro.paro_comm_check(comm)
+# every rank holds the same y
+yall = [torch.empty_like(y) for _ in range(world)]
+dist.all_gather(yall, y)
+same = all(torch.equal(yall[0], t) for t in yall)
+
+
+def dev_us(fn, reps=20):
+    with torch.cuda.stream(st):
+        fn()
+        st.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for _ in range(reps):
+                fn()
+        g.replay()
+        st.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        g.replay()
+        e1.record(st)
+        e1.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / reps * 1e3], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+ysh = torch.empty((B, r1 - r0), dtype=torch.float16, device=dev)
+us_gemv = dev_us(lambda: paro.paro_linear(x, packed, y=ysh, flags=paro.PARO_LINEAR_PDL, stream=st))
+us_tot = dev_us(lambda: paro.paro_linear_allgather(x, packed, comm, rank, world, y=y, flags=paro.PARO_LINEAR_PDL,
+                                                   stream=st))
+if rank == 0:
+    rows = np.sort(np.random.default_rng(7).choice(N, size=min(64, N), replace=False))
+    ref = O.oracle_pack(p["W"][rows], p["s"], p["theta"], p["pairs"])
+    y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"])
+    err = O.normwise_error(y.float().cpu().numpy()[:, rows], y_ref)
+    ok = err <= 2e-3 and same
+    print(f"world={world} N={N} K={K} B={B}: normwise err {err:.2e} (<= 2e-3), ranks agree {same}; "
+          f"GEMV {us_gemv:.2f} us, GEMV + all-gather {us_tot:.2f} us (all-gather {us_tot - us_gemv:.2f} us)"
+          f" -> {'PASS' if ok else 'FAIL'}", flush=True)
+paro.paro_comm_destroy(comm)
+dist.destroy_process_group()

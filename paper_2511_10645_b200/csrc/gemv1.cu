@@ -487,8 +487,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
   };
   auto wait_grid = [&]() {
     if (warp == 0 && !a.nobar) grid_wait_warp(gb, ep + nbar, lane);
-    __syncwarp();  // bar.sync is .aligned: the warp must be converged (lanes left the poll loop apart)
-    named_bar_sync(4, NW * 32);
+    // reached from different call sites (per warp) after lanes left the poll loop apart: the
+    // non-.aligned barrier form
+    named_bar_sync_na(4, NW * 32);
   };
 #pragma unroll 1
   for (int s = 0; s < n_st; ++s) {

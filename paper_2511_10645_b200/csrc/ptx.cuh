@@ -147,6 +147,10 @@ PARO_DEV void st_cluster_u32(uint32_t addr, uint32_t v) {
 PARO_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+// non-.aligned form: the threads of a warp may reach it from different branches
+PARO_DEV void named_bar_sync_na(uint32_t id, uint32_t nthreads) {
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 PARO_DEV void named_bar_arrive(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -702,6 +702,9 @@ bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, B
       for (int tps = 2 * NW; tps >= 8 && !best; tps -= 4)
         if (stages_of(tps) >= std::min<int64_t>(want, (cta_tiles + tps - 1) / tps)) best = tps;
     TPS = best ? best : 8;
+    // long-K launches (few groups per CTA in rows, many tiles): a third ring slot of 28 tiles beats
+    // two of 32 (LLaMA-3-8B down_proj 10.3 -> 9.7 us, same box, tools/ab_knobs.sh)
+    if (G >= 64 && TPS == 32 && stages_of(28) >= 3 && stages_of(32) < 3) TPS = 28;
   }
   a.TPS = TPS;
   a.sc_off = static_cast<uint32_t>(TPS) * TILE_CODE_BYTES;

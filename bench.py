@@ -579,11 +579,17 @@ def measure_70b_mlp(torch, paro, dev, stream, comm, rank, world):
     ysh = {n: torch.zeros((1, N // world), dtype=torch.float16, device=dev) for n, (N, K) in shapes.items()}
     ws = torch.empty(16 << 20, dtype=torch.uint8, device=dev)
     out = {"world": world}
-    tot = {"gemv_us": 0.0, "total_us": 0.0}
+    tot = {"gemv_us": 0.0, "total_us": 0.0, "p2p_total_us": 0.0}
+    from paper_2511_10645_b200 import dist as pd
+    p2p = {}
+    for name, (N, K) in shapes.items():
+        buf, ptrs, opened = pd.make_p2p(rank, world, N, torch.float16, device=dev) if world > 1 else \
+            (paro.p2p_buffer(N, 1, torch.float16, device=dev), None, [])
+        p2p[name] = (buf, ptrs if ptrs is not None else [buf.data_ptr()], opened)
     for name, (N, K) in shapes.items():
         xin = ys["up_proj"] if name == "down_proj" else x
         res = {}
-        for tag in ("gemv", "total", "norot"):
+        for tag in ("gemv", "total", "norot", "p2p"):
             cnt = [0]
 
             def call():
@@ -592,6 +598,10 @@ def measure_70b_mlp(torch, paro, dev, stream, comm, rank, world):
                 if tag == "total" and world > 1:
                     paro.paro_linear_allgather(xin, pk, comm, rank, world, y=ys[name], flags=paro.PARO_LINEAR_PDL,
                                                workspace=ws, stream=stream)
+                elif tag == "p2p":  # the NVLink-native exchange (GEMV epilogue peer stores + flags)
+                    buf, ptrs, _ = p2p[name]
+                    paro.paro_linear_allgather_p2p(xin, pk, ptrs, rank, world, buf, flags=paro.PARO_LINEAR_PDL,
+                                                   stream=stream)
                 else:
                     fl = paro.PARO_LINEAR_NO_ROTATION if tag == "norot" else 0
                     paro.paro_linear(xin, pk, y=ysh[name], flags=fl | paro.PARO_LINEAR_PDL, workspace=ws,
@@ -605,16 +615,21 @@ def measure_70b_mlp(torch, paro, dev, stream, comm, rank, world):
             res[tag] = us
         nbytes = algorithmic_bytes(N // world, K, 1)[0]
         out[name] = {"gemv_us": round(res["gemv"], 2), "allgather_us": round(res["total"] - res["gemv"], 2),
-                     "total_us": round(res["total"], 2), "GBps_per_gpu": round(nbytes / res["gemv"] / 1e3, 1),
+                     "total_us": round(res["total"], 2), "p2p_total_us": round(res["p2p"], 2),
+                     "GBps_per_gpu": round(nbytes / res["gemv"] / 1e3, 1),
                      "rot_overhead": round(res["gemv"] / res["norot"] - 1.0, 4)}
         tot["gemv_us"] += res["gemv"]
         tot["total_us"] += res["total"]
+        tot["p2p_total_us"] += res["p2p"]
     all_bytes = sum(algorithmic_bytes(N, K, 1)[0] for N, K in shapes.values())
     out["mlp"] = {"gemv_us": round(tot["gemv_us"], 2), "allgather_us": round(tot["total_us"] - tot["gemv_us"], 2),
-                  "total_us": round(tot["total_us"], 2),
+                  "total_us": round(tot["total_us"], 2), "p2p_total_us": round(tot["p2p_total_us"], 2),
                   "aggregate_GBps": round(all_bytes / tot["total_us"] / 1e3, 1),
                   "def": "one call per linear (gate, up, down reading up's y), each timed alone in a graph of 20"}
-    del pool
+    for buf, ptrs, opened in p2p.values():
+        for q in opened:
+            paro.paro_ipc_close_handle(q)
+    del pool, p2p
     torch.cuda.empty_cache()
     return out
 

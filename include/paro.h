@@ -288,6 +288,26 @@ paro_status paro_linear_allgather(const void* x, paro_dtype x_dtype, int64_t B, 
                                   void* stream);
 
 /* Message of the last error on the calling thread ("" if none). */
+/* ---- NVLink-native all-gather of y ----
+ * The N-sharded decode linear without NCCL: rank r's GEMV epilogue stores each of its y values
+ * straight into EVERY rank's y_full (P2P stores over NVLink / NVSwitch through CUDA IPC peer
+ * pointers) at columns [r Ns, (r+1) Ns), and the last of its CTAs releases flag[r] on every rank
+ * (system scope); a one-thread wait kernel then holds the stream until all ranks' flags arrived.
+ * Per-rank buffer (paro_p2p_buffer_bytes, zero before first use, never reset): y_full [1][N_full]
+ * of y_dtype, then the flags / epoch / CTA counter.  Epochs advance once per call on every rank, so
+ * calls must be matched across ranks (same order), and the buffers may be captured in CUDA graphs.
+ *   peer_bufs  host array [world]: the device pointer of every rank's buffer as seen from this
+ *              process (own rank: its local pointer; others: paro_ipc_open_handle)
+ *   B          must be 1 (decode).  Errors as paro_linear_allgather; PARO_ERR_UNSUPPORTED for B != 1.
+ * The result is this rank's y_full (its own buffer) once the call's kernels ran on `stream`. */
+size_t paro_p2p_buffer_bytes(int64_t B, int64_t N_full, paro_dtype y_dtype, int32_t world);
+paro_status paro_ipc_get_handle(const void* dev_ptr, void* handle /* 64 bytes, host */);
+paro_status paro_ipc_open_handle(const void* handle, void** dev_ptr);
+paro_status paro_ipc_close_handle(void* dev_ptr);
+paro_status paro_linear_allgather_p2p(const void* x, paro_dtype x_dtype, int64_t B, const paro_packed* packed_shard,
+                                      const float* bias_shard, paro_dtype y_dtype, uint32_t flags,
+                                      void* const* peer_bufs, int32_t rank, int32_t world, void* stream);
+
 const char* paro_last_error(void);
 /* Library version string. */
 const char* paro_version(void);

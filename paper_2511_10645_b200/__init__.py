@@ -75,6 +75,12 @@ SIGNATURES = {
     "paro_linear_allgather": (ctypes.c_int, [_P, ctypes.c_int, _I64, _PP, _P, _P, ctypes.c_int, _U32, _P, _SZ, _P,
                                              _I32, _I32, _P]),
     "paro_select_pairs": (ctypes.c_int, [_I64, _I32, _I32, _I32, ctypes.c_uint64, _P]),
+    "paro_p2p_buffer_bytes": (_SZ, [_I64, _I64, ctypes.c_int, _I32]),
+    "paro_ipc_get_handle": (ctypes.c_int, [_P, _P]),
+    "paro_ipc_open_handle": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_void_p)]),
+    "paro_ipc_close_handle": (ctypes.c_int, [_P]),
+    "paro_linear_allgather_p2p": (ctypes.c_int, [_P, ctypes.c_int, _I64, _PP, _P, ctypes.c_int, _U32,
+                                                 ctypes.POINTER(ctypes.c_void_p), _I32, _I32, _P]),
     "paro_fwht": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _P, ctypes.c_float, _P, _P]),
     "paro_last_error": (ctypes.c_char_p, []),
     "paro_version": (ctypes.c_char_p, []),
@@ -350,6 +356,48 @@ def paro_linear_allgather(x, packed_shard: PackedLinear, comm: int, rank: int, w
     _check(_lib.paro_linear_allgather(_ptr(x), _dt(x), B, ctypes.byref(st), _ptr(bias_shard), _ptr(y), _dt(y), flags,
                                       _ptr(workspace), workspace.numel(), comm, rank, world, _stream(stream)))
     return y
+
+
+# ---------------------------------------------------------------- NVLink-native all-gather (P2P)
+def p2p_buffer(N_full: int, world: int, out_dtype=None, device="cuda"):
+    """Zeroed per-rank exchange buffer (y_full + flags) for paro_linear_allgather_p2p."""
+    torch = _torch()
+    dt = out_dtype or torch.float16
+    nb = int(_lib.paro_p2p_buffer_bytes(1, N_full, _dt(torch.empty(0, dtype=dt)), world))
+    if nb == 0:
+        raise ParoError(PARO_ERR_INVALID_ARGUMENT, "bad p2p buffer arguments")
+    return torch.zeros(nb, dtype=torch.uint8, device=device)
+
+
+def paro_ipc_get_handle(t) -> bytes:
+    buf = ctypes.create_string_buffer(64)
+    _check(_lib.paro_ipc_get_handle(_ptr(t), buf))
+    return buf.raw
+
+
+def paro_ipc_open_handle(handle: bytes) -> int:
+    p = ctypes.c_void_p()
+    _check(_lib.paro_ipc_open_handle(ctypes.create_string_buffer(handle, 64), ctypes.byref(p)))
+    return p.value
+
+
+def paro_ipc_close_handle(ptr: int) -> None:
+    _check(_lib.paro_ipc_close_handle(ptr))
+
+
+def paro_linear_allgather_p2p(x, packed_shard: PackedLinear, peer_ptrs: list, rank: int, world: int, local_buf,
+                              bias_shard=None, out_dtype=None, flags: int = 0, stream=None):
+    """y_full [1, N] on every rank: this rank's shard GEMV stores into all ranks' buffers over NVLink
+    (include/paro.h, paro_linear_allgather_p2p); returns the view of y_full in local_buf."""
+    torch = _torch()
+    dt = out_dtype or x.dtype
+    N_full = packed_shard.N * world
+    ptrs = (ctypes.c_void_p * world)(*peer_ptrs)
+    st = packed_shard.struct()
+    _check(_lib.paro_linear_allgather_p2p(_ptr(x), _dt(x), x.shape[0], ctypes.byref(st), _ptr(bias_shard),
+                                          _dt(torch.empty(0, dtype=dt)), flags, ptrs, rank, world, _stream(stream)))
+    es = torch.empty(0, dtype=dt).element_size()
+    return local_buf[:N_full * es].view(dt).view(1, N_full)
 
 
 def shard_rows(N: int, world: int, rank: int) -> tuple[int, int]:

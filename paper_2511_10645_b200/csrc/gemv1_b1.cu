@@ -523,15 +523,66 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
     const int64_t n = static_cast<int64_t>(rb0) * TILE_ROWS + my_lo + rl;
     if (n < d.N) {
       if (d.bias) v += __ldg(d.bias + n);
-      const int64_t o = static_cast<int64_t>(b) * d.N + n;
-      if (a.y_dtype == 0)
-        static_cast<__half*>(d.y)[o] = __float2half_rn(v);
-      else if (a.y_dtype == 1)
-        static_cast<__nv_bfloat16*>(d.y)[o] = __float2bfloat16_rn(v);
-      else
-        static_cast<float*>(d.y)[o] = v;
+      if (!a.p2p) {
+        const int64_t o = static_cast<int64_t>(b) * d.N + n;
+        if (a.y_dtype == 0)
+          static_cast<__half*>(d.y)[o] = __float2half_rn(v);
+        else if (a.y_dtype == 1)
+          static_cast<__nv_bfloat16*>(d.y)[o] = __float2bfloat16_rn(v);
+        else
+          static_cast<float*>(d.y)[o] = v;
+      } else {
+        // NVLink-native all-gather: this rank's columns of every rank's y_full (P2P stores)
+        const int64_t o = static_cast<int64_t>(b) * a.y_ld + a.y_col0 + n;
+        for (int p = 0; p < a.world; ++p) {
+          if (a.y_dtype == 0)
+            static_cast<__half*>(a.peer_y[p])[o] = __float2half_rn(v);
+          else if (a.y_dtype == 1)
+            static_cast<__nv_bfloat16*>(a.peer_y[p])[o] = __float2bfloat16_rn(v);
+          else
+            static_cast<float*>(a.peer_y[p])[o] = v;
+        }
+      }
     }
   }
+  if (a.p2p) {
+    // every CTA's peer stores are ordered (system scope) before its arrival; the last CTA to arrive
+    // releases this rank's flag on every rank
+    named_bar_sync(1, NW * 32);
+    if (tid == 0) {
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      uint32_t old;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.done_ctr) : "memory");
+      if (old == gridDim.x - 1) {
+        asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(a.done_ctr) : "memory");
+        const uint32_t e = *a.epoch + 1u;
+        for (int p = 0; p < a.world; ++p)
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.peer_flags[p] + a.rank), "r"(e) : "memory");
+      }
+    }
+  }
+}
+
+// The consumer side of the NVLink-native all-gather: one thread waits until every rank released
+// its flag for this exchange (epoch + 1), then advances the local epoch.
+__global__ void p2p_wait_kernel(uint32_t* flags, uint32_t* epoch, int world) {
+  if (threadIdx.x != 0) return;
+  const uint32_t e = *epoch + 1u;
+  const uint64_t t0 = globaltimer_ns();
+  for (int q = 0; q < world; ++q) {
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + q) : "memory");
+      if (static_cast<int>(v - e) >= 0) break;
+      if (globaltimer_ns() - t0 > 4000000000ull) __trap();  // a peer never signalled
+    }
+  }
+  *epoch = e;
+}
+
+cudaError_t launch_p2p_wait(uint32_t* flags, uint32_t* epoch, int world, cudaStream_t st) {
+  p2p_wait_kernel<<<1, 32, 0, st>>>(flags, epoch, world);
+  return cudaGetLastError();
 }
 
 

@@ -865,4 +865,94 @@ paro_status paro_linear_allgather(const void* x, paro_dtype x_dtype, int64_t B, 
   return PARO_OK;
 }
 
+// ---------------------------------------------------------------- NVLink-native all-gather (P2P)
+static size_t p2p_y_bytes(int64_t B, int64_t N_full, paro_dtype y_dtype) {
+  return align256(static_cast<size_t>(B * N_full) * dtype_bytes(y_dtype));
+}
+
+size_t paro_p2p_buffer_bytes(int64_t B, int64_t N_full, paro_dtype y_dtype, int32_t world) {
+  if (B < 1 || N_full < 1 || world < 1 || world > paro::PARO_P2P_MAX_WORLD) return 0;
+  return p2p_y_bytes(B, N_full, y_dtype) + 256;  // + flags[world], epoch, CTA counter
+}
+
+paro_status paro_ipc_get_handle(const void* dev_ptr, void* handle) {
+  if (!dev_ptr || !handle) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_ipc_get_handle: NULL argument");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  std::memcpy(handle, &h, sizeof(h));
+  return PARO_OK;
+}
+
+paro_status paro_ipc_open_handle(const void* handle, void** dev_ptr) {
+  if (!dev_ptr || !handle) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_ipc_open_handle: NULL argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  return PARO_OK;
+}
+
+paro_status paro_ipc_close_handle(void* dev_ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
+  return PARO_OK;
+}
+
+paro_status paro_linear_allgather_p2p(const void* x, paro_dtype x_dtype, int64_t B, const paro_packed* packed_shard,
+                                      const float* bias_shard, paro_dtype y_dtype, uint32_t flags,
+                                      void* const* peer_bufs, int32_t rank, int32_t world, void* stream) {
+  paro_status st = check_packed(packed_shard);
+  if (st != PARO_OK) return st;
+  if (B != 1) return fail(PARO_ERR_UNSUPPORTED, "paro_linear_allgather_p2p: one token per call (decode)");
+  if (world < 1 || world > paro::PARO_P2P_MAX_WORLD || rank < 0 || rank >= world || !peer_bufs)
+    return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear_allgather_p2p: bad rank/world/peer_bufs");
+  for (int p = 0; p < world; ++p)
+    if (!peer_bufs[p] || !aligned16(peer_bufs[p]))
+      return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear_allgather_p2p: peer buffer %d NULL/misaligned", p);
+  if (!x || !aligned16(x)) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_linear_allgather_p2p: bad x");
+  if (x_dtype != PARO_F16 && x_dtype != PARO_BF16) return fail(PARO_ERR_UNSUPPORTED, "x must be fp16 or bf16");
+  if (y_dtype != PARO_F16 && y_dtype != PARO_BF16 && y_dtype != PARO_F32)
+    return fail(PARO_ERR_UNSUPPORTED, "y must be fp16, bf16 or fp32");
+  const int64_t Ns = packed_shard->N, K = packed_shard->K, N_full = Ns * world;
+  paro::B1Config c;
+  const char* why = "";
+  if (!paro::plan_gemv1_b1(1, 1, &Ns, K, (flags & PARO_LINEAR_NO_ROTATION) ? 0 : 1, &c, &why))
+    return fail(PARO_ERR_UNSUPPORTED, "paro_linear_allgather_p2p: %s", why);
+  paro::B1Args& a = c.a;
+  a.x = x;
+  a.x_bf16 = x_dtype == PARO_BF16;
+  paro::B1Linear& d = a.lin[0];
+  d.codes = static_cast<const uint8_t*>(packed_shard->codes);
+  d.scales = static_cast<const uint8_t*>(packed_shard->scales);
+  d.zeros = static_cast<const uint8_t*>(packed_shard->zeros);
+  d.rot_cs = static_cast<const float2*>(packed_shard->rot_cs);
+  d.rot_idx = static_cast<const uchar2*>(packed_shard->rot_idx);
+  d.svec = static_cast<const float*>(packed_shard->svec);
+  d.bias = bias_shard;
+  d.y = peer_bufs[rank];
+  d.L = packed_shard->n_rot;
+  a.y_dtype = static_cast<int>(y_dtype);
+  a.pdl = (flags & PARO_LINEAR_PDL) ? 1 : 0;
+  const size_t yb = p2p_y_bytes(1, N_full, y_dtype);
+  a.p2p = 1;
+  a.world = world;
+  a.rank = rank;
+  a.y_ld = N_full;
+  a.y_col0 = static_cast<int64_t>(rank) * Ns;
+  for (int p = 0; p < world; ++p) {
+    a.peer_y[p] = peer_bufs[p];
+    a.peer_flags[p] = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(peer_bufs[p]) + yb);
+  }
+  uint32_t* local_flags = a.peer_flags[rank];
+  uint32_t* epoch = local_flags + 32;
+  a.epoch = epoch;
+  a.done_ctr = local_flags + 48;
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  cudaError_t e = paro::launch_gemv1_b1(c, cs);
+  if (e == cudaSuccess) e = paro::launch_p2p_wait(local_flags, epoch, world, cs);
+  if (e != cudaSuccess) return cuda_fail(e, "paro_linear_allgather_p2p");
+  return PARO_OK;
+}
+
 }  // extern "C"

@@ -131,6 +131,7 @@ struct Gemv1Config {
   Gemv1Args a;
 };
 
+constexpr int PARO_P2P_MAX_WORLD = 8;
 // The one-launch B = 1 kernel (gemv1_b1.cu; the round-1 design): B = 1 single launches only.
 struct B1Linear {
   const uint8_t* codes;
@@ -159,12 +160,23 @@ struct B1Args {
   int TPS, S, pre_stages, params_first, atom, skip_math, R_max, RRmax;
   uint32_t slot_bytes, sc_off, z_off;
   uint32_t off_xp, off_xs, off_scr, off_part, off_recv, off_bar, off_ring, smem_total;
+  // NVLink-native all-gather (paro_linear_allgather_p2p): the epilogue stores every y value into
+  // each rank's y_full (peer pointers over NVLink) at columns y_col0 + n of rows of length y_ld, and
+  // the last CTA to finish releases flag[rank] = epoch + 1 on every rank (system scope)
+  int p2p, world, rank;
+  int64_t y_ld, y_col0;
+  void* peer_y[PARO_P2P_MAX_WORLD];
+  uint32_t* peer_flags[PARO_P2P_MAX_WORLD];
+  uint32_t* done_ctr;  // local: CTAs finished (the last one resets it)
+  const uint32_t* epoch;  // local: exchanges completed so far (advanced by the wait kernel)
 };
 struct B1Config {
   int CL, grid, NW, BT;
   B1Args a;
 };
 bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, B1Config* cfg, const char** why);
+// waits until every rank's flag reached this rank's epoch + 1, then advances the epoch
+cudaError_t launch_p2p_wait(uint32_t* flags, uint32_t* epoch, int world, cudaStream_t st);
 cudaError_t launch_gemv1_b1(const B1Config& cfg, cudaStream_t st);
 
 bool gemv1_enabled();

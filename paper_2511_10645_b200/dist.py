@@ -49,3 +49,24 @@ def max_over_ranks(value: float, device=None, group=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+def make_p2p(rank: int, world: int, N_full: int, out_dtype=None, device=None, group=None):
+    """Exchange buffers for paro_linear_allgather_p2p: every rank allocates one (zeroed), shares
+    its CUDA IPC handle over the process group and opens the peers'.  Returns (local_buf,
+    peer_ptrs, opened) -- close `opened` with paro_ipc_close_handle when done."""
+    import torch.distributed as dist
+
+    import paper_2511_10645_b200 as paro
+    buf = paro.p2p_buffer(N_full, world, out_dtype, device=device)
+    handles = [None] * world
+    dist.all_gather_object(handles, paro.paro_ipc_get_handle(buf), group=group)
+    ptrs, opened = [], []
+    for q in range(world):
+        if q == rank:
+            ptrs.append(buf.data_ptr())
+        else:
+            p = paro.paro_ipc_open_handle(handles[q])
+            ptrs.append(p)
+            opened.append(p)
+    return buf, ptrs, opened

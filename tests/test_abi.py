@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def declared_functions():
     src = open(os.path.join(ROOT, "include", "paro.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(paro_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(paro_[a-z0-9_]+)\s*\(", src)))
 
 
 @pytest.fixture(scope="module")
@@ -29,7 +29,7 @@ def test_header_declares_the_boundary():
     for f in ["paro_pack_sizes", "paro_pack", "paro_linear", "paro_linear_multi", "paro_linear_workspace",
               "paro_transform_activations",
               "paro_unpack_logical", "paro_comm_unique_id", "paro_comm_init", "paro_comm_destroy",
-              "paro_linear_allgather", "paro_linear_allgather_workspace", "paro_select_pairs", "paro_fwht", "paro_linear_chain", "paro_linear_chain_workspace", "paro_last_error",
+              "paro_linear_allgather", "paro_linear_allgather_workspace", "paro_select_pairs", "paro_fwht", "paro_linear_chain", "paro_linear_allgather_p2p", "paro_ipc_get_handle", "paro_linear_chain_workspace", "paro_last_error",
               "paro_version"]:
         assert f in fns
 

@@ -145,3 +145,22 @@ def test_llama8b_bench_step_launches(paro, group):
     shapes = {"qkv": [(4096, 4096), (1024, 4096), (1024, 4096)], "o": [(4096, 4096)],
               "gate_up": [(14336, 4096), (14336, 4096)], "down": [(4096, 14336)]}[group]
     _multi_sampled(paro, shapes, 1, 500 + len(group), flags=paro.PARO_LINEAR_PDL)
+
+
+def test_allgather_p2p_world1(paro):
+    """SURVEY.md 8(f) NEXT #4 at world = 1: the NVLink-native exchange (the B = 1 GEMV epilogue
+    storing into every rank's y_full through peer pointers, flags released by the last CTA, the
+    wait kernel) with this process as the only rank; repeated calls advance the epoch."""
+    p = synth.make_problem(512, 1024, 1, seed=430, with_bias=True)
+    t = dev_tensors(p)
+    packed, ref = check_pack(paro, p, t)
+    buf = paro.p2p_buffer(512, 1, torch.float16)
+    assert len(paro.paro_ipc_get_handle(buf)) == 64
+    for _ in range(3):
+        y = paro.paro_linear_allgather_p2p(t["x"], packed, [buf.data_ptr()], 0, 1, buf, bias_shard=t["bias"],
+                                           flags=paro.PARO_LINEAR_PDL)
+    torch.cuda.synchronize()
+    y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"], bias=p["bias"])
+    assert O.normwise_error(y.float().cpu().numpy(), y_ref) <= TOL
+    words = buf[-256:].view(torch.int32).cpu().numpy()
+    assert words[32 + 0] == 3 and words[0] == 3, "three exchanges: flag and epoch at 3"

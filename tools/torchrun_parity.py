@@ -69,7 +69,23 @@ ysh = torch.empty((B, r1 - r0), dtype=torch.float16, device=dev)
 us_gemv = dev_us(lambda: paro.paro_linear(x, packed, y=ysh, flags=paro.PARO_LINEAR_PDL, stream=st))
 us_tot = dev_us(lambda: paro.paro_linear_allgather(x, packed, comm, rank, world, y=y, flags=paro.PARO_LINEAR_PDL,
                                                    stream=st))
+# the NVLink-native exchange (B = 1): peer stores from the GEMV epilogue + flags, no NCCL
+p2p_ok, us_p2p = None, None
+if B == 1:
+    buf, ptrs, opened = pd.make_p2p(rank, world, N, torch.float16, device=dev)
+    with torch.cuda.stream(st):
+        y2 = paro.paro_linear_allgather_p2p(x, packed, ptrs, rank, world, buf, flags=paro.PARO_LINEAR_PDL, stream=st)
+        st.synchronize()
+    p2p_ok = bool(torch.equal(y2, y))
+    us_p2p = dev_us(lambda: paro.paro_linear_allgather_p2p(x, packed, ptrs, rank, world, buf,
+                                                           flags=paro.PARO_LINEAR_PDL, stream=st))
+    dist.barrier()
+    for q in opened:
+        paro.paro_ipc_close_handle(q)
 if rank == 0:
+    if p2p_ok is not None:
+        print(f"world={world}: NVLink P2P exchange == NCCL all-gather: {p2p_ok}; GEMV + P2P exchange {us_p2p:.2f} us",
+              flush=True)
     rows = np.sort(np.random.default_rng(7).choice(N, size=min(64, N), replace=False))
     ref = O.oracle_pack(p["W"][rows], p["s"], p["theta"], p["pairs"])
     y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"])

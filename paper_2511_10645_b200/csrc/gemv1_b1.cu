@@ -546,15 +546,17 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
     }
   }
   if (a.p2p) {
-    // every CTA's peer stores are ordered (system scope) before its arrival; the last CTA to arrive
-    // releases this rank's flag on every rank
+    // every CTA's peer stores are ordered before its arrival (release at GPU scope); the last CTA to
+    // arrive acquires them all and its system-scope release -- cumulative over what it observed --
+    // publishes this rank's flag on every rank
     named_bar_sync(1, NW * 32);
     if (tid == 0) {
-      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
       uint32_t old;
       asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.done_ctr) : "memory");
       if (old == gridDim.x - 1) {
         asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(a.done_ctr) : "memory");
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
         const uint32_t e = *a.epoch + 1u;
         for (int p = 0; p < a.world; ++p)
           asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.peer_flags[p] + a.rank), "r"(e) : "memory");
@@ -566,6 +568,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
 // The consumer side of the NVLink-native all-gather: one thread waits until every rank released
 // its flag for this exchange (epoch + 1), then advances the local epoch.
 __global__ void p2p_wait_kernel(uint32_t* flags, uint32_t* epoch, int world) {
+  // the next kernel may start its prologue (weight prefetch) now; its PDL wait still waits for this
+  // kernel's completion before it reads y_full
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (threadIdx.x != 0) return;
   const uint32_t e = *epoch + 1u;
   const uint64_t t0 = globaltimer_ns();
@@ -580,9 +585,20 @@ __global__ void p2p_wait_kernel(uint32_t* flags, uint32_t* epoch, int world) {
   *epoch = e;
 }
 
-cudaError_t launch_p2p_wait(uint32_t* flags, uint32_t* epoch, int world, cudaStream_t st) {
-  p2p_wait_kernel<<<1, 32, 0, st>>>(flags, epoch, world);
-  return cudaGetLastError();
+cudaError_t launch_p2p_wait(uint32_t* flags, uint32_t* epoch, int world, int pdl, cudaStream_t st) {
+  // under PDL the wait starts while the GEMV still runs (the GEMV triggers its dependents at its
+  // start): it only polls flags the GEMV's last CTA releases, and reads the epoch, which the
+  // previous wait kernel wrote before this GEMV could start
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(32);
+  cfg.stream = st;
+  cudaLaunchAttribute at;
+  at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, p2p_wait_kernel, flags, epoch, world);
 }
 
 

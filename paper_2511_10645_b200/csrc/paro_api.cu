@@ -950,7 +950,7 @@ paro_status paro_linear_allgather_p2p(const void* x, paro_dtype x_dtype, int64_t
   a.done_ctr = local_flags + 48;
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   cudaError_t e = paro::launch_gemv1_b1(c, cs);
-  if (e == cudaSuccess) e = paro::launch_p2p_wait(local_flags, epoch, world, cs);
+  if (e == cudaSuccess) e = paro::launch_p2p_wait(local_flags, epoch, world, 0, cs);
   if (e != cudaSuccess) return cuda_fail(e, "paro_linear_allgather_p2p");
   return PARO_OK;
 }

@@ -176,7 +176,7 @@ struct B1Config {
 };
 bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, B1Config* cfg, const char** why);
 // waits until every rank's flag reached this rank's epoch + 1, then advances the epoch
-cudaError_t launch_p2p_wait(uint32_t* flags, uint32_t* epoch, int world, cudaStream_t st);
+cudaError_t launch_p2p_wait(uint32_t* flags, uint32_t* epoch, int world, int pdl, cudaStream_t st);
 cudaError_t launch_gemv1_b1(const B1Config& cfg, cudaStream_t st);
 
 bool gemv1_enabled();

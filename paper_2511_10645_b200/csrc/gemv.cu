@@ -852,7 +852,6 @@ static bool plan_try(int B, int n_lin, const int64_t* Ns, const int* Ls, int64_t
   c.a.xfirst = env_int("PARO_XFIRST", 1);           // weights wait until the transform loads are out
   c.a.early_stages = env_int("PARO_EARLY_STAGES", 2);  // under PDL: stages requested before that
   c.a.stagger = env_int("PARO_STAGGER", 1);  // first stage lands before the rest of the ring is requested
-  c.a.skip_math = 0;
   GemvArgs& a = c.a;
   a.n_lin = n_lin;
   a.B = B;

@@ -278,34 +278,29 @@ __device__ __forceinline__ int2 g1_digits_umma(float* sc, int lane, uint8_t* grp
   return make_int2(X, static_cast<int>(static_cast<uint32_t>(113 + E) << 23));  // 2^(E - 14)
 }
 
-// B > 1: one transform task = (linear, group, set of four tokens) -> digits + (sum, scale) in the
-// linear's xq / xqs buffers (the layout the GEMV bulk-copies)
+// B > 1: one transform task = (linear, group, token) -> digits + (sum, scale) in the linear's
+// xq / xqs buffers (the layout the GEMV bulk-copies).  One token per warp: the tasks are
+// independent, so the transform's latency (it sits between two dependent GEMV launches) is that
+// of one token's 8 rotations, not four tokens' in lockstep.  Tokens B .. BT - 1 get x = 0.
 template <int BT, bool UM>
 __device__ __forceinline__ void g1_xform_task(const Gemv1Stage& S, int task, int B, int x_bf16, int rotate, float* scr,
                                               int lane, bool wait_pdl) {
   constexpr int NB = BT / 4, XPC = 4 * 8 * 32, XPG = NB * XPC;  // = 2 BT rows x 128 B (UMMA B tile)
   const int G = S.G;
-  const int li = task / (G * NB), rem = task - li * G * NB, gam = rem / NB, set = rem - gam * NB;
+  const int li = task / (G * BT), rem = task - li * G * BT, gam = rem / BT, b = rem - gam * BT;
   const Gemv1Linear& d = S.lin[li];
   const int L = rotate ? d.L : 0;
   float4 cs[8], sv;
   uint32_t ix[8];
   g1_params(d, gam, L, rotate, lane, cs, ix, sv);
   if (wait_pdl) pdl_wait();  // x may be written by the previous kernel on the stream
-  const int b0 = set * 4;
-  uint2 xv[4];
-#pragma unroll
-  for (int tb = 0; tb < 4; ++tb) xv[tb] = (b0 + tb < B) ? g1_ldx(S.x, S.K, b0 + tb, gam, lane, !wait_pdl) : make_uint2(0u, 0u);
-  g1_scale<4>(scr, xv, x_bf16, sv, lane);
-  g1_rot<4>(scr, cs, ix, L);
+  uint2 xv[1] = {b < B ? g1_ldx(S.x, S.K, b, gam, lane, !wait_pdl) : make_uint2(0u, 0u)};
+  g1_scale<1>(scr, xv, x_bf16, sv, lane);
+  g1_rot<1>(scr, cs, ix, L);
   uint8_t* xq = d.xq + static_cast<size_t>(gam) * XPG;
-#pragma unroll
-  for (int tb = 0; tb < 4; ++tb) {
-    // tcgen05 engine: the group's UMMA B tile; mma.sync engine: the column set's B fragments
-    const int2 r = UM ? g1_digits_umma(scr + tb * 128, lane, xq, b0 + tb)
-                      : g1_digits<8>(scr + tb * 128, lane, xq + set * XPC, tb);
-    if (lane == 0) d.xqs[static_cast<size_t>(gam) * BT + b0 + tb] = r;
-  }
+  // tcgen05 engine: the group's UMMA B tile; mma.sync engine: the column set's B fragments
+  const int2 r = UM ? g1_digits_umma(scr, lane, xq, b) : g1_digits<8>(scr, lane, xq + (b >> 2) * XPC, b & 3);
+  if (lane == 0) d.xqs[static_cast<size_t>(gam) * BT + b] = r;
 }
 
 }  // namespace
@@ -518,8 +513,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
         if (S.xq_in_kernel) {
           // this stage's x is an earlier stage's y: transform tasks over every warp of the grid,
           // then one more grid barrier before the slices are copied
-          float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * (4 * 128);
-          const int n_tasks = S.n_lin * S.G * NB;
+          float* scr = reinterpret_cast<float*>(smem + a.off_scr) + warp * 128;
+          const int n_tasks = S.n_lin * S.G * BT;
 #pragma unroll 1
           for (int task = static_cast<int>(blockIdx.x) * NW + warp; task < n_tasks;
                task += static_cast<int>(gridDim.x) * NW)
@@ -685,7 +680,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
       // B > 1 on the warp-level integer tensor cores: warp w takes a contiguous chunk of the batch's
       // tiles (row block ri, group gi), so that its consecutive tiles mostly share a row block and
       // the row partials (shared-memory atomics) are added once per row block; column sets of four
-      // tokens (hi / lo digits in the MMA's 8 columns)
+      // tokens (hi / lo digits in the MMA's 8 columns).  (Measured: plain per-warp partial slots
+      // summed after each batch instead of the atomics -- no faster; the batch loop is latency-bound.)
       const int gq = lane >> 2, tq = lane & 3;
       int r_lo = 0, off0 = 0;
 #pragma unroll 1
@@ -732,8 +728,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
           const float2 Sb = __half22float2(*reinterpret_cast<const __half2*>(&sp.y));  // rows gq + 16, gq + 24
           const float Sr[4] = {Sa.x, Sa.y, Sb.x, Sb.y};
 #pragma unroll
-          for (int set = 0; set < NB; ++set) {
-            if (set * 4 >= B) break;
+          for (int set = 0; set < NB; ++set) {  // every set (absent tokens: x' = 0): independent MMA chains
             uint4 bA = make_uint4(0u, 0u, 0u, 0u), bB = bA;  // B fragments (columns >= NCOL are zero)
             if (gq < NCOL) {
               const uint8_t* bp = xp + gi * XPG + set * XPC + tq * XTQ + gq * 32;
@@ -751,17 +746,16 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
               mma_u8s8(Dh[hh], r0.z & MH, r1.z & MH, r0.w & MH, r1.w & MH, bB.z, bB.w);
             }
             // lane (gq, tq) holds columns 2 tq (hi) and 2 tq + 1 (lo) = token tq of the set, rows gq + 8 q
+            // (tokens >= B: x' = 0 in every group, their sums never leave the CTA)
             const int b = set * 4 + tq;
-            if (b < B) {
-              const int2 xf = xs[gi * BT + b];
-              const float F = __int_as_float(xf.y);
+            const int2 xf = xs[gi * BT + b];
+            const float F = __int_as_float(xf.y);
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const int hh = q >> 1, e = (q & 1) * 2;
-                const int zq = static_cast<int>((zw >> (4 * q)) & 15u);
-                const int I = Dl[hh][e] * 256 + Dl[hh][e + 1] + ((Dh[hh][e] * 256 + Dh[hh][e + 1]) >> 4) - zq * xf.x;
-                acc[set][q] = fmaf(Sr[q] * F, static_cast<float>(I), acc[set][q]);
-              }
+            for (int q = 0; q < 4; ++q) {
+              const int hh = q >> 1, e = (q & 1) * 2;
+              const int zq = static_cast<int>((zw >> (4 * q)) & 15u);
+              const int I = Dl[hh][e] * 256 + Dl[hh][e + 1] + ((Dh[hh][e] * 256 + Dh[hh][e + 1]) >> 4) - zq * xf.x;
+              acc[set][q] = fmaf(Sr[q] * F, static_cast<float>(I), acc[set][q]);
             }
           }
           if (++gi == gc) {
@@ -933,7 +927,25 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __gr
     named_bar_sync(1, NW * 32);
     if (tid == 0) tl_mark(s, 4);
     if (s == 0 && CL > 1) cluster_wait();  // every CTA of the cluster is running: DSMEM is legal
-    if (g.active) {
+    if (BT > 1 && g.active) {
+      // four tokens per st.async (16 B), owner by owner (no per-element division)
+      constexpr int Q4 = BT / 4;
+#pragma unroll 1
+      for (int c = 0, r0 = 0; c < CL && r0 < g.R; ++c, r0 += g.RR) {
+        const int rows = min(g.RR, g.R - r0);
+#pragma unroll 1
+        for (int idx = tid; idx < rows * Q4; idx += NW * 32) {
+          const int rl = idx / Q4, q = idx & (Q4 - 1);
+          const uint4 v = *reinterpret_cast<const uint4*>(part + (r0 + rl) * BT + 4 * q);
+          float* dst = recv + (crank * S.RRmax + rl) * BT + 4 * q;
+          if (c == crank)
+            *reinterpret_cast<uint4*>(dst) = v;
+          else
+            st_async_v4(mapa(smem_u32(dst), static_cast<uint32_t>(c)), v,
+                        mapa(smem_u32(rbar), static_cast<uint32_t>(c)));
+        }
+      }
+    } else if (g.active) {
       for (int idx = tid; idx < g.R * BT; idx += NW * 32) {
         const int r = idx / BT, b = idx - r * BT;
         float sum;
@@ -1005,12 +1017,11 @@ struct Gemv1XformArgs {
 
 template <int BT, bool UM>
 __global__ void __launch_bounds__(128) paro_gemv1_xform_kernel(const __grid_constant__ Gemv1XformArgs a) {
-  constexpr int NB = BT / 4;
-  __shared__ __align__(16) float scr_all[4][4 * 128];
+  __shared__ __align__(16) float scr_all[4][128];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (a.pdl) pdl_launch_dependents();
   const int task = blockIdx.x * 4 + warp;
-  if (task >= a.st.n_lin * a.st.G * NB) return;
+  if (task >= a.st.n_lin * a.st.G * BT) return;
   g1_xform_task<BT, UM>(a.st, task, a.B, a.x_bf16, a.rotate, scr_all[warp], lane, a.pdl != 0);
 }
 
@@ -1047,7 +1058,7 @@ cudaError_t launch_gemv1_xform(const Gemv1Config& c, cudaStream_t st) {
   x.x_bf16 = c.a.x_bf16;
   x.rotate = c.a.rotate;
   x.pdl = c.a.pdl;
-  const int tasks = x.st.n_lin * x.st.G * (c.BT / 4);
+  const int tasks = x.st.n_lin * x.st.G * c.BT;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((tasks + 3) / 4);
   cfg.blockDim = dim3(128);
@@ -1236,10 +1247,7 @@ bool plan_gemv1_chain(int B, int n_stages, const int* n_lin, const int64_t (*Ns)
   a.off_part = off;
   off += g1_align(static_cast<uint32_t>(part_words) * 4, 128);
   a.off_scr = off;
-  if (BT == 1)
-    off += NW * 512;
-  else if (chain)
-    off += NW * 2048;  // in-kernel transform tasks of later stages (4 tokens x 128 channels)
+  if (BT == 1 || chain) off += NW * 512;  // per-warp 128-channel scratch (B > 1: later stages' transform tasks)
   a.off_recv = off;
   off += g1_align(static_cast<uint32_t>(CL) * rrmax_all * BT * 4, 128);
   a.off_bar = off;

@@ -308,7 +308,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
   // ------------------------------------------------------------ phase 2: tiles (a6)
   {
     const int gq = lane >> 2, tq = lane & 3;
-#pragma unroll 1
     const bool atom = a.atom != 0;
     // stage bookkeeping advanced incrementally (no divisions in the loop): ring slot and phase,
     // first tile u0 = st * TPS = r_lo * gc + off0
@@ -722,7 +721,6 @@ bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, B
   a.TPS = TPS;
   a.pre_stages = std::max(0, b1_env("PARO_G1_PRE", 2));
   a.params_first = b1_env("PARO_G1_PF", 1);
-  a.skip_math = 0;
   a.R_max = rmax;
   a.RRmax = (rmax + CL - 1) / CL;
   const int gcm = (G + CL - 1) / CL;

@@ -343,8 +343,8 @@ static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, 
   const size_t xe = 2, ye = dtype_bytes(y_dtype);
   paro::GemvConfig cfg;
   int planned_b = 0;
-  // token count -> kernel (measured, tools/time_batch.py): the K-split kernel (gemv1.cu) for one
-  // token and for 5..16 tokens per launch; the cluster-shared-transform kernel (gemv.cu) for 2..4
+  // token count -> kernel (measured, tools/time_batch.py): the K-split kernel (gemv1.cu; B = 1:
+  // gemv1_b1.cu) except B = 2 with K <= 3072 (the cluster-shared-transform kernel, gemv.cu)
 #if PARO_DEBUG_KNOBS
   static const int small_b = [] {
     const char* e = getenv("PARO_G1_SMALLB");
@@ -353,11 +353,10 @@ static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, 
 #else
   constexpr int small_b = 0;
 #endif
-  // 2..4 tokens (tools/time_batch.py): the cluster-shared-transform kernel for B = 2 and for wide
-  // launches with K < 8192 (e.g. gate+up), the K-split kernel otherwise
-  int64_t nk = 0;
-  for (int i = 0; i < n; ++i) nk += packed[i].N * K;
-  const bool old_small = B == 2 || (B <= 4 && nk >= (48LL << 20) && K < 8192);
+  // 2..4 tokens (tools/ab_smallb.sh, round 2, one-token transform tasks): the K-split kernel
+  // wins or ties everywhere (N = 28672 x K = 4096 at B = 4: 15.5 vs 25.2 us) except B = 2 with a
+  // short K (9728 x 2560: 8.2 vs 9.3 us), which keeps the cluster-shared-transform kernel
+  const bool old_small = B == 2 && K <= 3072;
   bool k_split = !debug && paro::gemv1_enabled() && (B == 1 || B > 4 || !old_small || small_b || tcgen05);
   if (!k_split && !debug && paro::gemv1_enabled()) {  // the other kernel must be able to plan this shape
     const int bt0 = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8;

@@ -45,7 +45,6 @@ struct GemvArgs {
   int xfirst;       // producer waits until the transform warps have issued their loads
   int early_stages; // under PDL: weight stages requested before that
   int stagger;      // experiment: stages issued (and the first awaited) before the rest of the ring
-  int skip_math;    // debug: stream the weights but skip the phase-2 math (timing only)
   int NW;           // compute warps
   int TPS;          // tiles per ring stage
   int scr_groups;   // transform groups per warp in lockstep (1 or 2)
@@ -157,7 +156,7 @@ struct B1Args {
   int K, G;
   int rotate;
   int pdl;
-  int TPS, S, pre_stages, params_first, atom, skip_math, R_max, RRmax;
+  int TPS, S, pre_stages, params_first, atom, R_max, RRmax;
   uint32_t slot_bytes, sc_off, z_off;
   uint32_t off_xp, off_xs, off_scr, off_part, off_recv, off_bar, off_ring, smem_total;
   // NVLink-native all-gather (paro_linear_allgather_p2p): the epilogue stores every y value into

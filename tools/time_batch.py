@@ -15,7 +15,7 @@ p = synth.make_problem(8, K, 1, seed=1)
 s, th, pr = (torch.from_numpy(p[k]).to(dev) for k in ("s", "theta", "pairs"))
 sets = [paro.paro_pack((torch.randn(N, K, device=dev) * 0.02).half(), s, th, pr) for _ in range(4)]
 st = torch.cuda.Stream()
-for B in (1, 2, 4, 8, 16):
+for B in (int(v) for v in os.environ.get("TB_BATCHES", "1,2,4,8,16").split(",")):
     x = torch.randn(B, K, device=dev).half()
     y = torch.empty(B, N, device=dev).half()
     with torch.cuda.stream(st):

@@ -479,6 +479,12 @@ def measure_transform_vs_fwht(torch, paro, dev, stream, tokens=(1, 2048)):
             uf = graph_time_us(torch, stream, lambda: paro.paro_fwht(x, signs, 1.0 / np.sqrt(n), out=yf, stream=stream),
                                reps)
             row[f"T{T}"] = {"rotation_us": round(ur, 3), "fwht_us": round(uf, 3), "speedup": round(uf / ur, 3)}
+            if T >= 64:  # the same transform as a dense per-group contraction (the prefill path's form)
+                yd = torch.empty((T, n), dtype=torch.float16, device=dev)
+                wsd = torch.empty(paro._lib.paro_transform_dense_workspace(n), dtype=torch.uint8, device=dev)
+                ud = graph_time_us(torch, stream, lambda: paro.paro_transform_activations_dense(
+                    x, packed, out=yd, workspace=wsd, stream=stream), reps)
+                row[f"T{T}"].update({"dense_rotation_us": round(ud, 3), "speedup_dense": round(uf / ud, 3)})
         out[str(n)] = row
     return out
 

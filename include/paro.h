@@ -219,6 +219,20 @@ paro_status paro_linear_chain(int32_t n_stages, const paro_chain_stage* stages, 
 paro_status paro_transform_activations(const void* x, paro_dtype x_dtype, int64_t B, const paro_packed* packed,
                                        void* x_out, void* stream);
 
+/* paro_transform_activations_dense: the same x' as paro_transform_activations,
+ * computed as a dense per-group contraction: per call, M_g = R_L ... R_1 diag(s_g)
+ * (128 x 128, the linear map Eq. 5 defines for one group) is
+ * built by the Givens kernel applied to the 128 unit vectors and rounded to fp16 into
+ * `workspace` (device, >= paro_transform_dense_workspace(K) bytes, 16-byte aligned,
+ * caller-owned scratch), then x'_g = M_g x_g for every token on the tensor cores (fp16
+ * operands, fp32 accumulation, fp16 out).  Results differ from the Givens kernel by
+ * the fp16 rounding of M (relative ~2^-11).  The prefill path uses this form for
+ * B >= 64 tokens.  x, x_out 16-byte aligned; fp16 / bf16 x (bf16 converted to fp16).
+ * Asynchronous. */
+size_t paro_transform_dense_workspace(int64_t K);
+paro_status paro_transform_activations_dense(const void* x, paro_dtype x_dtype, int64_t B, const paro_packed* packed,
+                                             void* x_out, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Test-only: expand the packed weight to logical arrays (device):
  * codes u8 [N, K], scales fp16 [N, K/128], zeros u8 [N, K/128].  Asynchronous. */
 paro_status paro_unpack_logical(const paro_packed* packed, void* codes_u8, void* scales_f16, void* zeros_u8,

@@ -66,6 +66,8 @@ SIGNATURES = {
     "paro_linear_chain": (ctypes.c_int, [_I32, ctypes.POINTER(paro_chain_stage), ctypes.c_int, _I64, ctypes.c_int, _U32,
                                          _P, _SZ, _P]),
     "paro_transform_activations": (ctypes.c_int, [_P, ctypes.c_int, _I64, _PP, _P, _P]),
+    "paro_transform_dense_workspace": (_SZ, [_I64]),
+    "paro_transform_activations_dense": (ctypes.c_int, [_P, ctypes.c_int, _I64, _PP, _P, _P, _SZ, _P]),
     "paro_unpack_logical": (ctypes.c_int, [_PP, _P, _P, _P, _P]),
     "paro_comm_unique_id": (ctypes.c_int, [_P]),
     "paro_comm_init": (ctypes.c_int, [_P, _I32, _I32, ctypes.POINTER(ctypes.c_void_p)]),
@@ -283,6 +285,20 @@ def paro_transform_activations(x, packed: PackedLinear, out=None, stream=None):
     st = packed.struct()
     _check(_lib.paro_transform_activations(_ptr(x), _dt(x), x.shape[0], ctypes.byref(st), _ptr(out),
                                            _stream(stream)))
+    return out
+
+
+def paro_transform_activations_dense(x, packed: PackedLinear, out=None, workspace=None, stream=None):
+    """x' via the dense per-group form (M_g = R_L..R_1 diag(s_g) built per call, fp16 contraction)."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty(x.shape, dtype=torch.float16, device=x.device)
+    need = _lib.paro_transform_dense_workspace(packed.K)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+    st = packed.struct()
+    _check(_lib.paro_transform_activations_dense(_ptr(x), _dt(x), x.shape[0], ctypes.byref(st), _ptr(out),
+                                                 _ptr(workspace), workspace.numel(), _stream(stream)))
     return out
 
 

@@ -23,6 +23,53 @@
 
 namespace paro {
 
+#ifndef PARO_TIMELINE
+#define PARO_TIMELINE 0
+#endif
+#if PARO_TIMELINE
+// per (CTA, launch slot, event) clock64 marks (tools/timeline_b1.py); launch slot = launch
+// sequence number mod 16 (paro_debug_b1_seq_reset restarts it); event 11 = %globaltimer at event 0
+__device__ unsigned long long g_tl_b1[1024 * 16 * 12];
+static int g_b1_seq = 0;
+extern "C" int paro_debug_timeline_b1(unsigned long long* host, int n) {
+  if (n > 1024 * 16 * 12) n = 1024 * 16 * 12;
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_tl_b1, sizeof(unsigned long long) * n));
+}
+extern "C" void paro_debug_b1_seq_reset() { g_b1_seq = 0; }
+// per-stage marks of launch slots 12..15: [slot - 12][CTA][stage][0 producer issued, 1 consumer data-ready, 2 consumer done]
+__device__ unsigned long long g_tl_b1_st[4 * 1024 * 64 * 3];
+extern "C" int paro_debug_timeline_b1_st(unsigned long long* host, int n) {
+  if (n > 4 * 1024 * 64 * 3) n = 4 * 1024 * 64 * 3;
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_tl_b1_st, sizeof(unsigned long long) * n));
+}
+#endif
+__device__ __forceinline__ void b1_mark(int slot, int ev) {
+#if PARO_TIMELINE
+  if (blockIdx.x < 1024) {
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    g_tl_b1[(blockIdx.x * 16 + slot) * 12 + ev] = c;
+    if (ev == 0) g_tl_b1[(blockIdx.x * 16 + slot) * 12 + 11] = globaltimer_ns();
+  }
+#else
+  (void)slot;
+  (void)ev;
+#endif
+}
+__device__ __forceinline__ void b1_mark_st(int slot, int st, int ev) {
+#if PARO_TIMELINE
+  if (slot >= 12 && blockIdx.x < 1024 && st < 64) {
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    g_tl_b1_st[(((slot - 12) * 1024 + blockIdx.x) * 64 + st) * 3 + ev] = c;
+  }
+#else
+  (void)slot;
+  (void)st;
+  (void)ev;
+#endif
+}
+
 namespace {
 constexpr int B1_NW = 16;  // compute warps per CTA (+ 1 producer warp)
 constexpr uint32_t TILE_B = TILE_CODE_BYTES + TILE_SCALE_BYTES + TILE_ZERO_BYTES;
@@ -95,6 +142,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
     fence_mbar_init();
   }
   __syncthreads();
+  if (threadIdx.x == 0) b1_mark(a.tl_slot, 0);
   // BT > 1: the cluster barrier arrive of the compute warps comes after phase 1, because the
   // transform scratch shares its shared memory with recv, which other CTAs write once the
   // barrier completes
@@ -116,6 +164,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
       __syncwarp();
     };
     if (a.params_first) named_bar_sync(3, (NW + 1) * 32);  // the rotation-parameter loads are out
+    if (lane == 0) b1_mark(a.tl_slot, 10);
 #pragma unroll 1
     for (int st = 0; st < n_stages; ++st) {
       const int slot = st % a.S;
@@ -124,6 +173,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
       if (st == pre) {
         if (BT > 1) issue_xq();
         named_bar_sync(2, (NW + 1) * 32);
+        if (lane == 0) b1_mark(a.tl_slot, 9);
       }
       if (st >= a.S) mbar_wait(&empty[slot], ((st / a.S) & 1) ^ 1);
       if (lane == 0) {
@@ -142,9 +192,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
           bulk_g2s(dst + a.z_off + i0 * TILE_ZERO_BYTES, d.zeros + T * TILE_ZERO_BYTES, n * TILE_ZERO_BYTES, &full[slot],
                    pol);
         }
+        b1_mark_st(a.tl_slot, st, 0);
       }
       __syncwarp();
     }
+    if (lane == 0) b1_mark(a.tl_slot, 8);
     if (pre >= n_stages) {
       if (BT > 1) issue_xq();
       named_bar_sync(2, (NW + 1) * 32);
@@ -210,6 +262,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
       if (!waited) {
         if (a.pdl) pdl_wait();  // x may be written by the previous kernel on the stream
         waited = true;
+        if (warp == 0 && lane == 0) b1_mark(a.tl_slot, 1);
       }
 #pragma unroll 1
       for (int b0 = 0; b0 < B; b0 += TB) {  // token chunks, TB tokens in lockstep
@@ -238,6 +291,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
           __syncwarp();
           named_bar_arrive(2, (NW + 1) * 32);  // my x and parameters are in
           arrived = true;
+          if (warp == 0 && lane == 0) b1_mark(a.tl_slot, 2);
         }
         __syncwarp();
         // a5: rotations t = 1..L, each pair from the pre-update values (Eq. 4 / Eq. 5)
@@ -303,6 +357,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
     }
   }
   named_bar_sync(1, NW * 32);  // every x' of the CTA is in shared memory (and BT > 1: part zeroed)
+  if (threadIdx.x == 0) b1_mark(a.tl_slot, 3);
   if (BT > 1 && CL > 1) cluster_arrive();  // my scratch is free: the cluster may now write recv
 
   // ------------------------------------------------------------ phase 2: tiles (a6)
@@ -318,6 +373,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
       const int u0 = st * a.TPS, nt = min(n_tiles, u0 + a.TPS) - u0;
       const int g_lo = ga, pl = gc;
       mbar_wait(&full[slot], phase);
+      if (st == 0 && threadIdx.x == 0) b1_mark(a.tl_slot, 4);
+      if (threadIdx.x == 0) b1_mark_st(a.tl_slot, st, 1);
       const uint8_t* sb = ring + static_cast<size_t>(slot) * a.slot_bytes;
       if constexpr (BT == 1) {
       int ri = 0, gi = off0 + warp;  // tile warp + k NW of the stage
@@ -476,6 +533,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
+      if (threadIdx.x == 0) b1_mark_st(a.tl_slot, st, 2);
       if (++slot == a.S) {
         slot = 0;
         phase ^= 1;
@@ -490,6 +548,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
 
   // ------------------------------------------------------------ reduction + epilogue (a8)
   named_bar_sync(1, NW * 32);
+  if (threadIdx.x == 0) b1_mark(a.tl_slot, 5);
   if (CL > 1) cluster_wait();  // every CTA of the cluster is running: DSMEM is legal
   const int tid = threadIdx.x;
   for (int idx = tid; idx < R * BT; idx += NW * 32) {
@@ -513,6 +572,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
   }
   named_bar_sync(1, NW * 32);  // my own partials are in recv
   if (CL > 1) mbar_wait(rbar, 0);  // and those of the other CTAs of the cluster
+  if (threadIdx.x == 0) b1_mark(a.tl_slot, 6);
   if (a.pdl) pdl_wait();  // y may still be read by the previous kernel
   for (int idx = tid; idx < my_n * BT; idx += NW * 32) {
     const int rl = idx / BT, b = idx - rl * BT;
@@ -544,6 +604,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
       }
     }
   }
+  if (threadIdx.x == 0) b1_mark(a.tl_slot, 7);
   if (a.p2p) {
     // every CTA's peer stores are ordered before its arrival (release at GPU scope); the last CTA to
     // arrive acquires them all and its system-scope release -- cumulative over what it observed --
@@ -798,6 +859,9 @@ static cudaError_t b1_launch(const B1Config& c, cudaLaunchConfig_t* cfg) {
 }
 
 cudaError_t launch_gemv1_b1(const B1Config& c, cudaStream_t st) {
+#if PARO_TIMELINE
+  const_cast<B1Config&>(c).a.tl_slot = g_b1_seq++ & 15;
+#endif
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(c.grid);
   cfg.blockDim = dim3((c.NW + 1) * 32);

@@ -1,5 +1,6 @@
 // misc.cu -- standalone activation transform (prefill pre-stage / microbenchmark),
 // on-the-fly transform preparation, logical unpack (tests), all-gather permute.
+#include <algorithm>
 #include <cstdint>
 #include <map>
 #include <mutex>
@@ -98,7 +99,8 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
                                                         int L, const float* __restrict__ svec,
                                                         const float2* __restrict__ rot_cs,
                                                         const uchar2* __restrict__ rot_idx, int rotate,
-                                                        __half* __restrict__ xo, int pdl, int prefill_order) {
+                                                        __half* __restrict__ xo, int pdl, int prefill_order,
+                                                        int identity) {
   __shared__ float scr_all[8][TOK_LOCK][TGRP];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = static_cast<int>(K / TGRP);
@@ -121,7 +123,9 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
   }
   const float4 sv = rotate ? __ldg(reinterpret_cast<const float4*>(svec + gam * TGRP) + lane)
                            : make_float4(1.f, 1.f, 1.f, 1.f);
-  if (pdl) pdl_wait();
+  // identity mode reads no activations: it runs under the previous kernel and waits for it only
+  // before exiting (so a PDL dependent of this kernel still sees the previous kernel complete)
+  if (pdl && !identity) pdl_wait();
   // output position p of the group: natural (channel p) or prefill order (channel prefill_channel(p))
   int src[4];
 #pragma unroll
@@ -131,10 +135,15 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
 #pragma unroll
     for (int tb = 0; tb < TOK_LOCK; ++tb) {
       const int64_t b = bc + tb;
-      xv[tb] = (b < B && b < b0 + TOK_PER_WARP)
-                   ? __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(x) +
-                                                          (b * K + static_cast<int64_t>(gam) * TGRP + 4 * lane) * 2))
-                   : make_uint2(0u, 0u);
+      if (identity) {  // token b = the unit vector e_b of every group (fp16 1.0 = 0x3C00; x_bf16 is 0)
+        const int64_t o = b - 4 * lane;
+        xv[tb] = make_uint2(o == 0 ? 0x3C00u : o == 1 ? 0x3C000000u : 0u, o == 2 ? 0x3C00u : o == 3 ? 0x3C000000u : 0u);
+      } else {
+        xv[tb] = (b < B && b < b0 + TOK_PER_WARP)
+                     ? __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(x) +
+                                                            (b * K + static_cast<int64_t>(gam) * TGRP + 4 * lane) * 2))
+                     : make_uint2(0u, 0u);
+      }
     }
 #pragma unroll
     for (int tb = 0; tb < TOK_LOCK; ++tb) {
@@ -181,6 +190,7 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
     }
     __syncwarp();
   }
+  if (pdl && identity) pdl_wait();
   if (pdl) pdl_launch_dependents();
 }
 
@@ -202,7 +212,190 @@ cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, in
     cfg.numAttrs = 1;
   }
   return cudaLaunchKernelEx(&cfg, transform_kernel, x, x_bf16, B, K, L, svec, rot_cs, rot_idx, rotate,
-                            static_cast<__half*>(x_out), pdl, prefill_order);
+                            static_cast<__half*>(x_out), pdl, prefill_order, 0);
+}
+
+// ---------------------------------------------------------------- dense form of the transform (many tokens)
+// Per group the transform is one fixed linear map x'_g = M_g x_g with M_g = P R_L ... R_1 diag(s_g)
+// (Eq. 5 with the scale first; P the output channel order), a 128 x 128
+// matrix.  For many tokens (prefill) applying M_g as a dense contraction on the tensor cores moves
+// ~2 KB of shared memory per (token, group) instead of the ~9 KB of eight Givens passes, so the
+// transform becomes HBM-bound.  M_g is built per call by transform_kernel itself (the same
+// cos/sin/pair tables, the same fp32 Givens arithmetic) applied to the 128 unit vectors e_j:
+// mrows[j][g 128 + p] = fp16(M_g[p][j]); the contraction then rounds M to fp16 (2^-11 relative,
+// the precision of the fp16 x' the GEMM consumes anyway) and accumulates in fp32.
+constexpr int DX_ROW = 136;  // padded fp16 row (272 B): conflict-free ldmatrix rows and epilogue writes
+constexpr int DX_SMEM = 3 * 128 * DX_ROW * 2;  // M + two token tiles
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void hmma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                          uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// One CTA = one group x a run of 128-token tiles: the group's M rows are staged once, the token
+// tiles stream through two shared-memory buffers (cp.async of tile i + 1 overlaps the MMAs of
+// tile i).  Warp w: tokens 16 w .. 16 w + 15 of a tile, all 128 outputs (16 m16n8k16 n-tiles x 8
+// k-steps); its result is staged back over its own input rows and stored with 16-byte stores.
+// bf16 x is converted to fp16 in shared memory (exact in fp16's normal range).
+__global__ void __launch_bounds__(256, 2) transform_dense_kernel(const void* __restrict__ x, int x_bf16, int64_t T,
+                                                              int64_t K, const __half* __restrict__ mrows,
+                                                              __half* __restrict__ xo, int tiles_per_cta, int pdl) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  __half* ms = reinterpret_cast<__half*>(dsm);  // [128 inputs j][DX_ROW]: M_g^T, row j = image of e_j
+  __half* const xb0 = ms + 128 * DX_ROW;  // [2][128 tokens][DX_ROW]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.y) * TGRP;
+  const int64_t n_tiles = (T + 127) / 128;
+  const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * tiles_per_cta;
+  const int64_t tile1 = min(n_tiles, tile0 + tiles_per_cta);
+  if (pdl) pdl_wait();  // M (previous kernel) and x (the kernel before it) are complete
+  auto load_x = [&](int64_t tile, __half* dst) {  // 2048 16-byte chunks; rows past T are zero
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int c = it * 256 + tid, r = c >> 4, q = c & 15;
+      const int64_t t = tile * 128 + r;
+      if (t < T)
+        cp_async16(dst + r * DX_ROW + 8 * q, static_cast<const uint8_t*>(x) + (t * K + c0 + 8 * q) * 2);
+      else
+        *reinterpret_cast<uint4*>(dst + r * DX_ROW + 8 * q) = make_uint4(0u, 0u, 0u, 0u);
+    }
+  };
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int c = it * 256 + tid, r = c >> 4, q = c & 15;
+    cp_async16(ms + r * DX_ROW + 8 * q, mrows + static_cast<int64_t>(r) * K + c0 + 8 * q);
+  }
+  if (tile0 < tile1) load_x(tile0, xb0);
+  cp_async_commit();
+  const uint32_t xa_off = ((16 * warp + (lane & 15)) * DX_ROW + ((lane >> 4) << 3)) * 2;
+  const uint32_t mb = smem_u32(ms + ((lane & 7) + (((lane >> 3) & 1) << 3)) * DX_ROW + ((lane >> 4) << 3));
+  const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll 1
+  for (int64_t tile = tile0; tile < tile1; ++tile) {
+    const int b = static_cast<int>(tile - tile0) & 1;
+    __half* xs = xb0 + b * (128 * DX_ROW);
+    if (tile + 1 < tile1) load_x(tile + 1, xb0 + (b ^ 1) * (128 * DX_ROW));  // released by the barrier below
+    cp_async_commit();
+    cp_async_wait<1>();  // this tile (and M) landed
+    if (x_bf16) {  // my own chunks, in place
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int c = it * 256 + tid, r = c >> 4, q = c & 15;
+        uint4* pv = reinterpret_cast<uint4*>(xs + r * DX_ROW + 8 * q);
+        uint4 v = *pv;
+        uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+          const __half2 h = __floats2half2_rn(f.x, f.y);
+          w[e] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        *pv = v;
+      }
+    }
+    __syncthreads();
+    float acc[16][4];
+#pragma unroll
+    for (int n = 0; n < 16; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+    const uint32_t xa = smem_u32(xs) + xa_off;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      uint32_t a0, a1, a2, a3;
+      ldsm_x4(xa + kk * 32, a0, a1, a2, a3);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {  // n-tiles 2 i, 2 i + 1
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(mb + (16 * kk * DX_ROW + 16 * i) * 2, b0, b1, b2, b3);
+        hmma16816(acc[2 * i], a0, a1, a2, a3, b0, b1);
+        hmma16816(acc[2 * i + 1], a0, a1, a2, a3, b2, b3);
+      }
+    }
+    __syncwarp();  // every lane's ldmatrix of this warp's rows is done: reuse them for the output
+    __half* orow = xs + (16 * warp + gq) * DX_ROW + 2 * tq;
+#pragma unroll
+    for (int n = 0; n < 16; ++n) {
+      *reinterpret_cast<__half2*>(orow + 8 * n) = __floats2half2_rn(acc[n][0], acc[n][1]);
+      *reinterpret_cast<__half2*>(orow + 8 * DX_ROW + 8 * n) = __floats2half2_rn(acc[n][2], acc[n][3]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int c = it * 32 + lane, r = c >> 4, q = c & 15;
+      const int64_t t = tile * 128 + 16 * warp + r;
+      if (t < T)
+        *reinterpret_cast<uint4*>(xo + t * K + c0 + 8 * q) =
+            *reinterpret_cast<const uint4*>(xs + (16 * warp + r) * DX_ROW + 8 * q);
+    }
+    __syncthreads();  // buffer b is free for the load of tile + 2
+  }
+  cp_async_wait<0>();
+  if (pdl) pdl_launch_dependents();
+}
+
+size_t transform_dense_ws_bytes(int64_t K) { return static_cast<size_t>(128 * K * 2); }
+
+cudaError_t launch_transform_dense(const void* x, int x_bf16, int64_t B, int64_t K, int L, const float* svec,
+                                   const float2* rot_cs, const uchar2* rot_idx, void* x_out, void* mrows_ws, int pdl,
+                                   int prefill_order, cudaStream_t st) {
+  const int64_t G = K / TGRP;
+  // 1) M rows: transform_kernel on the 128 unit vectors (its PDL wait keeps the dependency on the
+  //    kernel before it transitive for the contraction below)
+  {
+    const int64_t items = (128 / TOK_PER_WARP) * G;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>((items + 7) / 8));
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    if (pdl) {
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+    }
+    cudaError_t e = cudaLaunchKernelEx(&cfg, transform_kernel, static_cast<const void*>(nullptr), 0,
+                                       static_cast<int64_t>(128), K, L, svec, rot_cs, rot_idx, 1,
+                                       static_cast<__half*>(mrows_ws), pdl, prefill_order, 1);
+    if (e != cudaSuccess) return e;
+  }
+  // 2) the contraction
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(transform_dense_kernel), DX_SMEM);
+  if (e != cudaSuccess) return e;
+  // token tiles per CTA: about two CTAs per SM (two fit: 104 KB of shared memory each), at least one
+  const int64_t n_tiles = (B + 127) / 128;
+  const int64_t want = std::max<int64_t>(1, 2 * device_sm_count() / std::max<int64_t>(1, G));
+  const int tpc = static_cast<int>((n_tiles + want - 1) / want);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>((n_tiles + tpc - 1) / tpc), static_cast<unsigned>(G));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = DX_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;  // always PDL-chained to the M build (its wait is in the kernel)
+  return cudaLaunchKernelEx(&cfg, transform_dense_kernel, x, x_bf16, B, K, static_cast<const __half*>(mrows_ws),
+                            static_cast<__half*>(x_out), tpc, 1);
 }
 
 // On-the-fly preparation of (cos, sin, i, j) from device theta / pairs (no validation of

@@ -310,8 +310,10 @@ size_t paro_linear_workspace(int64_t B, int64_t N, int64_t K, int32_t n_rot, int
     ws += align256(static_cast<size_t>(G * n_rot * PARO_SLOTS * 8));
     ws += align256(static_cast<size_t>(G * n_rot * PARO_SLOTS * 2));
   }
-  if (use_prefill(B, N, K, flags))
+  if (use_prefill(B, N, K, flags)) {
     ws += align256(static_cast<size_t>(B * K * 2));
+    if (B >= paro::DENSE_XFORM_MIN_TOKENS) ws += align256(paro::transform_dense_ws_bytes(K));  // M rows
+  }
   else if (B > 1 && paro::gemv1_enabled())  // decode, 2..16 tokens: pre-transformed x' (gemv1.cu)
     ws += paro::gemv1_xq_bytes(static_cast<int>(std::min<int64_t>(B, paro::GEMV1_MAX_B)), K);
   return ws;
@@ -520,7 +522,12 @@ paro_status paro_linear(const void* x, paro_dtype x_dtype, int64_t B, const paro
   }
   if (use_prefill(B, N, K, flags)) {
     void* xq = wsp;
-    cudaError_t e = paro::launch_transform(x, x_dtype == PARO_BF16, B, K, L, svec, rot_cs, rot_idx, rotate, xq, pdl, 1, cs);
+    // many tokens: the transform as a dense per-group contraction (misc.cu), else Givens passes
+    cudaError_t e = (rotate && B >= paro::DENSE_XFORM_MIN_TOKENS)
+                        ? paro::launch_transform_dense(x, x_dtype == PARO_BF16, B, K, L, svec, rot_cs, rot_idx, xq,
+                                                       wsp + align256(static_cast<size_t>(B * K * 2)), pdl, 1, cs)
+                        : paro::launch_transform(x, x_dtype == PARO_BF16, B, K, L, svec, rot_cs, rot_idx, rotate, xq,
+                                                 pdl, 1, cs);
     if (e != cudaSuccess) return cuda_fail(e, "paro_linear: activation transform");
     e = paro::launch_prefill_gemm(xq, B, static_cast<const uint8_t*>(packed->codes),
                                   static_cast<const uint8_t*>(packed->scales), static_cast<const uint8_t*>(packed->zeros),
@@ -693,6 +700,28 @@ paro_status paro_transform_activations(const void* x, paro_dtype x_dtype, int64_
                                          static_cast<const uchar2*>(packed->rot_idx), 1, x_out, 0, 0,
                                          static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "paro_transform_activations");
+  return PARO_OK;
+}
+
+size_t paro_transform_dense_workspace(int64_t K) { return paro::transform_dense_ws_bytes(K); }
+
+paro_status paro_transform_activations_dense(const void* x, paro_dtype x_dtype, int64_t B, const paro_packed* packed,
+                                             void* x_out, void* workspace, size_t workspace_bytes, void* stream) {
+  paro_status st = check_packed(packed);
+  if (st != PARO_OK) return st;
+  if (!x || !x_out || B <= 0) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_transform_activations_dense: bad x/x_out/B");
+  if (x_dtype != PARO_F16 && x_dtype != PARO_BF16) return fail(PARO_ERR_UNSUPPORTED, "x must be fp16 or bf16");
+  if (!aligned16(x) || !aligned16(x_out) || !aligned16(workspace))
+    return fail(PARO_ERR_INVALID_ARGUMENT, "paro_transform_activations_dense: x, x_out, workspace must be 16-byte aligned");
+  if (!workspace || workspace_bytes < paro::transform_dense_ws_bytes(packed->K))
+    return fail(PARO_ERR_INVALID_ARGUMENT, "paro_transform_activations_dense: workspace too small (%zu < %zu)",
+                workspace_bytes, paro::transform_dense_ws_bytes(packed->K));
+  cudaError_t e = paro::launch_transform_dense(x, x_dtype == PARO_BF16, B, packed->K, packed->n_rot,
+                                               static_cast<const float*>(packed->svec),
+                                               static_cast<const float2*>(packed->rot_cs),
+                                               static_cast<const uchar2*>(packed->rot_idx), x_out, workspace, 0, 0,
+                                               static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "paro_transform_activations_dense");
   return PARO_OK;
 }
 

@@ -167,6 +167,7 @@ struct B1Args {
   void* peer_y[PARO_P2P_MAX_WORLD];
   uint32_t* peer_flags[PARO_P2P_MAX_WORLD];
   uint32_t* done_ctr;  // local: CTAs finished (the last one resets it)
+  int tl_slot;         // PARO_TIMELINE builds: launch slot of the per-CTA timeline
   const uint32_t* epoch;  // local: exchanges completed so far (advanced by the wait kernel)
 };
 struct B1Config {
@@ -195,6 +196,14 @@ cudaError_t launch_gemv1(const Gemv1Config& cfg, cudaStream_t st);
 cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, int L, const float* svec,
                              const float2* rot_cs, const uchar2* rot_idx, int rotate, void* x_out, int pdl,
                              int prefill_order, cudaStream_t st);
+
+// dense form for many tokens (prefill): M_g rows built by transform_kernel into mrows_ws
+// (transform_dense_ws_bytes(K)), then x' = M_g x on the tensor cores
+constexpr int64_t DENSE_XFORM_MIN_TOKENS = 64;
+size_t transform_dense_ws_bytes(int64_t K);
+cudaError_t launch_transform_dense(const void* x, int x_bf16, int64_t B, int64_t K, int L, const float* svec,
+                                   const float2* rot_cs, const uchar2* rot_idx, void* x_out, void* mrows_ws, int pdl,
+                                   int prefill_order, cudaStream_t st);
 
 // ---------------------------------------------------------------- on-the-fly transform preparation
 cudaError_t launch_prepare_transform(const float* theta, const int16_t* pairs, int G, int L, int P, float2* rot_cs,

@@ -107,6 +107,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_base_sh;
+  // every CTA of this (one-wave, persistent) grid is resident: the next kernel may launch now.
+  // Dependents wait (griddepcontrol.wait) before reading y; the next linear's transform-matrix
+  // build reads only packed tables, so it runs on the SMs' spare resources under this GEMM.
+  if (a.pdl) pdl_launch_dependents();
   if (a.pdl) pdl_wait();  // x' is written by the pre-stage kernel
 
   if (warp == 0) {
@@ -240,7 +244,6 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (a.pdl) pdl_launch_dependents();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tbase, PF_TMEM_COLS);

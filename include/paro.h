@@ -225,10 +225,10 @@ paro_status paro_transform_activations(const void* x, paro_dtype x_dtype, int64_
  * built by the Givens kernel applied to the 128 unit vectors and rounded to fp16 into
  * `workspace` (device, >= paro_transform_dense_workspace(K) bytes, 16-byte aligned,
  * caller-owned scratch), then x'_g = M_g x_g for every token on the tensor cores (fp16
- * operands, fp32 accumulation, fp16 out).  Results differ from the Givens kernel by
+ * operands, fp32 accumulation in TMEM, fp16 out).  Results differ from the Givens kernel by
  * the fp16 rounding of M (relative ~2^-11).  The prefill path uses this form for
- * B >= 64 tokens.  x, x_out 16-byte aligned; fp16 / bf16 x (bf16 converted to fp16).
- * Asynchronous. */
+ * B >= 64 fp16 tokens (bf16 x takes the Givens kernel).  x, x_out 16-byte aligned;
+ * fp16 x only (PARO_ERR_UNSUPPORTED otherwise).  Asynchronous. */
 size_t paro_transform_dense_workspace(int64_t K);
 paro_status paro_transform_activations_dense(const void* x, paro_dtype x_dtype, int64_t B, const paro_packed* packed,
                                              void* x_out, void* workspace, size_t workspace_bytes, void* stream);

@@ -8,6 +8,7 @@
 
 #include "paro_internal.h"
 #include "ptx.cuh"
+#include "umma.cuh"
 #include "tile_layout.cuh"
 
 namespace paro {
@@ -176,6 +177,23 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
       }
       __syncwarp();
     }
+    if (identity) {
+      // M^T rows for the dense form: mT[gamma 128 + p][j] = fp16(M_gamma[p][j]) (K-major B operand);
+      // the TOK_LOCK = 8 lockstep tokens are the unit vectors e_bc .. e_bc+7: one 16-byte store per p
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        uint32_t w[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const __half2 v = __floats2half2_rn(scr_all[warp][2 * h][src[e]], scr_all[warp][2 * h + 1][src[e]]);
+          w[h] = *reinterpret_cast<const uint32_t*>(&v);
+        }
+        *reinterpret_cast<uint4*>(xo + (static_cast<int64_t>(gam) * TGRP + 4 * lane + e) * TGRP + bc) =
+            make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      __syncwarp();
+      continue;
+    }
 #pragma unroll
     for (int tb = 0; tb < TOK_LOCK; ++tb) {
       const int64_t b = bc + tb;
@@ -218,137 +236,135 @@ cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, in
 // ---------------------------------------------------------------- dense form of the transform (many tokens)
 // Per group the transform is one fixed linear map x'_g = M_g x_g with M_g = P R_L ... R_1 diag(s_g)
 // (Eq. 5 with the scale first; P the output channel order), a 128 x 128
-// matrix.  For many tokens (prefill) applying M_g as a dense contraction on the tensor cores moves
-// ~2 KB of shared memory per (token, group) instead of the ~9 KB of eight Givens passes, so the
-// transform becomes HBM-bound.  M_g is built per call by transform_kernel itself (the same
-// cos/sin/pair tables, the same fp32 Givens arithmetic) applied to the 128 unit vectors e_j:
-// mrows[j][g 128 + p] = fp16(M_g[p][j]); the contraction then rounds M to fp16 (2^-11 relative,
-// the precision of the fp16 x' the GEMM consumes anyway) and accumulates in fp32.
-constexpr int DX_ROW = 136;  // padded fp16 row (272 B): conflict-free ldmatrix rows and epilogue writes
-constexpr int DX_SMEM = 3 * 128 * DX_ROW * 2;  // M + two token tiles
+// matrix.  For many tokens (prefill) applying M_g as a dense contraction on the 5th-generation
+// tensor cores replaces eight shared-memory-bound Givens passes (~9 KB of shared-memory traffic
+// per token and group) by one 128 x 128 x 128 MMA per 128 tokens, and the transform becomes
+// HBM-bound.  M_g is built per call by transform_kernel itself (the same cos/sin/pair tables and
+// fp32 Givens arithmetic) applied to the 128 unit vectors: mT[g 128 + p][j] = fp16(M_g[p][j]); the
+// contraction rounds M to fp16 (2^-11 relative, the precision of the fp16 x' the GEMM consumes
+// anyway) and accumulates in fp32 (TMEM).
+//
+// CTA = one group x a run of 128-token tiles.  warp 0: TMA producer (M^T once, x tiles into two
+// buffers, 128-byte swizzle); warp 1: TMEM allocator + MMA issuer (M = 128 tokens, N = 128
+// outputs, K = 16 x 8) into two TMEM accumulators; warps 2..5: epilogue (tcgen05.ld, fp16,
+// 16-byte stores: thread = token row).
+constexpr int DX_TILE_BYTES = 128 * 128 * 2;             // 32 KB: one operand tile (two 64-wide SW128 boxes)
+constexpr int DX_SMEM = 1024 + 3 * DX_TILE_BYTES + 256;  // M^T + two x tiles + barriers (1024-byte aligned)
 
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-__device__ __forceinline__ void hmma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                          uint32_t b0, uint32_t b1) {
-  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-               : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// One CTA = one group x a run of 128-token tiles: the group's M rows are staged once, the token
-// tiles stream through two shared-memory buffers (cp.async of tile i + 1 overlaps the MMAs of
-// tile i).  Warp w: tokens 16 w .. 16 w + 15 of a tile, all 128 outputs (16 m16n8k16 n-tiles x 8
-// k-steps); its result is staged back over its own input rows and stored with 16-byte stores.
-// bf16 x is converted to fp16 in shared memory (exact in fp16's normal range).
-__global__ void __launch_bounds__(256, 2) transform_dense_kernel(const void* __restrict__ x, int x_bf16, int64_t T,
-                                                              int64_t K, const __half* __restrict__ mrows,
-                                                              __half* __restrict__ xo, int tiles_per_cta, int pdl) {
-  extern __shared__ __align__(16) uint8_t dsm[];
-  __half* ms = reinterpret_cast<__half*>(dsm);  // [128 inputs j][DX_ROW]: M_g^T, row j = image of e_j
-  __half* const xb0 = ms + 128 * DX_ROW;  // [2][128 tokens][DX_ROW]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
-  const int64_t c0 = static_cast<int64_t>(blockIdx.y) * TGRP;
+__global__ void __launch_bounds__(192, 1) transform_dense_kernel(const __grid_constant__ CUtensorMap tmap_x,
+                                                                 const __grid_constant__ CUtensorMap tmap_m, int64_t T,
+                                                                 int64_t K, __half* __restrict__ xo, int tiles_per_cta,
+                                                                 int pdl) {
+  extern __shared__ uint8_t dsm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* m_s = sm;                        // M^T [128 p][128 j]: two [128][64] SW128 boxes
+  uint8_t* x_s = sm + DX_TILE_BYTES;        // [2][128 tokens][128 j]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 3 * DX_TILE_BYTES);
+  uint64_t* m_full = bar;                   // 1
+  uint64_t* x_full = bar + 1;               // 2
+  uint64_t* x_empty = bar + 3;              // 2
+  uint64_t* acc_full = bar + 5;             // 2
+  uint64_t* acc_empty = bar + 7;            // 2
+  uint32_t* tmem_sh = reinterpret_cast<uint32_t*>(bar + 9);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = static_cast<int>(blockIdx.y);
   const int64_t n_tiles = (T + 127) / 128;
   const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * tiles_per_cta;
-  const int64_t tile1 = min(n_tiles, tile0 + tiles_per_cta);
-  if (pdl) pdl_wait();  // M (previous kernel) and x (the kernel before it) are complete
-  auto load_x = [&](int64_t tile, __half* dst) {  // 2048 16-byte chunks; rows past T are zero
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const int c = it * 256 + tid, r = c >> 4, q = c & 15;
-      const int64_t t = tile * 128 + r;
-      if (t < T)
-        cp_async16(dst + r * DX_ROW + 8 * q, static_cast<const uint8_t*>(x) + (t * K + c0 + 8 * q) * 2);
-      else
-        *reinterpret_cast<uint4*>(dst + r * DX_ROW + 8 * q) = make_uint4(0u, 0u, 0u, 0u);
+  const int64_t tile_end = n_tiles < tile0 + tiles_per_cta ? n_tiles : tile0 + tiles_per_cta;
+  const int nt = tile_end > tile0 ? static_cast<int>(tile_end - tile0) : 0;
+  if (threadIdx.x == 0) {
+    mbar_init(m_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&x_full[i], 1);
+      mbar_init(&x_empty[i], 1);
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 128);
     }
-  };
-#pragma unroll
-  for (int it = 0; it < 8; ++it) {
-    const int c = it * 256 + tid, r = c >> 4, q = c & 15;
-    cp_async16(ms + r * DX_ROW + 8 * q, mrows + static_cast<int64_t>(r) * K + c0 + 8 * q);
+    fence_mbar_init();
+    prefetch_tmap(&tmap_x);
+    prefetch_tmap(&tmap_m);
   }
-  if (tile0 < tile1) load_x(tile0, xb0);
-  cp_async_commit();
-  const uint32_t xa_off = ((16 * warp + (lane & 15)) * DX_ROW + ((lane >> 4) << 3)) * 2;
-  const uint32_t mb = smem_u32(ms + ((lane & 7) + (((lane >> 3) & 1) << 3)) * DX_ROW + ((lane >> 4) << 3));
-  const int gq = lane >> 2, tq = lane & 3;
-#pragma unroll 1
-  for (int64_t tile = tile0; tile < tile1; ++tile) {
-    const int b = static_cast<int>(tile - tile0) & 1;
-    __half* xs = xb0 + b * (128 * DX_ROW);
-    if (tile + 1 < tile1) load_x(tile + 1, xb0 + (b ^ 1) * (128 * DX_ROW));  // released by the barrier below
-    cp_async_commit();
-    cp_async_wait<1>();  // this tile (and M) landed
-    if (x_bf16) {  // my own chunks, in place
+  if (warp == 1) tmem_alloc(tmem_sh, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_sh;
+  if (pdl) pdl_wait();  // M^T (previous kernel) and x (the kernel before it) are complete
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(m_full, DX_TILE_BYTES);
+      tma_load_2d(m_s, &tmap_m, 0, g * 128, m_full);
+      tma_load_2d(m_s + DX_TILE_BYTES / 2, &tmap_m, 64, g * 128, m_full);
+      for (int i = 0; i < nt; ++i) {
+        const int b = i & 1;
+        mbar_wait(&x_empty[b], ((i >> 1) & 1) ^ 1);
+        uint8_t* dst = x_s + b * DX_TILE_BYTES;
+        const int row = static_cast<int>((tile0 + i) * 128);
+        mbar_arrive_expect_tx(&x_full[b], DX_TILE_BYTES);
+        tma_load_2d(dst, &tmap_x, g * 128, row, &x_full[b]);
+        tma_load_2d(dst + DX_TILE_BYTES / 2, &tmap_x, g * 128 + 64, row, &x_full[b]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_f16_f32(128, 128);
+      mbar_wait(m_full, 0);
+      const uint64_t mdesc = smem_desc_sw128(m_s);
+      for (int i = 0; i < nt; ++i) {
+        const int b = i & 1;
+        mbar_wait(&acc_empty[b], ((i >> 1) & 1) ^ 1);
+        mbar_wait(&x_full[b], (i >> 1) & 1);
+        tc_fence_after();
+        const uint64_t xdesc = smem_desc_sw128(x_s + b * DX_TILE_BYTES);
 #pragma unroll
-      for (int it = 0; it < 8; ++it) {
-        const int c = it * 256 + tid, r = c >> 4, q = c & 15;
-        uint4* pv = reinterpret_cast<uint4*>(xs + r * DX_ROW + 8 * q);
-        uint4 v = *pv;
-        uint32_t* w = reinterpret_cast<uint32_t*>(&v);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
-          const __half2 h = __floats2half2_rn(f.x, f.y);
-          w[e] = *reinterpret_cast<const uint32_t*>(&h);
+        for (int kk = 0; kk < 8; ++kk) {  // K = 16 per MMA: 32 bytes within a 64-wide box, box 1 for kk >= 4
+          const uint64_t koff = static_cast<uint64_t>((kk >> 2) * (DX_TILE_BYTES / 2 / 16) + (kk & 3) * 2);
+          mma_f16_ss(tbase + b * 128, xdesc + koff, mdesc + koff, idesc, kk > 0 ? 1u : 0u);
         }
-        *pv = v;
+        mma_commit(&x_empty[b]);
+        mma_commit(&acc_full[b]);
       }
     }
-    __syncthreads();
-    float acc[16][4];
+  } else {
+    // epilogue: warp w reads TMEM lanes 32 (w % 4) .. + 31 = token rows of the tile
+    const int q = warp & 3;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    for (int i = 0; i < nt; ++i) {
+      const int b = i & 1;
+      mbar_wait(&acc_full[b], (i >> 1) & 1);
+      tc_fence_after();
+      const int64_t t = (tile0 + i) * 128 + q * 32 + lane;
+      __half* dst = xo + t * K + static_cast<int64_t>(g) * 128;
 #pragma unroll
-    for (int n = 0; n < 16; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
-    const uint32_t xa = smem_u32(xs) + xa_off;
+      for (int cb = 0; cb < 4; ++cb) {
+        uint32_t v[32];
+        tmem_ld32(tbase + b * 128 + cb * 32 + lane_off, v);
+        tmem_ld_wait();
+        if (cb == 3) {
+          tc_fence_before();
+          mbar_arrive(&acc_empty[b]);
+        }
+        if (t < T) {
+          uint32_t h[16];
 #pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      uint32_t a0, a1, a2, a3;
-      ldsm_x4(xa + kk * 32, a0, a1, a2, a3);
+          for (int e = 0; e < 16; ++e) {
+            const __half2 p2 = __floats2half2_rn(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
+            h[e] = *reinterpret_cast<const uint32_t*>(&p2);
+          }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {  // n-tiles 2 i, 2 i + 1
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(mb + (16 * kk * DX_ROW + 16 * i) * 2, b0, b1, b2, b3);
-        hmma16816(acc[2 * i], a0, a1, a2, a3, b0, b1);
-        hmma16816(acc[2 * i + 1], a0, a1, a2, a3, b2, b3);
+          for (int e = 0; e < 4; ++e)
+            *reinterpret_cast<uint4*>(dst + cb * 32 + 8 * e) = make_uint4(h[4 * e], h[4 * e + 1], h[4 * e + 2], h[4 * e + 3]);
+        }
       }
     }
-    __syncwarp();  // every lane's ldmatrix of this warp's rows is done: reuse them for the output
-    __half* orow = xs + (16 * warp + gq) * DX_ROW + 2 * tq;
-#pragma unroll
-    for (int n = 0; n < 16; ++n) {
-      *reinterpret_cast<__half2*>(orow + 8 * n) = __floats2half2_rn(acc[n][0], acc[n][1]);
-      *reinterpret_cast<__half2*>(orow + 8 * DX_ROW + 8 * n) = __floats2half2_rn(acc[n][2], acc[n][3]);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const int c = it * 32 + lane, r = c >> 4, q = c & 15;
-      const int64_t t = tile * 128 + 16 * warp + r;
-      if (t < T)
-        *reinterpret_cast<uint4*>(xo + t * K + c0 + 8 * q) =
-            *reinterpret_cast<const uint4*>(xs + (16 * warp + r) * DX_ROW + 8 * q);
-    }
-    __syncthreads();  // buffer b is free for the load of tile + 2
   }
-  cp_async_wait<0>();
+  tc_fence_before();
+  __syncthreads();
   if (pdl) pdl_launch_dependents();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 256);
+  }
 }
 
 size_t transform_dense_ws_bytes(int64_t K) { return static_cast<size_t>(128 * K * 2); }
@@ -378,15 +394,20 @@ cudaError_t launch_transform_dense(const void* x, int x_bf16, int64_t B, int64_t
     if (e != cudaSuccess) return e;
   }
   // 2) the contraction
+  CUtensorMap tx, tm;
+  if (x_bf16) return cudaErrorInvalidValue;  // the caller converts bf16 x first (x is read by TMA as fp16)
+  if (!make_tmap_2d_f16_sw128(&tx, x, static_cast<uint64_t>(K), static_cast<uint64_t>(B), 64, 128) ||
+      !make_tmap_2d_f16_sw128(&tm, mrows_ws, 128, static_cast<uint64_t>(K), 64, 128))
+    return cudaErrorInvalidValue;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(transform_dense_kernel), DX_SMEM);
   if (e != cudaSuccess) return e;
-  // token tiles per CTA: about two CTAs per SM (two fit: 104 KB of shared memory each), at least one
+  // token tiles per CTA: about two CTAs per SM (96 KB of shared memory and 256 TMEM columns each)
   const int64_t n_tiles = (B + 127) / 128;
   const int64_t want = std::max<int64_t>(1, 2 * device_sm_count() / std::max<int64_t>(1, G));
   const int tpc = static_cast<int>((n_tiles + want - 1) / want);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>((n_tiles + tpc - 1) / tpc), static_cast<unsigned>(G));
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(192);
   cfg.dynamicSmemBytes = DX_SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -394,8 +415,7 @@ cudaError_t launch_transform_dense(const void* x, int x_bf16, int64_t B, int64_t
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;  // always PDL-chained to the M build (its wait is in the kernel)
-  return cudaLaunchKernelEx(&cfg, transform_dense_kernel, x, x_bf16, B, K, static_cast<const __half*>(mrows_ws),
-                            static_cast<__half*>(x_out), tpc, 1);
+  return cudaLaunchKernelEx(&cfg, transform_dense_kernel, tx, tm, B, K, static_cast<__half*>(x_out), tpc, 1);
 }
 
 // On-the-fly preparation of (cos, sin, i, j) from device theta / pairs (no validation of

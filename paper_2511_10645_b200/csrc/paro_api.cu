@@ -523,7 +523,7 @@ paro_status paro_linear(const void* x, paro_dtype x_dtype, int64_t B, const paro
   if (use_prefill(B, N, K, flags)) {
     void* xq = wsp;
     // many tokens: the transform as a dense per-group contraction (misc.cu), else Givens passes
-    cudaError_t e = (rotate && B >= paro::DENSE_XFORM_MIN_TOKENS)
+    cudaError_t e = (rotate && x_dtype == PARO_F16 && B >= paro::DENSE_XFORM_MIN_TOKENS)
                         ? paro::launch_transform_dense(x, x_dtype == PARO_BF16, B, K, L, svec, rot_cs, rot_idx, xq,
                                                        wsp + align256(static_cast<size_t>(B * K * 2)), pdl, 1, cs)
                         : paro::launch_transform(x, x_dtype == PARO_BF16, B, K, L, svec, rot_cs, rot_idx, rotate, xq,
@@ -710,7 +710,7 @@ paro_status paro_transform_activations_dense(const void* x, paro_dtype x_dtype, 
   paro_status st = check_packed(packed);
   if (st != PARO_OK) return st;
   if (!x || !x_out || B <= 0) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_transform_activations_dense: bad x/x_out/B");
-  if (x_dtype != PARO_F16 && x_dtype != PARO_BF16) return fail(PARO_ERR_UNSUPPORTED, "x must be fp16 or bf16");
+  if (x_dtype != PARO_F16) return fail(PARO_ERR_UNSUPPORTED, "paro_transform_activations_dense: x must be fp16");
   if (!aligned16(x) || !aligned16(x_out) || !aligned16(workspace))
     return fail(PARO_ERR_INVALID_ARGUMENT, "paro_transform_activations_dense: x, x_out, workspace must be 16-byte aligned");
   if (!workspace || workspace_bytes < paro::transform_dense_ws_bytes(packed->K))

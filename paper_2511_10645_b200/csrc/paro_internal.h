@@ -1,6 +1,7 @@
 // paro_internal.h -- declarations shared by the host API and the kernels (not installed).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace paro {
@@ -197,6 +198,9 @@ cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, in
                              const float2* rot_cs, const uchar2* rot_idx, int rotate, void* x_out, int pdl,
                              int prefill_order, cudaStream_t st);
 
+// 2-D fp16 tensor map, 128-byte swizzle, box box_inner x box_outer (prefill.cu)
+bool make_tmap_2d_f16_sw128(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                            uint32_t box_outer);
 // dense form for many tokens (prefill): M_g rows built by transform_kernel into mrows_ws
 // (transform_dense_ws_bytes(K)), then x' = M_g x on the tensor cores
 constexpr int64_t DENSE_XFORM_MIN_TOKENS = 64;

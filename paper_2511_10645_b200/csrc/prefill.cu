@@ -37,9 +37,18 @@
 
 namespace paro {
 
+#ifndef PARO_PF_DEEP
+#define PARO_PF_DEEP 1  // dequant loads two iterations ahead (0: one)
+#endif
 constexpr int PF_BM = 128;    // weight rows per tile (MMA M)
 constexpr int PF_BK = 64;     // K per pipeline stage (4 MMAs of K=16)
-constexpr int PF_SX = 4;      // x' shared-memory stages (32 KB each)
+#ifndef PARO_PF_STAGE_EPI
+#define PARO_PF_STAGE_EPI 1  // 16-bit y staged in shared memory (coalesced stores, early TMEM release)
+#endif
+#ifndef PARO_PF_SX
+#define PARO_PF_SX 4
+#endif
+constexpr int PF_SX = PARO_PF_SX;  // x' shared-memory stages (32 KB each at 256 tokens)
 constexpr int PF_SA = 8;      // A (dequantised weight) TMEM stages (32 columns each)
 constexpr int PF_ACC_COL = 0;
 constexpr int PF_A_COL = 256;
@@ -163,30 +172,43 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       const int n = (tile % n_row_tiles) * PF_BM + r;
       const int rt = n % TILE_ROWS;
       const int64_t T0 = static_cast<int64_t>(n / TILE_ROWS) * G;  // first tile of the row block
-      // stage ks = half-row (32 bytes) ks & 1 of tile (row block, ks / 2)
+      // stage ks = half-row (32 bytes) ks & 1 of tile (row block, ks / 2).  The row's code bytes,
+      // scale and zero point of my parity's stages are loaded two iterations (four K-stages) ahead:
+      // the dequant chain must never wait on a load's full latency (long-scoreboard stalls)
       const uint8_t* crow = a.codes + T0 * TILE_CODE_BYTES + rt * 64;
-      uint4 c0 = __ldg(reinterpret_cast<const uint4*>(crow + par * 32));
-      uint4 c1 = __ldg(reinterpret_cast<const uint4*>(crow + par * 32 + 16));
+      struct Pf {
+        uint4 c0, c1;
+        uint32_t sz;  // S bits | z << 16
+      };
+      auto load = [&](int ks) {
+        Pf f;
+        const int64_t T = T0 + (ks >> 1);
+        const uint8_t* cp = crow + static_cast<int64_t>(ks >> 1) * TILE_CODE_BYTES + par * 32;
+        f.c0 = __ldg(reinterpret_cast<const uint4*>(cp));
+        f.c1 = __ldg(reinterpret_cast<const uint4*>(cp + 16));
+        const uint32_t sb = __ldg(reinterpret_cast<const unsigned short*>(a.scales) + T * TILE_ROWS + tile_scale_idx(rt));
+        const uint32_t zb = __ldg(a.zeros + T * TILE_ZERO_BYTES + tile_zero_byte(rt));
+        f.sz = sb | ((tile_zero_hi(rt) ? (zb >> 4) : (zb & 15u)) << 16);
+        return f;
+      };
+      Pf p1 = load(par), p2 = (PARO_PF_DEEP && par + 2 < n_ks) ? load(par + 2) : p1;
       uint32_t ss = 0, zz = 0;
       it += par;
       for (int ks = par; ks < n_ks; ks += 2, it += 2) {
+        const Pf cur = p1;
+        if (PARO_PF_DEEP) {
+          p1 = p2;
+          if (ks + 4 < n_ks) p2 = load(ks + 4);
+        } else if (ks + 2 < n_ks) {
+          p1 = load(ks + 2);
+        }
         {
-          const int64_t T = T0 + (ks >> 1);
-          const __half S = a.scales[T * TILE_ROWS + tile_scale_idx(rt)];
-          const uint8_t zb = a.zeros[T * TILE_ZERO_BYTES + tile_zero_byte(rt)];
-          const int z = tile_zero_hi(rt) ? (zb >> 4) : (zb & 15);
-          const __half2 S2 = __halves2half2(S, S);
-          const __half zh = __ushort_as_half(static_cast<unsigned short>(0x6400 + z));  // 1024 + z
-          const __half2 Z2 = __halves2half2(zh, zh);
-          ss = *reinterpret_cast<const uint32_t*>(&S2);
-          zz = *reinterpret_cast<const uint32_t*>(&Z2);
+          const uint32_t sbits = cur.sz & 0xffffu, z = cur.sz >> 16;
+          ss = sbits | (sbits << 16);
+          const uint32_t zh = 0x6400u + z;  // 1024 + z
+          zz = zh | (zh << 16);
         }
-        const uint4 w0 = c0, w1 = c1;
-        if (ks + 2 < n_ks) {  // prefetch this row's next 32 code bytes of my parity
-          const uint8_t* nx = crow + static_cast<int64_t>((ks + 2) >> 1) * TILE_CODE_BYTES + par * 32;
-          c0 = __ldg(reinterpret_cast<const uint4*>(nx));
-          c1 = __ldg(reinterpret_cast<const uint4*>(nx + 16));
-        }
+        const uint4 w0 = cur.c0, w1 = cur.c1;
         uint32_t v[32];
         const uint32_t wd[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
@@ -218,9 +240,41 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       const float bv = a.bias ? a.bias[n] : 0.f;
       mbar_wait(acc_full, tcount & 1);
       tc_fence_after();
+      if (PARO_PF_STAGE_EPI && a.y_dtype != 2) {
+        // 16-bit outputs: accumulator -> shared-memory staging [token][128 rows] (the MMA may start
+        // the next tile as soon as TMEM is read), then 16-byte coalesced row stores of y
+        uint16_t* stg = reinterpret_cast<uint16_t*>(smem + PF_SX * PF_X_STAGE_BYTES + 1024);
 #pragma unroll 1
-      for (int c = 0; c < PF_BN / 32; ++c) {
-        uint32_t v[32];
+        for (int c = 0; c < PF_BN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tbase + lane_addr + PF_ACC_COL + c * 32, v);
+          tmem_ld_wait();
+          if (c == PF_BN / 32 - 1) {
+            tc_fence_before();
+            mbar_arrive(acc_empty);
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float f = __uint_as_float(v[i]) + bv;
+            stg[(c * 32 + i) * PF_BM + r] = a.y_dtype == 0 ? __half_as_ushort(__float2half_rn(f))
+                                                           : __bfloat16_as_ushort(__float2bfloat16_rn(f));
+          }
+        }
+        named_bar_sync(7, 128);
+        const int n0 = (tile % n_row_tiles) * PF_BM;
+        const int et = (warp - 8) * 32 + lane;
+#pragma unroll 4
+        for (int q = et; q < PF_BN * 16; q += 128) {
+          const int tk = q >> 4, c16 = q & 15;
+          if (tok0 + tk < a.B)
+            *reinterpret_cast<uint4*>(static_cast<uint16_t*>(a.y) + static_cast<int64_t>(tok0 + tk) * a.N + n0 + 8 * c16) =
+                *reinterpret_cast<const uint4*>(stg + tk * PF_BM + 8 * c16);
+        }
+        named_bar_sync(7, 128);  // staging free for the next tile
+        continue;
+      }
+#pragma unroll 1
+      for (int c = 0; c < PF_BN / 32; ++c) {        uint32_t v[32];
         tmem_ld32(tbase + lane_addr + PF_ACC_COL + c * 32, v);
         tmem_ld_wait();
 #pragma unroll
@@ -268,6 +322,19 @@ static EncodeTiledFn get_encode() {
   return fn;
 }
 
+bool make_tmap_2d_f16_sw128(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                            uint32_t box_outer) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t gdim[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  cuuint64_t gstride[1] = {static_cast<cuuint64_t>(inner) * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), gdim, gstride, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool prefill_supported(int64_t B, int64_t N, int64_t K) {
   return B >= 1 && N % PF_BM == 0 && K % PF_BK == 0 && K >= PF_BK && N <= (int64_t(1) << 30) && B < (1 << 30);
 }
@@ -287,7 +354,8 @@ static cudaError_t prefill_launch(const void* xq, int64_t B, const PrefillArgs& 
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  const size_t smem = 1024 + PF_SX * PF_BN * PF_BK * 2 + 256;
+  // x' stages + barriers (1 KB) + the epilogue's y staging (PF_BN x 128 16-bit values)
+  const size_t smem = 1024 + PF_SX * PF_BN * PF_BK * 2 + 1024 + (PARO_PF_STAGE_EPI ? PF_BN * PF_BM * 2 : 0);
   auto kern = prefill_gemm_kernel<PF_BN>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
   if (e != cudaSuccess) return e;

@@ -170,17 +170,19 @@ def test_transform_activations(paro):
     assert np.all(np.abs(xp - ref) <= 2.0 ** -10 * np.abs(ref) + 1e-6 * np.max(np.abs(ref)))
 
 
-@pytest.mark.parametrize("B,K,bf16", [(300, 1024, False), (37, 512, False), (129, 2048, True)])
-def test_transform_activations_dense(paro, B, K, bf16):
+@pytest.mark.parametrize("B,K", [(300, 1024), (37, 512), (129, 2048), (2048, 4096)])
+def test_transform_activations_dense(paro, B, K):
     """Dense per-group form of the transform (M_g = R_L..R_1 diag(s_g) rounded to fp16, fp32
     accumulation): per channel within 2^-10 (|x'| + ||s . x_g||_2) of the oracle -- the fp16
     rounding of M (2^-11 relative per entry; rows of R have unit norm) plus the fp16 output.
-    Ragged token tiles (B not a multiple of 128) and bf16 input converted to fp16."""
+    Ragged token tiles (B not a multiple of 128); bf16 x is refused (the dense form reads fp16)."""
     import torch
     p = synth.make_problem(8, K, B, seed=64 + B)
     t = dev_tensors(p)
     packed, _ = check_pack(paro, p, t)
-    x = t["x"].to(torch.bfloat16) if bf16 else t["x"]
+    x = t["x"]
+    with pytest.raises(paro.ParoError):
+        paro.paro_transform_activations_dense(x.to(torch.bfloat16), packed)
     xin = x.float().cpu().numpy().astype(np.float64)
     xp = paro.paro_transform_activations_dense(x, packed).float().cpu().numpy()
     ref = O.transform_activations(xin, p["s"], p["theta"], p["pairs"])

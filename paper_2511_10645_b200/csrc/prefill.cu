@@ -74,6 +74,20 @@ __device__ __forceinline__ uint32_t hsub_hmul(uint32_t v, uint32_t zz, uint32_t 
   return *reinterpret_cast<uint32_t*>(&r);
 }
 
+#ifndef PARO_PF_MMA_SPIN
+#define PARO_PF_MMA_SPIN 0  // 1: the MMA issuer polls its stage barriers without the suspend hint
+#endif
+#ifndef PARO_PF_PROF
+#define PARO_PF_PROF 0  // 1: the MMA issuer's wait cycles per CTA (acc_empty, A stage, x' stage, total)
+#endif
+#if PARO_PF_PROF
+__device__ unsigned long long g_pf_prof[1024 * 4];
+extern "C" int paro_debug_pf_prof(unsigned long long* host, int n) {
+  if (n > 1024 * 4) n = 1024 * 4;
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_pf_prof, sizeof(unsigned long long) * n));
+}
+#endif
+
 // PF_BN: tokens per tile (MMA N): 256, or 128 when 256-token tiles would leave SMs idle (k / v)
 template <int PF_BN>
 __global__ void __launch_bounds__(PF_THREADS, 1)
@@ -141,13 +155,30 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_f16_f32(PF_BM, PF_BN);
       uint32_t it = 0, tcount = 0;
+#if PARO_PF_PROF
+      unsigned long long w_acc = 0, w_a = 0, w_x = 0, t_beg = clock64();
+#define PF_T0 const unsigned long long _t0 = clock64();
+#define PF_T1(v) v += clock64() - _t0;
+#else
+#define PF_T0
+#define PF_T1(v)
+#endif
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
-        mbar_wait(acc_empty, (tcount & 1) ^ 1);
+        {
+          PF_T0 mbar_wait(acc_empty, (tcount & 1) ^ 1);
+          PF_T1(w_acc)
+        }
         tc_fence_after();
         for (int ks = 0; ks < n_ks; ++ks, ++it) {
           const int sx = it % PF_SX, sa = it % PF_SA;
-          mbar_wait(&a_full[sa], (it / PF_SA) & 1);
-          mbar_wait(&x_full[sx], (it / PF_SX) & 1);
+          {
+            PF_T0 if (PARO_PF_MMA_SPIN) mbar_wait_spin(&a_full[sa], (it / PF_SA) & 1); else mbar_wait(&a_full[sa], (it / PF_SA) & 1);
+            PF_T1(w_a)
+          }
+          {
+            PF_T0 if (PARO_PF_MMA_SPIN) mbar_wait_spin(&x_full[sx], (it / PF_SX) & 1); else mbar_wait(&x_full[sx], (it / PF_SX) & 1);
+            PF_T1(w_x)
+          }
           tc_fence_after();
           const uint64_t bdesc = smem_desc_sw128(xs + sx * PF_X_STAGE_BYTES);
 #pragma unroll
@@ -160,6 +191,14 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         }
         mma_commit(acc_full);
       }
+#if PARO_PF_PROF
+      if (blockIdx.x < 1024) {
+        g_pf_prof[blockIdx.x * 4 + 0] = w_acc;
+        g_pf_prof[blockIdx.x * 4 + 1] = w_a;
+        g_pf_prof[blockIdx.x * 4 + 2] = w_x;
+        g_pf_prof[blockIdx.x * 4 + 3] = clock64() - t_beg;
+      }
+#endif
     }
   } else if ((warp >= 4 && warp < 8) || warp >= 12) {
     // ---------------- dequant producer: weight row r of the tile -> TMEM lane r
@@ -192,11 +231,16 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         return f;
       };
       Pf p1 = load(par), p2 = (PARO_PF_DEEP && par + 2 < n_ks) ? load(par + 2) : p1;
+      Pf p3 = (PARO_PF_DEEP > 1 && par + 4 < n_ks) ? load(par + 4) : p2;
       uint32_t ss = 0, zz = 0;
       it += par;
       for (int ks = par; ks < n_ks; ks += 2, it += 2) {
         const Pf cur = p1;
-        if (PARO_PF_DEEP) {
+        if (PARO_PF_DEEP > 1) {
+          p1 = p2;
+          p2 = p3;
+          if (ks + 6 < n_ks) p3 = load(ks + 6);
+        } else if (PARO_PF_DEEP) {
           p1 = p2;
           if (ks + 4 < n_ks) p2 = load(ks + 4);
         } else if (ks + 2 < n_ks) {

@@ -308,8 +308,20 @@ __device__ __forceinline__ void g1_xform_task(const Gemv1Stage& S, int task, int
 // NW compute warps + 1 producer warp (17 warps: up to 96 registers per thread).
 // BT: token capacity of the instance (1, 4, 8, 16).  MS: stage capacity of the argument block.
 // UM_: B > 1 tiles on the tcgen05 tensor cores (kind::i8, TMEM) instead of warp-level mma.sync.
+// B > 1 single launches leave one paro_gemv1_xform_kernel CTA's registers (128 threads x 64) and
+// shared memory free on every SM (PARO_G1_COXFORM): the NEXT launch's pre-kernel then runs beside
+// this GEMV's CTAs instead of holding the next GEMV's CTAs (and so its weight stream) back.
+#ifndef PARO_G1_COXFORM
+#define PARO_G1_COXFORM 1
+#endif
 template <int NW, int BT, int MS, bool UM_>
-__global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_kernel(const __grid_constant__ Gemv1ArgsT<MS> a) {
+__global__ void __launch_bounds__((NW + 1) * 32, 1)
+    __maxnreg__((PARO_G1_COXFORM && BT == 16 && MS == 1) ? 112 : 128)
+    paro_gemv1_kernel(const __grid_constant__ Gemv1ArgsT<MS> a);
+template <int NW, int BT, int MS, bool UM_>
+__global__ void __launch_bounds__((NW + 1) * 32, 1)
+    __maxnreg__((PARO_G1_COXFORM && BT == 16 && MS == 1) ? 112 : 128)
+    paro_gemv1_kernel(const __grid_constant__ Gemv1ArgsT<MS> a) {
   constexpr bool UM = BT > 1 && UM_;
   constexpr int TB = BT == 1 ? 1 : 4;          // tokens per MMA column set
   constexpr int NB = (BT + 3) / 4;             // column sets
@@ -1175,7 +1187,8 @@ bool plan_gemv1_chain(int B, int n_stages, const int* n_lin, const int64_t (*Ns)
   const int NW = g1_nw(BT, um, chain);
   const int threads = (NW + 1) * 32;
   c.NW = NW;
-  const int budget = device_smem_optin() - 1024;
+  // B > 1 single launches: 3 KB of the SM's shared memory stay free for a co-resident pre-kernel CTA
+  const int budget = device_smem_optin() - 1024 - ((PARO_G1_COXFORM && BT > 1 && !chain) ? 3072 : 0);
   int ncl_max = g1_active_clusters(BT, chain, um, CL, threads, budget);
   ncl_max = std::min(ncl_max, std::max(1, g1_env("PARO_G1_MAXCL", 1 << 20)));
   int grid = 0, rmax_all = 0, rrmax_all = 0, gcm = 0, part_words = 0;

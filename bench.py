@@ -328,10 +328,12 @@ def run_paro(args):
     n_e2e = max(10, min(args.steps, 200))
 
     def e2e_step(li):
+        # x in and y out over PCIe by the library's SM-driven copy (paro_copy), PDL-chained with the
+        # decode launches: no DMA copy node breaks the programmatic-dependent chain
         with torch.cuda.stream(stream):
-            x_all.copy_(hx, non_blocking=True)
+            paro.paro_copy(x_all, hx, flags=paro.PARO_LINEAR_PDL, stream=stream)
             run_step(li, 0, pdl=True)  # its x loads wait (PDL) for the copy before them
-            hy.copy_(y_all, non_blocking=True)
+            paro.paro_copy(hy, y_all, flags=paro.PARO_LINEAR_PDL, stream=stream)
 
     for li in range(3):
         e2e_step(li)
@@ -366,8 +368,9 @@ def run_paro(args):
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
            "api": ("paper_2511_10645_b200.paro_linear_multi (4 decode launches per step)" if world == 1 else
                    "paper_2511_10645_b200.paro_linear_allgather per linear") +
-                  " with the pinned-host x -> device and y -> host copies of every step, each step captured in a "
-                  "CUDA graph and replayed"}
+                  " with the pinned-host x -> device and y -> host copies of every step (paro_copy: SM-driven "
+                  "PCIe copies, PDL-chained with the decode launches), each step captured in a CUDA graph and "
+                  "replayed"}
 
     # prefill (SURVEY.md 8(d) "also prefill TFLOPS"): the same packed linears at 2048 tokens
     # through paro_linear's tcgen05 path (transform pre-stage + GEMM), one CUDA graph per linear

@@ -238,6 +238,16 @@ paro_status paro_transform_activations_dense(const void* x, paro_dtype x_dtype, 
 paro_status paro_unpack_logical(const paro_packed* packed, void* codes_u8, void* scales_f16, void* zeros_u8,
                                 void* stream);
 
+/* paro_copy: dst <- src (bytes, a multiple of 16; both pointers 16-byte aligned), copied by the
+ * SMs (one 16-byte load/store per thread).  Either side may be device memory or pinned host memory
+ * (cudaHostAlloc / torch pin_memory; unified addressing), so a serving loop moves a step's tokens
+ * in and its outputs out through PCIe without a DMA-engine copy node between its kernels.  With
+ * PARO_LINEAR_PDL the copy is a programmatic dependent of the previous kernel on the stream (reads
+ * src after that kernel completed) and lets the next kernel launch early.  Asynchronous; host
+ * memory written by it is complete once the stream work is complete.  Errors:
+ * PARO_ERR_INVALID_ARGUMENT (NULL / misaligned), PARO_ERR_CUDA. */
+paro_status paro_copy(void* dst, const void* src, size_t bytes, uint32_t flags, void* stream);
+
 /* ---- fast Walsh-Hadamard transform (comparison transform) ----
  * The transform the paper's kernel experiment compares against (fig:kernel-speedup,
  * PAPER.md:200-209): per token, y = scale * H_n diag(signs) x with H_n the

@@ -84,6 +84,7 @@ SIGNATURES = {
     "paro_linear_allgather_p2p": (ctypes.c_int, [_P, ctypes.c_int, _I64, _PP, _P, ctypes.c_int, _U32,
                                                  ctypes.POINTER(ctypes.c_void_p), _I32, _I32, _P]),
     "paro_fwht": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _P, ctypes.c_float, _P, _P]),
+    "paro_copy": (ctypes.c_int, [_P, _P, _SZ, _U32, _P]),
     "paro_last_error": (ctypes.c_char_p, []),
     "paro_version": (ctypes.c_char_p, []),
 }
@@ -312,6 +313,15 @@ def paro_unpack_logical(packed: PackedLinear, stream=None):
     st = packed.struct()
     _check(_lib.paro_unpack_logical(ctypes.byref(st), _ptr(codes), _ptr(scales), _ptr(zeros), _stream(stream)))
     return codes, scales, zeros
+
+
+def paro_copy(dst, src, flags: int = 0, stream=None):
+    """dst <- src by the SMs (device or pinned host tensors, same byte size; include/paro.h)."""
+    nbytes = dst.numel() * dst.element_size()
+    if src.numel() * src.element_size() != nbytes:
+        raise ValueError("paro_copy: dst and src differ in size")
+    _check(_lib.paro_copy(_ptr(dst), _ptr(src), nbytes, flags, _stream(stream)))
+    return dst
 
 
 def paro_fwht(x, signs=None, scale: float = 1.0, out=None, stream=None):

@@ -526,3 +526,39 @@ cudaError_t launch_permute_gather(const void* src, void* dst, int world, int64_t
 }
 
 }  // namespace paro
+
+namespace paro {
+// ---------------------------------------------------------------- SM-driven copy (serving loop I/O)
+// dst <- src, 16-byte chunks, grid-stride; either side may be pinned host memory (unified
+// addressing: reads / posted writes over PCIe by the SMs instead of a DMA-engine copy node).  Under
+// PDL the source is read only after the previous kernel completed, and the next kernel may launch
+// (and prefetch) at once.
+__global__ void __launch_bounds__(256) copy16_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n16,
+                                                     int pdl) {
+  if (pdl) {
+    pdl_launch_dependents();
+    pdl_wait();
+  }
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+
+cudaError_t launch_copy16(void* dst, const void* src, size_t bytes, int pdl, cudaStream_t st) {
+  const int64_t n16 = static_cast<int64_t>(bytes / 16);
+  // one 16-byte chunk per thread up to a wave of 148 x 256 threads (PCIe latency-bound: many in flight)
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n16 + 255) / 256, device_sm_count()));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (pdl) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, copy16_kernel, static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16, pdl);
+}
+}  // namespace paro

@@ -725,6 +725,16 @@ paro_status paro_transform_activations_dense(const void* x, paro_dtype x_dtype, 
   return PARO_OK;
 }
 
+paro_status paro_copy(void* dst, const void* src, size_t bytes, uint32_t flags, void* stream) {
+  if (!dst || !src) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_copy: NULL dst/src");
+  if (bytes % 16 || !aligned16(dst) || !aligned16(src))
+    return fail(PARO_ERR_INVALID_ARGUMENT, "paro_copy: bytes and both pointers must be multiples of 16");
+  if (!bytes) return PARO_OK;
+  cudaError_t e = paro::launch_copy16(dst, src, bytes, (flags & PARO_LINEAR_PDL) ? 1 : 0, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "paro_copy");
+  return PARO_OK;
+}
+
 paro_status paro_fwht(const void* x, paro_dtype x_dtype, int64_t T, int64_t n, const float* signs, float scale,
                       void* y, void* stream) {
   if (!x || !y || T <= 0) return fail(PARO_ERR_INVALID_ARGUMENT, "paro_fwht: bad x/y/T");

@@ -209,6 +209,9 @@ cudaError_t launch_transform_dense(const void* x, int x_bf16, int64_t B, int64_t
                                    const float2* rot_cs, const uchar2* rot_idx, void* x_out, void* mrows_ws, int pdl,
                                    int prefill_order, cudaStream_t st);
 
+// SM-driven 16-byte copy (device or pinned host memory on either side), PDL-capable
+cudaError_t launch_copy16(void* dst, const void* src, size_t bytes, int pdl, cudaStream_t st);
+
 // ---------------------------------------------------------------- on-the-fly transform preparation
 cudaError_t launch_prepare_transform(const float* theta, const int16_t* pairs, int G, int L, int P, float2* rot_cs,
                                      uchar2* rot_idx, cudaStream_t st);

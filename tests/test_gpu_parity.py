@@ -295,3 +295,28 @@ def test_linear_multi_shared_x(paro, B):
     for p, ref, y in zip(probs, refs, ys):
         y_ref = O.oracle_linear(x, ref, p["s"], p["theta"], p["pairs"], bias=p["bias"])
         assert O.normwise_error(y.float().cpu().numpy(), y_ref) <= TOL
+
+
+def test_copy_host_device(paro):
+    """paro_copy (SM-driven copy for the serving loop): pinned host -> device -> pinned host and
+    device -> device, byte-exact; PDL-chained with a decode launch in between; size errors."""
+    import torch
+    dev = torch.device("cuda")
+    src = torch.randint(-30000, 30000, (3 * 4096 + 8,), dtype=torch.int16).pin_memory()
+    d = torch.empty(src.shape, dtype=torch.int16, device=dev)
+    d2 = torch.empty_like(d)
+    back = torch.empty(src.shape, dtype=torch.int16).pin_memory()
+    p = synth.make_problem(256, 1024, 1, seed=5)
+    t = dev_tensors(p)
+    packed, _ = check_pack(paro, p, t)
+    paro.paro_copy(d, src, flags=paro.PARO_LINEAR_PDL)
+    y = paro.paro_linear(t["x"], packed, flags=paro.PARO_LINEAR_PDL)
+    paro.paro_copy(d2, d, flags=paro.PARO_LINEAR_PDL)
+    paro.paro_copy(back, d2, flags=paro.PARO_LINEAR_PDL)
+    torch.cuda.synchronize()
+    assert torch.equal(back, src)
+    assert torch.isfinite(y.float()).all()
+    with pytest.raises(ValueError):
+        paro.paro_copy(back[:-8], d2)
+    with pytest.raises(paro.ParoError):
+        paro.paro_copy(back[:-1], d2[:-1])  # 2 * 12295 bytes: not a multiple of 16

@@ -52,6 +52,9 @@
 
 namespace paro {
 
+#ifndef PARO_G1_MERGE_NIB
+#define PARO_G1_MERGE_NIB 1  // B > 1 mma.sync tiles: low and high nibbles into one accumulator
+#endif
 #ifndef PARO_TIMELINE
 #define PARO_TIMELINE 0  // 1: %globaltimer marks per (CTA, stage, event) for tools/timeline_chain.py
 #endif
@@ -748,6 +751,20 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
               bB = *reinterpret_cast<const uint4*>(bp + 16);
             }
             constexpr uint32_t ML = 0x0f0f0f0fu, MH = 0xf0f0f0f0u;
+#if PARO_G1_MERGE_NIB
+            // high nibbles shifted down (q, not 16 q): both halves of the word accumulate into one
+            // integer sum per (row, column) and the epilogue combines two digits, not four sums
+            (void)MH;
+            int D[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {  // rows gq + 16 hh (w[2 hh]) and gq + 16 hh + 8 (w[2 hh + 1])
+              const uint4 r0 = w[2 * hh], r1 = w[2 * hh + 1];
+              mma_u8s8(D[hh], r0.x & ML, r1.x & ML, r0.y & ML, r1.y & ML, bA.x, bA.y);
+              mma_u8s8(D[hh], r0.z & ML, r1.z & ML, r0.w & ML, r1.w & ML, bA.z, bA.w);
+              mma_u8s8(D[hh], (r0.x >> 4) & ML, (r1.x >> 4) & ML, (r0.y >> 4) & ML, (r1.y >> 4) & ML, bB.x, bB.y);
+              mma_u8s8(D[hh], (r0.z >> 4) & ML, (r1.z >> 4) & ML, (r0.w >> 4) & ML, (r1.w >> 4) & ML, bB.z, bB.w);
+            }
+#else
             int Dl[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}}, Dh[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {  // rows gq + 16 hh (w[2 hh]) and gq + 16 hh + 8 (w[2 hh + 1])
@@ -757,6 +774,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
               mma_u8s8(Dh[hh], r0.x & MH, r1.x & MH, r0.y & MH, r1.y & MH, bB.x, bB.y);
               mma_u8s8(Dh[hh], r0.z & MH, r1.z & MH, r0.w & MH, r1.w & MH, bB.z, bB.w);
             }
+#endif
             // lane (gq, tq) holds columns 2 tq (hi) and 2 tq + 1 (lo) = token tq of the set, rows gq + 8 q
             // (tokens >= B: x' = 0 in every group, their sums never leave the CTA)
             const int b = set * 4 + tq;
@@ -766,7 +784,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
             for (int q = 0; q < 4; ++q) {
               const int hh = q >> 1, e = (q & 1) * 2;
               const int zq = static_cast<int>((zw >> (4 * q)) & 15u);
+#if PARO_G1_MERGE_NIB
+              const int I = D[hh][e] * 256 + D[hh][e + 1] - zq * xf.x;
+#else
               const int I = Dl[hh][e] * 256 + Dl[hh][e + 1] + ((Dh[hh][e] * 256 + Dh[hh][e + 1]) >> 4) - zq * xf.x;
+#endif
               acc[set][q] = fmaf(Sr[q] * F, static_cast<float>(I), acc[set][q]);
             }
           }

@@ -736,7 +736,8 @@ bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, B
   else
     CL = wbytes < 20e6 ? 4 : 2;
   CL = b1_env("PARO_G1_CL", CL);
-  if (CL != 1 && CL != 2 && CL != 4 && CL != 8) CL = 2;
+  if (G >= 64) CL = b1_env("PARO_G1_CL_BIGK", CL);
+  if (CL < 1 || CL > 8) CL = 2;
   while (CL > 1 && CL > G) CL /= 2;
   const int NW = B1_NW;
   int TPS = std::max(1, std::min(64, b1_env("PARO_G1_TPS", 2 * NW)));

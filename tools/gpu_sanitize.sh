@@ -4,7 +4,7 @@
 TAG=${1:-san}; shift
 TOOLS=${@:-memcheck racecheck synccheck}
 OUT=gpurun_out/$TAG; mkdir -p $OUT
-CASES="c1 q_b1_pdl q_b3 q_b2 q_b16 otf_b5 otf_b1 prefill_b300 multi chain_b1 chain_b4 q_b8_tcgen05"
+CASES=${CASES:-"c1 q_b1_pdl q_b3 q_b2 q_b16 otf_b5 otf_b1 prefill_b300 dense copy multi chain_b1 chain_b4 q_b8_tcgen05"}
 for tool in $TOOLS; do
   for c in $CASES; do
     echo "=== $tool $c" >> $OUT/sanitize_$tool.log

@@ -17,6 +17,10 @@ for g in "4096,1024,1024 4096 1" "4096 4096 1" "14336,14336 4096 1" "4096 14336 
 done
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:prefill_gemm -s 1 -c 1 -f \
   -o $O/prefill_q python tools/ncu_prefill.py 4096 4096 2048 > $O/ncu_prefill.log 2>&1
-timeout 300 ncu --set full --clock-control none -k regex:transform_kernel -s 1 -c 1 -f \
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:prefill_gemm -s 1 -c 1 -f \
+  -o $O/prefill_gate python tools/ncu_prefill.py 14336 4096 2048 > $O/ncu_prefill_gate.log 2>&1
+timeout 300 ncu --set full --clock-control none -k regex:transform_dense -s 1 -c 1 -f \
   -o $O/prefill_transform python tools/ncu_prefill.py 4096 4096 2048 > $O/ncu_prefill_transform.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/prefill_launches.csv \
+  python tools/ncu_prefill.py 4096 4096 2048 3 > /dev/null 2>&1
 echo done

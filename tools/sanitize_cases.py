@@ -72,7 +72,32 @@ def chain(B):
     print(f"chain B={B} ok", flush=True)
 
 
+def dense(B=130, K=1024):
+    """Prefill-form transform: M rows by the Givens kernel on unit vectors, tcgen05 contraction."""
+    p = synth.make_problem(8, K, B, seed=30)
+    t = dev(p)
+    pk = paro.paro_pack(t["W"], t["s"], t["theta"], t["pairs"])
+    xp = paro.paro_transform_activations_dense(t["x"], pk).float().cpu().numpy()
+    ref = O.transform_activations(p["x"], p["s"], p["theta"], p["pairs"])
+    assert np.max(np.abs(xp - ref)) <= 2e-3 * np.max(np.abs(ref))
+    print("dense ok", flush=True)
+
+
+def copy():
+    """paro_copy: pinned host -> device -> pinned host, PDL-chained."""
+    src = torch.arange(4096 * 3, dtype=torch.int32).pin_memory()
+    d = torch.empty(src.shape, dtype=torch.int32, device="cuda")
+    back = torch.empty_like(src).pin_memory()
+    paro.paro_copy(d, src, flags=paro.PARO_LINEAR_PDL)
+    paro.paro_copy(back, d, flags=paro.PARO_LINEAR_PDL)
+    torch.cuda.synchronize()
+    assert torch.equal(back, src)
+    print("copy ok", flush=True)
+
+
 CASES = {
+    "dense": dense,
+    "copy": copy,
     "c1": lambda: case(256, 256, 1),
     "q_b1_pdl": lambda: case(1024, 4096, 1, paro.PARO_LINEAR_PDL),
     "q_b3": lambda: case(1024, 4096, 3),

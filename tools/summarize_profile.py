@@ -53,13 +53,15 @@ keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__pipe_tmem_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_uma.avg.pct_of_peak_sustained_active",
         "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
 groups = {0: "q_proj+k_proj+v_proj (N=4096,1024,1024, K=4096), B=1", 1: "o_proj (N=4096, K=4096), B=1",
           2: "gate_proj+up_proj (N=14336 x2, K=4096), B=1", 3: "down_proj (N=4096, K=14336), B=1",
           4: "Qwen3-4B q/k/v (N=4096,1024,1024, K=2560), B=16, mma.sync engine",
           5: "Qwen3-4B q/k/v (N=4096,1024,1024, K=2560), B=16, tcgen05 engine",
           "prefill_q": "prefill GEMM q_proj (N=4096, K=4096), 2048 tokens (tcgen05)",
-          "prefill_transform": "prefill activation transform (2048 x 4096)"}
+          "prefill_gate": "prefill GEMM gate_proj (N=14336, K=4096), 2048 tokens (tcgen05)",
+          "prefill_transform": "prefill activation transform, dense tcgen05 form (2048 x 4096)"}
 out = {"note": "ncu --set full --clock-control none, one launch each (tools/prof_multi.py, bs=1, rotation on); "
                "cold caches and ncu's replay: times are not bench values", "groups": {}}
 traffic = 0.0

@@ -252,7 +252,8 @@ constexpr int DX_TILE_BYTES = 128 * 128 * 2;             // 32 KB: one operand t
 constexpr int DX_SMEM = 1024 + 3 * DX_TILE_BYTES + 256;  // M^T + two x tiles + barriers (1024-byte aligned)
 
 __global__ void __launch_bounds__(192, 1) transform_dense_kernel(const __grid_constant__ CUtensorMap tmap_x,
-                                                                 const __grid_constant__ CUtensorMap tmap_m, int64_t T,
+                                                                 const __grid_constant__ CUtensorMap tmap_m,
+                                                                 const __grid_constant__ CUtensorMap tmap_o, int64_t T,
                                                                  int64_t K, __half* __restrict__ xo, int tiles_per_cta,
                                                                  int pdl) {
   extern __shared__ uint8_t dsm_raw[];
@@ -283,6 +284,7 @@ __global__ void __launch_bounds__(192, 1) transform_dense_kernel(const __grid_co
     fence_mbar_init();
     prefetch_tmap(&tmap_x);
     prefetch_tmap(&tmap_m);
+    prefetch_tmap(&tmap_o);
   }
   if (warp == 1) tmem_alloc(tmem_sh, 256);
   tc_fence_before();
@@ -321,20 +323,21 @@ __global__ void __launch_bounds__(192, 1) transform_dense_kernel(const __grid_co
           const uint64_t koff = static_cast<uint64_t>((kk >> 2) * (DX_TILE_BYTES / 2 / 16) + (kk & 3) * 2);
           mma_f16_ss(tbase + b * 128, xdesc + koff, mdesc + koff, idesc, kk > 0 ? 1u : 0u);
         }
-        mma_commit(&x_empty[b]);
-        mma_commit(&acc_full[b]);
+        mma_commit(&acc_full[b]);  // (x_empty: the epilogue, once its store has read the buffer)
       }
     }
   } else {
-    // epilogue: warp w reads TMEM lanes 32 (w % 4) .. + 31 = token rows of the tile
-    const int q = warp & 3;
+    // epilogue: warp w reads TMEM lanes 32 (w % 4) .. + 31 = token rows of the tile, rounds to
+    // fp16 and writes them into the tile's x buffer (the MMA has consumed it) in the same 128-byte
+    // swizzled layout; one thread then stores the tile with TMA (rows past T are clipped) and
+    // releases the buffer to the producer once the store has read it
+    const int q = warp & 3, r = q * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     for (int i = 0; i < nt; ++i) {
       const int b = i & 1;
+      uint8_t* stg = x_s + b * DX_TILE_BYTES;
       mbar_wait(&acc_full[b], (i >> 1) & 1);
       tc_fence_after();
-      const int64_t t = (tile0 + i) * 128 + q * 32 + lane;
-      __half* dst = xo + t * K + static_cast<int64_t>(g) * 128;
 #pragma unroll
       for (int cb = 0; cb < 4; ++cb) {
         uint32_t v[32];
@@ -344,19 +347,31 @@ __global__ void __launch_bounds__(192, 1) transform_dense_kernel(const __grid_co
           tc_fence_before();
           mbar_arrive(&acc_empty[b]);
         }
-        if (t < T) {
-          uint32_t h[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const __half2 p2 = __floats2half2_rn(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
-            h[e] = *reinterpret_cast<const uint32_t*>(&p2);
+        for (int e = 0; e < 4; ++e) {  // 16-byte chunk cc = 4 cb + e of the row: box cc / 8, swizzled
+          uint32_t h[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const __half2 p2 = __floats2half2_rn(__uint_as_float(v[8 * e + 2 * k]), __uint_as_float(v[8 * e + 2 * k + 1]));
+            h[k] = *reinterpret_cast<const uint32_t*>(&p2);
           }
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            *reinterpret_cast<uint4*>(dst + cb * 32 + 8 * e) = make_uint4(h[4 * e], h[4 * e + 1], h[4 * e + 2], h[4 * e + 3]);
+          const int cc = 4 * cb + e;
+          *reinterpret_cast<uint4*>(stg + (cc >> 3) * (DX_TILE_BYTES / 2) + r * 128 + (((cc & 7) ^ (r & 7)) << 4)) =
+              make_uint4(h[0], h[1], h[2], h[3]);
         }
       }
+      fence_async_smem();          // my writes -> the TMA engine
+      named_bar_sync(1, 128);      // every row of the tile is staged
+      if (warp == 2 && lane == 0) {
+        const int row = static_cast<int>((tile0 + i) * 128);
+        tma_store_2d(&tmap_o, stg, g * 128, row);
+        tma_store_2d(&tmap_o, stg + DX_TILE_BYTES / 2, g * 128 + 64, row);
+        bulk_commit();
+        bulk_wait_read0();
+        mbar_arrive(&x_empty[b]);
+      }
     }
+    if (warp == 2 && lane == 0) bulk_wait0();  // the stores are complete before the grid completes
   }
   tc_fence_before();
   __syncthreads();
@@ -394,10 +409,11 @@ cudaError_t launch_transform_dense(const void* x, int x_bf16, int64_t B, int64_t
     if (e != cudaSuccess) return e;
   }
   // 2) the contraction
-  CUtensorMap tx, tm;
+  CUtensorMap tx, tm, to;
   if (x_bf16) return cudaErrorInvalidValue;  // the caller converts bf16 x first (x is read by TMA as fp16)
   if (!make_tmap_2d_f16_sw128(&tx, x, static_cast<uint64_t>(K), static_cast<uint64_t>(B), 64, 128) ||
-      !make_tmap_2d_f16_sw128(&tm, mrows_ws, 128, static_cast<uint64_t>(K), 64, 128))
+      !make_tmap_2d_f16_sw128(&tm, mrows_ws, 128, static_cast<uint64_t>(K), 64, 128) ||
+      !make_tmap_2d_f16_sw128(&to, x_out, static_cast<uint64_t>(K), static_cast<uint64_t>(B), 64, 128))
     return cudaErrorInvalidValue;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(transform_dense_kernel), DX_SMEM);
   if (e != cudaSuccess) return e;
@@ -415,7 +431,7 @@ cudaError_t launch_transform_dense(const void* x, int x_bf16, int64_t B, int64_t
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;  // always PDL-chained to the M build (its wait is in the kernel)
-  return cudaLaunchKernelEx(&cfg, transform_dense_kernel, tx, tm, B, K, static_cast<__half*>(x_out), tpc, 1);
+  return cudaLaunchKernelEx(&cfg, transform_dense_kernel, tx, tm, to, B, K, static_cast<__half*>(x_out), tpc, 1);
 }
 
 // On-the-fly preparation of (cos, sin, i, j) from device theta / pairs (no validation of

@@ -80,34 +80,31 @@ int cached_device_int(const void* fn, int a, int b, int c, int (*compute)(const 
 }
 
 constexpr int TGRP = 128;
-#ifndef PARO_TOK_PER_WARP
-#define PARO_TOK_PER_WARP 8
-#endif
 #ifndef PARO_TOK_LOCK
 #define PARO_TOK_LOCK 8
 #endif
-constexpr int TOK_PER_WARP = PARO_TOK_PER_WARP;
 constexpr int TOK_LOCK = PARO_TOK_LOCK;  // tokens rotated in lockstep (independent shared-memory chains)
 
 // x' = R_L ... R_1 diag(s) x per (token, group); Eq. 5 in column form,
-// the scale first.  One warp = one group x TOK_PER_WARP tokens, TOK_LOCK of
+// the scale first.  One warp = one group x TOK tokens (TOK_LOCK = 8 for activations, 4 for the M build), all
 // them in lockstep; the rotation parameters of the group (L <= 8 rotations x 2 slots per
 // lane) stay in registers ("the rotation parameters ... fit into registers"),
 // the 128 activations of each token of the group in shared memory.  The rotations are
 // shared-memory bound (4 loads + 4 stores per lane per rotation); the lockstep tokens give
 // the pipe independent work instead of one dependent chain.
+template <int TOK>
 __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__ x, int x_bf16, int64_t B, int64_t K,
                                                         int L, const float* __restrict__ svec,
                                                         const float2* __restrict__ rot_cs,
                                                         const uchar2* __restrict__ rot_idx, int rotate,
                                                         __half* __restrict__ xo, int pdl, int prefill_order,
                                                         int identity) {
-  __shared__ float scr_all[8][TOK_LOCK][TGRP];
+  __shared__ float scr_all[8][TOK][TGRP];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = static_cast<int>(K / TGRP);
   const int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + warp;  // (token tile, group)
   const int gam = static_cast<int>(item % G);
-  const int64_t b0 = (item / G) * TOK_PER_WARP;
+  const int64_t b0 = (item / G) * TOK;
   if (b0 >= B) return;
   // records [G][L][32 lanes]: (cos0, sin0, cos1, sin1) / (i0, j0, i1, j1) of slots l and
   // l + 32 of rotation t
@@ -131,23 +128,23 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
   int src[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) src[e] = prefill_order ? prefill_channel(4 * lane + e) : 4 * lane + e;
-  for (int64_t bc = b0; bc < b0 + TOK_PER_WARP && bc < B; bc += TOK_LOCK) {
-    uint2 xv[TOK_LOCK];
+  for (int64_t bc = b0; bc < b0 + TOK && bc < B; bc += TOK) {
+    uint2 xv[TOK];
 #pragma unroll
-    for (int tb = 0; tb < TOK_LOCK; ++tb) {
+    for (int tb = 0; tb < TOK; ++tb) {
       const int64_t b = bc + tb;
       if (identity) {  // token b = the unit vector e_b of every group (fp16 1.0 = 0x3C00; x_bf16 is 0)
         const int64_t o = b - 4 * lane;
         xv[tb] = make_uint2(o == 0 ? 0x3C00u : o == 1 ? 0x3C000000u : 0u, o == 2 ? 0x3C00u : o == 3 ? 0x3C000000u : 0u);
       } else {
-        xv[tb] = (b < B && b < b0 + TOK_PER_WARP)
+        xv[tb] = (b < B && b < b0 + TOK)
                      ? __ldg(reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(x) +
                                                             (b * K + static_cast<int64_t>(gam) * TGRP + 4 * lane) * 2))
                      : make_uint2(0u, 0u);
       }
     }
 #pragma unroll
-    for (int tb = 0; tb < TOK_LOCK; ++tb) {
+    for (int tb = 0; tb < TOK; ++tb) {
       float2 f01, f23;
       if (x_bf16) {
         f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv[tb].x));
@@ -166,7 +163,7 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
       const uint32_t i0 = ixr[t] & 0xff, j0 = (ixr[t] >> 8) & 0xff;
       const uint32_t i1 = (ixr[t] >> 16) & 0xff, j1 = ixr[t] >> 24;
 #pragma unroll
-      for (int tb = 0; tb < TOK_LOCK; ++tb) {
+      for (int tb = 0; tb < TOK; ++tb) {
         float* scr = scr_all[warp][tb];
         const float a0 = scr[i0], c0 = scr[j0];
         const float a1 = scr[i1], c1 = scr[j1];
@@ -179,23 +176,26 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
     }
     if (identity) {
       // M^T rows for the dense form: mT[gamma 128 + p][j] = fp16(M_gamma[p][j]) (K-major B operand);
-      // the TOK_LOCK = 8 lockstep tokens are the unit vectors e_bc .. e_bc+7: one 16-byte store per p
+      // the TOK lockstep tokens are the unit vectors e_bc .. e_bc+TOK-1: one 2 TOK-byte store per p
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        uint32_t w[4];
+        uint32_t w[TOK / 2];
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
+        for (int h = 0; h < TOK / 2; ++h) {
           const __half2 v = __floats2half2_rn(scr_all[warp][2 * h][src[e]], scr_all[warp][2 * h + 1][src[e]]);
           w[h] = *reinterpret_cast<const uint32_t*>(&v);
         }
-        *reinterpret_cast<uint4*>(xo + (static_cast<int64_t>(gam) * TGRP + 4 * lane + e) * TGRP + bc) =
-            make_uint4(w[0], w[1], w[2], w[3]);
+        __half* o = xo + (static_cast<int64_t>(gam) * TGRP + 4 * lane + e) * TGRP + bc;
+        if constexpr (TOK == 8)
+          *reinterpret_cast<uint4*>(o) = make_uint4(w[0], w[1], w[2], w[3]);
+        else
+          *reinterpret_cast<uint2*>(o) = make_uint2(w[0], w[1]);
       }
       __syncwarp();
       continue;
     }
 #pragma unroll
-    for (int tb = 0; tb < TOK_LOCK; ++tb) {
+    for (int tb = 0; tb < TOK; ++tb) {
       const int64_t b = bc + tb;
       const float* scr = scr_all[warp][tb];
       const __half2 h01 = __floats2half2_rn(scr[src[0]], scr[src[1]]);
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
       uint2 pk;
       pk.x = *reinterpret_cast<const uint32_t*>(&h01);
       pk.y = *reinterpret_cast<const uint32_t*>(&h23);
-      if (b < B && b < b0 + TOK_PER_WARP)
+      if (b < B && b < b0 + TOK)
         *reinterpret_cast<uint2*>(xo + b * K + static_cast<int64_t>(gam) * TGRP + 4 * lane) = pk;
     }
     __syncwarp();
@@ -216,7 +216,7 @@ cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, in
                              const float2* rot_cs, const uchar2* rot_idx, int rotate, void* x_out, int pdl,
                              int prefill_order, cudaStream_t st) {
   const int64_t G = K / TGRP;
-  const int64_t items = ((B + TOK_PER_WARP - 1) / TOK_PER_WARP) * G;
+  const int64_t items = ((B + TOK_LOCK - 1) / TOK_LOCK) * G;
   const int64_t blocks = (items + 7) / 8;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(blocks));
@@ -229,7 +229,7 @@ cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, in
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  return cudaLaunchKernelEx(&cfg, transform_kernel, x, x_bf16, B, K, L, svec, rot_cs, rot_idx, rotate,
+  return cudaLaunchKernelEx(&cfg, transform_kernel<TOK_LOCK>, x, x_bf16, B, K, L, svec, rot_cs, rot_idx, rotate,
                             static_cast<__half*>(x_out), pdl, prefill_order, 0);
 }
 
@@ -391,7 +391,10 @@ cudaError_t launch_transform_dense(const void* x, int x_bf16, int64_t B, int64_t
   // 1) M rows: transform_kernel on the 128 unit vectors (its PDL wait keeps the dependency on the
   //    kernel before it transitive for the contraction below)
   {
-    const int64_t items = (128 / TOK_PER_WARP) * G;
+    // four unit vectors per warp up to K = 8192 (32 warps per group spread the build over the SMs;
+    // measured cold: K = 4096 5.8 vs 7.1 us), eight beyond (K = 16384: 10.7 vs 12.8 us)
+    const int tok = G <= 64 ? 4 : 8;
+    const int64_t items = (128 / tok) * G;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>((items + 7) / 8));
     cfg.blockDim = dim3(256);
@@ -403,7 +406,8 @@ cudaError_t launch_transform_dense(const void* x, int x_bf16, int64_t B, int64_t
       cfg.attrs = attr;
       cfg.numAttrs = 1;
     }
-    cudaError_t e = cudaLaunchKernelEx(&cfg, transform_kernel, static_cast<const void*>(nullptr), 0,
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tok == 4 ? transform_kernel<4> : transform_kernel<8>,
+                                       static_cast<const void*>(nullptr), 0,
                                        static_cast<int64_t>(128), K, L, svec, rot_cs, rot_idx, 1,
                                        static_cast<__half*>(mrows_ws), pdl, prefill_order, 1);
     if (e != cudaSuccess) return e;

@@ -522,10 +522,11 @@ paro_status paro_linear(const void* x, paro_dtype x_dtype, int64_t B, const paro
   }
   if (use_prefill(B, N, K, flags)) {
     void* xq = wsp;
+    uint8_t* mws = wsp + align256(static_cast<size_t>(B * K * 2));
     // many tokens: the transform as a dense per-group contraction (misc.cu), else Givens passes
     cudaError_t e = (rotate && x_dtype == PARO_F16 && B >= paro::DENSE_XFORM_MIN_TOKENS)
-                        ? paro::launch_transform_dense(x, x_dtype == PARO_BF16, B, K, L, svec, rot_cs, rot_idx, xq,
-                                                       wsp + align256(static_cast<size_t>(B * K * 2)), pdl, 1, cs)
+                        ? paro::launch_transform_dense(x, x_dtype == PARO_BF16, B, K, L, svec, rot_cs, rot_idx, xq, mws,
+                                                       pdl, 1, cs)
                         : paro::launch_transform(x, x_dtype == PARO_BF16, B, K, L, svec, rot_cs, rot_idx, rotate, xq,
                                                  pdl, 1, cs);
     if (e != cudaSuccess) return cuda_fail(e, "paro_linear: activation transform");

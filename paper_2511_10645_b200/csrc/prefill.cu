@@ -64,7 +64,33 @@ struct PrefillArgs {
   int y_dtype;
   int B, N, K;
   int pdl;
+  // split-K (few tiles, e.g. k / v): item c = (tile c / 2, K half c % 2), one per CTA; the two
+  // halves of a tile are a cluster pair and exchange fp32 partials of each other's tokens in DSMEM
+  int split;
 };
+
+struct PfItem {
+  int tile, kb, ke, half;  // half: K half of a split tile, or -1
+};
+// the i-th work item of this CTA (false past the last)
+__device__ __forceinline__ bool pf_item(const PrefillArgs& a, int n_tiles, int n_ks, int i, PfItem& it) {
+  if (a.split) {
+    const int c = static_cast<int>(blockIdx.x);
+    if (i > 0 || c >= 2 * n_tiles) return false;
+    it.tile = c >> 1;
+    it.half = c & 1;
+    it.kb = it.half * (n_ks / 2);
+    it.ke = it.half ? n_ks : n_ks / 2;
+    return true;
+  }
+  const int tile = static_cast<int>(blockIdx.x) + i * static_cast<int>(gridDim.x);
+  if (tile >= n_tiles) return false;
+  it.tile = tile;
+  it.kb = 0;
+  it.ke = n_ks;
+  it.half = -1;
+  return true;
+}
 
 __device__ __forceinline__ uint32_t hsub_hmul(uint32_t v, uint32_t zz, uint32_t ss) {
   __half2 a = *reinterpret_cast<__half2*>(&v);
@@ -74,6 +100,9 @@ __device__ __forceinline__ uint32_t hsub_hmul(uint32_t v, uint32_t zz, uint32_t 
   return *reinterpret_cast<uint32_t*>(&r);
 }
 
+#ifndef PARO_PF_SPLITK
+#define PARO_PF_SPLITK 1  // few tiles: split-K halves on two SMs (0: 128-token tiles)
+#endif
 #ifndef PARO_PF_MMA_SPIN
 #define PARO_PF_MMA_SPIN 0  // 1: the MMA issuer polls its stage barriers without the suspend hint
 #endif
@@ -103,7 +132,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   uint64_t* a_empty = a_full + PF_SA;
   uint64_t* acc_full = a_empty + PF_SA;
   uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_base_sh = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t* xchg = acc_empty + 1;  // split-K: the partner's partial of my tokens landed (st.async bytes)
+  uint32_t* tmem_base_sh = reinterpret_cast<uint32_t*>(xchg + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_row_tiles = a.N / PF_BM;
@@ -122,6 +152,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     }
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, 128);
+    mbar_init(xchg, 1);
+    // split-K: 128 rows x PF_BN / 2 fp32 of the partner's partial (armed before any byte can land)
+    if (a.split) mbar_arrive_expect_tx(xchg, PF_BM * (PF_BN / 2) * 4);
     fence_mbar_init();
     prefetch_tmap(&tmap_x);
   }
@@ -130,6 +163,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_base_sh;
+  if (a.split) {  // both CTAs of the pair initialised their barriers: DSMEM stores are legal
+    cluster_arrive_relaxed();
+    cluster_wait();
+  }
   // every CTA of this (one-wave, persistent) grid is resident: the next kernel may launch now.
   // Dependents wait (griddepcontrol.wait) before reading y; the next linear's transform-matrix
   // build reads only packed tables, so it runs on the SMs' spare resources under this GEMM.
@@ -140,9 +177,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     // ---------------- TMA producer: x' tiles [256 tokens x 64 K] (SW128)
     if (lane == 0) {
       uint32_t it = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int tok0 = (tile / n_row_tiles) * PF_BN;
-        for (int ks = 0; ks < n_ks; ++ks, ++it) {
+      PfItem w;
+      for (int item = 0; pf_item(a, n_tiles, n_ks, item, w); ++item) {
+        const int tok0 = (w.tile / n_row_tiles) * PF_BN;
+        for (int ks = w.kb; ks < w.ke; ++ks, ++it) {
           const int s = it % PF_SX;
           mbar_wait(&x_empty[s], ((it / PF_SX) & 1) ^ 1);
           mbar_arrive_expect_tx(&x_full[s], PF_X_STAGE_BYTES);
@@ -163,13 +201,14 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
 #define PF_T0
 #define PF_T1(v)
 #endif
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
+      PfItem w;
+      for (int item = 0; pf_item(a, n_tiles, n_ks, item, w); ++item, ++tcount) {
         {
           PF_T0 mbar_wait(acc_empty, (tcount & 1) ^ 1);
           PF_T1(w_acc)
         }
         tc_fence_after();
-        for (int ks = 0; ks < n_ks; ++ks, ++it) {
+        for (int ks = w.kb; ks < w.ke; ++ks, ++it) {
           const int sx = it % PF_SX, sa = it % PF_SA;
           {
             PF_T0 if (PARO_PF_MMA_SPIN) mbar_wait_spin(&a_full[sa], (it / PF_SA) & 1); else mbar_wait(&a_full[sa], (it / PF_SA) & 1);
@@ -184,7 +223,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
 #pragma unroll
           for (int kk = 0; kk < PF_BK / 16; ++kk) {
             mma_f16_ts(tbase + PF_ACC_COL, tbase + PF_A_COL + sa * 32 + kk * 8, bdesc + static_cast<uint64_t>(kk * 2),
-                       idesc, (ks | kk) ? 1u : 0u);
+                       idesc, (ks > w.kb || kk > 0) ? 1u : 0u);
           }
           mma_commit(&x_empty[sx]);
           mma_commit(&a_empty[sa]);
@@ -206,9 +245,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     const int r = (warp & 3) * 32 + lane;
     const uint32_t lane_addr = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const int G = a.K / 128;
-    uint32_t it = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const int n = (tile % n_row_tiles) * PF_BM + r;
+    uint32_t it_base = 0;  // K-stage counter at the item's first stage (both parity sets)
+    PfItem w;
+    for (int item = 0; pf_item(a, n_tiles, n_ks, item, w); ++item) {
+      const int n = (w.tile % n_row_tiles) * PF_BM + r;
       const int rt = n % TILE_ROWS;
       const int64_t T0 = static_cast<int64_t>(n / TILE_ROWS) * G;  // first tile of the row block
       // stage ks = half-row (32 bytes) ks & 1 of tile (row block, ks / 2).  The row's code bytes,
@@ -230,20 +270,28 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         f.sz = sb | ((tile_zero_hi(rt) ? (zb >> 4) : (zb & 15u)) << 16);
         return f;
       };
-      Pf p1 = load(par), p2 = (PARO_PF_DEEP && par + 2 < n_ks) ? load(par + 2) : p1;
-      Pf p3 = (PARO_PF_DEEP > 1 && par + 4 < n_ks) ? load(par + 4) : p2;
+      // my stages of the item: those whose global counter has my parity (n_ks / 2 is even here, so
+      // for the default round-robin items this is ks = par, par + 2, ...)
+      const int ks0 = w.kb + static_cast<int>((static_cast<uint32_t>(par) - it_base) & 1u);
+      const int kend = w.ke;
+      if (ks0 >= kend) {
+        it_base += static_cast<uint32_t>(w.ke - w.kb);
+        continue;
+      }
+      Pf p1 = load(ks0), p2 = (PARO_PF_DEEP && ks0 + 2 < kend) ? load(ks0 + 2) : p1;
+      Pf p3 = (PARO_PF_DEEP > 1 && ks0 + 4 < kend) ? load(ks0 + 4) : p2;
       uint32_t ss = 0, zz = 0;
-      it += par;
-      for (int ks = par; ks < n_ks; ks += 2, it += 2) {
+      uint32_t it = it_base + static_cast<uint32_t>(ks0 - w.kb);
+      for (int ks = ks0; ks < kend; ks += 2, it += 2) {
         const Pf cur = p1;
         if (PARO_PF_DEEP > 1) {
           p1 = p2;
           p2 = p3;
-          if (ks + 6 < n_ks) p3 = load(ks + 6);
+          if (ks + 6 < kend) p3 = load(ks + 6);
         } else if (PARO_PF_DEEP) {
           p1 = p2;
-          if (ks + 4 < n_ks) p2 = load(ks + 4);
-        } else if (ks + 2 < n_ks) {
+          if (ks + 4 < kend) p2 = load(ks + 4);
+        } else if (ks + 2 < kend) {
           p1 = load(ks + 2);
         }
         {
@@ -271,19 +319,87 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         tc_fence_before();
         mbar_arrive(&a_full[sa]);
       }
-      it -= par;  // it == (tiles so far) * n_ks for both sets (n_ks is even)
+      it_base += static_cast<uint32_t>(w.ke - w.kb);
     }
   } else if (warp >= 8) {
     // ---------------- epilogue: accumulator lane r = weight row, column = token
     const int r = (warp - 8) * 32 + lane;
     const uint32_t lane_addr = static_cast<uint32_t>((warp - 8) * 32) << 16;
     uint32_t tcount = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tcount) {
+    PfItem w;
+    for (int item = 0; pf_item(a, n_tiles, n_ks, item, w); ++item, ++tcount) {
+      const int tile = w.tile;
       const int n = (tile % n_row_tiles) * PF_BM + r;
       const int tok0 = (tile / n_row_tiles) * PF_BN;
       const float bv = a.bias ? a.bias[n] : 0.f;
       mbar_wait(acc_full, tcount & 1);
       tc_fence_after();
+      if (w.half >= 0) {
+        // split-K, the two halves of a tile (a cluster pair) finish it together: half h owns the
+        // tokens [128 h, 128 h + 128) of the tile.  Each half sends its partial of the OTHER half's
+        // tokens straight into the partner's shared memory (st.async, fp32 [row][128 tokens], 16-byte
+        // chunks XOR-swizzled by row), waits for the partner's partial of its own tokens, adds it to
+        // its accumulator in a fixed order (half 0's partial + half 1's) and stores y for them.
+        constexpr int HT = PF_BN / 2;
+        const int h = w.half, mine = h * HT, theirs = (1 - h) * HT;
+        uint8_t* rx = smem + PF_SX * PF_X_STAGE_BYTES + 1024;  // [128 rows][HT] fp32 = 64 KB
+        const uint32_t partner = cluster_ctarank() ^ 1u;
+        const uint32_t rx_remote = mapa(smem_u32(rx), partner), bar_remote = mapa(smem_u32(xchg), partner);
+#pragma unroll 1
+        for (int c = 0; c < HT / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tbase + lane_addr + PF_ACC_COL + theirs + c * 32, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int ch = c * 8 + e;  // 16-byte chunk of the row
+            st_async_v4(rx_remote + static_cast<uint32_t>(r * HT * 4 + ((ch ^ (r & 7)) << 4)),
+                        make_uint4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]), bar_remote);
+          }
+        }
+        mbar_wait(xchg, 0);  // the partner's partial of my tokens is in rx
+        const int n0 = (tile % n_row_tiles) * PF_BM;
+        uint16_t* stg = reinterpret_cast<uint16_t*>(smem);  // my x' stages are free: y staging [HT][128]
+#pragma unroll 1
+        for (int c = 0; c < HT / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tbase + lane_addr + PF_ACC_COL + mine + c * 32, v);
+          tmem_ld_wait();
+          if (c == HT / 32 - 1) {
+            tc_fence_before();
+            mbar_arrive(acc_empty);
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int ch = c * 8 + e;
+            const float4 q = *reinterpret_cast<const float4*>(rx + r * HT * 4 + ((ch ^ (r & 7)) << 4));
+            const float p4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float mv = __uint_as_float(v[4 * e + k]);
+              const float o = (h == 0 ? mv + p4[k] : p4[k] + mv) + bv;  // half 0's partial first
+              const int t = c * 32 + 4 * e + k;
+              if (a.y_dtype == 2) {
+                if (tok0 + mine + t < a.B) static_cast<float*>(a.y)[static_cast<int64_t>(tok0 + mine + t) * a.N + n] = o;
+              } else {
+                stg[t * PF_BM + r] = a.y_dtype == 0 ? __half_as_ushort(__float2half_rn(o))
+                                                    : __bfloat16_as_ushort(__float2bfloat16_rn(o));
+              }
+            }
+          }
+        }
+        if (a.y_dtype != 2) {
+          named_bar_sync(7, 128);
+#pragma unroll 4
+          for (int q = r; q < HT * 16; q += 128) {
+            const int tk = q >> 4, c16 = q & 15;
+            if (tok0 + mine + tk < a.B)
+              *reinterpret_cast<uint4*>(static_cast<uint16_t*>(a.y) + static_cast<int64_t>(tok0 + mine + tk) * a.N +
+                                        n0 + 8 * c16) = *reinterpret_cast<const uint4*>(stg + tk * PF_BM + 8 * c16);
+          }
+        }
+        continue;
+      }
       if (PARO_PF_STAGE_EPI && a.y_dtype != 2) {
         // 16-bit outputs: accumulator -> shared-memory staging [token][128 rows] (the MMA may start
         // the next tile as soon as TMEM is read), then 16-byte coalesced row stores of y
@@ -404,19 +520,29 @@ static cudaError_t prefill_launch(const void* xq, int64_t B, const PrefillArgs& 
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int64_t tiles = (N / PF_BM) * ((B + PF_BN - 1) / PF_BN);
-  const int grid = static_cast<int>(tiles < device_sm_count() ? tiles : device_sm_count());
+  const int grid = a.split ? static_cast<int>(2 * tiles)
+                           : static_cast<int>(tiles < device_sm_count() ? tiles : device_sm_count());
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(PF_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
+  int na = 0;
   if (pdl) {
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
   }
+  if (a.split) {  // the two K halves of a tile form a cluster (they exchange partials through DSMEM)
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = 2;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, kern, tmap, a);
 }
 
@@ -424,10 +550,15 @@ cudaError_t launch_prefill_gemm(const void* xq, int64_t B, const uint8_t* codes,
                                 const uint8_t* zeros, const float* bias, void* y, int y_dtype, int64_t N, int64_t K,
                                 int pdl, cudaStream_t st) {
   PrefillArgs a{codes, reinterpret_cast<const __half*>(scales), zeros, bias, y, y_dtype, static_cast<int>(B),
-                static_cast<int>(N), static_cast<int>(K), pdl};
-  // 256-token tiles unless they would fill fewer than 3/4 of the SMs (e.g. 1024 x 4096 at 2048
-  // tokens: 64 tiles): then 128-token tiles
+                static_cast<int>(N), static_cast<int>(K), pdl, 0};
   const int64_t tiles256 = (N / PF_BM) * ((B + 255) / 256);
+  // few 256-token tiles (e.g. k / v: 1024 x 4096 at 2048 tokens = 64 tiles): each tile as two K
+  // halves on a cluster pair of SMs (every SM busy, each half at N = 256; same-box k_proj 41.8 -> 34.7 us)
+  if (PARO_PF_SPLITK && 2 * tiles256 <= device_sm_count() && K / PF_BK >= 8) {
+    a.split = 1;
+    return prefill_launch<256>(xq, B, a, N, pdl, st);
+  }
+  // otherwise 256-token tiles unless they would fill fewer than 3/4 of the SMs: then 128-token tiles
   if (tiles256 * 4 < static_cast<int64_t>(device_sm_count()) * 3) return prefill_launch<128>(xq, B, a, N, pdl, st);
   return prefill_launch<256>(xq, B, a, N, pdl, st);
 }

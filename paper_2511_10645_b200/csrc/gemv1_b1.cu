@@ -26,6 +26,9 @@ namespace paro {
 #ifndef PARO_TIMELINE
 #define PARO_TIMELINE 0
 #endif
+#ifndef PARO_B1_SHORT_MULTI_CAP
+#define PARO_B1_SHORT_MULTI_CAP 1
+#endif
 #if PARO_TIMELINE
 // per (CTA, launch slot, event) clock64 marks (tools/timeline_b1.py); launch slot = launch
 // sequence number mod 16 (paro_debug_b1_seq_reset restarts it); event 11 = %globaltimer at event 0
@@ -747,6 +750,13 @@ bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, B
   // clusters that fit in one wave (occupancy API, cached per cluster size)
   int ncl_max = b1_active_clusters(BT, CL, threads, budget);
   ncl_max = std::min(ncl_max, std::max(1, b1_env("PARO_G1_MAXCL", 1 << 20)));
+  // short multi-linear launches (q/k/v: < 20 MB over several linears): three quarters of the
+  // clusters -- each CTA streams a longer run of tiles, and the SMs left free take the NEXT launch's
+  // CTAs early (PDL: they fill their rings while this launch finishes).  Measured on the LLaMA-3-8B
+  // step (same box, tools/ab_knobs.sh): q/k/v 6.77 -> 6.42 us, step 34.64 -> 34.15 us; 20 / 16 / 12 /
+  // 8 clusters and single-linear launches (o_proj) measured slower.
+  if (PARO_B1_SHORT_MULTI_CAP && n_lin > 1 && wbytes < 20e6) ncl_max = std::max(n_lin, ncl_max * 3 / 4);
+  if (wbytes < 20e6) ncl_max = std::min(ncl_max, std::max(1, b1_env("PARO_G1_SMALL_MAXCL", 1 << 20)));
   // clusters over linears in proportion to their row blocks (>= 1 each, <= row blocks)
   int64_t NB[GEMV_MAX_LIN], NBsum = 0;
   for (int i = 0; i < n_lin; ++i) {

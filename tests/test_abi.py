@@ -30,6 +30,7 @@ def test_header_declares_the_boundary():
               "paro_transform_activations",
               "paro_unpack_logical", "paro_comm_unique_id", "paro_comm_init", "paro_comm_destroy",
               "paro_linear_allgather", "paro_linear_allgather_workspace", "paro_select_pairs", "paro_fwht", "paro_linear_chain", "paro_linear_allgather_p2p", "paro_ipc_get_handle", "paro_linear_chain_workspace", "paro_last_error",
+              "paro_transform_activations_dense", "paro_transform_dense_workspace", "paro_copy",
               "paro_version"]:
         assert f in fns
 
@@ -117,3 +118,16 @@ def test_chain_workspace_and_argument_errors(paro):
     assert paro._lib.paro_linear_chain(2, st, 0, 17, 0, 0, 16, ws1, None) == paro.PARO_ERR_UNSUPPORTED
     assert paro._lib.paro_linear_chain(2, st, 0, 1, 0, 0, 16, 64, None) == paro.PARO_ERR_INVALID_ARGUMENT
     assert "workspace" in paro.last_error()
+
+
+def test_copy_and_dense_transform_argument_errors(paro):
+    """paro_copy and paro_transform_activations_dense reject bad arguments before any CUDA call."""
+    lib = paro._lib
+    INV = 1  # PARO_ERR_INVALID_ARGUMENT
+    assert lib.paro_copy(None, ctypes.c_void_p(16), 16, 0, None) == INV          # NULL dst
+    assert lib.paro_copy(ctypes.c_void_p(16), ctypes.c_void_p(16), 24, 0, None) == INV  # not a multiple of 16
+    assert lib.paro_copy(ctypes.c_void_p(8), ctypes.c_void_p(16), 16, 0, None) == INV   # misaligned
+    assert lib.paro_copy(ctypes.c_void_p(16), ctypes.c_void_p(32), 0, 0, None) == 0     # nothing to copy
+    assert lib.paro_transform_dense_workspace(4096) == 128 * 4096 * 2
+    assert lib.paro_transform_activations_dense(None, 0, 1, None, None, None, 0, None) != 0  # NULL packed
+    assert paro.last_error()  # a message for the failed call

@@ -53,7 +53,11 @@ constexpr int PF_SA = 8;      // A (dequantised weight) TMEM stages (32 columns 
 constexpr int PF_ACC_COL = 0;
 constexpr int PF_A_COL = 256;
 constexpr int PF_TMEM_COLS = 512;
-constexpr int PF_THREADS = 512;
+#ifndef PARO_PF_NSETS
+#define PARO_PF_NSETS 2  // dequant warp sets (4 warps each) taking K-stages round robin
+#endif
+constexpr int PF_NSETS = PARO_PF_NSETS;
+constexpr int PF_THREADS = 512 + 128 * (PF_NSETS - 2);
 
 struct PrefillArgs {
   const uint8_t* codes;
@@ -241,7 +245,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     }
   } else if ((warp >= 4 && warp < 8) || warp >= 12) {
     // ---------------- dequant producer: weight row r of the tile -> TMEM lane r
-    const int par = warp >= 12 ? 1 : 0;  // K-stage parity of this dequant warp set
+    const int par = warp < 8 ? 0 : (warp < 16 ? 1 : 2);  // this dequant warp set (K-stages round robin)
     const int r = (warp & 3) * 32 + lane;
     const uint32_t lane_addr = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const int G = a.K / 128;
@@ -262,7 +266,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       auto load = [&](int ks) {
         Pf f;
         const int64_t T = T0 + (ks >> 1);
-        const uint8_t* cp = crow + static_cast<int64_t>(ks >> 1) * TILE_CODE_BYTES + par * 32;
+        const uint8_t* cp = crow + static_cast<int64_t>(ks >> 1) * TILE_CODE_BYTES + (ks & 1) * 32;
         f.c0 = __ldg(reinterpret_cast<const uint4*>(cp));
         f.c1 = __ldg(reinterpret_cast<const uint4*>(cp + 16));
         const uint32_t sb = __ldg(reinterpret_cast<const unsigned short*>(a.scales) + T * TILE_ROWS + tile_scale_idx(rt));
@@ -272,27 +276,27 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       };
       // my stages of the item: those whose global counter has my parity (n_ks / 2 is even here, so
       // for the default round-robin items this is ks = par, par + 2, ...)
-      const int ks0 = w.kb + static_cast<int>((static_cast<uint32_t>(par) - it_base) & 1u);
+      const int ks0 = w.kb + static_cast<int>((static_cast<uint32_t>(par) + PF_NSETS * 4u - it_base % PF_NSETS) % PF_NSETS);
       const int kend = w.ke;
       if (ks0 >= kend) {
         it_base += static_cast<uint32_t>(w.ke - w.kb);
         continue;
       }
-      Pf p1 = load(ks0), p2 = (PARO_PF_DEEP && ks0 + 2 < kend) ? load(ks0 + 2) : p1;
-      Pf p3 = (PARO_PF_DEEP > 1 && ks0 + 4 < kend) ? load(ks0 + 4) : p2;
+      Pf p1 = load(ks0), p2 = (PARO_PF_DEEP && ks0 + PF_NSETS < kend) ? load(ks0 + PF_NSETS) : p1;
+      Pf p3 = (PARO_PF_DEEP > 1 && ks0 + 2 * PF_NSETS < kend) ? load(ks0 + 2 * PF_NSETS) : p2;
       uint32_t ss = 0, zz = 0;
       uint32_t it = it_base + static_cast<uint32_t>(ks0 - w.kb);
-      for (int ks = ks0; ks < kend; ks += 2, it += 2) {
+      for (int ks = ks0; ks < kend; ks += PF_NSETS, it += PF_NSETS) {
         const Pf cur = p1;
         if (PARO_PF_DEEP > 1) {
           p1 = p2;
           p2 = p3;
-          if (ks + 6 < kend) p3 = load(ks + 6);
+          if (ks + 3 * PF_NSETS < kend) p3 = load(ks + 3 * PF_NSETS);
         } else if (PARO_PF_DEEP) {
           p1 = p2;
-          if (ks + 4 < kend) p2 = load(ks + 4);
-        } else if (ks + 2 < kend) {
-          p1 = load(ks + 2);
+          if (ks + 2 * PF_NSETS < kend) p2 = load(ks + 2 * PF_NSETS);
+        } else if (ks + PF_NSETS < kend) {
+          p1 = load(ks + PF_NSETS);
         }
         {
           const uint32_t sbits = cur.sz & 0xffffu, z = cur.sz >> 16;

@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
 #pragma unroll
     for (int tb = 0; tb < TOK; ++tb) {
       const int64_t b = bc + tb;
-      if (identity) {  // token b = the unit vector e_b of every group (fp16 1.0 = 0x3C00; x_bf16 is 0)
+      if (TOK >= 4 && identity) {  // (the identity build always runs with 4 or 8 tokens per warp)  // token b = the unit vector e_b of every group (fp16 1.0 = 0x3C00; x_bf16 is 0)
         const int64_t o = b - 4 * lane;
         xv[tb] = make_uint2(o == 0 ? 0x3C00u : o == 1 ? 0x3C000000u : 0u, o == 2 ? 0x3C00u : o == 3 ? 0x3C000000u : 0u);
       } else {
@@ -174,14 +174,14 @@ __global__ void __launch_bounds__(256) transform_kernel(const void* __restrict__
       }
       __syncwarp();
     }
-    if (identity) {
+    if (TOK >= 4 && identity) {  // (the identity build always runs with 4 or 8 tokens per warp)
       // M^T rows for the dense form: mT[gamma 128 + p][j] = fp16(M_gamma[p][j]) (K-major B operand);
       // the TOK lockstep tokens are the unit vectors e_bc .. e_bc+TOK-1: one 2 TOK-byte store per p
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        uint32_t w[TOK / 2];
+        uint32_t w[TOK >= 4 ? TOK / 2 : 2];
 #pragma unroll
-        for (int h = 0; h < TOK / 2; ++h) {
+        for (int h = 0; h < (TOK >= 4 ? TOK / 2 : 0); ++h) {
           const __half2 v = __floats2half2_rn(scr_all[warp][2 * h][src[e]], scr_all[warp][2 * h + 1][src[e]]);
           w[h] = *reinterpret_cast<const uint32_t*>(&v);
         }
@@ -216,7 +216,10 @@ cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, in
                              const float2* rot_cs, const uchar2* rot_idx, int rotate, void* x_out, int pdl,
                              int prefill_order, cudaStream_t st) {
   const int64_t G = K / TGRP;
-  const int64_t items = ((B + TOK_LOCK - 1) / TOK_LOCK) * G;
+  // tokens per warp: eight in lockstep for many tokens; fewer tokens (decode-sized calls) take one
+  // per warp -- the lockstep slots past B would rotate zeros through shared memory for nothing
+  const int tok = B >= TOK_LOCK ? TOK_LOCK : 1;
+  const int64_t items = ((B + tok - 1) / tok) * G;
   const int64_t blocks = (items + 7) / 8;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(blocks));
@@ -229,8 +232,8 @@ cudaError_t launch_transform(const void* x, int x_bf16, int64_t B, int64_t K, in
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  return cudaLaunchKernelEx(&cfg, transform_kernel<TOK_LOCK>, x, x_bf16, B, K, L, svec, rot_cs, rot_idx, rotate,
-                            static_cast<__half*>(x_out), pdl, prefill_order, 0);
+  return cudaLaunchKernelEx(&cfg, tok == 1 ? transform_kernel<1> : transform_kernel<TOK_LOCK>, x, x_bf16, B, K, L, svec,
+                            rot_cs, rot_idx, rotate, static_cast<__half*>(x_out), pdl, prefill_order, 0);
 }
 
 // ---------------------------------------------------------------- dense form of the transform (many tokens)

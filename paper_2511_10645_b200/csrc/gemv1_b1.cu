@@ -59,6 +59,27 @@ __device__ __forceinline__ void b1_mark(int slot, int ev) {
   (void)ev;
 #endif
 }
+#if PARO_TIMELINE
+// per-tile marks of launch slot 13 (the step's o_proj): [CTA][warp][k-th tile of the warp]
+__device__ unsigned long long g_tl_b1_tile[1024 * 16 * 4];
+extern "C" int paro_debug_timeline_b1_tile(unsigned long long* host, int n) {
+  if (n > 1024 * 16 * 4) n = 1024 * 16 * 4;
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_tl_b1_tile, sizeof(unsigned long long) * n));
+}
+#endif
+__device__ __forceinline__ void b1_mark_tile(int slot, int warp, int k) {
+#if PARO_TIMELINE
+  if (slot == 13 && blockIdx.x < 1024 && k < 4) {
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    g_tl_b1_tile[(blockIdx.x * 16 + warp) * 4 + k] = c;
+  }
+#else
+  (void)slot;
+  (void)warp;
+  (void)k;
+#endif
+}
 __device__ __forceinline__ void b1_mark_st(int slot, int st, int ev) {
 #if PARO_TIMELINE
   if (slot >= 12 && blockIdx.x < 1024 && st < 64) {
@@ -438,6 +459,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
             }
           }
         }
+        if (lane == 0 && st == 0) b1_mark_tile(a.tl_slot, warp, (i - warp) / NW);
         gi += NW;
         while (gi >= pl) {
           gi -= pl;

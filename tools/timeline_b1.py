@@ -104,3 +104,18 @@ for li, s in ((0, 12), (1, 13), (2, 14), (3, 15)):
             ok = v > 0
             return int(np.median(v[ok] - c0[ok, 0])) if ok.any() else -1
         print(f"  stage {k}: {med(iss)} / {med(rdy)} / {med(don)}", flush=True)
+tt = np.zeros(1024 * 16 * 4, dtype=np.uint64)
+if hasattr(lib, "paro_debug_timeline_b1_tile"):
+    lib.paro_debug_timeline_b1_tile(tt.ctypes.data_as(ctypes.c_void_p), tt.size)
+    tt = tt.reshape(1024, 16, 4).astype(np.int64)
+    s = 13
+    n = int((raw[:, s, 0] > 0).sum())
+    st0 = st[1, :n, 0, 1]  # stage 0 data-ready (thread 0) of launch slot 13
+    print("o_proj per-warp tile completion (median cycles after stage-0 data-ready, over CTAs):", flush=True)
+    for w in (0, 4, 8, 15):
+        row = []
+        for k in range(2):
+            v = tt[:n, w, k]
+            ok = (v > 0) & (st0 > 0)
+            row.append(int(np.median(v[ok] - st0[ok])) if ok.any() else -1)
+        print(f"  warp {w}: tile 0 done +{row[0]}, tile 1 done +{row[1]}", flush=True)

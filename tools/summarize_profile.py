@@ -45,7 +45,9 @@ with open(os.path.join(dst, "bench_launches_summary.csv"), "w") as f:
 
 # 3. ncu --set full of each decode group
 keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "launch__grid_size", "launch__block_size",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "dram__bytes_read.sum.per_second", "dram__cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "launch__grid_size", "launch__block_size",
         "launch__cluster_dim_x", "launch__registers_per_thread", "sm__cycles_active.avg", "sm__cycles_elapsed.avg",
         "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",

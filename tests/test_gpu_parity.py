@@ -241,9 +241,12 @@ def test_prefill_gemm(paro, B, N, K):
     assert bool((ys[0] == ys[1]).all()), "split-K reduction is not deterministic"
 
 
-def test_prefill_full_size_sampled(paro):
-    """configs[3]: LLaMA-3-8B prefill 2048 tokens, q_proj, sampled tokens and rows."""
-    N, K, B = 4096, 4096, 2048
+@pytest.mark.parametrize("N,K", [(4096, 4096), (1024, 4096), (14336, 4096), (4096, 14336)])
+def test_prefill_full_size_sampled(paro, N, K):
+    """configs[3]: LLaMA-3-8B prefill 2048 tokens at the bench's shapes -- q/o (256 tiles), k/v
+    (split-K cluster pairs), gate/up (896 tiles), down (dense transform over 112 groups) -- sampled
+    tokens and rows against the oracle."""
+    B = 2048
     p = synth.make_problem(N, K, B, seed=90)
     t = dev_tensors(p)
     rows = np.sort(np.random.default_rng(1).choice(N, size=32, replace=False))

@@ -241,6 +241,40 @@ def test_prefill_gemm(paro, B, N, K):
     assert bool((ys[0] == ys[1]).all()), "split-K reduction is not deterministic"
 
 
+@pytest.mark.parametrize("n_rot", [0, 2, 4])
+def test_prefill_fewer_rotations(paro, n_rot):
+    """Table 6 #IR in {0, 2, 4} on the prefill path: the dense transform's
+    per-group matrix M_g = P R_L..R_1 diag(s_g) is built with L < 8 layers (L = 0: M_g = diag(s_g))."""
+    B, N, K = 192, 512, 1024
+    p = synth.make_problem(N, K, B, seed=130 + n_rot, n_rot=max(n_rot, 1))
+    p["theta"] = p["theta"][:, :n_rot].copy()
+    p["pairs"] = p["pairs"][:, :n_rot].copy()
+    t = dev_tensors(p)
+    packed, ref = check_pack(paro, p, t)
+    y = paro.paro_linear(t["x"], packed, flags=paro.PARO_LINEAR_FORCE_GEMM)
+    y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"])
+    assert O.normwise_error(y.float().cpu().numpy(), y_ref) <= TOL
+
+
+@pytest.mark.parametrize("out_dtype", ["bf16", "f32"])
+def test_prefill_bf16_activations(paro, out_dtype):
+    """bf16 x on the prefill path (the Givens transform pre-stage, not the fp16-only dense form),
+    with bf16 / fp32 output; tolerance as test_dtypes."""
+    p = synth.make_problem(768, 2048, 160, seed=140, x_dtype="bf16", with_bias=True)
+    t = dev_tensors(p)
+    packed, ref = check_pack(paro, p, t)
+    odt = {"bf16": torch.bfloat16, "f32": torch.float32}[out_dtype]
+    y = paro.paro_linear(t["x"], packed, bias=t["bias"], out_dtype=odt,
+                         flags=paro.PARO_LINEAR_FORCE_GEMM).float().cpu().numpy()
+    y_ref = O.oracle_linear(x_as_used(t), ref, p["s"], p["theta"], p["pairs"], bias=p["bias"])
+    if out_dtype == "bf16":
+        yr = torch.from_numpy(y_ref).to(torch.bfloat16).float().numpy()
+        ulp = np.abs(yr) * 2.0 ** -8
+        assert np.all(np.abs(y - yr) <= TOL * np.max(np.abs(y_ref)) + ulp)
+    else:
+        assert O.normwise_error(y, y_ref) <= TOL
+
+
 @pytest.mark.parametrize("N,K", [(4096, 4096), (1024, 4096), (14336, 4096), (4096, 14336)])
 def test_prefill_full_size_sampled(paro, N, K):
     """configs[3]: LLaMA-3-8B prefill 2048 tokens at the bench's shapes -- q/o (256 tiles), k/v

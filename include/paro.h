@@ -126,10 +126,14 @@ paro_status paro_pack_sizes(int64_t N, int64_t K, int32_t group, int32_t n_rot, 
 paro_status paro_pack(const void* W, const float* s, const float* theta, const int16_t* pairs, int64_t N,
                       int64_t K, int32_t group, int32_t n_rot, int32_t n_pairs, paro_packed* out, void* stream);
 
-/* Workspace bytes paro_linear needs for this call shape (0 for B = 1 with the packed
- * transform).  `on_the_fly` != 0 when paro_linear will be given s/theta/pairs pointers.
- * Decode with 2..16 tokens needs (G (B'/4) 1024 + G B' 8) bytes (G = K/128, B' = B
- * rounded up to 4, 8 or 16) for the pre-transformed activations. */
+/* Workspace bytes paro_linear needs for this call shape.  `on_the_fly` != 0 when paro_linear
+ * will be given s/theta/pairs pointers.  Decode with 2..16 tokens needs (G (B'/4) 1024 +
+ * G B' 8) bytes (G = K/128, B' = B rounded up to 4, 8 or 16) for the pre-transformed
+ * activations.  B = 1 with the packed transform needs 0 bytes, except for a long-K linear with a
+ * long weight stream (>= 64 MB, e.g. LLaMA-3-70B down_proj), whose K range is split over
+ * several thread-block clusters: 4096 bytes of arrival counters + KS x N fp32 row sums.  Those
+ * counters must be ZERO before the workspace is first used (e.g. one cudaMemsetAsync at
+ * allocation); every call leaves them zero.  A workspace serves one stream at a time. */
 size_t paro_linear_workspace(int64_t B, int64_t N, int64_t K, int32_t n_rot, int32_t n_pairs, int32_t on_the_fly,
                              uint32_t flags);
 

@@ -26,6 +26,9 @@ namespace paro {
 #ifndef PARO_TIMELINE
 #define PARO_TIMELINE 0
 #endif
+#ifndef PARO_B1_KS_MIN_BYTES
+#define PARO_B1_KS_MIN_BYTES 64e6  // weight stream from which a single long-K launch splits K over clusters
+#endif
 #ifndef PARO_B1_SHORT_MULTI_CAP
 #define PARO_B1_SHORT_MULTI_CAP 1
 #endif
@@ -131,11 +134,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
   const int CL = static_cast<int>(cluster_nctarank());
   const int crank = static_cast<int>(cluster_ctarank());
   const int G = a.G, B = a.B;
-  const int cl = (static_cast<int>(blockIdx.x) - d.cta_begin) / CL;
+  const int KS = a.KS > 1 ? a.KS : 1;
+  const int cl_all = (static_cast<int>(blockIdx.x) - d.cta_begin) / CL;
+  const int kq = cl_all % KS, cl = cl_all / KS;  // K slice, row range
   const int nrb = d.rb_base + (cl < d.rb_extra ? 1 : 0);
   const int rb0 = cl * d.rb_base + min(cl, d.rb_extra);
   const int R = nrb * TILE_ROWS;
-  const int ga = crank * G / CL, gb = (crank + 1) * G / CL, gc = gb - ga;
+  const int gs0 = kq * G / KS, Gs = (kq + 1) * G / KS - gs0;
+  const int ga = gs0 + crank * Gs / CL, gb = gs0 + (crank + 1) * Gs / CL, gc = gb - ga;
   // stages: TPS consecutive tiles of the CTA's tile sequence u = rb * gc + (gamma - ga)
   // (row block by row block, my groups within each; a stage may start or end inside a row block)
   const int n_tiles = nrb * gc;
@@ -605,6 +611,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
     float v = 0.f;
     for (int c = 0; c < CL; ++c) v += recv[(c * a.RRmax + rl) * BT + b];  // fixed order
     const int64_t n = static_cast<int64_t>(rb0) * TILE_ROWS + my_lo + rl;
+    if (KS > 1) {  // my K slice's row sums: the last cluster of the row range adds them below
+      if (n < d.N) __stcg(a.ks_part + static_cast<int64_t>(kq) * d.N + n, v);
+      continue;
+    }
     if (n < d.N) {
       if (d.bias) v += __ldg(d.bias + n);
       if (!a.p2p) {
@@ -626,6 +636,39 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
           else
             static_cast<float*>(a.peer_y[p])[o] = v;
         }
+      }
+    }
+  }
+  if (KS > 1) {
+    // last-arriver reduction over the KS clusters of this row range (no waiting: the CTA that
+    // completes the count adds the slices in the fixed order 0..KS-1 and stores y)
+    volatile int& s_last = *reinterpret_cast<int*>(smem + a.off_xs);  // x' sums are no longer read
+    __threadfence();  // my row sums are visible at GPU scope before the count below
+    named_bar_sync(1, NW * 32);
+    if (tid == 0) {
+      uint32_t* ctr = a.ks_ctr + (d.cta_begin / (CL * KS) + cl) * CL + crank;
+      const uint32_t old = atomicAdd(ctr, 1u);
+      const int last = old == static_cast<uint32_t>(KS - 1);
+      if (last) {
+        *ctr = 0u;  // every CTA of this row range has counted: ready for the next call
+        __threadfence();
+      }
+      s_last = last;
+    }
+    named_bar_sync(1, NW * 32);
+    if (s_last) {
+      for (int rl = tid; rl < my_n; rl += NW * 32) {
+        const int64_t n = static_cast<int64_t>(rb0) * TILE_ROWS + my_lo + rl;
+        if (n >= d.N) continue;
+        float v = 0.f;
+        for (int q = 0; q < KS; ++q) v += __ldcg(a.ks_part + static_cast<int64_t>(q) * d.N + n);  // fixed order
+        if (d.bias) v += __ldg(d.bias + n);
+        if (a.y_dtype == 0)
+          static_cast<__half*>(d.y)[n] = __float2half_rn(v);
+        else if (a.y_dtype == 1)
+          static_cast<__nv_bfloat16*>(d.y)[n] = __float2bfloat16_rn(v);
+        else
+          static_cast<float*>(d.y)[n] = v;
       }
     }
   }
@@ -729,7 +772,49 @@ static int b1_active_clusters(int BT, int CL, int threads, int budget) {
                            b1_active_clusters_compute);
 }
 
-bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, B1Config* cfg, const char** why) {
+// Cluster size = how many ways a row block's groups are split (G / CL groups transformed per CTA).
+// The rotations are shared-memory bound (8 accesses per pair-update, all warps at once), so fewer
+// groups per CTA shorten the transform; but clusters of 2 / 4 / 8 fill only 148 / 132 / 120 SMs
+// (occupancy API), which slows the weight stream.  Measured (tools/time_groups.py,
+// tools/time_70b.py): short streams (< 20 MB) at K = 4096 prefer 4, long ones 2; K >= 8192 prefers 8
+// (one transform round) unless the stream is very long and G small (70B gate+up: 2).
+static int b1_cluster_size(int n_lin, const int64_t* Ns, int64_t K, double* wbytes_out) {
+  const int G = static_cast<int>(K / 128);
+  double wbytes = 0;
+  for (int i = 0; i < n_lin; ++i) wbytes += static_cast<double>(Ns[i]) * K * 0.52;
+  int CL;
+  if (G >= 64)
+    CL = (wbytes < 64e6 || G >= 128) ? 8 : 2;
+  else
+    CL = wbytes < 20e6 ? 4 : 2;
+  CL = b1_env("PARO_G1_CL", CL);
+  if (G >= 64) CL = b1_env("PARO_G1_CL_BIGK", CL);
+  if (CL < 1 || CL > 8) CL = 2;
+  while (CL > 1 && CL > G) CL /= 2;
+  if (wbytes_out) *wbytes_out = wbytes;
+  return CL;
+}
+
+// Cross-cluster K split: a single long-K linear whose stream is long (>= 64 MB: LLaMA-3-70B
+// down_proj) runs on clusters of 2 (148 SMs) instead of 8 (120 SMs), its K range split over KS
+// clusters so that every CTA still transforms at most 16 groups (one round).  Shorter streams
+// (LLaMA-3-8B / Qwen3-4B down_proj) measured slower with the split: the global last-arriver
+// reduction costs more than the extra SMs bring (tools/ab_flag.sh).
+int b1_ks_slices(int n_lin, const int64_t* Ns, int64_t K) {
+  double wbytes = 0;
+  const int CL = b1_cluster_size(n_lin, Ns, K, &wbytes);
+  if (n_lin != 1 || CL != 8 || wbytes < PARO_B1_KS_MIN_BYTES) return 1;
+  const int G = static_cast<int>(K / 128);
+  const int ks = (G + 2 * B1_NW - 1) / (2 * B1_NW);
+  return ks > 1 ? ks : 1;
+}
+
+size_t b1_ks_bytes(int KS, int64_t N) {
+  return KS > 1 ? 4096 + (static_cast<size_t>(KS * N * 4) + 255) / 256 * 256 : 0;
+}
+
+bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, float* ks_part, uint32_t* ks_ctr,
+                   B1Config* cfg, const char** why) {
   if (B != 1) {
     *why = "the one-launch B = 1 kernel takes one token";
     return false;
@@ -747,23 +832,10 @@ bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, B
   }
   B1Config c{};
   B1Args& a = c.a;
-  // Cluster size = how many ways a row block's groups are split (G / CL groups transformed per
-  // CTA).  The rotations are shared-memory bound (8 accesses per pair-update, all warps at once),
-  // so fewer groups per CTA shorten the transform; but clusters of 2 / 4 / 8 fill only 148 / 132
-  // / 120 SMs (occupancy API), which slows the weight stream.  Measured (tools/time_groups.py,
-  // tools/time_70b.py): short streams (< 20 MB) at K = 4096 prefer 4, long ones 2; K >= 8192
-  // prefers 8 (one transform round) unless the stream is very long and G small (70B gate+up: 2).
   double wbytes = 0;
-  for (int i = 0; i < n_lin; ++i) wbytes += static_cast<double>(Ns[i]) * K * 0.52;
-  int CL;
-  if (G >= 64)
-    CL = (wbytes < 64e6 || G >= 128) ? 8 : 2;
-  else
-    CL = wbytes < 20e6 ? 4 : 2;
-  CL = b1_env("PARO_G1_CL", CL);
-  if (G >= 64) CL = b1_env("PARO_G1_CL_BIGK", CL);
-  if (CL < 1 || CL > 8) CL = 2;
-  while (CL > 1 && CL > G) CL /= 2;
+  int CL = b1_cluster_size(n_lin, Ns, K, &wbytes);
+  int KS = ks_part && ks_ctr ? b1_ks_slices(n_lin, Ns, K) : 1;
+  if (KS > 1) CL = 2;
   const int NW = B1_NW;
   int TPS = std::max(1, std::min(64, b1_env("PARO_G1_TPS", 2 * NW)));
   const int threads = (NW + 1) * 32;
@@ -785,6 +857,7 @@ bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, B
     NB[i] = (Ns[i] + TILE_ROWS - 1) / TILE_ROWS;
     NBsum += NB[i];
   }
+  if (KS > 1) ncl_max /= KS;  // row ranges (each KS clusters)
   int ncl = static_cast<int>(std::min<int64_t>(ncl_max, NBsum));
   if (ncl < n_lin) ncl = n_lin;
   int cls[GEMV_MAX_LIN], used = 0, big = 0;
@@ -802,9 +875,12 @@ bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, B
     d.rb_base = static_cast<int>(NB[i] / cls[i]);
     d.rb_extra = static_cast<int>(NB[i] % cls[i]);
     rmax = std::max(rmax, (d.rb_base + (d.rb_extra ? 1 : 0)) * TILE_ROWS);
-    begin += cls[i] * CL;
+    begin += cls[i] * CL * KS;
   }
   c.grid = begin;
+  a.KS = KS;
+  a.ks_part = KS > 1 ? ks_part : nullptr;
+  a.ks_ctr = KS > 1 ? ks_ctr : nullptr;
   c.CL = CL;
   c.BT = BT;
   a.B = B;
@@ -817,7 +893,7 @@ bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, B
   a.params_first = b1_env("PARO_G1_PF", 1);
   a.R_max = rmax;
   a.RRmax = (rmax + CL - 1) / CL;
-  const int gcm = (G + CL - 1) / CL;
+  const int gcm = ((G + KS - 1) / KS + CL - 1) / CL;
   a.sc_off = static_cast<uint32_t>(TPS) * TILE_CODE_BYTES;
   a.z_off = a.sc_off + static_cast<uint32_t>(TPS) * TILE_SCALE_BYTES;
   a.slot_bytes = b1_align(a.z_off + static_cast<uint32_t>(TPS) * TILE_ZERO_BYTES, 128);
@@ -829,7 +905,8 @@ bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, B
   a.off_part = off;
   // B = 1: per-warp row partials summed in a fixed order (deterministic) while they fit in
   // 48 KB; clusters with more rows (e.g. 70B gate+up: 3840 rows) add with shared atomics
-  a.atom = BT == 1 && (static_cast<int64_t>(NW) * rmax * 4 > (b1_env("PARO_G1_ATOM_KB", 48) << 10));
+  // (K split: up to 64 KB, so that its row ranges of ~26 row blocks keep the deterministic sums)
+  a.atom = BT == 1 && (static_cast<int64_t>(NW) * rmax * 4 > (b1_env("PARO_G1_ATOM_KB", KS > 1 ? 64 : 48) << 10));
   off += b1_align(static_cast<uint32_t>(BT == 1 && !a.atom ? NW : BT) * rmax * 4, 128);
   a.off_scr = a.off_recv = off;  // BT > 1: phase-1 scratch and the cluster reduction share this space
   if (BT == 1) {

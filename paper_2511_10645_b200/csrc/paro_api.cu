@@ -316,6 +316,8 @@ size_t paro_linear_workspace(int64_t B, int64_t N, int64_t K, int32_t n_rot, int
   }
   else if (B > 1 && paro::gemv1_enabled())  // decode, 2..16 tokens: pre-transformed x' (gemv1.cu)
     ws += paro::gemv1_xq_bytes(static_cast<int>(std::min<int64_t>(B, paro::GEMV1_MAX_B)), K);
+  else if (B == 1 && paro::gemv1_enabled() && !(flags & 0x100u))  // one token, long K: cross-cluster K split
+    ws += align256(paro::b1_ks_bytes(paro::b1_ks_slices(1, &N, K), N));
   return ws;
 }
 
@@ -371,7 +373,18 @@ static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, 
     if (k_split && live == 1) {  // one token: the one-launch kernel (gemv1_b1.cu)
       paro::B1Config c1;
       const char* why = "";
-      if (!paro::plan_gemv1_b1(1, n, Ns, K, rotate, &c1, &why))
+      // one linear, long K: the K range split over clusters when the workspace holds its counters
+      // and row sums (paro_linear_workspace reports them; zero before first use)
+      float* ks_part = nullptr;
+      uint32_t* ks_ctr = nullptr;
+      if (B == 1 && n == 1) {
+        const size_t kb = paro::b1_ks_bytes(paro::b1_ks_slices(1, Ns, K), Ns[0]);
+        if (kb && ws && ws_bytes >= kb) {
+          ks_ctr = static_cast<uint32_t*>(ws);
+          ks_part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + 4096);
+        }
+      }
+      if (!paro::plan_gemv1_b1(1, n, Ns, K, rotate, ks_part, ks_ctr, &c1, &why))
         return fail(PARO_ERR_UNSUPPORTED, "paro_linear: %s", why);
       paro::B1Args& a = c1.a;
       a.x = static_cast<const uint8_t*>(x) + b0 * K * xe;
@@ -956,7 +969,7 @@ paro_status paro_linear_allgather_p2p(const void* x, paro_dtype x_dtype, int64_t
   const int64_t Ns = packed_shard->N, K = packed_shard->K, N_full = Ns * world;
   paro::B1Config c;
   const char* why = "";
-  if (!paro::plan_gemv1_b1(1, 1, &Ns, K, (flags & PARO_LINEAR_NO_ROTATION) ? 0 : 1, &c, &why))
+  if (!paro::plan_gemv1_b1(1, 1, &Ns, K, (flags & PARO_LINEAR_NO_ROTATION) ? 0 : 1, nullptr, nullptr, &c, &why))
     return fail(PARO_ERR_UNSUPPORTED, "paro_linear_allgather_p2p: %s", why);
   paro::B1Args& a = c.a;
   a.x = x;

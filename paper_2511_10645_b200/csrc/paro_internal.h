@@ -170,15 +170,27 @@ struct B1Args {
   uint32_t* done_ctr;  // local: CTAs finished (the last one resets it)
   int tl_slot;         // PARO_TIMELINE builds: launch slot of the per-CTA timeline
   const uint32_t* epoch;  // local: exchanges completed so far (advanced by the wait kernel)
+  // cross-cluster K split (KS > 1, one linear): cluster c takes the K slice c % KS of the row range
+  // c / KS; its row sums go to ks_part[slice][n] and the last of the KS clusters to arrive (counter
+  // ks_ctr[row range * CL + rank], reset by that CTA) adds the KS slices in a fixed order
+  int KS;
+  float* ks_part;
+  uint32_t* ks_ctr;
 };
 struct B1Config {
   int CL, grid, NW, BT;
   B1Args a;
 };
-bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, B1Config* cfg, const char** why);
+// ks_part / ks_ctr: the K-split workspace (NULL: no split)
+bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, float* ks_part, uint32_t* ks_ctr,
+                   B1Config* cfg, const char** why);
 // waits until every rank's flag reached this rank's epoch + 1, then advances the epoch
 cudaError_t launch_p2p_wait(uint32_t* flags, uint32_t* epoch, int world, int pdl, cudaStream_t st);
 cudaError_t launch_gemv1_b1(const B1Config& cfg, cudaStream_t st);
+// cross-cluster K split of a B = 1 launch: slices (1 = none) and the workspace bytes it needs
+// (4 KB of counters, zero before first use and left zero by every call, then KS x N fp32 row sums)
+int b1_ks_slices(int n_lin, const int64_t* Ns, int64_t K);
+size_t b1_ks_bytes(int KS, int64_t N);
 
 bool gemv1_enabled();
 // B > 1: bytes of pre-transformed activations per linear (digits + per-group sums / scales)

@@ -79,6 +79,11 @@ def test_linear_rejects_null_before_cuda(paro):
 def test_workspace_arithmetic(paro):
     assert paro.paro_linear_workspace(1, 4096, 4096) == 0
     assert paro.paro_linear_workspace(1, 4096, 4096, 8, 64, True) >= 32 * 8 * 64 * 10
+    # one token, long K and a long stream (LLaMA-3-70B down_proj, G = 224): K split over 7 clusters
+    # of 2 -> 4 KB of counters + 7 x N fp32 row sums; shorter streams (8B down_proj) need none
+    assert paro.paro_linear_workspace(1, 8192, 28672) == 4096 + 7 * 8192 * 4
+    assert paro.paro_linear_workspace(1, 4096, 14336) == 0
+    assert paro.paro_linear_workspace(1, 28672, 8192) == 0  # 70B gate: clusters of 2 already
 
 
 def test_shard_rows(paro):

@@ -221,9 +221,16 @@ def test_full_size_sampled(paro, name, N, K):
     t = dev_tensors(p)
     rows = np.sort(np.random.default_rng(0).choice(N, size=64, replace=False))
     packed, ref = check_pack(paro, p, t, rows=rows)
-    y = paro.paro_linear(t["x"], packed, flags=paro.PARO_LINEAR_PDL).float().cpu().numpy()[:, rows]
+    # one zeroed workspace reused across calls, as a serving loop does (llama70b_down takes the
+    # cross-cluster K split: its arrival counters must be back at zero after every call)
+    ws = torch.zeros(max(1, paro.paro_linear_workspace(1, N, K)), dtype=torch.uint8, device="cuda")
+    ys = [paro.paro_linear(t["x"], packed, flags=paro.PARO_LINEAR_PDL, workspace=ws) for _ in range(3)]
+    y = ys[0].float().cpu().numpy()[:, rows]
     y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"])
     assert O.normwise_error(y, y_ref) <= TOL
+    assert all(bool((ys[0] == yk).all()) for yk in ys[1:]), "repeated calls differ"
+    if paro.paro_linear_workspace(1, N, K) > 0:
+        assert int(ws[:4096].count_nonzero()) == 0, "K-split counters not reset"
 
 
 @pytest.mark.parametrize("B,N,K", [(300, 256, 512), (17, 384, 1024), (520, 1024, 4096)])
@@ -273,6 +280,20 @@ def test_prefill_bf16_activations(paro, out_dtype):
         assert np.all(np.abs(y - yr) <= TOL * np.max(np.abs(y_ref)) + ulp)
     else:
         assert O.normwise_error(y, y_ref) <= TOL
+
+
+@pytest.mark.parametrize("N,K", [(1000, 8192), (520, 16384), (96, 28672)])
+def test_long_k_b1_all_rows(paro, N, K):
+    """One token at long K (the shapes planned with clusters of 8 or with the K range split over
+    several clusters): every row against the oracle, ragged row blocks, and two calls bit-identical
+    (fixed-order reductions)."""
+    p = synth.make_problem(N, K, 1, seed=150 + N)
+    t = dev_tensors(p)
+    packed, ref = check_pack(paro, p, t)
+    ys = [paro.paro_linear(t["x"], packed, flags=paro.PARO_LINEAR_PDL) for _ in range(2)]
+    y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"])
+    assert O.normwise_error(ys[0].float().cpu().numpy(), y_ref) <= TOL
+    assert bool((ys[0] == ys[1]).all())
 
 
 @pytest.mark.parametrize("N,K", [(4096, 4096), (1024, 4096), (14336, 4096), (4096, 14336)])

@@ -248,6 +248,22 @@ def test_prefill_gemm(paro, B, N, K):
     assert bool((ys[0] == ys[1]).all()), "split-K reduction is not deterministic"
 
 
+@pytest.mark.parametrize("B,N", [(2048, 2560), (1500, 4096)])
+def test_prefill_ragged_token_tiles(paro, B, N):
+    """Prefill with a ragged last 256-token tile (2048 tokens over 20 row tiles; 1500 = 5 x 256 + 220)
+    and a row-tile count that leaves the last tile round partly idle: every output against the
+    oracle, fp16 and fp32 outputs."""
+    K = 512
+    p = synth.make_problem(N, K, B, seed=160 + B, with_bias=True)
+    t = dev_tensors(p)
+    packed, ref = check_pack(paro, p, t)
+    y = paro.paro_linear(t["x"], packed, bias=t["bias"], flags=paro.PARO_LINEAR_FORCE_GEMM)
+    y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"], bias=p["bias"])
+    assert O.normwise_error(y.float().cpu().numpy(), y_ref) <= TOL
+    yf = paro.paro_linear(t["x"], packed, bias=t["bias"], out_dtype=torch.float32, flags=paro.PARO_LINEAR_FORCE_GEMM)
+    assert O.normwise_error(yf.cpu().numpy(), y_ref) <= TOL
+
+
 @pytest.mark.parametrize("n_rot", [0, 2, 4])
 def test_prefill_fewer_rotations(paro, n_rot):
     """Table 6 #IR in {0, 2, 4} on the prefill path: the dense transform's

@@ -208,7 +208,7 @@ def run_paro(args):
     for name, (N, K) in shapes.items():
         ys[name] = y_all[off:off + B * N].view(B, N)
         off += B * N
-    ws = torch.zeros(64 << 20, dtype=torch.uint8, device=dev)
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
     chains = [layer_chain(paro, layer, x_in, x_attn, ys) for layer in pool]
     chain_ws = paro.chain_workspace(B, chains[0])
 
@@ -517,7 +517,7 @@ def measure_prefill(torch, paro, dev, stream, layer, g):
         for name, N, K, packed in layer:
             xp = torch.randn((Bp, K), generator=g, device=dev).to(torch.float16)
             yp = torch.empty((Bp, N), dtype=torch.float16, device=dev)
-            wsp = torch.zeros(max(1, paro.paro_linear_workspace(Bp, N, K)), dtype=torch.uint8, device=dev)
+            wsp = torch.empty(max(1, paro.paro_linear_workspace(Bp, N, K)), dtype=torch.uint8, device=dev)
             us = graph_time_us(torch, stream, lambda: paro.paro_linear(xp, packed, y=yp, workspace=wsp, stream=stream),
                                10)
             fl = 2.0 * Bp * N * K
@@ -556,7 +556,7 @@ def measure_qwen_stack(torch, paro, dev, stream, batches):
         stages = []
         for layer in pool:
             stages += layer_chain(paro, layer, x_in, x_attn, ys)
-        ws = torch.zeros(64 << 20, dtype=torch.uint8, device=dev)
+        ws = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
 
         def step(fl):
             for st in stages:  # 144 PDL-chained decode launches
@@ -593,7 +593,7 @@ def measure_70b_mlp(torch, paro, dev, stream, comm, rank, world):
     x = torch.randn((1, 8192), device=dev).to(torch.float16)
     ys = {n: torch.zeros((1, N), dtype=torch.float16, device=dev) for n, (N, K) in shapes.items()}
     ysh = {n: torch.zeros((1, N // world), dtype=torch.float16, device=dev) for n, (N, K) in shapes.items()}
-    ws = torch.zeros(16 << 20, dtype=torch.uint8, device=dev)
+    ws = torch.empty(16 << 20, dtype=torch.uint8, device=dev)
     out = {"world": world}
     tot = {"gemv_us": 0.0, "total_us": 0.0, "p2p_total_us": 0.0}
     from paper_2511_10645_b200 import dist as pd

@@ -74,7 +74,9 @@ typedef enum { PARO_F16 = 0, PARO_BF16 = 1, PARO_F32 = 2 } paro_dtype;
  *                        reordered and oriented so every shared-memory gather/scatter of the
  *                        runtime transform is bank-conflict free.
  *   rot_idx: G*L*64*2    u8 (i, j) per slot in the same order.
- *   svec   : K*4         fp32 s.
+ *   svec   : K*4 + 4096  fp32 s, then the arrival counters of the long-K decode split
+ *                        (zeroed by paro_pack; every call leaves them zero, so calls that use
+ *                        the same packed linear must be stream-ordered).
  * Weight bytes are N*K/2 + N*G*2 + N*G/2 (0.5195 B/weight) when N % 32 == 0. */
 typedef struct {
   size_t codes, scales, zeros, rot_cs, rot_idx, svec;
@@ -131,9 +133,8 @@ paro_status paro_pack(const void* W, const float* s, const float* theta, const i
  * G B' 8) bytes (G = K/128, B' = B rounded up to 4, 8 or 16) for the pre-transformed
  * activations.  B = 1 with the packed transform needs 0 bytes, except for a long-K linear with a
  * long weight stream (>= 64 MB, e.g. LLaMA-3-70B down_proj), whose K range is split over
- * several thread-block clusters: 4096 bytes of arrival counters + KS x N fp32 row sums.  Those
- * counters must be ZERO before the workspace is first used (e.g. one cudaMemsetAsync at
- * allocation); every call leaves them zero.  A workspace serves one stream at a time. */
+ * KS thread-block clusters: KS x N fp32 row sums (fully written before they are read; no
+ * initialisation).  A workspace serves one stream at a time. */
 size_t paro_linear_workspace(int64_t B, int64_t N, int64_t K, int32_t n_rot, int32_t n_pairs, int32_t on_the_fly,
                              uint32_t flags);
 

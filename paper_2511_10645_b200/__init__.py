@@ -203,8 +203,8 @@ def paro_linear(x, packed: PackedLinear, s=None, theta=None, pairs=None, bias=No
         y = torch.empty((B, packed.N), dtype=out_dtype or x.dtype, device=x.device)
     P = 0 if theta is None else theta.shape[2]
     need = paro_linear_workspace(B, packed.N, packed.K, packed.n_rot, P or 64, s is not None, flags)
-    if need and (workspace is None or workspace.numel() < need):  # zeroed: K-split counters (paro.h)
-        workspace = torch.zeros(need, dtype=torch.uint8, device=x.device)
+    if need and (workspace is None or workspace.numel() < need):
+        workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
     st = packed.struct()
     _check(_lib.paro_linear(_ptr(x), _dt(x), B, ctypes.byref(st), _ptr(s), _ptr(theta), _ptr(pairs), P, _ptr(bias),
                             _ptr(y), _dt(y), flags, _ptr(workspace), 0 if workspace is None else workspace.numel(),
@@ -221,8 +221,8 @@ def paro_linear_multi(x, packed: list, bias=None, y=None, out_dtype=None, flags:
     if y is None:
         y = [torch.empty((B, p.N), dtype=out_dtype or x.dtype, device=x.device) for p in packed]
     need = len(packed) * max(paro_linear_workspace(B, p.N, p.K, p.n_rot, 64, False, flags) for p in packed)
-    if need and (workspace is None or workspace.numel() < need):  # zeroed: K-split counters (paro.h)
-        workspace = torch.zeros(need, dtype=torch.uint8, device=x.device)
+    if need and (workspace is None or workspace.numel() < need):
+        workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
     structs = (paro_packed * n)(*[p.struct() for p in packed])
     ys = (ctypes.c_void_p * n)(*[t.data_ptr() for t in y])
     bs = None if bias is None else (ctypes.c_void_p * n)(*[_ptr(b) for b in bias])
@@ -376,8 +376,8 @@ def paro_linear_allgather(x, packed_shard: PackedLinear, comm: int, rank: int, w
     if y is None:
         y = torch.empty((B, N), dtype=out_dtype or x.dtype, device=x.device)
     need = int(_lib.paro_linear_allgather_workspace(B, packed_shard.N, packed_shard.K, world, _dt(y), flags))
-    if workspace is None or workspace.numel() < need:  # zeroed: K-split counters (paro.h)
-        workspace = torch.zeros(need, dtype=torch.uint8, device=x.device)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
     st = packed_shard.struct()
     _check(_lib.paro_linear_allgather(_ptr(x), _dt(x), B, ctypes.byref(st), _ptr(bias_shard), _ptr(y), _dt(y), flags,
                                       _ptr(workspace), workspace.numel(), comm, rank, world, _stream(stream)))

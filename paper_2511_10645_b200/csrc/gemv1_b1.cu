@@ -810,7 +810,7 @@ int b1_ks_slices(int n_lin, const int64_t* Ns, int64_t K) {
 }
 
 size_t b1_ks_bytes(int KS, int64_t N) {
-  return KS > 1 ? 4096 + (static_cast<size_t>(KS * N * 4) + 255) / 256 * 256 : 0;
+  return KS > 1 ? (static_cast<size_t>(KS * N * 4) + 255) / 256 * 256 : 0;
 }
 
 bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, float* ks_part, uint32_t* ks_ctr,

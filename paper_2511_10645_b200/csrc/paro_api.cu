@@ -167,7 +167,7 @@ paro_status paro_pack_sizes(int64_t N, int64_t K, int32_t group, int32_t n_rot, 
   out->zeros = static_cast<size_t>(tiles * paro::TILE_ZERO_BYTES);
   out->rot_cs = static_cast<size_t>(G * n_rot * PARO_SLOTS * 8);
   out->rot_idx = static_cast<size_t>(G * n_rot * PARO_SLOTS * 2);
-  out->svec = static_cast<size_t>(K * 4);
+  out->svec = static_cast<size_t>(K * 4) + paro::KS_CTR_BYTES;  // s, then the K-split arrival counters
   return PARO_OK;
 }
 
@@ -273,6 +273,8 @@ paro_status paro_pack(const void* W, const float* s, const float* theta, const i
   if (e == cudaSuccess && L > 0) e = cudaMemcpyAsync(out->rot_cs, cs32.data(), cs32.size() * 4, cudaMemcpyHostToDevice, cs);
   if (e == cudaSuccess && L > 0) e = cudaMemcpyAsync(out->rot_idx, idx.data(), idx.size(), cudaMemcpyHostToDevice, cs);
   if (e == cudaSuccess) e = cudaMemcpyAsync(out->svec, s, K * 4, cudaMemcpyDeviceToDevice, cs);
+  if (e == cudaSuccess)  // the long-K decode split's arrival counters (every call leaves them zero)
+    e = cudaMemsetAsync(static_cast<uint8_t*>(out->svec) + K * 4, 0, paro::KS_CTR_BYTES, cs);
   // zero the packed buffers: rows >= N of the last row block stay zero, zero points are
   // OR-ed in nibble by nibble
   if (e == cudaSuccess) e = cudaMemsetAsync(out->codes, 0, sz.codes, cs);
@@ -373,15 +375,15 @@ static paro_status decode_linears(const void* x, paro_dtype x_dtype, int64_t B, 
     if (k_split && live == 1) {  // one token: the one-launch kernel (gemv1_b1.cu)
       paro::B1Config c1;
       const char* why = "";
-      // one linear, long K: the K range split over clusters when the workspace holds its counters
-      // and row sums (paro_linear_workspace reports them; zero before first use)
+      // one linear, long K: the K range split over clusters when the workspace holds the row sums
+      // (paro_linear_workspace reports them); the arrival counters live after s in packed svec
       float* ks_part = nullptr;
       uint32_t* ks_ctr = nullptr;
       if (B == 1 && n == 1) {
         const size_t kb = paro::b1_ks_bytes(paro::b1_ks_slices(1, Ns, K), Ns[0]);
         if (kb && ws && ws_bytes >= kb) {
-          ks_ctr = static_cast<uint32_t*>(ws);
-          ks_part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + 4096);
+          ks_part = static_cast<float*>(ws);
+          ks_ctr = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(packed[0].svec) + K * 4);
         }
       }
       if (!paro::plan_gemv1_b1(1, n, Ns, K, rotate, ks_part, ks_ctr, &c1, &why))

@@ -188,7 +188,9 @@ bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, f
 cudaError_t launch_p2p_wait(uint32_t* flags, uint32_t* epoch, int world, int pdl, cudaStream_t st);
 cudaError_t launch_gemv1_b1(const B1Config& cfg, cudaStream_t st);
 // cross-cluster K split of a B = 1 launch: slices (1 = none) and the workspace bytes it needs
-// (4 KB of counters, zero before first use and left zero by every call, then KS x N fp32 row sums)
+// (KS x N fp32 row sums); its arrival counters are the KS_CTR_BYTES after s in the packed svec
+// buffer (zeroed by paro_pack, left zero by every call)
+constexpr size_t KS_CTR_BYTES = 4096;
 int b1_ks_slices(int n_lin, const int64_t* Ns, int64_t K);
 size_t b1_ks_bytes(int KS, int64_t N);
 

@@ -48,7 +48,7 @@ def test_pack_sizes(paro):
     tiles = (4096 // 32) * G                   # tiles of 32 rows x one 128-group
     assert sz.codes == 4096 * 4096 // 2 == tiles * 2048
     assert sz.scales == 4096 * G * 2 == tiles * 64 and sz.zeros == 4096 * G // 2 == tiles * 16
-    assert sz.rot_cs == G * 8 * 64 * 8 and sz.rot_idx == G * 8 * 64 * 2 and sz.svec == 4096 * 4
+    assert sz.rot_cs == G * 8 * 64 * 8 and sz.rot_idx == G * 8 * 64 * 2 and sz.svec == 4096 * 4 + 4096  # s + K-split counters
     sz = paro.paro_pack_sizes(3, 384, 128, 0)   # a partial row block pads to 32 rows
     assert sz.codes == 3 * 2048 and sz.scales == 3 * 64 and sz.zeros == 3 * 16 and sz.rot_cs == 0
 
@@ -80,8 +80,8 @@ def test_workspace_arithmetic(paro):
     assert paro.paro_linear_workspace(1, 4096, 4096) == 0
     assert paro.paro_linear_workspace(1, 4096, 4096, 8, 64, True) >= 32 * 8 * 64 * 10
     # one token, long K and a long stream (LLaMA-3-70B down_proj, G = 224): K split over 7 clusters
-    # of 2 -> 4 KB of counters + 7 x N fp32 row sums; shorter streams (8B down_proj) need none
-    assert paro.paro_linear_workspace(1, 8192, 28672) == 4096 + 7 * 8192 * 4
+    # of 2 -> 7 x N fp32 row sums; shorter streams (8B down_proj) need none
+    assert paro.paro_linear_workspace(1, 8192, 28672) == 7 * 8192 * 4
     assert paro.paro_linear_workspace(1, 4096, 14336) == 0
     assert paro.paro_linear_workspace(1, 28672, 8192) == 0  # 70B gate: clusters of 2 already
 

@@ -32,7 +32,7 @@ XF = paro.PARO_LINEAR_TCGEN05 if (len(sys.argv) > 3 and sys.argv[3] == "tc") els
 x = torch.randn(B, 4096, device=dev).half()
 x2 = torch.randn(B, 14336, device=dev).half()
 ys = {n: torch.empty(B, N, device=dev, dtype=torch.half) for n, (N, K) in shapes.items()}
-ws = torch.zeros(64 << 20, dtype=torch.uint8, device=dev)
+ws = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
 groups = [["q_proj", "k_proj", "v_proj"], ["o_proj"], ["gate_proj", "up_proj"], ["down_proj"]]
 st = torch.cuda.Stream()
 

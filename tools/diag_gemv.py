@@ -26,7 +26,7 @@ def make_packed(codes_u8, S, z, n_rot=0):
     zb = (zz[:, 0::2] | (zz[:, 1::2] << 4)).astype(np.uint8).reshape(-1)
     pk.zeros.zero_()
     pk.zeros[: zb.size].copy_(torch.from_numpy(zb))
-    pk.svec.copy_(torch.from_numpy(np.ones(K, np.float32)).view(torch.uint8))
+    pk.svec[:K * 4].copy_(torch.from_numpy(np.ones(K, np.float32)).view(torch.uint8))
     return pk
 
 

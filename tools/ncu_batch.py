@@ -18,7 +18,7 @@ s, th, pr = (torch.from_numpy(p[k]).to(dev) for k in ("s", "theta", "pairs"))
 pool = [[paro.paro_pack((torch.randn(N, K, device=dev) * 0.02).half(), s, th, pr) for N in Ns] for _ in range(6)]
 x = torch.randn(B, K, device=dev).half()
 ys = [torch.empty(B, N, device=dev, dtype=torch.half) for N in Ns]
-ws = torch.zeros(64 << 20, dtype=torch.uint8, device=dev)
+ws = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
 for i in range(30):
     paro.paro_linear_multi(x, pool[i % 6], y=ys, flags=paro.PARO_LINEAR_PDL, workspace=ws)
 torch.cuda.synchronize()

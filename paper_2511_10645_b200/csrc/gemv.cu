@@ -518,17 +518,17 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 288 ? 2 : 1) paro_gemv_kernel(co
         const float v = acc[q] + __shfl_xor_sync(0xffffffffu, acc[q], 1);
         if ((t & 1) == 0 && (t >> 1) < BT && tok_l < B) pr[(gq + 8 * q) * BT + tok_l] = v;
       }
-      return;
-    }
+    } else {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (2 * t < B) {
-        pr[(gq + 16 * h) * BT + 2 * t] = acc[4 * h + 0];
-        pr[(gq + 16 * h + 8) * BT + 2 * t] = acc[4 * h + 2];
-      }
-      if (2 * t + 1 < B) {
-        pr[(gq + 16 * h) * BT + 2 * t + 1] = acc[4 * h + 1];
-        pr[(gq + 16 * h + 8) * BT + 2 * t + 1] = acc[4 * h + 3];
+      for (int h = 0; h < 2; ++h) {
+        if (2 * t < B) {
+          pr[(gq + 16 * h) * BT + 2 * t] = acc[4 * h + 0];
+          pr[(gq + 16 * h + 8) * BT + 2 * t] = acc[4 * h + 2];
+        }
+        if (2 * t + 1 < B) {
+          pr[(gq + 16 * h) * BT + 2 * t + 1] = acc[4 * h + 1];
+          pr[(gq + 16 * h + 8) * BT + 2 * t + 1] = acc[4 * h + 3];
+        }
       }
     }
   };

@@ -963,7 +963,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
     if (s == 0 && CL > 1) cluster_wait();  // every CTA of the cluster is running: DSMEM is legal
     if (BT > 1 && g.active) {
       // four tokens per st.async (16 B), owner by owner (no per-element division)
-      constexpr int Q4 = BT / 4;
+      constexpr int Q4 = BT >= 4 ? BT / 4 : 1;  // (BT = 1 never takes this branch)
 #pragma unroll 1
       for (int c = 0, r0 = 0; c < CL && r0 < g.R; ++c, r0 += g.RR) {
         const int rows = min(g.RR, g.R - r0);

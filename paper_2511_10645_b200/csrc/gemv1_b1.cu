@@ -117,7 +117,8 @@ __device__ __forceinline__ void mma_u8s8(int (&d)[4], uint32_t a0, uint32_t a1, 
 // lockstep and occupy the MMA's 8 columns in sets of four (columns 2b, 2b+1 = hi, lo digit of
 // token b of the set).  BT = 1 sums row partials per warp in a fixed order (deterministic);
 // BT > 1 adds them with shared-memory atomics.
-template <int NW, int BT>
+// KSP: the cross-cluster K split instance (a.KS > 1); the other instance has none of its code
+template <int NW, int BT, bool KSP>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B1Args a) {
   constexpr int TB = BT == 1 ? 1 : 4;          // tokens per transform chunk / MMA column set
   constexpr int NB = (BT + 3) / 4;             // column sets
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
   const int CL = static_cast<int>(cluster_nctarank());
   const int crank = static_cast<int>(cluster_ctarank());
   const int G = a.G, B = a.B;
-  const int KS = a.KS > 1 ? a.KS : 1;
+  const int KS = KSP ? a.KS : 1;
   const int cl_all = (static_cast<int>(blockIdx.x) - d.cta_begin) / CL;
   const int kq = cl_all % KS, cl = cl_all / KS;  // K slice, row range
   const int nrb = d.rb_base + (cl < d.rb_extra ? 1 : 0);
@@ -768,7 +769,7 @@ static int b1_active_clusters_compute(const void* k, int CL, int threads, int bu
 }
 static int b1_active_clusters(int BT, int CL, int threads, int budget) {
   (void)BT;
-  return cached_device_int(reinterpret_cast<const void*>(&paro_gemv1_b1_kernel<B1_NW, 1>), CL, threads, budget,
+  return cached_device_int(reinterpret_cast<const void*>(&paro_gemv1_b1_kernel<B1_NW, 1, false>), CL, threads, budget,
                            b1_active_clusters_compute);
 }
 
@@ -820,7 +821,7 @@ bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, f
     return false;
   }
   const int BT = B == 1 ? 1 : B <= 4 ? 4 : B <= 8 ? 8 : 16;
-  const int TB = BT == 1 ? 1 : 4, NSET = (BT + 3) / 4, NCOL = BT == 1 ? 2 : 8;
+  const int NSET = (BT + 3) / 4, NCOL = BT == 1 ? 2 : 8;
   if (n_lin < 1 || n_lin > GEMV_MAX_LIN) {
     *why = "1..4 linears per decode launch";
     return false;
@@ -962,7 +963,7 @@ bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, f
 
 template <int BT>
 static cudaError_t b1_launch(const B1Config& c, cudaLaunchConfig_t* cfg) {
-  auto kern = paro_gemv1_b1_kernel<B1_NW, BT>;
+  auto kern = c.a.KS > 1 ? paro_gemv1_b1_kernel<B1_NW, BT, true> : paro_gemv1_b1_kernel<B1_NW, BT, false>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(c.a.smem_total));
   if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(cfg, kern, c.a);

@@ -9,7 +9,7 @@ timeout 900 python bench.py --steps 200 --warmup 20 > $O/bench_long.json 2> $O/b
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extra --no-prefill --load-s 0 > $O/bench_under_ncu.log 2>&1
 i=0
-for g in "4096,1024,1024 4096 1" "4096 4096 1" "14336,14336 4096 1" "4096 14336 1" "4096,1024,1024 2560 16" "4096,1024,1024 2560 16 tc"; do
+for g in "4096,1024,1024 4096 1" "4096 4096 1" "14336,14336 4096 1" "4096 14336 1" "4096,1024,1024 2560 16" "4096,1024,1024 2560 16 tc" "8192 28672 1"; do
   set -- $g
   timeout 300 ncu --set full --clock-control none --import-source on -k regex:"paro_gemv1?(_b1)?_kernel" -s 2 -c 1 -f \
     -o $O/group$i python tools/prof_multi.py $1 $2 rot 4 $3 ${4:-} > $O/ncu_group$i.log 2>&1

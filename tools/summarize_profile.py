@@ -61,6 +61,7 @@ groups = {0: "q_proj+k_proj+v_proj (N=4096,1024,1024, K=4096), B=1", 1: "o_proj 
           2: "gate_proj+up_proj (N=14336 x2, K=4096), B=1", 3: "down_proj (N=4096, K=14336), B=1",
           4: "Qwen3-4B q/k/v (N=4096,1024,1024, K=2560), B=16, mma.sync engine",
           5: "Qwen3-4B q/k/v (N=4096,1024,1024, K=2560), B=16, tcgen05 engine",
+          6: "LLaMA-3-70B down_proj (N=8192, K=28672), B=1, cross-cluster K split (7 slices, clusters of 2)",
           "prefill_q": "prefill GEMM q_proj (N=4096, K=4096), 2048 tokens (tcgen05)",
           "prefill_gate": "prefill GEMM gate_proj (N=14336, K=4096), 2048 tokens (tcgen05)",
           "prefill_transform": "prefill activation transform, dense tcgen05 form (2048 x 4096)"}

@@ -298,6 +298,39 @@ def test_prefill_bf16_activations(paro, out_dtype):
         assert O.normwise_error(y, y_ref) <= TOL
 
 
+@pytest.mark.parametrize("out_dtype", ["bf16", "f32"])
+def test_k_split_bias_and_dtypes(paro, out_dtype):
+    """The cross-cluster K split (one token, LLaMA-3-70B down_proj: 7 K slices on clusters of 2)
+    with a bias and bf16 / fp32 output -- the last-arriver epilogue's other store paths -- on
+    sampled rows; PDL launches alternating with an unsplit launch on the same garbage-filled
+    workspace; the counters are back at zero afterwards."""
+    N, K = 8192, 28672
+    assert paro.paro_linear_workspace(1, N, K) == 7 * N * 4
+    p = synth.make_problem(N, K, 1, seed=171, with_bias=True)
+    t = dev_tensors(p)
+    rows = np.sort(np.random.default_rng(3).choice(N, size=48, replace=False))
+    packed, ref = check_pack(paro, p, t, rows=rows)
+    p2 = synth.make_problem(1024, K, 1, seed=172)
+    t2 = dev_tensors(p2)
+    packed2 = paro.paro_pack(t2["W"], t2["s"], t2["theta"], t2["pairs"])
+    odt = {"bf16": torch.bfloat16, "f32": torch.float32}[out_dtype]
+    ws = torch.full((paro.paro_linear_workspace(1, N, K),), 0x5A, dtype=torch.uint8, device="cuda")
+    ys = []
+    for _ in range(2):
+        ys.append(paro.paro_linear(t["x"], packed, bias=t["bias"], out_dtype=odt, flags=paro.PARO_LINEAR_PDL,
+                                   workspace=ws))
+        paro.paro_linear(t2["x"], packed2, flags=paro.PARO_LINEAR_PDL, workspace=ws)
+    y = ys[0].float().cpu().numpy()[:, rows]
+    y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"], bias=p["bias"][rows])
+    if out_dtype == "bf16":
+        yr = torch.from_numpy(y_ref).to(torch.bfloat16).float().numpy()
+        assert np.all(np.abs(y - yr) <= TOL * np.max(np.abs(y_ref)) + np.abs(yr) * 2.0 ** -8)
+    else:
+        assert O.normwise_error(y, y_ref) <= TOL
+    assert bool((ys[0] == ys[1]).all())
+    assert int(packed.svec[K * 4:].count_nonzero()) == 0
+
+
 @pytest.mark.parametrize("N,K", [(1000, 8192), (520, 16384), (96, 28672)])
 def test_long_k_b1_all_rows(paro, N, K):
     """One token at long K (the shapes planned with clusters of 8 or with the K range split over

@@ -117,8 +117,9 @@ __device__ __forceinline__ void mma_u8s8(int (&d)[4], uint32_t a0, uint32_t a1, 
 // lockstep and occupy the MMA's 8 columns in sets of four (columns 2b, 2b+1 = hi, lo digit of
 // token b of the set).  BT = 1 sums row partials per warp in a fixed order (deterministic);
 // BT > 1 adds them with shared-memory atomics.
-// KSP: the cross-cluster K split instance (a.KS > 1); the other instance has none of its code
-template <int NW, int BT, bool KSP>
+// KSP: the cross-cluster K split instance (a.KS > 1); the other instance has none of its code.
+// ATM: row partials added with shared-memory atomics (a.atom; many rows per cluster)
+template <int NW, int BT, bool KSP, bool ATM>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B1Args a) {
   constexpr int TB = BT == 1 ? 1 : 4;          // tokens per transform chunk / MMA column set
   constexpr int NB = (BT + 3) / 4;             // column sets
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
 
   // ------------------------------------------------------------ phase 1: x' of my groups (a4, a5)
   float* pw = part + static_cast<size_t>(warp) * a.R_max;
-  if (BT == 1 && !a.atom) {
+  if (BT == 1 && !ATM) {
     for (int i = lane; i < R; i += 32) pw[i] = 0.f;
   } else {
     for (int i = threadIdx.x; i < R * BT; i += NW * 32) part[i] = 0.f;
@@ -394,7 +395,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
   // ------------------------------------------------------------ phase 2: tiles (a6)
   {
     const int gq = lane >> 2, tq = lane & 3;
-    const bool atom = a.atom != 0;
+    constexpr bool atom = ATM;
     // stage bookkeeping advanced incrementally (no divisions in the loop): ring slot and phase,
     // first tile u0 = st * TPS = r_lo * gc + off0
     int slot = 0, phase = 0, r_lo = 0, off0 = 0;
@@ -586,7 +587,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
   for (int idx = tid; idx < R * BT; idx += NW * 32) {
     const int r = idx / BT, b = idx - r * BT;
     float sum;
-    if (BT == 1 && !a.atom) {
+    if (BT == 1 && !ATM) {
       float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
       for (int w = 0; w < NW; ++w) s4[w & 3] += part[static_cast<size_t>(w) * a.R_max + r];
@@ -769,7 +770,7 @@ static int b1_active_clusters_compute(const void* k, int CL, int threads, int bu
 }
 static int b1_active_clusters(int BT, int CL, int threads, int budget) {
   (void)BT;
-  return cached_device_int(reinterpret_cast<const void*>(&paro_gemv1_b1_kernel<B1_NW, 1, false>), CL, threads, budget,
+  return cached_device_int(reinterpret_cast<const void*>(&paro_gemv1_b1_kernel<B1_NW, 1, false, false>), CL, threads, budget,
                            b1_active_clusters_compute);
 }
 
@@ -963,7 +964,8 @@ bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, f
 
 template <int BT>
 static cudaError_t b1_launch(const B1Config& c, cudaLaunchConfig_t* cfg) {
-  auto kern = c.a.KS > 1 ? paro_gemv1_b1_kernel<B1_NW, BT, true> : paro_gemv1_b1_kernel<B1_NW, BT, false>;
+  auto kern = c.a.KS > 1 ? (c.a.atom ? paro_gemv1_b1_kernel<B1_NW, BT, true, true> : paro_gemv1_b1_kernel<B1_NW, BT, true, false>)
+                         : (c.a.atom ? paro_gemv1_b1_kernel<B1_NW, BT, false, true> : paro_gemv1_b1_kernel<B1_NW, BT, false, false>);
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(c.a.smem_total));
   if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(cfg, kern, c.a);

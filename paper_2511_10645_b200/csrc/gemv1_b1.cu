@@ -117,9 +117,10 @@ __device__ __forceinline__ void mma_u8s8(int (&d)[4], uint32_t a0, uint32_t a1, 
 // lockstep and occupy the MMA's 8 columns in sets of four (columns 2b, 2b+1 = hi, lo digit of
 // token b of the set).  BT = 1 sums row partials per warp in a fixed order (deterministic);
 // BT > 1 adds them with shared-memory atomics.
-// KSP: the cross-cluster K split instance (a.KS > 1); the other instance has none of its code.
+// MODE: 0 the regular epilogue, 1 the cross-cluster K split (a.KS > 1), 2 the NVLink peer-store
+// all-gather (a.p2p) -- each its own instance, so the regular one carries none of the others' code.
 // ATM: row partials added with shared-memory atomics (a.atom; many rows per cluster)
-template <int NW, int BT, bool KSP, bool ATM>
+template <int NW, int BT, int MODE, bool ATM>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B1Args a) {
   constexpr int TB = BT == 1 ? 1 : 4;          // tokens per transform chunk / MMA column set
   constexpr int NB = (BT + 3) / 4;             // column sets
@@ -136,7 +137,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
   const int CL = static_cast<int>(cluster_nctarank());
   const int crank = static_cast<int>(cluster_ctarank());
   const int G = a.G, B = a.B;
-  const int KS = KSP ? a.KS : 1;
+  const int KS = MODE == 1 ? a.KS : 1;
   const int cl_all = (static_cast<int>(blockIdx.x) - d.cta_begin) / CL;
   const int kq = cl_all % KS, cl = cl_all / KS;  // K slice, row range
   const int nrb = d.rb_base + (cl < d.rb_extra ? 1 : 0);
@@ -619,7 +620,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
     }
     if (n < d.N) {
       if (d.bias) v += __ldg(d.bias + n);
-      if (!a.p2p) {
+      if (MODE != 2) {
         const int64_t o = static_cast<int64_t>(b) * d.N + n;
         if (a.y_dtype == 0)
           static_cast<__half*>(d.y)[o] = __float2half_rn(v);
@@ -675,7 +676,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) paro_gemv1_b1_kernel(const B
     }
   }
   if (threadIdx.x == 0) b1_mark(a.tl_slot, 7);
-  if (a.p2p) {
+  if (MODE == 2) {
     // every CTA's peer stores are ordered before its arrival (release at GPU scope); the last CTA to
     // arrive acquires them all and its system-scope release -- cumulative over what it observed --
     // publishes this rank's flag on every rank
@@ -770,7 +771,7 @@ static int b1_active_clusters_compute(const void* k, int CL, int threads, int bu
 }
 static int b1_active_clusters(int BT, int CL, int threads, int budget) {
   (void)BT;
-  return cached_device_int(reinterpret_cast<const void*>(&paro_gemv1_b1_kernel<B1_NW, 1, false, false>), CL, threads, budget,
+  return cached_device_int(reinterpret_cast<const void*>(&paro_gemv1_b1_kernel<B1_NW, 1, 0, false>), CL, threads, budget,
                            b1_active_clusters_compute);
 }
 
@@ -964,8 +965,10 @@ bool plan_gemv1_b1(int B, int n_lin, const int64_t* Ns, int64_t K, int rotate, f
 
 template <int BT>
 static cudaError_t b1_launch(const B1Config& c, cudaLaunchConfig_t* cfg) {
-  auto kern = c.a.KS > 1 ? (c.a.atom ? paro_gemv1_b1_kernel<B1_NW, BT, true, true> : paro_gemv1_b1_kernel<B1_NW, BT, true, false>)
-                         : (c.a.atom ? paro_gemv1_b1_kernel<B1_NW, BT, false, true> : paro_gemv1_b1_kernel<B1_NW, BT, false, false>);
+  const bool at = c.a.atom != 0;
+  auto kern = c.a.p2p  ? (at ? paro_gemv1_b1_kernel<B1_NW, BT, 2, true> : paro_gemv1_b1_kernel<B1_NW, BT, 2, false>)
+              : c.a.KS > 1 ? (at ? paro_gemv1_b1_kernel<B1_NW, BT, 1, true> : paro_gemv1_b1_kernel<B1_NW, BT, 1, false>)
+                           : (at ? paro_gemv1_b1_kernel<B1_NW, BT, 0, true> : paro_gemv1_b1_kernel<B1_NW, BT, 0, false>);
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(c.a.smem_total));
   if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(cfg, kern, c.a);

@@ -77,8 +77,9 @@ struct PfItem {
   int tile, kb, ke, half;  // half: K half of a split tile, or -1
 };
 // the i-th work item of this CTA (false past the last)
+template <bool SPLIT>
 __device__ __forceinline__ bool pf_item(const PrefillArgs& a, int n_tiles, int n_ks, int i, PfItem& it) {
-  if (a.split) {
+  if (SPLIT) {
     const int c = static_cast<int>(blockIdx.x);
     if (i > 0 || c >= 2 * n_tiles) return false;
     it.tile = c >> 1;
@@ -122,7 +123,7 @@ extern "C" int paro_debug_pf_prof(unsigned long long* host, int n) {
 #endif
 
 // PF_BN: tokens per tile (MMA N): 256, or 128 when 256-token tiles would leave SMs idle (k / v)
-template <int PF_BN>
+template <int PF_BN, bool SPLIT>
 __global__ void __launch_bounds__(PF_THREADS, 1)
     prefill_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const PrefillArgs a) {
   constexpr uint32_t PF_X_STAGE_BYTES = PF_BN * PF_BK * 2;
@@ -158,7 +159,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     mbar_init(acc_empty, 128);
     mbar_init(xchg, 1);
     // split-K: 128 rows x PF_BN / 2 fp32 of the partner's partial (armed before any byte can land)
-    if (a.split) mbar_arrive_expect_tx(xchg, PF_BM * (PF_BN / 2) * 4);
+    if (SPLIT) mbar_arrive_expect_tx(xchg, PF_BM * (PF_BN / 2) * 4);
     fence_mbar_init();
     prefetch_tmap(&tmap_x);
   }
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_base_sh;
-  if (a.split) {  // both CTAs of the pair initialised their barriers: DSMEM stores are legal
+  if (SPLIT) {  // both CTAs of the pair initialised their barriers: DSMEM stores are legal
     cluster_arrive_relaxed();
     cluster_wait();
   }
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     if (lane == 0) {
       uint32_t it = 0;
       PfItem w;
-      for (int item = 0; pf_item(a, n_tiles, n_ks, item, w); ++item) {
+      for (int item = 0; pf_item<SPLIT>(a, n_tiles, n_ks, item, w); ++item) {
         const int tok0 = (w.tile / n_row_tiles) * PF_BN;
         for (int ks = w.kb; ks < w.ke; ++ks, ++it) {
           const int s = it % PF_SX;
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
 #define PF_T1(v)
 #endif
       PfItem w;
-      for (int item = 0; pf_item(a, n_tiles, n_ks, item, w); ++item, ++tcount) {
+      for (int item = 0; pf_item<SPLIT>(a, n_tiles, n_ks, item, w); ++item, ++tcount) {
         {
           PF_T0 mbar_wait(acc_empty, (tcount & 1) ^ 1);
           PF_T1(w_acc)
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     const int G = a.K / 128;
     uint32_t it_base = 0;  // K-stage counter at the item's first stage (both parity sets)
     PfItem w;
-    for (int item = 0; pf_item(a, n_tiles, n_ks, item, w); ++item) {
+    for (int item = 0; pf_item<SPLIT>(a, n_tiles, n_ks, item, w); ++item) {
       const int n = (w.tile % n_row_tiles) * PF_BM + r;
       const int rt = n % TILE_ROWS;
       const int64_t T0 = static_cast<int64_t>(n / TILE_ROWS) * G;  // first tile of the row block
@@ -331,14 +332,14 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     const uint32_t lane_addr = static_cast<uint32_t>((warp - 8) * 32) << 16;
     uint32_t tcount = 0;
     PfItem w;
-    for (int item = 0; pf_item(a, n_tiles, n_ks, item, w); ++item, ++tcount) {
+    for (int item = 0; pf_item<SPLIT>(a, n_tiles, n_ks, item, w); ++item, ++tcount) {
       const int tile = w.tile;
       const int n = (tile % n_row_tiles) * PF_BM + r;
       const int tok0 = (tile / n_row_tiles) * PF_BN;
       const float bv = a.bias ? a.bias[n] : 0.f;
       mbar_wait(acc_full, tcount & 1);
       tc_fence_after();
-      if (w.half >= 0) {
+      if (SPLIT) {
         // split-K, the two halves of a tile (a cluster pair) finish it together: half h owns the
         // tokens [128 h, 128 h + 128) of the tile.  Each half sends its partial of the OTHER half's
         // tokens straight into the partner's shared memory (st.async, fp32 [row][128 tokens], 16-byte
@@ -520,7 +521,7 @@ static cudaError_t prefill_launch(const void* xq, int64_t B, const PrefillArgs& 
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   // x' stages + barriers (1 KB) + the epilogue's y staging (PF_BN x 128 16-bit values)
   const size_t smem = 1024 + PF_SX * PF_BN * PF_BK * 2 + 1024 + (PARO_PF_STAGE_EPI ? PF_BN * PF_BM * 2 : 0);
-  auto kern = prefill_gemm_kernel<PF_BN>;
+  auto kern = a.split ? prefill_gemm_kernel<PF_BN, true> : prefill_gemm_kernel<PF_BN, false>;
   cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int64_t tiles = (N / PF_BM) * ((B + PF_BN - 1) / PF_BN);

@@ -76,7 +76,11 @@ if B == 1:
     with torch.cuda.stream(st):
         y2 = paro.paro_linear_allgather_p2p(x, packed, ptrs, rank, world, buf, flags=paro.PARO_LINEAR_PDL, stream=st)
         st.synchronize()
-    p2p_ok = bool(torch.equal(y2, y))
+    # bit-identical when both paths run the same plan; a shard taking the cross-cluster K split on
+    # the NCCL path (>= 64 MB long-K streams) sums in another fixed order: compare normwise then
+    p2p_same = bool(torch.equal(y2, y))
+    d_max = float((y2.float() - y.float()).abs().max()) / max(float(y.float().abs().max()), 1e-30)
+    p2p_ok = p2p_same or d_max <= 2e-3
     us_p2p = dev_us(lambda: paro.paro_linear_allgather_p2p(x, packed, ptrs, rank, world, buf,
                                                            flags=paro.PARO_LINEAR_PDL, stream=st))
     dist.barrier()
@@ -84,13 +88,13 @@ if B == 1:
         paro.paro_ipc_close_handle(q)
 if rank == 0:
     if p2p_ok is not None:
-        print(f"world={world}: NVLink P2P exchange == NCCL all-gather: {p2p_ok}; GEMV + P2P exchange {us_p2p:.2f} us",
-              flush=True)
+        print(f"world={world}: NVLink P2P exchange vs NCCL all-gather: bit-identical {p2p_same}, normwise diff "
+              f"{d_max:.2e}, ok {p2p_ok}; GEMV + P2P exchange {us_p2p:.2f} us", flush=True)
     rows = np.sort(np.random.default_rng(7).choice(N, size=min(64, N), replace=False))
     ref = O.oracle_pack(p["W"][rows], p["s"], p["theta"], p["pairs"])
     y_ref = O.oracle_linear(p["x"], ref, p["s"], p["theta"], p["pairs"])
     err = O.normwise_error(y.float().cpu().numpy()[:, rows], y_ref)
-    ok = err <= 2e-3 and same
+    ok = err <= 2e-3 and same and p2p_ok is not False
     print(f"world={world} N={N} K={K} B={B}: normwise err {err:.2e} (<= 2e-3), ranks agree {same}; "
           f"GEMV {us_gemv:.2f} us, GEMV + all-gather {us_tot:.2f} us (all-gather {us_tot - us_gemv:.2f} us)"
           f" -> {'PASS' if ok else 'FAIL'}", flush=True)
